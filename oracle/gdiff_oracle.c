@@ -1,0 +1,661 @@
+/*
+ * gdiff_oracle.c -- CPU restatement of the reference local-diffusion path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker and the CPU
+ * baseline ("port") for bench.py; it is never linked into, loaded by, or
+ * called from the product path (paper_2410_21634_b200/).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may use it.
+ *
+ * Every routine restates one function of the reference package
+ * (/root/reference/pkg/src/graphdiff, cited as src/<file>:<line>) with the
+ * same floating-point operation order so results are bit-identical:
+ *   - no fused multiply-add (build with -ffp-contract=off; numba emits
+ *     separate vmulsd/vaddsd),
+ *   - numpy reductions (np.abs(v).sum()) use numpy's pairwise summation,
+ *     restated in pw_sum() and pinned against numpy in tests/test_oracle.py.
+ *
+ * Parity is pinned against golden vectors produced by running the reference
+ * itself (tests/golden/make_golden.py -> the .npz files in tests/golden).
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* report container (library-owned arrays, freed by orc_report_free)        */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int32_t converged;
+    int32_t diverged;
+    int64_t sweeps;
+    int64_t total_ops;
+    double min_residual;
+    int64_t support_size;
+    int64_t n_logs;          /* entries in vol/gamma/sign/frontier_sizes */
+    int64_t *vol_log;
+    double *gamma_log;
+    double *l1_log;          /* n_logs + 1 entries */
+    int8_t *sign_log;
+    int64_t *frontier_sizes;
+    int64_t *trace;          /* concatenated frontiers (when recorded) */
+    int64_t trace_len;
+    double *l2_log;          /* global GD only: n_logs + 1 entries */
+    int64_t cap, trace_cap;
+} orc_report;
+
+static void rep_init(orc_report *rep) {
+    memset(rep, 0, sizeof(*rep));
+    rep->converged = 1;
+    rep->min_residual = INFINITY;
+    rep->cap = 64;
+    rep->vol_log = malloc(sizeof(int64_t) * rep->cap);
+    rep->gamma_log = malloc(sizeof(double) * rep->cap);
+    rep->l1_log = malloc(sizeof(double) * (rep->cap + 1));
+    rep->l2_log = malloc(sizeof(double) * (rep->cap + 1));
+    rep->sign_log = malloc(sizeof(int8_t) * rep->cap);
+    rep->frontier_sizes = malloc(sizeof(int64_t) * rep->cap);
+    rep->trace_cap = 0;
+    rep->trace = NULL;
+}
+
+static void rep_grow(orc_report *rep) {
+    if (rep->n_logs < rep->cap) return;
+    rep->cap *= 2;
+    rep->vol_log = realloc(rep->vol_log, sizeof(int64_t) * rep->cap);
+    rep->gamma_log = realloc(rep->gamma_log, sizeof(double) * rep->cap);
+    rep->l1_log = realloc(rep->l1_log, sizeof(double) * (rep->cap + 1));
+    rep->l2_log = realloc(rep->l2_log, sizeof(double) * (rep->cap + 1));
+    rep->sign_log = realloc(rep->sign_log, sizeof(int8_t) * rep->cap);
+    rep->frontier_sizes = realloc(rep->frontier_sizes, sizeof(int64_t) * rep->cap);
+}
+
+static void rep_trace(orc_report *rep, const int64_t *f, int64_t cnt) {
+    if (rep->trace_len + cnt > rep->trace_cap) {
+        int64_t nc = rep->trace_cap ? rep->trace_cap : 256;
+        while (nc < rep->trace_len + cnt) nc *= 2;
+        rep->trace = realloc(rep->trace, sizeof(int64_t) * nc);
+        rep->trace_cap = nc;
+    }
+    memcpy(rep->trace + rep->trace_len, f, sizeof(int64_t) * cnt);
+    rep->trace_len += cnt;
+}
+
+void orc_report_free(orc_report *rep) {
+    free(rep->vol_log);
+    free(rep->gamma_log);
+    free(rep->l1_log);
+    free(rep->l2_log);
+    free(rep->sign_log);
+    free(rep->frontier_sizes);
+    free(rep->trace);
+    memset(rep, 0, sizeof(*rep));
+}
+
+int64_t orc_report_sizeof(void) { return (int64_t)sizeof(orc_report); }
+
+/* ------------------------------------------------------------------------ */
+/* numpy helpers                                                            */
+/* ------------------------------------------------------------------------ */
+
+/* numpy's pairwise summation (DOUBLE_pairwise_sum, PW_BLOCKSIZE 128) of
+ * |a_i| (take_abs) or a_i: what float(np.abs(v).sum()) evaluates. */
+static double pw_sum(const double *a, int64_t n, int take_abs) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int64_t i = 0; i < n; i++) res += take_abs ? fabs(a[i]) : a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int k = 0; k < 8; k++) r[k] = take_abs ? fabs(a[k]) : a[k];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int k = 0; k < 8; k++) r[k] += take_abs ? fabs(a[i + k]) : a[i + k];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += take_abs ? fabs(a[i]) : a[i];
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pw_sum(a, n2, take_abs) + pw_sum(a + n2, n - n2, take_abs);
+    }
+}
+
+double orc_pairwise_sum(const double *a, int64_t n, int32_t take_abs) {
+    return pw_sum(a, n, take_abs);
+}
+
+static double sumsq_pw(const double *a, int64_t n) {
+    double *sq = malloc(sizeof(double) * (n ? n : 1));
+    for (int64_t i = 0; i < n; i++) sq[i] = a[i] * a[i];
+    double s = pw_sum(sq, n, 0);
+    free(sq);
+    return s;
+}
+
+/* src/local_solvers.py:353-361 */
+static void l1_and_min(const double *r, int64_t n, double *l1, double *mn) {
+    double s = 0.0, m = INFINITY;
+    for (int64_t i = 0; i < n; i++) {
+        s += fabs(r[i]);
+        if (r[i] < m) m = r[i];
+    }
+    *l1 = s;
+    *mn = m;
+}
+
+/* ------------------------------------------------------------------------ */
+/* sweep-synchronous kernels: LocalGD / LocalCH                             */
+/* ------------------------------------------------------------------------ */
+
+/* src/local_solvers.py:267-292 (_apply_update_seq) */
+static int64_t apply_update_seq(const int64_t *off, const int64_t *tgt, const double *w,
+                                double *r, const int64_t *fr, int64_t fc, const double *vals,
+                                uint8_t *cmark, int64_t *cand) {
+    int64_t cc = 0;
+    for (int64_t i = 0; i < fc; i++) {
+        int64_t u = fr[i];
+        r[u] -= vals[i];
+        if (!cmark[u]) {
+            cmark[u] = 1;
+            cand[cc++] = u;
+        }
+    }
+    for (int64_t i = 0; i < fc; i++) {
+        int64_t u = fr[i];
+        double val = vals[i];
+        for (int64_t j = off[u]; j < off[u + 1]; j++) {
+            int64_t v = tgt[j];
+            r[v] += val * w[j];
+            if (!cmark[v]) {
+                cmark[v] = 1;
+                cand[cc++] = v;
+            }
+        }
+    }
+    return cc;
+}
+
+/* src/local_solvers.py:336-350 (_filter_frontier) */
+static int64_t filter_frontier(const double *r, const double *theta, const int64_t *cand,
+                               int64_t cc, uint8_t *cmark, int64_t *out, int sgn) {
+    int64_t fc = 0;
+    for (int64_t i = 0; i < cc; i++) {
+        int64_t u = cand[i];
+        cmark[u] = 0;
+        double ru = r[u];
+        int act = sgn ? (fabs(ru) >= theta[u]) : (ru >= theta[u]);
+        if (act) out[fc++] = u;
+    }
+    return fc;
+}
+
+typedef struct {
+    int64_t n;
+    const int64_t *off, *tgt;
+    const double *w, *theta;
+    double *x, *r;
+    uint8_t *cmark;
+    int64_t *cand, *fbuf, *front, fcount;
+    int sgn;
+} sweep_driver;
+
+/* src/local_solvers.py:367-391 (_SweepDriver.__init__), x/r caller-owned */
+static void drv_init(sweep_driver *d, int64_t n, const int64_t *off, const int64_t *tgt,
+                     const double *w, const double *theta, const double *b, double *x,
+                     double *r, int sgn, orc_report *rep) {
+    d->n = n; d->off = off; d->tgt = tgt; d->w = w; d->theta = theta;
+    d->x = x; d->r = r; d->sgn = sgn;
+    memcpy(r, b, sizeof(double) * n);
+    memset(x, 0, sizeof(double) * n);
+    d->cmark = calloc(n ? n : 1, 1);
+    d->cand = malloc(sizeof(int64_t) * (n ? n : 1));
+    d->fbuf = malloc(sizeof(int64_t) * (n ? n : 1));
+    d->front = malloc(sizeof(int64_t) * (n ? n : 1));
+    int64_t ns = 0;
+    for (int64_t i = 0; i < n; i++)   /* np.flatnonzero(sys.b) */
+        if (b[i] != 0.0) d->cand[ns++] = i;
+    d->fcount = filter_frontier(r, theta, d->cand, ns, d->cmark, d->fbuf, sgn);
+    memcpy(d->front, d->fbuf, sizeof(int64_t) * d->fcount);
+    double l1, mn;
+    l1_and_min(r, n, &l1, &mn);
+    rep->l1_log[0] = l1;
+    rep->min_residual = mn;
+}
+
+static void drv_free(sweep_driver *d) {
+    free(d->cmark); free(d->cand); free(d->fbuf); free(d->front);
+}
+
+/* src/local_solvers.py:393-415 (sequential branch) */
+static void drv_apply(sweep_driver *d, const double *vals) {
+    int64_t cc = apply_update_seq(d->off, d->tgt, d->w, d->r, d->front, d->fcount, vals,
+                                  d->cmark, d->cand);
+    d->fcount = filter_frontier(d->r, d->theta, d->cand, cc, d->cmark, d->fbuf, d->sgn);
+    memcpy(d->front, d->fbuf, sizeof(int64_t) * d->fcount);
+}
+
+/* src/local_solvers.py:417-422 */
+static void drv_log(sweep_driver *d, orc_report *rep, int64_t svol, double sgamma) {
+    rep_grow(rep);
+    int64_t t = rep->n_logs;
+    double prev = rep->l1_log[t];
+    rep->vol_log[t] = svol;
+    rep->gamma_log[t] = prev > 0 ? sgamma / prev : 0.0;
+    double l1, mn;
+    l1_and_min(d->r, d->n, &l1, &mn);
+    rep->l1_log[t + 1] = l1;
+    if (mn < rep->min_residual) rep->min_residual = mn;
+    rep->n_logs = t + 1;
+}
+
+static int64_t count_nonzero(const double *r, int64_t n) {
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; i++) c += (r[i] != 0.0);
+    return c;
+}
+
+/* src/local_solvers.py:428-470 (local_gd, parallel=False) */
+int orc_local_gd(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                 const double *theta, const double *b, double *x, double *r,
+                 int64_t max_sweeps, int32_t record_trace, orc_report *rep) {
+    rep_init(rep);
+    sweep_driver d;
+    drv_init(&d, n, off, tgt, w, theta, b, x, r, 0, rep);
+    double *vals = malloc(sizeof(double) * (n ? n : 1));
+    while (d.fcount) {
+        if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
+        rep_grow(rep);
+        rep->frontier_sizes[rep->n_logs] = d.fcount;
+        if (record_trace) rep_trace(rep, d.front, d.fcount);
+        int64_t svol = 0;
+        for (int64_t i = 0; i < d.fcount; i++) {
+            int64_t u = d.front[i];
+            svol += off[u + 1] - off[u];
+            vals[i] = r[u];
+        }
+        double sgamma = pw_sum(vals, d.fcount, 1);
+        for (int64_t i = 0; i < d.fcount; i++) x[d.front[i]] += vals[i];
+        drv_apply(&d, vals);
+        drv_log(&d, rep, svol, sgamma);
+        rep->total_ops += svol;
+        rep->sweeps += 1;
+    }
+    rep->support_size = count_nonzero(r, n);
+    free(vals);
+    drv_free(&d);
+    return 0;
+}
+
+/* src/local_solvers.py:473-538 (local_ch); mu, L resolved by the caller via
+ * the _cheby_bounds rule (src/local_solvers.py:541-558). */
+int orc_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                 const double *theta, const double *b, double *x, double *r, double mu,
+                 double L, int64_t max_sweeps, int32_t record_trace, orc_report *rep) {
+    rep_init(rep);
+    sweep_driver d;
+    drv_init(&d, n, off, tgt, w, theta, b, x, r, 1, rep);
+    double rho = (L - mu) / (L + mu);
+    double step0 = 2.0 / (L + mu);
+    double *mom = calloc(n ? n : 1, sizeof(double));
+    int64_t *stamp = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t i = 0; i < n; i++) stamp[i] = -2;
+    double b_l1 = pw_sum(b, n, 1);
+    double *rvals = malloc(sizeof(double) * (n ? n : 1));
+    double *vals = malloc(sizeof(double) * (n ? n : 1));
+    double delta = rho;
+    while (d.fcount) {
+        if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
+        int64_t t = rep->sweeps;
+        rep_grow(rep);
+        rep->frontier_sizes[rep->n_logs] = d.fcount;
+        if (record_trace) rep_trace(rep, d.front, d.fcount);
+        int64_t svol = 0;
+        for (int64_t i = 0; i < d.fcount; i++) {
+            int64_t u = d.front[i];
+            svol += off[u + 1] - off[u];
+            rvals[i] = r[u];
+        }
+        double sgamma = pw_sum(rvals, d.fcount, 1);
+        if (t == 0) {
+            for (int64_t i = 0; i < d.fcount; i++) vals[i] = step0 * rvals[i];
+        } else {
+            double delta_next = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
+            double coef_r = 4.0 * delta_next / (L - mu);
+            double coef_m = delta * delta_next;
+            for (int64_t i = 0; i < d.fcount; i++) {
+                int64_t u = d.front[i];
+                double prev = (stamp[u] == t - 1) ? mom[u] : 0.0;
+                vals[i] = coef_r * rvals[i] + coef_m * prev;
+            }
+            delta = delta_next;
+        }
+        for (int64_t i = 0; i < d.fcount; i++) {
+            int64_t u = d.front[i];
+            x[u] += vals[i];
+            mom[u] = vals[i];
+            stamp[u] = t;
+        }
+        drv_apply(&d, vals);
+        drv_log(&d, rep, svol, sgamma);
+        rep->total_ops += svol;
+        rep->sweeps += 1;
+        if (rep->l1_log[rep->n_logs] > 10.0 * b_l1) {
+            rep->converged = 0;
+            rep->diverged = 1;
+            break;
+        }
+    }
+    rep->support_size = count_nonzero(r, n);
+    free(mom); free(stamp); free(rvals); free(vals);
+    drv_free(&d);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* FIFO push kernel: LocalGS / LocalSOR / dynamic repair                    */
+/* ------------------------------------------------------------------------ */
+
+/* src/local_solvers.py:48-188 (_push_kernel).  dim = len(theta). */
+int orc_push_kernel(int64_t dim, const int64_t *off, const int64_t *tgt, const double *w,
+                    const double *theta, double *x, double *r, const int64_t *seeds,
+                    int64_t n_seeds, double omega, double x_gain, int32_t sgn,
+                    int64_t max_sweeps, orc_report *rep) {
+    rep_init(rep);
+    const int64_t sent = dim, qcap = dim + 2;
+    int64_t *queue = malloc(sizeof(int64_t) * qcap);
+    uint8_t *qmark = calloc(dim ? dim : 1, 1);
+    int64_t front = 0, rear = 0;
+    for (int64_t i = 0; i < n_seeds; i++) {
+        int64_t u = seeds[i];
+        double ru = r[u];
+        int act = sgn ? (fabs(ru) >= theta[u]) : (ru >= theta[u]);
+        if (act && !qmark[u]) {
+            queue[rear] = u;
+            rear = (rear + 1) % qcap;
+            qmark[u] = 1;
+        }
+    }
+    double l1 = 0.0, min_r = INFINITY;
+    for (int64_t i = 0; i < dim; i++) {
+        l1 += fabs(r[i]);
+        if (r[i] < min_r) min_r = r[i];
+    }
+    rep->l1_log[0] = l1;
+    int64_t sweeps = 0, total_ops = 0;
+    if (front == rear) goto done;
+    queue[rear] = sent;
+    rear = (rear + 1) % qcap;
+    int64_t svol = 0;
+    double sgamma = 0.0;
+    int saw_pos = 0, saw_neg = 0;
+    while (front != rear) {
+        int64_t u = queue[front];
+        front = (front + 1) % qcap;
+        if (u == sent) {
+            rep->n_logs = sweeps;
+            rep_grow(rep);
+            rep->vol_log[sweeps] = svol;
+            rep->gamma_log[sweeps] = l1 > 0.0 ? sgamma / l1 : 0.0;
+            rep->sign_log[sweeps] = (saw_pos && saw_neg) ? 2 : saw_pos ? 1 : saw_neg ? -1 : 0;
+            total_ops += svol;
+            sweeps += 1;
+            l1 = 0.0;
+            for (int64_t i = 0; i < dim; i++) {
+                l1 += fabs(r[i]);
+                if (r[i] < min_r) min_r = r[i];
+            }
+            rep->l1_log[sweeps] = l1;
+            rep->n_logs = sweeps;
+            if (front == rear) break;
+            if (sweeps >= max_sweeps) { rep->converged = 0; break; }
+            queue[rear] = sent;
+            rear = (rear + 1) % qcap;
+            svol = 0;
+            sgamma = 0.0;
+            saw_pos = saw_neg = 0;
+            continue;
+        }
+        qmark[u] = 0;
+        double ru = r[u];
+        if (sgn ? (fabs(ru) < theta[u]) : (ru < theta[u])) continue;
+        svol += off[u + 1] - off[u];
+        sgamma += fabs(ru);
+        if (ru > 0.0) saw_pos = 1;
+        else if (ru < 0.0) saw_neg = 1;
+        double res = omega * ru;
+        x[u] += x_gain * res;
+        r[u] = ru - res;
+        for (int64_t j = off[u]; j < off[u + 1]; j++) {
+            int64_t v = tgt[j];
+            double rv = r[v] + res * w[j];
+            r[v] = rv;
+            if (!qmark[v]) {
+                int act = sgn ? (fabs(rv) >= theta[v]) : (rv >= theta[v]);
+                if (act) {
+                    queue[rear] = v;
+                    rear = (rear + 1) % qcap;
+                    qmark[v] = 1;
+                }
+            }
+        }
+        if (!qmark[u]) {
+            double ru2 = r[u];
+            int act = sgn ? (fabs(ru2) >= theta[u]) : (ru2 >= theta[u]);
+            if (act) {
+                queue[rear] = u;
+                rear = (rear + 1) % qcap;
+                qmark[u] = 1;
+            }
+        }
+    }
+done:
+    rep->sweeps = sweeps;
+    rep->total_ops = total_ops;
+    rep->min_residual = min_r;
+    rep->support_size = count_nonzero(r, dim);
+    free(queue);
+    free(qmark);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* heat kernel: push on the stage-expanded system                           */
+/* ------------------------------------------------------------------------ */
+
+/* src/local_solvers.py:566-661 (_hk_push_kernel); v, r have (N+1)*n entries */
+int orc_hk_push(int64_t n, int64_t n_stages, const int64_t *off, const int64_t *tgt,
+                const double *base_w, const double *stage_w, const double *theta, double *v,
+                double *r, int64_t seed, int64_t max_sweeps, orc_report *rep) {
+    rep_init(rep);
+    const int64_t dim = (n_stages + 1) * n, sent = dim, qcap = dim + 2;
+    int64_t *queue = malloc(sizeof(int64_t) * qcap);
+    uint8_t *qmark = calloc(dim ? dim : 1, 1);
+    int64_t front = 0, rear = 0;
+    if (r[seed] >= theta[seed]) {
+        queue[rear++] = seed;
+        qmark[seed] = 1;
+    }
+    double l1 = 0.0, min_r = INFINITY;
+    for (int64_t i = 0; i < dim; i++) {
+        l1 += fabs(r[i]);
+        if (r[i] < min_r) min_r = r[i];
+    }
+    rep->l1_log[0] = l1;
+    int64_t sweeps = 0, total_ops = 0;
+    if (front == rear) goto done;
+    queue[rear] = sent;
+    rear = (rear + 1) % qcap;
+    int64_t svol = 0;
+    double sgamma = 0.0;
+    while (front != rear) {
+        int64_t idx = queue[front];
+        front = (front + 1) % qcap;
+        if (idx == sent) {
+            rep->n_logs = sweeps;
+            rep_grow(rep);
+            rep->vol_log[sweeps] = svol;
+            rep->gamma_log[sweeps] = l1 > 0.0 ? sgamma / l1 : 0.0;
+            total_ops += svol;
+            sweeps += 1;
+            l1 = 0.0;
+            for (int64_t i = 0; i < dim; i++) {
+                l1 += fabs(r[i]);
+                if (r[i] < min_r) min_r = r[i];
+            }
+            rep->l1_log[sweeps] = l1;
+            rep->n_logs = sweeps;
+            if (front == rear) break;
+            if (sweeps >= max_sweeps) { rep->converged = 0; break; }
+            queue[rear] = sent;
+            rear = (rear + 1) % qcap;
+            svol = 0;
+            sgamma = 0.0;
+            continue;
+        }
+        qmark[idx] = 0;
+        double ri = r[idx];
+        if (ri < theta[idx]) continue;
+        int64_t k = idx / n, u = idx - k * n;
+        svol += off[u + 1] - off[u];
+        sgamma += fabs(ri);
+        v[idx] += ri;
+        r[idx] = 0.0;
+        if (k < n_stages) {
+            double wk = stage_w[k];
+            int64_t base = k * n + n;
+            for (int64_t j = off[u]; j < off[u + 1]; j++) {
+                int64_t t = base + tgt[j];
+                double rt = r[t] + ri * wk * base_w[j];
+                r[t] = rt;
+                if (!qmark[t] && rt >= theta[t]) {
+                    queue[rear] = t;
+                    rear = (rear + 1) % qcap;
+                    qmark[t] = 1;
+                }
+            }
+        }
+    }
+done:
+    rep->sweeps = sweeps;
+    rep->total_ops = total_ops;
+    rep->min_residual = min_r;
+    rep->support_size = count_nonzero(r, dim);
+    free(queue);
+    free(qmark);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* global gradient descent (reference point)                                */
+/* ------------------------------------------------------------------------ */
+
+/* src/global_solvers.py:41-47 */
+static int any_active(const double *r, const double *theta, int64_t n, int sgn) {
+    for (int64_t i = 0; i < n; i++) {
+        double ri = sgn ? fabs(r[i]) : r[i];
+        if (ri >= theta[i]) return 1;
+    }
+    return 0;
+}
+
+/* src/global_solvers.py:124-152 (gradient_descent) + _scatter_full :63-71.
+ * l2_log uses sqrt(pairwise sum of squares) (np.linalg.norm goes through BLAS,
+ * so l2 parity is by tolerance only). */
+int orc_gradient_descent(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                         const double *theta, const double *b, double *x, double *r,
+                         int64_t max_sweeps, orc_report *rep) {
+    rep_init(rep);
+    memcpy(r, b, sizeof(double) * n);
+    memset(x, 0, sizeof(double) * n);
+    int64_t vol = off[n];
+    rep->l1_log[0] = pw_sum(r, n, 1);
+    rep->l2_log[0] = sqrt(sumsq_pw(r, n));
+    double *nxt = malloc(sizeof(double) * (n ? n : 1));
+    int conv = !any_active(r, theta, n, 0);
+    while (!conv && rep->sweeps < max_sweeps) {
+        for (int64_t i = 0; i < n; i++) x[i] += r[i];
+        memset(nxt, 0, sizeof(double) * n);
+        for (int64_t u = 0; u < n; u++) {
+            double val = r[u];
+            if (val == 0.0) continue;
+            for (int64_t j = off[u]; j < off[u + 1]; j++) nxt[tgt[j]] += val * w[j];
+        }
+        memcpy(r, nxt, sizeof(double) * n);
+        rep->n_logs = rep->sweeps;
+        rep_grow(rep);
+        rep->vol_log[rep->sweeps] = vol;
+        rep->sweeps += 1;
+        rep->total_ops += vol;
+        rep->l1_log[rep->sweeps] = pw_sum(r, n, 1);
+        rep->l2_log[rep->sweeps] = sqrt(sumsq_pw(r, n));
+        rep->n_logs = rep->sweeps;
+        conv = !any_active(r, theta, n, 0);
+    }
+    rep->converged = conv;
+    free(nxt);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* batched CPU baseline: the reference's per-seed local_gd, many threads    */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int64_t n;
+    const int64_t *off, *tgt;
+    const double *w, *theta;
+    double alpha;
+    const int64_t *seeds;
+    int64_t n_seeds, max_sweeps;
+    int64_t *out_sweeps, *out_ops, *out_pushes;
+    int32_t *out_conv;
+    double *out_xsum;
+    int64_t next;
+} batch_job;
+
+/* One seed exactly as `local_gd(dataclasses.replace(sys, b=alpha*e_s))`
+ * would run it (src/local_solvers.py:428-470), including the per-solve O(n)
+ * allocations and per-sweep O(n) l1 scans of the reference. */
+static void *batch_worker(void *arg) {
+    batch_job *J = arg;
+    int64_t n = J->n;
+    for (;;) {
+        int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+        if (i >= J->n_seeds) break;
+        double *b = calloc(n, sizeof(double));
+        double *x = malloc(sizeof(double) * n);
+        double *r = malloc(sizeof(double) * n);
+        b[J->seeds[i]] = J->alpha;
+        orc_report rep;
+        orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
+        int64_t pushes = 0;
+        for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
+        J->out_sweeps[i] = rep.sweeps;
+        J->out_ops[i] = rep.total_ops;
+        J->out_pushes[i] = pushes;
+        J->out_conv[i] = rep.converged;
+        if (J->out_xsum) J->out_xsum[i] = pw_sum(x, n, 0);
+        orc_report_free(&rep);
+        free(b); free(x); free(r);
+    }
+    return NULL;
+}
+
+int orc_batch_local_gd(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                       const double *theta, double alpha, const int64_t *seeds,
+                       int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
+                       int64_t *out_sweeps, int64_t *out_ops, int64_t *out_pushes,
+                       int32_t *out_conv, double *out_xsum) {
+    batch_job J = {n, off, tgt, w, theta, alpha, seeds, n_seeds, max_sweeps,
+                   out_sweeps, out_ops, out_pushes, out_conv, out_xsum, 0};
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, batch_worker, &J);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+    return 0;
+}
