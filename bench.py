@@ -1,0 +1,363 @@
+"""Throughput benchmark: batched LocalGD-PPR on an R-MAT graph of an OGB shape.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One step = one batch of seeds per GPU solved to convergence (weak scaling:
+the per-GPU batch is fixed).  Default workload = the north-star target:
+LocalGD-PPR alpha=0.1, eps=1e-7 on the ogbn-products shape (2,385,902 nodes,
+61,859,140 edges), 1,024 seeds per GPU per step drawn with the reference's
+sample_sources.  Prints one JSON line (rank 0).
+
+--impl reference times the reference algorithm on the host cores instead:
+the C restatement in oracle/ (the reference itself is Python+numba and does
+not travel to the GPU box), all host threads, a bounded seed sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPES = {"cora": (2_708, 5_278), "arxiv": (169_343, 1_166_243),
+          "products": (2_385_902, 61_859_140), "papers100M": (111_059_433, 1_615_685_872)}
+METRIC = "local PPR solves/sec and GTEPS (edges touched/s) vs HBM roofline, 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--shape", default="products", choices=sorted(SHAPES))
+    p.add_argument("--alpha", type=float, default=0.1)
+    p.add_argument("--eps", type=float, default=1e-7)
+    p.add_argument("--seeds", type=int, default=1024, help="seeds per GPU per step")
+    p.add_argument("--slots", type=int, default=0, help="seeds in flight (0 = auto)")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--graph-seed", type=int, default=0)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def make_graph(shape, seed, device):
+    """GPU-built R-MAT graph: (DeviceGraph, host CsrGraph-like with degrees)."""
+    from paper_2410_21634_b200.device import DeviceGraph
+    from paper_2410_21634_b200.gen import rmat_csr_device
+
+    n, m = SHAPES[shape]
+    row, col = rmat_csr_device(n, m, seed=seed, device=device)
+    dg = DeviceGraph.from_device(n, row, col, device=device)
+    row_h = row.cpu().numpy()
+    return dg, row, col, row_h
+
+
+class _HostGraph:
+    def __init__(self, n, offsets, targets=None):
+        self.n, self.offsets, self.targets = n, offsets, targets
+        self.degrees = np.diff(offsets)
+
+
+def cpu_reference(hg, alpha, eps, seeds, threads):
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w, theta=hg.theta)
+    return out, time.perf_counter() - t0
+
+
+def host_graph_full(n, row_h, col_t, alpha, eps):
+    """Reference layout on the host: int64 targets, per-arc weights, theta."""
+    from paper_2410_21634_b200.systems import theta_vector
+
+    hg = _HostGraph(n, row_h, col_t.cpu().numpy().astype(np.int64))
+    d = np.repeat(hg.degrees.astype(np.float64), hg.degrees)
+    hg.arc_w = (1.0 / d) * (1.0 - alpha)  # == src/systems.py:85-108 for "rw"
+    hg.theta = theta_vector(hg, eps * alpha)
+    return hg
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores."""
+    import torch
+    from paper_2410_21634_b200.metrics import sample_sources
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    n, m = SHAPES[args.shape]
+    if torch.cuda.is_available():  # input synthesis only; the timed path is CPU
+        _, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
+        hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
+        del row, col
+    else:
+        from paper_2410_21634_b200.synth import rmat_graph
+        g = rmat_graph(n, m, seed=args.graph_seed)
+        from paper_2410_21634_b200.systems import theta_vector
+        hg = _HostGraph(n, g.offsets, g.targets)
+        d = np.repeat(hg.degrees.astype(np.float64), hg.degrees)
+        hg.arc_w = (1.0 / d) * (1.0 - args.alpha)
+        hg.theta = theta_vector(hg, args.eps * args.alpha)
+    seeds = sample_sources(hg, args.seeds * (args.steps + args.warmup), seed=0)
+    # size the per-step sample from one calibration batch (bounded CPU work)
+    per = max(threads, 1)
+    _, dt = cpu_reference(hg, args.alpha, args.eps, seeds[:per], threads)
+    per_step = int(max(threads, min(len(seeds), per * max(1.0, 3.0 / max(dt, 1e-3)))))
+    times, ops, done = [], 0, 0
+    for k in range(args.warmup + args.steps):
+        sl = seeds[(k * per_step) % len(seeds):][:per_step]
+        out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads)
+        if k >= args.warmup:
+            times.append(dt)
+            ops += int(out["total_ops"].sum())
+            done += len(sl)
+    tot = sum(times)
+    value = done / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, n, m),
+        "gteps": ops / tot / 1e9,
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} seeds per step of the sample_sources batch, "
+                                   "reference local_gd restated in C (oracle/), per-seed O(n) "
+                                   "state as in the reference, one seed per thread"},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n, m):
+    return {"workload": f"batched LocalGD-PPR alpha={args.alpha} eps={args.eps:g}, "
+                        f"R-MAT {args.shape}-shape ({n:,} nodes, {m:,} edges), "
+                        f"{args.seeds} seeds/GPU/step from sample_sources",
+            "graph": f"rmat-{args.shape}", "n": n, "edges": m, "alpha": args.alpha,
+            "eps": args.eps, "seeds_per_gpu_per_step": args.seeds, "slots": args.slots,
+            "l2": "inputs larger than L2 (int32 col_idx %.0f MB + per-seed state)" % (8.0 * m / 1e6),
+            "parallelism": f"seed-sharded x{args.gpus}"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2410_21634_b200.batch import BatchSolver
+    from paper_2410_21634_b200.metrics import b_alg_bytes, sample_sources
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m = SHAPES[args.shape]
+    dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
+    hdeg = _HostGraph(n, row_h)
+    steps_total = args.warmup + args.steps
+    allseeds = sample_sources(hdeg, args.seeds * world * steps_total, seed=0)
+    mine = allseeds[rank::world]  # round-robin over the degree-ranked sample
+    batches = [mine[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
+    dseeds = [torch.as_tensor(b, device="cuda") for b in batches]
+    solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots)
+    stream = torch.cuda.current_stream()
+
+    def gather(res):
+        """NCCL gather of per-seed results (the only collective)."""
+        if world == 1:
+            return res["total_ops"].sum()
+        cnt = torch.tensor([res["x_total"]], device="cuda", dtype=torch.int64)
+        stats = torch.stack([res["sweeps"], res["total_ops"], res["pushes"]])
+        out = [torch.empty_like(stats) for _ in range(world)]
+        dist.all_gather(out, stats)
+        dist.all_reduce(cnt)
+        return out[0].sum()
+
+    for k in range(args.warmup):
+        gather(solver.solve_device(dseeds[k], stream=stream))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ops = pushes = solved = 0
+    kern_ms = 0.0
+    launches = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for k in range(args.warmup, steps_total):
+            res = solver.solve_device(dseeds[k], stream=stream)
+            gather(res)
+            kern_ms += solver.last_kernel_ms
+            launches += res["kernel_launches"]
+            ops += int(res["total_ops"].sum())
+            pushes += int(res["pushes"].sum())
+            solved += len(batches[k])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms, ops, pushes, solved, kern_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        dist.all_reduce(tsum)
+        ms = float(tmax[0])
+        ops, pushes, solved, kern_all = (float(v) for v in tsum)
+    sec = ms / 1e3
+    value = solved / sec
+    balg = b_alg_bytes(int(ops), int(pushes))
+    # roofline of the dominant kernel (the sweep loop), rank-0 device events
+    peak, peak_kind = peaks()
+    my_balg = b_alg_bytes(int(t[1]), int(t[2]))
+    achieved = my_balg / (float(t[4]) / 1e3) / 1e9
+    # e2e: the public host API with host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pin = {}
+        for k in range(args.warmup):
+            solver.solve(batches[k], out=pin)
+        torch.cuda.synchronize()
+        h2d = d2h = 0
+        t0 = time.perf_counter()
+        for k in range(args.warmup, steps_total):
+            o = solver.solve(batches[k], out=pin)
+            h2d += 8 * len(batches[k])
+            d2h += len(batches[k]) * (8 * 5 + 4) + 12 * len(o.x_vals)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if world > 1:
+            w = torch.tensor([wall], dtype=torch.float64, device="cuda")
+            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            wall = float(w[0])
+        e2e = {"value": (args.seeds * args.steps * world) / wall, "unit": "solves/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "timing": "host wall clock around solve_host (H2D seeds, D2H stats + sparse x), max over ranks"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
+        sample, spent, outs = [], 0.0, []
+        chunk = max(threads, 8)
+        pos = 0
+        ref_sweeps, ref_ops = [], []
+        while spent < args.cpu_seconds and pos < len(batches[args.warmup]):
+            sl = batches[args.warmup][pos:pos + chunk]
+            o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads)
+            spent += dt
+            sample.extend(sl.tolist())
+            ref_sweeps.append(o["sweeps"])
+            ref_ops.append(o["total_ops"])
+            pos += chunk
+        res = solver.solve(np.asarray(sample, dtype=np.int64))
+        parity = bool(np.array_equal(np.concatenate(ref_ops), res.total_ops)
+                      and np.array_equal(np.concatenate(ref_sweeps), res.sweeps))
+        cpu = {"value": len(sample) / spent, "unit": "solves/s", "cores": threads, "kind": "port",
+               "sample": f"first {len(sample)} seeds of the first timed batch, reference local_gd "
+                         "restated in C (oracle/), one seed per thread",
+               "parity_sweeps_ops_identical": parity}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, n, m),
+            "gteps": ops / sec / 1e9,
+            "b_alg_gb": balg / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "k_rounds (persistent sweep loop)",
+                         "kernel_ms_per_step": float(t[4]) / args.steps},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "slots": solver_slots(solver),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def solver_slots(solver):
+    return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/*
+ * gdiff.h -- C ABI of the B200 local-diffusion library (libgdiff.so).
+ *
+ * Drop-in boundary for the reference package's native layer: the numba
+ * kernels of /root/reference/pkg/src/graphdiff (cited as src/<file>:<line>)
+ * and the Python sweep drivers around them.  Array arguments follow the
+ * numpy layouts those kernels take (int64 CSR offsets/targets, float64
+ * vectors), plain pointers and sizes, no framework types; a ctypes binding
+ * can pass numpy buffers straight through.
+ *
+ * Memory: functions named *_device take device pointers and a cudaStream_t
+ * (passed as void*); every other pointer argument is host memory.  The
+ * library keeps graphs resident in HBM (gd_graph) so repeated solves on one
+ * graph do not re-upload it.
+ *
+ * Errors: every function returns GD_OK (0) or a negative code; the message
+ * of the last failure on the calling thread is available from
+ * gd_last_error().  Non-convergence is NOT an error: it is reported through
+ * gd_report.converged, like the reference.
+ *
+ * Numerics: single-system solvers are bit-exact with the reference
+ * (identical x, r, frontier traces, sweep/operation counts); see DESIGN.md.
+ */
+#ifndef GDIFF_H
+#define GDIFF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GD_OK 0
+#define GD_ERR_ARG (-1)
+#define GD_ERR_CUDA (-2)
+#define GD_ERR_OOM (-3)
+#define GD_ERR_CAPACITY (-4)
+#define GD_ERR_UNSUPPORTED (-5)
+
+/* scatter-weight rules: replace OperatorQ.arc_weights (src/systems.py:43-108) */
+#define GD_W_RW 0    /* w_j = fl(fl(1/d_u) * beta)  ("rw", and "gen" with b=0)  */
+#define GD_W_CONST 1 /* w_j = beta                  ("adj", Katz)             */
+#define GD_W_ARC 2   /* w_j = arc_w[j]              (any other operator)       */
+
+/* threshold rules: replace DiffusionSystem.theta (src/systems.py:157-160) */
+#define GD_T_DEGREE 0 /* theta_u = fl(coeff * d_u), +inf where d_u == 0 */
+#define GD_T_ARRAY 1  /* theta_u = theta[u]                            */
+
+typedef struct gd_graph gd_graph;
+
+typedef struct {
+    int32_t weight_rule;  /* GD_W_* */
+    int32_t theta_rule;   /* GD_T_* */
+    double beta;          /* operator damping (GD_W_RW / GD_W_CONST) */
+    double theta_coeff;   /* GD_T_DEGREE */
+    const double *arc_w;  /* GD_W_ARC: n_arcs entries (host) */
+    const double *theta;  /* GD_T_ARRAY: dim entries (host) */
+} gd_operator;
+
+/* Run report: mirrors LocalReport / SolveReport (src/reports.py:25-79) plus
+ * the frontier trace of SolverState (src/reports.py:14-22).  Arrays are
+ * owned by the library; release them with gd_report_free. */
+typedef struct {
+    int32_t converged;
+    int32_t diverged;        /* LocalCH abort (src/local_solvers.py:527-530) */
+    int64_t sweeps;
+    int64_t total_ops;       /* sum of vol(S_t) */
+    int64_t pushes;          /* sum of |S_t| */
+    double min_residual;
+    int64_t support_size;    /* count_nonzero(r) */
+    int64_t n_logs;          /* == sweeps */
+    int64_t *vol_log;        /* n_logs */
+    double *gamma_log;       /* n_logs */
+    double *l1_log;          /* n_logs + 1 */
+    int8_t *sign_log;        /* n_logs (FIFO solvers) */
+    int64_t *frontier_sizes; /* n_logs (sweep-synchronous solvers) */
+    int64_t *trace;          /* concatenated S_t when recorded */
+    int64_t trace_len;
+    double *l2_log;          /* n_logs + 1 (global GD) */
+} gd_report;
+
+/* ---- library ---------------------------------------------------------- */
+const char *gd_last_error(void);
+int gd_version(void);
+void gd_report_free(gd_report *rep);
+
+/* ---- graph (replaces CsrGraph arrays, src/graph.py:62-81) --------------- */
+/* Upload host int64 offsets[n+1] / targets[n_arcs] (canonical symmetric CSR)
+ * to HBM as int64 row_ptr + int32 col_idx + int32 degree. */
+int gd_graph_create(int64_t n, const int64_t *offsets, const int64_t *targets,
+                    int64_t n_arcs, int32_t device, gd_graph **out);
+/* Same from device buffers (int64 row_ptr, int32 col_idx), e.g. a graph
+ * generated on the GPU; the data is copied. */
+int gd_graph_create_device(int64_t n, const int64_t *d_row_ptr, const int32_t *d_col,
+                           int64_t n_arcs, int32_t device, gd_graph **out);
+int gd_graph_destroy(gd_graph *g);
+int gd_graph_info(const gd_graph *g, int64_t *n, int64_t *n_arcs, int64_t *d_max);
+
+/* ---- single-system solvers (host buffers in/out, bit-exact) ------------ */
+
+/* LocalGD: replaces local_gd (src/local_solvers.py:428-470) with its kernels
+ * _apply_update_seq :267-292, _filter_frontier :336-350, _l1_and_min :353-361.
+ * b: dim source; x, r: dim outputs. */
+int gd_local_gd(const gd_graph *g, const gd_operator *op, const double *b, double *x,
+                double *r, int64_t max_sweeps, int32_t record_trace, gd_report *rep);
+
+/* LocalCH: replaces local_ch (src/local_solvers.py:473-538); mu, L already
+ * resolved (the _cheby_bounds rule, :541-558). */
+int gd_local_ch(const gd_graph *g, const gd_operator *op, const double *b, double *x,
+                double *r, double mu, double L, int64_t max_sweeps, int32_t record_trace,
+                gd_report *rep);
+
+/* FIFO push: replaces _push_kernel (src/local_solvers.py:48-188); x, r are
+ * updated in place (LocalGS/LocalSOR, dynamic repair). */
+int gd_push_kernel(const gd_graph *g, const gd_operator *op, double *x, double *r,
+                   const int64_t *seeds, int64_t n_seeds, double omega, double x_gain,
+                   int32_t is_signed, int64_t max_sweeps, gd_report *rep);
+
+/* Heat-kernel push: replaces _hk_push_kernel (src/local_solvers.py:566-661).
+ * v, r: (n_stages+1)*n, in place; thresholds theta_coeff * d_u per stage
+ * (src/systems.py:295-299); base weights fl(1/d_u). */
+int gd_hk_push(const gd_graph *g, int64_t n_stages, const double *stage_w,
+               double theta_coeff, double *v, double *r, int64_t seed, int64_t max_sweeps,
+               gd_report *rep);
+
+/* Global gradient descent (reference point): replaces gradient_descent +
+ * _scatter_full + _any_active (src/global_solvers.py:41-71, :124-152). */
+int gd_gradient_descent(const gd_graph *g, const gd_operator *op, const double *b,
+                        double *x, double *r, int64_t max_sweeps, gd_report *rep);
+
+/* ---- batched multi-seed solves (new; no reference counterpart) --------- */
+/* A batch solves PPR systems (I - (1-alpha) A D^-1) x = alpha e_s for many
+ * seeds s; the per-seed result equals local_gd(make_ppr_system(g, alpha, s,
+ * eps)) (same frontier sets, sweeps and operation counts; x to rounding of
+ * the atomic scatter order).  Per-seed state lives in `slots` dense HBM
+ * vectors that are reset through dirty lists, never memset. */
+#define GD_M_LOCAL_GD 0
+
+typedef struct gd_batch gd_batch;
+
+typedef struct {
+    int32_t method;      /* GD_M_* */
+    int32_t slots;       /* seeds in flight on the device; 0 = auto */
+    double alpha;
+    double eps;
+    int64_t max_sweeps;
+    int64_t frontier_cap; /* max frontier entries per round; 0 = auto */
+    int64_t out_cap;      /* max output (node, x) pairs per solve; 0 = auto */
+} gd_batch_params;
+
+typedef struct {
+    /* per-seed, device arrays of n_seeds entries owned by the batch */
+    int64_t *sweeps, *total_ops, *pushes, *support;
+    int32_t *converged;
+    int64_t *x_offset, *x_count;  /* segment of seed i in x_nodes/x_vals */
+    int32_t *x_nodes;
+    double *x_vals;
+    int64_t x_total;              /* filled after synchronisation */
+    int64_t kernel_launches;      /* kernels this solve launched */
+} gd_batch_result;
+
+int gd_batch_create(const gd_graph *g, const gd_batch_params *p, gd_batch **out);
+int gd_batch_destroy(gd_batch *b);
+/* d_seeds: device int64[n_seeds]; results stay on the device in *res.
+ * stream: cudaStream_t (NULL = legacy default stream). */
+int gd_batch_solve_device(gd_batch *b, const int64_t *d_seeds, int64_t n_seeds,
+                          gd_batch_result *res, void *stream);
+/* Host entry: seeds from host memory, per-seed stats and the sparse x
+ * copied back into caller buffers (pinned memory recommended).  x buffers
+ * hold x_cap pairs; GD_ERR_CAPACITY (with *x_total set) if too small. */
+int gd_batch_solve_host(gd_batch *b, const int64_t *seeds, int64_t n_seeds,
+                        int64_t *sweeps, int64_t *total_ops, int64_t *pushes,
+                        int32_t *converged, int64_t *x_offset, int64_t *x_count,
+                        int32_t *x_nodes, double *x_vals, int64_t x_cap, int64_t *x_total,
+                        void *stream);
+/* Device time (ms) of the dominant kernel (the sweep loop) in the last
+ * solve, measured with CUDA events on the launching stream. */
+int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
+
+/* ---- synthetic graphs -------------------------------------------------- */
+/* R-MAT candidate edges [first, first+count) at `scale`, ids permuted and
+ * encoded as key = min*n + max, or -1 when dropped (id >= n or self loop);
+ * identical to paper_2410_21634_b200.synth.rmat_edges + permute_ids. */
+int gd_rmat_keys_device(int32_t scale, int64_t n, int64_t first, int64_t count,
+                        uint64_t seed, double a, double b, double c, int64_t *d_keys,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDIFF_H */

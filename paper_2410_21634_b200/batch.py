@@ -1,0 +1,163 @@
+"""Batched multi-seed local diffusion (new API; no reference counterpart).
+
+A seed batch in the reference is a loop of ``local_gd`` calls, one system per
+seed (src/cli.py:150-190).  ``BatchSolver`` solves thousands of PPR systems
+per call on one GPU; per seed it returns what the reference's report holds
+for integer work (sweeps, total_ops, pushes, converged, support size) plus x
+as a sparse vector over the pushed nodes (x is zero elsewhere).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as gdl
+from .device import DeviceGraph, device_graph
+
+__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch"]
+
+
+class _CudaView:
+    """Expose a raw device pointer to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+@dataclass
+class BatchOutput:
+    sweeps: np.ndarray
+    total_ops: np.ndarray
+    pushes: np.ndarray
+    converged: np.ndarray
+    x_offset: np.ndarray
+    x_count: np.ndarray
+    x_nodes: np.ndarray
+    x_vals: np.ndarray
+
+    def x_sparse(self, i: int) -> tuple[np.ndarray, np.ndarray]:
+        a, c = int(self.x_offset[i]), int(self.x_count[i])
+        return self.x_nodes[a:a + c], self.x_vals[a:a + c]
+
+    def x_dense(self, i: int, n: int) -> np.ndarray:
+        x = np.zeros(n)
+        nodes, vals = self.x_sparse(i)
+        x[nodes] = vals
+        return x
+
+
+class BatchSolver:
+    """Solve (I - (1-alpha) A D^-1) x = alpha e_s for many seeds s."""
+
+    def __init__(self, g, alpha: float, eps: float, slots: int = 0,
+                 max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
+                 device: int = 0):
+        if not 0.0 < alpha <= 1.0:
+            raise ValueError("alpha must be in (0, 1]")
+        self.lib = gdl.load()
+        self.graph = g if isinstance(g, DeviceGraph) else device_graph(g, device)
+        self.alpha, self.eps = float(alpha), float(eps)
+        p = gdl.BatchParams(method=gdl.GD_M_LOCAL_GD, slots=int(slots), alpha=self.alpha,
+                            eps=self.eps, max_sweeps=int(max_sweeps),
+                            frontier_cap=int(frontier_cap), out_cap=int(out_cap))
+        h = C.c_void_p()
+        gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle and self.handle.value:
+            self.lib.gd_batch_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def last_kernel_ms(self) -> float:
+        ms = C.c_double()
+        gdl.check(self.lib.gd_batch_last_kernel_ms(self.handle, C.byref(ms)))
+        return ms.value
+
+    def solve_device(self, seeds, stream=None) -> dict:
+        """seeds: CUDA int64 tensor.  Returns torch CUDA tensors (views of the
+        solver's buffers, valid until the next solve)."""
+        import torch
+
+        seeds = seeds.to(dtype=torch.int64).contiguous()
+        k = int(seeds.numel())
+        res = gdl.BatchResult()
+        st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        gdl.check(self.lib.gd_batch_solve_device(self.handle, C.c_void_p(seeds.data_ptr()), k,
+                                                 C.byref(res), C.c_void_p(st)))
+
+        def view(p, cnt, typestr):
+            addr = C.cast(p, C.c_void_p).value
+            return torch.as_tensor(_CudaView(addr, (cnt,), typestr), device="cuda")
+
+        tot = int(res.x_total)
+        return {
+            "sweeps": view(res.sweeps, k, "<i8"), "total_ops": view(res.total_ops, k, "<i8"),
+            "pushes": view(res.pushes, k, "<i8"), "support": view(res.support, k, "<i8"),
+            "converged": view(res.converged, k, "<i4"), "x_offset": view(res.x_offset, k, "<i8"),
+            "x_count": view(res.x_count, k, "<i8"), "x_nodes": view(res.x_nodes, max(tot, 1), "<i4")[:tot],
+            "x_vals": view(res.x_vals, max(tot, 1), "<f8")[:tot], "x_total": tot,
+            "kernel_launches": int(res.kernel_launches),
+        }
+
+    def solve(self, seeds, x_cap: int | None = None, stream=None, out: dict | None = None) -> BatchOutput:
+        """Host path: seeds from host memory, results copied back to host.
+
+        ``out`` may hold preallocated (pinned) numpy buffers to reuse."""
+        sd = np.ascontiguousarray(seeds, dtype=np.int64)
+        k = sd.shape[0]
+        if out is None or out["sweeps"].shape[0] < k:
+            out = {"sweeps": np.empty(k, np.int64), "total_ops": np.empty(k, np.int64),
+                   "pushes": np.empty(k, np.int64), "converged": np.empty(k, np.int32),
+                   "x_offset": np.empty(k, np.int64), "x_count": np.empty(k, np.int64)}
+        cap = x_cap if x_cap is not None else (out["x_nodes"].shape[0] if "x_nodes" in out else 1 << 20)
+        st = 0
+        if stream is not None:
+            st = stream.cuda_stream
+        for _ in range(3):
+            if "x_nodes" not in out or out["x_nodes"].shape[0] < cap:
+                out["x_nodes"] = np.empty(cap, np.int32)
+                out["x_vals"] = np.empty(cap, np.float64)
+            tot = C.c_int64()
+            rc = self.lib.gd_batch_solve_host(
+                self.handle, gdl.ptr(sd, C.c_int64), k, gdl.ptr(out["sweeps"], C.c_int64),
+                gdl.ptr(out["total_ops"], C.c_int64), gdl.ptr(out["pushes"], C.c_int64),
+                gdl.ptr(out["converged"], C.c_int32), gdl.ptr(out["x_offset"], C.c_int64),
+                gdl.ptr(out["x_count"], C.c_int64), gdl.ptr(out["x_nodes"], C.c_int32),
+                gdl.ptr(out["x_vals"]), int(out["x_nodes"].shape[0]), C.byref(tot), C.c_void_p(st))
+            if rc == gdl.GD_ERR_CAPACITY and tot.value > out["x_nodes"].shape[0]:
+                cap = int(tot.value * 1.25) + 1024
+                continue
+            gdl.check(rc)
+            t = int(tot.value)
+            return BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
+                               out["converged"][:k].astype(bool), out["x_offset"][:k],
+                               out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
+        raise gdl.GdiffError(gdl.GD_ERR_CAPACITY, "output sizing failed")
+
+
+def local_gd_batch(g, seeds, alpha: float, eps: float, slots: int = 0,
+                   max_sweeps: int = 1_000_000) -> BatchOutput:
+    """Batched LocalGD-PPR over `seeds` (host in, host out)."""
+    deg = np.asarray(g.degrees)
+    sd = np.asarray(seeds, dtype=np.int64)
+    if sd.size and (sd.min() < 0 or sd.max() >= g.n):
+        raise ValueError("seed out of range")
+    if sd.size and np.any(deg[sd] < 1):
+        raise ValueError("source must have at least one neighbor")
+    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps)
+    try:
+        return solver.solve(sd)
+    finally:
+        solver.close()

@@ -1,0 +1,167 @@
+// common.cuh -- shared device/host helpers of libgdiff (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+#include <new>
+
+#include "../../include/gdiff.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libgdiff is built for sm_100a only"
+#endif
+
+namespace gd {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const char *fmt, ...);
+
+struct Error {
+    int code;
+};
+
+#define GD_CUDA(call)                                                               \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            ::gd::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                            cudaGetErrorString(e_));                                \
+            throw ::gd::Error{e_ == cudaErrorMemoryAllocation ? GD_ERR_OOM         \
+                                                               : GD_ERR_CUDA};      \
+        }                                                                           \
+    } while (0)
+
+#define GD_CHECK_ARG(cond, msg)                                                     \
+    do {                                                                            \
+        if (!(cond)) {                                                              \
+            ::gd::set_error("invalid argument: %s", msg);                          \
+            throw ::gd::Error{GD_ERR_ARG};                                          \
+        }                                                                           \
+    } while (0)
+
+#define GD_LAUNCH_CHECK() GD_CUDA(cudaGetLastError())
+
+// Run a C-ABI body, mapping exceptions to return codes.
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return GD_OK;
+    } catch (const Error &e) {
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        set_error("host allocation failed");
+        return GD_ERR_OOM;
+    } catch (...) {
+        set_error("unexpected exception");
+        return GD_ERR_CUDA;
+    }
+}
+
+// ----------------------------------------------------------- device memory --
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) GD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// ------------------------------------------------------------------ graph --
+// HBM layout: int64 row_ptr[n+1], int32 col[n_arcs] (n < 2^31), int32 deg[n].
+// The degree array (4 B/node, 9.5 MB on the products shape) stays L2
+// resident and serves every per-arc threshold test without touching row_ptr.
+struct DevGraph {
+    int64_t n;
+    int64_t n_arcs;
+    const int64_t *row;
+    const int32_t *col;
+    const int32_t *deg;
+};
+
+}  // namespace gd
+
+struct gd_graph {
+    int device;
+    int64_t n, n_arcs, d_max;
+    gd::DBuf<int64_t> row;
+    gd::DBuf<int32_t> col;
+    gd::DBuf<int32_t> deg;
+    gd::DevGraph view() const { return gd::DevGraph{n, n_arcs, row.p, col.p, deg.p}; }
+};
+
+namespace gd {
+
+// --------------------------------------------------------- operator rules --
+// Device form of gd_operator (arrays already in HBM).
+struct DevOp {
+    int32_t wrule, trule;
+    double beta, tcoeff;
+    const double *arc_w;  // GD_W_ARC
+    const double *theta;  // GD_T_ARRAY
+};
+
+// w for the arcs of node u with degree d (per-node rules).  Both roundings
+// are explicit: fl(fl(1/d) * beta), exactly what src/systems.py:85-108 stores.
+__device__ __forceinline__ double node_weight(const DevOp &op, int32_t d) {
+    if (op.wrule == GD_W_CONST) return op.beta;
+    return __dmul_rn(__ddiv_rn(1.0, (double)d), op.beta);
+}
+
+__device__ __forceinline__ double arc_weight(const DevOp &op, double wnode, int64_t j) {
+    return op.wrule == GD_W_ARC ? op.arc_w[j] : wnode;
+}
+
+// theta_u = fl(coeff * d_u) for d_u > 0, +inf otherwise (src/systems.py:157-160).
+__device__ __forceinline__ double theta_of(const DevOp &op, int64_t u, int32_t d) {
+    if (op.trule == GD_T_ARRAY) return op.theta[u];
+    return d > 0 ? __dmul_rn(op.tcoeff, (double)d) : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+__device__ __forceinline__ bool is_active(double ru, double th, bool sgn) {
+    return sgn ? (fabs(ru) >= th) : (ru >= th);
+}
+
+// ------------------------------------------------------------- host glue --
+struct HostOp {
+    DevOp dev;
+    DBuf<double> arc_w, theta;
+};
+void upload_op(const gd_graph *g, const gd_operator *op, int64_t dim, HostOp &out,
+               cudaStream_t s);
+
+void report_alloc(gd_report *rep, int64_t cap);
+void report_push_log(gd_report *rep, int64_t &cap, int64_t vol, double gamma, double l1,
+                     int8_t sign, int64_t fsize);
+void report_trace(gd_report *rep, int64_t &tcap, const int64_t *f, int64_t cnt);
+
+inline int n_sms(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v > 0 ? v : 148;
+}
+
+}  // namespace gd

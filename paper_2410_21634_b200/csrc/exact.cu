@@ -1,0 +1,498 @@
+// exact.cu -- bit-exact sweep-synchronous LocalGD / LocalCH for one system.
+//
+// Reproduces src/local_solvers.py:364-538 bit for bit on the device:
+//   * gather   : vals_i from r[S_t]; x[S_t] += vals; r[S_t] -= vals
+//   * expand   : every arc (i, j) of the frontier gets its global position
+//                p = arcoff[i] + j (frontier order, then CSR order)
+//   * sort     : stable radix sort of (target v, p) pairs by v groups each
+//                target's contributions in frontier-index order
+//   * fold     : r[v] = fl(...fl(fl(r[v] + c_1) + c_2)...) in that order,
+//                with c = fl(vals_i * w_j) (no FMA) -- the reference's
+//                sequential arc loop (_apply_update_seq :282-291)
+//   * frontier : S_{t+1} = [u in S_t, active] ++ [first-touch order of new
+//                nodes, active] (_apply_update_seq + _filter_frontier), via
+//                a head flag at each target's smallest arc position p and
+//                two order-preserving compactions.
+// The batched throughput path (batch.cu) trades the sort for fp64 atomics.
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace gd {
+namespace {
+
+constexpr int TPB = 256;
+
+inline int blocks_for(int64_t n, int cap = 1 << 20) {
+    int64_t b = (n + TPB - 1) / TPB;
+    if (b < 1) b = 1;
+    return (int)(b < cap ? b : cap);
+}
+
+__device__ __forceinline__ int64_t bsearch_le(const int64_t *a, int64_t cnt, int64_t p) {
+    // largest i in [0, cnt) with a[i] <= p (a[0] == 0 <= p)
+    int64_t lo = 0, hi = cnt;
+    while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// ---- seeds -> initial frontier flags (filter of flatnonzero(b), :383-386)
+__global__ void k_flag_active_nodes(const int32_t *__restrict__ nodes, int64_t cnt,
+                                    const double *__restrict__ r, DevGraph g, DevOp op,
+                                    bool sgn, uint8_t *__restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = nodes[i];
+        flag[i] = is_active(r[u], theta_of(op, u, g.deg[u]), sgn) ? 1 : 0;
+    }
+}
+
+// ---- gather (LocalGD): src/local_solvers.py:452-456 and the first loop of
+// _apply_update_seq (:275-281)
+__global__ void k_gather_gd(const int32_t *__restrict__ F, int64_t f, double *__restrict__ x,
+                            double *__restrict__ r, double *__restrict__ vals,
+                            double *__restrict__ absv, double *__restrict__ wnode,
+                            int64_t *__restrict__ fdeg, int32_t *__restrict__ fstamp, int32_t t,
+                            DevGraph g, DevOp op) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = F[i];
+        double val = r[u];
+        vals[i] = val;
+        absv[i] = fabs(val);
+        x[u] = __dadd_rn(x[u], val);
+        r[u] = __dsub_rn(r[u], val);
+        int32_t d = g.deg[u];
+        fdeg[i] = d;
+        wnode[i] = node_weight(op, d);
+        fstamp[u] = t;
+    }
+}
+
+// ---- gather (LocalCH): src/local_solvers.py:507-522
+__global__ void k_gather_ch(const int32_t *__restrict__ F, int64_t f, double *__restrict__ x,
+                            double *__restrict__ r, double *__restrict__ vals,
+                            double *__restrict__ absv, double *__restrict__ wnode,
+                            int64_t *__restrict__ fdeg, int32_t *__restrict__ fstamp, int32_t t,
+                            double *__restrict__ mom, int32_t *__restrict__ mstamp,
+                            double step0, double coef_r, double coef_m, DevGraph g, DevOp op) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = F[i];
+        double rv = r[u];
+        absv[i] = fabs(rv);
+        double v;
+        if (t == 0) {
+            v = __dmul_rn(step0, rv);
+        } else {
+            double prev = (mstamp[u] == t - 1) ? mom[u] : 0.0;
+            v = __dadd_rn(__dmul_rn(coef_r, rv), __dmul_rn(coef_m, prev));
+        }
+        vals[i] = v;
+        x[u] = __dadd_rn(x[u], v);
+        mom[u] = v;
+        mstamp[u] = t;
+        r[u] = __dsub_rn(rv, v);
+        int32_t d = g.deg[u];
+        fdeg[i] = d;
+        wnode[i] = node_weight(op, d);
+        fstamp[u] = t;
+    }
+}
+
+// ---- expand: arc position p -> (target key, p)
+__global__ void k_expand(const int32_t *__restrict__ F, const int64_t *__restrict__ arcoff,
+                         int64_t f, int64_t P, DevGraph g, uint32_t *__restrict__ keys,
+                         uint32_t *__restrict__ pidx) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = bsearch_le(arcoff, f, p);
+        int32_t u = F[i];
+        keys[p] = (uint32_t)g.col[g.row[u] + (p - arcoff[i])];
+        pidx[p] = (uint32_t)p;
+    }
+}
+
+// ---- ordered fold, one thread per target segment (second loop of
+// _apply_update_seq, :282-291)
+__global__ void k_fold(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ sp,
+                       int64_t P, const int64_t *__restrict__ arcoff, int64_t f,
+                       const int32_t *__restrict__ F, const double *__restrict__ vals,
+                       const double *__restrict__ wnode, DevGraph g, DevOp op,
+                       double *__restrict__ r, const int32_t *__restrict__ fstamp, int32_t t,
+                       uint8_t *__restrict__ head) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = skeys[q];
+        if (q > 0 && skeys[q - 1] == v) continue;
+        double acc = r[v];
+        for (int64_t q2 = q; q2 < P && skeys[q2] == v; ++q2) {
+            int64_t p = sp[q2];
+            int64_t i = bsearch_le(arcoff, f, p);
+            double w = wnode[i];
+            if (op.wrule == GD_W_ARC) w = op.arc_w[g.row[F[i]] + (p - arcoff[i])];
+            acc = __dadd_rn(acc, __dmul_rn(vals[i], w));
+        }
+        r[v] = acc;
+        if (fstamp[v] != t) head[sp[q]] = 1;  // first touch of a node outside S_t
+    }
+}
+
+// ---- candidates that survive the filter (_filter_frontier :336-350)
+__global__ void k_flag_heads(const uint32_t *__restrict__ keys, const uint8_t *__restrict__ head,
+                             int64_t P, const double *__restrict__ r, DevGraph g, DevOp op,
+                             bool sgn, uint8_t *__restrict__ flag) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t h = head[p];
+        if (h) {
+            uint32_t v = keys[p];
+            h = is_active(r[v], theta_of(op, v, g.deg[v]), sgn) ? 1 : 0;
+        }
+        flag[p] = h;
+    }
+}
+
+// ---- deterministic l1 / min over r (_l1_and_min :353-361; fixed-shape tree)
+constexpr int RED_BLOCKS = 512;
+__global__ void k_l1_min_part(const double *__restrict__ r, int64_t n, double *__restrict__ ps,
+                              double *__restrict__ pm) {
+    __shared__ double ss[TPB], sm[TPB];
+    double s = 0.0, m = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < n; i += (int64_t)RED_BLOCKS * TPB) {
+        double v = r[i];
+        s += fabs(v);
+        m = v < m ? v : m;
+    }
+    ss[threadIdx.x] = s;
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = TPB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            ss[threadIdx.x] += ss[threadIdx.x + o];
+            double b = sm[threadIdx.x + o];
+            sm[threadIdx.x] = b < sm[threadIdx.x] ? b : sm[threadIdx.x];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ps[blockIdx.x] = ss[0];
+        pm[blockIdx.x] = sm[0];
+    }
+}
+
+__global__ void k_l1_min_final(const double *__restrict__ ps, const double *__restrict__ pm,
+                               double *__restrict__ out) {
+    __shared__ double ss[RED_BLOCKS], sm[RED_BLOCKS];
+    for (int i = threadIdx.x; i < RED_BLOCKS; i += blockDim.x) {
+        ss[i] = ps[i];
+        sm[i] = pm[i];
+    }
+    __syncthreads();
+    for (int o = RED_BLOCKS / 2; o > 0; o >>= 1) {
+        for (int i = threadIdx.x; i < o; i += blockDim.x) {
+            ss[i] += ss[i + o];
+            sm[i] = sm[i + o] < sm[i] ? sm[i + o] : sm[i];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = ss[0];
+        out[1] = sm[0];
+    }
+}
+
+__global__ void k_sum_block(const double *__restrict__ a, int64_t n, double *__restrict__ out) {
+    // single-block deterministic sum (frontier |vals| -> sgamma)
+    __shared__ double ss[TPB];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += TPB) s += a[i];
+    ss[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = TPB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) ss[threadIdx.x] += ss[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = ss[0];
+}
+
+__global__ void k_to_i64(const int32_t *__restrict__ a, int64_t n, int64_t *__restrict__ o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = a[i];
+}
+
+// numpy pairwise sum of |b| (np.abs(sys.b).sum(), :496)
+double pw_sum_abs(const double *a, int64_t n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int64_t i = 0; i < n; i++) res += fabs(a[i]);
+        return res;
+    } else if (n <= 128) {
+        double rr[8];
+        int64_t i;
+        for (int k = 0; k < 8; k++) rr[k] = fabs(a[k]);
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int k = 0; k < 8; k++) rr[k] += fabs(a[i + k]);
+        double res = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+        for (; i < n; i++) res += fabs(a[i]);
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pw_sum_abs(a, n2) + pw_sum_abs(a + n2, n - n2);
+}
+
+struct SweepSolver {
+    const gd_graph *G;
+    DevGraph g;
+    HostOp op;
+    int64_t n;
+    bool sgn;
+    cudaStream_t s = 0;
+    DBuf<double> x, r, vals, absv, wnode, mom, red_ps, red_pm, scal;
+    DBuf<int32_t> F, Fn, fstamp, mstamp, seeds;
+    DBuf<int64_t> fdeg, arcoff, trace64, cnt;
+    DBuf<uint32_t> keys, skeys, pidx, sp;
+    DBuf<uint8_t> head, flag;
+    DBuf<char> tmp;
+    int bits = 1;
+
+    void tmp_need(size_t bytes) { tmp.ensure(bytes ? bytes : 1); }
+
+    SweepSolver(const gd_graph *G_, const gd_operator *o, bool sgn_) : G(G_), sgn(sgn_) {
+        g = G->view();
+        n = G->n;
+        upload_op(G, o, n, op, s);
+        size_t nn = n ? n : 1;
+        x.alloc(nn); r.alloc(nn); vals.alloc(nn); absv.alloc(nn); wnode.alloc(nn);
+        F.alloc(nn); Fn.alloc(nn); fstamp.alloc(nn); seeds.alloc(nn);
+        fdeg.alloc(nn + 1); arcoff.alloc(nn + 1); trace64.alloc(nn); cnt.alloc(4);
+        red_ps.alloc(RED_BLOCKS); red_pm.alloc(RED_BLOCKS); scal.alloc(4);
+        flag.alloc(nn);
+        while ((1LL << bits) < n) ++bits;
+        GD_CUDA(cudaMemset(fstamp.p, 0xFF, sizeof(int32_t) * nn));  // -1: never in S_t
+    }
+
+    void reduce_l1_min(double *host2) {
+        k_l1_min_part<<<RED_BLOCKS, TPB, 0, s>>>(r.p, n, red_ps.p, red_pm.p);
+        k_l1_min_final<<<1, 256, 0, s>>>(red_ps.p, red_pm.p, scal.p);
+        GD_LAUNCH_CHECK();
+        GD_CUDA(cudaMemcpyAsync(host2, scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+    }
+
+    // S_0 = filter(flatnonzero(b)) in index order
+    int64_t init(const double *b) {
+        GD_CUDA(cudaMemcpy(r.p, b, sizeof(double) * n, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemset(x.p, 0, sizeof(double) * (n ? n : 1)));
+        std::vector<int32_t> nz;
+        for (int64_t i = 0; i < n; i++)
+            if (b[i] != 0.0) nz.push_back((int32_t)i);
+        int64_t cnt0 = (int64_t)nz.size();
+        if (!cnt0) return 0;
+        GD_CUDA(cudaMemcpy(seeds.p, nz.data(), sizeof(int32_t) * cnt0, cudaMemcpyHostToDevice));
+        k_flag_active_nodes<<<blocks_for(cnt0), TPB, 0, s>>>(seeds.p, cnt0, r.p, g, op.dev, sgn,
+                                                             flag.p);
+        GD_LAUNCH_CHECK();
+        size_t bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, seeds.p, flag.p, F.p, cnt.p, cnt0, s);
+        tmp_need(bytes);
+        cub::DeviceSelect::Flagged(tmp.p, bytes, seeds.p, flag.p, F.p, cnt.p, cnt0, s);
+        int64_t f = 0;
+        GD_CUDA(cudaMemcpyAsync(&f, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        return f;
+    }
+
+    // one sweep after the gather kernel ran; returns |S_{t+1}| and P
+    int64_t scatter_and_filter(int64_t f, int32_t t, int64_t *P_out, double *sgamma) {
+        // arc offsets: exclusive scan of frontier degrees (fdeg[f] = 0 -> total)
+        GD_CUDA(cudaMemsetAsync(fdeg.p + f, 0, sizeof(int64_t), s));
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, fdeg.p, arcoff.p, f + 1, s);
+        tmp_need(bytes);
+        cub::DeviceScan::ExclusiveSum(tmp.p, bytes, fdeg.p, arcoff.p, f + 1, s);
+        k_sum_block<<<1, TPB, 0, s>>>(absv.p, f, scal.p + 2);
+        GD_LAUNCH_CHECK();
+        int64_t P = 0;
+        GD_CUDA(cudaMemcpyAsync(&P, arcoff.p + f, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaMemcpyAsync(sgamma, scal.p + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        GD_CHECK_ARG(P < (1LL << 32), "frontier volume exceeds 2^32 arcs");
+        *P_out = P;
+        if (P > 0) {
+            keys.ensure(P); skeys.ensure(P); pidx.ensure(P); sp.ensure(P);
+            head.ensure(P);
+            if (flag.n < (size_t)P) flag.alloc(P);
+            GD_CUDA(cudaMemsetAsync(head.p, 0, P, s));
+            k_expand<<<blocks_for(P), TPB, 0, s>>>(F.p, arcoff.p, f, P, g, keys.p, pidx.p);
+            GD_LAUNCH_CHECK();
+            bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, skeys.p, pidx.p, sp.p,
+                                            (int64_t)P, 0, bits, s);
+            tmp_need(bytes);
+            cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, skeys.p, pidx.p, sp.p,
+                                            (int64_t)P, 0, bits, s);
+            k_fold<<<blocks_for(P), TPB, 0, s>>>(skeys.p, sp.p, P, arcoff.p, f, F.p, vals.p,
+                                                 wnode.p, g, op.dev, r.p, fstamp.p, t, head.p);
+            GD_LAUNCH_CHECK();
+        }
+        // 1) frontier members that stay active, in S_t order
+        k_flag_active_nodes<<<blocks_for(f), TPB, 0, s>>>(F.p, f, r.p, g, op.dev, sgn, flag.p);
+        GD_LAUNCH_CHECK();
+        bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, F.p, flag.p, Fn.p, cnt.p, f, s);
+        tmp_need(bytes);
+        cub::DeviceSelect::Flagged(tmp.p, bytes, F.p, flag.p, Fn.p, cnt.p, f, s);
+        int64_t c1 = 0;
+        GD_CUDA(cudaMemcpyAsync(&c1, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        int64_t c2 = 0;
+        if (P > 0) {
+            k_flag_heads<<<blocks_for(P), TPB, 0, s>>>(keys.p, head.p, P, r.p, g, op.dev, sgn,
+                                                       flag.p);
+            GD_LAUNCH_CHECK();
+            bytes = 0;
+            cub::DeviceSelect::Flagged(nullptr, bytes, (int32_t *)keys.p, flag.p, Fn.p + c1,
+                                       cnt.p + 1, P, s);
+            tmp_need(bytes);
+            cub::DeviceSelect::Flagged(tmp.p, bytes, (int32_t *)keys.p, flag.p, Fn.p + c1,
+                                       cnt.p + 1, P, s);
+            GD_CUDA(cudaMemcpyAsync(&c2, cnt.p + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaStreamSynchronize(s));
+        }
+        std::swap(F.p, Fn.p);
+        return c1 + c2;
+    }
+
+    void record(gd_report *rep, int64_t &tcap, int64_t f) {
+        k_to_i64<<<blocks_for(f), TPB, 0, s>>>(F.p, f, trace64.p);
+        GD_LAUNCH_CHECK();
+        std::vector<int64_t> h(f);
+        GD_CUDA(cudaMemcpyAsync(h.data(), trace64.p, sizeof(int64_t) * f, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        report_trace(rep, tcap, h.data(), f);
+    }
+
+    void finish(double *hx, double *hr, gd_report *rep) {
+        GD_CUDA(cudaMemcpy(hx, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(hr, r.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        int64_t nz = 0;
+        for (int64_t i = 0; i < n; i++) nz += (hr[i] != 0.0);
+        rep->support_size = nz;
+    }
+};
+
+}  // namespace
+}  // namespace gd
+
+using namespace gd;
+
+extern "C" {
+
+int gd_local_gd(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
+                int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && o && b && x && r && rep, "null pointer");
+        GD_CUDA(cudaSetDevice(G->device));
+        int64_t cap = 64, tcap = 0;
+        report_alloc(rep, cap);
+        SweepSolver S(G, o, false);
+        int64_t f = S.init(b);
+        double lm[2];
+        S.reduce_l1_min(lm);
+        rep->l1_log[0] = lm[0];
+        rep->min_residual = lm[1];
+        int32_t t = 0;
+        while (f) {
+            if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
+            if (record_trace) S.record(rep, tcap, f);
+            k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
+                                                        S.wnode.p, S.fdeg.p, S.fstamp.p, t, S.g,
+                                                        S.op.dev);
+            GD_LAUNCH_CHECK();
+            int64_t P = 0;
+            double sgamma = 0.0;
+            int64_t fnext = S.scatter_and_filter(f, t, &P, &sgamma);
+            double prev = rep->l1_log[rep->n_logs];
+            S.reduce_l1_min(lm);
+            report_push_log(rep, cap, P, prev > 0 ? sgamma / prev : 0.0, lm[0], 0, f);
+            if (lm[1] < rep->min_residual) rep->min_residual = lm[1];
+            rep->total_ops += P;
+            rep->pushes += f;
+            rep->sweeps += 1;
+            f = fnext;
+            ++t;
+        }
+        S.finish(x, r, rep);
+    });
+}
+
+int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
+                double mu, double L, int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && o && b && x && r && rep, "null pointer");
+        GD_CHECK_ARG(mu < L, "need mu < L");
+        GD_CUDA(cudaSetDevice(G->device));
+        int64_t cap = 64, tcap = 0;
+        report_alloc(rep, cap);
+        SweepSolver S(G, o, true);
+        size_t nn = S.n ? S.n : 1;
+        S.mom.alloc(nn);
+        S.mstamp.alloc(nn);
+        GD_CUDA(cudaMemset(S.mom.p, 0, sizeof(double) * nn));
+        GD_CUDA(cudaMemset(S.mstamp.p, 0xFE, sizeof(int32_t) * nn));  // never t-1 >= -1
+        int64_t f = S.init(b);
+        double lm[2];
+        S.reduce_l1_min(lm);
+        rep->l1_log[0] = lm[0];
+        rep->min_residual = lm[1];
+        const double rho = (L - mu) / (L + mu);
+        const double step0 = 2.0 / (L + mu);
+        const double b_l1 = pw_sum_abs(b, S.n);
+        double delta = rho;
+        int32_t t = 0;
+        while (f) {
+            if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
+            if (record_trace) S.record(rep, tcap, f);
+            double coef_r = 0.0, coef_m = 0.0;
+            if (t > 0) {
+                double delta_next = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
+                coef_r = 4.0 * delta_next / (L - mu);
+                coef_m = delta * delta_next;
+                delta = delta_next;
+            }
+            k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
+                                                        S.wnode.p, S.fdeg.p, S.fstamp.p, t,
+                                                        S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
+                                                        S.g, S.op.dev);
+            GD_LAUNCH_CHECK();
+            int64_t P = 0;
+            double sgamma = 0.0;
+            int64_t fnext = S.scatter_and_filter(f, t, &P, &sgamma);
+            double prev = rep->l1_log[rep->n_logs];
+            S.reduce_l1_min(lm);
+            report_push_log(rep, cap, P, prev > 0 ? sgamma / prev : 0.0, lm[0], 0, f);
+            if (lm[1] < rep->min_residual) rep->min_residual = lm[1];
+            rep->total_ops += P;
+            rep->pushes += f;
+            rep->sweeps += 1;
+            f = fnext;
+            ++t;
+            if (lm[0] > 10.0 * b_l1) {
+                rep->converged = 0;
+                rep->diverged = 1;
+                break;
+            }
+        }
+        S.finish(x, r, rep);
+    });
+}
+
+}  // extern "C"

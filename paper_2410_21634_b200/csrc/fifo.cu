@@ -1,0 +1,367 @@
+// fifo.cu -- exact FIFO push (LocalGS / LocalSOR / dynamic repair) and the
+// stage-expanded heat-kernel push, one warp per system.
+//
+// The reference kernels (_push_kernel src/local_solvers.py:48-188 and
+// _hk_push_kernel :566-661) are sequential Gauss-Seidel pushes: every pop
+// reads residuals written by the previous one, so a system is inherently a
+// single chain.  The chain runs in one warp; what parallelises is the arc
+// loop of each push: 32 lanes take 32 consecutive arcs of the row, and the
+// activation test's ballot + popc gives every newly active neighbour its
+// queue slot in CSR order, which keeps the FIFO (and thus every later pop,
+// the sweep boundaries and all logs) identical to the reference.  At each
+// sentinel the whole CTA rescans the residual for the l1/min logs, as the
+// reference does (:127-132).
+#include "common.cuh"
+
+namespace gd {
+namespace {
+
+constexpr int FIFO_THREADS = 1024;
+
+struct FifoArgs {
+    DevGraph g;
+    DevOp op;
+    int64_t dim;           // coordinates (n, or (N+1) n for the heat kernel)
+    double *x, *r;
+    int32_t *queue;        // ring of dim + 2 slots
+    uint8_t *qmark;
+    const int32_t *seeds;
+    int64_t n_seeds;
+    double omega, x_gain;
+    int sgn;
+    int64_t max_sweeps;
+    // heat kernel
+    int64_t n_stages;
+    const double *stage_w;
+    // logs
+    int64_t log_cap;
+    int64_t *vol_log;
+    double *gamma_log, *l1_log;
+    int8_t *sign_log;
+    int64_t *out;          // sweeps, total_ops, converged, pushes
+    double *out_min;
+};
+
+template <bool HK>
+__device__ __forceinline__ double coord_theta(const FifoArgs &A, int64_t idx) {
+    if (HK) {
+        int64_t u = idx % A.g.n;
+        int32_t d = A.g.deg[u];
+        return d > 0 ? __dmul_rn(A.op.tcoeff, (double)d) : __longlong_as_double(0x7ff0000000000000LL);
+    }
+    return theta_of(A.op, idx, A.g.deg[idx]);
+}
+
+// Block-wide l1 / min over r[0, dim): fixed-shape, deterministic.
+__device__ void block_l1_min(const FifoArgs &A, double *s_s, double *s_m, double &l1,
+                             double &mn) {
+    double s = 0.0, m = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t i = threadIdx.x; i < A.dim; i += FIFO_THREADS) {
+        double v = A.r[i];
+        s += fabs(v);
+        m = v < m ? v : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        double mo = __shfl_xor_sync(0xffffffffu, m, o);
+        m = mo < m ? mo : m;
+    }
+    int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_s[w] = s;
+        s_m[w] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ts = 0.0, tm = __longlong_as_double(0x7ff0000000000000LL);
+        for (int k = 0; k < FIFO_THREADS / 32; k++) {
+            ts += s_s[k];
+            tm = s_m[k] < tm ? s_m[k] : tm;
+        }
+        s_s[0] = ts;
+        s_m[0] = tm;
+    }
+    __syncthreads();
+    l1 = s_s[0];
+    mn = s_m[0];
+    __syncthreads();
+}
+
+template <bool HK>
+__global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
+    __shared__ double s_s[32], s_m[32];
+    __shared__ int64_t sh_front, sh_rear, sh_sweeps, sh_ops, sh_pushes, sh_svol;
+    __shared__ double sh_sgamma, sh_l1, sh_min;
+    __shared__ int sh_pos, sh_neg, sh_cmd, sh_conv;
+    const int64_t sent = A.dim, qcap = A.dim + 2;
+    const int lane = threadIdx.x & 31;
+    const bool w0 = threadIdx.x < 32;
+
+    if (threadIdx.x == 0) {  // seed enqueue, sequential (:59-69)
+        int64_t rear = 0;
+        for (int64_t i = 0; i < A.n_seeds; i++) {
+            int32_t u = A.seeds[i];
+            bool act = is_active(A.r[u], coord_theta<HK>(A, u), A.sgn);
+            if (act && !A.qmark[u]) {
+                A.queue[rear] = u;
+                rear = (rear + 1) % qcap;
+                A.qmark[u] = 1;
+            }
+        }
+        sh_front = 0;
+        sh_rear = rear;
+        sh_sweeps = sh_ops = sh_pushes = sh_svol = 0;
+        sh_sgamma = 0.0;
+        sh_pos = sh_neg = 0;
+        sh_conv = 1;
+    }
+    __syncthreads();
+    double l1, mn;
+    block_l1_min(A, s_s, s_m, l1, mn);
+    if (threadIdx.x == 0) {
+        sh_l1 = l1;
+        sh_min = mn;
+        A.l1_log[0] = l1;
+        sh_cmd = (sh_front == sh_rear) ? 2 : 0;
+        if (sh_cmd == 0) {
+            A.queue[sh_rear] = (int32_t)sent;
+            sh_rear = (sh_rear + 1) % qcap;
+        }
+    }
+    __syncthreads();
+
+    while (sh_cmd != 2) {
+        if (w0) {
+            int64_t front = sh_front, rear = sh_rear, svol = sh_svol, pushes = sh_pushes;
+            double sgamma = sh_sgamma;
+            int pos = sh_pos, neg = sh_neg;
+            for (;;) {
+                int64_t idx = A.queue[front];
+                front = (front + 1 == qcap) ? 0 : front + 1;
+                if (idx == sent) break;
+                if (lane == 0) A.qmark[idx] = 0;
+                double ru = A.r[idx];
+                double th = coord_theta<HK>(A, idx);
+                if (!is_active(ru, th, A.sgn)) {
+                    __syncwarp();
+                    continue;
+                }
+                int64_t u = HK ? idx % A.g.n : idx;
+                int64_t k = HK ? idx / A.g.n : 0;
+                int32_t d = A.g.deg[u];
+                int64_t rs = A.g.row[u];
+                svol += d;
+                sgamma += fabs(ru);
+                pushes += 1;
+                if (ru > 0.0) pos = 1;
+                else if (ru < 0.0) neg = 1;
+                double res;            // mass pushed along the arcs
+                int64_t tbase = 0;     // target coordinate offset
+                bool scatter = true;
+                if (HK) {
+                    if (lane == 0) {
+                        A.x[idx] = __dadd_rn(A.x[idx], ru);
+                        A.r[idx] = 0.0;
+                    }
+                    scatter = k < A.n_stages;
+                    res = scatter ? __dmul_rn(ru, A.stage_w[scatter ? k : 0]) : 0.0;
+                    tbase = (k + 1) * A.g.n;
+                } else {
+                    res = __dmul_rn(A.omega, ru);
+                    if (lane == 0) {
+                        A.x[idx] = __dadd_rn(A.x[idx], __dmul_rn(A.x_gain, res));
+                        A.r[idx] = __dsub_rn(ru, res);
+                    }
+                }
+                if (scatter) {
+                    double wn = HK ? __ddiv_rn(1.0, (double)d) : node_weight(A.op, d);
+                    for (int64_t base = 0; base < d; base += 32) {
+                        int64_t j = base + lane;
+                        bool act = false;
+                        int64_t t = 0;
+                        if (j < d) {
+                            t = tbase + A.g.col[rs + j];
+                            double w = HK ? wn : arc_weight(A.op, wn, rs + j);
+                            double rv = __dadd_rn(A.r[t], __dmul_rn(res, w));
+                            A.r[t] = rv;
+                            act = !A.qmark[t] && is_active(rv, coord_theta<HK>(A, t), A.sgn);
+                        }
+                        unsigned bal = __ballot_sync(0xffffffffu, act);
+                        if (act) {
+                            int64_t slot = rear + __popc(bal & ((1u << lane) - 1u));
+                            if (slot >= qcap) slot -= qcap;
+                            A.queue[slot] = (int32_t)t;
+                            A.qmark[t] = 1;
+                        }
+                        rear += __popc(bal);
+                        if (rear >= qcap) rear -= qcap;
+                    }
+                }
+                __syncwarp();
+                if (!HK) {  // self re-check (:176-185); qmark[u] was cleared at pop
+                    double ru2 = __dsub_rn(ru, res);
+                    if (is_active(ru2, th, A.sgn)) {
+                        if (lane == 0) {
+                            A.queue[rear] = (int32_t)idx;
+                            A.qmark[idx] = 1;
+                        }
+                        rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {  // sentinel: close the sweep (:102-126)
+                int64_t t = sh_sweeps;
+                if (t < A.log_cap) {
+                    A.vol_log[t] = svol;
+                    A.gamma_log[t] = sh_l1 > 0.0 ? sgamma / sh_l1 : 0.0;
+                    A.sign_log[t] = (pos && neg) ? 2 : pos ? 1 : neg ? -1 : 0;
+                }
+                sh_ops += svol;
+                sh_sweeps = t + 1;
+                sh_front = front;
+                sh_rear = rear;
+                sh_pushes = pushes;
+            }
+        }
+        __syncthreads();
+        block_l1_min(A, s_s, s_m, l1, mn);
+        if (threadIdx.x == 0) {
+            int64_t t = sh_sweeps;
+            if (t < A.log_cap) A.l1_log[t] = l1;
+            sh_l1 = l1;
+            if (mn < sh_min) sh_min = mn;
+            if (sh_front == sh_rear) {
+                sh_cmd = 2;
+            } else if (t >= A.max_sweeps) {
+                sh_conv = 0;
+                sh_cmd = 2;
+            } else {
+                A.queue[sh_rear] = (int32_t)sent;
+                sh_rear = (sh_rear + 1) % qcap;
+                sh_svol = 0;
+                sh_sgamma = 0.0;
+                sh_pos = sh_neg = 0;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        A.out[0] = sh_sweeps;
+        A.out[1] = sh_ops;
+        A.out[2] = sh_conv;
+        A.out[3] = sh_pushes;
+        A.out_min[0] = sh_min;
+    }
+}
+
+void run_fifo(const gd_graph *G, FifoArgs A, bool hk, double *hx, double *hr,
+              const int64_t *seeds, int64_t n_seeds, gd_report *rep) {
+    const int64_t dim = A.dim;
+    GD_CHECK_ARG(dim + 2 < (1LL << 31), "coordinate count must be < 2^31");
+    DBuf<double> x(dim ? dim : 1), r(dim ? dim : 1);
+    DBuf<int32_t> queue(dim + 2), sd(n_seeds ? n_seeds : 1);
+    DBuf<uint8_t> qmark(dim ? dim : 1);
+    int64_t log_cap = A.max_sweeps < (1 << 20) ? A.max_sweeps + 1 : (1 << 20);
+    DBuf<int64_t> vol(log_cap), out(4);
+    DBuf<double> gam(log_cap), l1(log_cap + 1), mn(1);
+    DBuf<int8_t> sgn(log_cap);
+    GD_CUDA(cudaMemcpy(x.p, hx, sizeof(double) * dim, cudaMemcpyHostToDevice));
+    GD_CUDA(cudaMemcpy(r.p, hr, sizeof(double) * dim, cudaMemcpyHostToDevice));
+    GD_CUDA(cudaMemset(qmark.p, 0, dim ? dim : 1));
+    std::vector<int32_t> s32(n_seeds);
+    for (int64_t i = 0; i < n_seeds; i++) {
+        GD_CHECK_ARG(seeds[i] >= 0 && seeds[i] < dim, "seed out of range");
+        s32[i] = (int32_t)seeds[i];
+    }
+    if (n_seeds)
+        GD_CUDA(cudaMemcpy(sd.p, s32.data(), sizeof(int32_t) * n_seeds, cudaMemcpyHostToDevice));
+    A.x = x.p; A.r = r.p; A.queue = queue.p; A.qmark = qmark.p; A.seeds = sd.p;
+    A.n_seeds = n_seeds; A.log_cap = log_cap; A.vol_log = vol.p; A.gamma_log = gam.p;
+    A.l1_log = l1.p; A.sign_log = sgn.p; A.out = out.p; A.out_min = mn.p;
+    if (hk) k_fifo<true><<<1, FIFO_THREADS>>>(A);
+    else k_fifo<false><<<1, FIFO_THREADS>>>(A);
+    GD_LAUNCH_CHECK();
+    GD_CUDA(cudaDeviceSynchronize());
+    int64_t o[4];
+    GD_CUDA(cudaMemcpy(o, out.p, sizeof(o), cudaMemcpyDeviceToHost));
+    int64_t cap = 64;
+    report_alloc(rep, cap);
+    int64_t nl = o[0] < log_cap ? o[0] : log_cap;
+    std::vector<int64_t> hv(nl);
+    std::vector<double> hg(nl), hl(nl + 1);
+    std::vector<int8_t> hs(nl);
+    if (nl) {
+        GD_CUDA(cudaMemcpy(hv.data(), vol.p, sizeof(int64_t) * nl, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(hg.data(), gam.p, sizeof(double) * nl, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(hs.data(), sgn.p, nl, cudaMemcpyDeviceToHost));
+    }
+    GD_CUDA(cudaMemcpy(hl.data(), l1.p, sizeof(double) * (nl + 1), cudaMemcpyDeviceToHost));
+    rep->l1_log[0] = hl[0];
+    for (int64_t t = 0; t < nl; t++) report_push_log(rep, cap, hv[t], hg[t], hl[t + 1], hs[t], 0);
+    rep->sweeps = o[0];
+    rep->total_ops = o[1];
+    rep->converged = (int32_t)o[2];
+    rep->pushes = o[3];
+    GD_CUDA(cudaMemcpy(&rep->min_residual, mn.p, sizeof(double), cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(hx, x.p, sizeof(double) * dim, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(hr, r.p, sizeof(double) * dim, cudaMemcpyDeviceToHost));
+    int64_t nz = 0;
+    for (int64_t i = 0; i < dim; i++) nz += (hr[i] != 0.0);
+    rep->support_size = nz;
+}
+
+}  // namespace
+}  // namespace gd
+
+using namespace gd;
+
+extern "C" {
+
+int gd_push_kernel(const gd_graph *G, const gd_operator *o, double *x, double *r,
+                   const int64_t *seeds, int64_t n_seeds, double omega, double x_gain,
+                   int32_t is_signed, int64_t max_sweeps, gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && o && x && r && rep && (seeds || n_seeds == 0), "null pointer");
+        GD_CUDA(cudaSetDevice(G->device));
+        HostOp op;
+        upload_op(G, o, G->n, op, 0);
+        FifoArgs A{};
+        A.g = G->view();
+        A.op = op.dev;
+        A.dim = G->n;
+        A.omega = omega;
+        A.x_gain = x_gain;
+        A.sgn = is_signed ? 1 : 0;
+        A.max_sweeps = max_sweeps;
+        run_fifo(G, A, false, x, r, seeds, n_seeds, rep);
+    });
+}
+
+int gd_hk_push(const gd_graph *G, int64_t n_stages, const double *stage_w, double theta_coeff,
+               double *v, double *r, int64_t seed, int64_t max_sweeps, gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && v && r && rep && (stage_w || n_stages == 0), "null pointer");
+        GD_CHECK_ARG(n_stages >= 0, "n_stages must be >= 0");
+        GD_CUDA(cudaSetDevice(G->device));
+        DBuf<double> sw(n_stages ? n_stages : 1);
+        if (n_stages)
+            GD_CUDA(cudaMemcpy(sw.p, stage_w, sizeof(double) * n_stages, cudaMemcpyHostToDevice));
+        FifoArgs A{};
+        A.g = G->view();
+        A.op = DevOp{GD_W_RW, GD_T_DEGREE, 1.0, theta_coeff, nullptr, nullptr};
+        A.dim = (n_stages + 1) * G->n;
+        A.omega = 1.0;
+        A.x_gain = 1.0;
+        A.sgn = 0;
+        A.max_sweeps = max_sweeps;
+        A.n_stages = n_stages;
+        A.stage_w = sw.p;
+        int64_t s1 = seed;
+        GD_CHECK_ARG(seed >= 0 && seed < G->n, "seed out of range");
+        // the reference enqueues the seed only when r[seed] >= theta[seed] (:576-579)
+        run_fifo(G, A, true, v, r, &s1, 1, rep);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's golden
+vectors and the CPU oracle.  Integer work (sweeps, operation counts,
+frontier traces) and x / r are bit-identical for the single-system solvers;
+residual-l1 / gamma logs (device reductions) agree to 1e-12 relative."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_graph, load_golden
+from helpers import assert_matches, build_system, local_cases, method_of, report_dict, solver_kwargs
+from paper_2410_21634_b200 import local_solvers as LS
+from paper_2410_21634_b200 import systems as S
+from paper_2410_21634_b200.global_solvers import GlobalConfig, gradient_descent
+
+pytestmark = pytest.mark.gpu
+FIXTURES = ["small.npz", "pa2000.npz", "cora.npz"]
+
+
+def _gpu_run(d, key):
+    sys_ = build_system(d, key)
+    m, kw = method_of(key), solver_kwargs(d, key)
+    if m == "local_gd":
+        return report_dict(*LS.local_gd(sys_, **kw))
+    if m == "local_ch":
+        return report_dict(*LS.local_ch(sys_, **kw))
+    if m == "local_gs" or m.startswith("local_gs_"):
+        return report_dict(*LS.local_gs(sys_, **kw))
+    if m.startswith("local_sor"):
+        return report_dict(*LS.local_sor(sys_, **kw))
+    raise ValueError(m)
+
+
+@pytest.mark.parametrize("fixture", FIXTURES)
+def test_local_solvers_match_reference(gpu, fixture):
+    d = load_golden(fixture)
+    for key in local_cases(d):
+        assert_matches(d, key, _gpu_run(d, key), logs_exact=False)
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.0, 5.0])
+def test_heat_kernel_matches_reference(gpu, small, tau):
+    g = golden_graph(small, "er60")
+    f, rep = LS.local_hk(g, tau, 0, 1e-4)
+    k = f"er60/hk/tau{tau}"
+    assert np.array_equal(f, small[f"{k}/f_hat"])
+    assert rep.sweeps == small[f"{k}/sweeps"] and rep.total_ops == small[f"{k}/total_ops"]
+    assert rep.vol_log == small[f"{k}/vol_log"].tolist()
+    assert rep.notes["stage_count"] == small[f"{k}/stage_count"]
+    np.testing.assert_allclose(rep.residual_l1_trace, small[f"{k}/l1_log"], rtol=1e-12)
+    # the reference test's oracle bound (tests/test_local_solvers.py:213-233)
+    sys_ = S.make_hk_system(g, tau, 0, 1e-4)
+    assert np.abs(f - small[f"{k}/series60"]).sum() <= 1e-4 + S.hk_paper_bound(sys_.op.stage_count)
+
+
+def test_heat_kernel_tiny_tau(gpu, small):
+    f, rep = LS.local_hk(golden_graph(small, "p2"), 1e-9, 0, 1e-3)
+    assert rep.converged and rep.sweeps == 1
+    np.testing.assert_allclose(f, [1.0, 0.0], atol=1e-8)
+    assert np.array_equal(f, small["p2/hk/tiny/f_hat"])
+
+
+def test_global_gd_matches_reference(gpu, small):
+    g = golden_graph(small, "er500")
+    st, rep = gradient_descent(S.make_ppr_system(g, 0.15, 0, 1e-6, symmetrized=True))
+    k = "er500/ppr/gd"
+    assert np.array_equal(st.x, small[f"{k}/x"]) and np.array_equal(st.r, small[f"{k}/r"])
+    assert rep.sweeps == small[f"{k}/sweeps"] and rep.total_ops == small[f"{k}/total_ops"]
+    np.testing.assert_allclose(rep.residual_l1_trace, small[f"{k}/l1_log"], rtol=1e-12)
+
+
+def test_dynamic_snapshots_match_reference(gpu, dyn):
+    from paper_2410_21634_b200.dynamic import make_pair, run_snapshots
+    from paper_2410_21634_b200.graph import EdgeEvent
+    g0 = golden_graph(dyn, "er120")
+    ev = dyn["events"]
+    batches = [[EdgeEvent("insert" if k else "delete", int(u), int(v))
+                for b, k, u, v in ev if b == bi] for bi in range(int(ev[:, 0].max()) + 1)]
+    for mode in ("dynamic", "static"):
+        reps, pair, gf = run_snapshots(g0, batches, make_pair(g0, 0.2, 0.2 * 1e-4, 0), mode=mode)
+        assert np.array_equal(pair.p, dyn[f"{mode}/p"]) and np.array_equal(pair.r, dyn[f"{mode}/r"])
+        assert [r.sweeps for r in reps] == dyn[f"{mode}/sweeps"].tolist()
+        assert [r.total_ops for r in reps] == dyn[f"{mode}/total_ops"].tolist()
+        assert np.array_equal(np.concatenate([np.asarray(r.vol_log, np.int64) for r in reps]),
+                              dyn[f"{mode}/vol_flat"])
+        assert np.array_equal(np.concatenate([np.asarray(r.notes["sweep_signs"], np.int8) for r in reps]),
+                              dyn[f"{mode}/signs_flat"])
+    assert np.array_equal(gf.targets, golden_graph(dyn, "final").targets)
+
+
+# ---- reference test bodies with the GPU solvers swapped in ----------------
+
+def test_single_sweep_closure(gpu):
+    from paper_2410_21634_b200.synth import path_graph
+    sys_ = S.make_ppr_system(path_graph(2), 0.9, 0, 0.9)
+    st, rep = LS.local_gd(sys_)
+    assert rep.converged and rep.sweeps == 1
+    assert np.array_equal(st.x, sys_.b)
+
+
+def test_error_contract_p2(gpu):
+    from paper_2410_21634_b200.metrics import error_norms
+    from paper_2410_21634_b200.synth import path_graph
+    g = path_graph(2)
+    sys_ = S.make_ppr_system(g, 0.5, 0, 0.01, symmetrized=True)
+    st, _ = LS.local_gd(sys_)
+    assert error_norms(st.x, S.dense_solve(sys_), g)["linf_dscaled"] <= 0.01
+    st, rep = LS.local_ch(S.make_ppr_system(g, 0.5, 0, 1e-4, symmetrized=True))
+    assert rep.converged
+    assert error_norms(st.x, S.dense_solve(sys_), g)["linf_dscaled"] <= 1e-4
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ppr_ops_bound(gpu, seed):
+    from paper_2410_21634_b200.synth import erdos_renyi
+    g = erdos_renyi(80, 0.08, seed=seed)
+    _, rep = LS.local_gs(S.make_ppr_system(g, 0.15, 0, 1e-4))
+    assert rep.converged and rep.total_ops <= int(np.ceil(1.0 / (1e-4 * 0.15)))
+
+
+def test_validation_errors(gpu, small):
+    g = golden_graph(small, "k3")
+    sys_ = S.make_ppr_system(g, 0.5, 0, 0.1)
+    bad = S.DiffusionSystem(op=sys_.op, b=-sys_.b, theta_coeff=sys_.theta_coeff, problem="ppr",
+                            alpha=0.5, eps=0.1, source=0)
+    with pytest.raises(ValueError):
+        LS.local_gd(bad)
+    with pytest.raises(ValueError):
+        LS.local_sor(sys_, omega=2.5)
+    with pytest.raises(ValueError):
+        LS.local_ch(sys_, mu=1.0, L=1.0)
+
+
+def test_zero_source_and_nonconvergence(gpu, small):
+    g = golden_graph(small, "er60")
+    sys_ = S.make_ppr_system(g, 0.5, 0, 0.1)
+    z = S.DiffusionSystem(op=sys_.op, b=np.zeros(g.n), theta_coeff=sys_.theta_coeff,
+                          problem="ppr", alpha=0.5, eps=0.1, source=0)
+    for fn in (LS.local_gd, LS.local_gs, LS.local_ch):
+        st, rep = fn(z)
+        assert rep.converged and rep.sweeps == 0 and rep.total_ops == 0
+    _, rep = LS.local_gs(S.make_ppr_system(g, 0.1, 0, 1e-9), max_sweeps=2)
+    assert not rep.converged and rep.sweeps == 2
+    _, rep = LS.local_gd(S.make_ppr_system(g, 0.1, 0, 1e-9), max_sweeps=3)
+    assert not rep.converged and rep.sweeps == 3
+
+
+def test_reference_style_system_with_arc_array(gpu, small):
+    """A system whose operator is given only as a per-arc array (the
+    reference's OperatorQ layout) goes through the GD_W_ARC / GD_T_ARRAY path
+    with the same bits."""
+    from types import SimpleNamespace
+    from oracle import oracle as O
+    g = golden_graph(small, "er500")
+    sys_ = S.make_ppr_system(g, 0.15, 0, 1e-6)
+    w = S.arc_weights_for(g, 0.85, "sym")  # a non-rule operator
+    op = SimpleNamespace(pkind="sym", beta=0.85, arc_weights=w, graph=g)
+    alt = SimpleNamespace(op=op, b=sys_.b, theta=sys_.theta, problem="gen", graph=g, dim=g.n,
+                          eps=1e-6, alpha=0.15, beta_exp=0.5)
+    st, rep = LS.local_gd(alt)
+    ref_sys = SimpleNamespace(op=op, b=sys_.b, theta=sys_.theta, graph=g, dim=g.n)
+    ref = O.local_gd(ref_sys)
+    assert np.array_equal(st.x, ref["x"]) and np.array_equal(st.r, ref["r"])
+    assert rep.sweeps == ref["sweeps"] and rep.total_ops == ref["total_ops"]

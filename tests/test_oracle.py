@@ -1,0 +1,96 @@
+"""The CPU oracle is pinned bit-for-bit against vectors produced by running the
+reference implementation (tests/golden/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_graph, load_golden
+from helpers import assert_matches, build_system, local_cases, method_of, solver_kwargs
+from oracle import oracle as O
+from paper_2410_21634_b200 import systems as S
+from paper_2410_21634_b200.metrics import sample_sources
+
+FIXTURES = ["small.npz", "pa2000.npz", "cora.npz"]
+
+
+def _oracle_run(d, key):
+    sys_ = build_system(d, key)
+    m, kw = method_of(key), solver_kwargs(d, key)
+    if m == "local_gd":
+        return O.local_gd(sys_, **kw)
+    if m == "local_ch":
+        return O.local_ch(sys_, **kw)
+    if m == "local_gs" or m.startswith("local_gs_"):
+        return O.local_sor(sys_, 1.0, **kw)
+    if m.startswith("local_sor"):
+        return O.local_sor(sys_, **kw)
+    raise ValueError(m)
+
+
+@pytest.mark.parametrize("fixture", FIXTURES)
+def test_oracle_local_solvers_bitwise(fixture):
+    d = load_golden(fixture)
+    keys = local_cases(d)
+    assert keys
+    for key in keys:
+        assert_matches(d, key, _oracle_run(d, key), logs_exact=True)
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.0, 5.0])
+def test_oracle_heat_kernel_bitwise(small, tau):
+    g = golden_graph(small, "er60")
+    out = O.local_hk(g, tau, 0, 1e-4)
+    k = f"er60/hk/tau{tau}"
+    assert np.array_equal(out["f_hat"], small[f"{k}/f_hat"])
+    assert out["sweeps"] == small[f"{k}/sweeps"]
+    assert out["total_ops"] == small[f"{k}/total_ops"]
+    assert np.array_equal(out["vol_log"], small[f"{k}/vol_log"])
+    assert np.array_equal(out["gamma_log"], small[f"{k}/gamma_log"])
+    assert np.array_equal(out["l1_log"], small[f"{k}/l1_log"])
+    assert out["stage_count"] == small[f"{k}/stage_count"]
+    assert out["residual_mass"] == small[f"{k}/residual_mass"]
+
+
+def test_oracle_global_gd_bitwise(small):
+    g = golden_graph(small, "er500")
+    sys_ = S.make_ppr_system(g, 0.15, 0, 1e-6, symmetrized=True)
+    out = O.gradient_descent(sys_)
+    k = "er500/ppr/gd"
+    assert np.array_equal(out["x"], small[f"{k}/x"]) and np.array_equal(out["r"], small[f"{k}/r"])
+    assert out["sweeps"] == small[f"{k}/sweeps"] and out["total_ops"] == small[f"{k}/total_ops"]
+    assert np.array_equal(out["l1_log"], small[f"{k}/l1_log"])
+    np.testing.assert_allclose(out["l2_log"], small[f"{k}/l2_log"], rtol=1e-12)
+
+
+def test_oracle_batch_matches_reference_per_seed(cora):
+    """Config 1 (cora-shape, 50 seeds): the threaded CPU baseline reproduces
+    the reference's per-seed sweeps / ops / pushes and sum(x)."""
+    g = golden_graph(cora, "cora")
+    seeds = cora["seeds"]
+    assert np.array_equal(sample_sources(g, 50, seed=0), seeds)
+    out = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=4)
+    assert np.array_equal(out["sweeps"], cora["batch/sweeps"])
+    assert np.array_equal(out["total_ops"], cora["batch/total_ops"])
+    assert np.array_equal(out["pushes"], cora["batch/pushes"])
+    assert out["converged"].all()
+    ref_sums = np.array([O.pairwise_sum(x) for x in cora["batch/x"]])
+    assert np.array_equal(out["xsum"], ref_sums)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 4099])
+def test_pairwise_sum_is_numpys(n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal(n) * 10.0 ** rng.uniform(-6, 3, n)
+    assert O.pairwise_sum(a) == float(a.sum())
+    assert O.pairwise_sum(a, take_abs=True) == float(np.abs(a).sum())
+
+
+def test_oracle_zero_source_and_max_sweeps(small):
+    g = golden_graph(small, "er60")
+    sys_ = S.make_ppr_system(g, 0.5, 0, 0.1)
+    z = S.DiffusionSystem(op=sys_.op, b=np.zeros(g.n), theta_coeff=sys_.theta_coeff,
+                          problem="ppr", alpha=0.5, eps=0.1, source=0)
+    out = O.local_gd(z)
+    assert out["sweeps"] == 0 and out["total_ops"] == 0 and out["converged"]
+    out = O.local_sor(S.make_ppr_system(g, 0.1, 0, 1e-9), 1.0, max_sweeps=2)
+    assert not out["converged"] and out["sweeps"] == 2
