@@ -146,6 +146,11 @@ typedef struct {
     int64_t max_sweeps;
     int64_t frontier_cap; /* max frontier entries per round; 0 = auto */
     int64_t out_cap;      /* max output (node, x) pairs per solve; 0 = auto */
+    int32_t relabel;      /* 1: run on a degree-descending renumbering of the
+                             graph (hubs contiguous: residual updates share
+                             sectors / stay in L2); ids in and out are the
+                             caller's.  Results are invariant. */
+    int32_t reserved;
 } gd_batch_params;
 
 typedef struct {

@@ -54,7 +54,8 @@ class Report(C.Structure):
 class BatchParams(C.Structure):
     _fields_ = [("method", C.c_int32), ("slots", C.c_int32), ("alpha", C.c_double),
                 ("eps", C.c_double), ("max_sweeps", C.c_int64),
-                ("frontier_cap", C.c_int64), ("out_cap", C.c_int64)]
+                ("frontier_cap", C.c_int64), ("out_cap", C.c_int64),
+                ("relabel", C.c_int32), ("reserved", C.c_int32)]
 
 
 class BatchResult(C.Structure):

@@ -20,6 +20,17 @@ from .device import DeviceGraph, device_graph
 __all__ = ["BatchSolver", "BatchOutput", "local_gd_batch"]
 
 
+def _host_array(count: int, dtype, pinned: bool) -> np.ndarray:
+    """Host buffer; page-locked (via torch) when pinned, so copies are async DMA."""
+    if not pinned:
+        return np.empty(count, dtype)
+    import torch
+
+    tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+           np.dtype(np.float64): torch.float64}[np.dtype(dtype)]
+    return torch.empty(max(count, 1), dtype=tdt, pin_memory=True).numpy()[:count]
+
+
 class _CudaView:
     """Expose a raw device pointer to torch via __cuda_array_interface__."""
 
@@ -55,7 +66,7 @@ class BatchSolver:
 
     def __init__(self, g, alpha: float, eps: float, slots: int = 0,
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
-                 device: int = 0):
+                 device: int = 0, relabel: bool = True):
         if not 0.0 < alpha <= 1.0:
             raise ValueError("alpha must be in (0, 1]")
         self.lib = gdl.load()
@@ -63,7 +74,8 @@ class BatchSolver:
         self.alpha, self.eps = float(alpha), float(eps)
         p = gdl.BatchParams(method=gdl.GD_M_LOCAL_GD, slots=int(slots), alpha=self.alpha,
                             eps=self.eps, max_sweeps=int(max_sweeps),
-                            frontier_cap=int(frontier_cap), out_cap=int(out_cap))
+                            frontier_cap=int(frontier_cap), out_cap=int(out_cap),
+                            relabel=int(bool(relabel)))
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
@@ -117,18 +129,20 @@ class BatchSolver:
         ``out`` may hold preallocated (pinned) numpy buffers to reuse."""
         sd = np.ascontiguousarray(seeds, dtype=np.int64)
         k = sd.shape[0]
-        if out is None or out["sweeps"].shape[0] < k:
-            out = {"sweeps": np.empty(k, np.int64), "total_ops": np.empty(k, np.int64),
-                   "pushes": np.empty(k, np.int64), "converged": np.empty(k, np.int32),
-                   "x_offset": np.empty(k, np.int64), "x_count": np.empty(k, np.int64)}
+        out = {} if out is None else out
+        pinned = bool(out.get("pinned", False))
+        if "sweeps" not in out or out["sweeps"].shape[0] < k:
+            for name, dt in (("sweeps", np.int64), ("total_ops", np.int64), ("pushes", np.int64),
+                             ("converged", np.int32), ("x_offset", np.int64), ("x_count", np.int64)):
+                out[name] = _host_array(k, dt, pinned)
         cap = x_cap if x_cap is not None else (out["x_nodes"].shape[0] if "x_nodes" in out else 1 << 20)
         st = 0
         if stream is not None:
             st = stream.cuda_stream
         for _ in range(3):
             if "x_nodes" not in out or out["x_nodes"].shape[0] < cap:
-                out["x_nodes"] = np.empty(cap, np.int32)
-                out["x_vals"] = np.empty(cap, np.float64)
+                out["x_nodes"] = _host_array(cap, np.int32, pinned)
+                out["x_vals"] = _host_array(cap, np.float64, pinned)
             tot = C.c_int64()
             rc = self.lib.gd_batch_solve_host(
                 self.handle, gdl.ptr(sd, C.c_int64), k, gdl.ptr(out["sweeps"], C.c_int64),
@@ -148,7 +162,7 @@ class BatchSolver:
 
 
 def local_gd_batch(g, seeds, alpha: float, eps: float, slots: int = 0,
-                   max_sweeps: int = 1_000_000) -> BatchOutput:
+                   max_sweeps: int = 1_000_000, relabel: bool = True) -> BatchOutput:
     """Batched LocalGD-PPR over `seeds` (host in, host out)."""
     deg = np.asarray(g.degrees)
     sd = np.asarray(seeds, dtype=np.int64)
@@ -156,7 +170,7 @@ def local_gd_batch(g, seeds, alpha: float, eps: float, slots: int = 0,
         raise ValueError("seed out of range")
     if sd.size and np.any(deg[sd] < 1):
         raise ValueError("source must have at least one neighbor")
-    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps)
+    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, relabel=relabel)
     try:
         return solver.solve(sd)
     finally:

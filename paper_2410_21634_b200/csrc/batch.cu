@@ -30,6 +30,7 @@
 //  * Thresholds come from an L2-resident int32 degree array
 //    (theta_v = fl(eps*alpha*d_v)), not a per-node double.
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <vector>
 
@@ -50,6 +51,7 @@ struct RoundArgs {
     double beta;    // 1 - alpha
     double tcoeff;  // eps * alpha
     int64_t n;
+    int64_t ld;     // slot stride (n rounded up to even: 16 B aligned slots)
     int64_t max_sweeps;
     int64_t fcap;
     double *x, *r;
@@ -59,9 +61,10 @@ struct RoundArgs {
     int64_t *frow;
     double *fcval;
     unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
-    unsigned long long *s_ops, *s_pushes;
+    unsigned long long *s_ops, *s_pushes, *s_negz;
     int32_t *s_last, *s_conv;
     int32_t *overflow;
+    const int32_t *perm;  // caller id -> relabeled id (nullable)
 };
 
 __device__ __forceinline__ double theta_deg(double tc, int32_t d) {
@@ -86,6 +89,15 @@ __device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, 
     if (lane == leader) base = atomicAdd(cnt + k, (unsigned long long)__popc(peers));
     base = __shfl_sync(peers, base, leader);
     list[(int64_t)k * n + (int64_t)base + __popc(peers & lanemask_lt())] = item;
+}
+
+// Count `flag` lanes into the per-slot counter k (warp-aggregated).
+__device__ __forceinline__ void slot_count(bool flag, int32_t k, unsigned long long *cnt) {
+    unsigned am = __ballot_sync(FULL, flag);
+    if (!flag) return;
+    unsigned peers = __match_any_sync(am, k);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1)
+        atomicAdd(cnt + k, (unsigned long long)__popc(peers));
 }
 
 // Append (k, v) with degree d to the next frontier (warp-aggregated, one
@@ -122,8 +134,6 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
     const int64_t W = nthreads >> 5, wid = gtid >> 5;
-    const int64_t n = A.n;
-
     for (int32_t t = 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const unsigned long long packed = *(volatile unsigned long long *)(A.fctr + cur);
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 int64_t key = fk[e];
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
-                int64_t idx = (int64_t)k * n + u;
+                int64_t idx = (int64_t)k * A.ld + u;
                 double val = A.r[idx];
                 double xo = A.x[idx];
                 A.x[idx] = __dadd_rn(xo, val);
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 A.fcval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 u = __double_as_longlong(xo) == 0 ? u : -1;  // first push of u?
             }
-            slot_append(live && u >= 0, k, u, n, A.pushed, A.pushed_cnt);
+            slot_append(live && u >= 0, k, u, A.ld, A.pushed, A.pushed_cnt);
             // per-slot counters, aggregated over lanes of the same slot
             unsigned am = __ballot_sync(FULL, live);
             if (live) {
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
                 const int64_t p = base + lane;
                 bool valid = p < p1;
-                bool first = false, cross = false;
+                bool first = false, cross = false, negz = false;
                 int32_t k = 0, v = 0, dv = 0;
                 if (valid) {
                     const int64_t key = A.fkey[cur][me];
@@ -208,12 +218,14 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                     v = A.g.col[A.frow[me] + (p - fa[me])];
                     dv = A.g.deg[v];
                     const double th = theta_deg(A.tcoeff, dv);
-                    const double old = atomicAdd(A.r + (int64_t)k * n + v, c);
+                    const double old = atomicAdd(A.r + (int64_t)k * A.ld + v, c);
                     const double nw = __dadd_rn(old, c);
                     first = __double_as_longlong(old) == 0;
+                    negz = __double_as_longlong(old) == (long long)0x8000000000000000ULL;
                     cross = (old < th) && (nw >= th);
                 }
-                slot_append(first, k, v, n, A.dirty, A.dirty_cnt);
+                slot_append(first, k, v, A.ld, A.dirty, A.dirty_cnt);
+                slot_count(negz, k, A.s_negz);
                 frontier_append(cross, k, v, dv, A, nxt);
                 e += __popc(upto);
             }
@@ -228,12 +240,14 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, int6
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
     int32_t s = (int32_t)seeds[k];
-    A.r[k * A.n + s] = alpha;
-    A.dirty[k * A.n] = s;
+    if (A.perm) s = A.perm[s];
+    A.r[k * A.ld + s] = alpha;
+    A.dirty[k * A.ld] = s;
     A.dirty_cnt[k] = 1;
     A.pushed_cnt[k] = 0;
     A.s_ops[k] = 0;
     A.s_pushes[k] = 0;
+    A.s_negz[k] = 0;
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
     int32_t d = A.g.deg[s];
@@ -254,14 +268,16 @@ struct OutArgs {
     double *xvals;
     int64_t xcap;
     unsigned long long *cursor;
+    const int32_t *inv;  // relabeled id -> caller id (nullable)
 };
 
-// Extract x over the pushed list, reset x/r over the pushed/dirty lists.
-__global__ void k_wave_finish(RoundArgs A, OutArgs O, int64_t seed_base) {
+// Per slot: extract x over the pushed list (and zero it), write the seed's
+// counters.  support = |dirty| - |pushed nodes whose r is still -0.0|: every
+// push writes -0.0, the first later contribution observes it (s_negz).
+__global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
     const int k = blockIdx.x;
-    const int64_t off = (int64_t)k * A.n;
+    const int64_t off = (int64_t)k * A.ld;
     __shared__ unsigned long long s_base;
-    __shared__ int s_sup[32];
     const int64_t pc = (int64_t)A.pushed_cnt[k];
     if (threadIdx.x == 0) s_base = atomicAdd(O.cursor, (unsigned long long)pc);
     __syncthreads();
@@ -271,31 +287,70 @@ __global__ void k_wave_finish(RoundArgs A, OutArgs O, int64_t seed_base) {
         double xv = A.x[off + u];
         A.x[off + u] = 0.0;
         if (b + i < O.xcap) {
-            O.xnodes[b + i] = u;
+            O.xnodes[b + i] = O.inv ? O.inv[u] : u;
             O.xvals[b + i] = xv;
         }
     }
-    const int64_t dc = (int64_t)A.dirty_cnt[k];
-    int sup = 0;
-    for (int64_t i = threadIdx.x; i < dc; i += blockDim.x) {
-        int32_t v = A.dirty[off + i];
-        sup += A.r[off + v] != 0.0;
-        A.r[off + v] = 0.0;
-    }
-    for (int o = 16; o > 0; o >>= 1) sup += __shfl_xor_sync(FULL, sup, o);
-    if ((threadIdx.x & 31) == 0) s_sup[threadIdx.x >> 5] = sup;
-    __syncthreads();
     if (threadIdx.x == 0) {
-        int64_t tot = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += s_sup[w];
         const int64_t si = seed_base + k;
+        const int64_t pushes = (int64_t)A.s_pushes[k];
         O.sweeps[si] = (int64_t)A.s_last[k] + 1;
         O.ops[si] = (int64_t)A.s_ops[k];
-        O.pushes[si] = (int64_t)A.s_pushes[k];
+        O.pushes[si] = pushes;
         O.conv[si] = A.s_conv[k];
-        O.support[si] = tot;
+        O.support[si] = (int64_t)A.dirty_cnt[k] - (pushes - (int64_t)A.s_negz[k]);
         O.xoff[si] = b;
         O.xcnt[si] = pc;
+    }
+}
+
+// Reset r of every slot: a write-only stream of zeros over the slot when its
+// touched set is large (a random 8 B reset costs a 32 B sector RMW), else a
+// scatter over the dirty list.  grid = (RESET_CHUNKS, slots).
+constexpr int RESET_CHUNKS = 32;
+__global__ void k_wave_reset(RoundArgs A) {
+    const int k = blockIdx.y;
+    const int64_t off = (int64_t)k * A.ld;
+    const int64_t dc = (int64_t)A.dirty_cnt[k];
+    if (dc * 8 > A.ld) {
+        double2 *r2 = reinterpret_cast<double2 *>(A.r + off);
+        const int64_t h = A.ld >> 1;
+        const int64_t per = (h + RESET_CHUNKS - 1) / RESET_CHUNKS;
+        const int64_t lo = blockIdx.x * per, hi = min(h, lo + per);
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) r2[i] = make_double2(0.0, 0.0);
+    } else {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dc;
+             i += (int64_t)RESET_CHUNKS * blockDim.x)
+            A.r[off + A.dirty[off + i]] = 0.0;
+    }
+}
+
+// ---- degree relabeling (setup): new id = rank by descending degree ------
+__global__ void k_iota(int32_t *ids, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        ids[i] = (int32_t)i;
+}
+
+__global__ void k_invert(const int32_t *__restrict__ inv, int32_t *__restrict__ perm,
+                         const int32_t *__restrict__ dsorted, int64_t *__restrict__ deg64,
+                         int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        perm[inv[i]] = (int32_t)i;
+        deg64[i] = dsorted[i];
+    }
+}
+
+__global__ void k_remap_rows(DevGraph g, const int32_t *__restrict__ inv,
+                             const int32_t *__restrict__ perm, const int64_t *__restrict__ row2,
+                             int32_t *__restrict__ col2) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < g.n;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t o = inv[i];
+        const int64_t rs = g.row[o], d = g.row[o + 1] - rs, rs2 = row2[i];
+        for (int64_t j = lane; j < d; j += 32) col2[rs2 + j] = perm[g.col[rs + j]];
     }
 }
 
@@ -305,14 +360,16 @@ __global__ void k_wave_finish(RoundArgs A, OutArgs O, int64_t seed_base) {
 using namespace gd;
 
 struct gd_batch {
-    const gd_graph *G;
+    const gd_graph *G;   // caller's graph
+    gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
+    DBuf<int32_t> perm, inv;
     gd_batch_params p;
     int slots;
     int grid;
     int64_t fcap, xcap;
     DBuf<double> x, r, fcval;
     DBuf<int32_t> dirty, pushed, s_last, s_conv, overflow;
-    DBuf<unsigned long long> dirty_cnt, pushed_cnt, fctr, s_ops, s_pushes, cursor;
+    DBuf<unsigned long long> dirty_cnt, pushed_cnt, fctr, s_ops, s_pushes, s_negz, cursor;
     DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow;
     // results
     DBuf<int64_t> sweeps, ops, pushes, support, xoff, xcnt;
@@ -322,12 +379,15 @@ struct gd_batch {
     double last_ms = 0.0;
     int64_t last_launches = 0;
 
+    const gd_graph *work() const { return R ? R : G; }
+
     RoundArgs args() {
         RoundArgs A{};
-        A.g = G->view();
+        A.g = work()->view();
         A.beta = 1.0 - p.alpha;
         A.tcoeff = p.eps * p.alpha;
         A.n = G->n;
+        A.ld = (G->n + 1) & ~1LL;
         A.max_sweeps = p.max_sweeps;
         A.fcap = fcap;
         A.x = x.p; A.r = r.p; A.dirty = dirty.p; A.pushed = pushed.p;
@@ -335,11 +395,14 @@ struct gd_batch {
         A.fkey[0] = fkey0.p; A.fkey[1] = fkey1.p; A.farc[0] = farc0.p; A.farc[1] = farc1.p;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_last = s_last.p; A.s_conv = s_conv.p;
+        A.s_negz = s_negz.p;
         A.overflow = overflow.p;
+        A.perm = R ? perm.p : nullptr;
         return A;
     }
     ~gd_batch() {
         for (auto e : ev) cudaEventDestroy(e);
+        delete R;
     }
 };
 
@@ -358,7 +421,8 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         B->ev.push_back(e);
     }
     OutArgs O{B->sweeps.p, B->ops.p, B->pushes.p, B->support.p, B->xoff.p, B->xcnt.p,
-              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p};
+              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p,
+              B->R ? B->inv.p : nullptr};
     RoundArgs A = B->args();
     int64_t launches = 0;
     for (int64_t w = 0; w < waves; ++w) {
@@ -372,9 +436,10 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_rounds, dim3(B->grid), dim3(BT), kargs,
                                             0, st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
-        k_wave_finish<<<(int)m, 256, 0, st>>>(A, O, base);
+        k_wave_extract<<<(int)m, 256, 0, st>>>(A, O, base);
+        k_wave_reset<<<dim3(RESET_CHUNKS, (unsigned)m), 256, 0, st>>>(A);
         GD_LAUNCH_CHECK();
-        launches += 3;
+        launches += 4;
     }
     GD_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
@@ -385,6 +450,47 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     }
     B->last_ms = ms;
     B->last_launches = launches;
+}
+
+// Degree-descending renumbering of the graph on the device (one-time setup).
+static void build_relabeled(gd_batch *B) {
+    const gd_graph *G = B->G;
+    const int64_t n = G->n;
+    if (n == 0) return;
+    DevGraph g = G->view();
+    DBuf<int32_t> ids(n), dsorted(n);
+    B->perm.alloc(n);
+    B->inv.alloc(n);
+    const int blocks = 4 * n_sms(G->device);
+    k_iota<<<blocks, 256>>>(ids.p, n);
+    GD_LAUNCH_CHECK();
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, g.deg, dsorted.p, ids.p, B->inv.p,
+                                              (int64_t)n);
+    DBuf<char> tmp(bytes ? bytes : 1);
+    cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, g.deg, dsorted.p, ids.p, B->inv.p,
+                                              (int64_t)n);
+    gd_graph *R = new gd_graph();
+    B->R = R;
+    R->device = G->device;
+    R->n = n;
+    R->n_arcs = G->n_arcs;
+    R->d_max = G->d_max;
+    R->row.alloc(n + 1);
+    R->col.alloc(G->n_arcs ? G->n_arcs : 1);
+    R->deg.alloc(n);
+    DBuf<int64_t> deg64(n + 1);
+    k_invert<<<blocks, 256>>>(B->inv.p, B->perm.p, dsorted.p, deg64.p, n);
+    GD_LAUNCH_CHECK();
+    GD_CUDA(cudaMemset(deg64.p + n, 0, sizeof(int64_t)));
+    bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg64.p, R->row.p, n + 1);
+    tmp.ensure(bytes ? bytes : 1);
+    cub::DeviceScan::ExclusiveSum(tmp.p, bytes, deg64.p, R->row.p, n + 1);
+    GD_CUDA(cudaMemcpy(R->deg.p, dsorted.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice));
+    k_remap_rows<<<blocks, 256>>>(g, B->inv.p, B->perm.p, R->row.p, R->col.p);
+    GD_LAUNCH_CHECK();
+    GD_CUDA(cudaDeviceSynchronize());
 }
 
 extern "C" {
@@ -402,6 +508,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
         try {
             B->G = G;
             B->p = *p;
+            if (p->relabel) build_relabeled(B);
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
             int slots = p->slots;
             if (slots <= 0) {
@@ -415,13 +522,13 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             if (p->frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
             B->fcap = fc;
             B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
-            const size_t sn = (size_t)slots * n;
+            const size_t sn = (size_t)slots * (size_t)((n + 1) & ~1LL);
             B->x.alloc(sn); B->r.alloc(sn);
             GD_CUDA(cudaMemset(B->x.p, 0, sizeof(double) * sn));
             GD_CUDA(cudaMemset(B->r.p, 0, sizeof(double) * sn));
             B->dirty.alloc(sn); B->pushed.alloc(sn);
             B->dirty_cnt.alloc(slots); B->pushed_cnt.alloc(slots);
-            B->s_ops.alloc(slots); B->s_pushes.alloc(slots);
+            B->s_ops.alloc(slots); B->s_pushes.alloc(slots); B->s_negz.alloc(slots);
             B->s_last.alloc(slots); B->s_conv.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
             B->fkey0.alloc(fc); B->fkey1.alloc(fc); B->farc0.alloc(fc); B->farc1.alloc(fc);
