@@ -181,6 +181,9 @@ int gd_batch_solve_host(gd_batch *b, const int64_t *seeds, int64_t n_seeds,
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
+/* Instrumentation of the last wave: per sweep round (F entries, P arcs,
+ * device globaltimer ns) as 3*min(cap, rounds) int64 values. */
+int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *rounds);
 
 /* ---- synthetic graphs -------------------------------------------------- */
 /* R-MAT candidate edges [first, first+count) at `scale`, ids permuted and

@@ -97,6 +97,15 @@ class BatchSolver:
         gdl.check(self.lib.gd_batch_last_kernel_ms(self.handle, C.byref(ms)))
         return ms.value
 
+    def round_log(self) -> np.ndarray:
+        """(rounds, 3) int64: frontier entries, arcs, device ns at round start
+        for the last wave of the last solve (instrumentation)."""
+        buf = np.zeros(3 * 4096, np.int64)
+        cnt = C.c_int64()
+        gdl.check(self.lib.gd_batch_round_log(self.handle, gdl.ptr(buf, C.c_int64), 4096,
+                                              C.byref(cnt)))
+        return buf[:3 * min(cnt.value, 4096)].reshape(-1, 3)
+
     def solve_device(self, seeds, stream=None) -> dict:
         """seeds: CUDA int64 tensor.  Returns torch CUDA tensors (views of the
         solver's buffers, valid until the next solve)."""

@@ -8,30 +8,32 @@
 //
 // Design (B200):
 //  * `slots` seeds run concurrently, each with dense x/r vectors in HBM
-//    (slot-major, n doubles each).  They are never memset: every touched
-//    coordinate is on a per-slot dirty list and is reset after extraction.
-//  * One persistent cooperative kernel runs all sweeps of a wave of seeds;
-//    sweeps of all slots advance together ("rounds"), with two grid
-//    barriers per round:
-//      phase A (one thread per frontier entry): vals = r[u]; x[u] += vals;
-//              r[u] = -0.0 (a pushed node; +0.0 means "never touched");
+//    (slot-major).  Between waves they are reset either by walking the rows
+//    of the pushed nodes (small touched sets) or by a write-only zero stream
+//    (large ones), never by a read-modify-write memset of everything.
+//  * The graph is renumbered once by descending degree with sorted rows:
+//    hubs, which receive most residual updates, form a contiguous block, so
+//    a warp's 32 atomics land in few sectors and stay L2 resident.
+//  * One persistent cooperative kernel runs all sweeps of a wave; sweeps of
+//    all slots advance together ("rounds"), two grid barriers per round:
+//      phase A (thread per frontier entry): vals = r[u]; x[u] += vals;
+//              r[u] = -0.0 (pushed; +0.0 means "never touched");
 //              c_u = fl(vals * fl(fl(1/d_u)*(1-alpha))) staged per entry.
 //      phase B (arc-balanced: every warp owns an equal slice of the round's
-//              concatenated arc space): r[v] += c_u with a returning fp64
-//              atomic.  The returned old value decides, without any extra
-//              memory traffic, (1) first touch (old == +0.0 -> dirty list)
-//              and (2) frontier entry: residuals only grow inside a round
-//              (all c_u > 0, pushed nodes restart from 0), so exactly one
-//              arc observes old < theta_v <= old + c; that arc appends
-//              (slot, v) to S_{t+1}.  No candidate list, no filter pass.
-//  * Frontier appends reserve (entries, arcs) with ONE packed 64-bit
-//    atomic per warp, so entry order and arc-offset order agree and the
-//    next round's arc space is a prefix sum for free.
-//  * Thresholds come from an L2-resident int32 degree array
+//              concatenated arc space, 4 chunks of 32 arcs in flight per
+//              lane): r[v] += c_u with a returning fp64 atomic.  The old
+//              value decides, with no extra memory traffic, (1) first touch
+//              (old == +0.0, counted) and (2) frontier entry: residuals only
+//              grow inside a round, so exactly one arc observes
+//              old < theta_v <= old + c and appends (slot, v) to S_{t+1}.
+//  * Frontier appends reserve (entries, arcs) with ONE packed 64-bit atomic
+//    per warp, so entry order and arc-offset order agree and the next
+//    round's arc space is a prefix sum for free.
+//  * Thresholds come from the L2-resident int32 degree array
 //    (theta_v = fl(eps*alpha*d_v)), not a per-node double.
 #include <cooperative_groups.h>
-#include <cub/cub.cuh>
 
+#include <cub/cub.cuh>
 #include <vector>
 
 #include "common.cuh"
@@ -41,10 +43,12 @@ namespace cg = cooperative_groups;
 namespace gd {
 namespace {
 
-constexpr int BT = 512;  // threads per block of the round kernel
+constexpr int BT = 512;   // threads per block of the round kernel
+constexpr int UNROLL = 4; // 32-arc chunks in flight per warp in phase B
 constexpr int CNT_SHIFT = 36;
 constexpr unsigned long long ARC_MASK = (1ULL << CNT_SHIFT) - 1ULL;
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int CHUNKS = 32;  // blocks per slot in the extract / reset kernels
 
 struct RoundArgs {
     DevGraph g;
@@ -54,18 +58,32 @@ struct RoundArgs {
     int64_t ld;     // slot stride (n rounded up to even: 16 B aligned slots)
     int64_t max_sweeps;
     int64_t fcap;
+    int64_t m;      // slots in use this wave
     double *x, *r;
-    int32_t *dirty, *pushed;
-    unsigned long long *dirty_cnt, *pushed_cnt;
+    int32_t *pushed;
+    int32_t *seed;  // per slot: seed in working ids
+    unsigned long long *touched, *pushed_cnt;
     int64_t *fkey[2], *farc[2];
     int64_t *frow;
     double *fcval;
+    int32_t *chunk_e;     // entry holding arc 32c of the round (phase A -> B)
+    int64_t ccap;         // chunk_e capacity
     unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
-    unsigned long long *s_ops, *s_pushes, *s_negz;
+    unsigned long long *s_ops, *s_pushes, *s_negz, *s_pvol;
     int32_t *s_last, *s_conv;
     int32_t *overflow;
-    const int32_t *perm;  // caller id -> relabeled id (nullable)
+    const int32_t *perm;  // caller id -> working id (nullable)
+    unsigned long long *cursor;  // output pool allocation
+    int64_t *slot_base;
+    int64_t *rlog;      // per round: F, P, globaltimer ns (3 entries), debug
+    int64_t rlog_cap;   // rounds recorded
 };
+
+__device__ __forceinline__ int64_t globaltimer() {
+    int64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ double theta_deg(double tc, int32_t d) {
     return d > 0 ? __dmul_rn(tc, (double)d) : __longlong_as_double(0x7ff0000000000000LL);
@@ -78,7 +96,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Append `item` to the per-slot list k (warp-aggregated by slot).
-__device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, int64_t n,
+__device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, int64_t ld,
                                             int32_t *list, unsigned long long *cnt) {
     unsigned am = __ballot_sync(FULL, flag);
     if (!flag) return;
@@ -88,16 +106,18 @@ __device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, 
     unsigned long long base = 0;
     if (lane == leader) base = atomicAdd(cnt + k, (unsigned long long)__popc(peers));
     base = __shfl_sync(peers, base, leader);
-    list[(int64_t)k * n + (int64_t)base + __popc(peers & lanemask_lt())] = item;
+    list[(int64_t)k * ld + (int64_t)base + __popc(peers & lanemask_lt())] = item;
 }
 
-// Count `flag` lanes into the per-slot counter k (warp-aggregated).
-__device__ __forceinline__ void slot_count(bool flag, int32_t k, unsigned long long *cnt) {
+// Add `val` of the flagged lanes to per-slot counter k: one fire-and-forget
+// reduction per slot present in the warp (no returned value to wait for).
+__device__ __forceinline__ void slot_add(bool flag, int32_t k, unsigned val,
+                                         unsigned long long *cnt) {
     unsigned am = __ballot_sync(FULL, flag);
     if (!flag) return;
     unsigned peers = __match_any_sync(am, k);
-    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1)
-        atomicAdd(cnt + k, (unsigned long long)__popc(peers));
+    unsigned sum = __reduce_add_sync(peers, val);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, (unsigned long long)sum);
 }
 
 // Append (k, v) with degree d to the next frontier (warp-aggregated, one
@@ -128,18 +148,159 @@ __device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v,
     }
 }
 
+// Block-level staging (shared memory): per-slot counters of the block and a
+// buffer of the block's next-frontier entries.  Flushed once per phase, so
+// global atomics on the shared frontier counter drop from one per warp with
+// a crossing to one per block per round.
+constexpr int STAGE_CAP = 3072;  // staged frontier entries per block per round
+
+struct Stage {
+    unsigned long long *ops, *pvol;      // [S]
+    unsigned *push, *touch, *negz;       // [S]
+    int32_t *fk, *fv, *fd;               // [STAGE_CAP]
+    unsigned *fcnt;                      // [1]
+    unsigned long long *scan;            // [BT/32 + 2]
+};
+
+__host__ __device__ inline size_t stage_bytes(int S) {
+    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 2) + 64;
+}
+
+__device__ Stage stage_carve(void *base, int S) {
+    char *p = (char *)base;
+    Stage st;
+    st.ops = (unsigned long long *)p; p += 8 * S;
+    st.pvol = (unsigned long long *)p; p += 8 * S;
+    st.scan = (unsigned long long *)p; p += 8 * (BT / 32 + 2);
+    st.push = (unsigned *)p; p += 4 * S;
+    st.touch = (unsigned *)p; p += 4 * S;
+    st.negz = (unsigned *)p; p += 4 * S;
+    st.fcnt = (unsigned *)p; p += 16;
+    st.fk = (int32_t *)p; p += 4 * STAGE_CAP;
+    st.fv = (int32_t *)p; p += 4 * STAGE_CAP;
+    st.fd = (int32_t *)p;
+    return st;
+}
+
+// Warp-aggregated add of `val` over flagged lanes into counter array cnt[k]
+// (shared-memory counters: cheap, no global contention).
+template <class T>
+__device__ __forceinline__ void block_count(bool flag, int32_t k, unsigned val, T *cnt) {
+    unsigned am = __ballot_sync(FULL, flag);
+    if (!flag) return;
+    unsigned peers = __match_any_sync(am, k);
+    unsigned sum = __reduce_add_sync(peers, val);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, (T)sum);
+}
+
+// Stage (k, v, d) in the block buffer; lanes beyond its capacity append
+// straight to the global frontier.
+__device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, int32_t d,
+                                             const Stage &S, const RoundArgs &A, int nxt) {
+    unsigned am = __ballot_sync(FULL, flag);
+    if (am == 0) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(S.fcnt, (unsigned)__popc(am));
+    base = __shfl_sync(FULL, base, 0);
+    const unsigned my = base + __popc(am & lanemask_lt());
+    const bool spill = flag && my >= (unsigned)STAGE_CAP;
+    if (flag && !spill) {
+        S.fk[my] = k;
+        S.fv[my] = v;
+        S.fd[my] = d;
+    }
+    frontier_append(spill, k, v, d, A, nxt);
+}
+
+// Block-wide: move the staged entries to the global next frontier with ONE
+// reservation (entries and arc range), arc offsets by a block scan.
+__device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
+    __syncthreads();
+    const unsigned cnt = min(*S.fcnt, (unsigned)STAGE_CAP);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned per = (cnt + BT - 1) / BT;
+    const unsigned lo = min(cnt, tid * per), hi = min(cnt, lo + per);
+    unsigned long long mine = 0;
+    for (unsigned i = lo; i < hi; i++) mine += (unsigned long long)S.fd[i];
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.scan[w] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < BT / 32; i++) {
+            unsigned long long x = S.scan[i];
+            S.scan[i] = run;
+            run += x;
+        }
+        unsigned long long old = 0;
+        if (cnt) old = atomicAdd(A.fctr + nxt, ((unsigned long long)cnt << CNT_SHIFT) + run);
+        S.scan[BT / 32] = old;
+    }
+    __syncthreads();
+    const unsigned long long old = S.scan[BT / 32];
+    int64_t arc = (int64_t)(old & ARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
+    const int64_t ebase = (int64_t)(old >> CNT_SHIFT);
+    for (unsigned i = lo; i < hi; i++) {
+        const int64_t idx = ebase + i;
+        if (idx < A.fcap) {
+            A.fkey[nxt][idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
+            A.farc[nxt][idx] = arc;
+        } else {
+            A.overflow[0] = 1;
+        }
+        arc += S.fd[i];
+    }
+    __syncthreads();
+    if (tid == 0) *S.fcnt = 0;
+}
+
+template <class T>
+__device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
+    for (int64_t k = threadIdx.x; k < m; k += BT) {
+        const T v = sc[k];
+        if (v) {
+            atomicAdd(g + k, (unsigned long long)v);
+            sc[k] = 0;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
     cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Stage S = stage_carve(smem_raw, (int)A.m);
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
     const int64_t W = nthreads >> 5, wid = gtid >> 5;
+    for (int64_t k = threadIdx.x; k < A.m; k += BT) {
+        S.ops[k] = S.pvol[k] = 0;
+        S.push[k] = S.touch[k] = S.negz[k] = 0;
+    }
+    if (threadIdx.x == 0) *S.fcnt = 0;
+    __syncthreads();
+
     for (int32_t t = 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const unsigned long long packed = *(volatile unsigned long long *)(A.fctr + cur);
         const int64_t F = (int64_t)(packed >> CNT_SHIFT);
         const int64_t P = (int64_t)(packed & ARC_MASK);
+        if (gtid == 0 && t < A.rlog_cap) {
+            A.rlog[3 * t] = F;
+            A.rlog[3 * t + 1] = P;
+            A.rlog[3 * t + 2] = globaltimer();
+            A.rlog[3 * A.rlog_cap] = t + 1;
+        }
         if (F == 0) break;
+        if (((P + 31) >> 5) > A.ccap) {  // arc-chunk map too small: report, stop
+            if (gtid == 0) A.overflow[0] = 1;
+            break;
+        }
         if (t >= A.max_sweeps || F > A.fcap) {
             for (int64_t e = gtid; e < F && e < A.fcap; e += nthreads)
                 A.s_conv[A.fkey[cur][e] >> 32] = 0;
@@ -148,10 +309,12 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         // ---------------- phase A: push the frontier entries ----------------
         if (gtid == 0) A.fctr[nxt] = 0ULL;
         const int64_t *fk = A.fkey[cur];
+        const int64_t *fa_cur = A.farc[cur];
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
             const int64_t e = e0 + lane;
             const bool live = e < F;
             int32_t k = 0, u = 0, d = 0;
+            bool fresh = false;
             if (live) {
                 int64_t key = fk[e];
                 k = (int32_t)(key >> 32);
@@ -164,90 +327,100 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 d = A.g.deg[u];
                 A.frow[e] = A.g.row[u];
                 A.fcval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
-                u = __double_as_longlong(xo) == 0 ? u : -1;  // first push of u?
+                fresh = __double_as_longlong(xo) == 0;  // first push of u
+                // chunks (32 arcs) whose first arc lies in this entry
+                const int64_t a0 = fa_cur[e], a1 = e + 1 < F ? fa_cur[e + 1] : P;
+                for (int64_t c = (a0 + 31) >> 5; c < ((a1 + 31) >> 5); ++c)
+                    if (c < A.ccap) A.chunk_e[c] = (int32_t)e;
             }
-            slot_append(live && u >= 0, k, u, A.ld, A.pushed, A.pushed_cnt);
-            // per-slot counters, aggregated over lanes of the same slot
-            unsigned am = __ballot_sync(FULL, live);
-            if (live) {
-                unsigned peers = __match_any_sync(am, k);
-                unsigned sum = __reduce_add_sync(peers, (unsigned)d);
-                if (lane == __ffs(peers) - 1) {
-                    atomicAdd(A.s_ops + k, (unsigned long long)sum);
-                    atomicAdd(A.s_pushes + k, (unsigned long long)__popc(peers));
-                    A.s_last[k] = t;
-                }
-            }
+            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
+            block_count(fresh, k, (unsigned)d, S.pvol);
+            block_count(live, k, (unsigned)d, S.ops);
+            block_count(live, k, 1u, S.push);
+            if (live) A.s_last[k] = t;
         }
+        __syncthreads();
+        counters_flush(S.ops, A.s_ops, A.m);
+        counters_flush(S.pvol, A.s_pvol, A.m);
+        counters_flush(S.push, A.s_pushes, A.m);
         grid.sync();
         // ---------------- phase B: arc-balanced scatter ----------------------
-        const int64_t p0 = (int64_t)(((unsigned long long)P * (unsigned long long)wid) / W);
-        const int64_t p1 = (int64_t)(((unsigned long long)P * (unsigned long long)(wid + 1)) / W);
-        if (p0 < p1) {
-            const int64_t *fa = A.farc[cur];
-            // 32-ary search: entry e with fa[e] <= p0 < fa[e+1]
-            int64_t lo = 0, hi = F;
-            while (hi - lo > 32) {
-                int64_t step = (hi - lo + 31) >> 5;
-                int64_t i = lo + lane * step;
-                unsigned b = __ballot_sync(FULL, i < hi && fa[i] <= p0);
-                lo += (int64_t)(31 - __clz(b)) * step;
-                hi = min(hi, lo + step);
-            }
-            int64_t e;
-            {
-                int64_t i = lo + lane;
-                unsigned b = __ballot_sync(FULL, i < hi && fa[i] <= p0);
-                e = lo + (31 - __clz(b));
-            }
-            for (int64_t base = p0; base < p1; base += 32) {
+        // chunk c = arcs [32c, 32c+32); every warp owns a contiguous chunk range
+        // and keeps UNROLL independent chunks (each lane one atomic) in flight.
+        const int64_t C = (P + 31) >> 5;
+        const int64_t c0 = (int64_t)(((unsigned long long)C * (unsigned long long)wid) / W);
+        const int64_t c1 = (int64_t)(((unsigned long long)C * (unsigned long long)(wid + 1)) / W);
+        const int64_t *fa = A.farc[cur];
+        for (int64_t cb = c0; cb < c1; cb += UNROLL) {
+            int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
+            double c[UNROLL], old[UNROLL];
+            bool valid[UNROLL];
+            // stage 1: every load of all UNROLL chunks, before any atomic, so
+            // the chunks' dependent-load chains overlap
+#pragma unroll
+            for (int q = 0; q < UNROLL; q++) {
+                const int64_t ch = cb + q;
+                const bool live = ch < c1;
+                const int64_t e = live ? A.chunk_e[ch] : 0;
+                const int64_t a = ch << 5;
+                // entries starting inside (a, a+32): one bit per start offset
                 const int64_t wi = e + 1 + lane;
-                const int64_t st = wi < F ? fa[wi] : INT64_MAX;
-                const int64_t pos = st - base;  // >= 1
+                const int64_t st = (live && wi < F) ? fa[wi] : INT64_MAX;
+                const int64_t pos = st - a;
                 const unsigned starts = __reduce_or_sync(FULL, pos < 32 ? (1u << pos) : 0u);
-                const unsigned upto = __ballot_sync(FULL, pos <= 32);
                 const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
-                const int64_t p = base + lane;
-                bool valid = p < p1;
-                bool first = false, cross = false, negz = false;
-                int32_t k = 0, v = 0, dv = 0;
-                if (valid) {
-                    const int64_t key = A.fkey[cur][me];
-                    k = (int32_t)(key >> 32);
-                    const double c = A.fcval[me];
-                    v = A.g.col[A.frow[me] + (p - fa[me])];
-                    dv = A.g.deg[v];
-                    const double th = theta_deg(A.tcoeff, dv);
-                    const double old = atomicAdd(A.r + (int64_t)k * A.ld + v, c);
-                    const double nw = __dadd_rn(old, c);
-                    first = __double_as_longlong(old) == 0;
-                    negz = __double_as_longlong(old) == (long long)0x8000000000000000ULL;
-                    cross = (old < th) && (nw >= th);
+                const int64_t p = a + lane;
+                valid[q] = live && p < P;
+                k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
+                if (valid[q]) {
+                    k[q] = (int32_t)(A.fkey[cur][me] >> 32);
+                    c[q] = A.fcval[me];
+                    v[q] = __ldg(A.g.col + A.frow[me] + (p - fa[me]));
+                    dv[q] = __ldg(A.g.deg + v[q]);
                 }
-                slot_append(first, k, v, A.ld, A.dirty, A.dirty_cnt);
-                slot_count(negz, k, A.s_negz);
-                frontier_append(cross, k, v, dv, A, nxt);
-                e += __popc(upto);
+            }
+            // stage 2: the atomics, back to back (UNROLL in flight per lane)
+#pragma unroll
+            for (int q = 0; q < UNROLL; q++)
+                old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+            // stage 3: first touch / re-touch of a pushed node / frontier entry
+#pragma unroll
+            for (int q = 0; q < UNROLL; q++) {
+                const long long ob = __double_as_longlong(old[q]);
+                const double th = theta_deg(A.tcoeff, dv[q]);
+                const bool first = valid[q] && ob == 0;
+                const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
+                const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
+                block_count(first, k[q], 1u, S.touch);
+                block_count(negz, k[q], 1u, S.negz);
+                stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
         }
+        stage_flush(S, A, nxt);
+        counters_flush(S.touch, A.touched, A.m);
+        counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
     }
+    // reserve each slot's output segment (pushed counts are final here)
+    if (blockIdx.x == 0)
+        for (int64_t k = threadIdx.x; k < A.m; k += BT)
+            A.slot_base[k] = (int64_t)atomicAdd(A.cursor, A.pushed_cnt[k]);
 }
 
-// Seeds -> slots: r[s] = alpha, dirty = {s}, S_0 = {s} if alpha >= theta_s.
-__global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, int64_t m,
-                            double alpha) {
+// Seeds -> slots: r[s] = alpha, S_0 = {s} if alpha >= theta_s.
+__global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, double alpha) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= m) return;
+    if (k >= A.m) return;
     int32_t s = (int32_t)seeds[k];
     if (A.perm) s = A.perm[s];
+    A.seed[k] = s;
     A.r[k * A.ld + s] = alpha;
-    A.dirty[k * A.ld] = s;
-    A.dirty_cnt[k] = 1;
+    A.touched[k] = 1;
     A.pushed_cnt[k] = 0;
     A.s_ops[k] = 0;
     A.s_pushes[k] = 0;
     A.s_negz[k] = 0;
+    A.s_pvol[k] = 0;
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
     int32_t d = A.g.deg[s];
@@ -267,61 +440,66 @@ struct OutArgs {
     int32_t *xnodes;
     double *xvals;
     int64_t xcap;
-    unsigned long long *cursor;
-    const int32_t *inv;  // relabeled id -> caller id (nullable)
+    const int32_t *inv;  // working id -> caller id (nullable)
 };
 
-// Per slot: extract x over the pushed list (and zero it), write the seed's
-// counters.  support = |dirty| - |pushed nodes whose r is still -0.0|: every
-// push writes -0.0, the first later contribution observes it (s_negz).
+// grid (CHUNKS, slots): copy x over the pushed list out (caller ids) and zero
+// x and r there; block (0, k) writes the seed's counters.
+// support = touched - (pushes - negz): every push writes -0.0 into r[u] and
+// the first later contribution observes it, so the pushed nodes still at
+// zero are pushes - negz.
 __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
-    const int k = blockIdx.x;
+    const int k = blockIdx.y;
     const int64_t off = (int64_t)k * A.ld;
-    __shared__ unsigned long long s_base;
     const int64_t pc = (int64_t)A.pushed_cnt[k];
-    if (threadIdx.x == 0) s_base = atomicAdd(O.cursor, (unsigned long long)pc);
-    __syncthreads();
-    const int64_t b = (int64_t)s_base;
-    for (int64_t i = threadIdx.x; i < pc; i += blockDim.x) {
-        int32_t u = A.pushed[off + i];
-        double xv = A.x[off + u];
+    const int64_t b = A.slot_base[k];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pc;
+         i += (int64_t)CHUNKS * blockDim.x) {
+        const int32_t u = A.pushed[off + i];
+        const double xv = A.x[off + u];
         A.x[off + u] = 0.0;
+        A.r[off + u] = 0.0;
         if (b + i < O.xcap) {
             O.xnodes[b + i] = O.inv ? O.inv[u] : u;
             O.xvals[b + i] = xv;
         }
     }
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t si = seed_base + k;
         const int64_t pushes = (int64_t)A.s_pushes[k];
         O.sweeps[si] = (int64_t)A.s_last[k] + 1;
         O.ops[si] = (int64_t)A.s_ops[k];
         O.pushes[si] = pushes;
         O.conv[si] = A.s_conv[k];
-        O.support[si] = (int64_t)A.dirty_cnt[k] - (pushes - (int64_t)A.s_negz[k]);
+        O.support[si] = (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
         O.xoff[si] = b;
         O.xcnt[si] = pc;
+        if (pc == 0) A.r[off + A.seed[k]] = 0.0;  // an inactive seed keeps r = alpha
     }
 }
 
-// Reset r of every slot: a write-only stream of zeros over the slot when its
-// touched set is large (a random 8 B reset costs a 32 B sector RMW), else a
-// scatter over the dirty list.  grid = (RESET_CHUNKS, slots).
-constexpr int RESET_CHUNKS = 32;
+// grid (CHUNKS, slots): return r to +0.0.  Touched nodes are exactly the
+// rows of the pushed nodes, so either walk those rows (cost vol(pushed)
+// random 8 B writes) or, when that volume is a large fraction of n, stream
+// zeros over the whole slot (write-only, coalesced 16 B stores).
 __global__ void k_wave_reset(RoundArgs A) {
     const int k = blockIdx.y;
     const int64_t off = (int64_t)k * A.ld;
-    const int64_t dc = (int64_t)A.dirty_cnt[k];
-    if (dc * 8 > A.ld) {
+    if ((int64_t)A.s_pvol[k] * 4 > A.ld) {
         double2 *r2 = reinterpret_cast<double2 *>(A.r + off);
         const int64_t h = A.ld >> 1;
-        const int64_t per = (h + RESET_CHUNKS - 1) / RESET_CHUNKS;
+        const int64_t per = (h + CHUNKS - 1) / CHUNKS;
         const int64_t lo = blockIdx.x * per, hi = min(h, lo + per);
         for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) r2[i] = make_double2(0.0, 0.0);
-    } else {
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dc;
-             i += (int64_t)RESET_CHUNKS * blockDim.x)
-            A.r[off + A.dirty[off + i]] = 0.0;
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t pc = (int64_t)A.pushed_cnt[k];
+    const int64_t wpb = blockDim.x >> 5;
+    for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < pc; i += (int64_t)CHUNKS * wpb) {
+        const int32_t u = A.pushed[off + i];
+        const int64_t rs = A.g.row[u], d = A.g.row[u + 1] - rs;
+        for (int64_t j = lane; j < d; j += 32) A.r[off + A.g.col[rs + j]] = 0.0;
     }
 }
 
@@ -360,7 +538,7 @@ __global__ void k_remap_rows(DevGraph g, const int32_t *__restrict__ inv,
 using namespace gd;
 
 struct gd_batch {
-    const gd_graph *G;   // caller's graph
+    const gd_graph *G;      // caller's graph
     gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
     DBuf<int32_t> perm, inv;
     gd_batch_params p;
@@ -368,9 +546,13 @@ struct gd_batch {
     int grid;
     int64_t fcap, xcap;
     DBuf<double> x, r, fcval;
-    DBuf<int32_t> dirty, pushed, s_last, s_conv, overflow;
-    DBuf<unsigned long long> dirty_cnt, pushed_cnt, fctr, s_ops, s_pushes, s_negz, cursor;
-    DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow;
+    DBuf<int32_t> pushed, seed, s_last, s_conv, overflow;
+    DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
+    DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow, slot_base;
+    DBuf<int32_t> chunk_e;
+    int64_t ccap = 0;
+    DBuf<int64_t> rlog;
+    static constexpr int64_t RLOG_CAP = 4096;
     // results
     DBuf<int64_t> sweeps, ops, pushes, support, xoff, xcnt;
     DBuf<int32_t> conv, xnodes;
@@ -390,14 +572,18 @@ struct gd_batch {
         A.ld = (G->n + 1) & ~1LL;
         A.max_sweeps = p.max_sweeps;
         A.fcap = fcap;
-        A.x = x.p; A.r = r.p; A.dirty = dirty.p; A.pushed = pushed.p;
-        A.dirty_cnt = dirty_cnt.p; A.pushed_cnt = pushed_cnt.p;
+        A.x = x.p; A.r = r.p; A.pushed = pushed.p; A.seed = seed.p;
+        A.touched = touched.p; A.pushed_cnt = pushed_cnt.p;
         A.fkey[0] = fkey0.p; A.fkey[1] = fkey1.p; A.farc[0] = farc0.p; A.farc[1] = farc1.p;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
-        A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_last = s_last.p; A.s_conv = s_conv.p;
-        A.s_negz = s_negz.p;
+        A.chunk_e = chunk_e.p; A.ccap = ccap;
+        A.rlog = rlog.p; A.rlog_cap = RLOG_CAP;
+        A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
+        A.s_last = s_last.p; A.s_conv = s_conv.p;
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
+        A.cursor = cursor.p;
+        A.slot_base = slot_base.p;
         return A;
     }
     ~gd_batch() {
@@ -407,11 +593,9 @@ struct gd_batch {
 };
 
 static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cudaStream_t st) {
-    const int64_t n = B->G->n;
-    B->sweeps.ensure(n_seeds ? n_seeds : 1); B->ops.ensure(n_seeds ? n_seeds : 1);
-    B->pushes.ensure(n_seeds ? n_seeds : 1); B->support.ensure(n_seeds ? n_seeds : 1);
-    B->xoff.ensure(n_seeds ? n_seeds : 1); B->xcnt.ensure(n_seeds ? n_seeds : 1);
-    B->conv.ensure(n_seeds ? n_seeds : 1);
+    const size_t ns = n_seeds ? (size_t)n_seeds : 1;
+    B->sweeps.ensure(ns); B->ops.ensure(ns); B->pushes.ensure(ns); B->support.ensure(ns);
+    B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
     GD_CUDA(cudaMemsetAsync(B->overflow.p, 0, sizeof(int32_t), st));
     const int64_t waves = (n_seeds + B->slots - 1) / B->slots;
@@ -421,23 +605,22 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         B->ev.push_back(e);
     }
     OutArgs O{B->sweeps.p, B->ops.p, B->pushes.p, B->support.p, B->xoff.p, B->xcnt.p,
-              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p,
-              B->R ? B->inv.p : nullptr};
-    RoundArgs A = B->args();
+              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr};
     int64_t launches = 0;
     for (int64_t w = 0; w < waves; ++w) {
         const int64_t base = w * B->slots;
-        const int64_t m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
+        RoundArgs A = B->args();
+        A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
-        k_wave_init<<<(int)((m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, m, B->p.alpha);
+        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, B->p.alpha);
         GD_LAUNCH_CHECK();
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A};
         GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_rounds, dim3(B->grid), dim3(BT), kargs,
-                                            0, st));
+                                            stage_bytes(B->slots), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
-        k_wave_extract<<<(int)m, 256, 0, st>>>(A, O, base);
-        k_wave_reset<<<dim3(RESET_CHUNKS, (unsigned)m), 256, 0, st>>>(A);
+        k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
+        k_wave_reset<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A);
         GD_LAUNCH_CHECK();
         launches += 4;
     }
@@ -452,7 +635,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->last_launches = launches;
 }
 
-// Degree-descending renumbering of the graph on the device (one-time setup).
+// Degree-descending renumbering with sorted rows, on the device (setup).
 static void build_relabeled(gd_batch *B) {
     const gd_graph *G = B->G;
     const int64_t n = G->n;
@@ -488,8 +671,17 @@ static void build_relabeled(gd_batch *B) {
     tmp.ensure(bytes ? bytes : 1);
     cub::DeviceScan::ExclusiveSum(tmp.p, bytes, deg64.p, R->row.p, n + 1);
     GD_CUDA(cudaMemcpy(R->deg.p, dsorted.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice));
-    k_remap_rows<<<blocks, 256>>>(g, B->inv.p, B->perm.p, R->row.p, R->col.p);
+    DBuf<int32_t> unsorted(G->n_arcs ? G->n_arcs : 1);
+    k_remap_rows<<<blocks, 256>>>(g, B->inv.p, B->perm.p, R->row.p, unsorted.p);
     GD_LAUNCH_CHECK();
+    // sort every row by new id: a warp's 32 consecutive arcs then target
+    // nearby residual words (hubs are contiguous), so its atomics share sectors
+    bytes = 0;
+    cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, unsorted.p, R->col.p, G->n_arcs, n,
+                                       R->row.p, R->row.p + 1);
+    tmp.ensure(bytes ? bytes : 1);
+    cub::DeviceSegmentedSort::SortKeys(tmp.p, bytes, unsorted.p, R->col.p, G->n_arcs, n,
+                                       R->row.p, R->row.p + 1);
     GD_CUDA(cudaDeviceSynchronize());
 }
 
@@ -504,38 +696,47 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
         GD_CHECK_ARG(G->n_arcs < (1LL << CNT_SHIFT), "too many arcs");
         GD_CUDA(cudaSetDevice(G->device));
         const int64_t n = G->n ? G->n : 1;
+        const int64_t ld = (n + 1) & ~1LL;
         gd_batch *B = new gd_batch();
         try {
             B->G = G;
             B->p = *p;
-            if (p->relabel) build_relabeled(B);
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
+            if (p->relabel) build_relabeled(B);
             int slots = p->slots;
             if (slots <= 0) {
                 size_t fr = 0, tot = 0;
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
-                int64_t by_mem = (int64_t)(fr / 4) / (n * 24);
+                int64_t by_mem = (int64_t)(fr / 4) / (ld * 20);
                 slots = (int)(by_mem < 256 ? (by_mem < 1 ? 1 : by_mem) : 256);
             }
+            if (slots > 2048) slots = 2048;  // per-block slot counters live in shared memory
             B->slots = slots;
             int64_t fc = p->frontier_cap > 0 ? p->frontier_cap : (int64_t)slots * n;
             if (p->frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
             B->fcap = fc;
             B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
-            const size_t sn = (size_t)slots * (size_t)((n + 1) & ~1LL);
+            const size_t sn = (size_t)slots * (size_t)ld;
             B->x.alloc(sn); B->r.alloc(sn);
             GD_CUDA(cudaMemset(B->x.p, 0, sizeof(double) * sn));
             GD_CUDA(cudaMemset(B->r.p, 0, sizeof(double) * sn));
-            B->dirty.alloc(sn); B->pushed.alloc(sn);
-            B->dirty_cnt.alloc(slots); B->pushed_cnt.alloc(slots);
+            B->pushed.alloc(sn);
+            B->seed.alloc(slots); B->touched.alloc(slots); B->pushed_cnt.alloc(slots);
             B->s_ops.alloc(slots); B->s_pushes.alloc(slots); B->s_negz.alloc(slots);
-            B->s_last.alloc(slots); B->s_conv.alloc(slots);
+            B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
+            B->slot_base.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
             B->fkey0.alloc(fc); B->fkey1.alloc(fc); B->farc0.alloc(fc); B->farc1.alloc(fc);
             B->frow.alloc(fc); B->fcval.alloc(fc);
+            B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
+            B->chunk_e.alloc(B->ccap);
+            B->rlog.alloc(3 * gd_batch::RLOG_CAP + 1);
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
+            const size_t smem = stage_bytes(slots);
+            GD_CUDA(cudaFuncSetAttribute(k_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
             int per_sm = 0;
-            GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rounds, BT, 0));
+            GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rounds, BT, smem));
             GD_CHECK_ARG(per_sm > 0, "round kernel does not fit on an SM");
             B->grid = per_sm * n_sms(G->device);
         } catch (...) {
@@ -564,7 +765,8 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
             GD_CUDA(cudaMemcpy(&ovf, B->overflow.p, sizeof(ovf), cudaMemcpyDeviceToHost));
             GD_CUDA(cudaMemcpy(&used, B->cursor.p, sizeof(used), cudaMemcpyDeviceToHost));
             if (ovf) {
-                set_error("frontier capacity %lld exceeded; raise frontier_cap",
+                set_error("frontier capacity %lld (entries or arc chunks per round) exceeded; "
+                          "raise frontier_cap",
                           (long long)B->fcap);
                 throw Error{GD_ERR_CAPACITY};
             }
@@ -614,6 +816,18 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
         d2h(x_nodes, res.x_nodes, sizeof(int32_t) * res.x_total);
         d2h(x_vals, res.x_vals, sizeof(double) * res.x_total);
         GD_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int gd_batch_round_log(const gd_batch *B, int64_t *out, int64_t cap, int64_t *rounds) {
+    return guarded([&] {
+        GD_CHECK_ARG(B && out && rounds, "null pointer");
+        int64_t cnt = 0;
+        GD_CUDA(cudaMemcpy(&cnt, B->rlog.p + 3 * gd_batch::RLOG_CAP, sizeof(int64_t),
+                           cudaMemcpyDeviceToHost));
+        *rounds = cnt;
+        int64_t k = cnt < cap ? cnt : cap;
+        if (k) GD_CUDA(cudaMemcpy(out, B->rlog.p, sizeof(int64_t) * 3 * k, cudaMemcpyDeviceToHost));
     });
 }
 
