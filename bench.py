@@ -52,6 +52,18 @@ def parse():
     return p.parse_args()
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the sweep kernel from the committed ncu summary."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_k_rounds_*.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as fh:
+        d = json.load(fh)
+    return d.get("dram_bytes_per_launch"), os.path.basename(files[-1])
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -175,14 +187,15 @@ def run_reference(args):
         d = np.repeat(hg.degrees.astype(np.float64), hg.degrees)
         hg.arc_w = (1.0 / d) * (1.0 - args.alpha)
         hg.theta = theta_vector(hg, args.eps * args.alpha)
-    seeds = sample_sources(hg, args.seeds * (args.steps + args.warmup), seed=0)
-    # size the per-step sample from one calibration batch (bounded CPU work)
-    per = max(threads, 1)
-    _, dt = cpu_reference(hg, args.alpha, args.eps, seeds[:per], threads)
-    per_step = int(max(threads, min(len(seeds), per * max(1.0, 3.0 / max(dt, 1e-3)))))
+    steps_total = args.steps + args.warmup
+    allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
+    batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
+    # each step: a bounded prefix of that step's batch (about 3 s of CPU work)
+    _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][:threads], threads)
+    per_step = int(min(args.seeds, max(threads, threads * 3.0 / max(dt, 1e-3))))
     times, ops, done = [], 0, 0
-    for k in range(args.warmup + args.steps):
-        sl = seeds[(k * per_step) % len(seeds):][:per_step]
+    for k in range(steps_total):
+        sl = batches[k][:per_step]
         out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads)
         if k >= args.warmup:
             times.append(dt)
@@ -198,7 +211,7 @@ def run_reference(args):
         "config": workload_config(args, n, m),
         "gteps": ops / tot / 1e9,
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} seeds per step of the sample_sources batch, "
+                         "sample": f"first {per_step} seeds of each step's sample_sources batch, "
                                    "reference local_gd restated in C (oracle/), per-seed O(n) "
                                    "state as in the reference, one seed per thread"},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -290,6 +303,7 @@ def main():
     peak, peak_kind = peaks()
     my_balg = b_alg_bytes(int(t[1]), int(t[2]))
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic()
     # e2e: the public host API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -344,7 +358,9 @@ def main():
             "gteps": ops / sec / 1e9,
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "b_alg_per_launch": my_balg / max(1, launches // 4),
+                         "peak_kind": peak_kind,
                          "kernel": "k_rounds (persistent sweep loop)",
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -66,6 +66,7 @@ struct RoundArgs {
     int64_t *fkey[2], *farc[2];
     int64_t *frow;
     double *fcval;
+    const int2 *colp;     // per arc (neighbour, its degree): one 8 B load gives theta
     int32_t *chunk_e;     // entry holding arc 32c of the round (phase A -> B)
     int64_t ccap;         // chunk_e capacity
     unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
@@ -159,11 +160,12 @@ struct Stage {
     unsigned *push, *touch, *negz;       // [S]
     int32_t *fk, *fv, *fd;               // [STAGE_CAP]
     unsigned *fcnt;                      // [1]
+    unsigned long long *next;            // [1] phase-B chunk claim counter
     unsigned long long *scan;            // [BT/32 + 2]
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 2) + 64;
+    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 3) + 64;
 }
 
 __device__ Stage stage_carve(void *base, int S) {
@@ -172,6 +174,7 @@ __device__ Stage stage_carve(void *base, int S) {
     st.ops = (unsigned long long *)p; p += 8 * S;
     st.pvol = (unsigned long long *)p; p += 8 * S;
     st.scan = (unsigned long long *)p; p += 8 * (BT / 32 + 2);
+    st.next = (unsigned long long *)p; p += 8;
     st.push = (unsigned *)p; p += 4 * S;
     st.touch = (unsigned *)p; p += 4 * S;
     st.negz = (unsigned *)p; p += 4 * S;
@@ -277,12 +280,14 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
-    const int64_t W = nthreads >> 5, wid = gtid >> 5;
     for (int64_t k = threadIdx.x; k < A.m; k += BT) {
         S.ops[k] = S.pvol[k] = 0;
         S.push[k] = S.touch[k] = S.negz[k] = 0;
     }
-    if (threadIdx.x == 0) *S.fcnt = 0;
+    if (threadIdx.x == 0) {
+        *S.fcnt = 0;
+        *S.next = 0;
+    }
     __syncthreads();
 
     for (int32_t t = 0;; ++t) {
@@ -328,10 +333,24 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 A.frow[e] = A.g.row[u];
                 A.fcval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 fresh = __double_as_longlong(xo) == 0;  // first push of u
-                // chunks (32 arcs) whose first arc lies in this entry
+            }
+            // chunks (32 arcs) whose first arc lies in entry e: [clo, chi).
+            // Hubs own thousands of chunks, so the warp writes them together.
+            int64_t clo = 0, chi = 0;
+            if (live) {
                 const int64_t a0 = fa_cur[e], a1 = e + 1 < F ? fa_cur[e + 1] : P;
-                for (int64_t c = (a0 + 31) >> 5; c < ((a1 + 31) >> 5); ++c)
-                    if (c < A.ccap) A.chunk_e[c] = (int32_t)e;
+                clo = (a0 + 31) >> 5;
+                chi = min((a1 + 31) >> 5, A.ccap);
+            }
+            unsigned big = __ballot_sync(FULL, chi - clo > 4);
+            if (!(big >> lane & 1u))
+                for (int64_t c = clo; c < chi; ++c) A.chunk_e[c] = (int32_t)e;
+            while (big) {
+                const int src = __ffs(big) - 1;
+                big &= big - 1;
+                const int64_t lo2 = __shfl_sync(FULL, clo, src), hi2 = __shfl_sync(FULL, chi, src);
+                const int32_t e2 = (int32_t)__shfl_sync(FULL, e, src);
+                for (int64_t c = lo2 + lane; c < hi2; c += 32) A.chunk_e[c] = e2;
             }
             slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
@@ -348,10 +367,17 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         // chunk c = arcs [32c, 32c+32); every warp owns a contiguous chunk range
         // and keeps UNROLL independent chunks (each lane one atomic) in flight.
         const int64_t C = (P + 31) >> 5;
-        const int64_t c0 = (int64_t)(((unsigned long long)C * (unsigned long long)wid) / W);
-        const int64_t c1 = (int64_t)(((unsigned long long)C * (unsigned long long)(wid + 1)) / W);
+        // static split across blocks, dynamic (shared counter) across the
+        // block's warps: latency variation between warps evens out
+        const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
+        const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
         const int64_t *fa = A.farc[cur];
-        for (int64_t cb = c0; cb < c1; cb += UNROLL) {
+        for (;;) {
+            unsigned long long claim = 0;
+            if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)UNROLL);
+            const int64_t cb = bc0 + (int64_t)__shfl_sync(FULL, claim, 0);
+            if (cb >= bc1) break;
+            const int64_t c1 = bc1;
             int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
             double c[UNROLL], old[UNROLL];
             bool valid[UNROLL];
@@ -375,8 +401,9 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 if (valid[q]) {
                     k[q] = (int32_t)(A.fkey[cur][me] >> 32);
                     c[q] = A.fcval[me];
-                    v[q] = __ldg(A.g.col + A.frow[me] + (p - fa[me]));
-                    dv[q] = __ldg(A.g.deg + v[q]);
+                    const int2 vd = __ldg(A.colp + A.frow[me] + (p - fa[me]));
+                    v[q] = vd.x;
+                    dv[q] = vd.y;
                 }
             }
             // stage 2: the atomics, back to back (UNROLL in flight per lane)
@@ -396,7 +423,8 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
         }
-        stage_flush(S, A, nxt);
+        stage_flush(S, A, nxt);  // (its barriers also order the chunk counter reset)
+        if (threadIdx.x == 0) *S.next = 0;
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
@@ -503,6 +531,15 @@ __global__ void k_wave_reset(RoundArgs A) {
     }
 }
 
+// (neighbour, degree) per arc, for the threshold test without a second load
+__global__ void k_pack_cols(DevGraph g, int2 *__restrict__ colp) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g.n_arcs;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = g.col[j];
+        colp[j] = make_int2(v, g.deg[v]);
+    }
+}
+
 // ---- degree relabeling (setup): new id = rank by descending degree ------
 __global__ void k_iota(int32_t *ids, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -550,6 +587,7 @@ struct gd_batch {
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
     DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow, slot_base;
     DBuf<int32_t> chunk_e;
+    DBuf<int2> colp;
     int64_t ccap = 0;
     DBuf<int64_t> rlog;
     static constexpr int64_t RLOG_CAP = 4096;
@@ -577,6 +615,7 @@ struct gd_batch {
         A.fkey[0] = fkey0.p; A.fkey[1] = fkey1.p; A.farc[0] = farc0.p; A.farc[1] = farc1.p;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
         A.chunk_e = chunk_e.p; A.ccap = ccap;
+        A.colp = colp.p;
         A.rlog = rlog.p; A.rlog_cap = RLOG_CAP;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p;
@@ -703,12 +742,18 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->p = *p;
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
             if (p->relabel) build_relabeled(B);
+            B->colp.alloc(G->n_arcs ? G->n_arcs : 1);
+            k_pack_cols<<<4 * n_sms(G->device), 256>>>(B->work()->view(), B->colp.p);
+            GD_LAUNCH_CHECK();
+            GD_CUDA(cudaDeviceSynchronize());
             int slots = p->slots;
             if (slots <= 0) {
                 size_t fr = 0, tot = 0;
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
+                // 64 in flight measured best on the products shape (L2 reuse of
+                // the hub block vs. barrier amortisation); fewer if memory-bound
                 int64_t by_mem = (int64_t)(fr / 4) / (ld * 20);
-                slots = (int)(by_mem < 256 ? (by_mem < 1 ? 1 : by_mem) : 256);
+                slots = (int)(by_mem < 64 ? (by_mem < 1 ? 1 : by_mem) : 64);
             }
             if (slots > 2048) slots = 2048;  // per-block slot counters live in shared memory
             B->slots = slots;
