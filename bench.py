@@ -248,22 +248,21 @@ def main():
     hdeg = _HostGraph(n, row_h)
     steps_total = args.warmup + args.steps
     allseeds = sample_sources(hdeg, args.seeds * world * steps_total, seed=0)
-    mine = allseeds[rank::world]  # round-robin over the degree-ranked sample
+    from paper_2410_21634_b200.shard import STAT_FIELDS, gather_results, shard_seeds
+
+    mine = shard_seeds(allseeds, rank, world)  # round-robin over the degree-ranked sample
     batches = [mine[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     dseeds = [torch.as_tensor(b, device="cuda") for b in batches]
     solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots, relabel=not args.no_relabel)
     stream = torch.cuda.current_stream()
 
     def gather(res):
-        """NCCL gather of per-seed results (the only collective)."""
+        """NCCL gather of every seed's counters and sparse x to rank 0 (the
+        only collective of the data path)."""
         if world == 1:
-            return res["total_ops"].sum()
-        cnt = torch.tensor([res["x_total"]], device="cuda", dtype=torch.int64)
-        stats = torch.stack([res["sweeps"], res["total_ops"], res["pushes"]])
-        out = [torch.empty_like(stats) for _ in range(world)]
-        dist.all_gather(out, stats)
-        dist.all_reduce(cnt)
-        return out[0].sum()
+            return None
+        return gather_results({f: res[f] for f in STAT_FIELDS}, res["x_nodes"], res["x_vals"],
+                              dst=0)
 
     for k in range(args.warmup):
         gather(solver.solve_device(dseeds[k], stream=stream))

@@ -50,26 +50,6 @@ constexpr unsigned long long ARC_MASK = (1ULL << CNT_SHIFT) - 1ULL;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int CHUNKS = 32;  // blocks per slot in the extract / reset kernels
 
-// One double-buffered frontier list with its own arc space.  Small-list rows
-// (degree < LARGE_MIN) are processed in 32-arc chunks (a lane finds its row);
-// large-list rows in PIECE-arc chunks that a warp walks row segment by row
-// segment with coalesced column loads.  map[] gives the row holding each
-// chunk's first arc.
-constexpr int LARGE_MIN = 32;
-constexpr int PIECE = 512;
-constexpr int UNROLL_L = 4;  // 32-arc groups in flight per warp on large rows
-
-struct FList {
-    int64_t *key[2];   // (slot << 32) | node
-    int64_t *off[2];   // first arc of the entry in the list's arc space
-    int64_t *row;      // phase A -> B: row start
-    double *cval;      // phase A -> B: contribution fl(vals * w_u)
-    int32_t *deg;      // phase A -> B: row length
-    int32_t *map;      // chunk -> entry holding its first arc (32 / PIECE arcs)
-    int64_t mcap;
-    unsigned long long *ctr;  // [2] packed (entries << 36 | units)
-};
-
 struct RoundArgs {
     DevGraph g;
     double beta;    // 1 - alpha
@@ -77,14 +57,19 @@ struct RoundArgs {
     int64_t n;
     int64_t ld;     // slot stride (n rounded up to even: 16 B aligned slots)
     int64_t max_sweeps;
-    int64_t fcap;   // entries per list
+    int64_t fcap;
     int64_t m;      // slots in use this wave
     double *x, *r;
     int32_t *pushed;
     int32_t *seed;  // per slot: seed in working ids
     unsigned long long *touched, *pushed_cnt;
-    FList L[2];     // [0] small, [1] large
+    int64_t *fkey[2], *farc[2];
+    int64_t *frow;
+    double *fcval;
     const int2 *colp;     // per arc (neighbour, its degree): one 8 B load gives theta
+    int32_t *chunk_e;     // entry holding arc 32c of the round (phase A -> B)
+    int64_t ccap;         // chunk_e capacity
+    unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
     unsigned long long *s_ops, *s_pushes, *s_negz, *s_pvol;
     int32_t *s_last, *s_conv;
     int32_t *overflow;
@@ -111,12 +96,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-__device__ __forceinline__ int cls_of(int32_t d) { return d >= LARGE_MIN ? 1 : 0; }
-__device__ __forceinline__ unsigned long long units_of(int, int32_t d) {
-    return (unsigned long long)d;  // both lists are indexed by arcs
-}
-__device__ __forceinline__ int chunk_shift(int cls) { return cls ? 9 : 5; }  // PIECE = 2^9
-
 // Append `item` to the per-slot list k (warp-aggregated by slot).
 __device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, int64_t ld,
                                             int32_t *list, unsigned long long *cnt) {
@@ -131,16 +110,25 @@ __device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, 
     list[(int64_t)k * ld + (int64_t)base + __popc(peers & lanemask_lt())] = item;
 }
 
-// Append (k, v, d) of class cls straight to the global next frontier
-// (warp-aggregated: one packed atomic reserves entries and units together).
-__device__ __forceinline__ void frontier_append(bool flag, int cls, int32_t k, int32_t v,
-                                                int32_t d, const RoundArgs &A, int nxt) {
-    const FList &F = A.L[cls];
+// Add `val` of the flagged lanes to per-slot counter k: one fire-and-forget
+// reduction per slot present in the warp (no returned value to wait for).
+__device__ __forceinline__ void slot_add(bool flag, int32_t k, unsigned val,
+                                         unsigned long long *cnt) {
+    unsigned am = __ballot_sync(FULL, flag);
+    if (!flag) return;
+    unsigned peers = __match_any_sync(am, k);
+    unsigned sum = __reduce_add_sync(peers, val);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, (unsigned long long)sum);
+}
+
+// Append (k, v) with degree d to the next frontier (warp-aggregated, one
+// packed atomic reserving entry slots and arc range together).
+__device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v, int32_t d,
+                                                const RoundArgs &A, int nxt) {
     unsigned am = __ballot_sync(FULL, flag);
     if (am == 0) return;
     int lane = threadIdx.x & 31;
-    const unsigned long long un = flag ? units_of(cls, d) : 0ULL;
-    unsigned long long incl = un;
+    unsigned long long incl = flag ? (unsigned long long)d : 0ULL;
     for (int o = 1; o < 32; o <<= 1) {
         unsigned long long y = __shfl_up_sync(FULL, incl, o);
         if (lane >= o) incl += y;
@@ -148,13 +136,13 @@ __device__ __forceinline__ void frontier_append(bool flag, int cls, int32_t k, i
     unsigned long long total = __shfl_sync(FULL, incl, 31);
     unsigned long long old = 0;
     if (lane == 0)
-        old = atomicAdd(F.ctr + nxt, ((unsigned long long)__popc(am) << CNT_SHIFT) + total);
+        old = atomicAdd(A.fctr + nxt, ((unsigned long long)__popc(am) << CNT_SHIFT) + total);
     old = __shfl_sync(FULL, old, 0);
     if (flag) {
         int64_t idx = (int64_t)(old >> CNT_SHIFT) + __popc(am & lanemask_lt());
         if (idx < A.fcap) {
-            F.key[nxt][idx] = ((int64_t)k << 32) | (uint32_t)v;
-            F.off[nxt][idx] = (int64_t)(old & ARC_MASK) + (int64_t)(incl - un);
+            A.fkey[nxt][idx] = ((int64_t)k << 32) | (uint32_t)v;
+            A.farc[nxt][idx] = (int64_t)(old & ARC_MASK) + (int64_t)(incl - (unsigned long long)d);
         } else {
             A.overflow[0] = 1;
         }
@@ -163,8 +151,8 @@ __device__ __forceinline__ void frontier_append(bool flag, int cls, int32_t k, i
 
 // Block-level staging (shared memory): per-slot counters of the block and a
 // buffer of the block's next-frontier entries.  Flushed once per phase, so
-// global atomics on the shared frontier counters drop from one per warp
-// with a crossing to two per block per round.
+// global atomics on the shared frontier counter drop from one per warp with
+// a crossing to one per block per round.
 constexpr int STAGE_CAP = 3072;  // staged frontier entries per block per round
 
 struct Stage {
@@ -172,12 +160,12 @@ struct Stage {
     unsigned *push, *touch, *negz;       // [S]
     int32_t *fk, *fv, *fd;               // [STAGE_CAP]
     unsigned *fcnt;                      // [1]
-    unsigned long long *next;            // [2] phase-B claim counters (pieces, chunks)
+    unsigned long long *next;            // [1] phase-B chunk claim counter
     unsigned long long *scan;            // [BT/32 + 2]
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 4) + 64;
+    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 3) + 64;
 }
 
 __device__ Stage stage_carve(void *base, int S) {
@@ -186,7 +174,7 @@ __device__ Stage stage_carve(void *base, int S) {
     st.ops = (unsigned long long *)p; p += 8 * S;
     st.pvol = (unsigned long long *)p; p += 8 * S;
     st.scan = (unsigned long long *)p; p += 8 * (BT / 32 + 2);
-    st.next = (unsigned long long *)p; p += 16;
+    st.next = (unsigned long long *)p; p += 8;
     st.push = (unsigned *)p; p += 4 * S;
     st.touch = (unsigned *)p; p += 4 * S;
     st.negz = (unsigned *)p; p += 4 * S;
@@ -209,7 +197,7 @@ __device__ __forceinline__ void block_count(bool flag, int32_t k, unsigned val, 
 }
 
 // Stage (k, v, d) in the block buffer; lanes beyond its capacity append
-// straight to the global frontier of their class.
+// straight to the global frontier.
 __device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, int32_t d,
                                              const Stage &S, const RoundArgs &A, int nxt) {
     unsigned am = __ballot_sync(FULL, flag);
@@ -225,29 +213,20 @@ __device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, in
         S.fv[my] = v;
         S.fd[my] = d;
     }
-    const int c = cls_of(d);
-    frontier_append(spill && c == 0, 0, k, v, d, A, nxt);
-    frontier_append(spill && c == 1, 1, k, v, d, A, nxt);
+    frontier_append(spill, k, v, d, A, nxt);
 }
 
-// Block-wide: move the staged entries of class cls to the global next
-// frontier with ONE reservation (entries and units), offsets by block scan.
-__device__ void stage_flush_class(const Stage &S, const RoundArgs &A, int nxt, int cls,
-                                  unsigned cnt) {
-    const FList &F = A.L[cls];
+// Block-wide: move the staged entries to the global next frontier with ONE
+// reservation (entries and arc range), arc offsets by a block scan.
+__device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
+    __syncthreads();
+    const unsigned cnt = min(*S.fcnt, (unsigned)STAGE_CAP);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const unsigned per = (cnt + BT - 1) / BT;
     const unsigned lo = min(cnt, tid * per), hi = min(cnt, lo + per);
     unsigned long long mine = 0;
-    unsigned mine_n = 0;
-    for (unsigned i = lo; i < hi; i++)
-        if (cls_of(S.fd[i]) == cls) {
-            mine += units_of(cls, S.fd[i]);
-            ++mine_n;
-        }
-    // scan (units << 20 | entries) jointly: entries per block <= STAGE_CAP < 2^20
-    unsigned long long packed = (mine << 20) | mine_n;
-    unsigned long long incl = packed;
+    for (unsigned i = lo; i < hi; i++) mine += (unsigned long long)S.fd[i];
+    unsigned long long incl = mine;
     for (int o = 1; o < 32; o <<= 1) {
         unsigned long long y = __shfl_up_sync(FULL, incl, o);
         if (lane >= o) incl += y;
@@ -261,37 +240,26 @@ __device__ void stage_flush_class(const Stage &S, const RoundArgs &A, int nxt, i
             S.scan[i] = run;
             run += x;
         }
-        const unsigned long long ents = run & 0xFFFFFULL, units = run >> 20;
         unsigned long long old = 0;
-        if (ents) old = atomicAdd(F.ctr + nxt, (ents << CNT_SHIFT) + units);
+        if (cnt) old = atomicAdd(A.fctr + nxt, ((unsigned long long)cnt << CNT_SHIFT) + run);
         S.scan[BT / 32] = old;
     }
     __syncthreads();
     const unsigned long long old = S.scan[BT / 32];
-    const unsigned long long ex = S.scan[w] + incl - packed;
-    int64_t unit = (int64_t)(old & ARC_MASK) + (int64_t)(ex >> 20);
-    int64_t idx = (int64_t)(old >> CNT_SHIFT) + (int64_t)(ex & 0xFFFFFULL);
+    int64_t arc = (int64_t)(old & ARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
+    const int64_t ebase = (int64_t)(old >> CNT_SHIFT);
     for (unsigned i = lo; i < hi; i++) {
-        const int32_t d = S.fd[i];
-        if (cls_of(d) != cls) continue;
+        const int64_t idx = ebase + i;
         if (idx < A.fcap) {
-            F.key[nxt][idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
-            F.off[nxt][idx] = unit;
+            A.fkey[nxt][idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
+            A.farc[nxt][idx] = arc;
         } else {
             A.overflow[0] = 1;
         }
-        unit += (int64_t)units_of(cls, d);
-        ++idx;
+        arc += S.fd[i];
     }
     __syncthreads();
-}
-
-__device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
-    __syncthreads();
-    const unsigned cnt = min(*S.fcnt, (unsigned)STAGE_CAP);
-    stage_flush_class(S, A, nxt, 0, cnt);
-    stage_flush_class(S, A, nxt, 1, cnt);
-    if (threadIdx.x == 0) *S.fcnt = 0;
+    if (tid == 0) *S.fcnt = 0;
 }
 
 template <class T>
@@ -303,21 +271,6 @@ __device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
             sc[k] = 0;
         }
     }
-}
-
-// Threshold crossing / first touch / re-touch bookkeeping of one arc update.
-struct ArcOut {
-    bool first, negz, cross;
-};
-__device__ __forceinline__ ArcOut classify(bool valid, double old, double c, int32_t dv,
-                                           double tcoeff) {
-    const long long ob = __double_as_longlong(old);
-    const double th = theta_deg(tcoeff, dv);
-    ArcOut o;
-    o.first = valid && ob == 0;
-    o.negz = valid && ob == (long long)0x8000000000000000ULL;
-    o.cross = valid && old < th && __dadd_rn(old, c) >= th;
-    return o;
 }
 
 __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
@@ -333,86 +286,71 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
     }
     if (threadIdx.x == 0) {
         *S.fcnt = 0;
-        S.next[0] = S.next[1] = 0;
+        *S.next = 0;
     }
     __syncthreads();
 
     for (int32_t t = 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
-        int64_t Fc[2], Uc[2];
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-            const unsigned long long pk = *(volatile unsigned long long *)(A.L[c].ctr + cur);
-            Fc[c] = (int64_t)(pk >> CNT_SHIFT);
-            Uc[c] = (int64_t)(pk & ARC_MASK);
-        }
-        const int64_t F = Fc[0] + Fc[1];
+        const unsigned long long packed = *(volatile unsigned long long *)(A.fctr + cur);
+        const int64_t F = (int64_t)(packed >> CNT_SHIFT);
+        const int64_t P = (int64_t)(packed & ARC_MASK);
         if (gtid == 0 && t < A.rlog_cap) {
             A.rlog[3 * t] = F;
-            A.rlog[3 * t + 1] = Uc[0] + Uc[1];
+            A.rlog[3 * t + 1] = P;
             A.rlog[3 * t + 2] = globaltimer();
             A.rlog[3 * A.rlog_cap] = t + 1;
         }
         if (F == 0) break;
-        if (((Uc[0] + 31) >> 5) > A.L[0].mcap || ((Uc[1] + PIECE - 1) >> 9) > A.L[1].mcap) {
+        if (((P + 31) >> 5) > A.ccap) {  // arc-chunk map too small: report, stop
             if (gtid == 0) A.overflow[0] = 1;
             break;
         }
-        if (t >= A.max_sweeps || Fc[0] > A.fcap || Fc[1] > A.fcap) {
-            for (int c = 0; c < 2; c++)
-                for (int64_t e = gtid; e < Fc[c] && e < A.fcap; e += nthreads)
-                    A.s_conv[A.L[c].key[cur][e] >> 32] = 0;
+        if (t >= A.max_sweeps || F > A.fcap) {
+            for (int64_t e = gtid; e < F && e < A.fcap; e += nthreads)
+                A.s_conv[A.fkey[cur][e] >> 32] = 0;
             break;
         }
         // ---------------- phase A: push the frontier entries ----------------
-        if (gtid == 0) {
-            A.L[0].ctr[nxt] = 0ULL;
-            A.L[1].ctr[nxt] = 0ULL;
-        }
+        if (gtid == 0) A.fctr[nxt] = 0ULL;
+        const int64_t *fk = A.fkey[cur];
+        const int64_t *fa_cur = A.farc[cur];
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
-            const int64_t ge = e0 + lane;
-            const bool live = ge < F;
-            const int cls = ge >= Fc[0] ? 1 : 0;
-            const FList &L = A.L[cls];
-            const int64_t e = cls ? ge - Fc[0] : ge;
+            const int64_t e = e0 + lane;
+            const bool live = e < F;
             int32_t k = 0, u = 0, d = 0;
             bool fresh = false;
             if (live) {
-                const int64_t key = L.key[cur][e];
+                int64_t key = fk[e];
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
-                const int64_t idx = (int64_t)k * A.ld + u;
-                const double val = A.r[idx];
-                const double xo = A.x[idx];
+                int64_t idx = (int64_t)k * A.ld + u;
+                double val = A.r[idx];
+                double xo = A.x[idx];
                 A.x[idx] = __dadd_rn(xo, val);
                 A.r[idx] = -0.0;
                 d = A.g.deg[u];
-                L.row[e] = A.g.row[u];
-                L.deg[e] = d;
-                L.cval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                A.frow[e] = A.g.row[u];
+                A.fcval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 fresh = __double_as_longlong(xo) == 0;  // first push of u
             }
-            // map groups to this entry: small -> 32-arc chunks whose first arc
-            // is in the row, large -> the row's pieces.  Hubs own hundreds of
-            // groups, so the warp writes long ranges together.
-            int64_t glo = 0, ghi = 0;
+            // chunks (32 arcs) whose first arc lies in entry e: [clo, chi).
+            // Hubs own thousands of chunks, so the warp writes them together.
+            int64_t clo = 0, chi = 0;
             if (live) {
-                const int64_t a0 = L.off[cur][e];
-                const int sh = chunk_shift(cls), msk = (1 << sh) - 1;
-                glo = (a0 + msk) >> sh;
-                ghi = min((a0 + d + msk) >> sh, L.mcap);
+                const int64_t a0 = fa_cur[e], a1 = e + 1 < F ? fa_cur[e + 1] : P;
+                clo = (a0 + 31) >> 5;
+                chi = min((a1 + 31) >> 5, A.ccap);
             }
-            unsigned big = __ballot_sync(FULL, ghi - glo > 4);
+            unsigned big = __ballot_sync(FULL, chi - clo > 4);
             if (!(big >> lane & 1u))
-                for (int64_t c = glo; c < ghi; ++c) L.map[c] = (int32_t)e;
+                for (int64_t c = clo; c < chi; ++c) A.chunk_e[c] = (int32_t)e;
             while (big) {
                 const int src = __ffs(big) - 1;
                 big &= big - 1;
-                const int64_t lo2 = __shfl_sync(FULL, glo, src), hi2 = __shfl_sync(FULL, ghi, src);
+                const int64_t lo2 = __shfl_sync(FULL, clo, src), hi2 = __shfl_sync(FULL, chi, src);
                 const int32_t e2 = (int32_t)__shfl_sync(FULL, e, src);
-                const int c2 = __shfl_sync(FULL, cls, src);
-                int32_t *mp = A.L[c2].map;
-                for (int64_t c = lo2 + lane; c < hi2; c += 32) mp[c] = e2;
+                for (int64_t c = lo2 + lane; c < hi2; c += 32) A.chunk_e[c] = e2;
             }
             slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
@@ -425,120 +363,68 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         counters_flush(S.pvol, A.s_pvol, A.m);
         counters_flush(S.push, A.s_pushes, A.m);
         grid.sync();
-        // ---------------- phase B1: large rows, PIECE-arc chunks -------------
-        // static arc-balanced split of the chunks across blocks, dynamic across
-        // the block's warps; a warp walks the row segments of its chunk with
-        // coalesced column loads, UNROLL_L x 32 atomics in flight, and a
-        // warp-uniform slot / contribution per segment
-        {
-            const FList &L = A.L[1];
-            const int64_t PL = Uc[1], FL = Fc[1];
-            const int64_t NC = (PL + PIECE - 1) >> 9;
-            const int64_t b0 = (int64_t)(((unsigned long long)NC * blockIdx.x) / gridDim.x);
-            const int64_t b1 = (int64_t)(((unsigned long long)NC * (blockIdx.x + 1)) / gridDim.x);
-            const int64_t *fo = L.off[cur];
-            for (;;) {
-                unsigned long long claim = 0;
-                if (lane == 0) claim = atomicAdd(S.next + 0, 1ULL);
-                const int64_t ch = b0 + (int64_t)__shfl_sync(FULL, claim, 0);
-                if (ch >= b1) break;
-                int64_t pos = ch << 9;
-                const int64_t end = min(pos + PIECE, PL);
-                int64_t e = L.map[ch];
-                while (pos < end) {
-                    const int64_t e0 = fo[e];
-                    const int64_t e1 = e + 1 < FL ? fo[e + 1] : PL;
-                    const int64_t seg = min(end, e1);
-                    const int32_t k = (int32_t)(L.key[cur][e] >> 32);
-                    const double c = L.cval[e];
-                    const int2 *cp = A.colp + L.row[e] + (pos - e0);
-                    double *rk = A.r + (int64_t)k * A.ld;
-                    const int64_t cnt = seg - pos;
-                    for (int64_t i0 = 0; i0 < cnt; i0 += 32 * UNROLL_L) {
-                        int2 vd[UNROLL_L];
-                        double old[UNROLL_L];
-                        bool valid[UNROLL_L];
+        // ---------------- phase B: arc-balanced scatter ----------------------
+        // chunk c = arcs [32c, 32c+32); every warp owns a contiguous chunk range
+        // and keeps UNROLL independent chunks (each lane one atomic) in flight.
+        const int64_t C = (P + 31) >> 5;
+        // static split across blocks, dynamic (shared counter) across the
+        // block's warps: latency variation between warps evens out
+        const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
+        const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
+        const int64_t *fa = A.farc[cur];
+        for (;;) {
+            unsigned long long claim = 0;
+            if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)UNROLL);
+            const int64_t cb = bc0 + (int64_t)__shfl_sync(FULL, claim, 0);
+            if (cb >= bc1) break;
+            const int64_t c1 = bc1;
+            int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
+            double c[UNROLL], old[UNROLL];
+            bool valid[UNROLL];
+            // stage 1: every load of all UNROLL chunks, before any atomic, so
+            // the chunks' dependent-load chains overlap
 #pragma unroll
-                        for (int q = 0; q < UNROLL_L; q++) {
-                            const int64_t i = i0 + 32 * q + lane;
-                            valid[q] = i < cnt;
-                            vd[q] = valid[q] ? __ldg(cp + i) : make_int2(0, 0);
-                        }
-#pragma unroll
-                        for (int q = 0; q < UNROLL_L; q++)
-                            old[q] = valid[q] ? atomicAdd(rk + vd[q].x, c) : 0.0;
-                        unsigned nf = 0, nz = 0;
-#pragma unroll
-                        for (int q = 0; q < UNROLL_L; q++) {
-                            const ArcOut o = classify(valid[q], old[q], c, vd[q].y, A.tcoeff);
-                            nf += __popc(__ballot_sync(FULL, o.first));
-                            nz += __popc(__ballot_sync(FULL, o.negz));
-                            stage_append(o.cross, k, vd[q].x, vd[q].y, S, A, nxt);
-                        }
-                        if (lane == 0) {
-                            if (nf) atomicAdd(S.touch + k, nf);
-                            if (nz) atomicAdd(S.negz + k, nz);
-                        }
-                    }
-                    pos = seg;
-                    ++e;
+            for (int q = 0; q < UNROLL; q++) {
+                const int64_t ch = cb + q;
+                const bool live = ch < c1;
+                const int64_t e = live ? A.chunk_e[ch] : 0;
+                const int64_t a = ch << 5;
+                // entries starting inside (a, a+32): one bit per start offset
+                const int64_t wi = e + 1 + lane;
+                const int64_t st = (live && wi < F) ? fa[wi] : INT64_MAX;
+                const int64_t pos = st - a;
+                const unsigned starts = __reduce_or_sync(FULL, pos < 32 ? (1u << pos) : 0u);
+                const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
+                const int64_t p = a + lane;
+                valid[q] = live && p < P;
+                k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
+                if (valid[q]) {
+                    k[q] = (int32_t)(A.fkey[cur][me] >> 32);
+                    c[q] = A.fcval[me];
+                    const int2 vd = __ldg(A.colp + A.frow[me] + (p - fa[me]));
+                    v[q] = vd.x;
+                    dv[q] = vd.y;
                 }
             }
-        }
-        // ---------------- phase B2: small rows, 32-arc chunks ----------------
-        // chunk c = arcs [32c, 32c+32) of the small list (several rows); a
-        // lane finds its row from the chunk's first entry + start bitmask
-        {
-            const FList &L = A.L[0];
-            const int64_t P = Uc[0], Fs = Fc[0];
-            const int64_t C = (P + 31) >> 5;
-            const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
-            const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
-            const int64_t *fa = L.off[cur];
-            for (;;) {
-                unsigned long long claim = 0;
-                if (lane == 0) claim = atomicAdd(S.next + 1, (unsigned long long)UNROLL);
-                const int64_t cb = bc0 + (int64_t)__shfl_sync(FULL, claim, 0);
-                if (cb >= bc1) break;
-                int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
-                double c[UNROLL], old[UNROLL];
-                bool valid[UNROLL];
+            // stage 2: the atomics, back to back (UNROLL in flight per lane)
 #pragma unroll
-                for (int q = 0; q < UNROLL; q++) {
-                    const int64_t ch = cb + q;
-                    const bool live = ch < bc1;
-                    const int64_t e = live ? L.map[ch] : 0;
-                    const int64_t a = ch << 5;
-                    const int64_t wi = e + 1 + lane;
-                    const int64_t st = (live && wi < Fs) ? fa[wi] : INT64_MAX;
-                    const int64_t pos = st - a;
-                    const unsigned starts = __reduce_or_sync(FULL, pos < 32 ? (1u << pos) : 0u);
-                    const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
-                    const int64_t p = a + lane;
-                    valid[q] = live && p < P;
-                    k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
-                    if (valid[q]) {
-                        k[q] = (int32_t)(L.key[cur][me] >> 32);
-                        c[q] = L.cval[me];
-                        const int2 vd = __ldg(A.colp + L.row[me] + (p - fa[me]));
-                        v[q] = vd.x;
-                        dv[q] = vd.y;
-                    }
-                }
+            for (int q = 0; q < UNROLL; q++)
+                old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+            // stage 3: first touch / re-touch of a pushed node / frontier entry
 #pragma unroll
-                for (int q = 0; q < UNROLL; q++)
-                    old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
-#pragma unroll
-                for (int q = 0; q < UNROLL; q++) {
-                    const ArcOut o = classify(valid[q], old[q], c[q], dv[q], A.tcoeff);
-                    block_count(o.first, k[q], 1u, S.touch);
-                    block_count(o.negz, k[q], 1u, S.negz);
-                    stage_append(o.cross, k[q], v[q], dv[q], S, A, nxt);
-                }
+            for (int q = 0; q < UNROLL; q++) {
+                const long long ob = __double_as_longlong(old[q]);
+                const double th = theta_deg(A.tcoeff, dv[q]);
+                const bool first = valid[q] && ob == 0;
+                const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
+                const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
+                block_count(first, k[q], 1u, S.touch);
+                block_count(negz, k[q], 1u, S.negz);
+                stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
         }
-        stage_flush(S, A, nxt);  // (its barriers also order the claim counter reset)
-        if (threadIdx.x == 0) S.next[0] = S.next[1] = 0;
+        stage_flush(S, A, nxt);  // (its barriers also order the chunk counter reset)
+        if (threadIdx.x == 0) *S.next = 0;
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
@@ -567,13 +453,11 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.s_conv[k] = 1;
     int32_t d = A.g.deg[s];
     if (alpha >= theta_deg(A.tcoeff, d)) {
-        const int cls = cls_of(d);
-        const FList &F = A.L[cls];
-        unsigned long long old = atomicAdd(F.ctr, (1ULL << CNT_SHIFT) + units_of(cls, d));
+        unsigned long long old = atomicAdd(A.fctr, (1ULL << CNT_SHIFT) + (unsigned long long)d);
         int64_t idx = (int64_t)(old >> CNT_SHIFT);
         if (idx < A.fcap) {
-            F.key[0][idx] = (k << 32) | (uint32_t)s;
-            F.off[0][idx] = (int64_t)(old & ARC_MASK);
+            A.fkey[0][idx] = (k << 32) | (uint32_t)s;
+            A.farc[0][idx] = (int64_t)(old & ARC_MASK);
         }
     }
 }
@@ -698,30 +582,13 @@ struct gd_batch {
     int slots;
     int grid;
     int64_t fcap, xcap;
-    DBuf<double> x, r;
+    DBuf<double> x, r, fcval;
     DBuf<int32_t> pushed, seed, s_last, s_conv, overflow;
-    DBuf<unsigned long long> touched, pushed_cnt, s_ops, s_pushes, s_negz, s_pvol, cursor;
-    DBuf<int64_t> slot_base;
-    struct ListBufs {  // one frontier list (see FList)
-        DBuf<int64_t> key0, key1, off0, off1, row;
-        DBuf<double> cval;
-        DBuf<int32_t> deg, map;
-        DBuf<unsigned long long> ctr;
-        int64_t mcap = 0;
-        void alloc(int64_t fc, int64_t mc) {
-            key0.alloc(fc); key1.alloc(fc); off0.alloc(fc); off1.alloc(fc);
-            row.alloc(fc); cval.alloc(fc); deg.alloc(fc); map.alloc(mc); ctr.alloc(2);
-            mcap = mc;
-        }
-        FList view() {
-            FList f;
-            f.key[0] = key0.p; f.key[1] = key1.p; f.off[0] = off0.p; f.off[1] = off1.p;
-            f.row = row.p; f.cval = cval.p; f.deg = deg.p; f.map = map.p; f.mcap = mcap;
-            f.ctr = ctr.p;
-            return f;
-        }
-    } lists[2];
+    DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
+    DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow, slot_base;
+    DBuf<int32_t> chunk_e;
     DBuf<int2> colp;
+    int64_t ccap = 0;
     DBuf<int64_t> rlog;
     static constexpr int64_t RLOG_CAP = 4096;
     // results
@@ -745,8 +612,9 @@ struct gd_batch {
         A.fcap = fcap;
         A.x = x.p; A.r = r.p; A.pushed = pushed.p; A.seed = seed.p;
         A.touched = touched.p; A.pushed_cnt = pushed_cnt.p;
-        A.L[0] = lists[0].view();
-        A.L[1] = lists[1].view();
+        A.fkey[0] = fkey0.p; A.fkey[1] = fkey1.p; A.farc[0] = farc0.p; A.farc[1] = farc1.p;
+        A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
+        A.chunk_e = chunk_e.p; A.ccap = ccap;
         A.colp = colp.p;
         A.rlog = rlog.p; A.rlog_cap = RLOG_CAP;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
@@ -782,8 +650,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
-        GD_CUDA(cudaMemsetAsync(B->lists[0].ctr.p, 0, 2 * sizeof(unsigned long long), st));
-        GD_CUDA(cudaMemsetAsync(B->lists[1].ctr.p, 0, 2 * sizeof(unsigned long long), st));
+        GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
         k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, B->p.alpha);
         GD_LAUNCH_CHECK();
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
@@ -903,13 +770,11 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->s_ops.alloc(slots); B->s_pushes.alloc(slots); B->s_negz.alloc(slots);
             B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
             B->slot_base.alloc(slots);
-            B->cursor.alloc(1); B->overflow.alloc(1);
-            // small list: < LARGE_MIN arcs per entry -> chunks <= entries;
-            // large list: pieces <= entries + arcs / PIECE
-            B->lists[0].alloc(fc, fc);
-            // large list: PIECE-arc chunks <= arcs of a round / PIECE + 1
-            const int64_t pieces = ((int64_t)slots * G->n_arcs) / PIECE + 2;
-            B->lists[1].alloc(fc, pieces < fc ? pieces : fc);
+            B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
+            B->fkey0.alloc(fc); B->fkey1.alloc(fc); B->farc0.alloc(fc); B->farc1.alloc(fc);
+            B->frow.alloc(fc); B->fcval.alloc(fc);
+            B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
+            B->chunk_e.alloc(B->ccap);
             B->rlog.alloc(3 * gd_batch::RLOG_CAP + 1);
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
             const size_t smem = stage_bytes(slots);
