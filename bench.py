@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--graph-seed", type=int, default=0)
     p.add_argument("--no-relabel", action="store_true", help="run on the caller's node order")
+    p.add_argument("--method", default="local-gd", choices=["local-gd", "local-sor"])
+    p.add_argument("--omega", type=float, default=1.0, help="local-sor relaxation")
     return p.parse_args()
 
 
@@ -146,11 +148,12 @@ class _HostGraph:
         self.degrees = np.diff(offsets)
 
 
-def cpu_reference(hg, alpha, eps, seeds, threads):
+def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0):
     from oracle import oracle as O
 
     t0 = time.perf_counter()
-    out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w, theta=hg.theta)
+    out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w, theta=hg.theta,
+                           method=method, omega=omega)
     return out, time.perf_counter() - t0
 
 
@@ -191,12 +194,13 @@ def run_reference(args):
     allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
     batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     # each step: a bounded prefix of that step's batch (about 3 s of CPU work)
-    _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][:threads], threads)
+    _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][:threads], threads, args.method,
+                          args.omega)
     per_step = int(min(args.seeds, max(threads, threads * 3.0 / max(dt, 1e-3))))
     times, ops, done = [], 0, 0
     for k in range(steps_total):
         sl = batches[k][:per_step]
-        out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads)
+        out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega)
         if k >= args.warmup:
             times.append(dt)
             ops += int(out["total_ops"].sum())
@@ -220,13 +224,15 @@ def run_reference(args):
 
 
 def workload_config(args, n, m):
-    return {"workload": f"batched LocalGD-PPR alpha={args.alpha} eps={args.eps:g}, "
+    name = "LocalGD" if args.method == "local-gd" else f"LocalSOR(omega={args.omega:g})"
+    return {"workload": f"batched {name}-PPR alpha={args.alpha} eps={args.eps:g}, "
                         f"R-MAT {args.shape}-shape ({n:,} nodes, {m:,} edges), "
                         f"{args.seeds} seeds/GPU/step from sample_sources",
             "graph": f"rmat-{args.shape}", "n": n, "edges": m, "alpha": args.alpha,
             "eps": args.eps, "seeds_per_gpu_per_step": args.seeds, "slots": args.slots,
             "l2": "inputs larger than L2 (int32 col_idx %.0f MB + per-seed state)" % (8.0 * m / 1e6),
-            "parallelism": f"seed-sharded x{args.gpus}"}
+            "parallelism": f"seed-sharded x{args.gpus}", "method": args.method,
+            "omega": args.omega if args.method == "local-sor" else None}
 
 
 def main():
@@ -253,7 +259,8 @@ def main():
     mine = shard_seeds(allseeds, rank, world)  # round-robin over the degree-ranked sample
     batches = [mine[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     dseeds = [torch.as_tensor(b, device="cuda") for b in batches]
-    solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots, relabel=not args.no_relabel)
+    solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots, relabel=not args.no_relabel,
+                         method=args.method, omega=args.omega)
     stream = torch.cuda.current_stream()
 
     def gather(res):
@@ -297,10 +304,10 @@ def main():
         ops, pushes, solved, kern_all = (float(v) for v in tsum)
     sec = ms / 1e3
     value = solved / sec
-    balg = b_alg_bytes(int(ops), int(pushes))
+    balg = b_alg_bytes(int(ops), int(pushes), args.method)
     # roofline of the dominant kernel (the sweep loop), rank-0 device events
     peak, peak_kind = peaks()
-    my_balg = b_alg_bytes(int(t[1]), int(t[2]))
+    my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic()
     # e2e: the public host API with host buffers, copies inside the timed region
@@ -335,7 +342,7 @@ def main():
         ref_sweeps, ref_ops = [], []
         while spent < args.cpu_seconds and pos < len(batches[args.warmup]):
             sl = batches[args.warmup][pos:pos + chunk]
-            o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads)
+            o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega)
             spent += dt
             sample.extend(sl.tolist())
             ref_sweeps.append(o["sweeps"])
@@ -358,9 +365,9 @@ def main():
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "b_alg_per_launch": my_balg / max(1, launches // 4),
+                         "b_alg_per_launch": my_balg / max(1, launches // 4 if args.method == "local-gd" else launches),
                          "peak_kind": peak_kind,
-                         "kernel": "k_rounds (persistent sweep loop)",
+                         "kernel": "k_rounds (persistent sweep loop)" if args.method == "local-gd" else "k_fifo_batch (warp per seed)",
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "relabel": not args.no_relabel,

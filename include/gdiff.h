@@ -132,9 +132,11 @@ int gd_gradient_descent(const gd_graph *g, const gd_operator *op, const double *
 /* A batch solves PPR systems (I - (1-alpha) A D^-1) x = alpha e_s for many
  * seeds s; the per-seed result equals local_gd(make_ppr_system(g, alpha, s,
  * eps)) (same frontier sets, sweeps and operation counts; x to rounding of
- * the atomic scatter order).  Per-seed state lives in `slots` dense HBM
- * vectors that are reset through dirty lists, never memset. */
-#define GD_M_LOCAL_GD 0
+ * the atomic scatter order) for GD_M_LOCAL_GD, and local_sor(..., omega)
+ * bit for bit for GD_M_LOCAL_SOR.  Per-seed state lives in `slots` dense
+ * HBM vectors that are reset by walking what a seed touched. */
+#define GD_M_LOCAL_GD 0  /* sweep-synchronous LocalGD (batch.cu)                 */
+#define GD_M_LOCAL_SOR 1 /* FIFO LocalSOR / LocalGS, one warp per seed, bit-exact */
 
 typedef struct gd_batch gd_batch;
 
@@ -151,6 +153,8 @@ typedef struct {
                              sectors / stay in L2); ids in and out are the
                              caller's.  Results are invariant. */
     int32_t reserved;
+    double omega;         /* GD_M_LOCAL_SOR: relaxation (1 = LocalGS, signed
+                             frontier when > 1, src/local_solvers.py:238) */
 } gd_batch_params;
 
 typedef struct {

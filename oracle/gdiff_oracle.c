@@ -609,6 +609,8 @@ typedef struct {
     const int64_t *off, *tgt;
     const double *w, *theta;
     double alpha;
+    int32_t method;  /* 0 local_gd, 1 local_sor */
+    double omega;
     const int64_t *seeds;
     int64_t n_seeds, max_sweeps;
     int64_t *out_sweeps, *out_ops, *out_pushes;
@@ -618,8 +620,9 @@ typedef struct {
 } batch_job;
 
 /* One seed exactly as `local_gd(dataclasses.replace(sys, b=alpha*e_s))`
- * would run it (src/local_solvers.py:428-470), including the per-solve O(n)
- * allocations and per-sweep O(n) l1 scans of the reference. */
+ * (src/local_solvers.py:428-470) or `local_sor(..., omega)` (:221-253) would
+ * run it, including the per-solve O(n) allocations and per-sweep O(n) l1
+ * scans of the reference. */
 static void *batch_worker(void *arg) {
     batch_job *J = arg;
     int64_t n = J->n;
@@ -631,9 +634,19 @@ static void *batch_worker(void *arg) {
         double *r = malloc(sizeof(double) * n);
         b[J->seeds[i]] = J->alpha;
         orc_report rep;
-        orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
         int64_t pushes = 0;
-        for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
+        if (J->method == 1) {
+            /* local_sor (src/local_solvers.py:221-253): x = 0, r = b, seeds = [s] */
+            memcpy(r, b, sizeof(double) * n);
+            memset(x, 0, sizeof(double) * n);
+            int64_t sd = J->seeds[i];
+            orc_push_kernel(n, J->off, J->tgt, J->w, J->theta, x, r, &sd, 1, J->omega, 1.0,
+                            J->omega > 1.0, J->max_sweeps, &rep);
+            pushes = -1;
+        } else {
+            orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
+            for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
+        }
         J->out_sweeps[i] = rep.sweeps;
         J->out_ops[i] = rep.total_ops;
         J->out_pushes[i] = pushes;
@@ -645,12 +658,12 @@ static void *batch_worker(void *arg) {
     return NULL;
 }
 
-int orc_batch_local_gd(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
-                       const double *theta, double alpha, const int64_t *seeds,
-                       int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
-                       int64_t *out_sweeps, int64_t *out_ops, int64_t *out_pushes,
-                       int32_t *out_conv, double *out_xsum) {
-    batch_job J = {n, off, tgt, w, theta, alpha, seeds, n_seeds, max_sweeps,
+int orc_batch_local(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                    const double *theta, double alpha, int32_t method, double omega,
+                    const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
+                    int64_t *out_sweeps, int64_t *out_ops, int64_t *out_pushes,
+                    int32_t *out_conv, double *out_xsum) {
+    batch_job J = {n, off, tgt, w, theta, alpha, method, omega, seeds, n_seeds, max_sweeps,
                    out_sweeps, out_ops, out_pushes, out_conv, out_xsum, 0};
     if (n_threads < 1) n_threads = 1;
     pthread_t *th = malloc(sizeof(pthread_t) * n_threads);

@@ -205,8 +205,9 @@ def gradient_descent(sys, max_sweeps: int = 10_000) -> dict:
 
 
 def batch_local_gd(g, alpha: float, eps: float, seeds, threads: int,
-                   max_sweeps: int = 1_000_000, arc_w=None, theta=None) -> dict:
-    """Per-seed reference local_gd over many host threads (CPU baseline)."""
+                   max_sweeps: int = 1_000_000, arc_w=None, theta=None, method: str = "local-gd",
+                   omega: float = 1.0) -> dict:
+    """Per-seed reference local_gd (or local_sor) over many host threads (CPU baseline)."""
     from paper_2410_21634_b200.systems import arc_weights_for, theta_vector
     off, tg = _arr64(g.offsets), _arr64(g.targets)
     w = _arrf(arc_w if arc_w is not None else arc_weights_for(g, 1.0 - alpha, "rw"))
@@ -216,8 +217,9 @@ def batch_local_gd(g, alpha: float, eps: float, seeds, threads: int,
     sw, ops, pu = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k, np.int64)
     cv = np.zeros(k, np.int32)
     xs = np.zeros(k)
-    lib().orc_batch_local_gd(C.c_int64(g.n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th),
-                             C.c_double(alpha), _p(sd, C.c_int64), C.c_int64(k),
+    lib().orc_batch_local(C.c_int64(g.n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th),
+                             C.c_double(alpha), C.c_int32(1 if method == "local-sor" else 0),
+                             C.c_double(omega), _p(sd, C.c_int64), C.c_int64(k),
                              C.c_int64(max_sweeps), C.c_int32(threads), _p(sw, C.c_int64),
                              _p(ops, C.c_int64), _p(pu, C.c_int64), _p(cv, C.c_int32), _p(xs))
     return {"sweeps": sw, "total_ops": ops, "pushes": pu, "converged": cv.astype(bool), "xsum": xs}

@@ -14,6 +14,6 @@ from .local_solvers import (local_ch, local_gd, local_gs, local_hk, local_sor, o
                             push_sweeps)
 from .global_solvers import GlobalConfig, gradient_descent
 from .dynamic import PprPair, event_adjust, make_pair, parse_events, repair, run_snapshots
-from .batch import BatchOutput, BatchSolver, local_gd_batch
+from .batch import BatchOutput, BatchSolver, local_gd_batch, local_sor_batch
 
 __version__ = "0.1.0"

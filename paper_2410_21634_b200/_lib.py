@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libgdiff.so")
 GD_OK, GD_ERR_ARG, GD_ERR_CUDA, GD_ERR_OOM, GD_ERR_CAPACITY, GD_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GD_W_RW, GD_W_CONST, GD_W_ARC = 0, 1, 2
 GD_T_DEGREE, GD_T_ARRAY = 0, 1
-GD_M_LOCAL_GD = 0
+GD_M_LOCAL_GD, GD_M_LOCAL_SOR = 0, 1
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -55,7 +55,7 @@ class BatchParams(C.Structure):
     _fields_ = [("method", C.c_int32), ("slots", C.c_int32), ("alpha", C.c_double),
                 ("eps", C.c_double), ("max_sweeps", C.c_int64),
                 ("frontier_cap", C.c_int64), ("out_cap", C.c_int64),
-                ("relabel", C.c_int32), ("reserved", C.c_int32)]
+                ("relabel", C.c_int32), ("reserved", C.c_int32), ("omega", C.c_double)]
 
 
 class BatchResult(C.Structure):

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib as gdl
 from .device import DeviceGraph, device_graph
 
-__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch"]
+__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch"]
 
 
 def _host_array(count: int, dtype, pinned: bool) -> np.ndarray:
@@ -62,20 +62,31 @@ class BatchOutput:
 
 
 class BatchSolver:
-    """Solve (I - (1-alpha) A D^-1) x = alpha e_s for many seeds s."""
+    """Solve (I - (1-alpha) A D^-1) x = alpha e_s for many seeds s.
+
+    method "local-gd": sweep-synchronous LocalGD (frontier sets, sweeps and
+    operation counts identical to the reference, x to 1e-9);
+    method "local-sor": FIFO LocalSOR with relaxation omega (omega = 1:
+    LocalGS), one warp per seed, bit-identical with the reference."""
 
     def __init__(self, g, alpha: float, eps: float, slots: int = 0,
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
-                 device: int = 0, relabel: bool = True):
+                 device: int = 0, relabel: bool = True, method: str = "local-gd",
+                 omega: float = 1.0):
         if not 0.0 < alpha <= 1.0:
             raise ValueError("alpha must be in (0, 1]")
+        if method not in ("local-gd", "local-sor"):
+            raise ValueError(f"unknown batch method {method!r}")
+        if method == "local-sor" and not 0.0 < omega <= 2.0:
+            raise ValueError("omega must be in (0, 2]")
+        self.method = method
         self.lib = gdl.load()
         self.graph = g if isinstance(g, DeviceGraph) else device_graph(g, device)
         self.alpha, self.eps = float(alpha), float(eps)
-        p = gdl.BatchParams(method=gdl.GD_M_LOCAL_GD, slots=int(slots), alpha=self.alpha,
-                            eps=self.eps, max_sweeps=int(max_sweeps),
-                            frontier_cap=int(frontier_cap), out_cap=int(out_cap),
-                            relabel=int(bool(relabel)))
+        p = gdl.BatchParams(method=gdl.GD_M_LOCAL_SOR if method == "local-sor" else gdl.GD_M_LOCAL_GD,
+                            slots=int(slots), alpha=self.alpha, eps=self.eps,
+                            max_sweeps=int(max_sweeps), frontier_cap=int(frontier_cap),
+                            out_cap=int(out_cap), relabel=int(bool(relabel)), omega=float(omega))
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
@@ -170,16 +181,34 @@ class BatchSolver:
         raise gdl.GdiffError(gdl.GD_ERR_CAPACITY, "output sizing failed")
 
 
-def local_gd_batch(g, seeds, alpha: float, eps: float, slots: int = 0,
-                   max_sweeps: int = 1_000_000, relabel: bool = True) -> BatchOutput:
-    """Batched LocalGD-PPR over `seeds` (host in, host out)."""
+def _check_seeds(g, seeds) -> np.ndarray:
     deg = np.asarray(g.degrees)
     sd = np.asarray(seeds, dtype=np.int64)
     if sd.size and (sd.min() < 0 or sd.max() >= g.n):
         raise ValueError("seed out of range")
     if sd.size and np.any(deg[sd] < 1):
         raise ValueError("source must have at least one neighbor")
+    return sd
+
+
+def local_gd_batch(g, seeds, alpha: float, eps: float, slots: int = 0,
+                   max_sweeps: int = 1_000_000, relabel: bool = True) -> BatchOutput:
+    """Batched LocalGD-PPR over `seeds` (host in, host out)."""
+    sd = _check_seeds(g, seeds)
     solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, relabel=relabel)
+    try:
+        return solver.solve(sd)
+    finally:
+        solver.close()
+
+
+def local_sor_batch(g, seeds, alpha: float, eps: float, omega: float = 1.0, slots: int = 0,
+                    max_sweeps: int = 1_000_000) -> BatchOutput:
+    """Batched LocalSOR-PPR (omega = 1: LocalGS), bit-identical per seed with
+    local_sor(make_ppr_system(g, alpha, s, eps), omega)."""
+    sd = _check_seeds(g, seeds)
+    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method="local-sor",
+                         omega=omega)
     try:
         return solver.solve(sd)
     finally:

@@ -23,7 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{INCLUDE}"]
-SOURCES = ["graph.cu", "exact.cu", "fifo.cu", "global.cu", "batch.cu", "generate.cu"]
+SOURCES = ["graph.cu", "exact.cu", "fifo.cu", "fifo_batch.cu", "global.cu", "batch.cu",
+           "generate.cu"]
 
 
 def _deps_newer(obj: str, src: str) -> bool:

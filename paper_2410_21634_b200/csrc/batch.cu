@@ -40,6 +40,17 @@
 
 namespace cg = cooperative_groups;
 
+namespace gd {  // fifo_batch.cu
+struct FifoBatchState;
+FifoBatchState *fifo_batch_create(const gd_graph *G, int slots);
+void fifo_batch_destroy(FifoBatchState *F);
+int fifo_batch_slots(const FifoBatchState *F);
+void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
+                    const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
+                    int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
+                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st);
+}  // namespace gd
+
 namespace gd {
 namespace {
 
@@ -576,6 +587,7 @@ using namespace gd;
 
 struct gd_batch {
     const gd_graph *G;      // caller's graph
+    FifoBatchState *fifo = nullptr;  // GD_M_LOCAL_SOR state
     gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
     DBuf<int32_t> perm, inv;
     gd_batch_params p;
@@ -628,6 +640,7 @@ struct gd_batch {
     ~gd_batch() {
         for (auto e : ev) cudaEventDestroy(e);
         delete R;
+        if (fifo) fifo_batch_destroy(fifo);
     }
 };
 
@@ -637,6 +650,28 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
     GD_CUDA(cudaMemsetAsync(B->overflow.p, 0, sizeof(int32_t), st));
+    if (B->fifo) {  // FIFO methods: one persistent launch, warps pull seeds
+        if (B->ev.empty()) {
+            cudaEvent_t e0, e1;
+            GD_CUDA(cudaEventCreate(&e0));
+            GD_CUDA(cudaEventCreate(&e1));
+            B->ev.push_back(e0);
+            B->ev.push_back(e1);
+        }
+        GD_CUDA(cudaMemsetAsync(B->support.p, 0xFF, sizeof(int64_t) * ns, st));  // not tracked
+        GD_CUDA(cudaEventRecord(B->ev[0], st));
+        if (n_seeds)
+            fifo_batch_run(B->fifo, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
+                           B->pushes.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p,
+                           B->xvals.p, B->xcap, B->cursor.p, st);
+        GD_CUDA(cudaEventRecord(B->ev[1], st));
+        GD_CUDA(cudaStreamSynchronize(st));
+        float f = 0.f;
+        GD_CUDA(cudaEventElapsedTime(&f, B->ev[0], B->ev[1]));
+        B->last_ms = f;
+        B->last_launches = n_seeds ? 1 : 0;
+        return;
+    }
     const int64_t waves = (n_seeds + B->slots - 1) / B->slots;
     while ((int64_t)B->ev.size() < 2 * waves) {
         cudaEvent_t e;
@@ -729,7 +764,10 @@ extern "C" {
 int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out) {
     return guarded([&] {
         GD_CHECK_ARG(G && p && out, "null pointer");
-        GD_CHECK_ARG(p->method == GD_M_LOCAL_GD, "only GD_M_LOCAL_GD is batched");
+        GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR,
+                     "unknown batch method");
+        GD_CHECK_ARG(p->method != GD_M_LOCAL_SOR || (p->omega > 0.0 && p->omega <= 2.0),
+                     "omega must be in (0, 2]");
         GD_CHECK_ARG(p->alpha > 0.0 && p->alpha <= 1.0, "alpha must be in (0, 1]");
         GD_CHECK_ARG(p->eps > 0.0, "eps must be positive");
         GD_CHECK_ARG(G->n_arcs < (1LL << CNT_SHIFT), "too many arcs");
@@ -741,6 +779,16 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->G = G;
             B->p = *p;
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
+            if (p->method == GD_M_LOCAL_SOR) {
+                // exact FIFO replay needs the caller's CSR order: no relabeling
+                B->fifo = fifo_batch_create(G, p->slots);
+                B->slots = fifo_batch_slots(B->fifo);
+                B->cursor.alloc(1); B->overflow.alloc(1);
+                B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
+                B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
+                *out = B;
+                return;
+            }
             if (p->relabel) build_relabeled(B);
             B->colp.alloc(G->n_arcs ? G->n_arcs : 1);
             k_pack_cols<<<4 * n_sms(G->device), 256>>>(B->work()->view(), B->colp.p);

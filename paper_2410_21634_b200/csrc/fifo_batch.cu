@@ -1,0 +1,280 @@
+// fifo_batch.cu -- batched LocalSOR / LocalGS-PPR: one warp per seed.
+//
+// Every seed is an independent replay of the reference FIFO push
+// (_push_kernel src/local_solvers.py:48-188 via local_sor :221-253) on
+// b = alpha e_s: same pops, same enqueue order (ballot + popc over 32
+// consecutive arcs of the row keeps CSR order), same fl() sequence -- so x,
+// the sweep count and the operation count are bit-identical with the
+// reference, per seed.  A warp owns a slot (dense x / r, ring queue, queue
+// marks, touched marks) and pulls seeds from a global counter until the
+// batch is exhausted; the slot is cleaned by walking its touched list.
+//
+// Bound: latency of the per-pop dependent chain (a Gauss-Seidel push cannot
+// start before the previous one finished); throughput comes from many
+// warps, i.e. from slot count x SM residency, sized to HBM capacity.
+#include "common.cuh"
+
+namespace gd {
+namespace {
+
+constexpr int FB_THREADS = 256;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct FifoBatchArgs {
+    DevGraph g;
+    double alpha, beta, tcoeff, omega;
+    int sgn;
+    int64_t n, ld, max_sweeps, n_seeds, xcap;
+    double *x, *r;
+    int32_t *queue;        // ld + 2 per slot
+    uint8_t *qmark, *tmark;
+    int32_t *touched;      // touched list per slot (ld)
+    const int64_t *seeds;
+    unsigned long long *next_seed, *cursor;
+    int64_t *sweeps, *ops, *pushes, *xoff, *xcnt;
+    int32_t *conv;
+    int32_t *xnodes;
+    double *xvals;
+    int nslots;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ double theta_d(double tc, int32_t d) {
+    return d > 0 ? __dmul_rn(tc, (double)d) : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+__global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int slot = (int)((blockIdx.x * (int64_t)FB_THREADS + threadIdx.x) >> 5);
+    if (slot >= A.nslots) return;
+    const int64_t off = (int64_t)slot * A.ld;
+    double *x = A.x + off, *r = A.r + off;
+    int32_t *queue = A.queue + (int64_t)slot * (A.ld + 2);
+    uint8_t *qmark = A.qmark + off, *tmark = A.tmark + off;
+    int32_t *touched = A.touched + off;
+    const int64_t sent = A.n, qcap = A.n + 2;
+
+    for (;;) {
+        unsigned long long si = 0;
+        if (lane == 0) si = atomicAdd(A.next_seed, 1ULL);
+        si = __shfl_sync(FULL, si, 0);
+        if ((int64_t)si >= A.n_seeds) break;
+        const int32_t s = (int32_t)A.seeds[si];
+        // b = alpha e_s, x = 0 (slot is clean); seed enqueue (:59-69)
+        int64_t ntouch = 1;
+        if (lane == 0) {
+            r[s] = A.alpha;
+            tmark[s] = 1;
+            touched[0] = s;
+        }
+        __syncwarp();
+        int64_t front = 0, rear = 0;
+        const double ths = theta_d(A.tcoeff, A.g.deg[s]);
+        const bool act0 = A.sgn ? fabs(A.alpha) >= ths : A.alpha >= ths;
+        int64_t sweeps = 0, ops = 0, pushes = 0;
+        int conv = 1;
+        if (act0) {
+            if (lane == 0) {
+                queue[0] = s;
+                qmark[s] = 1;
+                queue[1] = (int32_t)sent;
+            }
+            rear = 2;
+            int64_t svol = 0;
+            __syncwarp();
+            for (;;) {
+                const int64_t u = queue[front];
+                front = (front + 1 == qcap) ? 0 : front + 1;
+                if (u == sent) {  // sweep boundary (:102-144)
+                    ops += svol;
+                    sweeps += 1;
+                    if (front == rear) break;
+                    if (sweeps >= A.max_sweeps) {
+                        conv = 0;
+                        break;
+                    }
+                    if (lane == 0) queue[rear] = (int32_t)sent;
+                    rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                    svol = 0;
+                    __syncwarp();
+                    continue;
+                }
+                if (lane == 0) qmark[u] = 0;
+                const double ru = r[u];
+                const int32_t d = A.g.deg[u];
+                const double th = theta_d(A.tcoeff, d);
+                if (A.sgn ? fabs(ru) < th : ru < th) {
+                    __syncwarp();
+                    continue;
+                }
+                svol += d;
+                pushes += 1;
+                const double res = __dmul_rn(A.omega, ru);
+                if (lane == 0) {
+                    x[u] = __dadd_rn(x[u], res);  // x_gain = 1
+                    r[u] = __dsub_rn(ru, res);
+                }
+                const double w = __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta);
+                const int64_t rs = A.g.row[u];
+                for (int64_t base = 0; base < d; base += 32) {
+                    const int64_t j = base + lane;
+                    bool act = false, fresh = false;
+                    int32_t v = 0;
+                    if (j < d) {
+                        v = A.g.col[rs + j];
+                        const double rv = __dadd_rn(r[v], __dmul_rn(res, w));
+                        r[v] = rv;
+                        fresh = !tmark[v];
+                        if (fresh) tmark[v] = 1;
+                        if (!qmark[v]) {
+                            const double tv = theta_d(A.tcoeff, A.g.deg[v]);
+                            act = A.sgn ? fabs(rv) >= tv : rv >= tv;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(FULL, act);
+                    if (act) {
+                        int64_t q = rear + __popc(bal & lanemask_lt());
+                        if (q >= qcap) q -= qcap;
+                        queue[q] = v;
+                        qmark[v] = 1;
+                    }
+                    rear += __popc(bal);
+                    if (rear >= qcap) rear -= qcap;
+                    const unsigned fb = __ballot_sync(FULL, fresh);
+                    if (fresh) touched[ntouch + __popc(fb & lanemask_lt())] = v;
+                    ntouch += __popc(fb);
+                }
+                __syncwarp();
+                const double ru2 = __dsub_rn(ru, res);  // self re-check (:176-185)
+                if (A.sgn ? fabs(ru2) >= th : ru2 >= th) {
+                    if (lane == 0) {
+                        queue[rear] = (int32_t)u;
+                        qmark[u] = 1;
+                    }
+                    rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                }
+                __syncwarp();
+            }
+        }
+        // outputs: x over touched nodes with x != 0, then clean the slot
+        int64_t nx = 0;
+        for (int64_t i = lane; i < ntouch; i += 32) nx += x[touched[i]] != 0.0;
+        for (int o = 16; o > 0; o >>= 1) nx += __shfl_xor_sync(FULL, nx, o);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.cursor, (unsigned long long)nx);
+        base = __shfl_sync(FULL, base, 0);
+        int64_t w = (int64_t)base;
+        for (int64_t i0 = 0; i0 < ntouch; i0 += 32) {
+            const int64_t i = i0 + lane;
+            int32_t v = 0;
+            double xv = 0.0;
+            if (i < ntouch) {
+                v = touched[i];
+                xv = x[v];
+                x[v] = 0.0;
+                r[v] = 0.0;
+                qmark[v] = 0;
+                tmark[v] = 0;
+            }
+            const unsigned nzb = __ballot_sync(FULL, xv != 0.0);
+            if (xv != 0.0) {
+                const int64_t pos = w + __popc(nzb & lanemask_lt());
+                if (pos < A.xcap) {
+                    A.xnodes[pos] = v;
+                    A.xvals[pos] = xv;
+                }
+            }
+            w += __popc(nzb);
+        }
+        if (lane == 0) {
+            A.sweeps[si] = sweeps;
+            A.ops[si] = ops;
+            A.pushes[si] = pushes;
+            A.conv[si] = conv;
+            A.xoff[si] = (int64_t)base;
+            A.xcnt[si] = nx;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+// Host side, called from batch.cu for GD_M_LOCAL_SOR batches.
+struct FifoBatchState {
+    int nslots = 0;
+    int64_t ld = 0;
+    DBuf<double> x, r;
+    DBuf<int32_t> queue, touched;
+    DBuf<uint8_t> qmark, tmark;
+    DBuf<unsigned long long> ctr;  // next_seed
+};
+
+FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
+    const int64_t n = G->n ? G->n : 1;
+    const int64_t ld = (n + 1) & ~1LL;
+    if (slots <= 0) {
+        size_t fr = 0, tot = 0;
+        GD_CUDA(cudaMemGetInfo(&fr, &tot));
+        const int64_t per = ld * (8 + 8 + 4 + 1 + 1 + 4) + 8;
+        int64_t by_mem = (int64_t)(fr / 3) / per;
+        int64_t resident = (int64_t)n_sms(G->device) * 64;  // warps
+        slots = (int)(by_mem < resident ? (by_mem < 1 ? 1 : by_mem) : resident);
+    }
+    FifoBatchState *F = new FifoBatchState();
+    try {
+        F->nslots = slots;
+        F->ld = ld;
+        const size_t sn = (size_t)slots * (size_t)ld;
+        F->x.alloc(sn); F->r.alloc(sn); F->touched.alloc(sn);
+        F->queue.alloc((size_t)slots * (size_t)(ld + 2));
+        F->qmark.alloc(sn); F->tmark.alloc(sn);
+        GD_CUDA(cudaMemset(F->x.p, 0, sizeof(double) * sn));
+        GD_CUDA(cudaMemset(F->r.p, 0, sizeof(double) * sn));
+        GD_CUDA(cudaMemset(F->qmark.p, 0, sn));
+        GD_CUDA(cudaMemset(F->tmark.p, 0, sn));
+        F->ctr.alloc(1);
+    } catch (...) {
+        delete F;
+        throw;
+    }
+    return F;
+}
+
+void fifo_batch_destroy(FifoBatchState *F) { delete F; }
+
+int fifo_batch_slots(const FifoBatchState *F) { return F->nslots; }
+
+void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
+                    const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
+                    int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
+                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st) {
+    FifoBatchArgs A{};
+    A.g = G->view();
+    A.alpha = p.alpha;
+    A.beta = 1.0 - p.alpha;
+    A.tcoeff = p.eps * p.alpha;
+    A.omega = p.omega;
+    A.sgn = p.omega > 1.0 ? 1 : 0;
+    A.n = G->n;
+    A.ld = F->ld;
+    A.max_sweeps = p.max_sweeps > 0 ? p.max_sweeps : 1000000;
+    A.n_seeds = n_seeds;
+    A.xcap = xcap;
+    A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p; A.tmark = F->tmark.p;
+    A.touched = F->touched.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
+    A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv; A.xoff = xoff;
+    A.xcnt = xcnt; A.xnodes = xnodes; A.xvals = xvals; A.nslots = F->nslots;
+    GD_CUDA(cudaMemsetAsync(F->ctr.p, 0, sizeof(unsigned long long), st));
+    const int64_t warps = F->nslots < n_seeds ? F->nslots : (n_seeds ? n_seeds : 1);
+    const int blocks = (int)((warps * 32 + FB_THREADS - 1) / FB_THREADS);
+    k_fifo_batch<<<blocks, FB_THREADS, 0, st>>>(A);
+    GD_LAUNCH_CHECK();
+}
+
+}  // namespace gd

@@ -101,3 +101,40 @@ def test_device_generator_equals_host(gpu):
         h = rmat_graph(n, m, seed=seed)
         assert np.array_equal(row.cpu().numpy(), h.offsets)
         assert np.array_equal(col.cpu().numpy().astype(np.int64), h.targets)
+
+
+# ---- batched FIFO (LocalSOR / LocalGS): bit-identical per seed ------------
+
+@pytest.mark.parametrize("omega", [1.0, 1.39301, 0.7])
+@pytest.mark.parametrize("slots", [0, 5])
+def test_sor_batch_bitwise_vs_oracle(gpu, cora, omega, slots):
+    from paper_2410_21634_b200.batch import local_sor_batch
+    from paper_2410_21634_b200.systems import make_ppr_system
+    g = golden_graph(cora, "cora")
+    seeds = cora["seeds"][:24]
+    out = local_sor_batch(g, seeds, 0.1, 1e-6, omega=omega, slots=slots)
+    for i, s in enumerate(seeds):
+        ref = O.local_sor(make_ppr_system(g, 0.1, int(s), 1e-6), omega)
+        assert out.sweeps[i] == ref["sweeps"] and out.total_ops[i] == ref["total_ops"]
+        assert bool(out.converged[i]) == ref["converged"]
+        assert np.array_equal(out.x_dense(i, g.n), ref["x"]), (i, s)
+
+
+def test_sor_batch_matches_reference_golden(gpu, pa):
+    from paper_2410_21634_b200.batch import local_sor_batch
+    g = golden_graph(pa, "pa2000")
+    seeds = pa["seeds"][:4]
+    for meth, omega in (("local_gs", 1.0), ("local_sor", float(pa["s0/local_sor/param/omega"]))):
+        out = local_sor_batch(g, seeds, 0.1, 1e-6, omega=omega, slots=2)
+        for i in range(4):
+            k = f"s{i}/{meth}"
+            assert out.sweeps[i] == pa[f"{k}/sweeps"] and out.total_ops[i] == pa[f"{k}/total_ops"]
+            assert np.array_equal(out.x_dense(i, g.n), pa[f"{k}/x"])
+
+
+def test_sor_batch_max_sweeps(gpu):
+    from paper_2410_21634_b200.batch import local_sor_batch
+    from paper_2410_21634_b200.graph import from_edges
+    g = from_edges(4, [(0, 1), (1, 2), (2, 0)])
+    out = local_sor_batch(g, [0, 1], 0.2, 1e-9, max_sweeps=2)
+    assert (out.sweeps == 2).all() and not out.converged.any()
