@@ -104,6 +104,15 @@ int gd_graph_info(const gd_graph *g, int64_t *n, int64_t *n_arcs, int64_t *d_max
 int gd_local_gd(const gd_graph *g, const gd_operator *op, const double *b, double *x,
                 double *r, int64_t max_sweeps, int32_t record_trace, gd_report *rep);
 
+/* Warm-started (signed) LocalGD from a pair: x = p, r = s - Q p on entry,
+ * updated in place; S_0 = filter(flatnonzero(r)).  The sweep loop of
+ * local_gd (src/local_solvers.py:364-470) with _filter_frontier(signed)
+ * :336-350, started from the event-adjusted pair of dynamic.py:110-128
+ * (the LocalGD form of repair, config 5). */
+int gd_local_gd_warm(const gd_graph *g, const gd_operator *op, double *x, double *r,
+                     int32_t is_signed, int64_t max_sweeps, int32_t record_trace,
+                     gd_report *rep);
+
 /* LocalCH: replaces local_ch (src/local_solvers.py:473-538); mu, L already
  * resolved (the _cheby_bounds rule, :541-558). */
 int gd_local_ch(const gd_graph *g, const gd_operator *op, const double *b, double *x,

@@ -290,6 +290,47 @@ int orc_local_gd(int64_t n, const int64_t *off, const int64_t *tgt, const double
     return 0;
 }
 
+/* Warm-started signed LocalGD: the reference
+ * sweep loop (src/local_solvers.py:364-470: _SweepDriver, _apply_update_seq,
+ * _filter_frontier with signed=True) started from a given pair (x = p,
+ * r = s - Q p) instead of (0, b); S_0 = filter(flatnonzero(r)).  x and r
+ * are read and updated in place. */
+int orc_local_gd_warm(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                      const double *theta, double *x, double *r, int32_t sgn,
+                      int64_t max_sweeps, int32_t record_trace, orc_report *rep) {
+    rep_init(rep);
+    double *r0 = calloc(n ? n : 1, sizeof(double));
+    double *x0 = calloc(n ? n : 1, sizeof(double));
+    memcpy(r0, r, sizeof(double) * n);
+    memcpy(x0, x, sizeof(double) * n);
+    sweep_driver d;
+    drv_init(&d, n, off, tgt, w, theta, r0, x, r, sgn, rep);
+    memcpy(x, x0, sizeof(double) * n); /* drv_init zeroes x; warm start keeps p */
+    double *vals = malloc(sizeof(double) * (n ? n : 1));
+    while (d.fcount) {
+        if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
+        rep_grow(rep);
+        rep->frontier_sizes[rep->n_logs] = d.fcount;
+        if (record_trace) rep_trace(rep, d.front, d.fcount);
+        int64_t svol = 0;
+        for (int64_t i = 0; i < d.fcount; i++) {
+            int64_t u = d.front[i];
+            svol += off[u + 1] - off[u];
+            vals[i] = r[u];
+        }
+        double sgamma = pw_sum(vals, d.fcount, 1);
+        for (int64_t i = 0; i < d.fcount; i++) x[d.front[i]] += vals[i];
+        drv_apply(&d, vals);
+        drv_log(&d, rep, svol, sgamma);
+        rep->total_ops += svol;
+        rep->sweeps += 1;
+    }
+    rep->support_size = count_nonzero(r, n);
+    free(vals); free(r0); free(x0);
+    drv_free(&d);
+    return 0;
+}
+
 /* src/local_solvers.py:473-538 (local_ch); mu, L resolved by the caller via
  * the _cheby_bounds rule (src/local_solvers.py:541-558). */
 int orc_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,

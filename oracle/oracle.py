@@ -108,6 +108,18 @@ def local_gd(sys, max_sweeps: int = 1_000_000, record_trace: bool = True) -> dic
     return out
 
 
+def local_gd_warm(offsets, targets, arc_w, theta, x, r, signed=True, max_sweeps=1_000_000,
+                  record_trace=True) -> dict:
+    """Warm-started signed LocalGD from (x, r), in place."""
+    off, tg, w, th = _arr64(offsets), _arr64(targets), _arrf(arc_w), _arrf(theta)
+    assert x.dtype == np.float64 and r.dtype == np.float64 and x.flags.c_contiguous
+    rep = _Report()
+    lib().orc_local_gd_warm(C.c_int64(th.shape[0]), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w),
+                            _p(th), _p(x), _p(r), C.c_int32(int(signed)), C.c_int64(max_sweeps),
+                            C.c_int32(int(record_trace)), C.byref(rep))
+    return _unpack(rep, with_trace=record_trace)
+
+
 def cheby_bounds(sys, mu=None, L=None):
     """src/local_solvers.py:541-558."""
     if mu is not None and L is not None:

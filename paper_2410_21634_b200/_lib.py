@@ -77,6 +77,8 @@ SIGNATURES = {
     "gd_graph_info": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p]),
     "gd_local_gd": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_int64,
                               C.c_int32, C.POINTER(Report)]),
+    "gd_local_gd_warm": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, C.c_int32,
+                                   C.c_int64, C.c_int32, C.POINTER(Report)]),
     "gd_local_ch": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_double,
                               C.c_double, C.c_int64, C.c_int32, C.POINTER(Report)]),
     "gd_push_kernel": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _i64p, C.c_int64,

@@ -16,6 +16,7 @@
 // The batched throughput path (batch.cu) trades the sort for fp64 atomics.
 #include <cub/cub.cuh>
 
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -265,18 +266,23 @@ struct SweepSolver {
 
     void tmp_need(size_t bytes) { tmp.ensure(bytes ? bytes : 1); }
 
-    SweepSolver(const gd_graph *G_, const gd_operator *o, bool sgn_) : G(G_), sgn(sgn_) {
+    // Buffers are kept across calls (per host thread, grown on demand): a
+    // drop-in call should not pay a dozen n-sized cudaMalloc/cudaFree pairs.
+    void prepare(const gd_graph *G_, const gd_operator *o, bool sgn_) {
+        G = G_;
+        sgn = sgn_;
         g = G->view();
         n = G->n;
         upload_op(G, o, n, op, s);
         size_t nn = n ? n : 1;
-        x.alloc(nn); r.alloc(nn); vals.alloc(nn); absv.alloc(nn); wnode.alloc(nn);
-        F.alloc(nn); Fn.alloc(nn); fstamp.alloc(nn); seeds.alloc(nn);
-        fdeg.alloc(nn + 1); arcoff.alloc(nn + 1); trace64.alloc(nn); cnt.alloc(4);
-        red_ps.alloc(RED_BLOCKS); red_pm.alloc(RED_BLOCKS); scal.alloc(4);
-        flag.alloc(nn);
+        x.ensure(nn); r.ensure(nn); vals.ensure(nn); absv.ensure(nn); wnode.ensure(nn);
+        F.ensure(nn); Fn.ensure(nn); fstamp.ensure(nn); seeds.ensure(nn);
+        fdeg.ensure(nn + 1); arcoff.ensure(nn + 1); trace64.ensure(nn); cnt.ensure(4);
+        red_ps.ensure(RED_BLOCKS); red_pm.ensure(RED_BLOCKS); scal.ensure(4);
+        flag.ensure(nn);
+        bits = 1;
         while ((1LL << bits) < n) ++bits;
-        GD_CUDA(cudaMemset(fstamp.p, 0xFF, sizeof(int32_t) * nn));  // -1: never in S_t
+        GD_CUDA(cudaMemsetAsync(fstamp.p, 0xFF, sizeof(int32_t) * nn, s));  // -1: never in S_t
     }
 
     void reduce_l1_min(double *host2) {
@@ -287,10 +293,13 @@ struct SweepSolver {
         GD_CUDA(cudaStreamSynchronize(s));
     }
 
-    // S_0 = filter(flatnonzero(b)) in index order
-    int64_t init(const double *b) {
+    // S_0 = filter(flatnonzero(b)) in index order; x = x0 (zero unless warm)
+    int64_t init(const double *b, const double *x0 = nullptr) {
         GD_CUDA(cudaMemcpy(r.p, b, sizeof(double) * n, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemset(x.p, 0, sizeof(double) * (n ? n : 1)));
+        if (x0)
+            GD_CUDA(cudaMemcpy(x.p, x0, sizeof(double) * n, cudaMemcpyHostToDevice));
+        else
+            GD_CUDA(cudaMemset(x.p, 0, sizeof(double) * (n ? n : 1)));
         std::vector<int32_t> nz;
         for (int64_t i = 0; i < n; i++)
             if (b[i] != 0.0) nz.push_back((int32_t)i);
@@ -389,6 +398,17 @@ struct SweepSolver {
     }
 };
 
+SweepSolver &solver_for(const gd_graph *G, const gd_operator *o, bool sgn) {
+    thread_local std::unique_ptr<SweepSolver> cache;
+    thread_local int device = -1;
+    if (!cache || device != G->device) {
+        cache.reset(new SweepSolver());
+        device = G->device;
+    }
+    cache->prepare(G, o, sgn);
+    return *cache;
+}
+
 }  // namespace
 }  // namespace gd
 
@@ -396,15 +416,15 @@ using namespace gd;
 
 extern "C" {
 
-int gd_local_gd(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
-                int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
-    return guarded([&] {
-        GD_CHECK_ARG(G && o && b && x && r && rep, "null pointer");
+static void local_gd_run(const gd_graph *G, const gd_operator *o, const double *b,
+                         const double *x0, bool sgn, double *x, double *r, int64_t max_sweeps,
+                         int32_t record_trace, gd_report *rep) {
+    {
         GD_CUDA(cudaSetDevice(G->device));
         int64_t cap = 64, tcap = 0;
         report_alloc(rep, cap);
-        SweepSolver S(G, o, false);
-        int64_t f = S.init(b);
+        SweepSolver &S = solver_for(G, o, sgn);
+        int64_t f = S.init(b, x0);
         double lm[2];
         S.reduce_l1_min(lm);
         rep->l1_log[0] = lm[0];
@@ -431,6 +451,25 @@ int gd_local_gd(const gd_graph *G, const gd_operator *o, const double *b, double
             ++t;
         }
         S.finish(x, r, rep);
+    }
+}
+
+int gd_local_gd(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
+                int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && o && b && x && r && rep, "null pointer");
+        local_gd_run(G, o, b, nullptr, false, x, r, max_sweeps, record_trace, rep);
+    });
+}
+
+int gd_local_gd_warm(const gd_graph *G, const gd_operator *o, double *x, double *r,
+                     int32_t is_signed, int64_t max_sweeps, int32_t record_trace,
+                     gd_report *rep) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && o && x && r && rep, "null pointer");
+        std::vector<double> r0(r, r + G->n), x0(x, x + G->n);
+        local_gd_run(G, o, r0.data(), x0.data(), is_signed != 0, x, r, max_sweeps, record_trace,
+                     rep);
     });
 }
 
@@ -442,10 +481,10 @@ int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double
         GD_CUDA(cudaSetDevice(G->device));
         int64_t cap = 64, tcap = 0;
         report_alloc(rep, cap);
-        SweepSolver S(G, o, true);
+        SweepSolver &S = solver_for(G, o, true);
         size_t nn = S.n ? S.n : 1;
-        S.mom.alloc(nn);
-        S.mstamp.alloc(nn);
+        S.mom.ensure(nn);
+        S.mstamp.ensure(nn);
         GD_CUDA(cudaMemset(S.mom.p, 0, sizeof(double) * nn));
         GD_CUDA(cudaMemset(S.mstamp.p, 0xFE, sizeof(int32_t) * nn));  // never t-1 >= -1
         int64_t f = S.init(b);

@@ -11,6 +11,8 @@
 // the sweep boundaries and all logs) identical to the reference.  At each
 // sentinel the whole CTA rescans the residual for the l1/min logs, as the
 // reference does (:127-132).
+#include <memory>
+
 #include "common.cuh"
 
 namespace gd {
@@ -255,17 +257,32 @@ __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
     }
 }
 
+// Device buffers of a FIFO solve, kept across calls on the host thread.
+struct FifoWS {
+    DBuf<double> x, r, gam, l1, mn;
+    DBuf<int32_t> queue, sd;
+    DBuf<uint8_t> qmark;
+    DBuf<int64_t> vol, out;
+    DBuf<int8_t> sgn;
+};
+
 void run_fifo(const gd_graph *G, FifoArgs A, bool hk, double *hx, double *hr,
               const int64_t *seeds, int64_t n_seeds, gd_report *rep) {
     const int64_t dim = A.dim;
     GD_CHECK_ARG(dim + 2 < (1LL << 31), "coordinate count must be < 2^31");
-    DBuf<double> x(dim ? dim : 1), r(dim ? dim : 1);
-    DBuf<int32_t> queue(dim + 2), sd(n_seeds ? n_seeds : 1);
-    DBuf<uint8_t> qmark(dim ? dim : 1);
+    thread_local std::unique_ptr<FifoWS> ws;
+    if (!ws) ws.reset(new FifoWS());
+    FifoWS &W = *ws;
     int64_t log_cap = A.max_sweeps < (1 << 20) ? A.max_sweeps + 1 : (1 << 20);
-    DBuf<int64_t> vol(log_cap), out(4);
-    DBuf<double> gam(log_cap), l1(log_cap + 1), mn(1);
-    DBuf<int8_t> sgn(log_cap);
+    W.x.ensure(dim ? dim : 1); W.r.ensure(dim ? dim : 1); W.queue.ensure(dim + 2);
+    W.sd.ensure(n_seeds ? n_seeds : 1); W.qmark.ensure(dim ? dim : 1);
+    W.vol.ensure(log_cap); W.out.ensure(4); W.gam.ensure(log_cap); W.l1.ensure(log_cap + 1);
+    W.mn.ensure(1); W.sgn.ensure(log_cap);
+    auto &x = W.x, &r = W.r, &gam = W.gam, &l1 = W.l1, &mn = W.mn;
+    auto &queue = W.queue, &sd = W.sd;
+    auto &qmark = W.qmark;
+    auto &vol = W.vol, &out = W.out;
+    auto &sgn = W.sgn;
     GD_CUDA(cudaMemcpy(x.p, hx, sizeof(double) * dim, cudaMemcpyHostToDevice));
     GD_CUDA(cudaMemcpy(r.p, hr, sizeof(double) * dim, cudaMemcpyHostToDevice));
     GD_CUDA(cudaMemset(qmark.p, 0, dim ? dim : 1));

@@ -161,3 +161,30 @@ def test_reference_style_system_with_arc_array(gpu, small):
     ref = O.local_gd(ref_sys)
     assert np.array_equal(st.x, ref["x"]) and np.array_equal(st.r, ref["r"])
     assert rep.sweeps == ref["sweeps"] and rep.total_ops == ref["total_ops"]
+
+
+
+def test_warm_gd_repair_matches_oracle(gpu, dyn):
+    """Config 5 form: warm-started signed LocalGD repair after edge events,
+    bit-identical with the oracle restatement; consistency invariant holds."""
+    from oracle import oracle as O
+    from paper_2410_21634_b200.dynamic import event_adjust_many, make_pair, repair_gd
+    from paper_2410_21634_b200.graph import EdgeEvent, apply_events
+    g = golden_graph(dyn, "er120")
+    pair, rep = repair_gd(g, make_pair(g, 0.2, 0.2 * 1e-4, 0))
+    assert rep.converged
+    ev = dyn["events"]
+    for bi in range(int(ev[:, 0].max()) + 1):
+        batch = [EdgeEvent("insert" if k else "delete", int(u), int(v)) for b, k, u, v in ev if b == bi]
+        pair = event_adjust_many(g, pair, batch)
+        g = apply_events(g, batch)
+        p2, r2 = pair.p.copy(), pair.r.copy()
+        w = S.arc_weights_for(g, 0.8, "gen", 0.0)
+        th = S.theta_vector(g, 0.2 * 1e-4)
+        ref = O.local_gd_warm(g.offsets, g.targets, w, th, p2, r2, signed=True)
+        pair, rep = repair_gd(g, pair)
+        assert np.array_equal(pair.p, p2) and np.array_equal(pair.r, r2)
+        assert rep.sweeps == ref["sweeps"] and rep.total_ops == ref["total_ops"]
+        assert np.abs(pair.consistency_residual(g)).max() <= 1e-9
+        fin = np.isfinite(th)
+        assert np.all(np.abs(pair.r[fin]) < th[fin])

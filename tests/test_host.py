@@ -124,3 +124,30 @@ def test_csr_cache_roundtrip(tmp_path, small):
     p = tmp_path / "g.csr"
     G.save_csr_cache(g, p)
     assert _same(G.load_csr_cache(p), g)
+
+
+def test_bulk_events_equal_sequential(small):
+    """event_adjust_many / vectorised apply_events == the per-event reference path."""
+    from paper_2410_21634_b200.dynamic import event_adjust_many, make_pair
+    g = golden_graph(small, "er500")
+    rng = np.random.default_rng(4)
+    pair = make_pair(g, 0.2, 1e-4, 0)
+    pair.p[:] = rng.random(g.n)
+    pair.r[:] = rng.random(g.n) - 0.5
+    sim, evs = g, []
+    for _ in range(400):  # includes repeated edits of the same edge
+        u, v = sorted(rng.choice(60, 2, replace=False).tolist())
+        e = EdgeEvent("delete" if sim.has_edge(u, v) else "insert", u, v)
+        evs.append(e)
+        sim = G.apply_event(sim, e)
+    seq = pair
+    gg = g
+    for e in evs:
+        seq = event_adjust(gg, seq, e)
+        gg = G.apply_event(gg, e)
+    bulk = event_adjust_many(g, pair, evs)
+    assert np.array_equal(bulk.p, seq.p) and np.array_equal(bulk.r, seq.r)
+    assert _same(G.apply_events(g, evs), gg)
+    with pytest.raises(G.GraphStructureError):
+        G.apply_events(g, evs + [EdgeEvent("insert", evs[-1].u, evs[-1].v)] * 70
+                       if evs[-1].kind == "insert" else evs + [EdgeEvent("delete", evs[-1].u, evs[-1].v)] * 70)

@@ -94,3 +94,17 @@ def test_oracle_zero_source_and_max_sweeps(small):
     assert out["sweeps"] == 0 and out["total_ops"] == 0 and out["converged"]
     out = O.local_sor(S.make_ppr_system(g, 0.1, 0, 1e-9), 1.0, max_sweeps=2)
     assert not out["converged"] and out["sweeps"] == 2
+
+
+def test_warm_gd_restatement_is_the_reference_sweep_loop(small):
+    """Cold start (x=0, r=b, unsigned) of the warm LocalGD restatement is the
+    reference local_gd bit for bit, so the warm form composes only reference
+    kernels."""
+    g = golden_graph(small, "er500")
+    sys_ = S.make_ppr_system(g, 0.15, 0, 1e-6)
+    k = "er500/ppr/local_gd"
+    x, r = np.zeros(g.n), sys_.b.copy()
+    out = O.local_gd_warm(g.offsets, g.targets, sys_.op.arc_weights, sys_.theta, x, r, signed=False)
+    assert np.array_equal(x, small[f"{k}/x"]) and np.array_equal(r, small[f"{k}/r"])
+    assert out["sweeps"] == small[f"{k}/sweeps"]
+    assert np.array_equal(np.concatenate(out["frontier_trace"]), small[f"{k}/trace_flat"])
