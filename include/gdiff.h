@@ -191,6 +191,12 @@ int gd_batch_solve_host(gd_batch *b, const int64_t *seeds, int64_t n_seeds,
                         int32_t *converged, int64_t *x_offset, int64_t *x_count,
                         int32_t *x_nodes, double *x_vals, int64_t x_cap, int64_t *x_total,
                         void *stream);
+/* Copy the results of the last solve into host buffers again (e.g. after
+ * GD_ERR_CAPACITY from gd_batch_solve_host) without re-solving. */
+int gd_batch_fetch_host(gd_batch *b, int64_t n_seeds, int64_t *sweeps, int64_t *total_ops,
+                        int64_t *pushes, int32_t *converged, int64_t *x_offset, int64_t *x_count,
+                        int32_t *x_nodes, double *x_vals, int64_t x_cap, int64_t *x_total,
+                        void *stream);
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);

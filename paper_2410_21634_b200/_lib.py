@@ -93,6 +93,8 @@ SIGNATURES = {
                                         C.c_void_p]),
     "gd_batch_solve_host": (C.c_int, [C.c_void_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i32p,
                                       _i64p, _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
+    "gd_batch_fetch_host": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _i64p, _i32p, _i64p,
+                                      _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
     "gd_batch_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
     "gd_batch_round_log": (C.c_int, [C.c_void_p, _i64p, C.c_int64, _i64p]),
     "gd_rmat_keys_device": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,

@@ -90,6 +90,7 @@ class BatchSolver:
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
+        self._last_total = 0
 
     def close(self):
         if self.handle and self.handle.value:
@@ -155,30 +156,38 @@ class BatchSolver:
             for name, dt in (("sweeps", np.int64), ("total_ops", np.int64), ("pushes", np.int64),
                              ("converged", np.int32), ("x_offset", np.int64), ("x_count", np.int64)):
                 out[name] = _host_array(k, dt, pinned)
-        cap = x_cap if x_cap is not None else (out["x_nodes"].shape[0] if "x_nodes" in out else 1 << 20)
+        cap = x_cap if x_cap is not None else max(out["x_nodes"].shape[0] if "x_nodes" in out else 0,
+                                                  int(1.25 * self._last_total) + 1024)
         st = 0
         if stream is not None:
             st = stream.cuda_stream
-        for _ in range(3):
-            if "x_nodes" not in out or out["x_nodes"].shape[0] < cap:
-                out["x_nodes"] = _host_array(cap, np.int32, pinned)
-                out["x_vals"] = _host_array(cap, np.float64, pinned)
-            tot = C.c_int64()
-            rc = self.lib.gd_batch_solve_host(
-                self.handle, gdl.ptr(sd, C.c_int64), k, gdl.ptr(out["sweeps"], C.c_int64),
-                gdl.ptr(out["total_ops"], C.c_int64), gdl.ptr(out["pushes"], C.c_int64),
-                gdl.ptr(out["converged"], C.c_int32), gdl.ptr(out["x_offset"], C.c_int64),
-                gdl.ptr(out["x_count"], C.c_int64), gdl.ptr(out["x_nodes"], C.c_int32),
-                gdl.ptr(out["x_vals"]), int(out["x_nodes"].shape[0]), C.byref(tot), C.c_void_p(st))
-            if rc == gdl.GD_ERR_CAPACITY and tot.value > out["x_nodes"].shape[0]:
-                cap = int(tot.value * 1.25) + 1024
-                continue
-            gdl.check(rc)
-            t = int(tot.value)
-            return BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
-                               out["converged"][:k].astype(bool), out["x_offset"][:k],
-                               out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
-        raise gdl.GdiffError(gdl.GD_ERR_CAPACITY, "output sizing failed")
+
+        def bufs():
+            return (gdl.ptr(out["sweeps"], C.c_int64), gdl.ptr(out["total_ops"], C.c_int64),
+                    gdl.ptr(out["pushes"], C.c_int64), gdl.ptr(out["converged"], C.c_int32),
+                    gdl.ptr(out["x_offset"], C.c_int64), gdl.ptr(out["x_count"], C.c_int64),
+                    gdl.ptr(out["x_nodes"], C.c_int32), gdl.ptr(out["x_vals"]),
+                    int(out["x_nodes"].shape[0]))
+
+        if "x_nodes" not in out or out["x_nodes"].shape[0] < cap:
+            out["x_nodes"] = _host_array(cap, np.int32, pinned)
+            out["x_vals"] = _host_array(cap, np.float64, pinned)
+        tot = C.c_int64()
+        rc = self.lib.gd_batch_solve_host(self.handle, gdl.ptr(sd, C.c_int64), k, *bufs(),
+                                          C.byref(tot), C.c_void_p(st))
+        if rc == gdl.GD_ERR_CAPACITY and tot.value > out["x_nodes"].shape[0]:
+            # results are still on the device: grow the host buffers, fetch again
+            cap = int(tot.value * 1.25) + 1024
+            out["x_nodes"] = _host_array(cap, np.int32, pinned)
+            out["x_vals"] = _host_array(cap, np.float64, pinned)
+            rc = self.lib.gd_batch_fetch_host(self.handle, k, *bufs(), C.byref(tot), C.c_void_p(st))
+        gdl.check(rc)
+        t = int(tot.value)
+        self._last_total = t
+        return BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
+                           out["converged"][:k].astype(bool), out["x_offset"][:k],
+                           out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
+
 
 
 def _check_seeds(g, seeds) -> np.ndarray:

@@ -610,6 +610,8 @@ struct gd_batch {
     std::vector<cudaEvent_t> ev;
     double last_ms = 0.0;
     int64_t last_launches = 0;
+    int64_t last_x_total = 0;
+    DBuf<int64_t> dseeds;  // host-entry staging of the seed list
 
     const gd_graph *work() const { return R ? R : G; }
 
@@ -808,7 +810,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             int64_t fc = p->frontier_cap > 0 ? p->frontier_cap : (int64_t)slots * n;
             if (p->frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
             B->fcap = fc;
-            B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
+            B->xcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
             const size_t sn = (size_t)slots * (size_t)ld;
             B->x.alloc(sn); B->r.alloc(sn);
             GD_CUDA(cudaMemset(B->x.p, 0, sizeof(double) * sn));
@@ -864,9 +866,11 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
                 throw Error{GD_ERR_CAPACITY};
             }
             res->x_total = (int64_t)used;
+            B->last_x_total = (int64_t)used;
             if ((int64_t)used <= B->xcap) break;
             GD_CHECK_ARG(attempt == 0, "output pool sizing failed");
-            B->xcap = (int64_t)used + (int64_t)used / 8 + 1024;  // grow and redo
+            // grow (doubling, so a growing workload redoes at most log times) and redo
+            B->xcap = 2 * ((int64_t)used > B->xcap ? (int64_t)used : B->xcap);
             B->xnodes.alloc(B->xcap);
             B->xvals.alloc(B->xcap);
         }
@@ -874,6 +878,39 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
         res->support = B->support.p; res->converged = B->conv.p; res->x_offset = B->xoff.p;
         res->x_count = B->xcnt.p; res->x_nodes = B->xnodes.p; res->x_vals = B->xvals.p;
         res->kernel_launches = B->last_launches;
+    });
+}
+
+// Copy the results of the last solve (still on the device) into host
+// buffers; GD_ERR_CAPACITY with *x_total set when x_cap is too small, in
+// which case the caller can grow its buffers and fetch again (no re-solve).
+int gd_batch_fetch_host(gd_batch *B, int64_t n_seeds, int64_t *sweeps, int64_t *total_ops,
+                        int64_t *pushes, int32_t *converged, int64_t *x_offset, int64_t *x_count,
+                        int32_t *x_nodes, double *x_vals, int64_t x_cap, int64_t *x_total,
+                        void *stream) {
+    return guarded([&] {
+        GD_CHECK_ARG(B && x_total, "null pointer");
+        GD_CUDA(cudaSetDevice(B->G->device));
+        cudaStream_t st = (cudaStream_t)stream;
+        *x_total = B->last_x_total;
+        auto d2h = [&](void *dst, const void *src, size_t bytes) {
+            if (dst && bytes) GD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        d2h(sweeps, B->sweeps.p, sizeof(int64_t) * n_seeds);
+        d2h(total_ops, B->ops.p, sizeof(int64_t) * n_seeds);
+        d2h(pushes, B->pushes.p, sizeof(int64_t) * n_seeds);
+        d2h(converged, B->conv.p, sizeof(int32_t) * n_seeds);
+        d2h(x_offset, B->xoff.p, sizeof(int64_t) * n_seeds);
+        d2h(x_count, B->xcnt.p, sizeof(int64_t) * n_seeds);
+        if (B->last_x_total > x_cap) {
+            GD_CUDA(cudaStreamSynchronize(st));
+            set_error("x buffers hold %lld pairs, %lld needed", (long long)x_cap,
+                      (long long)B->last_x_total);
+            throw Error{GD_ERR_CAPACITY};
+        }
+        d2h(x_nodes, B->xnodes.p, sizeof(int32_t) * B->last_x_total);
+        d2h(x_vals, B->xvals.p, sizeof(double) * B->last_x_total);
+        GD_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -885,30 +922,15 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
         GD_CHECK_ARG(B && (seeds || n_seeds == 0) && x_total, "null pointer");
         GD_CUDA(cudaSetDevice(B->G->device));
         cudaStream_t st = (cudaStream_t)stream;
-        DBuf<int64_t> ds(n_seeds ? n_seeds : 1);
-        GD_CUDA(cudaMemcpyAsync(ds.p, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice, st));
+        B->dseeds.ensure(n_seeds ? n_seeds : 1);
+        GD_CUDA(cudaMemcpyAsync(B->dseeds.p, seeds, sizeof(int64_t) * n_seeds,
+                                cudaMemcpyHostToDevice, st));
         gd_batch_result res{};
-        int rc = gd_batch_solve_device(B, ds.p, n_seeds, &res, stream);
+        int rc = gd_batch_solve_device(B, B->dseeds.p, n_seeds, &res, stream);
         if (rc != GD_OK) throw Error{rc};
-        *x_total = res.x_total;
-        auto d2h = [&](void *dst, const void *src, size_t bytes) {
-            if (dst && bytes) GD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-        };
-        d2h(sweeps, res.sweeps, sizeof(int64_t) * n_seeds);
-        d2h(total_ops, res.total_ops, sizeof(int64_t) * n_seeds);
-        d2h(pushes, res.pushes, sizeof(int64_t) * n_seeds);
-        d2h(converged, res.converged, sizeof(int32_t) * n_seeds);
-        d2h(x_offset, res.x_offset, sizeof(int64_t) * n_seeds);
-        d2h(x_count, res.x_count, sizeof(int64_t) * n_seeds);
-        if (res.x_total > x_cap) {
-            GD_CUDA(cudaStreamSynchronize(st));
-            set_error("x buffers hold %lld pairs, %lld needed", (long long)x_cap,
-                      (long long)res.x_total);
-            throw Error{GD_ERR_CAPACITY};
-        }
-        d2h(x_nodes, res.x_nodes, sizeof(int32_t) * res.x_total);
-        d2h(x_vals, res.x_vals, sizeof(double) * res.x_total);
-        GD_CUDA(cudaStreamSynchronize(st));
+        rc = gd_batch_fetch_host(B, n_seeds, sweeps, total_ops, pushes, converged, x_offset,
+                                 x_count, x_nodes, x_vals, x_cap, x_total, stream);
+        if (rc != GD_OK) throw Error{rc};
     });
 }
 
