@@ -66,7 +66,7 @@ struct RoundArgs {
     double beta;    // 1 - alpha
     double tcoeff;  // eps * alpha
     int64_t n;
-    int64_t ld;     // slot stride (n rounded up to even: 16 B aligned slots)
+    int64_t ld;     // slot stride (n rounded up to 4: 32 B aligned slots)
     int64_t max_sweeps;
     int64_t fcap;
     int64_t m;      // slots in use this wave
@@ -87,6 +87,8 @@ struct RoundArgs {
     const int32_t *perm;  // caller id -> working id (nullable)
     unsigned long long *cursor;  // output pool allocation
     int64_t *slot_base;
+    uint32_t *secmap;   // per slot: bit per 32 B sector of r ever written (reset map)
+    int64_t smw;        // words per slot in secmap
     int64_t *rlog;      // per round: F, P, globaltimer ns (3 entries), debug
     int64_t rlog_cap;   // rounds recorded
 };
@@ -430,6 +432,8 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
                 const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
                 block_count(first, k[q], 1u, S.touch);
+                if (first)  // first write of this r word: remember its 32 B sector
+                    atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                 block_count(negz, k[q], 1u, S.negz);
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
@@ -455,6 +459,7 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.seed[k] = s;
     A.r[k * A.ld + s] = alpha;
     A.touched[k] = 1;
+    A.secmap[k * A.smw + (s >> 7)] |= 1u << ((s >> 2) & 31);
     A.pushed_cnt[k] = 0;
     A.s_ops[k] = 0;
     A.s_pushes[k] = 0;
@@ -497,7 +502,6 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
         const int32_t u = A.pushed[off + i];
         const double xv = A.x[off + u];
         A.x[off + u] = 0.0;
-        A.r[off + u] = 0.0;
         if (b + i < O.xcap) {
             O.xnodes[b + i] = O.inv ? O.inv[u] : u;
             O.xvals[b + i] = xv;
@@ -517,28 +521,31 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
     }
 }
 
-// grid (CHUNKS, slots): return r to +0.0.  Touched nodes are exactly the
-// rows of the pushed nodes, so either walk those rows (cost vol(pushed)
-// random 8 B writes) or, when that volume is a large fraction of n, stream
-// zeros over the whole slot (write-only, coalesced 16 B stores).
+// grid (CHUNKS, slots): return r of every slot to +0.0.
 __global__ void k_wave_reset(RoundArgs A) {
+    // zero exactly the 32 B sectors of r this slot ever wrote (sector map
+    // set on first touch), then clear the map: ~touched sectors of traffic
+    // instead of a zero stream over the whole slot
     const int k = blockIdx.y;
     const int64_t off = (int64_t)k * A.ld;
-    if ((int64_t)A.s_pvol[k] * 4 > A.ld) {
-        double2 *r2 = reinterpret_cast<double2 *>(A.r + off);
-        const int64_t h = A.ld >> 1;
-        const int64_t per = (h + CHUNKS - 1) / CHUNKS;
-        const int64_t lo = blockIdx.x * per, hi = min(h, lo + per);
-        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) r2[i] = make_double2(0.0, 0.0);
-        return;
-    }
-    const int lane = threadIdx.x & 31;
-    const int64_t pc = (int64_t)A.pushed_cnt[k];
-    const int64_t wpb = blockDim.x >> 5;
-    for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < pc; i += (int64_t)CHUNKS * wpb) {
-        const int32_t u = A.pushed[off + i];
-        const int64_t rs = A.g.row[u], d = A.g.row[u + 1] - rs;
-        for (int64_t j = lane; j < d; j += 32) A.r[off + A.g.col[rs + j]] = 0.0;
+    uint32_t *map = A.secmap + (int64_t)k * A.smw;
+    const int64_t per = (A.smw + CHUNKS - 1) / CHUNKS;
+    const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
+    double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
+    for (int64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint32_t bits = map[w];
+        if (!bits) continue;
+        map[w] = 0u;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t sec = w * 32 + b;  // sector index: doubles [4 sec, 4 sec + 4)
+            if (4 * sec + 3 < A.ld) {
+                r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+            } else {
+                for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
+            }
+        }
     }
 }
 
@@ -603,6 +610,8 @@ struct gd_batch {
     int64_t ccap = 0;
     DBuf<int64_t> rlog;
     static constexpr int64_t RLOG_CAP = 4096;
+    DBuf<uint32_t> secmap;
+    int64_t smw = 0;
     // results
     DBuf<int64_t> sweeps, ops, pushes, support, xoff, xcnt;
     DBuf<int32_t> conv, xnodes;
@@ -621,7 +630,7 @@ struct gd_batch {
         A.beta = 1.0 - p.alpha;
         A.tcoeff = p.eps * p.alpha;
         A.n = G->n;
-        A.ld = (G->n + 1) & ~1LL;
+        A.ld = (G->n + 3) & ~3LL;
         A.max_sweeps = p.max_sweeps;
         A.fcap = fcap;
         A.x = x.p; A.r = r.p; A.pushed = pushed.p; A.seed = seed.p;
@@ -631,6 +640,7 @@ struct gd_batch {
         A.chunk_e = chunk_e.p; A.ccap = ccap;
         A.colp = colp.p;
         A.rlog = rlog.p; A.rlog_cap = RLOG_CAP;
+        A.secmap = secmap.p; A.smw = smw;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p;
         A.overflow = overflow.p;
@@ -775,7 +785,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
         GD_CHECK_ARG(G->n_arcs < (1LL << CNT_SHIFT), "too many arcs");
         GD_CUDA(cudaSetDevice(G->device));
         const int64_t n = G->n ? G->n : 1;
-        const int64_t ld = (n + 1) & ~1LL;
+        const int64_t ld = (n + 3) & ~3LL;
         gd_batch *B = new gd_batch();
         try {
             B->G = G;
@@ -826,6 +836,9 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
             B->chunk_e.alloc(B->ccap);
             B->rlog.alloc(3 * gd_batch::RLOG_CAP + 1);
+            B->smw = (ld / 4 + 31) / 32;  // one bit per 4 doubles (32 B sector)
+            B->secmap.alloc((size_t)slots * (size_t)B->smw);
+            GD_CUDA(cudaMemset(B->secmap.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
             const size_t smem = stage_bytes(slots);
             GD_CUDA(cudaFuncSetAttribute(k_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
