@@ -133,10 +133,11 @@ def dist_env():
 def make_graph(shape, seed, device):
     """GPU-built R-MAT graph: (DeviceGraph, host CsrGraph-like with degrees)."""
     from paper_2410_21634_b200.device import DeviceGraph
-    from paper_2410_21634_b200.gen import rmat_csr_device
+    from paper_2410_21634_b200.gen import rmat_csr_device, rmat_csr_device_big
 
     n, m = SHAPES[shape]
-    row, col = rmat_csr_device(n, m, seed=seed, device=device)
+    big = 2 * m > (1 << 30)  # beyond a single device sort
+    row, col = (rmat_csr_device_big if big else rmat_csr_device)(n, m, seed=seed, device=device)
     dg = DeviceGraph.from_device(n, row, col, device=device)
     row_h = row.cpu().numpy()
     return dg, row, col, row_h
@@ -252,6 +253,10 @@ def main():
     n, m = SHAPES[args.shape]
     dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
     hdeg = _HostGraph(n, row_h)
+    if args.no_cpu_baseline:  # the CPU leg is the only later user of the torch copies
+        del row, col
+        col = None
+        torch.cuda.empty_cache()
     steps_total = args.warmup + args.steps
     allseeds = sample_sources(hdeg, args.seeds * world * steps_total, seed=0)
     from paper_2410_21634_b200.shard import STAT_FIELDS, gather_results, shard_seeds

@@ -721,6 +721,12 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->last_launches = launches;
 }
 
+struct RebaseOp {
+    int64_t base;
+    __host__ __device__ int64_t operator()(int64_t v) const { return v - base; }
+};
+using RebaseIt = cub::TransformInputIterator<int64_t, RebaseOp, const int64_t *>;
+
 // Degree-descending renumbering with sorted rows, on the device (setup).
 static void build_relabeled(gd_batch *B) {
     const gd_graph *G = B->G;
@@ -761,13 +767,34 @@ static void build_relabeled(gd_batch *B) {
     k_remap_rows<<<blocks, 256>>>(g, B->inv.p, B->perm.p, R->row.p, unsorted.p);
     GD_LAUNCH_CHECK();
     // sort every row by new id: a warp's 32 consecutive arcs then target
-    // nearby residual words (hubs are contiguous), so its atomics share sectors
-    bytes = 0;
-    cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, unsorted.p, R->col.p, G->n_arcs, n,
-                                       R->row.p, R->row.p + 1);
-    tmp.ensure(bytes ? bytes : 1);
-    cub::DeviceSegmentedSort::SortKeys(tmp.p, bytes, unsorted.p, R->col.p, G->n_arcs, n,
-                                       R->row.p, R->row.p + 1);
+    // nearby residual words (hubs are contiguous), so its atomics share
+    // sectors.  CUB's segmented sort counts items in int: sort groups of
+    // whole rows holding <= 2^30 arcs each, offsets rebased per group.
+    std::vector<int64_t> hrow(n + 1);
+    GD_CUDA(cudaMemcpy(hrow.data(), R->row.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    const int64_t LIMIT = 1LL << 30;
+    for (int64_t r0 = 0; r0 < n;) {
+        int64_t r1 = r0 + 1;
+        {  // largest r1 with arcs(r0, r1) <= LIMIT (at least one row)
+            int64_t lo = r0 + 1, hi = n;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) / 2;
+                if (hrow[mid] - hrow[r0] <= LIMIT) lo = mid; else hi = mid - 1;
+            }
+            r1 = lo;
+        }
+        const int64_t base = hrow[r0], items = hrow[r1] - base;
+        if (items > 0) {
+            RebaseIt begin(R->row.p + r0, RebaseOp{base}), end(R->row.p + r0 + 1, RebaseOp{base});
+            bytes = 0;
+            cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, unsorted.p + base, R->col.p + base,
+                                               (int)items, (int)(r1 - r0), begin, end);
+            tmp.ensure(bytes ? bytes : 1);
+            cub::DeviceSegmentedSort::SortKeys(tmp.p, bytes, unsorted.p + base, R->col.p + base,
+                                               (int)items, (int)(r1 - r0), begin, end);
+        }
+        r0 = r1;
+    }
     GD_CUDA(cudaDeviceSynchronize());
 }
 
@@ -806,6 +833,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             k_pack_cols<<<4 * n_sms(G->device), 256>>>(B->work()->view(), B->colp.p);
             GD_LAUNCH_CHECK();
             GD_CUDA(cudaDeviceSynchronize());
+            if (B->R) B->R->col.release();  // the batch reads (neighbour, degree) pairs only
             int slots = p->slots;
             if (slots <= 0) {
                 size_t fr = 0, tot = 0;

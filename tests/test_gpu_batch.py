@@ -95,12 +95,13 @@ def test_edge_cases(gpu):
 
 
 def test_device_generator_equals_host(gpu):
-    from paper_2410_21634_b200.gen import rmat_csr_device
+    from paper_2410_21634_b200.gen import rmat_csr_device, rmat_csr_device_big
     for n, m, seed in ((2708, 5278, 0), (20000, 150000, 5)):
-        row, col = rmat_csr_device(n, m, seed=seed)
         h = rmat_graph(n, m, seed=seed)
-        assert np.array_equal(row.cpu().numpy(), h.offsets)
-        assert np.array_equal(col.cpu().numpy().astype(np.int64), h.targets)
+        for fn, kw in ((rmat_csr_device, {}), (rmat_csr_device_big, {"buckets": 7, "chunk": 50000})):
+            row, col = fn(n, m, seed=seed, **kw)
+            assert np.array_equal(row.cpu().numpy(), h.offsets), fn.__name__
+            assert np.array_equal(col.cpu().numpy().astype(np.int64), h.targets), fn.__name__
 
 
 # ---- batched FIFO (LocalSOR / LocalGS): bit-identical per seed ------------
