@@ -137,6 +137,12 @@ int gd_hk_push(const gd_graph *g, int64_t n_stages, const double *stage_w,
 int gd_gradient_descent(const gd_graph *g, const gd_operator *op, const double *b,
                         double *x, double *r, int64_t max_sweeps, gd_report *rep);
 
+/* Spectral norm estimate of A (Katz alpha / Chebyshev bounds): replaces
+ * spectral_norm_estimate (src/graph.py:267-295), the shifted power iteration
+ * on A + d_max I from the caller's start vector x0 (n entries); agrees with
+ * the reference to rounding (its dot products go through BLAS). */
+int gd_spectral_norm(const gd_graph *g, const double *x0, int64_t iters, double *lam_out);
+
 /* ---- batched multi-seed solves (new; no reference counterpart) --------- */
 /* A batch solves PPR systems (I - (1-alpha) A D^-1) x = alpha e_s for many
  * seeds s; the per-seed result equals local_gd(make_ppr_system(g, alpha, s,

@@ -188,3 +188,13 @@ def test_warm_gd_repair_matches_oracle(gpu, dyn):
         assert np.abs(pair.consistency_residual(g)).max() <= 1e-9
         fin = np.isfinite(th)
         assert np.all(np.abs(pair.r[fin]) < th[fin])
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_spectral_norm_gpu(gpu, seed):
+    from paper_2410_21634_b200.graph import spectral_norm_estimate
+    from paper_2410_21634_b200.synth import rmat_graph
+    g = rmat_graph(20000, 150000, seed=seed)
+    host = spectral_norm_estimate(g, iters=200, seed=0, device=False)
+    dev = spectral_norm_estimate(g, iters=200, seed=0, device=True)
+    assert abs(dev - host) <= 1e-9 * abs(host)
