@@ -109,38 +109,56 @@ __global__ void k_gather_ch(const int32_t *__restrict__ F, int64_t f, double *__
 // ---- expand: arc position p -> (target key, p)
 __global__ void k_expand(const int32_t *__restrict__ F, const int64_t *__restrict__ arcoff,
                          int64_t f, int64_t P, DevGraph g, uint32_t *__restrict__ keys,
-                         uint32_t *__restrict__ pidx) {
+                         uint32_t *__restrict__ pidx, int32_t *__restrict__ arc_i) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         int64_t i = bsearch_le(arcoff, f, p);
         int32_t u = F[i];
         keys[p] = (uint32_t)g.col[g.row[u] + (p - arcoff[i])];
         pidx[p] = (uint32_t)p;
+        arc_i[p] = (int32_t)i;
     }
 }
 
-// ---- ordered fold, one thread per target segment (second loop of
-// _apply_update_seq, :282-291)
-__global__ void k_fold(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ sp,
-                       int64_t P, const int64_t *__restrict__ arcoff, int64_t f,
+// ---- ordered fold, one warp per target segment (second loop of
+// _apply_update_seq, :282-291).  Segments come from a run-length encode of
+// the sorted targets.  Lanes form the products c = fl(vals_i * w_j) of 32
+// consecutive contributions in parallel; lane 0 then adds them in order
+// (shuffles), so r[v] = fl(...fl(fl(r[v] + c_1) + c_2)...) exactly.
+__global__ void k_fold(const uint32_t *__restrict__ ukeys, const int64_t *__restrict__ segoff,
+                       const int64_t *__restrict__ nseg_p, const uint32_t *__restrict__ sp,
+                       const int32_t *__restrict__ arc_i, const int64_t *__restrict__ arcoff,
                        const int32_t *__restrict__ F, const double *__restrict__ vals,
                        const double *__restrict__ wnode, DevGraph g, DevOp op,
                        double *__restrict__ r, const int32_t *__restrict__ fstamp, int32_t t,
                        uint8_t *__restrict__ head) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t v = skeys[q];
-        if (q > 0 && skeys[q - 1] == v) continue;
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = *nseg_p;
+    for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
+         sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t v = ukeys[sgi];
+        const int64_t q0 = segoff[sgi], q1 = segoff[sgi + 1];
         double acc = r[v];
-        for (int64_t q2 = q; q2 < P && skeys[q2] == v; ++q2) {
-            int64_t p = sp[q2];
-            int64_t i = bsearch_le(arcoff, f, p);
-            double w = wnode[i];
-            if (op.wrule == GD_W_ARC) w = op.arc_w[g.row[F[i]] + (p - arcoff[i])];
-            acc = __dadd_rn(acc, __dmul_rn(vals[i], w));
+        for (int64_t b = q0; b < q1; b += 32) {
+            const int64_t q = b + lane;
+            double c = 0.0;
+            if (q < q1) {
+                const int64_t p = sp[q];
+                const int32_t i = arc_i[p];
+                double w = wnode[i];
+                if (op.wrule == GD_W_ARC) w = op.arc_w[g.row[F[i]] + (p - arcoff[i])];
+                c = __dmul_rn(vals[i], w);
+            }
+            const int cnt = (int)min((int64_t)32, q1 - b);
+            for (int l = 0; l < cnt; l++) {
+                const double cl = __shfl_sync(0xffffffffu, c, l);
+                acc = __dadd_rn(acc, cl);
+            }
         }
-        r[v] = acc;
-        if (fstamp[v] != t) head[sp[q]] = 1;  // first touch of a node outside S_t
+        if (lane == 0) {
+            r[v] = acc;
+            if (fstamp[v] != t) head[sp[q0]] = 1;  // first touch of a node outside S_t
+        }
     }
 }
 
@@ -259,7 +277,9 @@ struct SweepSolver {
     DBuf<double> x, r, vals, absv, wnode, mom, red_ps, red_pm, scal;
     DBuf<int32_t> F, Fn, fstamp, mstamp, seeds;
     DBuf<int64_t> fdeg, arcoff, trace64, cnt;
-    DBuf<uint32_t> keys, skeys, pidx, sp;
+    DBuf<uint32_t> keys, skeys, pidx, sp, ukeys;
+    DBuf<int32_t> arc_i;
+    DBuf<int64_t> segcnt, segoff, nseg;
     DBuf<uint8_t> head, flag;
     DBuf<char> tmp;
     int bits = 1;
@@ -336,11 +356,12 @@ struct SweepSolver {
         GD_CHECK_ARG(P < (1LL << 32), "frontier volume exceeds 2^32 arcs");
         *P_out = P;
         if (P > 0) {
-            keys.ensure(P); skeys.ensure(P); pidx.ensure(P); sp.ensure(P);
+            keys.ensure(P); skeys.ensure(P); pidx.ensure(P); sp.ensure(P); arc_i.ensure(P);
+            ukeys.ensure(P); segcnt.ensure(P + 1); segoff.ensure(P + 1); nseg.ensure(1);
             head.ensure(P);
             if (flag.n < (size_t)P) flag.alloc(P);
             GD_CUDA(cudaMemsetAsync(head.p, 0, P, s));
-            k_expand<<<blocks_for(P), TPB, 0, s>>>(F.p, arcoff.p, f, P, g, keys.p, pidx.p);
+            k_expand<<<blocks_for(P), TPB, 0, s>>>(F.p, arcoff.p, f, P, g, keys.p, pidx.p, arc_i.p);
             GD_LAUNCH_CHECK();
             bytes = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, skeys.p, pidx.p, sp.p,
@@ -348,8 +369,22 @@ struct SweepSolver {
             tmp_need(bytes);
             cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, skeys.p, pidx.p, sp.p,
                                             (int64_t)P, 0, bits, s);
-            k_fold<<<blocks_for(P), TPB, 0, s>>>(skeys.p, sp.p, P, arcoff.p, f, F.p, vals.p,
-                                                 wnode.p, g, op.dev, r.p, fstamp.p, t, head.p);
+            // target segments: (unique target, run length) -> offsets
+            bytes = 0;
+            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, skeys.p, ukeys.p, segcnt.p, nseg.p,
+                                               (int64_t)P, s);
+            tmp_need(bytes);
+            cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, skeys.p, ukeys.p, segcnt.p, nseg.p,
+                                               (int64_t)P, s);
+            bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, segcnt.p, segoff.p, P + 1, s);
+            tmp_need(bytes);
+            // (only offsets [0, nseg] are read: exact whatever follows the runs)
+            cub::DeviceScan::ExclusiveSum(tmp.p, bytes, segcnt.p, segoff.p, P + 1, s);
+            k_fold<<<blocks_for(32 * P, 1 << 16), TPB, 0, s>>>(ukeys.p, segoff.p, nseg.p, sp.p,
+                                                               arc_i.p, arcoff.p, F.p, vals.p,
+                                                               wnode.p, g, op.dev, r.p, fstamp.p,
+                                                               t, head.p);
             GD_LAUNCH_CHECK();
         }
         // 1) frontier members that stay active, in S_t order
