@@ -152,6 +152,14 @@ int gd_spectral_norm(const gd_graph *g, const double *x0, int64_t iters, double 
  * HBM vectors that are reset by walking what a seed touched. */
 #define GD_M_LOCAL_GD 0  /* sweep-synchronous LocalGD (batch.cu)                 */
 #define GD_M_LOCAL_SOR 1 /* FIFO LocalSOR / LocalGS, one warp per seed, bit-exact */
+#define GD_M_LOCAL_CH 2  /* sweep-synchronous LocalCH, signed frontier
+                            (batch_signed.cu): per seed local_ch(sys, mu, L)
+                            with the same frontier sets, sweeps and operation
+                            counts, x to rounding of the atomic scatter */
+
+#define GD_P_PPR 0  /* (I - (1-alpha) A D^-1) x = alpha e_s, theta = eps alpha d */
+#define GD_P_KATZ 1 /* (I - alpha A) x = e_s, theta = eps d (src/systems.py:194-219);
+                       GD_M_LOCAL_CH only */
 
 typedef struct gd_batch gd_batch;
 
@@ -167,9 +175,12 @@ typedef struct {
                              graph (hubs contiguous: residual updates share
                              sectors / stay in L2); ids in and out are the
                              caller's.  Results are invariant. */
-    int32_t reserved;
+    int32_t problem;      /* GD_P_* (GD_P_KATZ with GD_M_LOCAL_CH only) */
     double omega;         /* GD_M_LOCAL_SOR: relaxation (1 = LocalGS, signed
                              frontier when > 1, src/local_solvers.py:238) */
+    double mu, L;         /* GD_M_LOCAL_CH: eigenvalue bounds, mu < L (the
+                             reference's cheby_bounds, src/local_solvers.py:541-558;
+                             0, 0 = PPR defaults alpha, 2 - alpha) */
 } gd_batch_params;
 
 typedef struct {
@@ -209,6 +220,36 @@ int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */
 int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *rounds);
+
+/* ---- resident PPR pairs on an evolving graph (config 5, batched) ------- */
+/* K pairs (p_i, r_i) with r_i = alpha e_{s_i} - (I - (1-alpha) A D^-1) p_i
+ * kept in HBM across snapshots.  Replaces, for K sources at once, the
+ * reference's per-source loop of event_adjust + repair (src/dynamic.py:
+ * 110-196): every event batch is applied to every pair in event order (the
+ * O(1) endpoint corrections, bit-exact), then all pairs are repaired on the
+ * new graph by one warm-started signed LocalGD solve (thresholds eps d_u,
+ * src/dynamic.py:139-141).  Per-pair sweeps / total_ops / pushes equal the
+ * single-pair warm LocalGD on the same state; p, r to rounding of the
+ * atomic scatter. */
+typedef struct gd_pairs gd_pairs;
+
+/* Pairs start at (0, alpha e_s) and are solved on g (stats: k entries each,
+ * any may be NULL).  frontier_cap / max_sweeps: 0 = auto. */
+int gd_pairs_create(const gd_graph *g, double alpha, double eps, const int64_t *sources,
+                    int64_t k, int64_t frontier_cap, int64_t max_sweeps, gd_pairs **out,
+                    int64_t *sweeps, int64_t *total_ops, int64_t *pushes, int32_t *converged);
+int gd_pairs_destroy(gd_pairs *p);
+/* g_new must be the previous graph with the events applied (checked on the
+ * degrees); kinds[i] = 1 insert, 0 delete of edge (us[i], vs[i]). */
+int gd_pairs_update(gd_pairs *p, const gd_graph *g_new, const int32_t *kinds, const int64_t *us,
+                    const int64_t *vs, int64_t n_events, int64_t max_sweeps, int64_t *sweeps,
+                    int64_t *total_ops, int64_t *pushes, int32_t *converged);
+/* Dense host copies of pair i (n doubles each; either pointer may be NULL). */
+int gd_pairs_get(const gd_pairs *p, int64_t i, double *p_out, double *r_out);
+/* Device view: pair i's p at p[i*ld .. i*ld+n), r likewise. */
+int gd_pairs_device(const gd_pairs *p, double **p_dev, double **r_dev, int64_t *ld);
+/* Device time (ms) of the last repair's sweep loop (CUDA events). */
+int gd_pairs_last_kernel_ms(const gd_pairs *p, double *ms);
 
 /* ---- synthetic graphs -------------------------------------------------- */
 /* R-MAT candidate edges [first, first+count) at `scale`, ids permuted and

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(HERE, "libgdiff.so")
 GD_OK, GD_ERR_ARG, GD_ERR_CUDA, GD_ERR_OOM, GD_ERR_CAPACITY, GD_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GD_W_RW, GD_W_CONST, GD_W_ARC = 0, 1, 2
 GD_T_DEGREE, GD_T_ARRAY = 0, 1
-GD_M_LOCAL_GD, GD_M_LOCAL_SOR = 0, 1
+GD_M_LOCAL_GD, GD_M_LOCAL_SOR, GD_M_LOCAL_CH = 0, 1, 2
+GD_P_PPR, GD_P_KATZ = 0, 1
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -55,7 +56,8 @@ class BatchParams(C.Structure):
     _fields_ = [("method", C.c_int32), ("slots", C.c_int32), ("alpha", C.c_double),
                 ("eps", C.c_double), ("max_sweeps", C.c_int64),
                 ("frontier_cap", C.c_int64), ("out_cap", C.c_int64),
-                ("relabel", C.c_int32), ("reserved", C.c_int32), ("omega", C.c_double)]
+                ("relabel", C.c_int32), ("problem", C.c_int32), ("omega", C.c_double),
+                ("mu", C.c_double), ("L", C.c_double)]
 
 
 class BatchResult(C.Structure):
@@ -98,6 +100,14 @@ SIGNATURES = {
                                       _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
     "gd_batch_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
     "gd_batch_round_log": (C.c_int, [C.c_void_p, _i64p, C.c_int64, _i64p]),
+    "gd_pairs_create": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, C.c_int64, C.c_int64,
+                                  C.c_int64, C.POINTER(C.c_void_p), _i64p, _i64p, _i64p, _i32p]),
+    "gd_pairs_destroy": (C.c_int, [C.c_void_p]),
+    "gd_pairs_update": (C.c_int, [C.c_void_p, C.c_void_p, _i32p, _i64p, _i64p, C.c_int64, C.c_int64,
+                                  _i64p, _i64p, _i64p, _i32p]),
+    "gd_pairs_get": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p]),
+    "gd_pairs_device": (C.c_int, [C.c_void_p, C.POINTER(_f64p), C.POINTER(_f64p), _i64p]),
+    "gd_pairs_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
     "gd_rmat_keys_device": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p]),
 }

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib as gdl
 from .device import DeviceGraph, device_graph
 
-__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch"]
+__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch", "local_ch_batch"]
 
 
 def _host_array(count: int, dtype, pinned: bool) -> np.ndarray:
@@ -67,26 +67,45 @@ class BatchSolver:
     method "local-gd": sweep-synchronous LocalGD (frontier sets, sweeps and
     operation counts identical to the reference, x to 1e-9);
     method "local-sor": FIFO LocalSOR with relaxation omega (omega = 1:
-    LocalGS), one warp per seed, bit-identical with the reference."""
+    LocalGS), one warp per seed, bit-identical with the reference;
+    method "local-ch": LocalCH (Chebyshev momentum, signed frontier) for
+    problem "ppr" or "katz" ((I - alpha A) x = e_s; needs mu, L), frontier
+    sets, sweeps and operation counts identical to the reference's
+    local_ch(sys, mu, L), x to 1e-9.  ``support`` is not tracked for it."""
 
     def __init__(self, g, alpha: float, eps: float, slots: int = 0,
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
-                 omega: float = 1.0):
-        if not 0.0 < alpha <= 1.0:
-            raise ValueError("alpha must be in (0, 1]")
-        if method not in ("local-gd", "local-sor"):
+                 omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
+                 L: float | None = None):
+        if method not in ("local-gd", "local-sor", "local-ch"):
             raise ValueError(f"unknown batch method {method!r}")
+        if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
+            raise ValueError("problem must be 'ppr', or 'katz' with method 'local-ch'")
+        if problem == "ppr" and not 0.0 < alpha <= 1.0:
+            raise ValueError("alpha must be in (0, 1]")
+        if problem == "katz" and not alpha > 0.0:
+            raise ValueError("alpha must be positive")
         if method == "local-sor" and not 0.0 < omega <= 2.0:
             raise ValueError("omega must be in (0, 2]")
+        if method == "local-ch":
+            if (mu is None) != (L is None):
+                raise ValueError("give both mu and L, or neither")
+            if mu is None and problem == "katz":
+                raise ValueError("Katz batches need mu, L (see local_ch_batch)")
+            if mu is not None and not mu < L:
+                raise ValueError(f"need mu < L, got mu={mu}, L={L}")
         self.method = method
         self.lib = gdl.load()
         self.graph = g if isinstance(g, DeviceGraph) else device_graph(g, device)
         self.alpha, self.eps = float(alpha), float(eps)
-        p = gdl.BatchParams(method=gdl.GD_M_LOCAL_SOR if method == "local-sor" else gdl.GD_M_LOCAL_GD,
-                            slots=int(slots), alpha=self.alpha, eps=self.eps,
+        mcode = {"local-gd": gdl.GD_M_LOCAL_GD, "local-sor": gdl.GD_M_LOCAL_SOR,
+                 "local-ch": gdl.GD_M_LOCAL_CH}[method]
+        p = gdl.BatchParams(method=mcode, slots=int(slots), alpha=self.alpha, eps=self.eps,
                             max_sweeps=int(max_sweeps), frontier_cap=int(frontier_cap),
-                            out_cap=int(out_cap), relabel=int(bool(relabel)), omega=float(omega))
+                            out_cap=int(out_cap), relabel=int(bool(relabel)),
+                            problem=gdl.GD_P_KATZ if problem == "katz" else gdl.GD_P_PPR,
+                            omega=float(omega), mu=float(mu or 0.0), L=float(L or 0.0))
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
@@ -218,6 +237,38 @@ def local_sor_batch(g, seeds, alpha: float, eps: float, omega: float = 1.0, slot
     sd = _check_seeds(g, seeds)
     solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method="local-sor",
                          omega=omega)
+    try:
+        return solver.solve(sd)
+    finally:
+        solver.close()
+
+
+def local_ch_batch(g, seeds, alpha: float, eps: float, problem: str = "ppr",
+                   mu: float | None = None, L: float | None = None,
+                   lam_hat: float | None = None, max_sweeps: int | None = None, slots: int = 0,
+                   relabel: bool = True) -> BatchOutput:
+    """Batched LocalCH over `seeds`: per seed the reference's
+    local_ch(make_ppr_system(g, alpha, s, eps)) or, for problem "katz",
+    local_ch(make_katz_system(g, alpha, s, eps)) with its default bounds
+    (cheby_bounds, src/local_solvers.py:541-558; Katz from lam_hat, the
+    spectral norm estimate, computed on the host when not given)."""
+    import math
+
+    sd = _check_seeds(g, seeds)
+    if mu is None or L is None:
+        if problem == "ppr":
+            mu, L = alpha, 2.0 - alpha
+        else:
+            if lam_hat is None:
+                from .graph import spectral_norm_estimate
+                lam_hat = spectral_norm_estimate(g, iters=200, seed=0)
+            lam = min(max(lam_hat, 1e-12), float(g.d_max))
+            mu, L = 1.0 - alpha * lam, 1.0 + alpha * lam
+    if max_sweeps is None:  # the reference default (src/local_solvers.py:500)
+        gap = max(mu, 1e-12)
+        max_sweeps = max(1000, int(10 * math.log(max(1.0 / max(eps, 1e-300), 2.0)) / gap))
+    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method="local-ch",
+                         problem=problem, mu=mu, L=L, relabel=relabel)
     try:
         return solver.solve(sd)
     finally:

@@ -34,6 +34,7 @@
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
@@ -44,6 +45,16 @@ namespace gd {  // fifo_batch.cu
 struct FifoBatchState;
 FifoBatchState *fifo_batch_create(const gd_graph *G, int slots);
 void fifo_batch_destroy(FifoBatchState *F);
+struct SignedState;
+SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, int slots);
+void signed_batch_destroy(SignedState *S);
+void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &p,
+                      const int64_t *d_seeds, int64_t n_seeds, const int32_t *perm,
+                      const int32_t *inv, int64_t *sweeps, int64_t *ops, int64_t *pushes,
+                      int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
+                      int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
+                      std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
+                      cudaStream_t st);
 int fifo_batch_slots(const FifoBatchState *F);
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
@@ -595,6 +606,7 @@ using namespace gd;
 struct gd_batch {
     const gd_graph *G;      // caller's graph
     FifoBatchState *fifo = nullptr;  // GD_M_LOCAL_SOR state
+    SignedState *sgn = nullptr;      // GD_M_LOCAL_CH state
     gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
     DBuf<int32_t> perm, inv;
     gd_batch_params p;
@@ -653,6 +665,7 @@ struct gd_batch {
         for (auto e : ev) cudaEventDestroy(e);
         delete R;
         if (fifo) fifo_batch_destroy(fifo);
+        if (sgn) signed_batch_destroy(sgn);
     }
 };
 
@@ -682,6 +695,18 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaEventElapsedTime(&f, B->ev[0], B->ev[1]));
         B->last_ms = f;
         B->last_launches = n_seeds ? 1 : 0;
+        return;
+    }
+    if (B->sgn) {  // signed sweep-synchronous waves (batch_signed.cu)
+        if (n_seeds == 0) {
+            B->last_ms = 0.0;
+            B->last_launches = 0;
+            return;
+        }
+        signed_batch_run(B->sgn, B->work(), B->p, d_seeds, n_seeds, B->R ? B->perm.p : nullptr,
+                         B->R ? B->inv.p : nullptr, B->sweeps.p, B->ops.p, B->pushes.p,
+                         B->support.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p, B->xvals.p,
+                         B->xcap, B->cursor.p, B->ev, &B->last_ms, &B->last_launches, st);
         return;
     }
     const int64_t waves = (n_seeds + B->slots - 1) / B->slots;
@@ -803,11 +828,15 @@ extern "C" {
 int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out) {
     return guarded([&] {
         GD_CHECK_ARG(G && p && out, "null pointer");
-        GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR,
+        GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR ||
+                         p->method == GD_M_LOCAL_CH,
                      "unknown batch method");
+        GD_CHECK_ARG(p->problem == GD_P_PPR || (p->problem == GD_P_KATZ && p->method == GD_M_LOCAL_CH),
+                     "Katz batches need GD_M_LOCAL_CH");
         GD_CHECK_ARG(p->method != GD_M_LOCAL_SOR || (p->omega > 0.0 && p->omega <= 2.0),
                      "omega must be in (0, 2]");
-        GD_CHECK_ARG(p->alpha > 0.0 && p->alpha <= 1.0, "alpha must be in (0, 1]");
+        GD_CHECK_ARG(p->alpha > 0.0 && (p->problem == GD_P_KATZ || p->alpha <= 1.0),
+                     "alpha must be in (0, 1]");
         GD_CHECK_ARG(p->eps > 0.0, "eps must be positive");
         GD_CHECK_ARG(G->n_arcs < (1LL << CNT_SHIFT), "too many arcs");
         GD_CUDA(cudaSetDevice(G->device));
@@ -829,6 +858,36 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 return;
             }
             if (p->relabel) build_relabeled(B);
+            if (p->method == GD_M_LOCAL_CH) {
+                if (B->p.mu == 0.0 && B->p.L == 0.0) {
+                    GD_CHECK_ARG(p->problem == GD_P_PPR, "Katz batches need mu, L");
+                    B->p.mu = p->alpha;
+                    B->p.L = 2.0 - p->alpha;
+                }
+                GD_CHECK_ARG(B->p.mu < B->p.L, "need mu < L");
+                if (p->max_sweeps <= 0) {  // the reference default (src/local_solvers.py:500)
+                    const double gap = B->p.mu > 1e-12 ? B->p.mu : 1e-12;
+                    const double inv = 1.0 / (p->eps > 1e-300 ? p->eps : 1e-300);
+                    const int64_t d =
+                        (int64_t)(10.0 * std::log(inv > 2.0 ? inv : 2.0) / gap);
+                    B->p.max_sweeps = d > 1000 ? d : 1000;
+                }
+                int slots = p->slots;
+                if (slots <= 0) {
+                    size_t fr = 0, tot = 0;
+                    GD_CUDA(cudaMemGetInfo(&fr, &tot));
+                    const int64_t by_mem = (int64_t)(fr / 4) / (ld * 33);
+                    slots = (int)(by_mem < 64 ? (by_mem < 1 ? 1 : by_mem) : 64);
+                }
+                if (slots > 2048) slots = 2048;
+                B->slots = slots;
+                B->xcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
+                B->cursor.alloc(1); B->overflow.alloc(1);
+                B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
+                B->sgn = signed_batch_create(B->work(), B->p, slots);
+                *out = B;
+                return;
+            }
             B->colp.alloc(G->n_arcs ? G->n_arcs : 1);
             k_pack_cols<<<4 * n_sms(G->device), 256>>>(B->work()->view(), B->colp.p);
             GD_LAUNCH_CHECK();

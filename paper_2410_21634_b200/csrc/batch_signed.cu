@@ -1,0 +1,1009 @@
+// batch_signed.cu -- batched sweep-synchronous solvers with SIGNED residuals:
+//   * LocalCH (Chebyshev momentum, src/local_solvers.py:473-538) for many
+//     seeds, PPR or Katz (gd_batch with GD_M_LOCAL_CH), and
+//   * warm-started signed LocalGD over a pool of resident PPR pairs (p, r)
+//     on an evolving graph (gd_pairs: config 5's incremental maintenance;
+//     event adjustment src/dynamic.py:40-107, repair on the new graph).
+//
+// Per slot (one seed / pair): dense x, r (+ momentum value and stamp for
+// CH).  Residuals change sign, so the unsigned kernel's "exactly one arc
+// observes the threshold crossing" does not hold.  The frontier of round t
+// is instead filtered from CANDIDATES -- under momentum the previous
+// frontier (whose r is r - vals, not 0) plus every node that received a
+// contribution in round t-1 -- which is exactly the reference's candidate
+// set (_apply_update_seq + _filter_frontier with a signed test).  A per-slot
+// bit map per round parity deduplicates candidates: the old word returned by
+// one atomicOr says whether the node is new this round.
+//
+// Round t:  phase A  candidates -> |r| >= theta ? push (x, r, momentum,
+//                    l1 delta) and stage (slot, node, c_u) : skip;
+//                    block flushes -> entries + arc offsets + chunk map
+//           phase B  32-arc chunks: r[v] += c_u (returning atomic: l1
+//                    delta, first touch -> sector map), candidate for t+1
+// The per-slot l1 norm is tracked incrementally (|old + c| - |old| per
+// update) for the LocalCH divergence abort (l1 > 10 ||b||_1, :527-530); it
+// equals the reference's pairwise sum to rounding, which can only matter when
+// l1 sits within rounding of the abort level.
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gd {
+namespace {
+
+constexpr int SBT = 512;
+constexpr int SUNROLL = 4;
+constexpr int SCNT_SHIFT = 36;
+constexpr unsigned long long SARC_MASK = (1ULL << SCNT_SHIFT) - 1ULL;
+constexpr unsigned SFULL = 0xffffffffu;
+constexpr int SSTAGE = 4 * SBT;  // staged entries / candidates per block
+constexpr int SCHUNKS = 32;
+
+struct SArgs {
+    DevGraph g;
+    DevOp op;        // weight rule (RW / CONST) and theta coefficient
+    int method;      // 0 signed GD, 1 CH
+    int64_t m, ld, max_sweeps, fcap, ccap, candcap;
+    double *x, *r, *mom;
+    int32_t *mstamp;  // round of the last momentum write; -1 = never pushed
+    const double *coef_r, *coef_m;  // CH coefficients per sweep index
+    double step0, l1cap;            // CH: first step, abort factor on ||b||_1
+    int32_t *pushed;                // CH: per slot first-pushed nodes (x support)
+    unsigned long long *pushed_cnt;
+    uint32_t *cmark[2];             // per slot candidate bit maps (cmw words each)
+    int64_t cmw;
+    uint32_t *secmap;               // per slot touched 32 B sectors of r (nullable)
+    int64_t smw;
+    int64_t *cand[2];               // (slot << 32 | node)
+    unsigned long long *candctr;    // [2]
+    int64_t *fkey, *farc, *frow;    // frontier of the current round
+    double *fcval;
+    int32_t *chunk_e;
+    unsigned long long *fctr;       // packed (entries << 36 | arcs)
+    unsigned long long *s_ops, *s_pushes;
+    double *s_l1, *s_b1;
+    int32_t *s_last, *s_conv;
+    int32_t *overflow;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt_s() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+struct SStage {
+    double *c;
+    double *l1;                      // [m] per-slot l1 deltas of the block
+    unsigned long long *ops, *push;  // [m]
+    unsigned long long *scan;        // [SBT/32 + 2]
+    unsigned long long *next;
+    int32_t *k, *v, *d;
+    int32_t *ck, *cv;  // staged candidates
+    unsigned *cnt, *ccnt;
+};
+
+inline size_t sstage_bytes(int64_t m) {
+    return (size_t)SSTAGE * 8 + (size_t)m * 24 + 8 * (SBT / 32 + 3) + (size_t)SSTAGE * 20 + 32;
+}
+
+__device__ SStage sstage_carve(void *base, int64_t m) {
+    char *p = (char *)base;
+    SStage s;
+    s.c = (double *)p; p += 8 * SSTAGE;
+    s.l1 = (double *)p; p += 8 * m;
+    s.ops = (unsigned long long *)p; p += 8 * m;
+    s.push = (unsigned long long *)p; p += 8 * m;
+    s.scan = (unsigned long long *)p; p += 8 * (SBT / 32 + 2);
+    s.next = (unsigned long long *)p; p += 8;
+    s.k = (int32_t *)p; p += 4 * SSTAGE;
+    s.v = (int32_t *)p; p += 4 * SSTAGE;
+    s.d = (int32_t *)p; p += 4 * SSTAGE;
+    s.ck = (int32_t *)p; p += 4 * SSTAGE;
+    s.cv = (int32_t *)p; p += 4 * SSTAGE;
+    s.cnt = (unsigned *)p; p += 16;
+    s.ccnt = (unsigned *)p;
+    return s;
+}
+
+__device__ __forceinline__ void slot_add_u(bool flag, int32_t k, unsigned val,
+                                           unsigned long long *cnt) {
+    unsigned am = __ballot_sync(SFULL, flag);
+    if (!flag) return;
+    unsigned peers = __match_any_sync(am, k);
+    unsigned sum = __reduce_add_sync(peers, val);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, (unsigned long long)sum);
+}
+
+// per-slot double sum into shared memory; one atomic per warp when the
+// warp's lanes share a slot (the common case: a chunk is one entry's arcs)
+__device__ __forceinline__ void slot_add_d(bool flag, int32_t k, double val, double *acc) {
+    const unsigned am = __ballot_sync(SFULL, flag);
+    if (!am) return;
+    const int32_t k0 = __shfl_sync(SFULL, k, __ffs(am) - 1);
+    if (__all_sync(SFULL, !flag || k == k0)) {
+        double s = flag ? val : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SFULL, s, o);
+        if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(acc + k0, s);
+    } else if (flag) {
+        atomicAdd(acc + k, val);
+    }
+}
+
+__device__ void cand_append_global(bool flag, int32_t k, int32_t v, const SArgs &A, int par) {
+    unsigned am = __ballot_sync(SFULL, flag);
+    if (!am) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(A.candctr + par, (unsigned long long)__popc(am));
+    base = __shfl_sync(SFULL, base, 0);
+    if (flag) {
+        const int64_t idx = (int64_t)base + __popc(am & lanemask_lt_s());
+        if (idx < A.candcap) A.cand[par][idx] = ((int64_t)k << 32) | (uint32_t)v;
+        else A.overflow[0] = 1;
+    }
+}
+
+// stage a candidate in the block buffer (spill to the global list when full)
+__device__ void cand_stage(bool flag, int32_t k, int32_t v, const SStage &S, const SArgs &A,
+                           int par) {
+    unsigned am = __ballot_sync(SFULL, flag);
+    if (!am) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(S.ccnt, (unsigned)__popc(am));
+    base = __shfl_sync(SFULL, base, 0);
+    const unsigned my = base + __popc(am & lanemask_lt_s());
+    const bool spill = flag && my >= (unsigned)SSTAGE;
+    if (flag && !spill) {
+        S.ck[my] = k;
+        S.cv[my] = v;
+    }
+    cand_append_global(spill, k, v, A, par);
+}
+
+__device__ void cand_flush(const SStage &S, const SArgs &A, int par) {
+    __syncthreads();
+    const unsigned cnt = min(*S.ccnt, (unsigned)SSTAGE);
+    __shared__ unsigned long long base;
+    if (threadIdx.x == 0) base = cnt ? atomicAdd(A.candctr + par, (unsigned long long)cnt) : 0ULL;
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < cnt; i += SBT) {
+        const int64_t idx = (int64_t)base + i;
+        if (idx < A.candcap) A.cand[par][idx] = ((int64_t)S.ck[i] << 32) | (uint32_t)S.cv[i];
+        else A.overflow[0] = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *S.ccnt = 0;
+    __syncthreads();
+}
+
+// first mark of (k, v) in the candidate map of parity par?
+__device__ __forceinline__ bool cand_mark(bool flag, int32_t k, int32_t v, const SArgs &A,
+                                          int par) {
+    if (!flag) return false;
+    uint32_t *w = A.cmark[par] + (int64_t)k * A.cmw + (v >> 5);
+    const uint32_t bit = 1u << (v & 31);
+    return !(atomicOr(w, bit) & bit);
+}
+
+__device__ void entry_stage(bool flag, int32_t k, int32_t u, int32_t d, double c, const SStage &S) {
+    unsigned am = __ballot_sync(SFULL, flag);
+    if (!am) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(S.cnt, (unsigned)__popc(am));
+    base = __shfl_sync(SFULL, base, 0);
+    const unsigned my = base + __popc(am & lanemask_lt_s());
+    if (flag) {  // the caller flushes before the buffer can overflow
+        S.k[my] = k;
+        S.v[my] = u;
+        S.d[my] = d;
+        S.c[my] = c;
+    }
+}
+
+// Block flush of staged frontier entries: one reservation, arc offsets by a
+// block scan, entry arrays + chunk map written here (the entries are final).
+__device__ void entry_flush(const SStage &S, const SArgs &A) {
+    __syncthreads();
+    const unsigned cnt = *S.cnt;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned per = (cnt + SBT - 1) / SBT;
+    const unsigned lo = min(cnt, tid * per), hi = min(cnt, lo + per);
+    unsigned long long mine = 0;
+    for (unsigned i = lo; i < hi; i++) mine += (unsigned long long)S.d[i];
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(SFULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.scan[w] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < SBT / 32; i++) {
+            unsigned long long x = S.scan[i];
+            S.scan[i] = run;
+            run += x;
+        }
+        unsigned long long old = 0;
+        if (cnt) old = atomicAdd(A.fctr, ((unsigned long long)cnt << SCNT_SHIFT) + run);
+        S.scan[SBT / 32] = old;
+    }
+    __syncthreads();
+    const unsigned long long old = S.scan[SBT / 32];
+    int64_t arc = (int64_t)(old & SARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
+    const int64_t ebase = (int64_t)(old >> SCNT_SHIFT);
+    for (unsigned i = lo; i < hi; i++) {
+        const int64_t e = ebase + i;
+        const int32_t u = S.v[i];
+        if (e < A.fcap) {
+            A.fkey[e] = ((int64_t)S.k[i] << 32) | (uint32_t)u;
+            A.farc[e] = arc;
+            A.frow[e] = A.g.row[u];
+            A.fcval[e] = S.c[i];
+            const int64_t c0 = (arc + 31) >> 5, c1 = min((arc + S.d[i] + 31) >> 5, A.ccap);
+            for (int64_t c = c0; c < c1; ++c) A.chunk_e[c] = (int32_t)e;
+        } else {
+            A.overflow[0] = 1;
+        }
+        arc += S.d[i];
+    }
+    __syncthreads();
+    if (tid == 0) *S.cnt = 0;
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool slot_diverged(const SArgs &A, int32_t k) {
+    return A.method == 1 && A.s_l1[k] > A.l1cap * A.s_b1[k];
+}
+
+__global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const SStage S = sstage_carve(sm_raw, A.m);
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = blockIdx.x * (int64_t)SBT + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * SBT;
+    const bool ch = A.method == 1;
+    for (int64_t k = threadIdx.x; k < A.m; k += SBT) {
+        S.l1[k] = 0.0;
+        S.ops[k] = S.push[k] = 0;
+    }
+    if (threadIdx.x == 0) {
+        *S.cnt = 0;
+        *S.ccnt = 0;
+        *S.next = 0;
+    }
+    __syncthreads();
+    for (int32_t t = 0;; ++t) {
+        const int cur = t & 1, nxt = cur ^ 1;
+        const int64_t NC = (int64_t)*(volatile unsigned long long *)(A.candctr + cur);
+        if (NC == 0) break;
+        if (NC > A.candcap) {
+            if (gtid == 0) A.overflow[0] = 1;
+            break;
+        }
+        // ---------------- phase A: filter candidates, push the frontier ------
+        if (gtid == 0) {
+            A.fctr[0] = 0ULL;
+            A.candctr[nxt] = 0ULL;
+        }
+        grid.sync();  // counter resets visible before any reservation
+        const double cr = (ch && t > 0) ? A.coef_r[t] : 0.0;
+        const double cm = (ch && t > 0) ? A.coef_m[t] : 0.0;
+        for (int64_t base = blockIdx.x * (int64_t)SBT; base < NC; base += nthreads) {
+            const int64_t ci = base + threadIdx.x;
+            bool act = false, fresh = false;
+            int32_t k = 0, u = 0, d = 0;
+            double cval = 0.0, dl1 = 0.0;
+            if (ci < NC) {
+                const int64_t key = A.cand[cur][ci];
+                k = (int32_t)(key >> 32);
+                u = (int32_t)(key & 0xffffffffLL);
+                atomicAnd(A.cmark[cur] + (int64_t)k * A.cmw + (u >> 5), ~(1u << (u & 31)));
+                const int64_t idx = (int64_t)k * A.ld + u;
+                const double ru = A.r[idx];
+                d = A.g.deg[u];
+                act = fabs(ru) >= theta_of(A.op, u, d) && !slot_diverged(A, k);
+                if (act && t >= A.max_sweeps) {  // sweep cap reached with work left
+                    A.s_conv[k] = 0;
+                    act = false;
+                }
+                if (act) {
+                    double v;
+                    if (!ch) {
+                        v = ru;
+                    } else if (t == 0) {
+                        v = __dmul_rn(A.step0, ru);
+                    } else {
+                        const double prev = (A.mstamp[idx] == t - 1) ? A.mom[idx] : 0.0;
+                        v = __dadd_rn(__dmul_rn(cr, ru), __dmul_rn(cm, prev));
+                    }
+                    A.x[idx] = __dadd_rn(A.x[idx], v);
+                    const double rn = __dsub_rn(ru, v);
+                    A.r[idx] = rn;
+                    if (ch) {
+                        dl1 = fabs(rn) - fabs(ru);
+                        fresh = A.mstamp[idx] == -1;
+                        A.mom[idx] = v;
+                        A.mstamp[idx] = t;
+                    }
+                    cval = __dmul_rn(v, node_weight(A.op, d));
+                    A.s_last[k] = t;
+                }
+            }
+            if (ch) {  // pushed-node list (x support; mstamp reset)
+                unsigned am = __ballot_sync(SFULL, fresh);
+                if (fresh) {
+                    unsigned peers = __match_any_sync(am, k);
+                    const int leader = __ffs(peers) - 1;
+                    unsigned long long b = 0;
+                    if (lane == leader)
+                        b = atomicAdd(A.pushed_cnt + k, (unsigned long long)__popc(peers));
+                    b = __shfl_sync(peers, b, leader);
+                    A.pushed[(int64_t)k * A.ld + (int64_t)b + __popc(peers & lanemask_lt_s())] = u;
+                }
+                slot_add_d(act, k, dl1, S.l1);
+            }
+            slot_add_u(act, k, (unsigned)d, S.ops);
+            slot_add_u(act, k, 1u, S.push);
+            entry_stage(act, k, u, d, cval, S);
+            // under momentum a pushed node keeps a residual: candidate again
+            const bool again = cand_mark(ch && act, k, u, A, nxt);
+            cand_stage(again, k, u, S, A, nxt);
+            __syncthreads();
+            if (*S.cnt > (unsigned)(SSTAGE - SBT)) entry_flush(S, A);
+        }
+        entry_flush(S, A);
+        for (int64_t k = threadIdx.x; k < A.m; k += SBT) {
+            if (S.ops[k]) { atomicAdd(A.s_ops + k, S.ops[k]); S.ops[k] = 0; }
+            if (S.push[k]) { atomicAdd(A.s_pushes + k, S.push[k]); S.push[k] = 0; }
+        }
+        grid.sync();
+        // ---------------- phase B: arc chunks -------------------------------
+        const unsigned long long pk = *(volatile unsigned long long *)A.fctr;
+        const int64_t F = (int64_t)(pk >> SCNT_SHIFT), P = (int64_t)(pk & SARC_MASK);
+        if (F > A.fcap || ((P + 31) >> 5) > A.ccap) {
+            if (gtid == 0) A.overflow[0] = 1;
+            break;
+        }
+        const int64_t C = (P + 31) >> 5;
+        const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
+        const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
+        for (;;) {
+            unsigned long long claim = 0;
+            if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)SUNROLL);
+            const int64_t cb = bc0 + (int64_t)__shfl_sync(SFULL, claim, 0);
+            if (cb >= bc1) break;
+            int32_t k[SUNROLL], v[SUNROLL];
+            double c[SUNROLL], old[SUNROLL];
+            bool valid[SUNROLL];
+#pragma unroll
+            for (int q = 0; q < SUNROLL; q++) {
+                const int64_t chn = cb + q;
+                const bool live = chn < bc1;
+                const int64_t e = live ? A.chunk_e[chn] : 0;
+                const int64_t a = chn << 5;
+                const int64_t wi = e + 1 + lane;
+                const int64_t st = (live && wi < F) ? A.farc[wi] : INT64_MAX;
+                const int64_t pos = st - a;
+                const unsigned starts = __reduce_or_sync(SFULL, pos < 32 ? (1u << pos) : 0u);
+                const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
+                const int64_t p = a + lane;
+                valid[q] = live && p < P;
+                k[q] = 0;
+                v[q] = 0;
+                c[q] = 0.0;
+                if (valid[q]) {
+                    k[q] = (int32_t)(A.fkey[me] >> 32);
+                    c[q] = A.fcval[me];
+                    v[q] = A.g.col[A.frow[me] + (p - A.farc[me])];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < SUNROLL; q++)
+                old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+#pragma unroll
+            for (int q = 0; q < SUNROLL; q++) {
+                if (ch) {
+                    const double dl1 =
+                        valid[q] ? fabs(__dadd_rn(old[q], c[q])) - fabs(old[q]) : 0.0;
+                    slot_add_d(valid[q], k[q], dl1, S.l1);
+                }
+                if (A.secmap && valid[q] && __double_as_longlong(old[q]) == 0)
+                    atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7),
+                             1u << ((v[q] >> 2) & 31));
+                const bool nw = cand_mark(valid[q], k[q], v[q], A, nxt);
+                cand_stage(nw, k[q], v[q], S, A, nxt);
+            }
+        }
+        cand_flush(S, A, nxt);
+        if (threadIdx.x == 0) *S.next = 0;
+        for (int64_t k = threadIdx.x; k < A.m; k += SBT)
+            if (S.l1[k] != 0.0) {
+                atomicAdd(A.s_l1 + k, S.l1[k]);
+                S.l1[k] = 0.0;
+            }
+        grid.sync();
+    }
+}
+
+// ---- cold waves (gd_batch, GD_M_LOCAL_CH) ---------------------------------
+
+// seeds -> slots: r[s] = b_s, the seed is the only round-0 candidate
+__global__ void k_s_init(SArgs A, const int64_t *__restrict__ seeds, const int32_t *perm,
+                         double bval) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k == 0) {
+        A.candctr[0] = (unsigned long long)A.m;
+        A.candctr[1] = 0ULL;
+    }
+    if (k >= A.m) return;
+    int32_t s = (int32_t)seeds[k];
+    if (perm) s = perm[s];
+    A.r[k * A.ld + s] = bval;
+    A.secmap[k * A.smw + (s >> 7)] |= 1u << ((s >> 2) & 31);
+    A.cmark[0][k * A.cmw + (s >> 5)] |= 1u << (s & 31);
+    A.cand[0][k] = (k << 32) | (uint32_t)s;
+    A.pushed_cnt[k] = 0;
+    A.s_ops[k] = 0;
+    A.s_pushes[k] = 0;
+    A.s_l1[k] = fabs(bval);
+    A.s_b1[k] = fabs(bval);
+    A.s_last[k] = -1;
+    A.s_conv[k] = 1;
+}
+
+__global__ void k_s_reserve(SArgs A, unsigned long long *cursor, int64_t *slot_base) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < A.m) slot_base[k] = (int64_t)atomicAdd(cursor, A.pushed_cnt[k]);
+}
+
+struct SOut {
+    int64_t *sweeps, *ops, *pushes, *support, *xoff, *xcnt;
+    int32_t *conv;
+    int32_t *xnodes;
+    double *xvals;
+    int64_t xcap;
+    const int32_t *inv;
+    const int64_t *slot_base;
+};
+
+// grid (SCHUNKS, slots): x over the pushed list out (caller ids); x, mstamp
+// back to their idle values; block (0, k) writes the seed's counters.
+__global__ void k_s_extract(SArgs A, SOut O, int64_t seed_base) {
+    const int k = blockIdx.y;
+    const int64_t off = (int64_t)k * A.ld;
+    const int64_t pc = (int64_t)A.pushed_cnt[k];
+    const int64_t b = O.slot_base[k];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pc;
+         i += (int64_t)SCHUNKS * blockDim.x) {
+        const int32_t u = A.pushed[off + i];
+        const double xv = A.x[off + u];
+        A.x[off + u] = 0.0;
+        A.mstamp[off + u] = -1;
+        if (b + i < O.xcap) {
+            O.xnodes[b + i] = O.inv ? O.inv[u] : u;
+            O.xvals[b + i] = xv;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t si = seed_base + k;
+        O.sweeps[si] = (int64_t)A.s_last[k] + 1;
+        O.ops[si] = (int64_t)A.s_ops[k];
+        O.pushes[si] = (int64_t)A.s_pushes[k];
+        O.conv[si] = (A.s_conv[k] && !slot_diverged(A, k)) ? 1 : 0;
+        O.support[si] = -1;  // not tracked for signed solves
+        O.xoff[si] = b;
+        O.xcnt[si] = pc;
+    }
+}
+
+// grid (SCHUNKS, slots): zero exactly the 32 B sectors of r a slot wrote
+__global__ void k_s_reset(SArgs A) {
+    const int k = blockIdx.y;
+    const int64_t off = (int64_t)k * A.ld;
+    uint32_t *map = A.secmap + (int64_t)k * A.smw;
+    const int64_t per = (A.smw + SCHUNKS - 1) / SCHUNKS;
+    const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
+    double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
+    for (int64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint32_t bits = map[w];
+        if (!bits) continue;
+        map[w] = 0u;
+        while (bits) {
+            const int bb = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t sec = w * 32 + bb;
+            if (4 * sec + 3 < A.ld) {
+                r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+            } else {
+                for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
+            }
+        }
+    }
+}
+
+// ---- resident pairs (gd_pairs) ------------------------------------------
+
+struct PairEvent {
+    int32_t u, v, du, dv;  // endpoints and their degrees before the event
+    int32_t step;          // +1 insert, -1 delete
+};
+
+// Endpoint a of edge (a, b), degree d0 -> d1 (src/dynamic.py:70-98), with
+// numpy's evaluation order: p*(d1/d0), (1-alpha)*p/d1 = fl(fl(q p) / d1).
+__device__ __forceinline__ void pair_endpoint(double *p, double *r, double q, int32_t a,
+                                              int32_t b, int32_t d0, int32_t d1) {
+    const double fd0 = (double)d0, fd1 = (double)d1;
+    if (d1 > d0) {
+        if (d0 > 0) {
+            p[a] = __dmul_rn(p[a], __ddiv_rn(fd1, fd0));
+            r[a] = __dsub_rn(r[a], __ddiv_rn(p[a], fd1));
+        }
+        r[b] = __dadd_rn(r[b], __ddiv_rn(__dmul_rn(q, p[a]), fd1));
+    } else {
+        const double ratio = __ddiv_rn(p[a], fd0);
+        if (d1 > 0) {
+            p[a] = __dmul_rn(p[a], __ddiv_rn(fd1, fd0));
+            r[a] = __dadd_rn(r[a], __ddiv_rn(p[a], fd1));
+        } else {
+            r[a] = __dadd_rn(r[a], p[a]);
+            p[a] = 0.0;
+        }
+        r[b] = __dsub_rn(r[b], __dmul_rn(q, ratio));
+    }
+}
+
+// one thread per pair: the event batch in order (per-pair sequential, as the
+// reference), endpoints become round-0 candidates of the repair
+__global__ void k_pair_events(SArgs A, const PairEvent *__restrict__ ev, int64_t n_ev, double q) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= A.m) return;
+    double *p = A.x + k * A.ld, *r = A.r + k * A.ld;
+    for (int64_t i = 0; i < n_ev; ++i) {
+        const PairEvent e = ev[i];
+        pair_endpoint(p, r, q, e.u, e.v, e.du, e.du + e.step);
+        pair_endpoint(p, r, q, e.v, e.u, e.dv, e.dv + e.step);
+        const int32_t ends[2] = {e.u, e.v};
+        for (int j = 0; j < 2; ++j) {
+            const int32_t a = ends[j];
+            uint32_t *w = A.cmark[0] + k * A.cmw + (a >> 5);
+            const uint32_t bit = 1u << (a & 31);
+            if (!(*w & bit)) {  // this thread owns pair k's map
+                *w |= bit;
+                const unsigned long long at = atomicAdd(A.candctr, 1ULL);
+                if ((int64_t)at < A.candcap) A.cand[0][at] = (k << 32) | (uint32_t)a;
+                else A.overflow[0] = 1;
+            }
+        }
+    }
+}
+
+// every active node of every pair as a round-0 candidate (pool creation,
+// or after a repair that stopped at max_sweeps)
+__global__ void k_pair_scan(SArgs A) {
+    const int64_t total = A.m * A.ld;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / A.ld, u = i - k * A.ld;
+        if (u >= A.g.n) continue;
+        const double ru = A.r[i];
+        if (ru == 0.0 || !(fabs(ru) >= theta_of(A.op, u, A.g.deg[u]))) continue;
+        uint32_t *w = A.cmark[0] + k * A.cmw + (u >> 5);
+        const uint32_t bit = 1u << (u & 31);
+        if (atomicOr(w, bit) & bit) continue;
+        const unsigned long long at = atomicAdd(A.candctr, 1ULL);
+        if ((int64_t)at < A.candcap) A.cand[0][at] = (k << 32) | (uint32_t)u;
+        else A.overflow[0] = 1;
+    }
+}
+
+__global__ void k_pair_stats_reset(SArgs A) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= A.m) return;
+    A.s_ops[k] = 0;
+    A.s_pushes[k] = 0;
+    A.s_last[k] = -1;
+    A.s_conv[k] = 1;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Shared state of both drivers.
+// ---------------------------------------------------------------------------
+struct SignedState {
+    int device = 0;
+    int method = 0;
+    int slots = 0, grid = 0;
+    int64_t n = 0, ld = 0, fcap = 0, ccap = 0, candcap = 0, cmw = 0, smw = 0, max_sweeps = 0;
+    DevOp op{};
+    double step0 = 0.0, l1cap = 10.0;
+    DBuf<double> coef_r, coef_m;
+    DBuf<double> x, r, mom, fcval, s_l1, s_b1;
+    DBuf<int32_t> mstamp, pushed, chunk_e, s_last, s_conv, overflow;
+    DBuf<uint32_t> cm0, cm1, secmap;
+    DBuf<int64_t> cand0, cand1, fkey, farc, frow, slot_base;
+    DBuf<unsigned long long> candctr, fctr, s_ops, s_pushes, pushed_cnt;
+    bool dirty = false;  // an aborted run left marks behind: full clear next time
+    size_t smem = 0;
+
+    void alloc(const gd_graph *W, int method_, int slots_, int64_t fcap_, bool cold) {
+        device = W->device;
+        method = method_;
+        slots = slots_;
+        n = W->n;
+        ld = ((n ? n : 1) + 3) & ~3LL;
+        cmw = (ld + 31) / 32;
+        smw = (ld / 4 + 31) / 32;
+        const size_t sn = (size_t)slots * (size_t)ld;
+        x.alloc(sn); r.alloc(sn);
+        GD_CUDA(cudaMemset(x.p, 0, sizeof(double) * sn));
+        GD_CUDA(cudaMemset(r.p, 0, sizeof(double) * sn));
+        if (method == 1) {
+            mom.alloc(sn);
+            mstamp.alloc(sn);
+            pushed.alloc(sn);
+            GD_CUDA(cudaMemset(mstamp.p, 0xFF, sizeof(int32_t) * sn));  // -1: never pushed
+        }
+        cm0.alloc((size_t)slots * cmw); cm1.alloc((size_t)slots * cmw);
+        GD_CUDA(cudaMemset(cm0.p, 0, sizeof(uint32_t) * (size_t)slots * cmw));
+        GD_CUDA(cudaMemset(cm1.p, 0, sizeof(uint32_t) * (size_t)slots * cmw));
+        if (cold) {
+            secmap.alloc((size_t)slots * smw);
+            GD_CUDA(cudaMemset(secmap.p, 0, sizeof(uint32_t) * (size_t)slots * smw));
+        }
+        fcap = fcap_;
+        ccap = fcap_;
+        candcap = fcap_;
+        cand0.alloc(candcap); cand1.alloc(candcap);
+        fkey.alloc(fcap); farc.alloc(fcap); frow.alloc(fcap); fcval.alloc(fcap);
+        chunk_e.alloc(ccap);
+        candctr.alloc(2); fctr.alloc(1); overflow.alloc(1);
+        s_ops.alloc(slots); s_pushes.alloc(slots); pushed_cnt.alloc(slots);
+        s_l1.alloc(slots); s_b1.alloc(slots); s_last.alloc(slots); s_conv.alloc(slots);
+        slot_base.alloc(slots);
+        GD_CUDA(cudaMemset(s_l1.p, 0, sizeof(double) * slots));
+        GD_CUDA(cudaMemset(s_b1.p, 0, sizeof(double) * slots));
+        smem = sstage_bytes(slots);
+        GD_CUDA(cudaFuncSetAttribute(k_signed_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        int per_sm = 0;
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signed_rounds, SBT, smem));
+        GD_CHECK_ARG(per_sm > 0, "signed round kernel does not fit on an SM");
+        grid = per_sm * n_sms(device);
+    }
+
+    void set_ch(double mu, double L, int64_t max_sweeps_) {
+        max_sweeps = max_sweeps_;
+        step0 = 2.0 / (L + mu);
+        // delta recurrence of src/local_solvers.py:508-520, per sweep index
+        const int64_t T = max_sweeps + 1;
+        std::vector<double> cr(T, 0.0), cmv(T, 0.0);
+        double delta = (L - mu) / (L + mu);
+        for (int64_t t = 1; t < T; ++t) {
+            const double dn = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
+            cr[t] = 4.0 * dn / (L - mu);
+            cmv[t] = delta * dn;
+            delta = dn;
+        }
+        coef_r.alloc(T);
+        coef_m.alloc(T);
+        GD_CUDA(cudaMemcpy(coef_r.p, cr.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(coef_m.p, cmv.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
+    }
+
+    SArgs args(const gd_graph *W, int64_t m) {
+        SArgs A{};
+        A.g = W->view();
+        A.op = op;
+        A.method = method;
+        A.m = m;
+        A.ld = ld;
+        A.max_sweeps = max_sweeps;
+        A.fcap = fcap; A.ccap = ccap; A.candcap = candcap;
+        A.x = x.p; A.r = r.p; A.mom = mom.p; A.mstamp = mstamp.p;
+        A.coef_r = coef_r.p; A.coef_m = coef_m.p;
+        A.step0 = step0; A.l1cap = l1cap;
+        A.pushed = pushed.p; A.pushed_cnt = pushed_cnt.p;
+        A.cmark[0] = cm0.p; A.cmark[1] = cm1.p; A.cmw = cmw;
+        A.secmap = secmap.p; A.smw = smw;
+        A.cand[0] = cand0.p; A.cand[1] = cand1.p; A.candctr = candctr.p;
+        A.fkey = fkey.p; A.farc = farc.p; A.frow = frow.p; A.fcval = fcval.p;
+        A.chunk_e = chunk_e.p; A.fctr = fctr.p;
+        A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_l1 = s_l1.p; A.s_b1 = s_b1.p;
+        A.s_last = s_last.p; A.s_conv = s_conv.p;
+        A.overflow = overflow.p;
+        return A;
+    }
+
+    void clear_marks(cudaStream_t st) {
+        GD_CUDA(cudaMemsetAsync(cm0.p, 0, sizeof(uint32_t) * (size_t)slots * cmw, st));
+        GD_CUDA(cudaMemsetAsync(cm1.p, 0, sizeof(uint32_t) * (size_t)slots * cmw, st));
+    }
+
+    void rounds(SArgs &A, cudaStream_t st) {
+        void *kargs[] = {&A};
+        GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_signed_rounds, dim3(grid), dim3(SBT),
+                                            kargs, smem, st));
+    }
+
+    void check_overflow(cudaStream_t st) {
+        int32_t ovf = 0;
+        GD_CUDA(cudaMemcpyAsync(&ovf, overflow.p, sizeof(ovf), cudaMemcpyDeviceToHost, st));
+        GD_CUDA(cudaStreamSynchronize(st));
+        if (ovf) {
+            dirty = true;
+            set_error("signed batch capacity %lld (frontier entries, arc chunks or candidates "
+                      "per round) exceeded; raise frontier_cap",
+                      (long long)fcap);
+            throw Error{GD_ERR_CAPACITY};
+        }
+    }
+};
+
+// ---- cold waves -----------------------------------------------------------
+
+SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, int slots) {
+    SignedState *S = new SignedState();
+    try {
+        const int64_t n = W->n ? W->n : 1;
+        int64_t fc = p.frontier_cap > 0 ? p.frontier_cap : (int64_t)slots * n;
+        if (p.frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
+        S->alloc(W, 1, slots, fc, true);
+        // operator: PPR  w = fl(1/d)(1-alpha), b = alpha e_s, theta = eps alpha d
+        //           Katz w = alpha,            b = e_s,       theta = eps d
+        S->op.wrule = p.problem == GD_P_KATZ ? GD_W_CONST : GD_W_RW;
+        S->op.trule = GD_T_DEGREE;
+        S->op.beta = p.problem == GD_P_KATZ ? p.alpha : 1.0 - p.alpha;
+        S->op.tcoeff = p.problem == GD_P_KATZ ? p.eps : p.eps * p.alpha;
+        S->set_ch(p.mu, p.L, p.max_sweeps);
+    } catch (...) {
+        delete S;
+        throw;
+    }
+    return S;
+}
+
+void signed_batch_destroy(SignedState *S) { delete S; }
+int signed_batch_slots(const SignedState *S) { return S->slots; }
+
+void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &p,
+                      const int64_t *d_seeds, int64_t n_seeds, const int32_t *perm,
+                      const int32_t *inv, int64_t *sweeps, int64_t *ops, int64_t *pushes,
+                      int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
+                      int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
+                      std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
+                      cudaStream_t st) {
+    if (S->dirty) {  // a capacity abort left marks / residuals behind
+        S->clear_marks(st);
+        const size_t sn = (size_t)S->slots * (size_t)S->ld;
+        GD_CUDA(cudaMemsetAsync(S->x.p, 0, sizeof(double) * sn, st));
+        GD_CUDA(cudaMemsetAsync(S->r.p, 0, sizeof(double) * sn, st));
+        GD_CUDA(cudaMemsetAsync(S->mstamp.p, 0xFF, sizeof(int32_t) * sn, st));
+        GD_CUDA(cudaMemsetAsync(S->secmap.p, 0, sizeof(uint32_t) * (size_t)S->slots * S->smw, st));
+        S->dirty = false;
+    }
+    GD_CUDA(cudaMemsetAsync(S->overflow.p, 0, sizeof(int32_t), st));
+    const double bval = p.problem == GD_P_KATZ ? 1.0 : p.alpha;
+    const int64_t waves = (n_seeds + S->slots - 1) / S->slots;
+    while ((int64_t)ev.size() < 2 * waves) {
+        cudaEvent_t e;
+        GD_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+    }
+    SOut O{sweeps, ops, pushes, support, xoff, xcnt, conv, xnodes, xvals, xcap, inv,
+           S->slot_base.p};
+    int64_t nl = 0;
+    for (int64_t w = 0; w < waves; ++w) {
+        const int64_t base = w * S->slots;
+        const int64_t m = n_seeds - base < S->slots ? n_seeds - base : S->slots;
+        SArgs A = S->args(W, m);
+        k_s_init<<<(int)((m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, perm, bval);
+        GD_LAUNCH_CHECK();
+        GD_CUDA(cudaEventRecord(ev[2 * w], st));
+        S->rounds(A, st);
+        GD_CUDA(cudaEventRecord(ev[2 * w + 1], st));
+        k_s_reserve<<<(int)((m + 255) / 256), 256, 0, st>>>(A, cursor, S->slot_base.p);
+        k_s_extract<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A, O, base);
+        k_s_reset<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A);
+        GD_LAUNCH_CHECK();
+        nl += 5;
+    }
+    S->check_overflow(st);
+    double tot = 0.0;
+    for (int64_t w = 0; w < waves; ++w) {
+        float f = 0.f;
+        GD_CUDA(cudaEventElapsedTime(&f, ev[2 * w], ev[2 * w + 1]));
+        tot += f;
+    }
+    *ms = tot;
+    *launches = nl;
+}
+
+}  // namespace gd
+
+using namespace gd;
+
+// ---------------------------------------------------------------------------
+// gd_pairs: K resident PPR pairs on an evolving graph.
+// ---------------------------------------------------------------------------
+struct gd_pairs {
+    SignedState S;
+    double alpha = 0.0, eps = 0.0;
+    int64_t k = 0;
+    std::vector<int32_t> deg;  // host copy of the current degrees (event bookkeeping)
+    DBuf<PairEvent> dev_events;
+    bool all_converged = true;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    double last_ms = 0.0;
+    ~gd_pairs() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_sweeps,
+                         const PairEvent *dev_ev, int64_t n_ev, int64_t *sweeps, int64_t *ops,
+                         int64_t *pushes, int32_t *conv) {
+    SignedState &S = P->S;
+    cudaStream_t st = 0;
+    if (S.dirty) {
+        S.clear_marks(st);
+        S.dirty = false;
+        scan = true;
+    }
+    S.max_sweeps = max_sweeps;
+    SArgs A = S.args(G, P->k);
+    GD_CUDA(cudaMemsetAsync(S.overflow.p, 0, sizeof(int32_t), st));
+    GD_CUDA(cudaMemsetAsync(S.candctr.p, 0, 2 * sizeof(unsigned long long), st));
+    k_pair_stats_reset<<<(int)((P->k + 255) / 256), 256, 0, st>>>(A);
+    if (n_ev)
+        k_pair_events<<<(int)((P->k + 127) / 128), 128, 0, st>>>(A, dev_ev, n_ev, 1.0 - P->alpha);
+    if (scan) k_pair_scan<<<4 * n_sms(S.device), 256, 0, st>>>(A);
+    GD_LAUNCH_CHECK();
+    GD_CUDA(cudaEventRecord(P->e0, st));
+    S.rounds(A, st);
+    GD_CUDA(cudaEventRecord(P->e1, st));
+    S.check_overflow(st);
+    float f = 0.f;
+    GD_CUDA(cudaEventElapsedTime(&f, P->e0, P->e1));
+    P->last_ms = f;
+    const int64_t K = P->k;
+    std::vector<int32_t> last(K), cv(K);
+    std::vector<unsigned long long> o(K), pu(K);
+    GD_CUDA(cudaMemcpy(last.data(), S.s_last.p, 4 * K, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(cv.data(), S.s_conv.p, 4 * K, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(o.data(), S.s_ops.p, 8 * K, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(pu.data(), S.s_pushes.p, 8 * K, cudaMemcpyDeviceToHost));
+    P->all_converged = true;
+    for (int64_t i = 0; i < K; ++i) {
+        if (sweeps) sweeps[i] = (int64_t)last[i] + 1;
+        if (ops) ops[i] = (int64_t)o[i];
+        if (pushes) pushes[i] = (int64_t)pu[i];
+        if (conv) conv[i] = cv[i];
+        P->all_converged = P->all_converged && cv[i];
+    }
+}
+
+extern "C" {
+
+int gd_pairs_create(const gd_graph *G, double alpha, double eps, const int64_t *sources,
+                    int64_t k, int64_t frontier_cap, int64_t max_sweeps, gd_pairs **out,
+                    int64_t *sweeps, int64_t *total_ops, int64_t *pushes, int32_t *converged) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && sources && out, "null pointer");
+        GD_CHECK_ARG(k >= 1 && k <= 4096, "pair count must be in [1, 4096]");
+        GD_CHECK_ARG(alpha > 0.0 && alpha < 1.0, "alpha must be in (0, 1)");
+        GD_CHECK_ARG(eps > 0.0, "eps must be positive");
+        GD_CUDA(cudaSetDevice(G->device));
+        gd_pairs *P = new gd_pairs();
+        try {
+            P->alpha = alpha;
+            P->eps = eps;
+            P->k = k;
+            P->deg.resize(G->n);
+            if (G->n)
+                GD_CUDA(cudaMemcpy(P->deg.data(), G->deg.p, 4 * G->n, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < k; ++i) {
+                GD_CHECK_ARG(sources[i] >= 0 && sources[i] < G->n, "source out of range");
+                GD_CHECK_ARG(P->deg[sources[i]] >= 1, "source must have at least one neighbor");
+            }
+            const int64_t n = G->n ? G->n : 1;
+            int64_t fc = frontier_cap > 0 ? frontier_cap : k * n;
+            if (frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
+            P->S.alloc(G, 0, (int)k, fc, false);
+            P->S.op.wrule = GD_W_RW;
+            P->S.op.trule = GD_T_DEGREE;
+            P->S.op.beta = 1.0 - alpha;
+            P->S.op.tcoeff = eps;  // repair thresholds eps * d_u (src/dynamic.py:139-141)
+            for (int64_t i = 0; i < k; ++i)
+                GD_CUDA(cudaMemcpy(P->S.r.p + i * P->S.ld + sources[i], &alpha, sizeof(double),
+                                   cudaMemcpyHostToDevice));
+            GD_CUDA(cudaEventCreate(&P->e0));
+            GD_CUDA(cudaEventCreate(&P->e1));
+            pairs_repair(P, G, true, max_sweeps > 0 ? max_sweeps : 1000000, nullptr, 0, sweeps,
+                         total_ops, pushes, converged);
+        } catch (...) {
+            delete P;
+            throw;
+        }
+        *out = P;
+    });
+}
+
+int gd_pairs_destroy(gd_pairs *P) {
+    delete P;
+    return GD_OK;
+}
+
+int gd_pairs_update(gd_pairs *P, const gd_graph *G_new, const int32_t *kinds, const int64_t *us,
+                    const int64_t *vs, int64_t n_events, int64_t max_sweeps, int64_t *sweeps,
+                    int64_t *total_ops, int64_t *pushes, int32_t *converged) {
+    return guarded([&] {
+        GD_CHECK_ARG(P && G_new && (n_events == 0 || (kinds && us && vs)), "null pointer");
+        GD_CHECK_ARG(G_new->n == (int64_t)P->deg.size(), "node count changed");
+        GD_CUDA(cudaSetDevice(G_new->device));
+        // degrees evolve event by event (event_adjust_many semantics)
+        std::vector<PairEvent> ev(n_events);
+        std::vector<int32_t> deg = P->deg;
+        for (int64_t i = 0; i < n_events; ++i) {
+            const int64_t u = us[i], v = vs[i];
+            GD_CHECK_ARG(u >= 0 && v >= 0 && u < G_new->n && v < G_new->n && u != v,
+                         "bad event endpoints");
+            const int32_t step = kinds[i] ? 1 : -1;
+            GD_CHECK_ARG(deg[u] + step >= 0 && deg[v] + step >= 0,
+                         "delete would make a degree negative");
+            ev[i] = PairEvent{(int32_t)u, (int32_t)v, deg[u], deg[v], step};
+            deg[u] += step;
+            deg[v] += step;
+        }
+        std::vector<int32_t> gdeg(G_new->n);
+        if (G_new->n)
+            GD_CUDA(cudaMemcpy(gdeg.data(), G_new->deg.p, 4 * G_new->n, cudaMemcpyDeviceToHost));
+        GD_CHECK_ARG(gdeg == deg, "G_new is not the old graph with these events applied");
+        P->dev_events.ensure(n_events ? n_events : 1);
+        if (n_events)
+            GD_CUDA(cudaMemcpy(P->dev_events.p, ev.data(), sizeof(PairEvent) * n_events,
+                               cudaMemcpyHostToDevice));
+        pairs_repair(P, G_new, !P->all_converged, max_sweeps > 0 ? max_sweeps : 1000000,
+                     P->dev_events.p, n_events, sweeps, total_ops, pushes, converged);
+        P->deg.swap(deg);
+    });
+}
+
+// Dense copies of pair i (p, r: n doubles each; either may be NULL).
+int gd_pairs_get(const gd_pairs *P, int64_t i, double *p, double *r) {
+    return guarded([&] {
+        GD_CHECK_ARG(P, "null pointer");
+        GD_CHECK_ARG(i >= 0 && i < P->k, "pair index out of range");
+        const size_t n = P->deg.size();
+        if (p) GD_CUDA(cudaMemcpy(p, P->S.x.p + i * P->S.ld, 8 * n, cudaMemcpyDeviceToHost));
+        if (r) GD_CUDA(cudaMemcpy(r, P->S.r.p + i * P->S.ld, 8 * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+// Device view of the pool: pair i's p at p[i * ld], r at r[i * ld].
+int gd_pairs_device(const gd_pairs *P, double **p, double **r, int64_t *ld) {
+    if (!P || !p || !r || !ld) return GD_ERR_ARG;
+    *p = P->S.x.p;
+    *r = P->S.r.p;
+    *ld = P->S.ld;
+    return GD_OK;
+}
+
+int gd_pairs_last_kernel_ms(const gd_pairs *P, double *ms) {
+    if (!P || !ms) return GD_ERR_ARG;
+    *ms = P->last_ms;
+    return GD_OK;
+}
+
+}  // extern "C"

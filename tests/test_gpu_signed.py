@@ -1,0 +1,183 @@
+"""Batched signed solvers on the GPU: LocalCH (PPR / Katz) seed batches and
+the resident pair pool (warm-started signed LocalGD after edge events)
+against the reference's golden vectors and the CPU oracle.  Integer work
+(sweeps, operation counts, convergence / divergence) is identical per seed;
+x, p, r agree within 1e-9 relative l1 (the atomic scatter only changes the
+summation order)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_graph, load_golden
+from helpers import build_system, local_cases, param
+from oracle import oracle as O
+from paper_2410_21634_b200 import systems as S
+from paper_2410_21634_b200.batch import BatchSolver, local_ch_batch
+from paper_2410_21634_b200.metrics import sample_sources
+from paper_2410_21634_b200.synth import rmat_graph
+
+pytestmark = pytest.mark.gpu
+X_RTOL = 1e-9
+
+
+def _close(a, ref, rtol=X_RTOL):
+    return np.abs(a - ref).sum() <= rtol * max(np.abs(ref).sum(), 1e-300)
+
+
+def _check_seed(out, i, x_ref, n):
+    x = out.x_dense(i, n)
+    nodes, _ = out.x_sparse(i)
+    assert len(np.unique(nodes)) == len(nodes)
+    assert set(np.flatnonzero(x_ref).tolist()) <= set(nodes.tolist())
+    assert _close(x, x_ref)
+
+
+@pytest.mark.parametrize("slots", [0, 1, 3])
+def test_ch_batch_matches_reference_pa(gpu, pa, slots):
+    g = golden_graph(pa, "pa2000")
+    keys = [k for k in local_cases(pa) if k.endswith("/local_ch")]
+    seeds = np.array([int(param(pa, k, "source")) for k in keys])
+    out = local_ch_batch(g, seeds, 0.1, 1e-6, slots=slots)
+    for i, k in enumerate(keys):
+        assert out.sweeps[i] == pa[f"{k}/sweeps"] and out.total_ops[i] == pa[f"{k}/total_ops"]
+        assert out.converged[i] == bool(pa[f"{k}/converged"])
+        _check_seed(out, i, pa[f"{k}/x"], g.n)
+
+
+@pytest.mark.parametrize("key", ["er500/ppr/local_ch", "er60/ppr/local_ch", "er60/katz/local_ch"])
+def test_ch_batch_matches_reference_small(gpu, small, key):
+    sys_ = build_system(small, key)
+    g = sys_.graph
+    prob = str(param(small, key, "problem"))
+    mu, L = param(small, key, "mu"), param(small, key, "L")
+    for relabel in (True, False):
+        out = local_ch_batch(g, [sys_.source], sys_.alpha, sys_.eps, problem=prob, mu=mu, L=L,
+                             relabel=relabel)
+        assert out.sweeps[0] == small[f"{key}/sweeps"]
+        assert out.total_ops[0] == small[f"{key}/total_ops"]
+        assert out.converged[0] == bool(small[f"{key}/converged"])
+        _check_seed(out, 0, small[f"{key}/x"], g.n)
+
+
+@pytest.mark.parametrize("problem", ["ppr", "katz"])
+def test_ch_batch_rmat_matches_oracle(gpu, problem):
+    from paper_2410_21634_b200.graph import spectral_norm_estimate
+    g = rmat_graph(20000, 150000, seed=5)
+    seeds = sample_sources(g, 40, seed=2)
+    if problem == "ppr":
+        alpha, eps, lam = 0.1, 1e-6, None
+        mk = lambda s: S.make_ppr_system(g, alpha, s, eps)
+    else:
+        lam = spectral_norm_estimate(g, iters=200, seed=0)
+        alpha, eps = 1.0 / (lam + 1.0), 1e-6
+        mk = lambda s: S.make_katz_system(g, alpha, s, eps, lam_hat=lam)
+    out = local_ch_batch(g, seeds, alpha, eps, problem=problem, lam_hat=lam, slots=16)
+    for i, s in enumerate(seeds):
+        ref = O.local_ch(mk(int(s)), record_trace=False) if problem == "ppr" else \
+            O.local_ch(mk(int(s)), *_katz_bounds(g, alpha, lam), record_trace=False)
+        assert out.sweeps[i] == ref["sweeps"] and out.total_ops[i] == ref["total_ops"], i
+        assert out.converged[i] == bool(ref["converged"])
+        _check_seed(out, i, ref["x"], g.n)
+
+
+def _katz_bounds(g, alpha, lam):
+    lam = min(max(lam, 1e-12), float(g.d_max))
+    return 1.0 - alpha * lam, 1.0 + alpha * lam
+
+
+def test_ch_batch_divergence_and_sweep_cap(gpu):
+    """Bad bounds make LocalCH diverge (abort at l1 > 10 ||b||_1); a sweep cap
+    stops unconverged -- both per seed exactly as the reference."""
+    g = rmat_graph(5000, 30000, seed=3)
+    seeds = sample_sources(g, 12, seed=4)
+    solver = BatchSolver(g, 0.1, 1e-6, slots=5, method="local-ch", mu=0.6, L=0.7,
+                         max_sweeps=400)
+    out = solver.solve(seeds)
+    diverged = 0
+    for i, s in enumerate(seeds):
+        ref = O.local_ch(S.make_ppr_system(g, 0.1, int(s), 1e-6), mu=0.6, L=0.7, max_sweeps=400,
+                         record_trace=False)
+        assert out.sweeps[i] == ref["sweeps"] and out.total_ops[i] == ref["total_ops"]
+        assert out.converged[i] == bool(ref["converged"])
+        diverged += int(ref["diverged"])
+    assert diverged > 0
+    capped = local_ch_batch(g, seeds, 0.1, 1e-6, max_sweeps=4)
+    assert (capped.sweeps == 4).all() and not capped.converged.any()
+    solver.close()
+
+
+def test_ch_batch_solver_reuse(gpu):
+    g = rmat_graph(5000, 30000, seed=9)
+    seeds = sample_sources(g, 30, seed=1)
+    solver = BatchSolver(g, 0.15, 1e-5, slots=8, method="local-ch", max_sweeps=2000)
+    a = solver.solve(seeds)
+    a = {k: np.array(getattr(a, k)) for k in ("sweeps", "total_ops", "pushes")}
+    b = solver.solve(seeds[::-1].copy())
+    assert np.array_equal(b.total_ops[::-1], a["total_ops"])
+    assert np.array_equal(b.sweeps[::-1], a["sweeps"])
+    solver.close()
+
+
+# ---- resident pair pool (config 5, batched) --------------------------------
+
+def _warm_ref(g, p, r, alpha, eps):
+    w = S.arc_weights_for(g, 1.0 - alpha, "gen", 0.0)
+    th = S.theta_vector(g, eps)
+    return O.local_gd_warm(g.offsets, g.targets, w, th, p, r, signed=True, record_trace=False)
+
+
+def _pool_against_oracle(g, batches, sources, alpha, eps):
+    from paper_2410_21634_b200.dynamic import PairPool, event_adjust_many
+    from paper_2410_21634_b200.graph import apply_events
+    pool = PairPool(g, sources, alpha, eps)
+    n = g.n
+    for i, s in enumerate(sources):
+        p, r = np.zeros(n), np.zeros(n)
+        r[s] = alpha
+        ref = _warm_ref(g, p, r, alpha, eps)
+        assert pool.last["sweeps"][i] == ref["sweeps"] and pool.last["total_ops"][i] == ref["total_ops"]
+        got = pool.pair(i)
+        assert _close(got.p, p) and _close(got.r, r)
+    for batch in batches:
+        before = [pool.pair(i) for i in range(len(sources))]
+        st = pool.update(batch)
+        g2 = apply_events(g, batch)
+        for i in range(len(sources)):
+            adj = event_adjust_many(g, before[i], batch)
+            p, r = adj.p.copy(), adj.r.copy()
+            ref = _warm_ref(g2, p, r, alpha, eps)
+            assert st["sweeps"][i] == ref["sweeps"] and st["total_ops"][i] == ref["total_ops"]
+            assert st["converged"][i] == int(ref["converged"])
+            got = pool.pair(i)
+            assert _close(got.p, p) and _close(got.r, r, rtol=1e-7)
+            assert np.abs(got.consistency_residual(g2)).max() <= 1e-9
+        g = g2
+    pool.close()
+
+
+def test_pair_pool_dynamic_fixture(gpu, dyn):
+    from paper_2410_21634_b200.graph import EdgeEvent
+    g = golden_graph(dyn, "er120")
+    ev = dyn["events"]
+    batches = [[EdgeEvent("insert" if k else "delete", int(u), int(v)) for b, k, u, v in ev if b == bi]
+               for bi in range(int(ev[:, 0].max()) + 1)]
+    sources = [int(s) for s in np.flatnonzero(g.degrees > 0)[:9]]
+    _pool_against_oracle(g, batches, sources, 0.2, 0.2 * 1e-4)
+
+
+def test_pair_pool_rmat_stream(gpu):
+    from paper_2410_21634_b200.graph import EdgeEvent, apply_events
+    g = rmat_graph(6000, 40000, seed=11)
+    rng = np.random.default_rng(0)
+    batches, sim = [], g
+    for _ in range(4):
+        b = []
+        for _ in range(60):
+            u, v = sorted(rng.choice(g.n, 2, replace=False).tolist())
+            if any((e.u, e.v) == (u, v) for e in b):
+                continue
+            b.append(EdgeEvent("delete" if sim.has_edge(u, v) else "insert", u, v))
+        sim = apply_events(sim, b)
+        batches.append(b)
+    sources = sample_sources(g, 24, seed=3).tolist()
+    _pool_against_oracle(g, batches, sources, 0.15, 1e-5)
