@@ -650,8 +650,9 @@ typedef struct {
     const int64_t *off, *tgt;
     const double *w, *theta;
     double alpha;
-    int32_t method;  /* 0 local_gd, 1 local_sor */
+    int32_t method;  /* 0 local_gd, 1 local_sor, 2 local_ch */
     double omega;
+    double mu, L;    /* local_ch bounds */
     const int64_t *seeds;
     int64_t n_seeds, max_sweeps;
     int64_t *out_sweeps, *out_ops, *out_pushes;
@@ -684,6 +685,11 @@ static void *batch_worker(void *arg) {
             orc_push_kernel(n, J->off, J->tgt, J->w, J->theta, x, r, &sd, 1, J->omega, 1.0,
                             J->omega > 1.0, J->max_sweeps, &rep);
             pushes = -1;
+        } else if (J->method == 2) {
+            /* local_ch (src/local_solvers.py:473-538) on b = bval e_s */
+            orc_local_ch(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->mu, J->L, J->max_sweeps,
+                         0, &rep);
+            pushes = -1;
         } else {
             orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
             for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
@@ -704,12 +710,32 @@ int orc_batch_local(int64_t n, const int64_t *off, const int64_t *tgt, const dou
                     const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
                     int64_t *out_sweeps, int64_t *out_ops, int64_t *out_pushes,
                     int32_t *out_conv, double *out_xsum) {
-    batch_job J = {n, off, tgt, w, theta, alpha, method, omega, seeds, n_seeds, max_sweeps,
-                   out_sweeps, out_ops, out_pushes, out_conv, out_xsum, 0};
+    batch_job J = {n, off, tgt, w, theta, alpha, method, omega, 0.0, 0.0, seeds, n_seeds,
+                   max_sweeps, out_sweeps, out_ops, out_pushes, out_conv, out_xsum, 0};
     if (n_threads < 1) n_threads = 1;
     pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
     for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, batch_worker, &J);
     for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
     free(th);
+    return 0;
+}
+
+/* Per-seed local_ch over many threads: b = bval e_s (alpha for PPR, 1 for
+ * Katz), operator given by the arc weights / thresholds. */
+int orc_batch_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                       const double *theta, double bval, double mu, double L,
+                       const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps,
+                       int32_t n_threads, int64_t *out_sweeps, int64_t *out_ops,
+                       int32_t *out_conv, double *out_xsum) {
+    batch_job J = {n, off, tgt, w, theta, bval, 2, 1.0, mu, L, seeds, n_seeds, max_sweeps,
+                   out_sweeps, out_ops, NULL, out_conv, out_xsum, 0};
+    int64_t *pushes = malloc(sizeof(int64_t) * (n_seeds ? n_seeds : 1));
+    J.out_pushes = pushes;
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, batch_worker, &J);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+    free(pushes);
     return 0;
 }

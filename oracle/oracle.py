@@ -237,6 +237,32 @@ def batch_local_gd(g, alpha: float, eps: float, seeds, threads: int,
     return {"sweeps": sw, "total_ops": ops, "pushes": pu, "converged": cv.astype(bool), "xsum": xs}
 
 
+def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, L: float,
+                   problem: str = "ppr", max_sweeps: int | None = None) -> dict:
+    """Per-seed reference local_ch over many host threads (CPU baseline of
+    the LocalCH batch): PPR (b = alpha e_s) or Katz (b = e_s, w = alpha)."""
+    from paper_2410_21634_b200.systems import arc_weights_for, theta_vector
+    if max_sweeps is None:
+        gap = max(mu, 1e-12)
+        max_sweeps = max(1000, int(10 * math.log(max(1.0 / max(eps, 1e-300), 2.0)) / gap))
+    off, tg = _arr64(g.offsets), _arr64(g.targets)
+    if problem == "ppr":
+        w, th, bval = arc_weights_for(g, 1.0 - alpha, "rw"), theta_vector(g, eps * alpha), alpha
+    else:
+        w, th, bval = np.full(tg.shape[0], float(alpha)), theta_vector(g, eps), 1.0
+    w, th = _arrf(w), _arrf(th)
+    sd = _arr64(seeds)
+    k = sd.shape[0]
+    sw, ops = np.zeros(k, np.int64), np.zeros(k, np.int64)
+    cv = np.zeros(k, np.int32)
+    xs = np.zeros(k)
+    lib().orc_batch_local_ch(C.c_int64(g.n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th),
+                             C.c_double(bval), C.c_double(mu), C.c_double(L), _p(sd, C.c_int64),
+                             C.c_int64(k), C.c_int64(max_sweeps), C.c_int32(threads),
+                             _p(sw, C.c_int64), _p(ops, C.c_int64), _p(cv, C.c_int32), _p(xs))
+    return {"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "xsum": xs}
+
+
 def pairwise_sum(a, take_abs: bool = False) -> float:
     a = _arrf(a)
     return float(lib().orc_pairwise_sum(_p(a), C.c_int64(a.shape[0]), C.c_int32(int(take_abs))))

@@ -108,3 +108,15 @@ def test_warm_gd_restatement_is_the_reference_sweep_loop(small):
     assert np.array_equal(x, small[f"{k}/x"]) and np.array_equal(r, small[f"{k}/r"])
     assert out["sweeps"] == small[f"{k}/sweeps"]
     assert np.array_equal(np.concatenate(out["frontier_trace"]), small[f"{k}/trace_flat"])
+
+
+def test_oracle_batch_local_ch_matches_reference(pa):
+    """Threaded LocalCH CPU baseline == the reference's per-seed local_ch."""
+    from helpers import local_cases, param
+    g = golden_graph(pa, "pa2000")
+    keys = [k for k in local_cases(pa) if k.endswith("/local_ch")]
+    seeds = [int(param(pa, k, "source")) for k in keys]
+    out = O.batch_local_ch(g, 0.1, 1e-6, seeds, threads=3, mu=0.1, L=1.9)
+    for i, k in enumerate(keys):
+        assert out["sweeps"][i] == pa[f"{k}/sweeps"] and out["total_ops"][i] == pa[f"{k}/total_ops"]
+        assert out["xsum"][i] == O.pairwise_sum(pa[f"{k}/x"])
