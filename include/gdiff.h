@@ -93,6 +93,15 @@ int gd_graph_create(int64_t n, const int64_t *offsets, const int64_t *targets,
  * generated on the GPU; the data is copied. */
 int gd_graph_create_device(int64_t n, const int64_t *d_row_ptr, const int32_t *d_col,
                            int64_t n_arcs, int32_t device, gd_graph **out);
+/* A new graph: g with an ordered batch of undirected edge events applied
+ * (kinds[i] = 1 insert, 0 delete of (us[i], vs[i])), built on the device;
+ * the same canonical CSR as apply_events (src/graph.py:235-258).  Errors
+ * (GD_ERR_ARG) on an insert of a present / delete of a missing edge. */
+int gd_graph_apply_events(const gd_graph *g, const int32_t *kinds, const int64_t *us,
+                          const int64_t *vs, int64_t n_events, gd_graph **out);
+/* Copy a device graph back in the reference layout (int64 n+1 offsets,
+ * int64 n_arcs targets). */
+int gd_graph_export(const gd_graph *g, int64_t *offsets, int64_t *targets);
 int gd_graph_destroy(gd_graph *g);
 int gd_graph_info(const gd_graph *g, int64_t *n, int64_t *n_arcs, int64_t *d_max);
 

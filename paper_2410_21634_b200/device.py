@@ -46,6 +46,27 @@ class DeviceGraph:
         L.check(lib.gd_graph_info(h, C.byref(n), C.byref(a), C.byref(d)))
         return cls(h.value, n.value, a.value, d.value, device)
 
+    def apply_events(self, events) -> "DeviceGraph":
+        """New device graph with the event batch applied in order (on the
+        device; same CSR as graph.apply_events)."""
+        lib = L.load()
+        kinds = np.array([1 if e.kind == "insert" else 0 for e in events], np.int32)
+        us = np.array([e.u for e in events], np.int64)
+        vs = np.array([e.v for e in events], np.int64)
+        h = C.c_void_p()
+        L.check(lib.gd_graph_apply_events(self.handle, L.ptr(kinds, C.c_int32), L.ptr(us, C.c_int64),
+                                          L.ptr(vs, C.c_int64), len(events), C.byref(h)))
+        return DeviceGraph._wrap(h, self.device)
+
+    def to_host(self):
+        """The graph in the reference layout (CsrGraph)."""
+        from .graph import CsrGraph
+
+        off = np.empty(self.n + 1, np.int64)
+        tg = np.empty(self.n_arcs, np.int64)
+        L.check(L.load().gd_graph_export(self.handle, L.ptr(off, C.c_int64), L.ptr(tg, C.c_int64)))
+        return CsrGraph(n=self.n, offsets=off, targets=tg)
+
     def close(self):
         if self.handle and self.handle.value:
             L.load(require_gpu=False).gd_graph_destroy(self.handle)

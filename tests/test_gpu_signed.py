@@ -181,3 +181,37 @@ def test_pair_pool_rmat_stream(gpu):
         batches.append(b)
     sources = sample_sources(g, 24, seed=3).tolist()
     _pool_against_oracle(g, batches, sources, 0.15, 1e-5)
+
+
+def test_device_graph_edit_matches_host(gpu, small):
+    """gd_graph_apply_events == graph.apply_events (canonical CSR), including
+    repeated edits of one edge, deletes down to isolated nodes, and the
+    reference's errors on invalid events."""
+    from paper_2410_21634_b200.device import DeviceGraph
+    from paper_2410_21634_b200.graph import EdgeEvent, GraphStructureError, apply_events
+    from paper_2410_21634_b200._lib import GdiffError
+    rng = np.random.default_rng(7)
+    for g in (golden_graph(small, "er60"), rmat_graph(3000, 20000, seed=2)):
+        dg = DeviceGraph.from_host(g)
+        sim = g
+        for _ in range(3):
+            evs = []
+            for _ in range(300):
+                u, v = sorted(rng.choice(min(g.n, 80), 2, replace=False).tolist())
+                e = EdgeEvent("delete" if sim.has_edge(u, v) else "insert", u, v)
+                evs.append(e)
+                sim = apply_events(sim, [e])
+            host = apply_events(g, evs)
+            dn = dg.apply_events(evs)
+            back = dn.to_host()
+            assert np.array_equal(back.offsets, host.offsets)
+            assert np.array_equal(back.targets, host.targets)
+            assert dn.d_max == host.d_max and dn.n_arcs == host.targets.shape[0]
+            dg.close()
+            dg, g = dn, host
+        bad = [EdgeEvent("delete", 0, 1)] if not g.has_edge(0, 1) else [EdgeEvent("insert", 0, 1)]
+        with pytest.raises(GdiffError):
+            dg.apply_events(bad)
+        with pytest.raises(GraphStructureError):
+            apply_events(g, bad * 70)
+        dg.close()
