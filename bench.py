@@ -49,16 +49,18 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--graph-seed", type=int, default=0)
     p.add_argument("--no-relabel", action="store_true", help="run on the caller's node order")
-    p.add_argument("--method", default="local-gd", choices=["local-gd", "local-sor"])
+    p.add_argument("--method", default="local-gd", choices=["local-gd", "local-sor", "local-ch"])
     p.add_argument("--omega", type=float, default=1.0, help="local-sor relaxation")
+    p.add_argument("--problem", default="ppr", choices=["ppr", "katz"],
+                   help="local-ch: PPR, or Katz with alpha = 1/(lambda+1) (--alpha ignored)")
     return p.parse_args()
 
 
-def ncu_traffic():
+def ncu_traffic(kernel="k_rounds"):
     """DRAM bytes per launch of the sweep kernel from the committed ncu summary."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_k_rounds_*.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{kernel}_r*.json")))
     if not files:
         return None, None
     with open(files[-1]) as fh:
@@ -149,13 +151,55 @@ class _HostGraph:
         self.degrees = np.diff(offsets)
 
 
-def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0):
+def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, ch=None):
     from oracle import oracle as O
 
     t0 = time.perf_counter()
-    out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w, theta=hg.theta,
-                           method=method, omega=omega)
+    if method == "local-ch":
+        out = O.batch_local_ch(hg, alpha, eps, seeds, threads, ch["mu"], ch["L"],
+                               problem=ch["problem"], max_sweeps=ch["max_sweeps"])
+        out["pushes"] = np.zeros_like(out["total_ops"])
+    else:
+        out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w,
+                               theta=hg.theta, method=method, omega=omega)
     return out, time.perf_counter() - t0
+
+
+def spectral_radius(row, col, n, iters=100):
+    """lambda_max(A) by plain power iteration (torch CSR SpMV on the device).
+    Input synthesis for the Katz workload only: the reference's shifted
+    estimator (src/graph.py:267-295) does not converge in 200 iterations when
+    d_max is large, and a Katz alpha above 1/lambda diverges."""
+    import torch
+
+    import warnings
+
+    with warnings.catch_warnings():  # torch flags sparse CSR as beta
+        warnings.simplefilter("ignore")
+        A = torch.sparse_csr_tensor(row, col.to(torch.int64),
+                                    torch.ones(col.numel(), dtype=torch.float64, device=col.device),
+                                    size=(n, n))
+    x = torch.ones(n, dtype=torch.float64, device=col.device) / n ** 0.5
+    lam = 0.0
+    for _ in range(iters):
+        y = torch.mv(A, x)
+        lam = float(torch.dot(x, y))
+        x = y / torch.linalg.vector_norm(y)
+    return lam
+
+
+def ch_params(args, row, col, n):
+    """LocalCH bounds (the reference's cheby_bounds) and default sweep cap."""
+    import math
+
+    if args.problem == "ppr":
+        mu, L, lam = args.alpha, 2.0 - args.alpha, None
+    else:
+        lam = spectral_radius(row, col, n)
+        args.alpha = 1.0 / (lam + 1.0)  # default_katz_alpha (src/systems.py) with this lambda
+        mu, L = 1.0 - args.alpha * lam, 1.0 + args.alpha * lam
+    ms = max(1000, int(10 * math.log(max(1.0 / max(args.eps, 1e-300), 2.0)) / max(mu, 1e-12)))
+    return {"problem": args.problem, "mu": mu, "L": L, "max_sweeps": ms, "lambda": lam}
 
 
 def host_graph_full(n, row_h, col_t, alpha, eps):
@@ -163,6 +207,7 @@ def host_graph_full(n, row_h, col_t, alpha, eps):
     from paper_2410_21634_b200.systems import theta_vector
 
     hg = _HostGraph(n, row_h, col_t.cpu().numpy().astype(np.int64))
+    hg.d_max = int(hg.degrees.max()) if n else 0
     d = np.repeat(hg.degrees.astype(np.float64), hg.degrees)
     hg.arc_w = (1.0 / d) * (1.0 - alpha)  # == src/systems.py:85-108 for "rw"
     hg.theta = theta_vector(hg, eps * alpha)
@@ -181,6 +226,7 @@ def run_reference(args):
     n, m = SHAPES[args.shape]
     if torch.cuda.is_available():  # input synthesis only; the timed path is CPU
         _, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
+        args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
         hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
         del row, col
     else:
@@ -191,17 +237,21 @@ def run_reference(args):
         d = np.repeat(hg.degrees.astype(np.float64), hg.degrees)
         hg.arc_w = (1.0 / d) * (1.0 - args.alpha)
         hg.theta = theta_vector(hg, args.eps * args.alpha)
+        hg.d_max = int(hg.degrees.max()) if n else 0
+        args.ch = (ch_params(args, torch.as_tensor(g.offsets), torch.as_tensor(g.targets), n)
+                   if args.method == "local-ch" else None)
     steps_total = args.steps + args.warmup
     allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
     batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     # each step: a bounded prefix of that step's batch (about 3 s of CPU work)
     _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][:threads], threads, args.method,
-                          args.omega)
+                          args.omega, args.ch)
     per_step = int(min(args.seeds, max(threads, threads * 3.0 / max(dt, 1e-3))))
     times, ops, done = [], 0, 0
     for k in range(steps_total):
         sl = batches[k][:per_step]
-        out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega)
+        out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega,
+                                args.ch)
         if k >= args.warmup:
             times.append(dt)
             ops += int(out["total_ops"].sum())
@@ -217,7 +267,8 @@ def run_reference(args):
         "gteps": ops / tot / 1e9,
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
                          "sample": f"first {per_step} seeds of each step's sample_sources batch, "
-                                   "reference local_gd restated in C (oracle/), per-seed O(n) "
+                                   f"reference {args.method.replace('-', '_')} restated in C "
+                                   "(oracle/), per-seed O(n) "
                                    "state as in the reference, one seed per thread"},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -225,15 +276,18 @@ def run_reference(args):
 
 
 def workload_config(args, n, m):
-    name = "LocalGD" if args.method == "local-gd" else f"LocalSOR(omega={args.omega:g})"
-    return {"workload": f"batched {name}-PPR alpha={args.alpha} eps={args.eps:g}, "
+    name = {"local-gd": "LocalGD", "local-ch": "LocalCH",
+            "local-sor": f"LocalSOR(omega={args.omega:g})"}[args.method]
+    prob = "Katz" if args.method == "local-ch" and args.problem == "katz" else "PPR"
+    return {"workload": f"batched {name}-{prob} alpha={args.alpha:.6g} eps={args.eps:g}, "
                         f"R-MAT {args.shape}-shape ({n:,} nodes, {m:,} edges), "
                         f"{args.seeds} seeds/GPU/step from sample_sources",
             "graph": f"rmat-{args.shape}", "n": n, "edges": m, "alpha": args.alpha,
             "eps": args.eps, "seeds_per_gpu_per_step": args.seeds, "slots": args.slots,
             "l2": "inputs larger than L2 (int32 col_idx %.0f MB + per-seed state)" % (8.0 * m / 1e6),
             "parallelism": f"seed-sharded x{args.gpus}", "method": args.method,
-            "omega": args.omega if args.method == "local-sor" else None}
+            "omega": args.omega if args.method == "local-sor" else None,
+            "problem": prob.lower(), "chebyshev": getattr(args, "ch", None)}
 
 
 def main():
@@ -253,6 +307,7 @@ def main():
     n, m = SHAPES[args.shape]
     dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
     hdeg = _HostGraph(n, row_h)
+    args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
     if args.no_cpu_baseline:  # the CPU leg is the only later user of the torch copies
         del row, col
         col = None
@@ -264,8 +319,11 @@ def main():
     mine = shard_seeds(allseeds, rank, world)  # round-robin over the degree-ranked sample
     batches = [mine[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     dseeds = [torch.as_tensor(b, device="cuda") for b in batches]
+    ch = args.ch or {}
     solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots, relabel=not args.no_relabel,
-                         method=args.method, omega=args.omega)
+                         method=args.method, omega=args.omega, problem=ch.get("problem", "ppr"),
+                         mu=ch.get("mu"), L=ch.get("L"),
+                         max_sweeps=ch.get("max_sweeps", 1_000_000))
     stream = torch.cuda.current_stream()
 
     def gather(res):
@@ -314,7 +372,8 @@ def main():
     peak, peak_kind = peaks()
     my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic({"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
+                                        "local-sor": "k_fifo_batch"}[args.method])
     # e2e: the public host API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -347,7 +406,8 @@ def main():
         ref_sweeps, ref_ops = [], []
         while spent < args.cpu_seconds and pos < len(batches[args.warmup]):
             sl = batches[args.warmup][pos:pos + chunk]
-            o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega)
+            o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega,
+                                  args.ch)
             spent += dt
             sample.extend(sl.tolist())
             ref_sweeps.append(o["sweeps"])
@@ -357,8 +417,8 @@ def main():
         parity = bool(np.array_equal(np.concatenate(ref_ops), res.total_ops)
                       and np.array_equal(np.concatenate(ref_sweeps), res.sweeps))
         cpu = {"value": len(sample) / spent, "unit": "solves/s", "cores": threads, "kind": "port",
-               "sample": f"first {len(sample)} seeds of the first timed batch, reference local_gd "
-                         "restated in C (oracle/), one seed per thread",
+               "sample": f"first {len(sample)} seeds of the first timed batch, reference "
+                         f"{args.method.replace('-', '_')} restated in C (oracle/), one seed per thread",
                "parity_sweeps_ops_identical": parity}
     if rank == 0:
         line = {
@@ -370,9 +430,12 @@ def main():
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "b_alg_per_launch": my_balg / max(1, launches // 4 if args.method == "local-gd" else launches),
+                         "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // 4,
+                                                                "local-ch": launches // 5}.get(args.method, launches)),
                          "peak_kind": peak_kind,
-                         "kernel": "k_rounds (persistent sweep loop)" if args.method == "local-gd" else "k_fifo_batch (warp per seed)",
+                         "kernel": {"local-gd": "k_rounds (persistent sweep loop)",
+                                    "local-ch": "k_signed_rounds (persistent signed sweep loop)",
+                                    "local-sor": "k_fifo_batch (warp per seed)"}[args.method],
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "relabel": not args.no_relabel,

@@ -8,12 +8,14 @@
 // Per slot (one seed / pair): dense x, r (+ momentum value and stamp for
 // CH).  Residuals change sign, so the unsigned kernel's "exactly one arc
 // observes the threshold crossing" does not hold.  The frontier of round t
-// is instead filtered from CANDIDATES -- under momentum the previous
-// frontier (whose r is r - vals, not 0) plus every node that received a
-// contribution in round t-1 -- which is exactly the reference's candidate
-// set (_apply_update_seq + _filter_frontier with a signed test).  A per-slot
-// bit map per round parity deduplicates candidates: the old word returned by
-// one atomicOr says whether the node is new this round.
+// is instead filtered from CANDIDATES: under momentum the previous frontier
+// (whose r is r - vals, not 0), plus every node that received a
+// contribution in round t-1 AND saw |r| >= theta right after one of its
+// updates.  The reference filters every touched node (_apply_update_seq +
+// _filter_frontier, signed test); the two sets agree on the active nodes
+// because the last update of a node stores its final value.  A per-slot bit
+// map per round parity deduplicates candidates (the old word returned by
+// one atomicOr says whether the node is new this round).
 //
 // Round t:  phase A  candidates -> |r| >= theta ? push (x, r, momentum,
 //                    l1 delta) and stage (slot, node, c_u) : skip;
@@ -61,6 +63,7 @@ struct SArgs {
     int64_t smw;
     int64_t *cand[2];               // (slot << 32 | node)
     unsigned long long *candctr;    // [2]
+    const int2 *colp;               // (neighbour, degree) per arc
     int64_t *fkey, *farc, *frow;    // frontier of the current round
     double *fcval;
     int32_t *chunk_e;
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
             if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)SUNROLL);
             const int64_t cb = bc0 + (int64_t)__shfl_sync(SFULL, claim, 0);
             if (cb >= bc1) break;
-            int32_t k[SUNROLL], v[SUNROLL];
+            int32_t k[SUNROLL], v[SUNROLL], dv[SUNROLL];
             double c[SUNROLL], old[SUNROLL];
             bool valid[SUNROLL];
 #pragma unroll
@@ -401,10 +404,13 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 k[q] = 0;
                 v[q] = 0;
                 c[q] = 0.0;
+                dv[q] = 0;
                 if (valid[q]) {
                     k[q] = (int32_t)(A.fkey[me] >> 32);
                     c[q] = A.fcval[me];
-                    v[q] = A.g.col[A.frow[me] + (p - A.farc[me])];
+                    const int2 nd = A.colp[A.frow[me] + (p - A.farc[me])];
+                    v[q] = nd.x;
+                    dv[q] = nd.y;
                 }
             }
 #pragma unroll
@@ -412,15 +418,16 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
 #pragma unroll
             for (int q = 0; q < SUNROLL; q++) {
-                if (ch) {
-                    const double dl1 =
-                        valid[q] ? fabs(__dadd_rn(old[q], c[q])) - fabs(old[q]) : 0.0;
-                    slot_add_d(valid[q], k[q], dl1, S.l1);
-                }
+                // the value this atomic stored; the LAST update of a node in
+                // the round stores its final value, so a node active at the
+                // end of the round is marked by at least one of its updates
+                const double nv = __dadd_rn(old[q], c[q]);
+                if (ch) slot_add_d(valid[q], k[q], valid[q] ? fabs(nv) - fabs(old[q]) : 0.0, S.l1);
                 if (A.secmap && valid[q] && __double_as_longlong(old[q]) == 0)
                     atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7),
                              1u << ((v[q] >> 2) & 31));
-                const bool nw = cand_mark(valid[q], k[q], v[q], A, nxt);
+                const bool hot = valid[q] && fabs(nv) >= theta_of(A.op, v[q], dv[q]);
+                const bool nw = cand_mark(hot, k[q], v[q], A, nxt);
                 cand_stage(nw, k[q], v[q], S, A, nxt);
             }
         }
@@ -432,6 +439,14 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 S.l1[k] = 0.0;
             }
         grid.sync();
+    }
+}
+
+__global__ void k_s_pack_cols(DevGraph g, int2 *__restrict__ colp) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g.n_arcs;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = g.col[j];
+        colp[j] = make_int2(v, g.deg[v]);
     }
 }
 
@@ -632,6 +647,7 @@ struct SignedState {
     DBuf<int32_t> mstamp, pushed, chunk_e, s_last, s_conv, overflow;
     DBuf<uint32_t> cm0, cm1, secmap;
     DBuf<int64_t> cand0, cand1, fkey, farc, frow, slot_base;
+    DBuf<int2> colp;
     DBuf<unsigned long long> candctr, fctr, s_ops, s_pushes, pushed_cnt;
     bool dirty = false;  // an aborted run left marks behind: full clear next time
     size_t smem = 0;
@@ -682,6 +698,13 @@ struct SignedState {
         grid = per_sm * n_sms(device);
     }
 
+    // (neighbour, degree) per arc of the graph the next solves run on
+    void pack(const gd_graph *W, cudaStream_t st) {
+        colp.ensure(W->n_arcs ? W->n_arcs : 1);
+        if (W->n_arcs) k_s_pack_cols<<<4 * n_sms(device), 256, 0, st>>>(W->view(), colp.p);
+        GD_LAUNCH_CHECK();
+    }
+
     void set_ch(double mu, double L, int64_t max_sweeps_) {
         max_sweeps = max_sweeps_;
         step0 = 2.0 / (L + mu);
@@ -717,6 +740,7 @@ struct SignedState {
         A.cmark[0] = cm0.p; A.cmark[1] = cm1.p; A.cmw = cmw;
         A.secmap = secmap.p; A.smw = smw;
         A.cand[0] = cand0.p; A.cand[1] = cand1.p; A.candctr = candctr.p;
+        A.colp = colp.p;
         A.fkey = fkey.p; A.farc = farc.p; A.frow = frow.p; A.fcval = fcval.p;
         A.chunk_e = chunk_e.p; A.fctr = fctr.p;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_l1 = s_l1.p; A.s_b1 = s_b1.p;
@@ -759,6 +783,7 @@ SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, in
         int64_t fc = p.frontier_cap > 0 ? p.frontier_cap : (int64_t)slots * n;
         if (p.frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
         S->alloc(W, 1, slots, fc, true);
+        S->pack(W, 0);
         // operator: PPR  w = fl(1/d)(1-alpha), b = alpha e_s, theta = eps alpha d
         //           Katz w = alpha,            b = e_s,       theta = eps d
         S->op.wrule = p.problem == GD_P_KATZ ? GD_W_CONST : GD_W_RW;
@@ -862,6 +887,7 @@ static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_
         scan = true;
     }
     S.max_sweeps = max_sweeps;
+    S.pack(G, st);  // the graph changes per snapshot
     SArgs A = S.args(G, P->k);
     GD_CUDA(cudaMemsetAsync(S.overflow.p, 0, sizeof(int32_t), st));
     GD_CUDA(cudaMemsetAsync(S.candctr.p, 0, 2 * sizeof(unsigned long long), st));
