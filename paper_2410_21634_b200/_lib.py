@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgdiff.so")
+LIB_PATH = os.environ.get("GDIFF_LIB") or os.path.join(HERE, "libgdiff.so")  # override: A/B experiments
 
 GD_OK, GD_ERR_ARG, GD_ERR_CUDA, GD_ERR_OOM, GD_ERR_CAPACITY, GD_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GD_W_RW, GD_W_CONST, GD_W_ARC = 0, 1, 2

@@ -85,7 +85,11 @@ struct RoundArgs {
     int32_t *pushed;
     int32_t *seed;  // per slot: seed in working ids
     unsigned long long *touched, *pushed_cnt;
-    int64_t *fkey[2], *farc[2];
+    int64_t *ukey;        // next frontier as appended: (slot << 32 | node), any order
+    int64_t *skey, *sarc; // current frontier grouped by slot: key, first arc offset
+    unsigned long long *scnt[2];  // per slot, per round parity: packed (entries << 36 | arcs)
+    unsigned long long *sfill;    // per slot fill of the grouped frontier (phase A)
+    unsigned long long *cctr;     // phase-B chunk claim counter
     int64_t *frow;
     double *fcval;
     const int2 *colp;     // per arc (neighbour, its degree): one 8 B load gives theta
@@ -164,12 +168,9 @@ __device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v,
     old = __shfl_sync(FULL, old, 0);
     if (flag) {
         int64_t idx = (int64_t)(old >> CNT_SHIFT) + __popc(am & lanemask_lt());
-        if (idx < A.fcap) {
-            A.fkey[nxt][idx] = ((int64_t)k << 32) | (uint32_t)v;
-            A.farc[nxt][idx] = (int64_t)(old & ARC_MASK) + (int64_t)(incl - (unsigned long long)d);
-        } else {
-            A.overflow[0] = 1;
-        }
+        if (idx < A.fcap) A.ukey[idx] = ((int64_t)k << 32) | (uint32_t)v;
+        else A.overflow[0] = 1;
+        atomicAdd(A.scnt[nxt] + k, (1ULL << CNT_SHIFT) + (unsigned long long)d);
     }
 }
 
@@ -181,6 +182,8 @@ constexpr int STAGE_CAP = 3072;  // staged frontier entries per block per round
 
 struct Stage {
     unsigned long long *ops, *pvol;      // [S]
+    unsigned long long *scnt;            // [S] packed entries/arcs staged for the next round
+    unsigned long long *sbase;           // [S] slot offsets of the grouped frontier
     unsigned *push, *touch, *negz;       // [S]
     int32_t *fk, *fv, *fd;               // [STAGE_CAP]
     unsigned *fcnt;                      // [1]
@@ -189,7 +192,8 @@ struct Stage {
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 3) + 64;
+    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 3) +
+           64;
 }
 
 __device__ Stage stage_carve(void *base, int S) {
@@ -197,6 +201,8 @@ __device__ Stage stage_carve(void *base, int S) {
     Stage st;
     st.ops = (unsigned long long *)p; p += 8 * S;
     st.pvol = (unsigned long long *)p; p += 8 * S;
+    st.scnt = (unsigned long long *)p; p += 8 * S;
+    st.sbase = (unsigned long long *)p; p += 8 * S;
     st.scan = (unsigned long long *)p; p += 8 * (BT / 32 + 2);
     st.next = (unsigned long long *)p; p += 8;
     st.push = (unsigned *)p; p += 4 * S;
@@ -241,7 +247,8 @@ __device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, in
 }
 
 // Block-wide: move the staged entries to the global next frontier with ONE
-// reservation (entries and arc range), arc offsets by a block scan.
+// reservation (entries and the arc total), and add the block's per-slot
+// entry / arc counts (the next round groups the frontier by slot).
 __device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
     __syncthreads();
     const unsigned cnt = min(*S.fcnt, (unsigned)STAGE_CAP);
@@ -249,7 +256,46 @@ __device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
     const unsigned per = (cnt + BT - 1) / BT;
     const unsigned lo = min(cnt, tid * per), hi = min(cnt, lo + per);
     unsigned long long mine = 0;
-    for (unsigned i = lo; i < hi; i++) mine += (unsigned long long)S.fd[i];
+    for (unsigned i = lo; i < hi; i++) {
+        mine += (unsigned long long)S.fd[i];
+        atomicAdd(S.scnt + S.fk[i], (1ULL << CNT_SHIFT) + (unsigned long long)S.fd[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FULL, mine, o);
+    if (lane == 0) S.scan[w] = mine;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < BT / 32; i++) run += S.scan[i];
+        unsigned long long old = 0;
+        if (cnt) old = atomicAdd(A.fctr + nxt, ((unsigned long long)cnt << CNT_SHIFT) + run);
+        S.scan[BT / 32] = old;
+    }
+    __syncthreads();
+    const int64_t ebase = (int64_t)(S.scan[BT / 32] >> CNT_SHIFT);
+    for (unsigned i = lo; i < hi; i++) {
+        const int64_t idx = ebase + i;
+        if (idx < A.fcap) A.ukey[idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
+        else A.overflow[0] = 1;
+    }
+    for (int64_t k = tid; k < A.m; k += BT) {
+        const unsigned long long v = S.scnt[k];
+        if (v) {
+            atomicAdd(A.scnt[nxt] + k, v);
+            S.scnt[k] = 0;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *S.fcnt = 0;
+}
+
+// S.sbase[k] = sum over j < k of A.scnt[cur][j] (packed: entries and arcs
+// together), computed by every block for itself.
+__device__ void slot_bases(const Stage &S, const RoundArgs &A, int cur) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t per = (A.m + BT - 1) / BT;
+    const int64_t lo = min(A.m, tid * per), hi = min(A.m, lo + per);
+    unsigned long long mine = 0;
+    for (int64_t k = lo; k < hi; k++) mine += A.scnt[cur][k];
     unsigned long long incl = mine;
     for (int o = 1; o < 32; o <<= 1) {
         unsigned long long y = __shfl_up_sync(FULL, incl, o);
@@ -264,26 +310,14 @@ __device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
             S.scan[i] = run;
             run += x;
         }
-        unsigned long long old = 0;
-        if (cnt) old = atomicAdd(A.fctr + nxt, ((unsigned long long)cnt << CNT_SHIFT) + run);
-        S.scan[BT / 32] = old;
     }
     __syncthreads();
-    const unsigned long long old = S.scan[BT / 32];
-    int64_t arc = (int64_t)(old & ARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
-    const int64_t ebase = (int64_t)(old >> CNT_SHIFT);
-    for (unsigned i = lo; i < hi; i++) {
-        const int64_t idx = ebase + i;
-        if (idx < A.fcap) {
-            A.fkey[nxt][idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
-            A.farc[nxt][idx] = arc;
-        } else {
-            A.overflow[0] = 1;
-        }
-        arc += S.fd[i];
+    unsigned long long b = S.scan[w] + incl - mine;
+    for (int64_t k = lo; k < hi; k++) {
+        S.sbase[k] = b;
+        b += A.scnt[cur][k];
     }
     __syncthreads();
-    if (tid == 0) *S.fcnt = 0;
 }
 
 template <class T>
@@ -305,7 +339,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
     for (int64_t k = threadIdx.x; k < A.m; k += BT) {
-        S.ops[k] = S.pvol[k] = 0;
+        S.ops[k] = S.pvol[k] = S.scnt[k] = 0;
         S.push[k] = S.touch[k] = S.negz[k] = 0;
     }
     if (threadIdx.x == 0) {
@@ -332,51 +366,62 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         }
         if (t >= A.max_sweeps || F > A.fcap) {
             for (int64_t e = gtid; e < F && e < A.fcap; e += nthreads)
-                A.s_conv[A.fkey[cur][e] >> 32] = 0;
+                A.s_conv[A.ukey[e] >> 32] = 0;
             break;
         }
         // ---------------- phase A: push the frontier entries ----------------
-        if (gtid == 0) A.fctr[nxt] = 0ULL;
-        const int64_t *fk = A.fkey[cur];
-        const int64_t *fa_cur = A.farc[cur];
+        // Entries arrive in append order; each is also placed into a copy of
+        // the frontier grouped by slot (per-slot packed reservation gives its
+        // position and first arc), so phase B walks the arcs slot by slot and
+        // the residual words it updates at any moment belong to a few slots
+        // (an L2-sized working set instead of all slots' vectors).
+        if (gtid == 0) {
+            A.fctr[nxt] = 0ULL;
+            A.cctr[0] = 0ULL;
+        }
+        for (int64_t k = gtid; k < A.m; k += nthreads) A.scnt[nxt][k] = 0ULL;
+        slot_bases(S, A, cur);
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
             const int64_t e = e0 + lane;
             const bool live = e < F;
             int32_t k = 0, u = 0, d = 0;
             bool fresh = false;
+            int64_t clo = 0, chi = 0, pos = 0;
             if (live) {
-                int64_t key = fk[e];
+                const int64_t key = A.ukey[e];
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
-                int64_t idx = (int64_t)k * A.ld + u;
-                double val = A.r[idx];
-                double xo = A.x[idx];
+                const int64_t idx = (int64_t)k * A.ld + u;
+                const double val = A.r[idx];
+                const double xo = A.x[idx];
                 A.x[idx] = __dadd_rn(xo, val);
                 A.r[idx] = -0.0;
                 d = A.g.deg[u];
-                A.frow[e] = A.g.row[u];
-                A.fcval[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                const unsigned long long b =
+                    S.sbase[k] + atomicAdd(A.sfill + k, (1ULL << CNT_SHIFT) + (unsigned long long)d);
+                pos = (int64_t)(b >> CNT_SHIFT);
+                const int64_t a0 = (int64_t)(b & ARC_MASK);
+                A.skey[pos] = key;
+                A.sarc[pos] = a0;
+                A.frow[pos] = A.g.row[u];
+                A.fcval[pos] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 fresh = __double_as_longlong(xo) == 0;  // first push of u
-            }
-            // chunks (32 arcs) whose first arc lies in entry e: [clo, chi).
-            // Hubs own thousands of chunks, so the warp writes them together.
-            int64_t clo = 0, chi = 0;
-            if (live) {
-                const int64_t a0 = fa_cur[e], a1 = e + 1 < F ? fa_cur[e + 1] : P;
+                // chunks (32 arcs) whose first arc lies in this entry: [clo, chi)
                 clo = (a0 + 31) >> 5;
-                chi = min((a1 + 31) >> 5, A.ccap);
+                chi = min((a0 + d + 31) >> 5, A.ccap);
             }
+            // hubs own thousands of chunks, so the warp writes them together
             unsigned big = __ballot_sync(FULL, chi - clo > 4);
             if (!(big >> lane & 1u))
-                for (int64_t c = clo; c < chi; ++c) A.chunk_e[c] = (int32_t)e;
+                for (int64_t c = clo; c < chi; ++c) A.chunk_e[c] = (int32_t)pos;
             while (big) {
                 const int src = __ffs(big) - 1;
                 big &= big - 1;
                 const int64_t lo2 = __shfl_sync(FULL, clo, src), hi2 = __shfl_sync(FULL, chi, src);
-                const int32_t e2 = (int32_t)__shfl_sync(FULL, e, src);
+                const int32_t e2 = (int32_t)__shfl_sync(FULL, pos, src);
                 for (int64_t c = lo2 + lane; c < hi2; c += 32) A.chunk_e[c] = e2;
             }
-            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
+        slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
             block_count(live, k, (unsigned)d, S.ops);
             block_count(live, k, 1u, S.push);
@@ -388,20 +433,17 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         counters_flush(S.push, A.s_pushes, A.m);
         grid.sync();
         // ---------------- phase B: arc-balanced scatter ----------------------
-        // chunk c = arcs [32c, 32c+32); every warp owns a contiguous chunk range
-        // and keeps UNROLL independent chunks (each lane one atomic) in flight.
+        // chunk c = arcs [32c, 32c+32) of the slot-grouped frontier.  Warp w
+        // takes chunk groups w, w + W, w + 2W, ... (UNROLL chunks, each lane
+        // one atomic in flight per chunk), so the whole grid sweeps the arc
+        // space front to back, slot by slot, without a claim counter.
+        for (int64_t k = gtid; k < A.m; k += nthreads) A.sfill[k] = 0ULL;  // for the next round
         const int64_t C = (P + 31) >> 5;
-        // static split across blocks, dynamic (shared counter) across the
-        // block's warps: latency variation between warps evens out
-        const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
-        const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
-        const int64_t *fa = A.farc[cur];
-        for (;;) {
-            unsigned long long claim = 0;
-            if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)UNROLL);
-            const int64_t cb = bc0 + (int64_t)__shfl_sync(FULL, claim, 0);
-            if (cb >= bc1) break;
-            const int64_t c1 = bc1;
+        const int64_t *fa = A.sarc;
+        const int64_t wid = gtid >> 5, nwarps = nthreads >> 5;
+        {
+            const int64_t c1 = C;
+          for (int64_t cb = wid * UNROLL; cb < c1; cb += nwarps * UNROLL) {
             int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
             double c[UNROLL], old[UNROLL];
             bool valid[UNROLL];
@@ -423,7 +465,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 valid[q] = live && p < P;
                 k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
                 if (valid[q]) {
-                    k[q] = (int32_t)(A.fkey[cur][me] >> 32);
+                    k[q] = (int32_t)(A.skey[me] >> 32);
                     c[q] = A.fcval[me];
                     const int2 vd = __ldg(A.colp + A.frow[me] + (p - fa[me]));
                     v[q] = vd.x;
@@ -448,9 +490,9 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 block_count(negz, k[q], 1u, S.negz);
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
+          }
         }
-        stage_flush(S, A, nxt);  // (its barriers also order the chunk counter reset)
-        if (threadIdx.x == 0) *S.next = 0;
+        stage_flush(S, A, nxt);
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
@@ -479,13 +521,14 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
     int32_t d = A.g.deg[s];
+    A.scnt[0][k] = 0ULL;
+    A.scnt[1][k] = 0ULL;
+    A.sfill[k] = 0ULL;
     if (alpha >= theta_deg(A.tcoeff, d)) {
         unsigned long long old = atomicAdd(A.fctr, (1ULL << CNT_SHIFT) + (unsigned long long)d);
         int64_t idx = (int64_t)(old >> CNT_SHIFT);
-        if (idx < A.fcap) {
-            A.fkey[0][idx] = (k << 32) | (uint32_t)s;
-            A.farc[0][idx] = (int64_t)(old & ARC_MASK);
-        }
+        if (idx < A.fcap) A.ukey[idx] = (k << 32) | (uint32_t)s;
+        A.scnt[0][k] = (1ULL << CNT_SHIFT) + (unsigned long long)d;
     }
 }
 
@@ -616,7 +659,8 @@ struct gd_batch {
     DBuf<double> x, r, fcval;
     DBuf<int32_t> pushed, seed, s_last, s_conv, overflow;
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
-    DBuf<int64_t> fkey0, fkey1, farc0, farc1, frow, slot_base;
+    DBuf<int64_t> ukey, skey, sarc, frow, slot_base;
+    DBuf<unsigned long long> scnt, sfill, cctr;
     DBuf<int32_t> chunk_e;
     DBuf<int2> colp;
     int64_t ccap = 0;
@@ -647,7 +691,8 @@ struct gd_batch {
         A.fcap = fcap;
         A.x = x.p; A.r = r.p; A.pushed = pushed.p; A.seed = seed.p;
         A.touched = touched.p; A.pushed_cnt = pushed_cnt.p;
-        A.fkey[0] = fkey0.p; A.fkey[1] = fkey1.p; A.farc[0] = farc0.p; A.farc[1] = farc1.p;
+        A.ukey = ukey.p; A.skey = skey.p; A.sarc = sarc.p;
+        A.scnt[0] = scnt.p; A.scnt[1] = scnt.p + slots; A.sfill = sfill.p; A.cctr = cctr.p;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
         A.chunk_e = chunk_e.p; A.ccap = ccap;
         A.colp = colp.p;
@@ -918,7 +963,8 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
             B->slot_base.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
-            B->fkey0.alloc(fc); B->fkey1.alloc(fc); B->farc0.alloc(fc); B->farc1.alloc(fc);
+            B->ukey.alloc(fc); B->skey.alloc(fc); B->sarc.alloc(fc);
+            B->scnt.alloc(2 * (size_t)slots); B->sfill.alloc(slots); B->cctr.alloc(1);
             B->frow.alloc(fc); B->fcval.alloc(fc);
             B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
             B->chunk_e.alloc(B->ccap);
