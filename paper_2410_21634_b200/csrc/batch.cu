@@ -8,9 +8,10 @@
 //
 // Design (B200):
 //  * `slots` seeds run concurrently, each with dense x/r vectors in HBM
-//    (slot-major).  Between waves they are reset either by walking the rows
-//    of the pushed nodes (small touched sets) or by a write-only zero stream
-//    (large ones), never by a read-modify-write memset of everything.
+//    (slot-major).  Between waves a slot is reset by zeroing exactly the
+//    32 B sectors of r it wrote (sector bit map set on first touch, cleared
+//    warp-cooperatively in coalesced 1 KB runs) and x over its pushed-node
+//    list -- never by a memset of the whole slot.
 //  * The graph is renumbered once by descending degree with sorted rows:
 //    hubs, which receive most residual updates, form a contiguous block, so
 //    a warp's 32 atomics land in few sectors and stay L2 resident.
@@ -575,31 +576,35 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
     }
 }
 
-// grid (CHUNKS, slots): return r of every slot to +0.0.
+// grid (CHUNKS, slots): return r of every slot to +0.0 -- zero exactly the
+// 32 B sectors this slot ever wrote (sector map set on first touch) and clear
+// the map.  A warp takes 32 map words at a time and, word by word, each lane
+// stores one sector, so the stores of a word are one coalesced 1 KB run.
 __global__ void k_wave_reset(RoundArgs A) {
-    // zero exactly the 32 B sectors of r this slot ever wrote (sector map
-    // set on first touch), then clear the map: ~touched sectors of traffic
-    // instead of a zero stream over the whole slot
     const int k = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t off = (int64_t)k * A.ld;
     uint32_t *map = A.secmap + (int64_t)k * A.smw;
     const int64_t per = (A.smw + CHUNKS - 1) / CHUNKS;
     const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
     double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
-    for (int64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
-        uint32_t bits = map[w];
-        if (!bits) continue;
-        map[w] = 0u;
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int64_t sec = w * 32 + b;  // sector index: doubles [4 sec, 4 sec + 4)
-            if (4 * sec + 3 < A.ld) {
-                r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
-            } else {
-                for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
+    for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
+        const uint32_t mine = (w0 + lane < hi) ? map[w0 + lane] : 0u;
+        unsigned any = __ballot_sync(FULL, mine != 0u);
+        while (any) {
+            const int src = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t wb = __shfl_sync(FULL, mine, src);
+            if ((wb >> lane) & 1u) {
+                const int64_t sec = (w0 + src) * 32 + lane;  // doubles [4 sec, 4 sec + 4)
+                if (4 * sec + 3 < A.ld) {
+                    r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+                } else {
+                    for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
+                }
             }
         }
+        if (mine) map[w0 + lane] = 0u;
     }
 }
 
