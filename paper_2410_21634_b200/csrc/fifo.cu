@@ -1,5 +1,5 @@
-// fifo.cu -- exact FIFO push (LocalGS / LocalSOR / dynamic repair) and the
-// stage-expanded heat-kernel push, one warp per system.
+// fifo.cu -- exact FIFO push (LocalGS / LocalSOR / dynamic repair), one
+// warp per system.  (The heat-kernel push runs as layered sweeps, hk.cu.)
 //
 // The reference kernels (_push_kernel src/local_solvers.py:48-188 and
 // _hk_push_kernel :566-661) are sequential Gauss-Seidel pushes: every pop
@@ -352,32 +352,6 @@ int gd_push_kernel(const gd_graph *G, const gd_operator *o, double *x, double *r
         A.sgn = is_signed ? 1 : 0;
         A.max_sweeps = max_sweeps;
         run_fifo(G, A, false, x, r, seeds, n_seeds, rep);
-    });
-}
-
-int gd_hk_push(const gd_graph *G, int64_t n_stages, const double *stage_w, double theta_coeff,
-               double *v, double *r, int64_t seed, int64_t max_sweeps, gd_report *rep) {
-    return guarded([&] {
-        GD_CHECK_ARG(G && v && r && rep && (stage_w || n_stages == 0), "null pointer");
-        GD_CHECK_ARG(n_stages >= 0, "n_stages must be >= 0");
-        GD_CUDA(cudaSetDevice(G->device));
-        DBuf<double> sw(n_stages ? n_stages : 1);
-        if (n_stages)
-            GD_CUDA(cudaMemcpy(sw.p, stage_w, sizeof(double) * n_stages, cudaMemcpyHostToDevice));
-        FifoArgs A{};
-        A.g = G->view();
-        A.op = DevOp{GD_W_RW, GD_T_DEGREE, 1.0, theta_coeff, nullptr, nullptr};
-        A.dim = (n_stages + 1) * G->n;
-        A.omega = 1.0;
-        A.x_gain = 1.0;
-        A.sgn = 0;
-        A.max_sweeps = max_sweeps;
-        A.n_stages = n_stages;
-        A.stage_w = sw.p;
-        int64_t s1 = seed;
-        GD_CHECK_ARG(seed >= 0 && seed < G->n, "seed out of range");
-        // the reference enqueues the seed only when r[seed] >= theta[seed] (:576-579)
-        run_fifo(G, A, true, v, r, &s1, 1, rep);
     });
 }
 

@@ -52,6 +52,25 @@ def test_heat_kernel_matches_reference(gpu, small, tau):
     assert np.abs(f - small[f"{k}/series60"]).sum() <= 1e-4 + S.hk_paper_bound(sys_.op.stage_count)
 
 
+@pytest.mark.parametrize("tau,eps", [(1.0, 1e-5), (5.0, 1e-6), (10.0, 1e-7)])
+def test_heat_kernel_layered_matches_oracle(gpu, tau, eps):
+    """The layered-sweep heat kernel reproduces the FIFO reference push bit
+    for bit (f_hat, every stage's v and r, vol log) on an R-MAT graph."""
+    from oracle import oracle as O
+    from paper_2410_21634_b200.metrics import sample_sources
+    from paper_2410_21634_b200.synth import rmat_graph
+    g = rmat_graph(20000, 150000, seed=2)
+    for s in sample_sources(g, 3, seed=1):
+        f, rep = LS.local_hk(g, tau, int(s), eps)
+        ref = O.local_hk(g, tau, int(s), eps)
+        assert np.array_equal(f, ref["f_hat"])
+        assert rep.sweeps == ref["sweeps"] and rep.total_ops == ref["total_ops"]
+        assert rep.vol_log == ref["vol_log"].tolist()
+        assert rep.notes["residual_mass"] == ref["residual_mass"]
+        np.testing.assert_allclose(rep.residual_l1_trace, ref["l1_log"], rtol=1e-12)
+        np.testing.assert_allclose(rep.gamma_log, ref["gamma_log"], rtol=1e-12)
+
+
 def test_heat_kernel_tiny_tau(gpu, small):
     f, rep = LS.local_hk(golden_graph(small, "p2"), 1e-9, 0, 1e-3)
     assert rep.converged and rep.sweeps == 1
