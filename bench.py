@@ -49,7 +49,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--graph-seed", type=int, default=0)
     p.add_argument("--no-relabel", action="store_true", help="run on the caller's node order")
-    p.add_argument("--method", default="local-gd", choices=["local-gd", "local-sor", "local-ch"])
+    p.add_argument("--method", default="local-gd",
+                   choices=["local-gd", "local-sor", "local-ch", "local-hk"])
+    p.add_argument("--tau", type=float, default=10.0, help="local-hk: heat-kernel time")
     p.add_argument("--omega", type=float, default=1.0, help="local-sor relaxation")
     p.add_argument("--problem", default="ppr", choices=["ppr", "katz"],
                    help="local-ch: PPR, or Katz with alpha = 1/(lambda+1) (--alpha ignored)")
@@ -155,7 +157,15 @@ def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, 
     from oracle import oracle as O
 
     t0 = time.perf_counter()
-    if method == "local-ch":
+    if method == "local-hk":
+        import psutil
+
+        per = 25 * (ch["n_stages"] + 1) * hg.n  # v, r, queue, marks per thread (reference layout)
+        th = max(1, min(threads, int(0.5 * psutil.virtual_memory().available // max(per, 1))))
+        out = O.batch_local_hk(hg, ch["tau"], eps, seeds, th)
+        out["pushes"] = np.zeros_like(out["total_ops"])
+        out["threads"] = th
+    elif method == "local-ch":
         out = O.batch_local_ch(hg, alpha, eps, seeds, threads, ch["mu"], ch["L"],
                                problem=ch["problem"], max_sweeps=ch["max_sweeps"])
         out["pushes"] = np.zeros_like(out["total_ops"])
@@ -186,6 +196,13 @@ def spectral_radius(row, col, n, iters=100):
         lam = float(torch.dot(x, y))
         x = y / torch.linalg.vector_norm(y)
     return lam
+
+
+def hk_config(args, hg):
+    """Seed-independent heat-kernel system parameters (make_hk_system)."""
+    from paper_2410_21634_b200.batch import hk_params
+
+    return hk_params(hg, args.tau, args.eps, int(np.argmax(hg.degrees)))
 
 
 def ch_params(args, row, col, n):
@@ -228,6 +245,8 @@ def run_reference(args):
         _, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
         args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
         hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
+        if args.method == "local-hk":
+            args.ch = {k: v for k, v in hk_config(args, hg).items() if k != "stage_w"}
         del row, col
     else:
         from paper_2410_21634_b200.synth import rmat_graph
@@ -240,6 +259,8 @@ def run_reference(args):
         hg.d_max = int(hg.degrees.max()) if n else 0
         args.ch = (ch_params(args, torch.as_tensor(g.offsets), torch.as_tensor(g.targets), n)
                    if args.method == "local-ch" else None)
+        if args.method == "local-hk":
+            args.ch = {k: v for k, v in hk_config(args, hg).items() if k != "stage_w"}
     steps_total = args.steps + args.warmup
     allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
     batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
@@ -276,10 +297,12 @@ def run_reference(args):
 
 
 def workload_config(args, n, m):
-    name = {"local-gd": "LocalGD", "local-ch": "LocalCH",
+    name = {"local-gd": "LocalGD", "local-ch": "LocalCH", "local-hk": "push",
             "local-sor": f"LocalSOR(omega={args.omega:g})"}[args.method]
-    prob = "Katz" if args.method == "local-ch" and args.problem == "katz" else "PPR"
-    return {"workload": f"batched {name}-{prob} alpha={args.alpha:.6g} eps={args.eps:g}, "
+    prob = ("Katz" if args.method == "local-ch" and args.problem == "katz" else
+            "heat-kernel" if args.method == "local-hk" else "PPR")
+    par = f"tau={args.tau:g}" if args.method == "local-hk" else f"alpha={args.alpha:.6g}"
+    return {"workload": f"batched {name}-{prob} {par} eps={args.eps:g}, "
                         f"R-MAT {args.shape}-shape ({n:,} nodes, {m:,} edges), "
                         f"{args.seeds} seeds/GPU/step from sample_sources",
             "graph": f"rmat-{args.shape}", "n": n, "edges": m, "alpha": args.alpha,
@@ -308,6 +331,10 @@ def main():
     dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
     hdeg = _HostGraph(n, row_h)
     args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
+    hkp = None
+    if args.method == "local-hk":
+        hkp = hk_config(args, hdeg)
+        args.ch = {k: v for k, v in hkp.items() if k != "stage_w"}
     if args.no_cpu_baseline:  # the CPU leg is the only later user of the torch copies
         del row, col
         col = None
@@ -323,7 +350,7 @@ def main():
     solver = BatchSolver(dg, args.alpha, args.eps, slots=args.slots, relabel=not args.no_relabel,
                          method=args.method, omega=args.omega, problem=ch.get("problem", "ppr"),
                          mu=ch.get("mu"), L=ch.get("L"),
-                         max_sweeps=ch.get("max_sweeps", 1_000_000))
+                         max_sweeps=ch.get("max_sweeps", 1_000_000), hk=hkp)
     stream = torch.cuda.current_stream()
 
     def gather(res):
@@ -373,6 +400,7 @@ def main():
     my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic({"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
+                                        "local-hk": "k_rounds_hk",
                                         "local-sor": "k_fifo_batch"}[args.method])
     # e2e: the public host API with host buffers, copies inside the timed region
     e2e = None
@@ -404,6 +432,7 @@ def main():
         chunk = max(threads, 8)
         pos = 0
         ref_sweeps, ref_ops = [], []
+        used = threads
         while spent < args.cpu_seconds and pos < len(batches[args.warmup]):
             sl = batches[args.warmup][pos:pos + chunk]
             o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega,
@@ -412,11 +441,12 @@ def main():
             sample.extend(sl.tolist())
             ref_sweeps.append(o["sweeps"])
             ref_ops.append(o["total_ops"])
+            used = int(o.get("threads", threads))
             pos += chunk
         res = solver.solve(np.asarray(sample, dtype=np.int64))
         parity = bool(np.array_equal(np.concatenate(ref_ops), res.total_ops)
                       and np.array_equal(np.concatenate(ref_sweeps), res.sweeps))
-        cpu = {"value": len(sample) / spent, "unit": "solves/s", "cores": threads, "kind": "port",
+        cpu = {"value": len(sample) / spent, "unit": "solves/s", "cores": used, "kind": "port",
                "sample": f"first {len(sample)} seeds of the first timed batch, reference "
                          f"{args.method.replace('-', '_')} restated in C (oracle/), one seed per thread",
                "parity_sweeps_ops_identical": parity}
@@ -431,10 +461,12 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // 4,
-                                                                "local-ch": launches // 5}.get(args.method, launches)),
+                                                                "local-ch": launches // 5,
+                                                                "local-hk": launches // 5}.get(args.method, launches)),
                          "peak_kind": peak_kind,
                          "kernel": {"local-gd": "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
+                                    "local-hk": "k_rounds<HK> (layered heat-kernel stage sweeps)",
                                     "local-sor": "k_fifo_batch (warp per seed)"}[args.method],
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

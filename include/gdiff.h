@@ -166,6 +166,11 @@ int gd_spectral_norm(const gd_graph *g, const double *x0, int64_t iters, double 
                             with the same frontier sets, sweeps and operation
                             counts, x to rounding of the atomic scatter */
 
+#define GD_M_HK 3        /* heat-kernel push on the stage-expanded system, run as
+                            layered sweeps (batch.cu): per seed local_hk(g, tau,
+                            s, eps) with the same sweeps and operation counts,
+                            f_hat (x out, e^-tau applied) to rounding */
+
 #define GD_P_PPR 0  /* (I - (1-alpha) A D^-1) x = alpha e_s, theta = eps alpha d */
 #define GD_P_KATZ 1 /* (I - alpha A) x = e_s, theta = eps d (src/systems.py:194-219);
                        GD_M_LOCAL_CH only */
@@ -190,6 +195,11 @@ typedef struct {
     double mu, L;         /* GD_M_LOCAL_CH: eigenvalue bounds, mu < L (the
                              reference's cheby_bounds, src/local_solvers.py:541-558;
                              0, 0 = PPR defaults alpha, 2 - alpha) */
+    /* GD_M_HK: the system of make_hk_system (src/systems.py:269-301): */
+    double tau;
+    int64_t n_stages;        /* N */
+    const double *stage_w;   /* host, N entries: tau/(k+1) as the system stores them */
+    double theta_coeff;      /* eps / (2 (N+1) vol); theta = fl(coeff * d) */
 } gd_batch_params;
 
 typedef struct {

@@ -739,3 +739,70 @@ int orc_batch_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const 
     free(pushes);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* batched CPU baseline of the heat kernel: the reference's local_hk per   */
+/* seed (src/local_solvers.py:664-696), one seed per thread, dense         */
+/* (N+1) n state per thread as in the reference                            */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int64_t n, n_stages;
+    const int64_t *off, *tgt;
+    const double *base_w, *stage_w, *theta;
+    double tau;
+    const int64_t *seeds;
+    int64_t n_seeds, max_sweeps;
+    int64_t *out_sweeps, *out_ops;
+    int32_t *out_conv;
+    double *out_fsum;
+    int64_t next;
+} hk_job;
+
+static void *hk_worker(void *arg) {
+    hk_job *J = arg;
+    const int64_t dim = (J->n_stages + 1) * J->n;
+    double *v = malloc(sizeof(double) * (dim ? dim : 1));
+    double *r = malloc(sizeof(double) * (dim ? dim : 1));
+    for (;;) {
+        int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+        if (i >= J->n_seeds) break;
+        memset(v, 0, sizeof(double) * dim);
+        memset(r, 0, sizeof(double) * dim);
+        r[J->seeds[i]] = 1.0; /* b = e_s at stage 0 */
+        orc_report rep;
+        orc_hk_push(J->n, J->n_stages, J->off, J->tgt, J->base_w, J->stage_w, J->theta, v, r,
+                    J->seeds[i], J->max_sweeps, &rep);
+        J->out_sweeps[i] = rep.sweeps;
+        J->out_ops[i] = rep.total_ops;
+        J->out_conv[i] = rep.converged;
+        if (J->out_fsum) { /* sum of f_hat = e^-tau * sum_k v_k (stage order per node) */
+            const double e = exp(-J->tau);
+            double s = 0.0;
+            for (int64_t u = 0; u < J->n; u++) {
+                double acc = v[u];
+                for (int64_t k = 1; k <= J->n_stages; k++) acc += v[k * J->n + u];
+                s += e * acc;
+            }
+            J->out_fsum[i] = s;
+        }
+        orc_report_free(&rep);
+    }
+    free(v);
+    free(r);
+    return NULL;
+}
+
+int orc_batch_hk(int64_t n, int64_t n_stages, const int64_t *off, const int64_t *tgt,
+                 const double *base_w, const double *stage_w, const double *theta, double tau,
+                 const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
+                 int64_t *out_sweeps, int64_t *out_ops, int32_t *out_conv, double *out_fsum) {
+    hk_job J = {n, n_stages, off, tgt, base_w, stage_w, theta, tau, seeds, n_seeds, max_sweeps,
+                out_sweeps, out_ops, out_conv, out_fsum, 0};
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, hk_worker, &J);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+    return 0;
+}

@@ -263,6 +263,30 @@ def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, 
     return {"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "xsum": xs}
 
 
+def batch_local_hk(g, tau: float, eps: float, seeds, threads: int,
+                   max_sweeps: int = 1_000_000) -> dict:
+    """Per-seed reference local_hk over many host threads (CPU baseline of
+    the heat-kernel batch); dense (N+1) n state per thread as the reference."""
+    from paper_2410_21634_b200.systems import make_hk_system
+    sd = _arr64(seeds)
+    sys = make_hk_system(g, tau, int(sd[0]) if sd.size else 0, eps)
+    N = sys.op.stage_count
+    base_w = _arrf(sys.op.arc_weights)
+    stage_w = _arrf(sys.op.stage_weights if N else np.zeros(1))
+    th = _arrf(sys.theta)
+    off, tg = _arr64(g.offsets), _arr64(g.targets)
+    k = sd.shape[0]
+    sw, ops = np.zeros(k, np.int64), np.zeros(k, np.int64)
+    cv = np.zeros(k, np.int32)
+    fs = np.zeros(k)
+    lib().orc_batch_hk(C.c_int64(g.n), C.c_int64(N), _p(off, C.c_int64), _p(tg, C.c_int64),
+                       _p(base_w), _p(stage_w), _p(th), C.c_double(tau), _p(sd, C.c_int64),
+                       C.c_int64(k), C.c_int64(max_sweeps), C.c_int32(threads), _p(sw, C.c_int64),
+                       _p(ops, C.c_int64), _p(cv, C.c_int32), _p(fs))
+    return {"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "fsum": fs,
+            "stage_count": N}
+
+
 def pairwise_sum(a, take_abs: bool = False) -> float:
     a = _arrf(a)
     return float(lib().orc_pairwise_sum(_p(a), C.c_int64(a.shape[0]), C.c_int32(int(take_abs))))

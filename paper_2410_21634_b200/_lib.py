@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GDIFF_LIB") or os.path.join(HERE, "libgdiff.so")  # o
 GD_OK, GD_ERR_ARG, GD_ERR_CUDA, GD_ERR_OOM, GD_ERR_CAPACITY, GD_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GD_W_RW, GD_W_CONST, GD_W_ARC = 0, 1, 2
 GD_T_DEGREE, GD_T_ARRAY = 0, 1
-GD_M_LOCAL_GD, GD_M_LOCAL_SOR, GD_M_LOCAL_CH = 0, 1, 2
+GD_M_LOCAL_GD, GD_M_LOCAL_SOR, GD_M_LOCAL_CH, GD_M_HK = 0, 1, 2, 3
 GD_P_PPR, GD_P_KATZ = 0, 1
 
 _i64p = C.POINTER(C.c_int64)
@@ -57,7 +57,8 @@ class BatchParams(C.Structure):
                 ("eps", C.c_double), ("max_sweeps", C.c_int64),
                 ("frontier_cap", C.c_int64), ("out_cap", C.c_int64),
                 ("relabel", C.c_int32), ("problem", C.c_int32), ("omega", C.c_double),
-                ("mu", C.c_double), ("L", C.c_double)]
+                ("mu", C.c_double), ("L", C.c_double), ("tau", C.c_double),
+                ("n_stages", C.c_int64), ("stage_w", _f64p), ("theta_coeff", C.c_double)]
 
 
 class BatchResult(C.Structure):

@@ -17,7 +17,8 @@ import numpy as np
 from . import _lib as gdl
 from .device import DeviceGraph, device_graph
 
-__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch", "local_ch_batch"]
+__all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch", "local_ch_batch",
+           "local_hk_batch"]
 
 
 def _host_array(count: int, dtype, pinned: bool) -> np.ndarray:
@@ -77,12 +78,14 @@ class BatchSolver:
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
-                 L: float | None = None):
-        if method not in ("local-gd", "local-sor", "local-ch"):
+                 L: float | None = None, hk: dict | None = None):
+        if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
         if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
             raise ValueError("problem must be 'ppr', or 'katz' with method 'local-ch'")
-        if problem == "ppr" and not 0.0 < alpha <= 1.0:
+        if method == "local-hk" and not hk:
+            raise ValueError("local-hk needs hk={tau, n_stages, stage_w, theta_coeff}")
+        if method != "local-hk" and problem == "ppr" and not 0.0 < alpha <= 1.0:
             raise ValueError("alpha must be in (0, 1]")
         if problem == "katz" and not alpha > 0.0:
             raise ValueError("alpha must be positive")
@@ -100,12 +103,16 @@ class BatchSolver:
         self.graph = g if isinstance(g, DeviceGraph) else device_graph(g, device)
         self.alpha, self.eps = float(alpha), float(eps)
         mcode = {"local-gd": gdl.GD_M_LOCAL_GD, "local-sor": gdl.GD_M_LOCAL_SOR,
-                 "local-ch": gdl.GD_M_LOCAL_CH}[method]
+                 "local-ch": gdl.GD_M_LOCAL_CH, "local-hk": gdl.GD_M_HK}[method]
+        hk = hk or {}
+        sw = np.ascontiguousarray(hk.get("stage_w", np.zeros(1)), dtype=np.float64)
         p = gdl.BatchParams(method=mcode, slots=int(slots), alpha=self.alpha, eps=self.eps,
                             max_sweeps=int(max_sweeps), frontier_cap=int(frontier_cap),
                             out_cap=int(out_cap), relabel=int(bool(relabel)),
                             problem=gdl.GD_P_KATZ if problem == "katz" else gdl.GD_P_PPR,
-                            omega=float(omega), mu=float(mu or 0.0), L=float(L or 0.0))
+                            omega=float(omega), mu=float(mu or 0.0), L=float(L or 0.0),
+                            tau=float(hk.get("tau", 0.0)), n_stages=int(hk.get("n_stages", 0)),
+                            stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)))
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
@@ -269,6 +276,32 @@ def local_ch_batch(g, seeds, alpha: float, eps: float, problem: str = "ppr",
         max_sweeps = max(1000, int(10 * math.log(max(1.0 / max(eps, 1e-300), 2.0)) / gap))
     solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method="local-ch",
                          problem=problem, mu=mu, L=L, relabel=relabel)
+    try:
+        return solver.solve(sd)
+    finally:
+        solver.close()
+
+
+def hk_params(g, tau: float, eps: float, s: int = 0) -> dict:
+    """Seed-independent part of make_hk_system (src/systems.py:269-301)."""
+    from .systems import make_hk_system
+
+    sys = make_hk_system(g, tau, int(s), eps)
+    N = int(sys.op.stage_count)
+    return {"tau": float(tau), "n_stages": N,
+            "stage_w": np.asarray(sys.op.stage_weights if N else np.zeros(1), dtype=np.float64),
+            "theta_coeff": float(sys.theta_coeff)}
+
+
+def local_hk_batch(g, seeds, tau: float, eps: float, slots: int = 0, relabel: bool = True,
+                   max_sweeps: int = 1_000_000) -> BatchOutput:
+    """Batched heat kernel: per seed the reference's local_hk(g, tau, s, eps)
+    (same sweeps and operation counts; x = f_hat to rounding), as layered
+    stage sweeps over many seeds at once."""
+    sd = _check_seeds(g, seeds)
+    hk = hk_params(g, tau, eps, int(sd[0]) if sd.size else 0)
+    solver = BatchSolver(g, 1.0, eps, slots=slots, max_sweeps=max_sweeps, method="local-hk",
+                         relabel=relabel, hk=hk)
     try:
         return solver.solve(sd)
     finally:

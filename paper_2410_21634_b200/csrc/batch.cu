@@ -83,6 +83,10 @@ struct RoundArgs {
     int64_t fcap;
     int64_t m;      // slots in use this wave
     double *x, *r;
+    double *r2;              // heat kernel: second residual layer (stages alternate)
+    uint32_t *secmap2;       // heat kernel: sector map of r2
+    const double *stage_w;   // heat kernel: tau/(k+1) per stage (device)
+    int64_t n_stages;        // heat kernel: N (stage N is absorbing)
     int32_t *pushed;
     int32_t *seed;  // per slot: seed in working ids
     unsigned long long *touched, *pushed_cnt;
@@ -332,7 +336,15 @@ __device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
     }
 }
 
-__global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
+// Heat kernel (HK = true, GD_M_HK): the stage-expanded push of
+// _hk_push_kernel (src/local_solvers.py:566-661).  Round t pops stage t and
+// feeds stage t+1 only (see hk.cu), so all seeds of a wave are at the same
+// stage: layer t lives in r (t even) or r2 (t odd), the layer receiving
+// stage t+1 is cleared of its stage t-1 leftovers in phase A, and the
+// products are fl(fl(r * tau/(t+1)) * fl(1/d_u)).  x accumulates the pushed
+// values stage by stage -- the reference's stages.sum(axis=0) order.
+template <bool HK>
+__global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Stage S = stage_carve(smem_raw, (int)A.m);
@@ -381,6 +393,33 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
             A.cctr[0] = 0ULL;
         }
         for (int64_t k = gtid; k < A.m; k += nthreads) A.scnt[nxt][k] = 0ULL;
+        double *const rc = (HK && (t & 1)) ? A.r2 : A.r;        // layer t
+        double *const rn = (HK && !(t & 1)) ? A.r2 : A.r;       // layer t+1 (HK)
+        uint32_t *const mapn = (HK && !(t & 1)) ? A.secmap2 : A.secmap;
+        if (HK && t >= 1 && t < A.n_stages) {
+            // layer t+1 reuses layer t-1's array: zero its touched sectors
+            const int64_t total = A.m * A.smw;
+            const int64_t gw = gtid >> 5, nw = nthreads >> 5;
+            for (int64_t w0 = gw * 32; w0 < total; w0 += nw * 32) {
+                const uint32_t mine = (w0 + lane < total) ? mapn[w0 + lane] : 0u;
+                unsigned any = __ballot_sync(FULL, mine != 0u);
+                while (any) {
+                    const int src = __ffs(any) - 1;
+                    any &= any - 1;
+                    const uint32_t wb = __shfl_sync(FULL, mine, src);
+                    if ((wb >> lane) & 1u) {
+                        const int64_t w = w0 + src, kk = w / A.smw;
+                        const int64_t sec = (w - kk * A.smw) * 32 + lane;
+                        double *base = rn + kk * A.ld;
+                        if (4 * sec + 3 < A.ld)
+                            reinterpret_cast<double4 *>(base)[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+                        else
+                            for (int64_t i = 4 * sec; i < A.ld; ++i) base[i] = 0.0;
+                    }
+                }
+                if (mine) mapn[w0 + lane] = 0u;
+            }
+        }
         slot_bases(S, A, cur);
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
             const int64_t e = e0 + lane;
@@ -393,10 +432,10 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
                 const int64_t idx = (int64_t)k * A.ld + u;
-                const double val = A.r[idx];
+                const double val = rc[idx];
                 const double xo = A.x[idx];
                 A.x[idx] = __dadd_rn(xo, val);
-                A.r[idx] = -0.0;
+                rc[idx] = HK ? 0.0 : -0.0;
                 d = A.g.deg[u];
                 const unsigned long long b =
                     S.sbase[k] + atomicAdd(A.sfill + k, (1ULL << CNT_SHIFT) + (unsigned long long)d);
@@ -405,7 +444,10 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 A.skey[pos] = key;
                 A.sarc[pos] = a0;
                 A.frow[pos] = A.g.row[u];
-                A.fcval[pos] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                A.fcval[pos] =
+                    HK ? __dmul_rn(__dmul_rn(val, A.stage_w[t < A.n_stages ? t : 0]),
+                                   __ddiv_rn(1.0, (double)d))
+                       : __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 fresh = __double_as_longlong(xo) == 0;  // first push of u
                 // chunks (32 arcs) whose first arc lies in this entry: [clo, chi)
                 clo = (a0 + 31) >> 5;
@@ -442,7 +484,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
         const int64_t C = (P + 31) >> 5;
         const int64_t *fa = A.sarc;
         const int64_t wid = gtid >> 5, nwarps = nthreads >> 5;
-        {
+        if (!HK || t < A.n_stages) {  // (the last heat-kernel stage is absorbing)
             const int64_t c1 = C;
           for (int64_t cb = wid * UNROLL; cb < c1; cb += nwarps * UNROLL) {
             int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
@@ -476,7 +518,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
             // stage 2: the atomics, back to back (UNROLL in flight per lane)
 #pragma unroll
             for (int q = 0; q < UNROLL; q++)
-                old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+                old[q] = valid[q] ? atomicAdd(rn + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
             // stage 3: first touch / re-touch of a pushed node / frontier entry
 #pragma unroll
             for (int q = 0; q < UNROLL; q++) {
@@ -487,7 +529,7 @@ __global__ void __launch_bounds__(BT) k_rounds(RoundArgs A) {
                 const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
                 block_count(first, k[q], 1u, S.touch);
                 if (first)  // first write of this r word: remember its 32 B sector
-                    atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
+                    atomicOr(mapn + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                 block_count(negz, k[q], 1u, S.negz);
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
             }
@@ -540,6 +582,8 @@ struct OutArgs {
     double *xvals;
     int64_t xcap;
     const int32_t *inv;  // working id -> caller id (nullable)
+    double xscale;       // x out = fl(xscale * x) (heat kernel: e^-tau; else 1)
+    int hk;
 };
 
 // grid (CHUNKS, slots): copy x over the pushed list out (caller ids) and zero
@@ -559,7 +603,7 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
         A.x[off + u] = 0.0;
         if (b + i < O.xcap) {
             O.xnodes[b + i] = O.inv ? O.inv[u] : u;
-            O.xvals[b + i] = xv;
+            O.xvals[b + i] = __dmul_rn(O.xscale, xv);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -569,7 +613,7 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
         O.ops[si] = (int64_t)A.s_ops[k];
         O.pushes[si] = pushes;
         O.conv[si] = A.s_conv[k];
-        O.support[si] = (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
+        O.support[si] = O.hk ? -1 : (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
         O.xoff[si] = b;
         O.xcnt[si] = pc;
         if (pc == 0) A.r[off + A.seed[k]] = 0.0;  // an inactive seed keeps r = alpha
@@ -673,6 +717,9 @@ struct gd_batch {
     static constexpr int64_t RLOG_CAP = 4096;
     DBuf<uint32_t> secmap;
     int64_t smw = 0;
+    bool hk = false;           // GD_M_HK: layered stage sweeps
+    DBuf<double> r2, stage_w;  // (heat kernel) second residual layer, tau/(k+1)
+    DBuf<uint32_t> secmap2;
     // results
     DBuf<int64_t> sweeps, ops, pushes, support, xoff, xcnt;
     DBuf<int32_t> conv, xnodes;
@@ -689,7 +736,9 @@ struct gd_batch {
         RoundArgs A{};
         A.g = work()->view();
         A.beta = 1.0 - p.alpha;
-        A.tcoeff = p.eps * p.alpha;
+        A.tcoeff = hk ? p.theta_coeff : p.eps * p.alpha;
+        A.r2 = r2.p; A.secmap2 = secmap2.p; A.stage_w = stage_w.p;
+        A.n_stages = hk ? p.n_stages : 0;
         A.n = G->n;
         A.ld = (G->n + 3) & ~3LL;
         A.max_sweeps = p.max_sweeps;
@@ -766,24 +815,33 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         B->ev.push_back(e);
     }
     OutArgs O{B->sweeps.p, B->ops.p, B->pushes.p, B->support.p, B->xoff.p, B->xcnt.p,
-              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr};
+              B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr,
+              B->hk ? std::exp(-B->p.tau) : 1.0, B->hk ? 1 : 0};
     int64_t launches = 0;
     for (int64_t w = 0; w < waves; ++w) {
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
-        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, B->p.alpha);
+        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
+                                                               B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A};
-        GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_rounds, dim3(B->grid), dim3(BT), kargs,
+        const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
+        GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
         k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
         k_wave_reset<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A);
+        if (B->hk) {  // the other residual layer
+            RoundArgs A2 = A;
+            A2.r = A.r2;
+            A2.secmap = A.secmap2;
+            k_wave_reset<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A2);
+        }
         GD_LAUNCH_CHECK();
-        launches += 4;
+        launches += B->hk ? 5 : 4;
     }
     GD_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
@@ -879,15 +937,20 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
     return guarded([&] {
         GD_CHECK_ARG(G && p && out, "null pointer");
         GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR ||
-                         p->method == GD_M_LOCAL_CH,
+                         p->method == GD_M_LOCAL_CH || p->method == GD_M_HK,
                      "unknown batch method");
+        GD_CHECK_ARG(p->method != GD_M_HK ||
+                         (p->n_stages >= 0 && (p->stage_w || p->n_stages == 0) &&
+                          p->theta_coeff > 0.0 && p->tau >= 0.0),
+                     "heat kernel batches need tau >= 0, n_stages, stage_w, theta_coeff > 0");
         GD_CHECK_ARG(p->problem == GD_P_PPR || (p->problem == GD_P_KATZ && p->method == GD_M_LOCAL_CH),
                      "Katz batches need GD_M_LOCAL_CH");
         GD_CHECK_ARG(p->method != GD_M_LOCAL_SOR || (p->omega > 0.0 && p->omega <= 2.0),
                      "omega must be in (0, 2]");
-        GD_CHECK_ARG(p->alpha > 0.0 && (p->problem == GD_P_KATZ || p->alpha <= 1.0),
+        GD_CHECK_ARG(p->method == GD_M_HK ||
+                         (p->alpha > 0.0 && (p->problem == GD_P_KATZ || p->alpha <= 1.0)),
                      "alpha must be in (0, 1]");
-        GD_CHECK_ARG(p->eps > 0.0, "eps must be positive");
+        GD_CHECK_ARG(p->method == GD_M_HK || p->eps > 0.0, "eps must be positive");
         GD_CHECK_ARG(G->n_arcs < (1LL << CNT_SHIFT), "too many arcs");
         GD_CUDA(cudaSetDevice(G->device));
         const int64_t n = G->n ? G->n : 1;
@@ -907,6 +970,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 *out = B;
                 return;
             }
+            B->hk = p->method == GD_M_HK;
             if (p->relabel) build_relabeled(B);
             if (p->method == GD_M_LOCAL_CH) {
                 if (B->p.mu == 0.0 && B->p.L == 0.0) {
@@ -949,13 +1013,16 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
                 // 64 in flight measured best on the products shape (L2 reuse of
                 // the hub block vs. barrier amortisation); fewer if memory-bound
-                int64_t by_mem = (int64_t)(fr / 4) / (ld * 20);
+                int64_t by_mem = (int64_t)(fr / 4) / (ld * (B->hk ? 28 : 20));
+                // the heat kernel at large tau is effectively global: a stage's
+                // frontier approaches n per seed, so bound slots * n as well
+                if (B->hk && by_mem > (64LL << 20) / n) by_mem = (64LL << 20) / n;
                 slots = (int)(by_mem < 64 ? (by_mem < 1 ? 1 : by_mem) : 64);
             }
             if (slots > 2048) slots = 2048;  // per-block slot counters live in shared memory
             B->slots = slots;
             int64_t fc = p->frontier_cap > 0 ? p->frontier_cap : (int64_t)slots * n;
-            if (p->frontier_cap <= 0 && fc > (64LL << 20)) fc = 64LL << 20;
+            if (p->frontier_cap <= 0 && fc > (64LL << 20) && !B->hk) fc = 64LL << 20;
             B->fcap = fc;
             B->xcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
             const size_t sn = (size_t)slots * (size_t)ld;
@@ -972,17 +1039,34 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->scnt.alloc(2 * (size_t)slots); B->sfill.alloc(slots); B->cctr.alloc(1);
             B->frow.alloc(fc); B->fcval.alloc(fc);
             B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
+            if (B->hk && p->frontier_cap <= 0) {  // global stages: up to slots * 2m arcs
+                const int64_t cc = ((int64_t)slots * G->n_arcs + 31) / 32 + slots;
+                if (cc > B->ccap) B->ccap = cc;
+            }
             B->chunk_e.alloc(B->ccap);
             B->rlog.alloc(3 * gd_batch::RLOG_CAP + 1);
             B->smw = (ld / 4 + 31) / 32;  // one bit per 4 doubles (32 B sector)
             B->secmap.alloc((size_t)slots * (size_t)B->smw);
             GD_CUDA(cudaMemset(B->secmap.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
+            if (B->hk) {
+                B->r2.alloc(sn);
+                GD_CUDA(cudaMemset(B->r2.p, 0, sizeof(double) * sn));
+                B->secmap2.alloc((size_t)slots * (size_t)B->smw);
+                GD_CUDA(cudaMemset(B->secmap2.p, 0,
+                                   sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
+                B->stage_w.alloc(p->n_stages ? p->n_stages : 1);
+                if (p->n_stages)
+                    GD_CUDA(cudaMemcpy(B->stage_w.p, p->stage_w, sizeof(double) * p->n_stages,
+                                       cudaMemcpyHostToDevice));
+                B->p.stage_w = nullptr;  // (the caller's array is not kept)
+            }
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
             const size_t smem = stage_bytes(slots);
-            GD_CUDA(cudaFuncSetAttribute(k_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
+            GD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             int per_sm = 0;
-            GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rounds, BT, smem));
+            GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, BT, smem));
             GD_CHECK_ARG(per_sm > 0, "round kernel does not fit on an SM");
             B->grid = per_sm * n_sms(G->device);
         } catch (...) {

@@ -139,3 +139,34 @@ def test_sor_batch_max_sweeps(gpu):
     g = from_edges(4, [(0, 1), (1, 2), (2, 0)])
     out = local_sor_batch(g, [0, 1], 0.2, 1e-9, max_sweeps=2)
     assert (out.sweeps == 2).all() and not out.converged.any()
+
+
+# ---- batched heat kernel (layered stage sweeps) ---------------------------
+
+@pytest.mark.parametrize("tau", [0.5, 1.0, 5.0])
+def test_hk_batch_matches_reference(gpu, small, tau):
+    from paper_2410_21634_b200.batch import local_hk_batch
+    g = golden_graph(small, "er60")
+    out = local_hk_batch(g, [0, 0, 0], tau, 1e-4, slots=2)
+    k = f"er60/hk/tau{tau}"
+    for i in range(3):
+        assert out.sweeps[i] == small[f"{k}/sweeps"] and out.total_ops[i] == small[f"{k}/total_ops"]
+        f = small[f"{k}/f_hat"]
+        assert np.abs(out.x_dense(i, g.n) - f).sum() <= X_RTOL * np.abs(f).sum()
+
+
+@pytest.mark.parametrize("tau,eps", [(1.0, 1e-5), (5.0, 1e-6), (10.0, 1e-6)])
+def test_hk_batch_matches_oracle(gpu, tau, eps):
+    from paper_2410_21634_b200.batch import local_hk_batch
+    g = rmat_graph(20000, 150000, seed=2)
+    seeds = sample_sources(g, 20, seed=3)
+    for slots, relabel in ((8, True), (3, False)):
+        out = local_hk_batch(g, seeds, tau, eps, slots=slots, relabel=relabel)
+        for i, s in enumerate(seeds):
+            ref = O.local_hk(g, tau, int(s), eps)
+            assert out.sweeps[i] == ref["sweeps"] and out.total_ops[i] == ref["total_ops"], i
+            assert out.converged[i]
+            f = ref["f_hat"]
+            x = out.x_dense(i, g.n)
+            assert np.abs(x - f).sum() <= X_RTOL * np.abs(f).sum()
+            assert set(np.flatnonzero(f).tolist()) <= set(out.x_sparse(i)[0].tolist())

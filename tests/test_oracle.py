@@ -120,3 +120,13 @@ def test_oracle_batch_local_ch_matches_reference(pa):
     for i, k in enumerate(keys):
         assert out["sweeps"][i] == pa[f"{k}/sweeps"] and out["total_ops"][i] == pa[f"{k}/total_ops"]
         assert out["xsum"][i] == O.pairwise_sum(pa[f"{k}/x"])
+
+
+def test_oracle_batch_local_hk_matches_single(small):
+    """Threaded heat-kernel CPU baseline == per-seed local_hk (golden er60)."""
+    g = golden_graph(small, "er60")
+    out = O.batch_local_hk(g, 1.0, 1e-4, [0, 0], threads=2)
+    k = "er60/hk/tau1.0"
+    assert (out["sweeps"] == small[f"{k}/sweeps"]).all()
+    assert (out["total_ops"] == small[f"{k}/total_ops"]).all()
+    np.testing.assert_allclose(out["fsum"], small[f"{k}/f_hat"].sum(), rtol=1e-12)
