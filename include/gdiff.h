@@ -146,6 +146,18 @@ int gd_hk_push(const gd_graph *g, int64_t n_stages, const double *stage_w,
 int gd_gradient_descent(const gd_graph *g, const gd_operator *op, const double *b,
                         double *x, double *r, int64_t max_sweeps, gd_report *rep);
 
+/* Global Chebyshev (reference point): replaces chebyshev (src/global_solvers.py:
+ * 155-204); mu < L resolved by the caller (cheby_bounds).  x, r: n doubles out;
+ * rep: l1 and l2 per sweep. */
+int gd_chebyshev(const gd_graph *g, const gd_operator *op, const double *b, double *x,
+                 double *r, double mu, double L, int64_t max_sweeps, gd_report *rep);
+
+/* Heat-kernel Taylor stages: replaces hk_taylor_global (src/global_solvers.py:
+ * 207-235).  b0: stage-0 vector (n); v: (n_stages+1)*n out, v_{k+1} =
+ * fl(stage_w[k] * P v_k) with P the bare 1/d_u column scatter. */
+int gd_hk_taylor(const gd_graph *g, int64_t n_stages, const double *stage_w, const double *b0,
+                 double *v);
+
 /* Spectral norm estimate of A (Katz alpha / Chebyshev bounds): replaces
  * spectral_norm_estimate (src/graph.py:267-295), the shifted power iteration
  * on A + d_max I from the caller's start vector x0 (n entries); agrees with

@@ -94,6 +94,9 @@ SIGNATURES = {
     "gd_gradient_descent": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p,
                                       C.c_int64, C.POINTER(Report)]),
     "gd_spectral_norm": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
+    "gd_chebyshev": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_double,
+                               C.c_double, C.c_int64, C.POINTER(Report)]),
+    "gd_hk_taylor": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, _f64p]),
     "gd_batch_create": (C.c_int, [C.c_void_p, C.POINTER(BatchParams), C.POINTER(C.c_void_p)]),
     "gd_batch_destroy": (C.c_int, [C.c_void_p]),
     "gd_batch_solve_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(BatchResult),

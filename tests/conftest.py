@@ -45,6 +45,11 @@ def dyn():
 
 
 @pytest.fixture(scope="session")
+def glob():
+    return load_golden("global.npz")
+
+
+@pytest.fixture(scope="session")
 def gpu():
     """Skip-free guard: GPU tests must run on a GPU box and load the library."""
     import torch

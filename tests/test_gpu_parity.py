@@ -217,3 +217,37 @@ def test_spectral_norm_gpu(gpu, seed):
     host = spectral_norm_estimate(g, iters=200, seed=0, device=False)
     dev = spectral_norm_estimate(g, iters=200, seed=0, device=True)
     assert abs(dev - host) <= 1e-9 * abs(host)
+
+
+# ---- global Chebyshev / heat-kernel Taylor -----------
+
+@pytest.mark.parametrize("key", ["er500/ppr/ch", "er60/ppr/ch", "er60/katz/ch", "er60/ppr/ch_cap"])
+def test_global_chebyshev_matches_reference(gpu, glob, key):
+    from paper_2410_21634_b200.global_solvers import GlobalConfig, chebyshev
+    gname, prob, which = key.split("/")
+    g = golden_graph(glob, gname)
+    if prob == "ppr":
+        sys_ = S.make_ppr_system(g, 0.15, 0, 1e-6) if gname == "er500" else \
+            S.make_ppr_system(g, 0.2, 3, 1e-8)
+        cfg = GlobalConfig(max_sweeps=3) if which == "ch_cap" else None
+    else:
+        ka = float(glob["katz_alpha"])
+        sys_ = S.make_katz_system(g, ka, 0, 1e-6, lam_hat=0.0)
+        cfg = GlobalConfig(mu=1.0 - ka * g.d_max, L=1.0 + ka * g.d_max)
+    st, rep = chebyshev(sys_, cfg)
+    assert np.array_equal(st.x, glob[f"{key}/x"]) and np.array_equal(st.r, glob[f"{key}/r"])
+    assert rep.sweeps == glob[f"{key}/sweeps"] and rep.total_ops == glob[f"{key}/total_ops"]
+    assert rep.converged == bool(glob[f"{key}/converged"])
+    np.testing.assert_allclose(rep.residual_l1_trace, glob[f"{key}/l1_log"], rtol=1e-12)
+    np.testing.assert_allclose(rep.notes["l2_trace"], glob[f"{key}/l2_log"], rtol=1e-12)
+    assert rep.notes["delta_trace"] == glob[f"{key}/delta_log"].tolist()
+
+
+@pytest.mark.parametrize("tau", [1.0, 5.0])
+def test_hk_taylor_matches_reference(gpu, glob, tau):
+    from paper_2410_21634_b200.global_solvers import hk_taylor_global
+    g = golden_graph(glob, "er500")
+    st, rep = hk_taylor_global(S.make_hk_system(g, tau, 0, 1e-5))
+    k = f"er500/hk/taylor{tau}"
+    assert np.array_equal(st.x, glob[f"{k}/x"]) and np.array_equal(st.r, glob[f"{k}/r"])
+    assert rep.sweeps == glob[f"{k}/sweeps"] and rep.total_ops == glob[f"{k}/total_ops"]
