@@ -1,5 +1,6 @@
 """Golden vectors of the reference's global Chebyshev and heat-kernel Taylor
-solvers (src/global_solvers.py:155-235), produced by running the reference.
+solvers (src/global_solvers.py:155-235) and the degree-generalized feature
+push (src/dynamic.py:199-222), produced by running the reference.
 
     PYTHONPATH=/root/reference/pkg/src:. NUMBA_CACHE_DIR=/tmp/nb \\
         python tests/golden/make_golden_global.py
@@ -53,6 +54,18 @@ def main():
     for tau in (1.0, 5.0):
         put(f"er500/hk/taylor{tau}", *rgs.hk_taylor_global(rsys.make_hk_system(er500, tau, 0, 1e-5)))
     d["katz_alpha"] = np.float64(ka)
+    # degree-generalized signed feature push (src/dynamic.py:199-222)
+    from graphdiff import dynamic as rdyn
+    rng = np.random.default_rng(5)
+    src = rng.standard_normal(er500.n) * (rng.random(er500.n) < 0.05)
+    for beta in (0.0, 0.5, 1.0):
+        pair, rp = rdyn.beta_push(er500, src, 0.15, beta, 1e-4)
+        k = f"er500/betapush{beta}"
+        d[f"{k}/p"], d[f"{k}/r"] = pair.p, pair.r
+        d[f"{k}/sweeps"] = np.int64(rp.sweeps)
+        d[f"{k}/total_ops"] = np.int64(rp.total_ops)
+        d[f"{k}/parked"] = np.float64(rp.notes["parked_mass"])
+    d["betapush/source"] = src
     np.savez_compressed(os.path.join(HERE, "global.npz"), **d)
     print("wrote global.npz", len(d))
 

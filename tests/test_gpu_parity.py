@@ -251,3 +251,15 @@ def test_hk_taylor_matches_reference(gpu, glob, tau):
     k = f"er500/hk/taylor{tau}"
     assert np.array_equal(st.x, glob[f"{k}/x"]) and np.array_equal(st.r, glob[f"{k}/r"])
     assert rep.sweeps == glob[f"{k}/sweeps"] and rep.total_ops == glob[f"{k}/total_ops"]
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0])
+def test_beta_push_matches_reference(gpu, glob, beta):
+    """Degree-generalized signed feature push."""
+    from paper_2410_21634_b200.dynamic import beta_push
+    g = golden_graph(glob, "er500")
+    pair, rep = beta_push(g, glob["betapush/source"], 0.15, beta, 1e-4)
+    k = f"er500/betapush{beta}"
+    assert np.array_equal(pair.p, glob[f"{k}/p"]) and np.array_equal(pair.r, glob[f"{k}/r"])
+    assert rep.sweeps == glob[f"{k}/sweeps"] and rep.total_ops == glob[f"{k}/total_ops"]
+    assert rep.notes["parked_mass"] == glob[f"{k}/parked"]
