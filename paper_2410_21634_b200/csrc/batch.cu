@@ -427,18 +427,39 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             int32_t k = 0, u = 0, d = 0;
             bool fresh = false;
             int64_t clo = 0, chi = 0, pos = 0;
+            int64_t key = 0;
+            double val = 0.0, xo = 0.0;
             if (live) {
-                const int64_t key = A.ukey[e];
+                key = A.ukey[e];
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
                 const int64_t idx = (int64_t)k * A.ld + u;
-                const double val = rc[idx];
-                const double xo = A.x[idx];
+                val = rc[idx];
+                xo = A.x[idx];
                 A.x[idx] = __dadd_rn(xo, val);
                 rc[idx] = HK ? 0.0 : -0.0;
                 d = A.g.deg[u];
-                const unsigned long long b =
-                    S.sbase[k] + atomicAdd(A.sfill + k, (1ULL << CNT_SHIFT) + (unsigned long long)d);
+            }
+            // slot-grouped position: one packed reservation per (warp, slot)
+            unsigned long long b = 0;
+            {
+                const unsigned long long pv = live ? (1ULL << CNT_SHIFT) + (unsigned long long)d : 0ULL;
+                const unsigned peers = __match_any_sync(FULL, live ? k : -1);
+                unsigned long long pre = 0, tot = 0;
+                for (int i = 0; i < 32; ++i) {
+                    const unsigned long long vi = __shfl_sync(FULL, pv, i);
+                    if ((peers >> i) & 1u) {
+                        tot += vi;
+                        if (i < lane) pre += vi;
+                    }
+                }
+                const int leader = __ffs(peers) - 1;
+                unsigned long long old = 0;
+                if (live && lane == leader) old = atomicAdd(A.sfill + k, tot);
+                old = __shfl_sync(FULL, old, leader);
+                if (live) b = S.sbase[k] + old + pre;
+            }
+            if (live) {
                 pos = (int64_t)(b >> CNT_SHIFT);
                 const int64_t a0 = (int64_t)(b & ARC_MASK);
                 A.skey[pos] = key;
