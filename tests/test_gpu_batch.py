@@ -170,3 +170,54 @@ def test_hk_batch_matches_oracle(gpu, tau, eps):
             x = out.x_dense(i, g.n)
             assert np.abs(x - f).sum() <= X_RTOL * np.abs(f).sum()
             assert set(np.flatnonzero(f).tolist()) <= set(out.x_sparse(i)[0].tolist())
+
+
+# ---- edge cases -------------------------------------------------------------
+
+def test_batch_edge_cases(gpu):
+    """Empty batches, duplicate seeds, sweep caps and a frontier-capacity
+    overflow (reported as an error, the solver stays usable)."""
+    from paper_2410_21634_b200._lib import GdiffError
+    g = rmat_graph(5000, 30000, seed=4)
+    seeds = sample_sources(g, 24, seed=2)
+    for method in ("local-gd", "local-ch", "local-sor"):
+        solver = BatchSolver(g, 0.1, 1e-5, slots=8, method=method, max_sweeps=1_000_000)
+        empty = solver.solve(np.empty(0, np.int64))
+        assert empty.sweeps.shape == (0,) and empty.x_nodes.shape == (0,)
+        dup = np.array([seeds[0]] * 5 + [seeds[1]] * 3)
+        out = solver.solve(dup)
+        assert len(set(out.total_ops[:5].tolist())) == 1 and len(set(out.sweeps[5:].tolist())) == 1
+        assert np.array_equal(out.x_dense(0, g.n), out.x_dense(4, g.n)) or method == "local-ch" \
+            or np.abs(out.x_dense(0, g.n) - out.x_dense(4, g.n)).sum() <= 1e-12
+        solver.close()
+    # sweep cap: identical to the reference's max_sweeps behaviour
+    capped = local_gd_batch(g, seeds, 0.1, 1e-7, max_sweeps=3, slots=8)
+    ref = O.batch_local_gd(g, 0.1, 1e-7, seeds, threads=4, max_sweeps=3)
+    assert np.array_equal(capped.sweeps, ref["sweeps"]) and np.array_equal(capped.total_ops, ref["total_ops"])
+    assert np.array_equal(capped.converged, ref["converged"])
+    # capacity overflow, then a normal solve on the same solver
+    tiny = BatchSolver(g, 0.1, 1e-6, slots=8, frontier_cap=64)
+    with pytest.raises(GdiffError):
+        tiny.solve(seeds)
+    tiny.close()
+    solver = BatchSolver(g, 0.1, 1e-6, slots=8)
+    a = solver.solve(seeds)
+    ref = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=4)
+    assert np.array_equal(a.total_ops, ref["total_ops"])
+    solver.close()
+
+
+def test_batch_rejects_bad_input(gpu):
+    g = rmat_graph(2000, 8000, seed=1)
+    iso = int(np.flatnonzero(g.degrees == 0)[0]) if (g.degrees == 0).any() else None
+    with pytest.raises(ValueError):
+        local_gd_batch(g, [g.n], 0.1, 1e-6)
+    if iso is not None:
+        with pytest.raises(ValueError):
+            local_gd_batch(g, [iso], 0.1, 1e-6)
+    with pytest.raises(ValueError):
+        BatchSolver(g, 1.5, 1e-6)
+    with pytest.raises(ValueError):
+        BatchSolver(g, 0.1, 1e-6, method="local-sor", omega=2.5)
+    with pytest.raises(ValueError):
+        BatchSolver(g, 0.1, 1e-6, method="local-ch", mu=0.5, L=0.4)
