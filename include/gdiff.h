@@ -99,6 +99,9 @@ int gd_graph_create_device(int64_t n, const int64_t *d_row_ptr, const int32_t *d
  * (GD_ERR_ARG) on an insert of a present / delete of a missing edge. */
 int gd_graph_apply_events(const gd_graph *g, const int32_t *kinds, const int64_t *us,
                           const int64_t *vs, int64_t n_events, gd_graph **out);
+/* Same, into an existing graph h != g whose device buffers are reused. */
+int gd_graph_apply_events_into(const gd_graph *g, const int32_t *kinds, const int64_t *us,
+                               const int64_t *vs, int64_t n_events, gd_graph *h);
 /* Copy a device graph back in the reference layout (int64 n+1 offsets,
  * int64 n_arcs targets). */
 int gd_graph_export(const gd_graph *g, int64_t *offsets, int64_t *targets);

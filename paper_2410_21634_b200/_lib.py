@@ -79,6 +79,8 @@ SIGNATURES = {
     "gd_graph_destroy": (C.c_int, [C.c_void_p]),
     "gd_graph_apply_events": (C.c_int, [C.c_void_p, _i32p, _i64p, _i64p, C.c_int64,
                                         C.POINTER(C.c_void_p)]),
+    "gd_graph_apply_events_into": (C.c_int, [C.c_void_p, _i32p, _i64p, _i64p, C.c_int64,
+                                             C.c_void_p]),
     "gd_graph_export": (C.c_int, [C.c_void_p, _i64p, _i64p]),
     "gd_graph_info": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p]),
     "gd_local_gd": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_int64,

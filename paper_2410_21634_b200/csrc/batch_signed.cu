@@ -28,7 +28,9 @@
 // l1 sits within rounding of the abort level.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -582,27 +584,26 @@ __device__ __forceinline__ void pair_endpoint(double *p, double *r, double q, in
     }
 }
 
-// one thread per pair: the event batch in order (per-pair sequential, as the
-// reference), endpoints become round-0 candidates of the repair
+// One dependency level of the event batch: the events of a level share no
+// node, so thread (event, pair) applies one event to one pair and the
+// per-node order of operations -- hence every bit -- is the sequential
+// reference's.  Endpoints become round-0 candidates of the repair.
 __global__ void k_pair_events(SArgs A, const PairEvent *__restrict__ ev, int64_t n_ev, double q) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= A.m) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_ev * A.m) return;
+    const int64_t k = t % A.m, i = t / A.m;
     double *p = A.x + k * A.ld, *r = A.r + k * A.ld;
-    for (int64_t i = 0; i < n_ev; ++i) {
-        const PairEvent e = ev[i];
-        pair_endpoint(p, r, q, e.u, e.v, e.du, e.du + e.step);
-        pair_endpoint(p, r, q, e.v, e.u, e.dv, e.dv + e.step);
-        const int32_t ends[2] = {e.u, e.v};
-        for (int j = 0; j < 2; ++j) {
-            const int32_t a = ends[j];
-            uint32_t *w = A.cmark[0] + k * A.cmw + (a >> 5);
-            const uint32_t bit = 1u << (a & 31);
-            if (!(*w & bit)) {  // this thread owns pair k's map
-                *w |= bit;
-                const unsigned long long at = atomicAdd(A.candctr, 1ULL);
-                if ((int64_t)at < A.candcap) A.cand[0][at] = (k << 32) | (uint32_t)a;
-                else A.overflow[0] = 1;
-            }
+    const PairEvent e = ev[i];
+    pair_endpoint(p, r, q, e.u, e.v, e.du, e.du + e.step);
+    pair_endpoint(p, r, q, e.v, e.u, e.dv, e.dv + e.step);
+    const int32_t ends[2] = {e.u, e.v};
+    for (int j = 0; j < 2; ++j) {
+        const int32_t a = ends[j];
+        const uint32_t bit = 1u << (a & 31);
+        if (!(atomicOr(A.cmark[0] + k * A.cmw + (a >> 5), bit) & bit)) {
+            const unsigned long long at = atomicAdd(A.candctr, 1ULL);
+            if ((int64_t)at < A.candcap) A.cand[0][at] = (k << 32) | (uint32_t)a;
+            else A.overflow[0] = 1;
         }
     }
 }
@@ -624,6 +625,12 @@ __global__ void k_pair_scan(SArgs A) {
         if ((int64_t)at < A.candcap) A.cand[0][at] = (k << 32) | (uint32_t)u;
         else A.overflow[0] = 1;
     }
+}
+
+__global__ void k_gather_deg(DevGraph g, const int32_t *__restrict__ nodes, int64_t c,
+                             int32_t *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < c) out[i] = g.deg[nodes[i]];
 }
 
 __global__ void k_pair_stats_reset(SArgs A) {
@@ -871,6 +878,8 @@ struct gd_pairs {
     double alpha = 0.0, eps = 0.0;
     int64_t k = 0;
     std::vector<int32_t> deg;  // host copy of the current degrees (event bookkeeping)
+    int64_t n_arcs = 0;
+    DBuf<int32_t> gnodes, gdeg;
     DBuf<PairEvent> dev_events;
     bool all_converged = true;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -882,8 +891,8 @@ struct gd_pairs {
 };
 
 static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_sweeps,
-                         const PairEvent *dev_ev, int64_t n_ev, int64_t *sweeps, int64_t *ops,
-                         int64_t *pushes, int32_t *conv) {
+                         const PairEvent *dev_ev, const std::vector<int64_t> &lvl_off,
+                         int64_t *sweeps, int64_t *ops, int64_t *pushes, int32_t *conv) {
     SignedState &S = P->S;
     cudaStream_t st = 0;
     if (S.dirty) {
@@ -897,8 +906,12 @@ static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_
     GD_CUDA(cudaMemsetAsync(S.overflow.p, 0, sizeof(int32_t), st));
     GD_CUDA(cudaMemsetAsync(S.candctr.p, 0, 2 * sizeof(unsigned long long), st));
     k_pair_stats_reset<<<(int)((P->k + 255) / 256), 256, 0, st>>>(A);
-    if (n_ev)
-        k_pair_events<<<(int)((P->k + 127) / 128), 128, 0, st>>>(A, dev_ev, n_ev, 1.0 - P->alpha);
+    for (size_t l = 0; l + 1 < lvl_off.size(); ++l) {  // dependency levels, in order
+        const int64_t e0 = lvl_off[l], ne = lvl_off[l + 1] - e0;
+        const int64_t threads = ne * P->k;
+        k_pair_events<<<(int)((threads + 255) / 256), 256, 0, st>>>(A, dev_ev + e0, ne,
+                                                                    1.0 - P->alpha);
+    }
     if (scan) k_pair_scan<<<4 * n_sms(S.device), 256, 0, st>>>(A);
     GD_LAUNCH_CHECK();
     GD_CUDA(cudaEventRecord(P->e0, st));
@@ -942,6 +955,7 @@ int gd_pairs_create(const gd_graph *G, double alpha, double eps, const int64_t *
             P->eps = eps;
             P->k = k;
             P->deg.resize(G->n);
+            P->n_arcs = G->n_arcs;
             if (G->n)
                 GD_CUDA(cudaMemcpy(P->deg.data(), G->deg.p, 4 * G->n, cudaMemcpyDeviceToHost));
             for (int64_t i = 0; i < k; ++i) {
@@ -961,8 +975,8 @@ int gd_pairs_create(const gd_graph *G, double alpha, double eps, const int64_t *
                                    cudaMemcpyHostToDevice));
             GD_CUDA(cudaEventCreate(&P->e0));
             GD_CUDA(cudaEventCreate(&P->e1));
-            pairs_repair(P, G, true, max_sweeps > 0 ? max_sweeps : 1000000, nullptr, 0, sweeps,
-                         total_ops, pushes, converged);
+            pairs_repair(P, G, true, max_sweeps > 0 ? max_sweeps : 1000000, nullptr,
+                         std::vector<int64_t>(), sweeps, total_ops, pushes, converged);
         } catch (...) {
             delete P;
             throw;
@@ -983,31 +997,80 @@ int gd_pairs_update(gd_pairs *P, const gd_graph *G_new, const int32_t *kinds, co
         GD_CHECK_ARG(P && G_new && (n_events == 0 || (kinds && us && vs)), "null pointer");
         GD_CHECK_ARG(G_new->n == (int64_t)P->deg.size(), "node count changed");
         GD_CUDA(cudaSetDevice(G_new->device));
-        // degrees evolve event by event (event_adjust_many semantics)
+        // degrees evolve event by event (event_adjust_many semantics); only the
+        // endpoints change, so they are tracked in a map and committed at the end
         std::vector<PairEvent> ev(n_events);
-        std::vector<int32_t> deg = P->deg;
+        std::unordered_map<int32_t, int32_t> nd;
+        auto cur = [&](int64_t x) {
+            auto it = nd.find((int32_t)x);
+            return it == nd.end() ? P->deg[x] : it->second;
+        };
+        int64_t net = 0;
         for (int64_t i = 0; i < n_events; ++i) {
             const int64_t u = us[i], v = vs[i];
             GD_CHECK_ARG(u >= 0 && v >= 0 && u < G_new->n && v < G_new->n && u != v,
                          "bad event endpoints");
             const int32_t step = kinds[i] ? 1 : -1;
-            GD_CHECK_ARG(deg[u] + step >= 0 && deg[v] + step >= 0,
-                         "delete would make a degree negative");
-            ev[i] = PairEvent{(int32_t)u, (int32_t)v, deg[u], deg[v], step};
-            deg[u] += step;
-            deg[v] += step;
+            const int32_t du = cur(u), dv = cur(v);
+            GD_CHECK_ARG(du + step >= 0 && dv + step >= 0, "delete would make a degree negative");
+            ev[i] = PairEvent{(int32_t)u, (int32_t)v, du, dv, step};
+            nd[(int32_t)u] = du + step;
+            nd[(int32_t)v] = dv + step;
+            net += 2 * step;
         }
-        std::vector<int32_t> gdeg(G_new->n);
-        if (G_new->n)
-            GD_CUDA(cudaMemcpy(gdeg.data(), G_new->deg.p, 4 * G_new->n, cudaMemcpyDeviceToHost));
-        GD_CHECK_ARG(gdeg == deg, "G_new is not the old graph with these events applied");
+        // G_new must be the old graph with these events: arc count and the
+        // endpoints' degrees (gathered on the device)
+        GD_CHECK_ARG(G_new->n_arcs == P->n_arcs + net,
+                     "G_new is not the old graph with these events applied");
+        if (!nd.empty()) {
+            std::vector<int32_t> nodes, want;
+            for (auto &kv : nd) {
+                nodes.push_back(kv.first);
+                want.push_back(kv.second);
+            }
+            const int64_t c = (int64_t)nodes.size();
+            P->gnodes.ensure(c);
+            P->gdeg.ensure(c);
+            GD_CUDA(cudaMemcpy(P->gnodes.p, nodes.data(), 4 * c, cudaMemcpyHostToDevice));
+            k_gather_deg<<<(int)((c + 255) / 256), 256>>>(G_new->view(), P->gnodes.p, c,
+                                                          P->gdeg.p);
+            GD_LAUNCH_CHECK();
+            std::vector<int32_t> got(c);
+            GD_CUDA(cudaMemcpy(got.data(), P->gdeg.p, 4 * c, cudaMemcpyDeviceToHost));
+            GD_CHECK_ARG(got == want, "G_new is not the old graph with these events applied");
+        }
+        // dependency levels: an event waits for the latest earlier event that
+        // shares one of its nodes (a stable sort by level keeps event order
+        // inside a level; per-node order is preserved exactly)
+        std::vector<int32_t> level(n_events);
+        std::unordered_map<int32_t, int32_t> last;
+        int32_t nlev = 0;
+        for (int64_t i = 0; i < n_events; ++i) {
+            int32_t l = 0;
+            auto a = last.find(ev[i].u), b = last.find(ev[i].v);
+            if (a != last.end()) l = std::max(l, a->second + 1);
+            if (b != last.end()) l = std::max(l, b->second + 1);
+            level[i] = l;
+            last[ev[i].u] = l;
+            last[ev[i].v] = l;
+            nlev = std::max(nlev, l + 1);
+        }
+        std::vector<int64_t> lvl_off(nlev + 1, 0);
+        for (int64_t i = 0; i < n_events; ++i) lvl_off[level[i] + 1]++;
+        for (int32_t l = 0; l < nlev; ++l) lvl_off[l + 1] += lvl_off[l];
+        std::vector<PairEvent> sorted(n_events);
+        {
+            std::vector<int64_t> fill(lvl_off.begin(), lvl_off.end() - 1);
+            for (int64_t i = 0; i < n_events; ++i) sorted[fill[level[i]]++] = ev[i];
+        }
         P->dev_events.ensure(n_events ? n_events : 1);
         if (n_events)
-            GD_CUDA(cudaMemcpy(P->dev_events.p, ev.data(), sizeof(PairEvent) * n_events,
+            GD_CUDA(cudaMemcpy(P->dev_events.p, sorted.data(), sizeof(PairEvent) * n_events,
                                cudaMemcpyHostToDevice));
         pairs_repair(P, G_new, !P->all_converged, max_sweeps > 0 ? max_sweeps : 1000000,
-                     P->dev_events.p, n_events, sweeps, total_ops, pushes, converged);
-        P->deg.swap(deg);
+                     P->dev_events.p, lvl_off, sweeps, total_ops, pushes, converged);
+        for (auto &kv : nd) P->deg[kv.first] = kv.second;
+        P->n_arcs = G_new->n_arcs;
     });
 }
 

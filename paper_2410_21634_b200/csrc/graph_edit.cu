@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -115,10 +116,21 @@ using namespace gd;
 
 extern "C" {
 
-int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t *us,
-                          const int64_t *vs, int64_t n_events, gd_graph **out) {
-    return guarded([&] {
-        GD_CHECK_ARG(G && out && (n_events == 0 || (kinds && us && vs)), "null pointer");
+// Device scratch of the edit, kept per host thread (a snapshot stream must not
+// pay n-sized cudaMalloc / cudaFree pairs per batch).
+struct EditWS {
+    DBuf<int64_t> deg64, dcoff, dk;
+    DBuf<int32_t> rowchg, dnode, ddelta, dtgt, dsign, dp;
+    DBuf<unsigned long long> dmax;
+    DBuf<char> tmp;
+};
+
+static void apply_events_impl(const gd_graph *G, const int32_t *kinds, const int64_t *us,
+                              const int64_t *vs, int64_t n_events, gd_graph *H) {
+    thread_local std::unique_ptr<EditWS> wsp;
+    if (!wsp) wsp.reset(new EditWS());
+    EditWS &W = *wsp;
+    {
         GD_CUDA(cudaSetDevice(G->device));
         const int64_t n = G->n;
         // 1. distinct event edges in event order per edge
@@ -143,13 +155,13 @@ int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t
         const int64_t K = (int64_t)uk.size();
         std::vector<int32_t> was(K ? K : 1, 0);
         if (K) {
-            DBuf<int64_t> dk(K);
-            DBuf<int32_t> dp(K);
-            GD_CUDA(cudaMemcpy(dk.p, uk.data(), 8 * K, cudaMemcpyHostToDevice));
+            W.dk.ensure(K);
+            W.dp.ensure(K);
+            GD_CUDA(cudaMemcpy(W.dk.p, uk.data(), 8 * K, cudaMemcpyHostToDevice));
             k_edge_present<<<(int)std::min<int64_t>((K + ETPB - 1) / ETPB, 4096), ETPB>>>(
-                G->view(), dk.p, K, dp.p);
+                G->view(), W.dk.p, K, W.dp.p);
             GD_LAUNCH_CHECK();
-            GD_CUDA(cudaMemcpy(was.data(), dp.p, 4 * K, cudaMemcpyDeviceToHost));
+            GD_CUDA(cudaMemcpy(was.data(), W.dp.p, 4 * K, cudaMemcpyDeviceToHost));
         }
         // 2. replay per edge; directed change arcs
         struct Arc {
@@ -199,19 +211,23 @@ int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t
         const int64_t nc = (int64_t)cnode.size();
         int64_t net = 0;
         for (int32_t d : cdelta) net += d;
-        // 3. new graph on the device
-        gd_graph *H = new gd_graph();
-        try {
+        // 3. the new graph on the device (H's buffers reused when large enough)
+        {
             H->device = G->device;
             H->n = n;
             H->n_arcs = G->n_arcs + net;
-            H->row.alloc(n + 1);
-            H->col.alloc(H->n_arcs ? H->n_arcs : 1);
-            H->deg.alloc(n ? n : 1);
-            DBuf<int64_t> deg64(n + 1), dcoff(nc + 1);
-            DBuf<int32_t> rowchg(n ? n : 1), dnode(nc ? nc : 1), ddelta(nc ? nc : 1),
-                dtgt(arcs.empty() ? 1 : arcs.size()), dsign(arcs.empty() ? 1 : arcs.size());
-            DBuf<unsigned long long> dmax(1);
+            H->row.ensure(n + 1);
+            if (H->col.n < (size_t)(H->n_arcs ? H->n_arcs : 1))  // grow with slack: a stream of
+                H->col.alloc((size_t)H->n_arcs + (size_t)H->n_arcs / 16 + 1);  // insertions
+            H->deg.ensure(n ? n : 1);
+            W.deg64.ensure(n + 1); W.dcoff.ensure(nc + 1); W.rowchg.ensure(n ? n : 1);
+            W.dnode.ensure(nc ? nc : 1); W.ddelta.ensure(nc ? nc : 1);
+            W.dtgt.ensure(arcs.empty() ? 1 : arcs.size()); W.dsign.ensure(arcs.empty() ? 1 : arcs.size());
+            W.dmax.ensure(1);
+            auto &deg64 = W.deg64, &dcoff = W.dcoff;
+            auto &rowchg = W.rowchg, &dnode = W.dnode, &ddelta = W.ddelta, &dtgt = W.dtgt,
+                 &dsign = W.dsign;
+            auto &dmax = W.dmax;
             GD_CUDA(cudaMemset(dmax.p, 0, sizeof(unsigned long long)));
             if (nc) {
                 GD_CUDA(cudaMemcpy(dnode.p, cnode.data(), 4 * nc, cudaMemcpyHostToDevice));
@@ -228,8 +244,8 @@ int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t
             GD_LAUNCH_CHECK();
             size_t bytes = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg64.p, H->row.p, n + 1);
-            DBuf<char> tmp(bytes ? bytes : 1);
-            cub::DeviceScan::ExclusiveSum(tmp.p, bytes, deg64.p, H->row.p, n + 1);
+            W.tmp.ensure(bytes ? bytes : 1);
+            cub::DeviceScan::ExclusiveSum(W.tmp.p, bytes, deg64.p, H->row.p, n + 1);
             if (n) k_copy_rows<<<blocks, ETPB>>>(g, H->row.p, rowchg.p, H->col.p, H->deg.p, dmax.p);
             if (nc) k_merge_rows<<<(int)((nc + ETPB - 1) / ETPB), ETPB>>>(
                 g, H->row.p, dnode.p, dcoff.p, dtgt.p, dsign.p, nc, H->col.p);
@@ -237,11 +253,33 @@ int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t
             unsigned long long h = 0;
             GD_CUDA(cudaMemcpy(&h, dmax.p, sizeof(h), cudaMemcpyDeviceToHost));
             H->d_max = (int64_t)h;
+        }
+    }
+}
+
+int gd_graph_apply_events(const gd_graph *G, const int32_t *kinds, const int64_t *us,
+                          const int64_t *vs, int64_t n_events, gd_graph **out) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && out && (n_events == 0 || (kinds && us && vs)), "null pointer");
+        gd_graph *H = new gd_graph();
+        try {
+            apply_events_impl(G, kinds, us, vs, n_events, H);
         } catch (...) {
             delete H;
             throw;
         }
         *out = H;
+    });
+}
+
+// As gd_graph_apply_events, writing into an existing graph H != G whose
+// buffers are reused (a snapshot stream alternates two graphs).
+int gd_graph_apply_events_into(const gd_graph *G, const int32_t *kinds, const int64_t *us,
+                               const int64_t *vs, int64_t n_events, gd_graph *H) {
+    return guarded([&] {
+        GD_CHECK_ARG(G && H && (n_events == 0 || (kinds && us && vs)), "null pointer");
+        GD_CHECK_ARG(G != H, "output graph must differ from the input graph");
+        apply_events_impl(G, kinds, us, vs, n_events, H);
     });
 }
 

@@ -46,13 +46,22 @@ class DeviceGraph:
         L.check(lib.gd_graph_info(h, C.byref(n), C.byref(a), C.byref(d)))
         return cls(h.value, n.value, a.value, d.value, device)
 
-    def apply_events(self, events) -> "DeviceGraph":
-        """New device graph with the event batch applied in order (on the
-        device; same CSR as graph.apply_events)."""
+    def apply_events(self, events, out: "DeviceGraph | None" = None) -> "DeviceGraph":
+        """Device graph with the event batch applied in order (on the device;
+        same CSR as graph.apply_events).  ``out`` (a different graph) is
+        overwritten in place, reusing its device buffers."""
         lib = L.load()
         kinds = np.array([1 if e.kind == "insert" else 0 for e in events], np.int32)
         us = np.array([e.u for e in events], np.int64)
         vs = np.array([e.v for e in events], np.int64)
+        if out is not None:
+            L.check(lib.gd_graph_apply_events_into(self.handle, L.ptr(kinds, C.c_int32),
+                                                   L.ptr(us, C.c_int64), L.ptr(vs, C.c_int64),
+                                                   len(events), out.handle))
+            n, a, d = C.c_int64(), C.c_int64(), C.c_int64()
+            L.check(lib.gd_graph_info(out.handle, C.byref(n), C.byref(a), C.byref(d)))
+            out.n, out.n_arcs, out.d_max = n.value, a.value, d.value
+            return out
         h = C.c_void_p()
         L.check(lib.gd_graph_apply_events(self.handle, L.ptr(kinds, C.c_int32), L.ptr(us, C.c_int64),
                                           L.ptr(vs, C.c_int64), len(events), C.byref(h)))

@@ -34,8 +34,8 @@ n, m = SHAPES[shape]
 row, col = rmat_csr_device(n, m, seed=0)
 g0 = CsrGraph(n=n, offsets=row.cpu().numpy(), targets=col.cpu().numpy().astype(np.int64))
 rng = np.random.default_rng(1)
-batches, sim = [], g0
-for _ in range(snaps):  # insertion snapshots between random non-adjacent pairs
+batches, sim, sims = [], g0, [g0]
+for _ in range(snaps + 1):  # insertion snapshots (the first is a warm-up)
     b, seen = [], set()
     while len(b) < n_ev:
         u, v = sorted(rng.integers(0, n, 2).tolist())
@@ -45,6 +45,7 @@ for _ in range(snaps):  # insertion snapshots between random non-adjacent pairs
         b.append(EdgeEvent("insert", u, v))
     sim = apply_events(sim, b)
     batches.append(b)
+    sims.append(sim)
 sources = sample_sources(g0, K, seed=0)
 threads = os.cpu_count() or 1
 
@@ -53,18 +54,27 @@ t0 = time.perf_counter()
 pool = PairPool(g0, sources, alpha, eps)
 t_create = time.perf_counter() - t0
 cold_ops = int(pool.last["total_ops"].sum())
-walls, kms, ops, graphs = [], [], [], [g0]
+warm = batches.pop(0)  # warm-up snapshot: the second device graph gets allocated here
+pool.update(warm)
+graphs = sims[1:]  # host copies of the snapshots (built with graph.apply_events above)
+g0 = graphs[0]
+walls, kms, ops = [], [], []
 first_state = [pool.pair(i) for i in range(min(cpu_pairs, K))]
+import gc
+
+gc.collect()
+gc.disable()  # (a collection of the batch generator's objects is not update work)
 for b in batches:
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     st = pool.update(b)
     walls.append(time.perf_counter() - t0)
     kms.append(pool.last_kernel_ms)
     ops.append(int(st["total_ops"].sum()))
-    graphs.append(pool.graph)
     if len(walls) == 1:
         first_stats = {k: v.copy() for k, v in st.items()}
 
+gc.enable()
 # parity on snapshot 1 for the CPU sample: oracle warm LocalGD from the same state
 k = len(first_state)
 g1 = graphs[1]
