@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             const bool live = e < F;
             int32_t k = 0, u = 0, d = 0;
             bool fresh = false;
-            int64_t clo = 0, chi = 0, pos = 0;
+            int64_t clo = 0, chi = 0, cfull = 0, pos = 0;
             int64_t key = 0;
             double val = 0.0, xo = 0.0;
             if (live) {
@@ -473,17 +473,22 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
                 // chunks (32 arcs) whose first arc lies in this entry: [clo, chi)
                 clo = (a0 + 31) >> 5;
                 chi = min((a0 + d + 31) >> 5, A.ccap);
+                cfull = (a0 + d) >> 5;  // chunks below this one lie entirely in the entry
             }
-            // hubs own thousands of chunks, so the warp writes them together
+            // hubs own thousands of chunks, so the warp writes them together;
+            // bit 31 marks a chunk whose 32 arcs all belong to this entry
             unsigned big = __ballot_sync(FULL, chi - clo > 4);
             if (!(big >> lane & 1u))
-                for (int64_t c = clo; c < chi; ++c) A.chunk_e[c] = (int32_t)pos;
+                for (int64_t c = clo; c < chi; ++c)
+                    A.chunk_e[c] = (int32_t)((uint32_t)pos | (c < cfull ? 0x80000000u : 0u));
             while (big) {
                 const int src = __ffs(big) - 1;
                 big &= big - 1;
                 const int64_t lo2 = __shfl_sync(FULL, clo, src), hi2 = __shfl_sync(FULL, chi, src);
-                const int32_t e2 = (int32_t)__shfl_sync(FULL, pos, src);
-                for (int64_t c = lo2 + lane; c < hi2; c += 32) A.chunk_e[c] = e2;
+                const int64_t cf2 = __shfl_sync(FULL, cfull, src);
+                const uint32_t e2 = (uint32_t)__shfl_sync(FULL, pos, src);
+                for (int64_t c = lo2 + lane; c < hi2; c += 32)
+                    A.chunk_e[c] = (int32_t)(e2 | (c < cf2 ? 0x80000000u : 0u));
             }
         slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
@@ -517,14 +522,18 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             for (int q = 0; q < UNROLL; q++) {
                 const int64_t ch = cb + q;
                 const bool live = ch < c1;
-                const int64_t e = live ? A.chunk_e[ch] : 0;
+                const uint32_t raw = live ? (uint32_t)A.chunk_e[ch] : 0u;  // same for all lanes
+                const int64_t e = raw & 0x7fffffffu;
                 const int64_t a = ch << 5;
-                // entries starting inside (a, a+32): one bit per start offset
-                const int64_t wi = e + 1 + lane;
-                const int64_t st = (live && wi < F) ? fa[wi] : INT64_MAX;
-                const int64_t pos = st - a;
-                const unsigned starts = __reduce_or_sync(FULL, pos < 32 ? (1u << pos) : 0u);
-                const int64_t me = e + __popc(starts & ((2u << lane) - 1u));
+                int64_t me = e;
+                if (!(raw >> 31)) {
+                    // entries starting inside (a, a+32): one bit per start offset
+                    const int64_t wi = e + 1 + lane;
+                    const int64_t st = (live && wi < F) ? fa[wi] : INT64_MAX;
+                    const int64_t pos = st - a;
+                    const unsigned starts = __reduce_or_sync(FULL, pos < 32 ? (1u << pos) : 0u);
+                    me = e + __popc(starts & ((2u << lane) - 1u));
+                }
                 const int64_t p = a + lane;
                 valid[q] = live && p < P;
                 k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
