@@ -27,7 +27,7 @@ struct FifoBatchArgs {
     int64_t n, ld, max_sweeps, n_seeds, xcap;
     double *x, *r;
     int32_t *queue;        // ld + 2 per slot
-    uint8_t *qmark, *tmark;
+    uint8_t *qmark;
     int32_t *touched;      // touched list per slot (ld)
     const int64_t *seeds;
     unsigned long long *next_seed, *cursor;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
     const int64_t off = (int64_t)slot * A.ld;
     double *x = A.x + off, *r = A.r + off;
     int32_t *queue = A.queue + (int64_t)slot * (A.ld + 2);
-    uint8_t *qmark = A.qmark + off, *tmark = A.tmark + off;
+    uint8_t *qmark = A.qmark + off;
     int32_t *touched = A.touched + off;
     const int64_t sent = A.n, qcap = A.n + 2;
 
@@ -65,11 +65,12 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
         si = __shfl_sync(FULL, si, 0);
         if ((int64_t)si >= A.n_seeds) break;
         const int32_t s = (int32_t)A.seeds[si];
-        // b = alpha e_s, x = 0 (slot is clean); seed enqueue (:59-69)
+        // b = alpha e_s, x = 0 (slot is clean); seed enqueue (:59-69).  A node
+        // is "touched" once its r word is not +0.0: residuals that become
+        // exactly zero are stored as -0.0, which adds like +0.0.
         int64_t ntouch = 1;
         if (lane == 0) {
             r[s] = A.alpha;
-            tmark[s] = 1;
             touched[0] = s;
         }
         __syncwarp();
@@ -86,6 +87,11 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
             }
             rear = 2;
             int64_t svol = 0;
+            // software pipeline: the next pop's node, r, degree and row are
+            // loaded while the current pop scatters (r re-read if it was hit)
+            int64_t pu = -1, prs = 0;
+            double pr = 0.0;
+            int32_t pd = 0, pcol = 0;  // (pcol: this lane's first neighbour of the next pop)
             __syncwarp();
             for (;;) {
                 const int64_t u = queue[front];
@@ -93,6 +99,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 if (u == sent) {  // sweep boundary (:102-144)
                     ops += svol;
                     sweeps += 1;
+                    pu = -1;
                     if (front == rear) break;
                     if (sweeps >= A.max_sweeps) {
                         conv = 0;
@@ -104,33 +111,58 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                     __syncwarp();
                     continue;
                 }
+                double ru;
+                int32_t d, c0;
+                int64_t rs;
+                if (u == pu) {
+                    ru = pr;
+                    d = pd;
+                    rs = prs;
+                    c0 = pcol;
+                } else {
+                    ru = r[u];
+                    d = A.g.deg[u];
+                    rs = A.g.row[u];
+                    c0 = lane < d ? A.g.col[rs + lane] : 0;
+                }
+                pu = -1;
                 if (lane == 0) qmark[u] = 0;
-                const double ru = r[u];
-                const int32_t d = A.g.deg[u];
                 const double th = theta_d(A.tcoeff, d);
                 if (A.sgn ? fabs(ru) < th : ru < th) {
                     __syncwarp();
                     continue;
+                }
+                if (front != rear) {  // prefetch the next pop
+                    const int64_t nx = queue[front];
+                    if (nx != sent) {
+                        pu = nx;
+                        pr = r[nx];
+                        pd = A.g.deg[nx];
+                        prs = A.g.row[nx];
+                        pcol = lane < pd ? A.g.col[prs + lane] : 0;
+                    }
                 }
                 svol += d;
                 pushes += 1;
                 const double res = __dmul_rn(A.omega, ru);
                 if (lane == 0) {
                     x[u] = __dadd_rn(x[u], res);  // x_gain = 1
-                    r[u] = __dsub_rn(ru, res);
+                    const double rn = __dsub_rn(ru, res);
+                    r[u] = __double_as_longlong(rn) == 0 ? -0.0 : rn;
                 }
                 const double w = __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta);
-                const int64_t rs = A.g.row[u];
+                bool hit = false;
                 for (int64_t base = 0; base < d; base += 32) {
                     const int64_t j = base + lane;
                     bool act = false, fresh = false;
                     int32_t v = 0;
                     if (j < d) {
-                        v = A.g.col[rs + j];
-                        const double rv = __dadd_rn(r[v], __dmul_rn(res, w));
-                        r[v] = rv;
-                        fresh = !tmark[v];
-                        if (fresh) tmark[v] = 1;
+                        v = base == 0 ? c0 : A.g.col[rs + j];
+                        const double old = r[v];
+                        const double rv = __dadd_rn(old, __dmul_rn(res, w));
+                        r[v] = __double_as_longlong(rv) == 0 ? -0.0 : rv;
+                        fresh = __double_as_longlong(old) == 0;
+                        hit |= v == pu;
                         if (!qmark[v]) {
                             const double tv = theta_d(A.tcoeff, A.g.deg[v]);
                             act = A.sgn ? fabs(rv) >= tv : rv >= tv;
@@ -150,6 +182,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                     ntouch += __popc(fb);
                 }
                 __syncwarp();
+                if (__any_sync(FULL, hit)) pr = r[pu];  // the scatter changed the next pop's r
                 const double ru2 = __dsub_rn(ru, res);  // self re-check (:176-185)
                 if (A.sgn ? fabs(ru2) >= th : ru2 >= th) {
                     if (lane == 0) {
@@ -179,7 +212,6 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 x[v] = 0.0;
                 r[v] = 0.0;
                 qmark[v] = 0;
-                tmark[v] = 0;
             }
             const unsigned nzb = __ballot_sync(FULL, xv != 0.0);
             if (xv != 0.0) {
@@ -211,7 +243,7 @@ struct FifoBatchState {
     int64_t ld = 0;
     DBuf<double> x, r;
     DBuf<int32_t> queue, touched;
-    DBuf<uint8_t> qmark, tmark;
+    DBuf<uint8_t> qmark;
     DBuf<unsigned long long> ctr;  // next_seed
 };
 
@@ -221,7 +253,7 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
     if (slots <= 0) {
         size_t fr = 0, tot = 0;
         GD_CUDA(cudaMemGetInfo(&fr, &tot));
-        const int64_t per = ld * (8 + 8 + 4 + 1 + 1 + 4) + 8;
+        const int64_t per = ld * (8 + 8 + 4 + 1 + 4) + 8;
         int64_t by_mem = (int64_t)(fr / 3) / per;
         int64_t resident = (int64_t)n_sms(G->device) * 64;  // warps
         slots = (int)(by_mem < resident ? (by_mem < 1 ? 1 : by_mem) : resident);
@@ -233,11 +265,10 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
         const size_t sn = (size_t)slots * (size_t)ld;
         F->x.alloc(sn); F->r.alloc(sn); F->touched.alloc(sn);
         F->queue.alloc((size_t)slots * (size_t)(ld + 2));
-        F->qmark.alloc(sn); F->tmark.alloc(sn);
+        F->qmark.alloc(sn);
         GD_CUDA(cudaMemset(F->x.p, 0, sizeof(double) * sn));
         GD_CUDA(cudaMemset(F->r.p, 0, sizeof(double) * sn));
         GD_CUDA(cudaMemset(F->qmark.p, 0, sn));
-        GD_CUDA(cudaMemset(F->tmark.p, 0, sn));
         F->ctr.alloc(1);
     } catch (...) {
         delete F;
@@ -266,7 +297,7 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
     A.max_sweeps = p.max_sweeps > 0 ? p.max_sweeps : 1000000;
     A.n_seeds = n_seeds;
     A.xcap = xcap;
-    A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p; A.tmark = F->tmark.p;
+    A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p;
     A.touched = F->touched.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv; A.xoff = xoff;
     A.xcnt = xcnt; A.xnodes = xnodes; A.xvals = xvals; A.nslots = F->nslots;
