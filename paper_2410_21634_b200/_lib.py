@@ -135,6 +135,8 @@ def load(require_gpu: bool = True):
                     f"{LIB_PATH} not built; run `python -m paper_2410_21634_b200.build`")
             lib = C.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
+                if os.environ.get("GDIFF_LIB") and not hasattr(lib, name):
+                    continue  # (A/B experiments against an older build)
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -68,6 +68,7 @@ namespace {
 
 constexpr int BT = 512;   // threads per block of the round kernel
 constexpr int UNROLL = 4; // 32-arc chunks in flight per warp in phase B
+constexpr int SUPER = 16; // UNROLL-chunk groups per block super-chunk in phase B
 constexpr int CNT_SHIFT = 36;
 constexpr unsigned long long ARC_MASK = (1ULL << CNT_SHIFT) - 1ULL;
 constexpr unsigned FULL = 0xffffffffu;
@@ -91,9 +92,18 @@ struct RoundArgs {
     int32_t *seed;  // per slot: seed in working ids
     unsigned long long *touched, *pushed_cnt;
     int64_t *ukey;        // next frontier as appended: (slot << 32 | node), any order
+    int64_t *uarc;        // its first arc offsets in append order (ungrouped mode)
+    int grouped;          // 1: phase A regroups the frontier by slot group and phase B
+                          //    walks it with a grid-wide window (slot vectors > L2);
+                          // 0: append order, contiguous per-block ranges (L2 holds
+                          //    every slot; spreading blocks over slots avoids
+                          //    same-word atomic contention)
     int64_t *skey, *sarc; // current frontier grouped by slot: key, first arc offset
     unsigned long long *scnt[2];  // per slot, per round parity: packed (entries << 36 | arcs)
-    unsigned long long *sfill;    // per slot fill of the grouped frontier (phase A)
+    unsigned long long *sfill;    // per slot group: fill of the grouped frontier (phase A)
+    int64_t sgroup;               // slots per group: the frontier copy is grouped by
+                                  // k / sgroup (L2-sized groups; slots inside a group
+                                  // interleave, spreading same-word atomics)
     unsigned long long *cctr;     // phase-B chunk claim counter
     int64_t *frow;
     double *fcval;
@@ -173,9 +183,14 @@ __device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v,
     old = __shfl_sync(FULL, old, 0);
     if (flag) {
         int64_t idx = (int64_t)(old >> CNT_SHIFT) + __popc(am & lanemask_lt());
-        if (idx < A.fcap) A.ukey[idx] = ((int64_t)k << 32) | (uint32_t)v;
-        else A.overflow[0] = 1;
-        atomicAdd(A.scnt[nxt] + k, (1ULL << CNT_SHIFT) + (unsigned long long)d);
+        if (idx < A.fcap) {
+            A.ukey[idx] = ((int64_t)k << 32) | (uint32_t)v;
+            A.uarc[idx] = (int64_t)(old & ARC_MASK) + (int64_t)(incl - (unsigned long long)d);
+        } else {
+            A.overflow[0] = 1;
+        }
+        if (A.grouped)
+            atomicAdd(A.scnt[nxt] + k / A.sgroup, (1ULL << CNT_SHIFT) + (unsigned long long)d);
     }
 }
 
@@ -243,10 +258,30 @@ __device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, in
     base = __shfl_sync(FULL, base, 0);
     const unsigned my = base + __popc(am & lanemask_lt());
     const bool spill = flag && my >= (unsigned)STAGE_CAP;
-    if (flag && !spill) {
+    const bool staged = flag && !spill;
+    if (staged) {
         S.fk[my] = k;
         S.fv[my] = v;
         S.fd[my] = d;
+    }
+    // grouped mode: per slot group (entries, arcs) of the staged lanes, one
+    // shared atomic per group present in the warp (usually one)
+    if (A.grouped) {
+        const unsigned sm = __ballot_sync(FULL, staged);
+        if (sm) {
+            const int32_t g = k / (int32_t)A.sgroup;
+            const int32_t g0 = __shfl_sync(FULL, g, __ffs(sm) - 1);
+            if (__all_sync(FULL, !staged || g == g0)) {
+                const unsigned dsum = __reduce_add_sync(FULL, staged ? (unsigned)d : 0u);
+                if (lane == 0)
+                    atomicAdd(S.scnt + g0, ((unsigned long long)__popc(sm) << CNT_SHIFT) + dsum);
+            } else if (staged) {
+                const unsigned peers = __match_any_sync(sm, g);
+                const unsigned dsum = __reduce_add_sync(peers, (unsigned)d);
+                if (lane == __ffs(peers) - 1)
+                    atomicAdd(S.scnt + g, ((unsigned long long)__popc(peers) << CNT_SHIFT) + dsum);
+            }
+        }
     }
     frontier_append(spill, k, v, d, A, nxt);
 }
@@ -261,40 +296,53 @@ __device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
     const unsigned per = (cnt + BT - 1) / BT;
     const unsigned lo = min(cnt, tid * per), hi = min(cnt, lo + per);
     unsigned long long mine = 0;
-    for (unsigned i = lo; i < hi; i++) {
-        mine += (unsigned long long)S.fd[i];
-        atomicAdd(S.scnt + S.fk[i], (1ULL << CNT_SHIFT) + (unsigned long long)S.fd[i]);
+    for (unsigned i = lo; i < hi; i++) mine += (unsigned long long)S.fd[i];
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
     }
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FULL, mine, o);
-    if (lane == 0) S.scan[w] = mine;
+    if (lane == 31) S.scan[w] = incl;
     __syncthreads();
     if (tid == 0) {
         unsigned long long run = 0;
-        for (int i = 0; i < BT / 32; i++) run += S.scan[i];
+        for (int i = 0; i < BT / 32; i++) {
+            unsigned long long x = S.scan[i];
+            S.scan[i] = run;
+            run += x;
+        }
         unsigned long long old = 0;
         if (cnt) old = atomicAdd(A.fctr + nxt, ((unsigned long long)cnt << CNT_SHIFT) + run);
         S.scan[BT / 32] = old;
     }
     __syncthreads();
-    const int64_t ebase = (int64_t)(S.scan[BT / 32] >> CNT_SHIFT);
+    const unsigned long long old = S.scan[BT / 32];
+    const int64_t ebase = (int64_t)(old >> CNT_SHIFT);
+    int64_t arc = (int64_t)(old & ARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
     for (unsigned i = lo; i < hi; i++) {
         const int64_t idx = ebase + i;
-        if (idx < A.fcap) A.ukey[idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
-        else A.overflow[0] = 1;
-    }
-    for (int64_t k = tid; k < A.m; k += BT) {
-        const unsigned long long v = S.scnt[k];
-        if (v) {
-            atomicAdd(A.scnt[nxt] + k, v);
-            S.scnt[k] = 0;
+        if (idx < A.fcap) {
+            A.ukey[idx] = ((int64_t)S.fk[i] << 32) | (uint32_t)S.fv[i];
+            A.uarc[idx] = arc;  // (read in the ungrouped mode only)
+        } else {
+            A.overflow[0] = 1;
         }
+        arc += S.fd[i];
     }
+    if (A.grouped)
+        for (int64_t k = tid; k < A.m; k += BT) {
+            const unsigned long long v = S.scnt[k];
+            if (v) {
+                atomicAdd(A.scnt[nxt] + k, v);
+                S.scnt[k] = 0;
+            }
+        }
     __syncthreads();
     if (tid == 0) *S.fcnt = 0;
 }
 
-// S.sbase[k] = sum over j < k of A.scnt[cur][j] (packed: entries and arcs
-// together), computed by every block for itself.
+// S.sbase[g] = sum over slot groups j < g of A.scnt[cur][j] (packed: entries
+// and arcs together), computed by every block for itself.
 __device__ void slot_bases(const Stage &S, const RoundArgs &A, int cur) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t per = (A.m + BT - 1) / BT;
@@ -420,7 +468,7 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
                 if (mine) mapn[w0 + lane] = 0u;
             }
         }
-        slot_bases(S, A, cur);
+        if (A.grouped) slot_bases(S, A, cur);
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
             const int64_t e = e0 + lane;
             const bool live = e < F;
@@ -440,11 +488,15 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
                 rc[idx] = HK ? 0.0 : -0.0;
                 d = A.g.deg[u];
             }
-            // slot-grouped position: one packed reservation per (warp, slot)
+            // group-sorted position: one packed reservation per (warp, slot group);
+            // ungrouped: the entry keeps its append position and arc offset
             unsigned long long b = 0;
-            {
+            if (!A.grouped) {
+                if (live) b = ((unsigned long long)e << CNT_SHIFT) | (unsigned long long)A.uarc[e];
+            } else {
+                const int32_t kg = k / (int32_t)A.sgroup;
                 const unsigned long long pv = live ? (1ULL << CNT_SHIFT) + (unsigned long long)d : 0ULL;
-                const unsigned peers = __match_any_sync(FULL, live ? k : -1);
+                const unsigned peers = __match_any_sync(FULL, live ? kg : -1);
                 unsigned long long pre = 0, tot = 0;
                 for (int i = 0; i < 32; ++i) {
                     const unsigned long long vi = __shfl_sync(FULL, pv, i);
@@ -455,9 +507,9 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
                 }
                 const int leader = __ffs(peers) - 1;
                 unsigned long long old = 0;
-                if (live && lane == leader) old = atomicAdd(A.sfill + k, tot);
+                if (live && lane == leader) old = atomicAdd(A.sfill + kg, tot);
                 old = __shfl_sync(FULL, old, leader);
-                if (live) b = S.sbase[k] + old + pre;
+                if (live) b = S.sbase[kg] + old + pre;
             }
             if (live) {
                 pos = (int64_t)(b >> CNT_SHIFT);
@@ -509,10 +561,26 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
         for (int64_t k = gtid; k < A.m; k += nthreads) A.sfill[k] = 0ULL;  // for the next round
         const int64_t C = (P + 31) >> 5;
         const int64_t *fa = A.sarc;
-        const int64_t wid = gtid >> 5, nwarps = nthreads >> 5;
         if (!HK || t < A.n_stages) {  // (the last heat-kernel stage is absorbing)
             const int64_t c1 = C;
-          for (int64_t cb = wid * UNROLL; cb < c1; cb += nwarps * UNROLL) {
+          for (;;) {
+            // block b owns super-chunks b, b + G, b + 2G, ... (SUPER groups of
+            // UNROLL chunks each); its warps claim groups in order from a
+            // shared counter, so the grid advances through the arc space
+            // together while latency differences between warps even out
+            unsigned long long claim = 0;
+            if (lane == 0) claim = atomicAdd(S.next, 1ULL);
+            const int64_t i = (int64_t)__shfl_sync(FULL, claim, 0);
+            int64_t cb, cend;
+            if (A.grouped) {
+                const int64_t sup = i / SUPER, within = i - sup * SUPER;
+                cb = ((sup * gridDim.x + blockIdx.x) * SUPER + within) * UNROLL;
+                cend = c1;
+            } else {  // this block's contiguous range
+                cb = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x) + i * UNROLL;
+                cend = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
+            }
+            if (cb >= cend) break;
             int32_t k[UNROLL], v[UNROLL], dv[UNROLL];
             double c[UNROLL], old[UNROLL];
             bool valid[UNROLL];
@@ -521,7 +589,7 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
 #pragma unroll
             for (int q = 0; q < UNROLL; q++) {
                 const int64_t ch = cb + q;
-                const bool live = ch < c1;
+                const bool live = ch < cend;
                 const uint32_t raw = live ? (uint32_t)A.chunk_e[ch] : 0u;  // same for all lanes
                 const int64_t e = raw & 0x7fffffffu;
                 const int64_t a = ch << 5;
@@ -565,7 +633,8 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             }
           }
         }
-        stage_flush(S, A, nxt);
+        stage_flush(S, A, nxt);  // (its barriers also order the claim counter reset)
+        if (threadIdx.x == 0) *S.next = 0;
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
@@ -594,14 +663,16 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
     int32_t d = A.g.deg[s];
-    A.scnt[0][k] = 0ULL;
-    A.scnt[1][k] = 0ULL;
     A.sfill[k] = 0ULL;
     if (alpha >= theta_deg(A.tcoeff, d)) {
         unsigned long long old = atomicAdd(A.fctr, (1ULL << CNT_SHIFT) + (unsigned long long)d);
         int64_t idx = (int64_t)(old >> CNT_SHIFT);
-        if (idx < A.fcap) A.ukey[idx] = (k << 32) | (uint32_t)s;
-        A.scnt[0][k] = (1ULL << CNT_SHIFT) + (unsigned long long)d;
+        if (idx < A.fcap) {
+            A.ukey[idx] = (k << 32) | (uint32_t)s;
+            A.uarc[idx] = (int64_t)(old & ARC_MASK);
+        }
+        if (A.grouped)  // (zeroed by the host before this kernel)
+            atomicAdd(A.scnt[0] + k / A.sgroup, (1ULL << CNT_SHIFT) + (unsigned long long)d);
     }
 }
 
@@ -738,8 +809,9 @@ struct gd_batch {
     DBuf<double> x, r, fcval;
     DBuf<int32_t> pushed, seed, s_last, s_conv, overflow;
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
-    DBuf<int64_t> ukey, skey, sarc, frow, slot_base;
+    DBuf<int64_t> ukey, uarc, skey, sarc, frow, slot_base;
     DBuf<unsigned long long> scnt, sfill, cctr;
+    int64_t sgroup = 1;
     DBuf<int32_t> chunk_e;
     DBuf<int2> colp;
     int64_t ccap = 0;
@@ -777,6 +849,9 @@ struct gd_batch {
         A.touched = touched.p; A.pushed_cnt = pushed_cnt.p;
         A.ukey = ukey.p; A.skey = skey.p; A.sarc = sarc.p;
         A.scnt[0] = scnt.p; A.scnt[1] = scnt.p + slots; A.sfill = sfill.p; A.cctr = cctr.p;
+        A.sgroup = sgroup;
+        A.uarc = uarc.p;
+        A.grouped = sgroup < slots ? 1 : 0;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
         A.chunk_e = chunk_e.p; A.ccap = ccap;
         A.colp = colp.p;
@@ -853,6 +928,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
+        GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
         k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
                                                                B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
@@ -1065,8 +1141,14 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
             B->slot_base.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
-            B->ukey.alloc(fc); B->skey.alloc(fc); B->sarc.alloc(fc);
+            B->ukey.alloc(fc); B->uarc.alloc(fc); B->skey.alloc(fc); B->sarc.alloc(fc);
             B->scnt.alloc(2 * (size_t)slots); B->sfill.alloc(slots); B->cctr.alloc(1);
+            {  // slot groups of about 96 MB of residual vectors (see RoundArgs::sgroup,
+               // ::grouped): all slots in one group = the ungrouped mode
+                int64_t gsz = (96LL << 20) / (ld * 8);
+                if (const char *e = getenv("GDIFF_SLOT_GROUP")) gsz = atoll(e);  // experiments
+                B->sgroup = gsz < 1 ? 1 : (gsz > slots ? slots : gsz);
+            }
             B->frow.alloc(fc); B->fcval.alloc(fc);
             B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32
             if (B->hk && p->frontier_cap <= 0) {  // global stages: up to slots * 2m arcs
