@@ -47,6 +47,7 @@ constexpr unsigned long long SARC_MASK = (1ULL << SCNT_SHIFT) - 1ULL;
 constexpr unsigned SFULL = 0xffffffffu;
 constexpr int SSTAGE = 4 * SBT;  // staged entries / candidates per block
 constexpr int SCHUNKS = 32;
+constexpr int SSUPER = 16;  // SUNROLL-chunk groups per block super-chunk (grouped mode)
 
 struct SArgs {
     DevGraph g;
@@ -66,6 +67,12 @@ struct SArgs {
     int64_t *cand[2];               // (slot << 32 | node)
     unsigned long long *candctr;    // [2]
     const int2 *colp;               // (neighbour, degree) per arc
+    int grouped;                    // 1: entries regrouped by slot group before phase B
+    int64_t sgroup;                 //    (slot vectors exceed L2; see batch.cu)
+    int64_t group_min;              //    ... in rounds with at least this many candidates
+    int64_t *ukey;                  //    unsorted entries of the round and their c_u
+    double *ucval;
+    unsigned long long *gcnt, *gfill;  // per slot group: packed (entries, arcs), fill
     int64_t *fkey, *farc, *frow;    // frontier of the current round
     double *fcval;
     int32_t *chunk_e;
@@ -85,6 +92,8 @@ __device__ __forceinline__ unsigned lanemask_lt_s() {
 struct SStage {
     double *c;
     double *l1;                      // [m] per-slot l1 deltas of the block
+    unsigned long long *gc;          // [m] per slot group (entries, arcs) of the block
+    unsigned long long *gbase;       // [m] group offsets of the grouped frontier
     unsigned long long *ops, *push;  // [m]
     unsigned long long *scan;        // [SBT/32 + 2]
     unsigned long long *next;
@@ -94,7 +103,7 @@ struct SStage {
 };
 
 inline size_t sstage_bytes(int64_t m) {
-    return (size_t)SSTAGE * 8 + (size_t)m * 24 + 8 * (SBT / 32 + 3) + (size_t)SSTAGE * 20 + 32;
+    return (size_t)SSTAGE * 8 + (size_t)m * 40 + 8 * (SBT / 32 + 3) + (size_t)SSTAGE * 20 + 32;
 }
 
 __device__ SStage sstage_carve(void *base, int64_t m) {
@@ -102,6 +111,8 @@ __device__ SStage sstage_carve(void *base, int64_t m) {
     SStage s;
     s.c = (double *)p; p += 8 * SSTAGE;
     s.l1 = (double *)p; p += 8 * m;
+    s.gc = (unsigned long long *)p; p += 8 * m;
+    s.gbase = (unsigned long long *)p; p += 8 * m;
     s.ops = (unsigned long long *)p; p += 8 * m;
     s.push = (unsigned long long *)p; p += 8 * m;
     s.scan = (unsigned long long *)p; p += 8 * (SBT / 32 + 2);
@@ -215,7 +226,7 @@ __device__ void entry_stage(bool flag, int32_t k, int32_t u, int32_t d, double c
 
 // Block flush of staged frontier entries: one reservation, arc offsets by a
 // block scan, entry arrays + chunk map written here (the entries are final).
-__device__ void entry_flush(const SStage &S, const SArgs &A) {
+__device__ void entry_flush(const SStage &S, const SArgs &A, bool grp) {
     __syncthreads();
     const unsigned cnt = *S.cnt;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -245,6 +256,28 @@ __device__ void entry_flush(const SStage &S, const SArgs &A) {
     const unsigned long long old = S.scan[SBT / 32];
     int64_t arc = (int64_t)(old & SARC_MASK) + (int64_t)(S.scan[w] + incl - mine);
     const int64_t ebase = (int64_t)(old >> SCNT_SHIFT);
+    if (grp) {  // unsorted entries + per-group counts; placed after the barrier
+        for (unsigned i = lo; i < hi; i++) {
+            const int64_t e = ebase + i;
+            if (e < A.fcap) {
+                A.ukey[e] = ((int64_t)S.k[i] << 32) | (uint32_t)S.v[i];
+                A.ucval[e] = S.c[i];
+            } else {
+                A.overflow[0] = 1;
+            }
+            atomicAdd(S.gc + S.k[i] / A.sgroup, (1ULL << SCNT_SHIFT) + (unsigned long long)S.d[i]);
+        }
+        __syncthreads();
+        for (int64_t g = tid; g < A.m; g += SBT)
+            if (S.gc[g]) {
+                atomicAdd(A.gcnt + g, S.gc[g]);
+                S.gc[g] = 0;
+            }
+        __syncthreads();
+        if (tid == 0) *S.cnt = 0;
+        __syncthreads();
+        return;
+    }
     for (unsigned i = lo; i < hi; i++) {
         const int64_t e = ebase + i;
         const int32_t u = S.v[i];
@@ -265,6 +298,37 @@ __device__ void entry_flush(const SStage &S, const SArgs &A) {
     __syncthreads();
 }
 
+// S.gbase[g] = sum over groups j < g of A.gcnt[j] (packed), per block.
+__device__ void group_bases(const SStage &S, const SArgs &A) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t per = (A.m + SBT - 1) / SBT;
+    const int64_t lo = min(A.m, tid * per), hi = min(A.m, lo + per);
+    unsigned long long mine = 0;
+    for (int64_t g = lo; g < hi; g++) mine += A.gcnt[g];
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(SFULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.scan[w] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < SBT / 32; i++) {
+            unsigned long long x = S.scan[i];
+            S.scan[i] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    unsigned long long b = S.scan[w] + incl - mine;
+    for (int64_t g = lo; g < hi; g++) {
+        S.gbase[g] = b;
+        b += A.gcnt[g];
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ bool slot_diverged(const SArgs &A, int32_t k) {
     return A.method == 1 && A.s_l1[k] > A.l1cap * A.s_b1[k];
 }
@@ -280,6 +344,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
     for (int64_t k = threadIdx.x; k < A.m; k += SBT) {
         S.l1[k] = 0.0;
         S.ops[k] = S.push[k] = 0;
+        S.gc[k] = 0;
     }
     if (threadIdx.x == 0) {
         *S.cnt = 0;
@@ -301,6 +366,9 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
             A.candctr[nxt] = 0ULL;
         }
         grid.sync();  // counter resets visible before any reservation
+        // group only rounds with enough work to pay for the placement pass and
+        // its barrier (small rounds are barrier-bound, not L2-bound)
+        const bool grp = A.grouped && NC >= A.group_min;
         const double cr = (ch && t > 0) ? A.coef_r[t] : 0.0;
         const double cm = (ch && t > 0) ? A.coef_m[t] : 0.0;
         for (int64_t base = blockIdx.x * (int64_t)SBT; base < NC; base += nthreads) {
@@ -364,36 +432,91 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
             const bool again = cand_mark(ch && act, k, u, A, nxt);
             cand_stage(again, k, u, S, A, nxt);
             __syncthreads();
-            if (*S.cnt > (unsigned)(SSTAGE - SBT)) entry_flush(S, A);
+            if (*S.cnt > (unsigned)(SSTAGE - SBT)) entry_flush(S, A, grp);
         }
-        entry_flush(S, A);
+        entry_flush(S, A, grp);
         for (int64_t k = threadIdx.x; k < A.m; k += SBT) {
             if (S.ops[k]) { atomicAdd(A.s_ops + k, S.ops[k]); S.ops[k] = 0; }
             if (S.push[k]) { atomicAdd(A.s_pushes + k, S.push[k]); S.push[k] = 0; }
         }
         grid.sync();
-        // ---------------- phase B: arc chunks -------------------------------
         const unsigned long long pk = *(volatile unsigned long long *)A.fctr;
         const int64_t F = (int64_t)(pk >> SCNT_SHIFT), P = (int64_t)(pk & SARC_MASK);
         if (F > A.fcap || ((P + 31) >> 5) > A.ccap) {
             if (gtid == 0) A.overflow[0] = 1;
             break;
         }
+        if (grp) {
+            // ---------------- placement: frontier grouped by slot group -------
+            group_bases(S, A);
+            for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {
+                const int64_t e = e0 + lane;
+                const bool live = e < F;
+                int64_t key = 0;
+                int32_t k = 0, u = 0, d = 0;
+                if (live) {
+                    key = A.ukey[e];
+                    k = (int32_t)(key >> 32);
+                    u = (int32_t)(key & 0xffffffffLL);
+                    d = A.g.deg[u];
+                }
+                const int32_t g = k / (int32_t)A.sgroup;
+                const unsigned long long pv = live ? (1ULL << SCNT_SHIFT) + (unsigned long long)d : 0ULL;
+                const unsigned peers = __match_any_sync(SFULL, live ? g : -1);
+                unsigned long long pre = 0, tot = 0;
+                for (int i = 0; i < 32; ++i) {
+                    const unsigned long long vi = __shfl_sync(SFULL, pv, i);
+                    if ((peers >> i) & 1u) {
+                        tot += vi;
+                        if (i < lane) pre += vi;
+                    }
+                }
+                const int leader = __ffs(peers) - 1;
+                unsigned long long o = 0;
+                if (live && lane == leader) o = atomicAdd(A.gfill + g, tot);
+                o = __shfl_sync(SFULL, o, leader);
+                if (live) {
+                    const unsigned long long b = S.gbase[g] + o + pre;
+                    const int64_t pos = (int64_t)(b >> SCNT_SHIFT), a0 = (int64_t)(b & SARC_MASK);
+                    A.fkey[pos] = key;
+                    A.farc[pos] = a0;
+                    A.frow[pos] = A.g.row[u];
+                    A.fcval[pos] = A.ucval[e];
+                    const int64_t c0 = (a0 + 31) >> 5, c1 = min((a0 + d + 31) >> 5, A.ccap);
+                    for (int64_t c = c0; c < c1; ++c) A.chunk_e[c] = (int32_t)pos;
+                }
+            }
+            grid.sync();
+            for (int64_t g = gtid; g < A.m; g += nthreads) {  // (read by every block above)
+                A.gcnt[g] = 0ULL;
+                A.gfill[g] = 0ULL;
+            }
+        }
+        // ---------------- phase B: arc chunks -------------------------------
         const int64_t C = (P + 31) >> 5;
         const int64_t bc0 = (int64_t)(((unsigned long long)C * blockIdx.x) / gridDim.x);
         const int64_t bc1 = (int64_t)(((unsigned long long)C * (blockIdx.x + 1)) / gridDim.x);
         for (;;) {
             unsigned long long claim = 0;
-            if (lane == 0) claim = atomicAdd(S.next, (unsigned long long)SUNROLL);
-            const int64_t cb = bc0 + (int64_t)__shfl_sync(SFULL, claim, 0);
-            if (cb >= bc1) break;
+            if (lane == 0) claim = atomicAdd(S.next, 1ULL);
+            const int64_t ci = (int64_t)__shfl_sync(SFULL, claim, 0);
+            int64_t cb, cend;
+            if (grp) {  // super-chunks b, b + G, ...: the grid advances together
+                const int64_t sup = ci / SSUPER, within = ci - sup * SSUPER;
+                cb = ((sup * gridDim.x + blockIdx.x) * SSUPER + within) * SUNROLL;
+                cend = C;
+            } else {  // this block's contiguous range
+                cb = bc0 + ci * SUNROLL;
+                cend = bc1;
+            }
+            if (cb >= cend) break;
             int32_t k[SUNROLL], v[SUNROLL], dv[SUNROLL];
             double c[SUNROLL], old[SUNROLL];
             bool valid[SUNROLL];
 #pragma unroll
             for (int q = 0; q < SUNROLL; q++) {
                 const int64_t chn = cb + q;
-                const bool live = chn < bc1;
+                const bool live = chn < cend;
                 const int64_t e = live ? A.chunk_e[chn] : 0;
                 const int64_t a = chn << 5;
                 const int64_t wi = e + 1 + lane;
@@ -660,6 +783,11 @@ struct SignedState {
     DBuf<uint32_t> cm0, cm1, secmap;
     DBuf<int64_t> cand0, cand1, fkey, farc, frow, slot_base;
     DBuf<int2> colp;
+    int grouped = 0;
+    int64_t sgroup = 1, group_min = 1 << 16;
+    DBuf<int64_t> ukey;
+    DBuf<double> ucval;
+    DBuf<unsigned long long> gcnt, gfill;
     DBuf<unsigned long long> candctr, fctr, s_ops, s_pushes, pushed_cnt;
     bool dirty = false;  // an aborted run left marks behind: full clear next time
     size_t smem = 0;
@@ -694,6 +822,19 @@ struct SignedState {
         candcap = fcap_;
         cand0.alloc(candcap); cand1.alloc(candcap);
         fkey.alloc(fcap); farc.alloc(fcap); frow.alloc(fcap); fcval.alloc(fcap);
+        {  // slot groups of ~96 MB of residual vectors; one group = ungrouped mode
+            int64_t gsz = (96LL << 20) / (ld * 8);
+            if (const char *e = getenv("GDIFF_SLOT_GROUP")) gsz = atoll(e);  // experiments
+            sgroup = gsz < 1 ? 1 : (gsz > slots ? slots : gsz);
+            grouped = sgroup < slots ? 1 : 0;
+            if (const char *e = getenv("GDIFF_GROUP_MIN")) group_min = atoll(e);  // (tests)
+        }
+        if (grouped) {
+            ukey.alloc(fcap); ucval.alloc(fcap);
+        }
+        gcnt.alloc(slots); gfill.alloc(slots);
+        GD_CUDA(cudaMemset(gcnt.p, 0, sizeof(unsigned long long) * slots));
+        GD_CUDA(cudaMemset(gfill.p, 0, sizeof(unsigned long long) * slots));
         chunk_e.alloc(ccap);
         candctr.alloc(2); fctr.alloc(1); overflow.alloc(1);
         s_ops.alloc(slots); s_pushes.alloc(slots); pushed_cnt.alloc(slots);
@@ -753,6 +894,9 @@ struct SignedState {
         A.secmap = secmap.p; A.smw = smw;
         A.cand[0] = cand0.p; A.cand[1] = cand1.p; A.candctr = candctr.p;
         A.colp = colp.p;
+        A.grouped = grouped; A.sgroup = sgroup; A.ukey = ukey.p; A.ucval = ucval.p;
+        A.group_min = group_min;
+        A.gcnt = gcnt.p; A.gfill = gfill.p;
         A.fkey = fkey.p; A.farc = farc.p; A.frow = frow.p; A.fcval = fcval.p;
         A.chunk_e = chunk_e.p; A.fctr = fctr.p;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_l1 = s_l1.p; A.s_b1 = s_b1.p;

@@ -221,3 +221,26 @@ def test_batch_rejects_bad_input(gpu):
         BatchSolver(g, 0.1, 1e-6, method="local-sor", omega=2.5)
     with pytest.raises(ValueError):
         BatchSolver(g, 0.1, 1e-6, method="local-ch", mu=0.5, L=0.4)
+
+
+@pytest.mark.parametrize("group", ["1", "3"])
+def test_grouped_mode_matches_oracle(gpu, monkeypatch, group):
+    """Slot-grouped frontier + windowed phase B (the mode large graphs use,
+    forced here on a small one) gives the reference's integer work, for
+    LocalGD and the heat kernel."""
+    from paper_2410_21634_b200.batch import local_hk_batch
+    monkeypatch.setenv("GDIFF_SLOT_GROUP", group)
+    g = rmat_graph(20000, 150000, seed=5)
+    seeds = sample_sources(g, 40, seed=0)
+    ref = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=8)
+    out = local_gd_batch(g, seeds, 0.1, 1e-6, slots=16)
+    assert np.array_equal(out.sweeps, ref["sweeps"]) and np.array_equal(out.total_ops, ref["total_ops"])
+    assert np.array_equal(out.pushes, ref["pushes"])
+    xs = np.array([out.x_sparse(i)[1].sum() for i in range(len(seeds))])
+    np.testing.assert_allclose(xs, ref["xsum"], rtol=1e-12)
+    hk = local_hk_batch(g, seeds[:12], 5.0, 1e-6, slots=5)
+    for i, s in enumerate(seeds[:12]):
+        r = O.local_hk(g, 5.0, int(s), 1e-6)
+        assert hk.sweeps[i] == r["sweeps"] and hk.total_ops[i] == r["total_ops"]
+        f = r["f_hat"]
+        assert np.abs(hk.x_dense(i, g.n) - f).sum() <= X_RTOL * np.abs(f).sum()

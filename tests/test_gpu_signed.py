@@ -215,3 +215,25 @@ def test_device_graph_edit_matches_host(gpu, small):
         with pytest.raises(GraphStructureError):
             apply_events(g, bad * 70)
         dg.close()
+
+
+@pytest.mark.parametrize("group", ["1", "4"])
+def test_signed_grouped_mode(gpu, monkeypatch, group):
+    """LocalCH batches and the pair pool in the slot-grouped mode."""
+    monkeypatch.setenv("GDIFF_SLOT_GROUP", group)
+    monkeypatch.setenv("GDIFF_GROUP_MIN", "0")  # every round grouped
+    g = rmat_graph(20000, 150000, seed=5)
+    seeds = sample_sources(g, 24, seed=2)
+    out = local_ch_batch(g, seeds, 0.1, 1e-6, slots=10)
+    for i, s in enumerate(seeds):
+        ref = O.local_ch(S.make_ppr_system(g, 0.1, int(s), 1e-6), record_trace=False)
+        assert out.sweeps[i] == ref["sweeps"] and out.total_ops[i] == ref["total_ops"], i
+        _check_seed(out, i, ref["x"], g.n)
+    from paper_2410_21634_b200.graph import EdgeEvent, apply_events
+    rng = np.random.default_rng(1)
+    b = []
+    for _ in range(50):
+        u, v = sorted(rng.choice(g.n, 2, replace=False).tolist())
+        if not g.has_edge(u, v) and all((e.u, e.v) != (u, v) for e in b):
+            b.append(EdgeEvent("insert", u, v))
+    _pool_against_oracle(g, [b], sample_sources(g, 12, seed=4).tolist(), 0.15, 1e-5)
