@@ -93,6 +93,7 @@ struct RoundArgs {
     unsigned long long *touched, *pushed_cnt;
     int64_t *ukey;        // next frontier as appended: (slot << 32 | node), any order
     int64_t *uarc;        // its first arc offsets in append order (ungrouped mode)
+    int64_t group_min;    // (rounds with fewer frontier arcs stay ungrouped)
     int grouped;          // 1: phase A regroups the frontier by slot group and phase B
                           //    walks it with a grid-wide window (slot vectors > L2);
                           // 0: append order, contiguous per-block ranges (L2 holds
@@ -468,7 +469,10 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
                 if (mine) mapn[w0 + lane] = 0u;
             }
         }
-        if (A.grouped) slot_bases(S, A, cur);
+        // group this round only when it is large enough to be L2-bound (small
+        // rounds are barrier-bound and keep the append order)
+        const bool grp = A.grouped && P >= A.group_min;
+        if (grp) slot_bases(S, A, cur);
         for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
             const int64_t e = e0 + lane;
             const bool live = e < F;
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             // group-sorted position: one packed reservation per (warp, slot group);
             // ungrouped: the entry keeps its append position and arc offset
             unsigned long long b = 0;
-            if (!A.grouped) {
+            if (!grp) {
                 if (live) b = ((unsigned long long)e << CNT_SHIFT) | (unsigned long long)A.uarc[e];
             } else {
                 const int32_t kg = k / (int32_t)A.sgroup;
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
             if (lane == 0) claim = atomicAdd(S.next, 1ULL);
             const int64_t i = (int64_t)__shfl_sync(FULL, claim, 0);
             int64_t cb, cend;
-            if (A.grouped) {
+            if (grp) {
                 const int64_t sup = i / SUPER, within = i - sup * SUPER;
                 cb = ((sup * gridDim.x + blockIdx.x) * SUPER + within) * UNROLL;
                 cend = c1;
@@ -730,7 +734,7 @@ __global__ void k_wave_reset(RoundArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t off = (int64_t)k * A.ld;
     uint32_t *map = A.secmap + (int64_t)k * A.smw;
-    const int64_t per = (A.smw + CHUNKS - 1) / CHUNKS;
+    const int64_t per = (A.smw + gridDim.x - 1) / gridDim.x;  // gridDim.x scales with the map
     const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
     double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
     for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
@@ -811,7 +815,7 @@ struct gd_batch {
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
     DBuf<int64_t> ukey, uarc, skey, sarc, frow, slot_base;
     DBuf<unsigned long long> scnt, sfill, cctr;
-    int64_t sgroup = 1;
+    int64_t sgroup = 1, group_min = 1 << 22;
     DBuf<int32_t> chunk_e;
     DBuf<int2> colp;
     int64_t ccap = 0;
@@ -833,6 +837,11 @@ struct gd_batch {
     DBuf<int64_t> dseeds;  // host-entry staging of the seed list
 
     const gd_graph *work() const { return R ? R : G; }
+    // blocks per slot of the reset: ~2,048 map words (256 KB of r) per block
+    unsigned reset_chunks() const {
+        const int64_t c = (smw + 2047) / 2048;
+        return (unsigned)(c < CHUNKS ? CHUNKS : (c > 4096 ? 4096 : c));
+    }
 
     RoundArgs args() {
         RoundArgs A{};
@@ -852,6 +861,7 @@ struct gd_batch {
         A.sgroup = sgroup;
         A.uarc = uarc.p;
         A.grouped = sgroup < slots ? 1 : 0;
+        A.group_min = group_min;
         A.frow = frow.p; A.fcval = fcval.p; A.fctr = fctr.p;
         A.chunk_e = chunk_e.p; A.ccap = ccap;
         A.colp = colp.p;
@@ -939,12 +949,12 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
                                             stage_bytes(B->slots), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
         k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
-        k_wave_reset<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A);
+        k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A);
         if (B->hk) {  // the other residual layer
             RoundArgs A2 = A;
             A2.r = A.r2;
             A2.secmap = A.secmap2;
-            k_wave_reset<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A2);
+            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A2);
         }
         GD_LAUNCH_CHECK();
         launches += B->hk ? 5 : 4;
@@ -1119,7 +1129,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
                 // 64 in flight measured best on the products shape (L2 reuse of
                 // the hub block vs. barrier amortisation); fewer if memory-bound
-                int64_t by_mem = (int64_t)(fr / 4) / (ld * (B->hk ? 28 : 20));
+                int64_t by_mem = (int64_t)(fr / 3) / (ld * (B->hk ? 28 : 20));
                 // the heat kernel at large tau is effectively global: a stage's
                 // frontier approaches n per seed, so bound slots * n as well
                 if (B->hk && by_mem > (64LL << 20) / n) by_mem = (64LL << 20) / n;
@@ -1148,6 +1158,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 int64_t gsz = (96LL << 20) / (ld * 8);
                 if (const char *e = getenv("GDIFF_SLOT_GROUP")) gsz = atoll(e);  // experiments
                 B->sgroup = gsz < 1 ? 1 : (gsz > slots ? slots : gsz);
+                if (const char *e = getenv("GDIFF_GROUP_MIN")) B->group_min = atoll(e);  // (tests)
             }
             B->frow.alloc(fc); B->fcval.alloc(fc);
             B->ccap = fc;  // chunks of 32 arcs per round: P/32 <= entries * avg degree / 32

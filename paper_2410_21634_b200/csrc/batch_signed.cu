@@ -653,7 +653,7 @@ __global__ void k_s_reset(SArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t off = (int64_t)k * A.ld;
     uint32_t *map = A.secmap + (int64_t)k * A.smw;
-    const int64_t per = (A.smw + SCHUNKS - 1) / SCHUNKS;
+    const int64_t per = (A.smw + gridDim.x - 1) / gridDim.x;  // gridDim.x scales with the map
     const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
     double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
     for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
@@ -995,7 +995,9 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
         GD_CUDA(cudaEventRecord(ev[2 * w + 1], st));
         k_s_reserve<<<(int)((m + 255) / 256), 256, 0, st>>>(A, cursor, S->slot_base.p);
         k_s_extract<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A, O, base);
-        k_s_reset<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A);
+        const int64_t rc = (S->smw + 2047) / 2048;  // ~2,048 map words per block
+        k_s_reset<<<dim3((unsigned)(rc < SCHUNKS ? SCHUNKS : (rc > 4096 ? 4096 : rc)), (unsigned)m), 256,
+                    0, st>>>(A);
         GD_LAUNCH_CHECK();
         nl += 5;
     }

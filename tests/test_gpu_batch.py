@@ -230,6 +230,7 @@ def test_grouped_mode_matches_oracle(gpu, monkeypatch, group):
     LocalGD and the heat kernel."""
     from paper_2410_21634_b200.batch import local_hk_batch
     monkeypatch.setenv("GDIFF_SLOT_GROUP", group)
+    monkeypatch.setenv("GDIFF_GROUP_MIN", "0")  # every round grouped
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 40, seed=0)
     ref = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=8)
