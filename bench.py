@@ -359,7 +359,7 @@ def main():
         if world == 1:
             return None
         return gather_results({f: res[f] for f in STAT_FIELDS}, res["x_nodes"], res["x_vals"],
-                              dst=0)
+                              dst=0, to_host=False)  # (results stay in rank 0's HBM)
 
     for k in range(args.warmup):
         gather(solver.solve_device(dseeds[k], stream=stream))

@@ -27,7 +27,7 @@ def shard_seeds(seeds, rank: int, world: int) -> np.ndarray:
 
 
 def gather_results(stats: dict, x_nodes, x_vals, group=None, device=None,
-                   dst: int | None = 0) -> dict | None:
+                   dst: int | None = 0, to_host: bool = True) -> dict | None:
     """Gather per-seed results of all ranks (round-robin order restored).
 
     stats: dict of per-seed tensors (STAT_FIELDS, int64 / int32), x_nodes
@@ -35,7 +35,8 @@ def gather_results(stats: dict, x_nodes, x_vals, group=None, device=None,
     rank receives everything (all_gather); otherwise only rank dst does
     (gather) and the others return None.  The result is a dict of numpy
     arrays in global seed order with x_offset rebased into the concatenated
-    pool.
+    pool.  to_host=False keeps the result on the receiving device (torch
+    tensors, nothing copied to the host: the form a GPU pipeline consumes).
     """
     import torch
     import torch.distributed as dist
@@ -52,9 +53,9 @@ def gather_results(stats: dict, x_nodes, x_vals, group=None, device=None,
     st = torch.zeros((len(STAT_FIELDS), kmax), dtype=torch.int64, device=dev)
     for i, f in enumerate(STAT_FIELDS):
         st[i, :k] = stats[f].to(device=dev, dtype=torch.int64)
-    xn = torch.zeros(xmax, dtype=torch.int64, device=dev)
+    xn = torch.zeros(xmax, dtype=torch.int32, device=dev)
     xv = torch.zeros(xmax, dtype=torch.float64, device=dev)
-    xn[:x_nodes.numel()] = x_nodes.to(device=dev, dtype=torch.int64)
+    xn[:x_nodes.numel()] = x_nodes.to(device=dev, dtype=torch.int32)
     xv[:x_vals.numel()] = x_vals.to(device=dev)
     me = dist.get_rank(group)
     if dst is None or me == dst:
@@ -75,6 +76,22 @@ def gather_results(stats: dict, x_nodes, x_vals, group=None, device=None,
             return None
 
     total = int(all_sizes[:, 0].sum())
+    if not to_host:  # assemble on the device
+        stats_d = torch.empty((len(STAT_FIELDS), total), dtype=torch.int64, device=dev)
+        nodes_d, vals_d, base = [], [], 0
+        for r in range(world):
+            kr, xr = int(all_sizes[r, 0]), int(all_sizes[r, 1])
+            s_r = g_st[r][:, :kr].clone()
+            s_r[STAT_FIELDS.index("x_offset")] += base
+            stats_d[:, r::world] = s_r
+            nodes_d.append(g_xn[r][:xr])
+            vals_d.append(g_xv[r][:xr])
+            base += xr
+        out = {f: stats_d[i] for i, f in enumerate(STAT_FIELDS)}
+        out["converged"] = out["converged"].to(torch.bool)
+        out["x_nodes"] = torch.cat(nodes_d) if nodes_d else torch.empty(0, dtype=torch.int32, device=dev)
+        out["x_vals"] = torch.cat(vals_d) if vals_d else torch.empty(0, dtype=torch.float64, device=dev)
+        return out
     out = {f: np.empty(total, dtype=np.int64) for f in STAT_FIELDS}
     nodes, vals, base = [], [], 0
     for r in range(world):
@@ -85,7 +102,7 @@ def gather_results(stats: dict, x_nodes, x_vals, group=None, device=None,
         nodes.append(g_xn[r][:xr].cpu().numpy())
         vals.append(g_xv[r][:xr].cpu().numpy())
         base += xr
-    out["x_nodes"] = np.concatenate(nodes) if nodes else np.empty(0, np.int64)
+    out["x_nodes"] = (np.concatenate(nodes) if nodes else np.empty(0, np.int32)).astype(np.int64)
     out["x_vals"] = np.concatenate(vals) if vals else np.empty(0)
     out["converged"] = out["converged"].astype(bool)
     return out

@@ -40,11 +40,14 @@ def _worker(rank, world, port, seeds, q):
             torch.as_tensor(nodes, dtype=torch.int32), torch.as_tensor(vals))
     out = gather_results(*args, device=torch.device("cpu"), dst=0)
     both = gather_results(*args, device=torch.device("cpu"), dst=None)
+    dev = gather_results(*args, device=torch.device("cpu"), dst=0, to_host=False)
     if rank == 0:
         assert all(np.array_equal(out[k], both[k]) for k in out)
+        # the device-resident form (what bench.py keeps in rank 0's HBM) is the same data
+        assert all(np.array_equal(out[k], dev[k].numpy()) for k in out)
         q.put({k: v.tolist() for k, v in out.items()})
     else:
-        assert out is None and both is not None
+        assert out is None and both is not None and dev is None
     dist.barrier()
     dist.destroy_process_group()
 
