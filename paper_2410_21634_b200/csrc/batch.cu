@@ -154,17 +154,6 @@ __device__ __forceinline__ void slot_append(bool flag, int32_t k, int32_t item, 
     list[(int64_t)k * ld + (int64_t)base + __popc(peers & lanemask_lt())] = item;
 }
 
-// Add `val` of the flagged lanes to per-slot counter k: one fire-and-forget
-// reduction per slot present in the warp (no returned value to wait for).
-__device__ __forceinline__ void slot_add(bool flag, int32_t k, unsigned val,
-                                         unsigned long long *cnt) {
-    unsigned am = __ballot_sync(FULL, flag);
-    if (!flag) return;
-    unsigned peers = __match_any_sync(am, k);
-    unsigned sum = __reduce_add_sync(peers, val);
-    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, (unsigned long long)sum);
-}
-
 // Append (k, v) with degree d to the next frontier (warp-aggregated, one
 // packed atomic reserving entry slots and arc range together).
 __device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v, int32_t d,

@@ -266,7 +266,7 @@ struct FifoWS {
     DBuf<int8_t> sgn;
 };
 
-void run_fifo(const gd_graph *G, FifoArgs A, bool hk, double *hx, double *hr,
+void run_fifo(const gd_graph *G, FifoArgs A, double *hx, double *hr,
               const int64_t *seeds, int64_t n_seeds, gd_report *rep) {
     const int64_t dim = A.dim;
     GD_CHECK_ARG(dim + 2 < (1LL << 31), "coordinate count must be < 2^31");
@@ -296,8 +296,7 @@ void run_fifo(const gd_graph *G, FifoArgs A, bool hk, double *hx, double *hr,
     A.x = x.p; A.r = r.p; A.queue = queue.p; A.qmark = qmark.p; A.seeds = sd.p;
     A.n_seeds = n_seeds; A.log_cap = log_cap; A.vol_log = vol.p; A.gamma_log = gam.p;
     A.l1_log = l1.p; A.sign_log = sgn.p; A.out = out.p; A.out_min = mn.p;
-    if (hk) k_fifo<true><<<1, FIFO_THREADS>>>(A);
-    else k_fifo<false><<<1, FIFO_THREADS>>>(A);
+    k_fifo<false><<<1, FIFO_THREADS>>>(A);  // (the HK instantiation is unused: hk.cu)
     GD_LAUNCH_CHECK();
     GD_CUDA(cudaDeviceSynchronize());
     int64_t o[4];
@@ -351,7 +350,7 @@ int gd_push_kernel(const gd_graph *G, const gd_operator *o, double *x, double *r
         A.x_gain = x_gain;
         A.sgn = is_signed ? 1 : 0;
         A.max_sweeps = max_sweeps;
-        run_fifo(G, A, false, x, r, seeds, n_seeds, rep);
+        run_fifo(G, A, x, r, seeds, n_seeds, rep);
     });
 }
 
