@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
             // software pipeline: the next pop's node, r, degree and row are
             // loaded while the current pop scatters (r re-read if it was hit)
             int64_t pu = -1, prs = 0;
-            double pr = 0.0;
+            double pr = 0.0, px = 0.0;
             int32_t pd = 0, pcol = 0;  // (pcol: this lane's first neighbour of the next pop)
             __syncwarp();
             for (;;) {
@@ -111,19 +111,21 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                     __syncwarp();
                     continue;
                 }
-                double ru;
+                double ru, xu;
                 int32_t d, c0;
                 int64_t rs;
-                if (u == pu) {
+                if (u == pu) {  // (x[u] is written only by u's own pops: px is exact)
                     ru = pr;
                     d = pd;
                     rs = prs;
                     c0 = pcol;
+                    xu = px;
                 } else {
                     ru = r[u];
                     d = A.g.deg[u];
                     rs = A.g.row[u];
                     c0 = lane < d ? A.g.col[rs + lane] : 0;
+                    xu = x[u];
                 }
                 pu = -1;
                 if (lane == 0) qmark[u] = 0;
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                         pr = r[nx];
                         pd = A.g.deg[nx];
                         prs = A.g.row[nx];
+                        px = x[nx];
                         pcol = lane < pd ? A.g.col[prs + lane] : 0;
                     }
                 }
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 pushes += 1;
                 const double res = __dmul_rn(A.omega, ru);
                 if (lane == 0) {
-                    x[u] = __dadd_rn(x[u], res);  // x_gain = 1
+                    x[u] = __dadd_rn(xu, res);  // x_gain = 1
                     const double rn = __dsub_rn(ru, res);
                     r[u] = __double_as_longlong(rn) == 0 ? -0.0 : rn;
                 }
