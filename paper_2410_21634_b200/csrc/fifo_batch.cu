@@ -27,7 +27,8 @@ struct FifoBatchArgs {
     int64_t n, ld, max_sweeps, n_seeds, xcap;
     double *x, *r;
     int32_t *queue;        // ld + 2 per slot
-    uint8_t *qmark;
+    uint32_t *qmark;       // queued-node bit map per slot (qw words): L2-resident
+    int64_t qw;
     int32_t *touched;      // touched list per slot (ld)
     const int64_t *seeds;
     unsigned long long *next_seed, *cursor;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
     const int64_t off = (int64_t)slot * A.ld;
     double *x = A.x + off, *r = A.r + off;
     int32_t *queue = A.queue + (int64_t)slot * (A.ld + 2);
-    uint8_t *qmark = A.qmark + off;
+    uint32_t *qmark = A.qmark + (int64_t)slot * A.qw;
     int32_t *touched = A.touched + off;
     const int64_t sent = A.n, qcap = A.n + 2;
 
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
         if (act0) {
             if (lane == 0) {
                 queue[0] = s;
-                qmark[s] = 1;
+                qmark[s >> 5] |= 1u << (s & 31);
                 queue[1] = (int32_t)sent;
             }
             rear = 2;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                     xu = x[u];
                 }
                 pu = -1;
-                if (lane == 0) qmark[u] = 0;
+                if (lane == 0) atomicAnd(qmark + (u >> 5), ~(1u << (u & 31)));
                 const double th = theta_d(A.tcoeff, d);
                 if (A.sgn ? fabs(ru) < th : ru < th) {
                     __syncwarp();
@@ -161,13 +162,16 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                     int32_t v = 0;
                     if (j < d) {
                         v = base == 0 ? c0 : A.g.col[rs + j];
+                        // the three loads of the arc, issued together
                         const double old = r[v];
+                        const uint32_t qm = qmark[v >> 5];
+                        const int32_t dv = A.g.deg[v];
                         const double rv = __dadd_rn(old, __dmul_rn(res, w));
                         r[v] = __double_as_longlong(rv) == 0 ? -0.0 : rv;
                         fresh = __double_as_longlong(old) == 0;
                         hit |= v == pu;
-                        if (!qmark[v]) {
-                            const double tv = theta_d(A.tcoeff, A.g.deg[v]);
+                        if (!((qm >> (v & 31)) & 1u)) {
+                            const double tv = theta_d(A.tcoeff, dv);
                             act = A.sgn ? fabs(rv) >= tv : rv >= tv;
                         }
                     }
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                         int64_t q = rear + __popc(bal & lanemask_lt());
                         if (q >= qcap) q -= qcap;
                         queue[q] = v;
-                        qmark[v] = 1;
+                        atomicOr(qmark + (v >> 5), 1u << (v & 31));
                     }
                     rear += __popc(bal);
                     if (rear >= qcap) rear -= qcap;
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 if (A.sgn ? fabs(ru2) >= th : ru2 >= th) {
                     if (lane == 0) {
                         queue[rear] = (int32_t)u;
-                        qmark[u] = 1;
+                        atomicOr(qmark + (u >> 5), 1u << (u & 31));
                     }
                     rear = (rear + 1 == qcap) ? 0 : rear + 1;
                 }
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 xv = x[v];
                 x[v] = 0.0;
                 r[v] = 0.0;
-                qmark[v] = 0;
+                atomicAnd(qmark + (v >> 5), ~(1u << (v & 31)));
             }
             const unsigned nzb = __ballot_sync(FULL, xv != 0.0);
             if (xv != 0.0) {
@@ -246,7 +250,8 @@ struct FifoBatchState {
     int64_t ld = 0;
     DBuf<double> x, r;
     DBuf<int32_t> queue, touched;
-    DBuf<uint8_t> qmark;
+    DBuf<uint32_t> qmark;
+    int64_t qw = 0;
     DBuf<unsigned long long> ctr;  // next_seed
 };
 
@@ -256,7 +261,7 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
     if (slots <= 0) {
         size_t fr = 0, tot = 0;
         GD_CUDA(cudaMemGetInfo(&fr, &tot));
-        const int64_t per = ld * (8 + 8 + 4 + 1 + 4) + 8;
+        const int64_t per = ld * (8 + 8 + 4 + 4) + ld / 8 + 16;
         int64_t by_mem = (int64_t)(fr / 3) / per;
         int64_t resident = (int64_t)n_sms(G->device) * 64;  // warps
         slots = (int)(by_mem < resident ? (by_mem < 1 ? 1 : by_mem) : resident);
@@ -268,10 +273,11 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
         const size_t sn = (size_t)slots * (size_t)ld;
         F->x.alloc(sn); F->r.alloc(sn); F->touched.alloc(sn);
         F->queue.alloc((size_t)slots * (size_t)(ld + 2));
-        F->qmark.alloc(sn);
+        F->qw = ld / 32 + 1;
+        F->qmark.alloc((size_t)slots * (size_t)F->qw);
         GD_CUDA(cudaMemset(F->x.p, 0, sizeof(double) * sn));
         GD_CUDA(cudaMemset(F->r.p, 0, sizeof(double) * sn));
-        GD_CUDA(cudaMemset(F->qmark.p, 0, sn));
+        GD_CUDA(cudaMemset(F->qmark.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)F->qw));
         F->ctr.alloc(1);
     } catch (...) {
         delete F;
@@ -300,7 +306,7 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
     A.max_sweeps = p.max_sweeps > 0 ? p.max_sweeps : 1000000;
     A.n_seeds = n_seeds;
     A.xcap = xcap;
-    A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p;
+    A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p; A.qw = F->qw;
     A.touched = F->touched.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv; A.xoff = xoff;
     A.xcnt = xcnt; A.xnodes = xnodes; A.xvals = xvals; A.nslots = F->nslots;
