@@ -30,6 +30,7 @@ struct FifoBatchArgs {
     uint32_t *qmark;       // queued-node bit map per slot (qw words): L2-resident
     int64_t qw;
     int32_t *touched;      // touched list per slot (ld)
+    int32_t *plist;        // pushed-node list per slot (ld): x support
     const int64_t *seeds;
     unsigned long long *next_seed, *cursor;
     int64_t *sweeps, *ops, *pushes, *xoff, *xcnt;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
     int32_t *queue = A.queue + (int64_t)slot * (A.ld + 2);
     uint32_t *qmark = A.qmark + (int64_t)slot * A.qw;
     int32_t *touched = A.touched + off;
+    int32_t *plist = A.plist + off;
     const int64_t sent = A.n, qcap = A.n + 2;
 
     for (;;) {
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
         // b = alpha e_s, x = 0 (slot is clean); seed enqueue (:59-69).  A node
         // is "touched" once its r word is not +0.0: residuals that become
         // exactly zero are stored as -0.0, which adds like +0.0.
-        int64_t ntouch = 1;
+        int64_t ntouch = 1, npl = 0;
         if (lane == 0) {
             r[s] = A.alpha;
             touched[0] = s;
@@ -149,8 +151,13 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 svol += d;
                 pushes += 1;
                 const double res = __dmul_rn(A.omega, ru);
+                if (__double_as_longlong(xu) == 0) {  // first push of u (x never returns to +0.0)
+                    if (lane == 0) plist[npl] = (int32_t)u;
+                    ++npl;
+                }
                 if (lane == 0) {
-                    x[u] = __dadd_rn(xu, res);  // x_gain = 1
+                    const double xn = __dadd_rn(xu, res);  // x_gain = 1
+                    x[u] = __double_as_longlong(xn) == 0 ? -0.0 : xn;
                     const double rn = __dsub_rn(ru, res);
                     r[u] = __double_as_longlong(rn) == 0 ? -0.0 : rn;
                 }
@@ -201,24 +208,27 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
                 __syncwarp();
             }
         }
-        // outputs: x over touched nodes with x != 0, then clean the slot
+        // outputs: x over the pushed nodes with x != 0; then r back to +0.0
+        // over the touched nodes (stores only) and, after a sweep cap, the
+        // marks of the nodes still queued
         int64_t nx = 0;
-        for (int64_t i = lane; i < ntouch; i += 32) nx += x[touched[i]] != 0.0;
+        for (int64_t i = lane; i < npl; i += 32) nx += x[plist[i]] != 0.0;
         for (int o = 16; o > 0; o >>= 1) nx += __shfl_xor_sync(FULL, nx, o);
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(A.cursor, (unsigned long long)nx);
         base = __shfl_sync(FULL, base, 0);
+        for (int64_t i = lane; i < ntouch; i += 32) r[touched[i]] = 0.0;
+        if (!conv)
+            for (int64_t w = lane; w < A.qw; w += 32) qmark[w] = 0u;
         int64_t w = (int64_t)base;
-        for (int64_t i0 = 0; i0 < ntouch; i0 += 32) {
+        for (int64_t i0 = 0; i0 < npl; i0 += 32) {
             const int64_t i = i0 + lane;
             int32_t v = 0;
             double xv = 0.0;
-            if (i < ntouch) {
-                v = touched[i];
+            if (i < npl) {
+                v = plist[i];
                 xv = x[v];
                 x[v] = 0.0;
-                r[v] = 0.0;
-                atomicAnd(qmark + (v >> 5), ~(1u << (v & 31)));
             }
             const unsigned nzb = __ballot_sync(FULL, xv != 0.0);
             if (xv != 0.0) {
@@ -249,7 +259,7 @@ struct FifoBatchState {
     int nslots = 0;
     int64_t ld = 0;
     DBuf<double> x, r;
-    DBuf<int32_t> queue, touched;
+    DBuf<int32_t> queue, touched, plist;
     DBuf<uint32_t> qmark;
     int64_t qw = 0;
     DBuf<unsigned long long> ctr;  // next_seed
@@ -261,7 +271,7 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
     if (slots <= 0) {
         size_t fr = 0, tot = 0;
         GD_CUDA(cudaMemGetInfo(&fr, &tot));
-        const int64_t per = ld * (8 + 8 + 4 + 4) + ld / 8 + 16;
+        const int64_t per = ld * (8 + 8 + 4 + 4 + 4) + ld / 8 + 16;
         int64_t by_mem = (int64_t)(fr / 3) / per;
         int64_t resident = (int64_t)n_sms(G->device) * 64;  // warps
         slots = (int)(by_mem < resident ? (by_mem < 1 ? 1 : by_mem) : resident);
@@ -271,7 +281,7 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
         F->nslots = slots;
         F->ld = ld;
         const size_t sn = (size_t)slots * (size_t)ld;
-        F->x.alloc(sn); F->r.alloc(sn); F->touched.alloc(sn);
+        F->x.alloc(sn); F->r.alloc(sn); F->touched.alloc(sn); F->plist.alloc(sn);
         F->queue.alloc((size_t)slots * (size_t)(ld + 2));
         F->qw = ld / 32 + 1;
         F->qmark.alloc((size_t)slots * (size_t)F->qw);
@@ -307,7 +317,7 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
     A.n_seeds = n_seeds;
     A.xcap = xcap;
     A.x = F->x.p; A.r = F->r.p; A.queue = F->queue.p; A.qmark = F->qmark.p; A.qw = F->qw;
-    A.touched = F->touched.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
+    A.touched = F->touched.p; A.plist = F->plist.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv; A.xoff = xoff;
     A.xcnt = xcnt; A.xnodes = xnodes; A.xvals = xvals; A.nslots = F->nslots;
     GD_CUDA(cudaMemsetAsync(F->ctr.p, 0, sizeof(unsigned long long), st));
