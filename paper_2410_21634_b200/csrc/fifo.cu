@@ -23,18 +23,15 @@ constexpr int FIFO_THREADS = 1024;
 struct FifoArgs {
     DevGraph g;
     DevOp op;
-    int64_t dim;           // coordinates (n, or (N+1) n for the heat kernel)
+    int64_t dim;           // coordinates (n)
     double *x, *r;
     int32_t *queue;        // ring of dim + 2 slots
-    uint8_t *qmark;
+    uint32_t *qmark;       // queued-node bit map (dim / 32 + 1 words, L2/L1-resident)
     const int32_t *seeds;
     int64_t n_seeds;
     double omega, x_gain;
     int sgn;
     int64_t max_sweeps;
-    // heat kernel
-    int64_t n_stages;
-    const double *stage_w;
     // logs
     int64_t log_cap;
     int64_t *vol_log;
@@ -44,14 +41,8 @@ struct FifoArgs {
     double *out_min;
 };
 
-template <bool HK>
-__device__ __forceinline__ double coord_theta(const FifoArgs &A, int64_t idx) {
-    if (HK) {
-        int64_t u = idx % A.g.n;
-        int32_t d = A.g.deg[u];
-        return d > 0 ? __dmul_rn(A.op.tcoeff, (double)d) : __longlong_as_double(0x7ff0000000000000LL);
-    }
-    return theta_of(A.op, idx, A.g.deg[idx]);
+__device__ __forceinline__ bool qm_test(const uint32_t *q, int64_t v) {
+    return (q[v >> 5] >> (v & 31)) & 1u;
 }
 
 // Block-wide l1 / min over r[0, dim): fixed-shape, deterministic.
@@ -89,7 +80,11 @@ __device__ void block_l1_min(const FifoArgs &A, double *s_s, double *s_m, double
     __syncthreads();
 }
 
-template <bool HK>
+// One warp runs the pop chain; at each sentinel the whole block rescans r
+// for the l1 / min logs (:127-132).  Per pop the next queue entry's r, x,
+// degree, row and first 32 neighbours are prefetched while the current pop
+// scatters (r is re-read if the scatter touched it; x is written only by a
+// node's own pops), and each arc's r / mark / threshold loads issue together.
 __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
     __shared__ double s_s[32], s_m[32];
     __shared__ int64_t sh_front, sh_rear, sh_sweeps, sh_ops, sh_pushes, sh_svol;
@@ -98,16 +93,17 @@ __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
     const int64_t sent = A.dim, qcap = A.dim + 2;
     const int lane = threadIdx.x & 31;
     const bool w0 = threadIdx.x < 32;
+    const unsigned FULLM = 0xffffffffu;
 
     if (threadIdx.x == 0) {  // seed enqueue, sequential (:59-69)
         int64_t rear = 0;
         for (int64_t i = 0; i < A.n_seeds; i++) {
             int32_t u = A.seeds[i];
-            bool act = is_active(A.r[u], coord_theta<HK>(A, u), A.sgn);
-            if (act && !A.qmark[u]) {
+            bool act = is_active(A.r[u], theta_of(A.op, u, A.g.deg[u]), A.sgn);
+            if (act && !qm_test(A.qmark, u)) {
                 A.queue[rear] = u;
                 rear = (rear + 1) % qcap;
-                A.qmark[u] = 1;
+                A.qmark[u >> 5] |= 1u << (u & 31);
             }
         }
         sh_front = 0;
@@ -137,78 +133,95 @@ __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
             int64_t front = sh_front, rear = sh_rear, svol = sh_svol, pushes = sh_pushes;
             double sgamma = sh_sgamma;
             int pos = sh_pos, neg = sh_neg;
+            int64_t pu = -1, prs = 0;
+            double pr = 0.0, px = 0.0;
+            int32_t pd = 0, pcol = 0;
             for (;;) {
-                int64_t idx = A.queue[front];
+                const int64_t u = A.queue[front];
                 front = (front + 1 == qcap) ? 0 : front + 1;
-                if (idx == sent) break;
-                if (lane == 0) A.qmark[idx] = 0;
-                double ru = A.r[idx];
-                double th = coord_theta<HK>(A, idx);
+                if (u == sent) break;
+                double ru, xu;
+                int32_t d, c0;
+                int64_t rs;
+                if (u == pu) {
+                    ru = pr;
+                    d = pd;
+                    rs = prs;
+                    c0 = pcol;
+                    xu = px;
+                } else {
+                    ru = A.r[u];
+                    d = A.g.deg[u];
+                    rs = A.g.row[u];
+                    c0 = lane < d ? A.g.col[rs + lane] : 0;
+                    xu = A.x[u];
+                }
+                pu = -1;
+                if (lane == 0) atomicAnd(A.qmark + (u >> 5), ~(1u << (u & 31)));
+                const double th = theta_of(A.op, u, d);
                 if (!is_active(ru, th, A.sgn)) {
                     __syncwarp();
                     continue;
                 }
-                int64_t u = HK ? idx % A.g.n : idx;
-                int64_t k = HK ? idx / A.g.n : 0;
-                int32_t d = A.g.deg[u];
-                int64_t rs = A.g.row[u];
+                if (front != rear) {  // prefetch the next pop
+                    const int64_t nx = A.queue[front];
+                    if (nx != sent) {
+                        pu = nx;
+                        pr = A.r[nx];
+                        pd = A.g.deg[nx];
+                        prs = A.g.row[nx];
+                        px = A.x[nx];
+                        pcol = lane < pd ? A.g.col[prs + lane] : 0;
+                    }
+                }
                 svol += d;
                 sgamma += fabs(ru);
                 pushes += 1;
                 if (ru > 0.0) pos = 1;
                 else if (ru < 0.0) neg = 1;
-                double res;            // mass pushed along the arcs
-                int64_t tbase = 0;     // target coordinate offset
-                bool scatter = true;
-                if (HK) {
-                    if (lane == 0) {
-                        A.x[idx] = __dadd_rn(A.x[idx], ru);
-                        A.r[idx] = 0.0;
-                    }
-                    scatter = k < A.n_stages;
-                    res = scatter ? __dmul_rn(ru, A.stage_w[scatter ? k : 0]) : 0.0;
-                    tbase = (k + 1) * A.g.n;
-                } else {
-                    res = __dmul_rn(A.omega, ru);
-                    if (lane == 0) {
-                        A.x[idx] = __dadd_rn(A.x[idx], __dmul_rn(A.x_gain, res));
-                        A.r[idx] = __dsub_rn(ru, res);
-                    }
+                const double res = __dmul_rn(A.omega, ru);
+                if (lane == 0) {
+                    A.x[u] = __dadd_rn(xu, __dmul_rn(A.x_gain, res));
+                    A.r[u] = __dsub_rn(ru, res);
                 }
-                if (scatter) {
-                    double wn = HK ? __ddiv_rn(1.0, (double)d) : node_weight(A.op, d);
-                    for (int64_t base = 0; base < d; base += 32) {
-                        int64_t j = base + lane;
-                        bool act = false;
-                        int64_t t = 0;
-                        if (j < d) {
-                            t = tbase + A.g.col[rs + j];
-                            double w = HK ? wn : arc_weight(A.op, wn, rs + j);
-                            double rv = __dadd_rn(A.r[t], __dmul_rn(res, w));
-                            A.r[t] = rv;
-                            act = !A.qmark[t] && is_active(rv, coord_theta<HK>(A, t), A.sgn);
-                        }
-                        unsigned bal = __ballot_sync(0xffffffffu, act);
-                        if (act) {
-                            int64_t slot = rear + __popc(bal & ((1u << lane) - 1u));
-                            if (slot >= qcap) slot -= qcap;
-                            A.queue[slot] = (int32_t)t;
-                            A.qmark[t] = 1;
-                        }
-                        rear += __popc(bal);
-                        if (rear >= qcap) rear -= qcap;
+                const double wn = node_weight(A.op, d);
+                bool hit = false;
+                for (int64_t base = 0; base < d; base += 32) {
+                    const int64_t j = base + lane;
+                    bool act = false;
+                    int32_t t = 0;
+                    if (j < d) {
+                        t = base == 0 ? c0 : A.g.col[rs + j];
+                        // the arc's loads, issued together
+                        const double old = A.r[t];
+                        const uint32_t qm = A.qmark[t >> 5];
+                        const double tht = theta_of(A.op, t, A.g.deg[t]);
+                        const double w = arc_weight(A.op, wn, rs + j);
+                        const double rv = __dadd_rn(old, __dmul_rn(res, w));
+                        A.r[t] = rv;
+                        hit |= t == pu;
+                        act = !((qm >> (t & 31)) & 1u) && is_active(rv, tht, A.sgn);
                     }
+                    const unsigned bal = __ballot_sync(FULLM, act);
+                    if (act) {
+                        int64_t slot = rear + __popc(bal & ((1u << lane) - 1u));
+                        if (slot >= qcap) slot -= qcap;
+                        A.queue[slot] = t;
+                        atomicOr(A.qmark + (t >> 5), 1u << (t & 31));
+                    }
+                    rear += __popc(bal);
+                    if (rear >= qcap) rear -= qcap;
                 }
                 __syncwarp();
-                if (!HK) {  // self re-check (:176-185); qmark[u] was cleared at pop
-                    double ru2 = __dsub_rn(ru, res);
-                    if (is_active(ru2, th, A.sgn)) {
-                        if (lane == 0) {
-                            A.queue[rear] = (int32_t)idx;
-                            A.qmark[idx] = 1;
-                        }
-                        rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                if (__any_sync(FULLM, hit)) pr = A.r[pu];  // the scatter changed the next pop's r
+                // self re-check (:176-185); the mark of u was cleared at pop
+                const double ru2 = __dsub_rn(ru, res);
+                if (is_active(ru2, th, A.sgn)) {
+                    if (lane == 0) {
+                        A.queue[rear] = (int32_t)u;
+                        atomicOr(A.qmark + (u >> 5), 1u << (u & 31));
                     }
+                    rear = (rear + 1 == qcap) ? 0 : rear + 1;
                 }
                 __syncwarp();
             }
@@ -261,7 +274,7 @@ __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
 struct FifoWS {
     DBuf<double> x, r, gam, l1, mn;
     DBuf<int32_t> queue, sd;
-    DBuf<uint8_t> qmark;
+    DBuf<uint32_t> qmark;
     DBuf<int64_t> vol, out;
     DBuf<int8_t> sgn;
 };
@@ -275,7 +288,7 @@ void run_fifo(const gd_graph *G, FifoArgs A, double *hx, double *hr,
     FifoWS &W = *ws;
     int64_t log_cap = A.max_sweeps < (1 << 20) ? A.max_sweeps + 1 : (1 << 20);
     W.x.ensure(dim ? dim : 1); W.r.ensure(dim ? dim : 1); W.queue.ensure(dim + 2);
-    W.sd.ensure(n_seeds ? n_seeds : 1); W.qmark.ensure(dim ? dim : 1);
+    W.sd.ensure(n_seeds ? n_seeds : 1); W.qmark.ensure(dim / 32 + 1);
     W.vol.ensure(log_cap); W.out.ensure(4); W.gam.ensure(log_cap); W.l1.ensure(log_cap + 1);
     W.mn.ensure(1); W.sgn.ensure(log_cap);
     auto &x = W.x, &r = W.r, &gam = W.gam, &l1 = W.l1, &mn = W.mn;
@@ -285,7 +298,7 @@ void run_fifo(const gd_graph *G, FifoArgs A, double *hx, double *hr,
     auto &sgn = W.sgn;
     GD_CUDA(cudaMemcpy(x.p, hx, sizeof(double) * dim, cudaMemcpyHostToDevice));
     GD_CUDA(cudaMemcpy(r.p, hr, sizeof(double) * dim, cudaMemcpyHostToDevice));
-    GD_CUDA(cudaMemset(qmark.p, 0, dim ? dim : 1));
+    GD_CUDA(cudaMemset(qmark.p, 0, sizeof(uint32_t) * (dim / 32 + 1)));
     std::vector<int32_t> s32(n_seeds);
     for (int64_t i = 0; i < n_seeds; i++) {
         GD_CHECK_ARG(seeds[i] >= 0 && seeds[i] < dim, "seed out of range");
@@ -296,7 +309,7 @@ void run_fifo(const gd_graph *G, FifoArgs A, double *hx, double *hr,
     A.x = x.p; A.r = r.p; A.queue = queue.p; A.qmark = qmark.p; A.seeds = sd.p;
     A.n_seeds = n_seeds; A.log_cap = log_cap; A.vol_log = vol.p; A.gamma_log = gam.p;
     A.l1_log = l1.p; A.sign_log = sgn.p; A.out = out.p; A.out_min = mn.p;
-    k_fifo<false><<<1, FIFO_THREADS>>>(A);  // (the HK instantiation is unused: hk.cu)
+    k_fifo<<<1, FIFO_THREADS>>>(A);
     GD_LAUNCH_CHECK();
     GD_CUDA(cudaDeviceSynchronize());
     int64_t o[4];
