@@ -31,33 +31,60 @@ __device__ __forceinline__ double pull_weight(const DevGraph &g, const DevOp &op
     return op.arc_w[lo];
 }
 
-// r_next = beta P r (pull), plus any-active flag and partial l1 / l2 sums.
+// Ordered pull of row v by one warp: lanes form c_j = fl(src[u_j] w_j) for 32
+// consecutive arcs (sources ascending: the reference's scatter order), lane 0
+// adds the nonzero ones in order (zeros are skipped as _scatter_full does).
+// Hub rows no longer serialise one thread for thousands of arcs.
+__device__ __forceinline__ double warp_row_fold(const DevGraph &g, const DevOp &op,
+                                                const double *__restrict__ src, int64_t v,
+                                                int lane) {
+    const int64_t rs = g.row[v], re = g.row[v + 1];
+    double acc = 0.0;
+    for (int64_t b = rs; b < re; b += 32) {
+        const int64_t j = b + lane;
+        double c = 0.0;
+        bool nz = false;
+        if (j < re) {
+            const int32_t u = g.col[j];
+            const double val = src[u];
+            nz = val != 0.0;
+            if (nz) c = __dmul_rn(val, pull_weight(g, op, u, v));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, nz);
+        const int cnt = (int)min((int64_t)32, re - b);
+        for (int l = 0; l < cnt; l++) {
+            const double cl = __shfl_sync(0xffffffffu, c, l);
+            if ((m >> l) & 1u) acc = __dadd_rn(acc, cl);
+        }
+    }
+    return acc;  // (valid in every lane: all lanes run the same adds)
+}
+
+// r_next = beta P r (pull, warp per row), plus any-active flag and partial
+// l1 / l2 sums.
 __global__ void k_pull(DevGraph g, DevOp op, const double *__restrict__ r,
                        double *__restrict__ nxt, int *__restrict__ active,
                        double *__restrict__ part) {
     __shared__ double s1[TPB / 32], s2[TPB / 32];
+    const int lane = threadIdx.x & 31;
     double a1 = 0.0, a2 = 0.0;
     int any = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int64_t j = g.row[v]; j < g.row[v + 1]; j++) {
-            int32_t u = g.col[j];
-            double val = r[u];
-            if (val == 0.0) continue;
-            acc = __dadd_rn(acc, __dmul_rn(val, pull_weight(g, op, u, v)));
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < g.n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double acc = warp_row_fold(g, op, r, v, lane);
+        if (lane == 0) {
+            nxt[v] = acc;
+            a1 += fabs(acc);
+            a2 += acc * acc;
+            any |= acc >= theta_of(op, v, g.deg[v]);
         }
-        nxt[v] = acc;
-        a1 += fabs(acc);
-        a2 += acc * acc;
-        any |= acc >= theta_of(op, v, g.deg[v]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         a1 += __shfl_xor_sync(0xffffffffu, a1, o);
         a2 += __shfl_xor_sync(0xffffffffu, a2, o);
     }
     any = __any_sync(0xffffffffu, any);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         s1[threadIdx.x >> 5] = a1;
         s2[threadIdx.x >> 5] = a2;
         if (any) atomicOr(active, 1);
@@ -115,7 +142,7 @@ extern "C" int gd_gradient_descent(const gd_graph *G, const gd_operator *o, cons
         HostOp op;
         upload_op(G, o, G->n, op, 0);
         const int64_t n = G->n;
-        const int blocks = 4 * n_sms(G->device);
+        const int blocks = 16 * n_sms(G->device);  // (warp-per-row pulls)
         DevGraph g = G->view();
         DBuf<double> x(n ? n : 1), r(n ? n : 1), nx(n ? n : 1), part(2 * blocks);
         DBuf<int> act(1);
@@ -264,16 +291,11 @@ namespace {
 // out[v] = sum over u in N(v), ascending, of src[u] * w(u -> v); src[u] == 0 skipped
 __global__ void k_pull_plain(DevGraph g, DevOp op, const double *__restrict__ src,
                              double *__restrict__ out) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int64_t j = g.row[v]; j < g.row[v + 1]; j++) {
-            const int32_t u = g.col[j];
-            const double val = src[u];
-            if (val == 0.0) continue;
-            acc = __dadd_rn(acc, __dmul_rn(val, pull_weight(g, op, u, v)));
-        }
-        out[v] = acc;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < g.n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double acc = warp_row_fold(g, op, src, v, lane);
+        if (lane == 0) out[v] = acc;
     }
 }
 
@@ -376,7 +398,7 @@ extern "C" int gd_chebyshev(const gd_graph *G, const gd_operator *o, const doubl
         upload_op(G, o, G->n, op, 0);
         const int64_t n = G->n;
         const size_t nn = n ? n : 1;
-        const int blocks = 4 * n_sms(G->device);
+        const int blocks = 16 * n_sms(G->device);  // (warp-per-row pulls)
         DevGraph g = G->view();
         DBuf<double> x(nn), r(nn), inc(nn), prev(nn), scat(nn), part(2 * blocks);
         DBuf<int> act(1);
@@ -446,7 +468,7 @@ extern "C" int gd_hk_taylor(const gd_graph *G, int64_t n_stages, const double *s
         GD_CUDA(cudaSetDevice(G->device));
         const int64_t n = G->n;
         const size_t nn = n ? n : 1;
-        const int blocks = 4 * n_sms(G->device);
+        const int blocks = 16 * n_sms(G->device);  // (warp-per-row pulls)
         DevGraph g = G->view();
         const DevOp op{GD_W_RW, GD_T_DEGREE, 1.0, 0.0, nullptr, nullptr};  // bare 1/d_u
         DBuf<double> vk(nn), nxt(nn);
