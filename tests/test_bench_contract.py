@@ -27,3 +27,21 @@ def test_reference_arm_json_line(method):
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert "workload" in line["config"] and "model" not in line["config"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["local-gd", "local-ch", "local-sor", "local-hk"])
+def test_gpu_arm_json_line(method):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--shape", "arxiv", "--eps", "1e-5",
+           "--seeds", "64", "--steps", "2", "--warmup", "3", "--method", method,
+           "--cpu-seconds", "1", "--tau", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert line["gpu_launches"] > 0 and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]
+    assert line["cpu_baseline"]["parity_sweeps_ops_identical"] is True
