@@ -215,6 +215,9 @@ typedef struct {
     int64_t n_stages;        /* N */
     const double *stage_w;   /* host, N entries: tau/(k+1) as the system stores them */
     double theta_coeff;      /* eps / (2 (N+1) vol); theta = fl(coeff * d) */
+    int32_t want_r;          /* 1: also return each seed's final r as a sparse vector
+                                (GD_M_LOCAL_GD / GD_M_LOCAL_CH / GD_M_LOCAL_SOR) */
+    int32_t reserved;
 } gd_batch_params;
 
 typedef struct {
@@ -248,6 +251,15 @@ int gd_batch_fetch_host(gd_batch *b, int64_t n_seeds, int64_t *sweeps, int64_t *
                         int64_t *pushes, int32_t *converged, int64_t *x_offset, int64_t *x_count,
                         int32_t *x_nodes, double *x_vals, int64_t x_cap, int64_t *x_total,
                         void *stream);
+/* Sparse r of the last solve (want_r): device arrays owned by the batch
+ * (r_offset / r_count per seed, then (node, value) pairs, caller ids). */
+int gd_batch_r_device(const gd_batch *b, int64_t **r_offset, int64_t **r_count,
+                      int32_t **r_nodes, double **r_vals, int64_t *r_total);
+/* The same copied into host buffers; GD_ERR_CAPACITY with *r_total set when
+ * r_cap is too small (fetch again with larger buffers). */
+int gd_batch_fetch_r_host(gd_batch *b, int64_t n_seeds, int64_t *r_offset, int64_t *r_count,
+                          int32_t *r_nodes, double *r_vals, int64_t r_cap, int64_t *r_total,
+                          void *stream);
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);

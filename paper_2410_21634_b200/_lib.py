@@ -58,7 +58,8 @@ class BatchParams(C.Structure):
                 ("frontier_cap", C.c_int64), ("out_cap", C.c_int64),
                 ("relabel", C.c_int32), ("problem", C.c_int32), ("omega", C.c_double),
                 ("mu", C.c_double), ("L", C.c_double), ("tau", C.c_double),
-                ("n_stages", C.c_int64), ("stage_w", _f64p), ("theta_coeff", C.c_double)]
+                ("n_stages", C.c_int64), ("stage_w", _f64p), ("theta_coeff", C.c_double),
+                ("want_r", C.c_int32), ("reserved", C.c_int32)]
 
 
 class BatchResult(C.Structure):
@@ -108,6 +109,10 @@ SIGNATURES = {
     "gd_batch_fetch_host": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _i64p, _i32p, _i64p,
                                       _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
     "gd_batch_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
+    "gd_batch_r_device": (C.c_int, [C.c_void_p, C.POINTER(_i64p), C.POINTER(_i64p), C.POINTER(_i32p),
+                                    C.POINTER(_f64p), _i64p]),
+    "gd_batch_fetch_r_host": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _i32p, _f64p, C.c_int64,
+                                        _i64p, C.c_void_p]),
     "gd_batch_round_log": (C.c_int, [C.c_void_p, _i64p, C.c_int64, _i64p]),
     "gd_pairs_create": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, C.c_int64, C.c_int64,
                                   C.c_int64, C.POINTER(C.c_void_p), _i64p, _i64p, _i64p, _i32p]),

@@ -50,6 +50,22 @@ class BatchOutput:
     x_count: np.ndarray
     x_nodes: np.ndarray
     x_vals: np.ndarray
+    r_offset: np.ndarray | None = None  # (want_r) final residual, sparse per seed
+    r_count: np.ndarray | None = None
+    r_nodes: np.ndarray | None = None
+    r_vals: np.ndarray | None = None
+
+    def r_sparse(self, i: int) -> tuple[np.ndarray, np.ndarray]:
+        if self.r_offset is None:
+            raise ValueError("the solver was created without want_r")
+        a, c = int(self.r_offset[i]), int(self.r_count[i])
+        return self.r_nodes[a:a + c], self.r_vals[a:a + c]
+
+    def r_dense(self, i: int, n: int) -> np.ndarray:
+        r = np.zeros(n)
+        nodes, vals = self.r_sparse(i)
+        r[nodes] = vals
+        return r
 
     def x_sparse(self, i: int) -> tuple[np.ndarray, np.ndarray]:
         a, c = int(self.x_offset[i]), int(self.x_count[i])
@@ -78,7 +94,7 @@ class BatchSolver:
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
-                 L: float | None = None, hk: dict | None = None):
+                 L: float | None = None, hk: dict | None = None, want_r: bool = False):
         if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
         if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
@@ -112,7 +128,9 @@ class BatchSolver:
                             problem=gdl.GD_P_KATZ if problem == "katz" else gdl.GD_P_PPR,
                             omega=float(omega), mu=float(mu or 0.0), L=float(L or 0.0),
                             tau=float(hk.get("tau", 0.0)), n_stages=int(hk.get("n_stages", 0)),
-                            stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)))
+                            stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)),
+                            want_r=int(bool(want_r) and method != "local-hk"))
+        self.want_r = bool(want_r) and method != "local-hk"
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
         self.handle = h
@@ -210,9 +228,26 @@ class BatchSolver:
         gdl.check(rc)
         t = int(tot.value)
         self._last_total = t
-        return BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
-                           out["converged"][:k].astype(bool), out["x_offset"][:k],
-                           out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
+        res = BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
+                          out["converged"][:k].astype(bool), out["x_offset"][:k],
+                          out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
+        if self.want_r:
+            roff, rcnt = np.empty(k, np.int64), np.empty(k, np.int64)
+            rt = C.c_int64()
+            cap = max(int(1.25 * getattr(self, "_last_rtotal", 0)) + 1024, 1024)
+            for _ in range(2):
+                rn, rv = np.empty(cap, np.int32), np.empty(cap)
+                rc = self.lib.gd_batch_fetch_r_host(self.handle, k, gdl.ptr(roff, C.c_int64),
+                                                    gdl.ptr(rcnt, C.c_int64), gdl.ptr(rn, C.c_int32),
+                                                    gdl.ptr(rv), cap, C.byref(rt), C.c_void_p(st))
+                if rc != gdl.GD_ERR_CAPACITY:
+                    break
+                cap = int(rt.value) + 1024
+            gdl.check(rc)
+            self._last_rtotal = int(rt.value)
+            res.r_offset, res.r_count = roff, rcnt
+            res.r_nodes, res.r_vals = rn[:rt.value], rv[:rt.value]
+        return res
 
 
 

@@ -43,6 +43,20 @@
 namespace cg = cooperative_groups;
 
 namespace gd {  // fifo_batch.cu
+// optional sparse r output of a solve (want_r); null pointer = not wanted
+struct RPool {
+    int64_t *off, *cnt;          // per seed
+    int32_t *nodes;
+    double *vals;
+    int64_t cap;
+    unsigned long long *cursor;  // pairs used
+    unsigned long long *scratch; // per (slot, chunk) counts
+};
+void r_extract_wave(uint32_t *secmap, int64_t smw, double *r, int64_t ld, int64_t m,
+                    const int32_t *inv, int64_t seed_base, unsigned long long *cnt_scratch,
+                    unsigned long long *cursor, int64_t *r_off, int64_t *r_cnt,
+                    int32_t *r_nodes, double *r_vals, int64_t rcap, cudaStream_t st);
+int r_extract_chunks(int64_t smw);
 struct FifoBatchState;
 FifoBatchState *fifo_batch_create(const gd_graph *G, int slots);
 void fifo_batch_destroy(FifoBatchState *F);
@@ -55,12 +69,13 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
                       int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
-                      cudaStream_t st);
+                      cudaStream_t st, const RPool *rp);
 int fifo_batch_slots(const FifoBatchState *F);
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
                     int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
-                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st);
+                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st,
+                    const RPool *rp);
 }  // namespace gd
 
 namespace gd {
@@ -784,7 +799,114 @@ __global__ void k_remap_rows(DevGraph g, const int32_t *__restrict__ inv,
     }
 }
 
+// ---- optional sparse r out (gd_batch_params.want_r) ----------------------
+// r of a slot is nonzero only inside its touched 32 B sectors (sector map),
+// so the reset walk doubles as the extraction: count the nonzero entries per
+// (slot, chunk), reserve each slot's segment of the r pool, then emit (node,
+// value) pairs and zero the sectors / clear the map in one more walk.
+__global__ void k_r_count(const uint32_t *__restrict__ secmap, int64_t smw,
+                          const double *__restrict__ r, int64_t ld,
+                          unsigned long long *__restrict__ cnt) {
+    __shared__ unsigned long long bsum;
+    const int k = blockIdx.y;
+    const int64_t per = (smw + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = min(smw, lo + per);
+    const uint32_t *map = secmap + (int64_t)k * smw;
+    const double *rk = r + (int64_t)k * ld;
+    if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
+    unsigned long long c = 0;
+    for (int64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint32_t bits = map[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t i0 = (w * 32 + b) * 4;
+            for (int q = 0; q < 4 && i0 + q < ld; ++q) c += rk[i0 + q] != 0.0;
+        }
+    }
+    atomicAdd(&bsum, c);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[(int64_t)k * gridDim.x + blockIdx.x] = bsum;
+}
+
+// one thread per slot: chunk offsets (exclusive, in place) and the slot's
+// segment of the pool
+__global__ void k_r_reserve(int64_t m, int chunks, unsigned long long *__restrict__ cnt,
+                            unsigned long long *__restrict__ cursor, int64_t seed_base,
+                            int64_t *__restrict__ r_off, int64_t *__restrict__ r_cnt) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    unsigned long long run = 0;
+    for (int c = 0; c < chunks; ++c) {
+        const unsigned long long x = cnt[k * chunks + c];
+        cnt[k * chunks + c] = run;
+        run += x;
+    }
+    const unsigned long long base = atomicAdd(cursor, run);
+    for (int c = 0; c < chunks; ++c) cnt[k * chunks + c] += base;
+    r_off[seed_base + k] = (int64_t)base;
+    r_cnt[seed_base + k] = (int64_t)run;
+}
+
+__global__ void k_r_emit(uint32_t *__restrict__ secmap, int64_t smw, double *__restrict__ r,
+                         int64_t ld, const unsigned long long *__restrict__ cnt,
+                         const int32_t *__restrict__ inv, int32_t *__restrict__ r_nodes,
+                         double *__restrict__ r_vals, int64_t rcap) {
+    __shared__ unsigned long long bpos;
+    const int k = blockIdx.y;
+    const int64_t per = (smw + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = min(smw, lo + per);
+    uint32_t *map = secmap + (int64_t)k * smw;
+    double *rk = r + (int64_t)k * ld;
+    if (threadIdx.x == 0) bpos = cnt[(int64_t)k * gridDim.x + blockIdx.x];
+    __syncthreads();
+    for (int64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint32_t bits = map[w];
+        if (!bits) continue;
+        map[w] = 0u;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t i0 = (w * 32 + b) * 4;
+            for (int q = 0; q < 4 && i0 + q < ld; ++q) {
+                const double v = rk[i0 + q];
+                rk[i0 + q] = 0.0;
+                if (v != 0.0) {
+                    const unsigned long long at = atomicAdd(&bpos, 1ULL);
+                    if ((int64_t)at < rcap) {
+                        r_nodes[at] = inv ? inv[i0 + q] : (int32_t)(i0 + q);
+                        r_vals[at] = v;
+                    }
+                }
+            }
+        }
+    }
+}
+
 }  // namespace
+
+// Sparse r of the m slots of a wave into the pool (and the slots' r back to
+// +0.0, sector map cleared): replaces the reset of that wave.
+void r_extract_wave(uint32_t *secmap, int64_t smw, double *r, int64_t ld, int64_t m,
+                    const int32_t *inv, int64_t seed_base, unsigned long long *cnt_scratch,
+                    unsigned long long *cursor, int64_t *r_off, int64_t *r_cnt,
+                    int32_t *r_nodes, double *r_vals, int64_t rcap, cudaStream_t st) {
+    const int64_t c = (smw + 2047) / 2048;
+    const int chunks = (int)(c < 32 ? 32 : (c > 4096 ? 4096 : c));
+    k_r_count<<<dim3(chunks, (unsigned)m), 256, 0, st>>>(secmap, smw, r, ld, cnt_scratch);
+    k_r_reserve<<<(int)((m + 127) / 128), 128, 0, st>>>(m, chunks, cnt_scratch, cursor, seed_base,
+                                                         r_off, r_cnt);
+    k_r_emit<<<dim3(chunks, (unsigned)m), 256, 0, st>>>(secmap, smw, r, ld, cnt_scratch, inv,
+                                                        r_nodes, r_vals, rcap);
+    GD_LAUNCH_CHECK();
+}
+
+int r_extract_chunks(int64_t smw) {
+    const int64_t c = (smw + 2047) / 2048;
+    return (int)(c < 32 ? 32 : (c > 4096 ? 4096 : c));
+}
+
 }  // namespace gd
 
 using namespace gd;
@@ -813,6 +935,16 @@ struct gd_batch {
     DBuf<uint32_t> secmap;
     int64_t smw = 0;
     bool hk = false;           // GD_M_HK: layered stage sweeps
+    // optional sparse r output (want_r)
+    DBuf<int64_t> roff, rcnt;
+    DBuf<int32_t> rnodes;
+    DBuf<double> rvals;
+    DBuf<unsigned long long> rcursor, rscratch;
+    int64_t rcap = 0, last_r_total = 0;
+    bool want_r() const { return p.want_r != 0 && !hk; }
+    RPool rpool() {
+        return RPool{roff.p, rcnt.p, rnodes.p, rvals.p, rcap, rcursor.p, rscratch.p};
+    }
     DBuf<double> r2, stage_w;  // (heat kernel) second residual layer, tau/(k+1)
     DBuf<uint32_t> secmap2;
     // results
@@ -877,6 +1009,13 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->sweeps.ensure(ns); B->ops.ensure(ns); B->pushes.ensure(ns); B->support.ensure(ns);
     B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
+    RPool rp{};
+    if (B->want_r()) {
+        B->roff.ensure(ns); B->rcnt.ensure(ns);
+        GD_CUDA(cudaMemsetAsync(B->rcursor.p, 0, sizeof(unsigned long long), st));
+        rp = B->rpool();
+    }
+    const RPool *rpp = B->want_r() ? &rp : nullptr;
     GD_CUDA(cudaMemsetAsync(B->overflow.p, 0, sizeof(int32_t), st));
     if (B->fifo) {  // FIFO methods: one persistent launch, warps pull seeds
         if (B->ev.empty()) {
@@ -891,7 +1030,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         if (n_seeds)
             fifo_batch_run(B->fifo, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
                            B->pushes.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p,
-                           B->xvals.p, B->xcap, B->cursor.p, st);
+                           B->xvals.p, B->xcap, B->cursor.p, st, rpp);
         GD_CUDA(cudaEventRecord(B->ev[1], st));
         GD_CUDA(cudaStreamSynchronize(st));
         float f = 0.f;
@@ -909,7 +1048,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         signed_batch_run(B->sgn, B->work(), B->p, d_seeds, n_seeds, B->R ? B->perm.p : nullptr,
                          B->R ? B->inv.p : nullptr, B->sweeps.p, B->ops.p, B->pushes.p,
                          B->support.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p, B->xvals.p,
-                         B->xcap, B->cursor.p, B->ev, &B->last_ms, &B->last_launches, st);
+                         B->xcap, B->cursor.p, B->ev, &B->last_ms, &B->last_launches, st, rpp);
         return;
     }
     const int64_t waves = (n_seeds + B->slots - 1) / B->slots;
@@ -938,7 +1077,11 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
                                             stage_bytes(B->slots), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
         k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
-        k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A);
+        if (rpp)  // the r extraction zeroes the slots' r itself
+            r_extract_wave(A.secmap, A.smw, A.r, A.ld, A.m, B->R ? B->inv.p : nullptr, base,
+                           rp.scratch, rp.cursor, rp.off, rp.cnt, rp.nodes, rp.vals, rp.cap, st);
+        else
+            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A);
         if (B->hk) {  // the other residual layer
             RoundArgs A2 = A;
             A2.r = A.r2;
@@ -1065,6 +1208,12 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->G = G;
             B->p = *p;
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
+            if (p->want_r && p->method != GD_M_HK) {  // sparse r pool (per-slot scratch below)
+                B->rcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
+                B->rnodes.alloc(B->rcap);
+                B->rvals.alloc(B->rcap);
+                B->rcursor.alloc(1);
+            }
             if (p->method == GD_M_LOCAL_SOR) {
                 // exact FIFO replay needs the caller's CSR order: no relabeling
                 B->fifo = fifo_batch_create(G, p->slots);
@@ -1100,6 +1249,8 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 }
                 if (slots > 2048) slots = 2048;
                 B->slots = slots;
+                { const int64_t ldr = (n + 3) & ~3LL, smwr = (ldr / 4 + 31) / 32;  // r extraction scratch
+                  if (B->rcap) B->rscratch.alloc((size_t)B->slots * (size_t)r_extract_chunks(smwr)); }
                 B->xcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
                 B->cursor.alloc(1); B->overflow.alloc(1);
                 B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
@@ -1126,6 +1277,8 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             }
             if (slots > 2048) slots = 2048;  // per-block slot counters live in shared memory
             B->slots = slots;
+            { const int64_t ldr = (n + 3) & ~3LL, smwr = (ldr / 4 + 31) / 32;  // r extraction scratch
+              if (B->rcap) B->rscratch.alloc((size_t)B->slots * (size_t)r_extract_chunks(smwr)); }
             int64_t fc = p->frontier_cap > 0 ? p->frontier_cap : (int64_t)slots * n;
             if (p->frontier_cap <= 0 && fc > (64LL << 20) && !B->hk) fc = 64LL << 20;
             B->fcap = fc;
@@ -1214,12 +1367,23 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
             }
             res->x_total = (int64_t)used;
             B->last_x_total = (int64_t)used;
-            if ((int64_t)used <= B->xcap) break;
+            unsigned long long rused = 0;
+            if (B->want_r())
+                GD_CUDA(cudaMemcpy(&rused, B->rcursor.p, sizeof(rused), cudaMemcpyDeviceToHost));
+            B->last_r_total = (int64_t)rused;
+            if ((int64_t)used <= B->xcap && (int64_t)rused <= B->rcap) break;
             GD_CHECK_ARG(attempt == 0, "output pool sizing failed");
             // grow (doubling, so a growing workload redoes at most log times) and redo
-            B->xcap = 2 * ((int64_t)used > B->xcap ? (int64_t)used : B->xcap);
-            B->xnodes.alloc(B->xcap);
-            B->xvals.alloc(B->xcap);
+            if ((int64_t)used > B->xcap) {
+                B->xcap = 2 * (int64_t)used;
+                B->xnodes.alloc(B->xcap);
+                B->xvals.alloc(B->xcap);
+            }
+            if ((int64_t)rused > B->rcap) {
+                B->rcap = 2 * (int64_t)rused;
+                B->rnodes.alloc(B->rcap);
+                B->rvals.alloc(B->rcap);
+            }
         }
         res->sweeps = B->sweeps.p; res->total_ops = B->ops.p; res->pushes = B->pushes.p;
         res->support = B->support.p; res->converged = B->conv.p; res->x_offset = B->xoff.p;
@@ -1290,6 +1454,47 @@ int gd_batch_round_log(const gd_batch *B, int64_t *out, int64_t cap, int64_t *ro
         *rounds = cnt;
         int64_t k = cnt < cap ? cnt : cap;
         if (k) GD_CUDA(cudaMemcpy(out, B->rlog.p, sizeof(int64_t) * 3 * k, cudaMemcpyDeviceToHost));
+    });
+}
+
+int gd_batch_r_device(const gd_batch *B, int64_t **r_offset, int64_t **r_count, int32_t **r_nodes,
+                      double **r_vals, int64_t *r_total) {
+    if (!B || !r_offset || !r_count || !r_nodes || !r_vals || !r_total) return GD_ERR_ARG;
+    if (!B->want_r()) {
+        set_error("the batch was created without want_r");
+        return GD_ERR_ARG;
+    }
+    *r_offset = B->roff.p;
+    *r_count = B->rcnt.p;
+    *r_nodes = B->rnodes.p;
+    *r_vals = B->rvals.p;
+    *r_total = B->last_r_total;
+    return GD_OK;
+}
+
+int gd_batch_fetch_r_host(gd_batch *B, int64_t n_seeds, int64_t *r_offset, int64_t *r_count,
+                          int32_t *r_nodes, double *r_vals, int64_t r_cap, int64_t *r_total,
+                          void *stream) {
+    return guarded([&] {
+        GD_CHECK_ARG(B && r_total, "null pointer");
+        GD_CHECK_ARG(B->want_r(), "the batch was created without want_r");
+        GD_CUDA(cudaSetDevice(B->G->device));
+        cudaStream_t st = (cudaStream_t)stream;
+        *r_total = B->last_r_total;
+        auto d2h = [&](void *dst, const void *src, size_t bytes) {
+            if (dst && bytes) GD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        d2h(r_offset, B->roff.p, sizeof(int64_t) * n_seeds);
+        d2h(r_count, B->rcnt.p, sizeof(int64_t) * n_seeds);
+        if (B->last_r_total > r_cap) {
+            GD_CUDA(cudaStreamSynchronize(st));
+            set_error("r buffers hold %lld pairs, %lld needed", (long long)r_cap,
+                      (long long)B->last_r_total);
+            throw Error{GD_ERR_CAPACITY};
+        }
+        d2h(r_nodes, B->rnodes.p, sizeof(int32_t) * B->last_r_total);
+        d2h(r_vals, B->rvals.p, sizeof(double) * B->last_r_total);
+        GD_CUDA(cudaStreamSynchronize(st));
     });
 }
 

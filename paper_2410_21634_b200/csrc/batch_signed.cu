@@ -38,6 +38,18 @@
 namespace cg = cooperative_groups;
 
 namespace gd {
+struct RPool {  // (batch.cu)
+    int64_t *off, *cnt;
+    int32_t *nodes;
+    double *vals;
+    int64_t cap;
+    unsigned long long *cursor;
+    unsigned long long *scratch;
+};
+void r_extract_wave(uint32_t *secmap, int64_t smw, double *r, int64_t ld, int64_t m,
+                    const int32_t *inv, int64_t seed_base, unsigned long long *cnt_scratch,
+                    unsigned long long *cursor, int64_t *r_off, int64_t *r_cnt,
+                    int32_t *r_nodes, double *r_vals, int64_t rcap, cudaStream_t st);
 namespace {
 
 constexpr int SBT = 512;
@@ -963,7 +975,7 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
                       int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
-                      cudaStream_t st) {
+                      cudaStream_t st, const RPool *rp) {
     if (S->dirty) {  // a capacity abort left marks / residuals behind
         S->clear_marks(st);
         const size_t sn = (size_t)S->slots * (size_t)S->ld;
@@ -995,9 +1007,14 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
         GD_CUDA(cudaEventRecord(ev[2 * w + 1], st));
         k_s_reserve<<<(int)((m + 255) / 256), 256, 0, st>>>(A, cursor, S->slot_base.p);
         k_s_extract<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A, O, base);
-        const int64_t rc = (S->smw + 2047) / 2048;  // ~2,048 map words per block
-        k_s_reset<<<dim3((unsigned)(rc < SCHUNKS ? SCHUNKS : (rc > 4096 ? 4096 : rc)), (unsigned)m), 256,
-                    0, st>>>(A);
+        if (rp) {  // sparse r out; zeroes the slots' r itself
+            r_extract_wave(A.secmap, A.smw, A.r, A.ld, m, inv, base, rp->scratch, rp->cursor,
+                           rp->off, rp->cnt, rp->nodes, rp->vals, rp->cap, st);
+        } else {
+            const int64_t rc = (S->smw + 2047) / 2048;  // ~2,048 map words per block
+            k_s_reset<<<dim3((unsigned)(rc < SCHUNKS ? SCHUNKS : (rc > 4096 ? 4096 : rc)),
+                             (unsigned)m), 256, 0, st>>>(A);
+        }
         GD_LAUNCH_CHECK();
         nl += 5;
     }

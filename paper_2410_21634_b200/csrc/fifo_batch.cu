@@ -15,6 +15,14 @@
 #include "common.cuh"
 
 namespace gd {
+struct RPool {  // (batch.cu)
+    int64_t *off, *cnt;
+    int32_t *nodes;
+    double *vals;
+    int64_t cap;
+    unsigned long long *cursor;
+    unsigned long long *scratch;
+};
 namespace {
 
 constexpr int FB_THREADS = 256;
@@ -31,6 +39,12 @@ struct FifoBatchArgs {
     int64_t qw;
     int32_t *touched;      // touched list per slot (ld)
     int32_t *plist;        // pushed-node list per slot (ld): x support
+    // optional sparse r out (want_r; r_off null = not wanted)
+    int64_t *r_off, *r_cnt;
+    int32_t *r_nodes;
+    double *r_vals;
+    int64_t rcap;
+    unsigned long long *rcursor;
     const int64_t *seeds;
     unsigned long long *next_seed, *cursor;
     int64_t *sweeps, *ops, *pushes, *xoff, *xcnt;
@@ -217,7 +231,40 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(A.cursor, (unsigned long long)nx);
         base = __shfl_sync(FULL, base, 0);
-        for (int64_t i = lane; i < ntouch; i += 32) r[touched[i]] = 0.0;
+        if (A.r_off) {  // sparse r out over the touched nodes (count, reserve, emit)
+            int64_t nr = 0;
+            for (int64_t i = lane; i < ntouch; i += 32) nr += r[touched[i]] != 0.0;
+            for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(FULL, nr, o);
+            unsigned long long rb = 0;
+            if (lane == 0) rb = atomicAdd(A.rcursor, (unsigned long long)nr);
+            rb = __shfl_sync(FULL, rb, 0);
+            if (lane == 0) {
+                A.r_off[si] = (int64_t)rb;
+                A.r_cnt[si] = nr;
+            }
+            int64_t wr = (int64_t)rb;
+            for (int64_t i0 = 0; i0 < ntouch; i0 += 32) {
+                const int64_t i = i0 + lane;
+                int32_t v = 0;
+                double rv = 0.0;
+                if (i < ntouch) {
+                    v = touched[i];
+                    rv = r[v];
+                    r[v] = 0.0;
+                }
+                const unsigned nzb = __ballot_sync(FULL, rv != 0.0);
+                if (rv != 0.0) {
+                    const int64_t at = wr + __popc(nzb & lanemask_lt());
+                    if (at < A.rcap) {
+                        A.r_nodes[at] = v;
+                        A.r_vals[at] = rv;
+                    }
+                }
+                wr += __popc(nzb);
+            }
+        } else {
+            for (int64_t i = lane; i < ntouch; i += 32) r[touched[i]] = 0.0;
+        }
         if (!conv)
             for (int64_t w = lane; w < A.qw; w += 32) qmark[w] = 0u;
         int64_t w = (int64_t)base;
@@ -303,7 +350,8 @@ int fifo_batch_slots(const FifoBatchState *F) { return F->nslots; }
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
                     int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
-                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st) {
+                    double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st,
+                    const RPool *rp) {
     FifoBatchArgs A{};
     A.g = G->view();
     A.alpha = p.alpha;
@@ -320,6 +368,10 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
     A.touched = F->touched.p; A.plist = F->plist.p; A.seeds = d_seeds; A.next_seed = F->ctr.p; A.cursor = cursor;
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv; A.xoff = xoff;
     A.xcnt = xcnt; A.xnodes = xnodes; A.xvals = xvals; A.nslots = F->nslots;
+    if (rp) {
+        A.r_off = rp->off; A.r_cnt = rp->cnt; A.r_nodes = rp->nodes; A.r_vals = rp->vals;
+        A.rcap = rp->cap; A.rcursor = rp->cursor;
+    }
     GD_CUDA(cudaMemsetAsync(F->ctr.p, 0, sizeof(unsigned long long), st));
     const int64_t warps = F->nslots < n_seeds ? F->nslots : (n_seeds ? n_seeds : 1);
     const int blocks = (int)((warps * 32 + FB_THREADS - 1) / FB_THREADS);

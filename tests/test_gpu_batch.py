@@ -8,6 +8,7 @@ import pytest
 
 from conftest import golden_graph
 from oracle import oracle as O
+from paper_2410_21634_b200 import systems as S
 from paper_2410_21634_b200.batch import BatchSolver, local_gd_batch
 from paper_2410_21634_b200.metrics import sample_sources
 from paper_2410_21634_b200.synth import rmat_graph
@@ -245,3 +246,27 @@ def test_grouped_mode_matches_oracle(gpu, monkeypatch, group):
         assert hk.sweeps[i] == r["sweeps"] and hk.total_ops[i] == r["total_ops"]
         f = r["f_hat"]
         assert np.abs(hk.x_dense(i, g.n) - f).sum() <= X_RTOL * np.abs(f).sum()
+
+
+@pytest.mark.parametrize("method", ["local-gd", "local-ch", "local-sor"])
+def test_batch_sparse_r(gpu, method):
+    """want_r: each seed's final residual as a sparse vector, against the
+    CPU oracle's dense r (bitwise for the FIFO batch, 1e-9 otherwise)."""
+    g = rmat_graph(20000, 150000, seed=6)
+    seeds = sample_sources(g, 12, seed=1)
+    solver = BatchSolver(g, 0.1, 1e-6, slots=5, method=method, want_r=True, max_sweeps=100000)
+    out = solver.solve(seeds)
+    for i, s in enumerate(seeds):
+        sys_ = S.make_ppr_system(g, 0.1, int(s), 1e-6)
+        ref = (O.local_gd(sys_, record_trace=False) if method == "local-gd" else
+               O.local_ch(sys_, record_trace=False) if method == "local-ch" else
+               O.local_sor(sys_, 1.0))
+        r = out.r_dense(i, g.n)
+        nodes, _ = out.r_sparse(i)
+        assert len(np.unique(nodes)) == len(nodes)
+        if method == "local-sor":
+            assert np.array_equal(r, ref["r"])
+        else:
+            assert np.abs(r - ref["r"]).sum() <= 1e-9 * np.abs(ref["r"]).sum() + 1e-300
+            assert set(np.flatnonzero(ref["r"]).tolist()) <= set(nodes.tolist())
+    solver.close()
