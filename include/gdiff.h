@@ -267,6 +267,18 @@ int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */
 int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *rounds);
 
+/* ---- multi-column degree-generalized feature push (new) -------------- */
+/* beta_push (src/dynamic.py:199-222) for every column of a source matrix:
+ * per column a signed FIFO push (_push_kernel) from p = 0, r = source with
+ * per-arc weights arc_w (n_arcs) and thresholds theta (n), x_gain = alpha;
+ * one warp per column, each column bit-identical with beta_push.
+ * source, p_out, r_out: n x ncols host arrays, column-major; the per-column
+ * statistics may be NULL. */
+int gd_feature_push(const gd_graph *g, const double *arc_w, const double *theta, double x_gain,
+                    double omega, int64_t ncols, const double *source, int64_t max_sweeps,
+                    double *p_out, double *r_out, int64_t *sweeps, int64_t *total_ops,
+                    int64_t *pushes, int32_t *converged);
+
 /* ---- resident PPR pairs on an evolving graph (config 5, batched) ------- */
 /* K pairs (p_i, r_i) with r_i = alpha e_{s_i} - (I - (1-alpha) A D^-1) p_i
  * kept in HBM across snapshots.  Replaces, for K sources at once, the

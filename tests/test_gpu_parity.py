@@ -263,3 +263,24 @@ def test_beta_push_matches_reference(gpu, glob, beta):
     assert np.array_equal(pair.p, glob[f"{k}/p"]) and np.array_equal(pair.r, glob[f"{k}/r"])
     assert rep.sweeps == glob[f"{k}/sweeps"] and rep.total_ops == glob[f"{k}/total_ops"]
     assert rep.notes["parked_mass"] == glob[f"{k}/parked"]
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0])
+def test_beta_push_batch_columns_bitwise(gpu, glob, beta):
+    """Multi-column feature push: every column equals beta_push on it."""
+    from paper_2410_21634_b200.dynamic import beta_push, beta_push_batch
+    from paper_2410_21634_b200.synth import rmat_graph
+    for g in (golden_graph(glob, "er500"), rmat_graph(5000, 30000, seed=3)):
+        rng = np.random.default_rng(int(beta * 10) + g.n)
+        src = rng.standard_normal((g.n, 7)) * (rng.random((g.n, 7)) < 0.03)
+        out = beta_push_batch(g, src, 0.15, beta, 1e-4, omega=1.2)
+        for c in range(src.shape[1]):
+            pair, rep = beta_push(g, src[:, c], 0.15, beta, 1e-4, omega=1.2)
+            assert np.array_equal(out["p"][:, c], pair.p) and np.array_equal(out["r"][:, c], pair.r)
+            assert out["sweeps"][c] == rep.sweeps and out["total_ops"][c] == rep.total_ops
+            assert out["parked_mass"][c] == rep.notes["parked_mass"]
+    # the reference's golden column
+    g = golden_graph(glob, "er500")
+    out = beta_push_batch(g, glob["betapush/source"], 0.15, beta, 1e-4)
+    k = f"er500/betapush{beta}"
+    assert np.array_equal(out["p"][:, 0], glob[f"{k}/p"]) and np.array_equal(out["r"][:, 0], glob[f"{k}/r"])
