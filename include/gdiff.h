@@ -272,7 +272,7 @@ int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *ro
  * per column a signed FIFO push (_push_kernel) from p = 0, r = source with
  * per-arc weights arc_w (n_arcs) and thresholds theta (n), x_gain = alpha;
  * one warp per column, each column bit-identical with beta_push.
- * source, p_out, r_out: n x ncols host arrays, column-major; the per-column
+ * source, p_out, r_out: n x ncols host arrays, row-major; the per-column
  * statistics may be NULL. */
 int gd_feature_push(const gd_graph *g, const double *arc_w, const double *theta, double x_gain,
                     double omega, int64_t ncols, const double *source, int64_t max_sweeps,

@@ -32,7 +32,8 @@ def _deps_newer(obj: str, src: str) -> bool:
     if not os.path.exists(obj):
         return True
     t = os.path.getmtime(obj)
-    dep = [src, os.path.join(CSRC, "common.cuh"), os.path.join(INCLUDE, "gdiff.h")]
+    dep = [src, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "window.cuh"),
+           os.path.join(INCLUDE, "gdiff.h")]
     return any(os.path.getmtime(d) > t for d in dep)
 
 

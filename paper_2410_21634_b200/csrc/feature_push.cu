@@ -10,6 +10,7 @@
 // Per column the pops, the enqueue order and every fl() step are the
 // reference's, so each column is bit-identical with beta_push on it.
 #include "common.cuh"
+#include "window.cuh"
 
 namespace gd {
 namespace {
@@ -154,12 +155,113 @@ __global__ void __launch_bounds__(FP_THREADS) k_feature_push(FpArgs A) {
     }
 }
 
+// The same column solves in exact windows (window.cuh): one CTA per column at
+// a time, persistent over the columns.
+struct FwArgs {
+    DevGraph g;
+    DevOp op;
+    double x_gain, omega;
+    int64_t n, ncols, max_sweeps;
+    double *p, *r;
+    int32_t *queue;   // per CTA: n + 2
+    uint32_t *qmark;  // per CTA: qw words
+    int64_t qw;
+    unsigned long long *next_col;
+    int64_t *sweeps, *ops, *pushes;
+    int32_t *conv;
+};
+
+__global__ void __launch_bounds__(win::WT, 1) k_feature_win(FwArgs A) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    win::Smem &S = *reinterpret_cast<win::Smem *>(smraw);
+    __shared__ long long sh_col;
+    __shared__ int64_t sh_sweeps, sh_ops;
+    __shared__ int sh_done, sh_conv;
+    win::init_smem(S);
+    const int64_t qcap = A.n + 2;
+    win::Sys Y{A.g, A.op, nullptr, nullptr, A.queue + (int64_t)blockIdx.x * qcap,
+               A.qmark + (int64_t)blockIdx.x * A.qw, qcap, A.omega, A.x_gain, 1, 0};
+    for (;;) {
+        if (threadIdx.x == 0) sh_col = (long long)atomicAdd(A.next_col, 1ULL);
+        __syncthreads();
+        const int64_t ci = sh_col;
+        if (ci >= A.ncols) break;
+        Y.x = A.p + ci * A.n;
+        Y.r = A.r + ci * A.n;
+        // seeds = flatnonzero(|r| >= theta), enqueued in order (dynamic.py:141)
+        const int64_t cnt = win::scan_enqueue(Y, S, A.n);
+        if (threadIdx.x == 0) {
+            S.front = 0;
+            S.svol = S.pushes = 0;
+            sh_sweeps = sh_ops = 0;
+            sh_conv = 1;
+            sh_done = cnt == 0;
+            S.sentpos = cnt;
+            S.rear = cnt + 1;
+        }
+        __syncthreads();
+        while (!sh_done) {
+            win::run_sweep(Y, S);
+            if (threadIdx.x == 0) {
+                sh_ops += S.svol;
+                sh_sweeps += 1;
+                S.front = S.sentpos + 1 == qcap ? 0 : S.sentpos + 1;
+                if (S.front == S.rear) {
+                    sh_done = 1;
+                } else if (sh_sweeps >= A.max_sweeps) {
+                    sh_conv = 0;
+                    sh_done = 1;
+                } else {
+                    S.sentpos = S.rear;
+                    S.rear = S.rear + 1 == qcap ? 0 : S.rear + 1;
+                    S.svol = 0;
+                }
+            }
+            __syncthreads();
+        }
+        if (!sh_conv)  // marks of the nodes still queued
+            for (int64_t w = threadIdx.x; w < A.qw; w += win::WT) Y.qmark[w] = 0u;
+        if (threadIdx.x == 0) {
+            A.sweeps[ci] = sh_sweeps;
+            A.ops[ci] = sh_ops;
+            A.pushes[ci] = S.pushes;
+            A.conv[ci] = sh_conv;
+        }
+        __syncthreads();
+    }
+}
+
+// out (cols x rows) = in (rows x cols)^T, 32 x 32 tiles through shared memory.
+__global__ void k_transpose(const double *__restrict__ in, double *__restrict__ out, int64_t rows,
+                            int64_t cols) {
+    __shared__ double tile[32][33];
+    const int64_t tr = (rows + 31) / 32;  // tiles flattened into grid.x
+    const int64_t r0 = ((int64_t)blockIdx.x % tr) * 32, c0 = ((int64_t)blockIdx.x / tr) * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t rr = r0 + i, cc = c0 + threadIdx.x;
+        if (rr < rows && cc < cols) tile[i][threadIdx.x] = in[rr * cols + cc];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t cc = c0 + i, rr = r0 + threadIdx.x;
+        if (rr < rows && cc < cols) out[cc * rows + rr] = tile[threadIdx.x][i];
+    }
+}
+
+void transpose(const double *in, double *out, int64_t rows, int64_t cols) {
+    const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+    k_transpose<<<(unsigned)tiles, dim3(32, 8)>>>(in, out, rows, cols);
+    GD_LAUNCH_CHECK();
+}
+
 }  // namespace
 }  // namespace gd
 
 using namespace gd;
 
-// Columns c = 0..ncols-1 of the host source matrix (n x ncols, column-major)
+// Columns c = 0..ncols-1 of the host source matrix (n x ncols, row-major: the
+// feature-matrix layout; transposed on the device so each column is
+// contiguous while it is pushed)
 // are pushed independently; p and r come back in the same layout.  arc_w /
 // theta: the operator of beta_push (per arc / per node, host arrays).
 extern "C" int gd_feature_push(const gd_graph *G, const double *arc_w, const double *theta,
@@ -177,49 +279,101 @@ extern "C" int gd_feature_push(const gd_graph *G, const double *arc_w, const dou
         DBuf<double> aw(G->n_arcs ? G->n_arcs : 1), th(n), p(nc), r(nc);
         GD_CUDA(cudaMemcpy(aw.p, arc_w, sizeof(double) * G->n_arcs, cudaMemcpyHostToDevice));
         GD_CUDA(cudaMemcpy(th.p, theta, sizeof(double) * n, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(r.p, source, sizeof(double) * nc, cudaMemcpyHostToDevice));
+        {
+            DBuf<double> rowm(nc);
+            GD_CUDA(cudaMemcpy(rowm.p, source, sizeof(double) * nc, cudaMemcpyHostToDevice));
+            transpose(rowm.p, r.p, n, ncols);  // (n x C) -> (C x n)
+        }
         GD_CUDA(cudaMemset(p.p, 0, sizeof(double) * nc));
-        // warps: one per column, capped by the resident warp count and memory
         size_t fr = 0, tot = 0;
         GD_CUDA(cudaMemGetInfo(&fr, &tot));
         const int64_t qw = n / 32 + 1;
         const int64_t per = 4 * (n + 2) + 4 * qw;
-        int64_t nw = ncols;
-        const int64_t resident = (int64_t)n_sms(G->device) * 64;
-        if (nw > resident) nw = resident;
-        if (nw > (int64_t)(fr / 4) / per) nw = (int64_t)(fr / 4) / per;
-        if (nw < 1) nw = 1;
-        DBuf<int32_t> queue((size_t)nw * (n + 2));
-        DBuf<uint32_t> qmark((size_t)nw * qw);
-        GD_CUDA(cudaMemset(qmark.p, 0, sizeof(uint32_t) * (size_t)nw * qw));
         DBuf<int64_t> d_sw(ncols), d_ops(ncols), d_pu(ncols);
         DBuf<int32_t> d_cv(ncols);
         DBuf<unsigned long long> ctr(1);
         GD_CUDA(cudaMemset(ctr.p, 0, sizeof(unsigned long long)));
-        FpArgs A{};
-        A.g = G->view();
-        A.arc_w = aw.p;
-        A.theta = th.p;
-        A.x_gain = x_gain;
-        A.omega = omega;
-        A.n = n;
-        A.ncols = ncols;
-        A.max_sweeps = max_sweeps > 0 ? max_sweeps : 1000000;
-        A.p = p.p;
-        A.r = r.p;
-        A.queue = queue.p;
-        A.qmark = qmark.p;
-        A.qw = qw;
-        A.nwarps = (int)nw;
-        A.next_col = ctr.p;
-        A.sweeps = d_sw.p;
-        A.ops = d_ops.p;
-        A.pushes = d_pu.p;
-        A.conv = d_cv.p;
-        k_feature_push<<<(int)((nw * 32 + FP_THREADS - 1) / FP_THREADS), FP_THREADS>>>(A);
-        GD_LAUNCH_CHECK();
-        GD_CUDA(cudaMemcpy(p_out, p.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
-        GD_CUDA(cudaMemcpy(r_out, r.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+        static const bool warp_chain = [] {
+            const char *e = getenv("GDIFF_FIFO");
+            return e && e[0] == 'w';
+        }();
+        if (!warp_chain) {  // one CTA per column at a time
+            int64_t nb = ncols < n_sms(G->device) ? ncols : n_sms(G->device);
+            if (nb > (int64_t)(fr / 4) / per) nb = (int64_t)(fr / 4) / per;
+            if (nb < 1) nb = 1;
+            DBuf<int32_t> queue((size_t)nb * (n + 2));
+            DBuf<uint32_t> qmark((size_t)nb * qw);
+            GD_CUDA(cudaMemset(qmark.p, 0, sizeof(uint32_t) * (size_t)nb * qw));
+            FwArgs A{};
+            A.g = G->view();
+            A.op.wrule = GD_W_ARC;
+            A.op.trule = GD_T_ARRAY;
+            A.op.arc_w = aw.p;
+            A.op.theta = th.p;
+            A.x_gain = x_gain;
+            A.omega = omega;
+            A.n = n;
+            A.ncols = ncols;
+            A.max_sweeps = max_sweeps > 0 ? max_sweeps : 1000000;
+            A.p = p.p;
+            A.r = r.p;
+            A.queue = queue.p;
+            A.qmark = qmark.p;
+            A.qw = qw;
+            A.next_col = ctr.p;
+            A.sweeps = d_sw.p;
+            A.ops = d_ops.p;
+            A.pushes = d_pu.p;
+            A.conv = d_cv.p;
+            static bool attr = false;
+            if (!attr) {
+                GD_CUDA(cudaFuncSetAttribute(k_feature_win, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(win::Smem)));
+                attr = true;
+            }
+            k_feature_win<<<(int)nb, win::WT, sizeof(win::Smem)>>>(A);
+            GD_LAUNCH_CHECK();
+            GD_CUDA(cudaDeviceSynchronize());
+        } else {  // one warp per column
+            int64_t nw = ncols;
+            const int64_t resident = (int64_t)n_sms(G->device) * 64;
+            if (nw > resident) nw = resident;
+            if (nw > (int64_t)(fr / 4) / per) nw = (int64_t)(fr / 4) / per;
+            if (nw < 1) nw = 1;
+            DBuf<int32_t> queue((size_t)nw * (n + 2));
+            DBuf<uint32_t> qmark((size_t)nw * qw);
+            GD_CUDA(cudaMemset(qmark.p, 0, sizeof(uint32_t) * (size_t)nw * qw));
+            FpArgs A{};
+            A.g = G->view();
+            A.arc_w = aw.p;
+            A.theta = th.p;
+            A.x_gain = x_gain;
+            A.omega = omega;
+            A.n = n;
+            A.ncols = ncols;
+            A.max_sweeps = max_sweeps > 0 ? max_sweeps : 1000000;
+            A.p = p.p;
+            A.r = r.p;
+            A.queue = queue.p;
+            A.qmark = qmark.p;
+            A.qw = qw;
+            A.nwarps = (int)nw;
+            A.next_col = ctr.p;
+            A.sweeps = d_sw.p;
+            A.ops = d_ops.p;
+            A.pushes = d_pu.p;
+            A.conv = d_cv.p;
+            k_feature_push<<<(int)((nw * 32 + FP_THREADS - 1) / FP_THREADS), FP_THREADS>>>(A);
+            GD_LAUNCH_CHECK();
+            GD_CUDA(cudaDeviceSynchronize());
+        }
+        {
+            DBuf<double> rowm(nc);
+            transpose(p.p, rowm.p, ncols, n);
+            GD_CUDA(cudaMemcpy(p_out, rowm.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+            transpose(r.p, rowm.p, ncols, n);
+            GD_CUDA(cudaMemcpy(r_out, rowm.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+        }
         if (sweeps) GD_CUDA(cudaMemcpy(sweeps, d_sw.p, 8 * ncols, cudaMemcpyDeviceToHost));
         if (total_ops) GD_CUDA(cudaMemcpy(total_ops, d_ops.p, 8 * ncols, cudaMemcpyDeviceToHost));
         if (pushes) GD_CUDA(cudaMemcpy(pushes, d_pu.p, 8 * ncols, cudaMemcpyDeviceToHost));

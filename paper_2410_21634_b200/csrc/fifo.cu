@@ -14,6 +14,7 @@
 #include <memory>
 
 #include "common.cuh"
+#include "window.cuh"
 
 namespace gd {
 namespace {
@@ -270,6 +271,104 @@ __global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo(FifoArgs A) {
     }
 }
 
+// The same solve with the pops taken in exact windows (window.cuh): one CTA,
+// the sentinel / log handling of k_fifo around win::run_sweep.
+__global__ void __launch_bounds__(FIFO_THREADS, 1) k_fifo_win(FifoArgs A) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    win::Smem &S = *reinterpret_cast<win::Smem *>(smraw);
+    __shared__ double s_s[32], s_m[32];
+    __shared__ double sh_l1, sh_min;
+    __shared__ int64_t sh_sweeps, sh_ops;
+    __shared__ int sh_cmd, sh_conv;
+    static_assert(win::WT == FIFO_THREADS, "one CTA shape");
+    const win::Sys Y{A.g, A.op, A.x, A.r, A.queue, A.qmark, A.dim + 2, A.omega, A.x_gain, A.sgn, 1};
+    win::init_smem(S);
+    if (threadIdx.x == 0) {  // seed enqueue, sequential (:59-69)
+        int64_t rear = 0;
+        for (int64_t i = 0; i < A.n_seeds; i++) {
+            int32_t u = A.seeds[i];
+            bool act = is_active(A.r[u], theta_of(A.op, u, A.g.deg[u]), A.sgn);
+            if (act && !qm_test(A.qmark, u)) {
+                A.queue[rear] = u;
+                rear = rear + 1;
+                A.qmark[u >> 5] |= 1u << (u & 31);
+            }
+        }
+        S.front = 0;
+        S.rear = rear;
+        S.svol = S.pushes = 0;
+        S.sgamma = 0.0;
+        S.pos = S.neg = 0;
+        sh_sweeps = sh_ops = 0;
+        sh_conv = 1;
+    }
+    __syncthreads();
+    double l1, mn;
+    block_l1_min(A, s_s, s_m, l1, mn);
+    if (threadIdx.x == 0) {
+        sh_l1 = l1;
+        sh_min = mn;
+        A.l1_log[0] = l1;
+        sh_cmd = (S.front == S.rear) ? 2 : 0;
+        if (sh_cmd == 0) {
+            S.sentpos = S.rear;
+            S.rear = S.rear + 1;
+        }
+    }
+    __syncthreads();
+    const int64_t qcap = A.dim + 2;
+    while (sh_cmd != 2) {
+        win::run_sweep(Y, S);
+        if (threadIdx.x == 0) {  // the sentinel: close the sweep (:102-126)
+            const int64_t t = sh_sweeps;
+            if (t < A.log_cap) {
+                A.vol_log[t] = S.svol;
+                A.gamma_log[t] = sh_l1 > 0.0 ? S.sgamma / sh_l1 : 0.0;
+                A.sign_log[t] = (S.pos && S.neg) ? 2 : S.pos ? 1 : S.neg ? -1 : 0;
+            }
+            sh_ops += S.svol;
+            sh_sweeps = t + 1;
+            S.front = S.sentpos + 1 == qcap ? 0 : S.sentpos + 1;
+        }
+        __syncthreads();
+        block_l1_min(A, s_s, s_m, l1, mn);
+        if (threadIdx.x == 0) {
+            const int64_t t = sh_sweeps;
+            if (t < A.log_cap) A.l1_log[t] = l1;
+            sh_l1 = l1;
+            if (mn < sh_min) sh_min = mn;
+            if (S.front == S.rear) {
+                sh_cmd = 2;
+            } else if (t >= A.max_sweeps) {
+                sh_conv = 0;
+                sh_cmd = 2;
+            } else {
+                S.sentpos = S.rear;
+                S.rear = S.rear + 1 == qcap ? 0 : S.rear + 1;
+                S.svol = 0;
+                S.sgamma = 0.0;
+                S.pos = S.neg = 0;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        A.out[0] = sh_sweeps;
+        A.out[1] = sh_ops;
+        A.out[2] = sh_conv;
+        A.out[3] = S.pushes;
+        A.out_min[0] = sh_min;
+#ifdef GD_WIN_PROF
+        printf("wprof windows=%llu", win::g_wprof[31]);
+        for (int i = 0; i < 12; i++) printf(" p%d=%.1fus", i, win::g_wprof[i] / 1.9e3);
+        printf("\n  windows=%llu pops/win=%.1f conflict=%llu arcbudget=%llu slice/win=%.1f arcs/win=%.1f sweepend=%llu big=%llu\n",
+               win::g_wprof[20], (double)win::g_wprof[21] / win::g_wprof[20], win::g_wprof[22], win::g_wprof[23],
+               (double)win::g_wprof[24] / win::g_wprof[20], (double)win::g_wprof[25] / win::g_wprof[20], win::g_wprof[26], win::g_wprof[27]);
+        for (int i = 0; i < 32; i++) win::g_wprof[i] = 0;
+#endif
+    }
+}
+
 // Device buffers of a FIFO solve, kept across calls on the host thread.
 struct FifoWS {
     DBuf<double> x, r, gam, l1, mn;
@@ -309,7 +408,21 @@ void run_fifo(const gd_graph *G, FifoArgs A, double *hx, double *hr,
     A.x = x.p; A.r = r.p; A.queue = queue.p; A.qmark = qmark.p; A.seeds = sd.p;
     A.n_seeds = n_seeds; A.log_cap = log_cap; A.vol_log = vol.p; A.gamma_log = gam.p;
     A.l1_log = l1.p; A.sign_log = sgn.p; A.out = out.p; A.out_min = mn.p;
-    k_fifo<<<1, FIFO_THREADS>>>(A);
+    static const bool warp_chain = [] {
+        const char *e = getenv("GDIFF_FIFO");
+        return e && e[0] == 'w';
+    }();
+    if (warp_chain) {
+        k_fifo<<<1, FIFO_THREADS>>>(A);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            GD_CUDA(cudaFuncSetAttribute(k_fifo_win, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(win::Smem)));
+            attr = true;
+        }
+        k_fifo_win<<<1, FIFO_THREADS, sizeof(win::Smem)>>>(A);
+    }
     GD_LAUNCH_CHECK();
     GD_CUDA(cudaDeviceSynchronize());
     int64_t o[4];
