@@ -75,7 +75,7 @@ struct Smem {
     uint32_t keypre[KW];
     double pr[WMAX], pth[WMAX], px[WMAX], pw[WMAX];
     int64_t prow[WMAX];
-    int32_t pu[WMAX], pdeg[WMAX], pre[WMAX + 1];
+    int32_t pu[WMAX], pdeg[WMAX], pre[WMAX + 1], cpre[WMAX + 1];
     uint8_t pact[WMAX];
     int32_t wsum[WT / 32];
     int64_t front, rear, sentpos, svol, pushes;
@@ -152,6 +152,15 @@ __device__ __forceinline__ void pop_stats(const Sys &Y, Smem &S, int j) {
     }
 }
 
+// Thread 0: the next window's slice length and fresh per-window counters.
+__device__ __forceinline__ void next_window(const Sys &Y, Smem &S) {
+    const int64_t av = S.sentpos >= S.front ? S.sentpos - S.front : S.sentpos + Y.qcap - S.front;
+    S.nslice = av < WMAX ? (int)av : WMAX;
+    S.cut = WMAX;
+    S.nslots = 0;
+    S.alloc = 0;
+}
+
 // Slice entry 0 is active and its row exceeds ACAP: a window of one pop,
 // its arcs in CTA-wide chunks, enqueue order by a CTA prefix over the chunk.
 __device__ void big_pop(const Sys &Y, Smem &S) {
@@ -161,6 +170,7 @@ __device__ void big_pop(const Sys &Y, Smem &S) {
     const double res = __dmul_rn(Y.omega, ru);
     const int32_t d = S.pdeg[0];
     const int64_t rs = S.prow[0];
+    const int nslots = S.nslots;  // (thread 0 resets it at the end)
     if (t == 0) {
         atomicAnd(Y.qmark + (u >> 5), ~(1u << (u & 31)));
         Y.r[u] = __dsub_rn(ru, res);
@@ -203,7 +213,6 @@ __device__ void big_pop(const Sys &Y, Smem &S) {
         if (rear >= Y.qcap) rear -= Y.qcap;
         __syncthreads();
     }
-    const int nslots = S.nslots;
     for (int s = t; s < nslots; s += WT) {
         const int h = S.slot_h[s];
         S.hk[h] = -1;
@@ -218,33 +227,74 @@ __device__ void big_pop(const Sys &Y, Smem &S) {
         }
         S.rear = rear;
         S.front = S.front + 1 == Y.qcap ? 0 : S.front + 1;
+        next_window(Y, S);
     }
     __syncthreads();
+}
+
+// Warp-redundant prefix over the slice: lane l holds entries 4l..4l+3 (arcs
+// of active pops, capped at ACAP + 1, and active-pop counts).  Returns jlim,
+// the first pop whose arcs overflow the budget (or nslice).
+__device__ __forceinline__ int slice_prefix(const Smem &S, int nslice, int lane, int (&pa)[4],
+                                            int (&pc)[4], int &ta, int &tc) {
+    int la[4], lc[4], sa = 0, sc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int i = lane * 4 + q;
+        const bool act = i < nslice && S.pact[i];
+        const int l = act ? S.pdeg[i] : 0;
+        la[q] = l > ACAP ? ACAP + 1 : l;
+        lc[q] = act ? 1 : 0;
+        sa += la[q];
+        sc += lc[q];
+    }
+    int ia = sa, ic = sc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(FULL, ia, o), yc = __shfl_up_sync(FULL, ic, o);
+        if (lane >= o) {
+            ia += ya;
+            ic += yc;
+        }
+    }
+    ta = __shfl_sync(FULL, ia, 31);
+    tc = __shfl_sync(FULL, ic, 31);
+    int ea = ia - sa, ec = ic - sc, first = WMAX;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int i = lane * 4 + q;
+        pa[q] = ea;
+        pc[q] = ec;
+        if (i < nslice && ea + la[q] > ACAP && first == WMAX) first = i;
+        ea += la[q];
+        ec += lc[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int y = __shfl_xor_sync(FULL, first, o);
+        first = y < first ? y : first;
+    }
+    return first < nslice ? first : nslice;
 }
 
 // Pops every queue entry before the sweep's sentinel (S.sentpos), in windows.
 // Entry: S.front / S.rear / S.sentpos set and visible to the CTA.
 __device__ void run_sweep(const Sys &Y, Smem &S) {
+    static_assert(WMAX == 128, "slice_prefix holds 4 entries per lane");
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int wbase = t & ~31;
 #ifdef GD_WIN_PROF
     long long wlast = clock64();
     if (t == 0) g_wprof[31] += 1;
 #endif
+    if (t == 0) next_window(Y, S);
+    __syncthreads();
     for (;;) {
-        if (t == 0) {
-            const int64_t av = S.sentpos >= S.front ? S.sentpos - S.front
-                                                    : S.sentpos + Y.qcap - S.front;
-            S.nslice = av < WMAX ? (int)av : WMAX;
-            S.cut = WMAX;
-            S.nslots = 0;
-            S.alloc = 0;
-        }
-        if (t < KW) S.keybits[t] = 0u;
-        __syncthreads();
         WPROF(0);
         const int nslice = S.nslice;
         if (nslice == 0) break;
         // ---- slice: the entries and their state at window start
+        if (t < KW) S.keybits[t] = 0u;
         if (t < WMAX) {  // whole warps (slot_alloc)
             bool isnew = false;
             int h = 0;
@@ -273,57 +323,45 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
         }
         __syncthreads();
         WPROF(1);
-        // ---- arc prefix over the active pops; the arc budget bounds the window
-        if (wid == 0) {
-            int len[WMAX / 32], s = 0;
-#pragma unroll
-            for (int q = 0; q < WMAX / 32; q++) {
-                const int i = lane * (WMAX / 32) + q;
-                int l = (i < nslice && S.pact[i]) ? S.pdeg[i] : 0;
-                len[q] = l > ACAP ? ACAP + 1 : l;
-                s += len[q];
-            }
-            int inc = s;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULL, inc, o);
-                if (lane >= o) inc += y;
-            }
-            int ex = inc - s, first = WMAX;
-#pragma unroll
-            for (int q = 0; q < WMAX / 32; q++) {
-                const int i = lane * (WMAX / 32) + q;
-                S.pre[i] = ex;
-                if (i < nslice && ex + len[q] > ACAP && first == WMAX) first = i;
-                ex += len[q];
-            }
-            if (lane == 31) S.pre[WMAX] = inc;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const int y = __shfl_xor_sync(FULL, first, o);
-                first = y < first ? y : first;
-            }
-            if (lane == 0) S.jlim = first < nslice ? first : nslice;
-        }
-        __syncthreads();
-        WPROF(2);
-        const int jlim = S.jlim;
+        // ---- arc prefix (every warp computes it); the arc budget bounds the
+        //      window; record -> pop map, warp w filling pops w, w+32, ...
+        int pa[4], pc[4], ta, tc;
+        const int jlim = slice_prefix(S, nslice, lane, pa, pc, ta, tc);
         if (jlim == 0) {
-#ifdef GD_WIN_PROF
-            if (t == 0) g_wprof[27] += 1;
-#endif
             big_pop(Y, S);
             continue;
         }
-        // ---- record -> pop map: warp w fills the arc ranges of pops w, w+32, ..
-        const int narcs = S.pre[jlim];
-        for (int j = wid; j < jlim; j += WT / 32) {
-            const int e = S.pre[j + 1];
-            for (int k = S.pre[j] + lane; k < e; k += 32) S.rec_j[k] = (uint8_t)j;
+        if (wid == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                S.pre[lane * 4 + q] = pa[q];
+                S.cpre[lane * 4 + q] = pc[q];
+            }
+            if (lane == 0) {
+                S.pre[WMAX] = ta;
+                S.cpre[WMAX] = tc;
+            }
         }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; q4++) {  // pops j = wid + 32 q4; lane j / 4 holds pre[j]
+            const int j = wid + 32 * q4, j1 = j + 1;
+            int b = 0, e = ta;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int v = __shfl_sync(FULL, pa[q], j >> 2);
+                const int v1 = __shfl_sync(FULL, pa[q], (j1 >> 2) & 31);
+                if (q == (j & 3)) b = v;
+                if (j1 < WMAX && q == (j1 & 3)) e = v1;
+            }
+            if (j < jlim)
+                for (int k = b + lane; k < e; k += 32) S.rec_j[k] = (uint8_t)j;
+        }
+        const int64_t rear = S.rear;  // (thread 0 moves it in the last phase)
         __syncthreads();
+        WPROF(2);
         // ---- records: every arc of the pops before jlim; a pop is cut when
         //      an earlier active pop pushes to it
+        const int narcs = S.pre[jlim];
         int32_t rv[RPT];
         double rw[RPT];
         int rh[RPT], rj[RPT];
@@ -342,6 +380,7 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
         }
 #pragma unroll
         for (int q = 0; q < RPT; q++) {
+            if (wbase + q * WT >= narcs) break;
             bool isnew = false;
             int h = 0;
             if (rj[q] >= 0) {
@@ -364,7 +403,6 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
             g_wprof[23] += jlim < nslice && S.cut >= jlim;  // arc budget
             g_wprof[24] += nslice;
             g_wprof[25] += nvalid;
-            g_wprof[26] += nslice < WMAX && S.cut >= jlim && jlim == nslice;  // sweep end
         }
 #endif
         const int nslots = S.nslots;
@@ -384,7 +422,7 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
 #pragma unroll
         for (int q = 0; q < SPT; q++) {
             const int s = t + q * WT;
-            sinfo[q] = 0;
+            sinfo[q] = 0xff << 8;
             if (s >= nslots) continue;
             const int32_t v = S.slot_node[s];
             const int hp = S.hpos[S.slot_h[s]];
@@ -403,44 +441,18 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
                 sinfo[q] = 1 | (hp << 8);
             }
         }
-        if (wid == WT / 32 - 1) {  // sweep volume / pushes; the ordered |r| sum of the logs
-            int64_t vol = 0;
-            int np = 0;
-            for (int j = lane; j < cut; j += 32)
-                if (S.pact[j]) {
-                    vol += S.pdeg[j];
-                    np += 1;
-                }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                vol += __shfl_xor_sync(FULL, vol, o);
-                np += __shfl_xor_sync(FULL, np, o);
-            }
-            if (lane == 0) {
-                S.svol += vol;
-                S.pushes += np;
-                if (Y.stats) {
-                    double g = S.sgamma;
-                    int pos = S.pos, neg = S.neg;
-                    for (int j = 0; j < cut; j++) {
-                        if (!S.pact[j]) continue;
-                        const double ru = S.pr[j];
-                        g = __dadd_rn(g, fabs(ru));
-                        pos |= ru > 0.0;
-                        neg |= ru < 0.0;
-                    }
-                    S.sgamma = g;
-                    S.pos = pos;
-                    S.neg = neg;
-                }
-            }
-        }
         __syncthreads();
         WPROF(4);
         // ---- per-node record ranges (warp-aggregated allocation)
         int scnt[SPT], sbase[SPT];
 #pragma unroll
         for (int q = 0; q < SPT; q++) {
+            scnt[q] = 0;
+            sbase[q] = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < SPT; q++) {
+            if (wbase + q * WT >= nslots) break;
             const int s = t + q * WT;
             int c = 0;
             if (s < nslots) {
@@ -527,46 +539,51 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
                 atomicOr(Y.qmark + (v >> 5), 1u << (v & 31));
             }
         }
-        if (t < cut && S.pact[t])
-            Y.x[S.pu[t]] = __dadd_rn(S.px[t], __dmul_rn(Y.gain, __dmul_rn(Y.omega, S.pr[t])));
+        if (t < cut && S.pact[t]) {
+            const double ru = S.pr[t];
+            Y.x[S.pu[t]] = __dadd_rn(S.px[t], __dmul_rn(Y.gain, __dmul_rn(Y.omega, ru)));
+            if (Y.stats) {
+                if (ru > 0.0) S.pos = 1;
+                else if (ru < 0.0) S.neg = 1;
+            }
+        }
+        if (Y.stats && t == WT - 1) {  // the logs' ordered sum of |r| over the pushes
+            double g = S.sgamma;
+            for (int j = 0; j < cut; j++) g = __dadd_rn(g, S.pact[j] ? fabs(S.pr[j]) : 0.0);
+            S.sgamma = g;
+        }
         __syncthreads();
         WPROF(7);
-        // ---- queue slots of the new entries: prefix over the key bitmap
+        // ---- queue slots of the new entries: every warp scans the key bitmap
+        //      (lane l holds words l, l + 32, ...; warp w places words w + 32 i)
         const int nkeys = nvalid + cut;
         const int nkw = (nkeys + 31) >> 5;
-        if (wid == 0) {
-            constexpr int PER = (KW + 31) / 32;
-            int c[PER], s = 0;
+        constexpr int PER = (KW + 31) / 32;
+        int kpre[PER];
+        int run = 0;
 #pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const int w2 = lane * PER + q;
-                c[q] = w2 < nkw ? __popc(S.keybits[w2]) : 0;
-                s += c[q];
-            }
-            int inc = s;
+        for (int q = 0; q < PER; q++) {
+            const int w2 = q * 32 + lane;
+            const int c = w2 < nkw ? __popc(S.keybits[w2]) : 0;
+            int inc = c;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(FULL, inc, o);
                 if (lane >= o) inc += y;
             }
-            int ex = inc - s;
-#pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const int w2 = lane * PER + q;
-                if (w2 < KW) S.keypre[w2] = ex;
-                ex += c[q];
-            }
-            if (lane == 31) S.nenq = inc;
+            kpre[q] = run + inc - c;
+            run += __shfl_sync(FULL, inc, 31);
         }
-        __syncthreads();
-        WPROF(8);
-        const int64_t rear = S.rear;
-        for (int key = t; key < nkeys; key += WT) {
-            const uint32_t bits = S.keybits[key >> 5];
-            if (!((bits >> (key & 31)) & 1u)) continue;
-            int64_t p = rear + S.keypre[key >> 5] + __popc(bits & ((1u << (key & 31)) - 1u));
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const int w2 = q * 32 + wid;  // this warp's word in block q
+            const int wpre = __shfl_sync(FULL, kpre[q], wid);
+            if (w2 >= nkw) continue;
+            const uint32_t bits = S.keybits[w2];
+            if (!((bits >> lane) & 1u)) continue;
+            int64_t p = rear + wpre + __popc(bits & lanemask_lt());
             if (p >= Y.qcap) p -= Y.qcap;
-            Y.queue[p] = S.keynode[key];
+            Y.queue[p] = S.keynode[w2 * 32 + lane];
         }
         for (int s = t; s < nslots; s += WT) {
             const int h = S.slot_h[s];
@@ -575,17 +592,18 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
 #pragma unroll
             for (int w2 = 0; w2 < MW; w2++) S.mask[s][w2] = 0u;
         }
-        __syncthreads();
-        WPROF(9);
         if (t == 0) {
-            int64_t r2 = rear + S.nenq;
+            int64_t r2 = rear + run;
             if (r2 >= Y.qcap) r2 -= Y.qcap;
             S.rear = r2;
             int64_t f2 = S.front + cut;
             if (f2 >= Y.qcap) f2 -= Y.qcap;
             S.front = f2;
+            S.svol += nvalid;
+            S.pushes += S.cpre[cut];
+            next_window(Y, S);
         }
-        // (the next iteration's first barrier publishes front / rear)
+        __syncthreads();
     }
 }
 
