@@ -97,6 +97,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            # nvidia-smi's start-up (process + NVML init) stalls the driver for
+            # tens of ms: let it finish before the timed region opens, sampling
+            # then continues every 100 ms inside it
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
         return self
@@ -361,14 +367,21 @@ def main():
         return gather_results({f: res[f] for f in STAT_FIELDS}, res["x_nodes"], res["x_vals"],
                               dst=0, to_host=False)  # (results stay in rank 0's HBM)
 
-    for k in range(args.warmup):
-        gather(solver.solve_device(dseeds[k], stream=stream))
+    ops_d = torch.zeros((), dtype=torch.int64, device="cuda")  # summed on the device: no
+    pushes_d = torch.zeros((), dtype=torch.int64, device="cuda")  # per-step host read-back
+    for k in range(args.warmup):  # (also loads the reduction kernels used below)
+        res = solver.solve_device(dseeds[k], stream=stream)
+        gather(res)
+        ops_d += res["total_ops"].sum()
+        pushes_d += res["pushes"].sum()
     torch.cuda.synchronize()
+    ops_d.zero_()
+    pushes_d.zero_()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ops = pushes = solved = 0
+    solved = 0
     kern_ms = 0.0
     launches = 0
     with ClockSampler(local) as clk:
@@ -378,11 +391,12 @@ def main():
             gather(res)
             kern_ms += solver.last_kernel_ms
             launches += res["kernel_launches"]
-            ops += int(res["total_ops"].sum())
-            pushes += int(res["pushes"].sum())
+            ops_d += res["total_ops"].sum()
+            pushes_d += res["pushes"].sum()
             solved += len(batches[k])
         ev1.record(stream)
         torch.cuda.synchronize()
+    ops, pushes = int(ops_d), int(pushes_d)
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms, ops, pushes, solved, kern_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -399,7 +413,9 @@ def main():
     peak, peak_kind = peaks()
     my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic({"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
+    cta = solver.mode == "cta"  # small graphs: one CTA per seed, one launch per solve
+    traffic, traffic_src = ncu_traffic("k_seed_cta" if cta else
+                                       {"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
                                         "local-hk": "k_rounds_hk",
                                         "local-sor": "k_fifo_batch"}[args.method])
     # e2e: the public host API with host buffers, copies inside the timed region
@@ -460,11 +476,12 @@ def main():
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // 4,
+                         "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // (1 if cta else 4),
                                                                 "local-ch": launches // 5,
                                                                 "local-hk": launches // 5}.get(args.method, launches)),
                          "peak_kind": peak_kind,
-                         "kernel": {"local-gd": "k_rounds (persistent sweep loop)",
+                         "kernel": {"local-gd": "k_seed_cta (one CTA per seed)" if cta else
+                                                    "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
                                     "local-hk": "k_rounds<HK> (layered heat-kernel stage sweeps)",
                                     "local-sor": "k_fifo_batch (warp per seed)"}[args.method],

@@ -263,6 +263,14 @@ int gd_batch_fetch_r_host(gd_batch *b, int64_t n_seeds, int64_t *r_offset, int64
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
+/* Execution form chosen at creation: GD_BATCH_ROUNDS (the wave round kernel,
+ * k_rounds / k_signed_rounds), GD_BATCH_CTA (LocalGD on small graphs: one CTA
+ * per seed, k_seed_cta) or GD_BATCH_FIFO (LocalSOR/GS, warp per seed); and
+ * the number of seeds in flight. */
+#define GD_BATCH_ROUNDS 0
+#define GD_BATCH_CTA 1
+#define GD_BATCH_FIFO 2
+int gd_batch_info(const gd_batch *b, int32_t *mode, int64_t *slots);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */
 int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *rounds);

@@ -153,6 +153,14 @@ class BatchSolver:
         gdl.check(self.lib.gd_batch_last_kernel_ms(self.handle, C.byref(ms)))
         return ms.value
 
+    @property
+    def mode(self) -> str:
+        """Execution form: "rounds" (wave round kernel), "cta" (one CTA per
+        seed, LocalGD on small graphs) or "fifo" (LocalSOR/GS)."""
+        m, s = C.c_int32(), C.c_int64()
+        gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
+        return ("rounds", "cta", "fifo")[m.value]
+
     def round_log(self) -> np.ndarray:
         """(rounds, 3) int64: frontier entries, arcs, device ns at round start
         for the last wave of the last solve (instrumentation)."""

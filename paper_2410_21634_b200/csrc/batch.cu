@@ -71,6 +71,17 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
                       cudaStream_t st, const RPool *rp);
 int fifo_batch_slots(const FifoBatchState *F);
+struct CtaState;  // batch_cta.cu: one CTA per seed (small graphs)
+CtaState *cta_batch_create(const gd_graph *W, int max_slots);
+void cta_batch_destroy(CtaState *S);
+int cta_batch_slots(const CtaState *S);
+int64_t cta_slot_bytes(int64_t n, int64_t n_arcs);
+void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alpha, double eps,
+                   int64_t max_sweeps, const int64_t *d_seeds, int64_t n_seeds,
+                   const int32_t *perm, const int32_t *inv, int64_t *sweeps, int64_t *ops,
+                   int64_t *pushes, int64_t *support, int32_t *conv, int64_t *xoff,
+                   int64_t *xcnt, int32_t *xnodes, double *xvals, int64_t xcap,
+                   unsigned long long *cursor, cudaStream_t st);
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
                     int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
@@ -88,6 +99,7 @@ constexpr int CNT_SHIFT = 36;
 constexpr unsigned long long ARC_MASK = (1ULL << CNT_SHIFT) - 1ULL;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int CHUNKS = 32;  // blocks per slot in the extract / reset kernels
+constexpr int64_t CTA_MAX_N = 1LL << 18;  // one-CTA-per-seed mode up to this many nodes
 
 struct RoundArgs {
     DevGraph g;
@@ -915,6 +927,7 @@ struct gd_batch {
     const gd_graph *G;      // caller's graph
     FifoBatchState *fifo = nullptr;  // GD_M_LOCAL_SOR state
     SignedState *sgn = nullptr;      // GD_M_LOCAL_CH state
+    CtaState *cta = nullptr;         // GD_M_LOCAL_GD, small graphs: one CTA per seed
     gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
     DBuf<int32_t> perm, inv;
     gd_batch_params p;
@@ -1001,6 +1014,7 @@ struct gd_batch {
         delete R;
         if (fifo) fifo_batch_destroy(fifo);
         if (sgn) signed_batch_destroy(sgn);
+        if (cta) cta_batch_destroy(cta);
     }
 };
 
@@ -1031,6 +1045,27 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             fifo_batch_run(B->fifo, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
                            B->pushes.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p,
                            B->xvals.p, B->xcap, B->cursor.p, st, rpp);
+        GD_CUDA(cudaEventRecord(B->ev[1], st));
+        GD_CUDA(cudaStreamSynchronize(st));
+        float f = 0.f;
+        GD_CUDA(cudaEventElapsedTime(&f, B->ev[0], B->ev[1]));
+        B->last_ms = f;
+        B->last_launches = n_seeds ? 1 : 0;
+        return;
+    }
+    if (B->cta) {  // one CTA per seed (batch_cta.cu): no waves, no grid barriers
+        if (B->ev.size() < 2) {
+            for (size_t i = B->ev.size(); i < 2; ++i) {
+                cudaEvent_t e;
+                GD_CUDA(cudaEventCreate(&e));
+                B->ev.push_back(e);
+            }
+        }
+        GD_CUDA(cudaEventRecord(B->ev[0], st));
+        cta_batch_run(B->cta, B->work(), B->colp.p, B->p.alpha, B->p.eps, B->p.max_sweeps, d_seeds,
+                      n_seeds, B->R ? B->perm.p : nullptr, B->R ? B->inv.p : nullptr, B->sweeps.p,
+                      B->ops.p, B->pushes.p, B->support.p, B->conv.p, B->xoff.p, B->xcnt.p,
+                      B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p, st);
         GD_CUDA(cudaEventRecord(B->ev[1], st));
         GD_CUDA(cudaStreamSynchronize(st));
         float f = 0.f;
@@ -1334,6 +1369,21 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, BT, smem));
             GD_CHECK_ARG(per_sm > 0, "round kernel does not fit on an SM");
             B->grid = per_sm * n_sms(G->device);
+            if (!B->hk && !B->want_r() && p->frontier_cap <= 0) {
+                // small graphs: sweeps scatter too few arcs to amortise two grid
+                // barriers, so each seed runs in a CTA of its own (batch_cta.cu)
+                bool use_cta = G->n <= CTA_MAX_N;
+                if (const char *e = getenv("GDIFF_BATCH_MODE"))  // (tests, A/B)
+                    use_cta = strcmp(e, "cta") == 0 ? true : (strcmp(e, "rounds") == 0 ? false : use_cta);
+                if (use_cta) {
+                    size_t fr = 0, tot = 0;
+                    GD_CUDA(cudaMemGetInfo(&fr, &tot));
+                    const int64_t per = cta_slot_bytes(G->n, G->n_arcs);
+                    int64_t cap = (int64_t)(fr / 4) / per;
+                    if (p->slots > 0 && p->slots < cap) cap = p->slots;
+                    if (cap >= 1) B->cta = cta_batch_create(B->work(), (int)(cap < (1 << 20) ? cap : (1 << 20)));
+                }
+            }
         } catch (...) {
             delete B;
             throw;
@@ -1501,6 +1551,13 @@ int gd_batch_fetch_r_host(gd_batch *B, int64_t n_seeds, int64_t *r_offset, int64
 int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {
     if (!B || !ms) return GD_ERR_ARG;
     *ms = B->last_ms;
+    return GD_OK;
+}
+
+int gd_batch_info(const gd_batch *B, int32_t *mode, int64_t *slots) {
+    if (!B || !mode || !slots) return GD_ERR_ARG;
+    *mode = B->cta ? GD_BATCH_CTA : (B->fifo ? GD_BATCH_FIFO : GD_BATCH_ROUNDS);
+    *slots = B->cta ? (int64_t)cta_batch_slots(B->cta) : (int64_t)B->slots;
     return GD_OK;
 }
 

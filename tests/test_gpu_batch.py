@@ -28,8 +28,13 @@ def _check_x(out, i, x_ref):
     assert np.array_equal(np.argsort(-x, kind="stable")[:10], top)
 
 
+MODES = ["cta", "rounds"]  # one CTA per seed (small graphs) / the round kernel (large graphs)
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("slots,relabel", [(0, True), (1, True), (7, False), (64, True), (64, False)])
-def test_cora_config1_batch(gpu, cora, slots, relabel):
+def test_cora_config1_batch(gpu, cora, monkeypatch, mode, slots, relabel):
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
     g = golden_graph(cora, "cora")
     seeds = cora["seeds"]
     out = local_gd_batch(g, seeds, 0.1, 1e-6, slots=slots, relabel=relabel)
@@ -51,7 +56,9 @@ def test_pa_batch_matches_reference(gpu, pa):
         _check_x(out, i, pa[f"{k}/x"])
 
 
-def test_rmat_batch_matches_oracle(gpu):
+@pytest.mark.parametrize("mode", MODES)
+def test_rmat_batch_matches_oracle(gpu, monkeypatch, mode):
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 48, seed=0)
     ref = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=8)
@@ -64,8 +71,10 @@ def test_rmat_batch_matches_oracle(gpu):
     np.testing.assert_allclose(xs, ref["xsum"], rtol=1e-12)
 
 
-def test_solver_reuse_and_device_path(gpu):
+@pytest.mark.parametrize("mode", MODES)
+def test_solver_reuse_and_device_path(gpu, monkeypatch, mode):
     import torch
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
     g = rmat_graph(5000, 30000, seed=9)
     seeds = sample_sources(g, 40, seed=1)
     solver = BatchSolver(g, 0.15, 1e-5, slots=8)
@@ -76,12 +85,14 @@ def test_solver_reuse_and_device_path(gpu):
     d = solver.solve_device(torch.as_tensor(seeds, device="cuda"))
     assert np.array_equal(d["total_ops"].cpu().numpy(), a["total_ops"])
     assert np.array_equal(d["sweeps"].cpu().numpy(), a["sweeps"])
-    assert d["kernel_launches"] == 4 * 5
+    assert d["kernel_launches"] == (4 * 5 if mode == "rounds" else 1)
     assert solver.last_kernel_ms > 0.0
 
 
-def test_edge_cases(gpu):
+@pytest.mark.parametrize("mode", MODES)
+def test_edge_cases(gpu, monkeypatch, mode):
     from paper_2410_21634_b200.graph import from_edges
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
     # isolated nodes, a leaf, max_sweeps cap, empty batch
     g = from_edges(6, [(0, 1), (1, 2), (2, 0), (3, 4)])
     out = local_gd_batch(g, [0, 3], 0.2, 1e-9, max_sweeps=2)
@@ -175,10 +186,12 @@ def test_hk_batch_matches_oracle(gpu, tau, eps):
 
 # ---- edge cases -------------------------------------------------------------
 
-def test_batch_edge_cases(gpu):
+@pytest.mark.parametrize("mode", MODES)
+def test_batch_edge_cases(gpu, monkeypatch, mode):
     """Empty batches, duplicate seeds, sweep caps and a frontier-capacity
     overflow (reported as an error, the solver stays usable)."""
     from paper_2410_21634_b200._lib import GdiffError
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
     g = rmat_graph(5000, 30000, seed=4)
     seeds = sample_sources(g, 24, seed=2)
     for method in ("local-gd", "local-ch", "local-sor"):
@@ -231,6 +244,7 @@ def test_grouped_mode_matches_oracle(gpu, monkeypatch, group):
     LocalGD and the heat kernel."""
     from paper_2410_21634_b200.batch import local_hk_batch
     monkeypatch.setenv("GDIFF_SLOT_GROUP", group)
+    monkeypatch.setenv("GDIFF_BATCH_MODE", "rounds")
     monkeypatch.setenv("GDIFF_GROUP_MIN", "0")  # every round grouped
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 40, seed=0)
