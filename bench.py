@@ -414,7 +414,8 @@ def main():
     my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
     cta = solver.mode == "cta"  # small graphs: one CTA per seed, one launch per solve
-    traffic, traffic_src = ncu_traffic("k_seed_cta" if cta else
+    win = solver.mode == "fifo-win"  # LocalGS / unsigned SOR: exact windows, CTA per seed
+    traffic, traffic_src = ncu_traffic("k_seed_cta" if cta else "k_sor_win" if win else
                                        {"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
                                         "local-hk": "k_rounds_hk",
                                         "local-sor": "k_fifo_batch"}[args.method])
@@ -484,7 +485,8 @@ def main():
                                                     "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
                                     "local-hk": "k_rounds<HK> (layered heat-kernel stage sweeps)",
-                                    "local-sor": "k_fifo_batch (warp per seed)"}[args.method],
+                                    "local-sor": "k_sor_win (exact windows, CTA per seed)" if win
+                                                 else "k_fifo_batch (warp per seed)"}[args.method],
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "relabel": not args.no_relabel,

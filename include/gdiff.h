@@ -270,6 +270,7 @@ int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
 #define GD_BATCH_ROUNDS 0
 #define GD_BATCH_CTA 1
 #define GD_BATCH_FIFO 2
+#define GD_BATCH_FIFO_WIN 3 /* LocalSOR/GS in exact windows, one CTA per seed */
 int gd_batch_info(const gd_batch *b, int32_t *mode, int64_t *slots);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */

@@ -156,10 +156,11 @@ class BatchSolver:
     @property
     def mode(self) -> str:
         """Execution form: "rounds" (wave round kernel), "cta" (one CTA per
-        seed, LocalGD on small graphs) or "fifo" (LocalSOR/GS)."""
+        seed, LocalGD on small graphs), "fifo" (LocalSOR/GS, warp per seed) or
+        "fifo-win" (LocalSOR/GS in exact windows, CTA per seed)."""
         m, s = C.c_int32(), C.c_int64()
         gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
-        return ("rounds", "cta", "fifo")[m.value]
+        return ("rounds", "cta", "fifo", "fifo-win")[m.value]
 
     def round_log(self) -> np.ndarray:
         """(rounds, 3) int64: frontier entries, arcs, device ns at round start

@@ -24,6 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{INCLUDE}"]
 SOURCES = ["graph.cu", "exact.cu", "fifo.cu", "fifo_batch.cu", "global.cu", "batch.cu", "batch_cta.cu",
+           "sor_win.cu",
            "batch_signed.cu",
            "generate.cu", "graph_edit.cu", "hk.cu",
            "feature_push.cu"]

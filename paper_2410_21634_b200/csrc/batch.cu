@@ -71,6 +71,13 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
                       cudaStream_t st, const RPool *rp);
 int fifo_batch_slots(const FifoBatchState *F);
+struct SorWinState;  // sor_win.cu: LocalSOR/GS seeds in exact windows, one CTA per seed
+SorWinState *sorwin_create(const gd_graph *G, int max_ctas);
+void sorwin_destroy(SorWinState *W);
+void sorwin_run(SorWinState *W, const gd_graph *G, const gd_batch_params &p,
+                const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
+                int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
+                double *xvals, int64_t xcap, unsigned long long *cursor, cudaStream_t st);
 struct CtaState;  // batch_cta.cu: one CTA per seed (small graphs)
 CtaState *cta_batch_create(const gd_graph *W, int max_slots);
 void cta_batch_destroy(CtaState *S);
@@ -928,6 +935,7 @@ struct gd_batch {
     FifoBatchState *fifo = nullptr;  // GD_M_LOCAL_SOR state
     SignedState *sgn = nullptr;      // GD_M_LOCAL_CH state
     CtaState *cta = nullptr;         // GD_M_LOCAL_GD, small graphs: one CTA per seed
+    SorWinState *sorwin = nullptr;   // GD_M_LOCAL_SOR in exact windows, one CTA per seed
     gd_graph *R = nullptr;  // degree-relabeled copy (when p.relabel)
     DBuf<int32_t> perm, inv;
     gd_batch_params p;
@@ -1015,6 +1023,7 @@ struct gd_batch {
         if (fifo) fifo_batch_destroy(fifo);
         if (sgn) signed_batch_destroy(sgn);
         if (cta) cta_batch_destroy(cta);
+        if (sorwin) sorwin_destroy(sorwin);
     }
 };
 
@@ -1041,7 +1050,11 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         }
         GD_CUDA(cudaMemsetAsync(B->support.p, 0xFF, sizeof(int64_t) * ns, st));  // not tracked
         GD_CUDA(cudaEventRecord(B->ev[0], st));
-        if (n_seeds)
+        if (n_seeds && B->sorwin && !rpp)
+            sorwin_run(B->sorwin, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
+                       B->pushes.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p, B->xvals.p,
+                       B->xcap, B->cursor.p, st);
+        else if (n_seeds)
             fifo_batch_run(B->fifo, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
                            B->pushes.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p,
                            B->xvals.p, B->xcap, B->cursor.p, st, rpp);
@@ -1253,6 +1266,17 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 // exact FIFO replay needs the caller's CSR order: no relabeling
                 B->fifo = fifo_batch_create(G, p->slots);
                 B->slots = fifo_batch_slots(B->fifo);
+                // exact windows, one CTA per seed (sor_win.cu), for the unsigned
+                // push (omega <= 1): windows of ~80 pops beat the one-pop-at-a-time
+                // warp chain (arxiv LocalGS eps=1e-6: 38.4 -> 24.0 ms per 1,024
+                // seeds, cora 39.8 -> 11.0 ms per 50).  Signed SOR (omega > 1)
+                // keeps adjacent nodes queued together, windows shrink to ~10 pops
+                // and the warp chain wins (arxiv 214 vs 740 ms).  GDIFF_SOR_MODE=
+                // win|warp forces either; not with want_r.
+                bool use_win = p->omega <= 1.0;
+                if (const char *e = getenv("GDIFF_SOR_MODE"))
+                    use_win = strcmp(e, "win") == 0 ? true : (strcmp(e, "warp") == 0 ? false : use_win);
+                if (use_win && !p->want_r) B->sorwin = sorwin_create(G, p->slots);
                 B->cursor.alloc(1); B->overflow.alloc(1);
                 B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
                 B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
@@ -1556,7 +1580,8 @@ int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {
 
 int gd_batch_info(const gd_batch *B, int32_t *mode, int64_t *slots) {
     if (!B || !mode || !slots) return GD_ERR_ARG;
-    *mode = B->cta ? GD_BATCH_CTA : (B->fifo ? GD_BATCH_FIFO : GD_BATCH_ROUNDS);
+    *mode = B->cta ? GD_BATCH_CTA
+                   : (B->sorwin ? GD_BATCH_FIFO_WIN : (B->fifo ? GD_BATCH_FIFO : GD_BATCH_ROUNDS));
     *slots = B->cta ? (int64_t)cta_batch_slots(B->cta) : (int64_t)B->slots;
     return GD_OK;
 }

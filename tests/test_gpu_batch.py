@@ -118,9 +118,11 @@ def test_device_generator_equals_host(gpu):
 
 # ---- batched FIFO (LocalSOR / LocalGS): bit-identical per seed ------------
 
+@pytest.mark.parametrize("mode", ["win", "warp"])  # exact windows (CTA per seed) / warp chain
 @pytest.mark.parametrize("omega", [1.0, 1.39301, 0.7])
 @pytest.mark.parametrize("slots", [0, 5])
-def test_sor_batch_bitwise_vs_oracle(gpu, cora, omega, slots):
+def test_sor_batch_bitwise_vs_oracle(gpu, cora, monkeypatch, mode, omega, slots):
+    monkeypatch.setenv("GDIFF_SOR_MODE", mode)
     from paper_2410_21634_b200.batch import local_sor_batch
     from paper_2410_21634_b200.systems import make_ppr_system
     g = golden_graph(cora, "cora")
