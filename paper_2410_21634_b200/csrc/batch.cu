@@ -724,14 +724,32 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
     const int64_t off = (int64_t)k * A.ld;
     const int64_t pc = (int64_t)A.pushed_cnt[k];
     const int64_t b = A.slot_base[k];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pc;
-         i += (int64_t)CHUNKS * blockDim.x) {
-        const int32_t u = A.pushed[off + i];
-        const double xv = A.x[off + u];
-        A.x[off + u] = 0.0;
-        if (b + i < O.xcap) {
-            O.xnodes[b + i] = O.inv ? O.inv[u] : u;
-            O.xvals[b + i] = __dmul_rn(O.xscale, xv);
+    // XU entries per thread with every load issued before any store (the x
+    // stores would otherwise order each gather behind the previous one)
+    constexpr int XU = 4;
+    const int64_t stride = (int64_t)CHUNKS * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < pc; i0 += XU * stride) {
+        int32_t u[XU], id[XU];
+        double xv[XU];
+#pragma unroll
+        for (int j = 0; j < XU; ++j) {
+            const int64_t i = i0 + j * stride;
+            u[j] = i < pc ? __ldg(A.pushed + off + i) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < XU; ++j) {
+            xv[j] = u[j] >= 0 ? A.x[off + u[j]] : 0.0;
+            id[j] = (u[j] >= 0 && O.inv) ? __ldg(O.inv + u[j]) : u[j];
+        }
+#pragma unroll
+        for (int j = 0; j < XU; ++j) {
+            const int64_t i = i0 + j * stride;
+            if (u[j] < 0) continue;
+            A.x[off + u[j]] = 0.0;
+            if (b + i < O.xcap) {
+                O.xnodes[b + i] = id[j];
+                O.xvals[b + i] = __dmul_rn(O.xscale, xv[j]);
+            }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
