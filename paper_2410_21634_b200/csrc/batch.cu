@@ -995,6 +995,19 @@ struct gd_batch {
     int64_t last_launches = 0;
     int64_t last_x_total = 0;
     DBuf<int64_t> dseeds;  // host-entry staging of the seed list
+    // Host entry (gd_batch_solve_host): the sparse x of wave w is copied to the
+    // caller's buffers on a copy stream while wave w+1 runs (rounds mode).
+    struct HostStream {
+        int32_t *nodes = nullptr;
+        double *vals = nullptr;
+        int64_t cap = 0;        // caller's pairs
+        int64_t streamed = 0;   // pairs [0, streamed) already queued on `cs`
+        cudaStream_t cs = nullptr;
+        unsigned long long *curh = nullptr;  // pinned: pool cursor after each wave
+        int64_t curh_n = 0;
+        std::vector<cudaEvent_t> wev;
+    } hs;
+    bool hs_on = false;
 
     const gd_graph *work() const { return R ? R : G; }
     // blocks per slot of the reset: ~2,048 map words (256 KB of r) per block
@@ -1035,7 +1048,45 @@ struct gd_batch {
         A.slot_base = slot_base.p;
         return A;
     }
+    // Queue the copy of wave w's pairs [cursor after w-1, cursor after w).
+    void hs_drain(int64_t w) {
+        GD_CUDA(cudaEventSynchronize(hs.wev[w]));
+        int64_t end = (int64_t)hs.curh[w];
+        const int64_t lim = hs.cap < xcap ? hs.cap : xcap;
+        if (end > lim) end = lim;
+        if (end > hs.streamed) {
+            const int64_t k = end - hs.streamed;
+            GD_CUDA(cudaMemcpyAsync(hs.nodes + hs.streamed, xnodes.p + hs.streamed,
+                                    sizeof(int32_t) * k, cudaMemcpyDeviceToHost, hs.cs));
+            GD_CUDA(cudaMemcpyAsync(hs.vals + hs.streamed, xvals.p + hs.streamed,
+                                    sizeof(double) * k, cudaMemcpyDeviceToHost, hs.cs));
+            hs.streamed = end;
+        }
+    }
+    // Called after wave w is enqueued on st: record its cursor, drain wave w-1
+    // (the GPU already holds wave w, so the host wait does not idle it).
+    void hs_wave(int64_t w, int64_t waves, cudaStream_t st) {
+        if (!hs_on) return;
+        if (hs.curh_n < waves) {
+            if (hs.curh) cudaFreeHost(hs.curh);
+            GD_CUDA(cudaMallocHost(&hs.curh, sizeof(unsigned long long) * waves));
+            hs.curh_n = waves;
+        }
+        while ((int64_t)hs.wev.size() < waves) {
+            cudaEvent_t e;
+            GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            hs.wev.push_back(e);
+        }
+        GD_CUDA(cudaMemcpyAsync(hs.curh + w, cursor.p, sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st));
+        GD_CUDA(cudaEventRecord(hs.wev[w], st));
+        if (w >= 1) hs_drain(w - 1);
+        if (w == waves - 1) hs_drain(w);
+    }
     ~gd_batch() {
+        if (hs.curh) cudaFreeHost(hs.curh);
+        for (auto e : hs.wev) cudaEventDestroy(e);
+        if (hs.cs) cudaStreamDestroy(hs.cs);
         for (auto e : ev) cudaEventDestroy(e);
         delete R;
         if (fifo) fifo_batch_destroy(fifo);
@@ -1050,6 +1101,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->sweeps.ensure(ns); B->ops.ensure(ns); B->pushes.ensure(ns); B->support.ensure(ns);
     B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
+    B->hs.streamed = 0;
     RPool rp{};
     if (B->want_r()) {
         B->roff.ensure(ns); B->rcnt.ensure(ns);
@@ -1156,6 +1208,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         }
         GD_LAUNCH_CHECK();
         launches += B->hk ? 5 : 4;
+        B->hs_wave(w, waves, st);
     }
     GD_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
@@ -1465,7 +1518,9 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
             B->last_r_total = (int64_t)rused;
             if ((int64_t)used <= B->xcap && (int64_t)rused <= B->rcap) break;
             GD_CHECK_ARG(attempt == 0, "output pool sizing failed");
-            // grow (doubling, so a growing workload redoes at most log times) and redo
+            // grow (doubling, so a growing workload redoes at most log times) and redo;
+            // host-entry copies still reading the old pool finish first
+            if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));
             if ((int64_t)used > B->xcap) {
                 B->xcap = 2 * (int64_t)used;
                 B->xnodes.alloc(B->xcap);
@@ -1511,9 +1566,14 @@ int gd_batch_fetch_host(gd_batch *B, int64_t n_seeds, int64_t *sweeps, int64_t *
                       (long long)B->last_x_total);
             throw Error{GD_ERR_CAPACITY};
         }
-        d2h(x_nodes, B->xnodes.p, sizeof(int32_t) * B->last_x_total);
-        d2h(x_vals, B->xvals.p, sizeof(double) * B->last_x_total);
+        // pairs the wave loop already queued on the copy stream (host entry)
+        int64_t done = 0;
+        if (B->hs_on && B->hs.nodes == x_nodes && B->hs.vals == x_vals) done = B->hs.streamed;
+        if (done > B->last_x_total) done = B->last_x_total;
+        d2h(x_nodes + done, B->xnodes.p + done, sizeof(int32_t) * (B->last_x_total - done));
+        d2h(x_vals + done, B->xvals.p + done, sizeof(double) * (B->last_x_total - done));
         GD_CUDA(cudaStreamSynchronize(st));
+        if (done) GD_CUDA(cudaStreamSynchronize(B->hs.cs));
     });
 }
 
@@ -1529,10 +1589,23 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
         GD_CUDA(cudaMemcpyAsync(B->dseeds.p, seeds, sizeof(int64_t) * n_seeds,
                                 cudaMemcpyHostToDevice, st));
         gd_batch_result res{};
+        if (x_nodes && x_vals && x_cap > 0) {  // stream finished waves' x to the host
+            if (!B->hs.cs) GD_CUDA(cudaStreamCreateWithFlags(&B->hs.cs, cudaStreamNonBlocking));
+            B->hs.nodes = x_nodes;
+            B->hs.vals = x_vals;
+            B->hs.cap = x_cap;
+            B->hs_on = true;
+        }
         int rc = gd_batch_solve_device(B, B->dseeds.p, n_seeds, &res, stream);
-        if (rc != GD_OK) throw Error{rc};
-        rc = gd_batch_fetch_host(B, n_seeds, sweeps, total_ops, pushes, converged, x_offset,
-                                 x_count, x_nodes, x_vals, x_cap, x_total, stream);
+        if (rc == GD_OK)
+            rc = gd_batch_fetch_host(B, n_seeds, sweeps, total_ops, pushes, converged, x_offset,
+                                     x_count, x_nodes, x_vals, x_cap, x_total, stream);
+        if (B->hs_on) {
+            cudaStreamSynchronize(B->hs.cs);  // no copy may outlive the call
+            B->hs_on = false;
+            B->hs.nodes = nullptr;
+            B->hs.vals = nullptr;
+        }
         if (rc != GD_OK) throw Error{rc};
     });
 }

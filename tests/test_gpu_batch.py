@@ -286,3 +286,32 @@ def test_batch_sparse_r(gpu, method):
             assert np.abs(r - ref["r"]).sum() <= 1e-9 * np.abs(ref["r"]).sum() + 1e-300
             assert set(np.flatnonzero(ref["r"]).tolist()) <= set(nodes.tolist())
     solver.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", MODES)
+def test_host_entry_streams_x_per_wave(gpu, monkeypatch, mode):
+    """gd_batch_solve_host copies each finished wave's sparse x while the next
+    wave runs: the host result equals a device-path solve per seed, on a cold
+    call (host buffers too small: capacity path) and on warm calls."""
+    import torch
+    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    g = rmat_graph(20000, 150000, seed=3)
+    seeds = sample_sources(g, 70, seed=4)
+    solver = BatchSolver(g, 0.1, 1e-6, slots=8)
+    for pinned in (False, True, True):
+        out = {"pinned": pinned}
+        h = solver.solve(seeds, out=out)
+        d = solver.solve_device(torch.as_tensor(seeds, device="cuda"))
+        assert h.x_nodes.shape[0] == d["x_total"]
+        off, cnt = d["x_offset"].cpu().numpy(), d["x_count"].cpu().numpy()
+        dn, dv = d["x_nodes"].cpu().numpy(), d["x_vals"].cpu().numpy()
+        assert np.array_equal(h.x_count, cnt)
+        for i in range(len(seeds)):  # pool positions are per call in the CTA mode
+            a = np.argsort(h.x_nodes[h.x_offset[i]:h.x_offset[i] + cnt[i]], kind="stable")
+            b = np.argsort(dn[off[i]:off[i] + cnt[i]], kind="stable")
+            assert np.array_equal(h.x_nodes[h.x_offset[i]:][:cnt[i]][a], dn[off[i]:][:cnt[i]][b])
+            # fp64 atomics: values agree to rounding between two solves
+            np.testing.assert_allclose(h.x_vals[h.x_offset[i]:][:cnt[i]][a],
+                                       dv[off[i]:][:cnt[i]][b], rtol=1e-9, atol=1e-15)
+    solver.close()
