@@ -86,3 +86,41 @@ def test_papers100m_shape_batch_properties(gpu):
         assert abs(alpha * xv.sum() + rv.sum() - alpha) <= 1e-11
     # every pushed node was pushed at least once: support of x <= pushes
     assert (out.x_count <= out.pushes).all()
+
+
+def test_products_shape_local_ch_batch(gpu):
+    """Config 3's LocalCH-PPR (mu = alpha, L = 2 - alpha, src/local_solvers.py:541-558)
+    at the products shape: termination and sweeps / ops / convergence identical to
+    the reference algorithm on a seed sample."""
+    import math
+
+    from bench import SHAPES, host_graph_full, make_graph
+    from oracle import oracle as O
+    from paper_2410_21634_b200.batch import BatchSolver
+    from paper_2410_21634_b200.metrics import sample_sources
+
+    alpha, eps = 0.1, 1e-7
+    mu, L = alpha, 2.0 - alpha
+    cap = max(1000, int(10 * math.log(1.0 / eps) / mu))
+    n, _ = SHAPES["products"]
+    dg, row, col, row_h = make_graph("products", 0, 0)
+    hg = host_graph_full(n, row_h, col, alpha, eps)
+    del row, col
+    seeds = sample_sources(hg, 32, seed=1)
+    solver = BatchSolver(dg, alpha, eps, method="local-ch", mu=mu, L=L, max_sweeps=cap,
+                         want_r=True)
+    try:
+        out = solver.solve(seeds)
+    finally:
+        solver.close()
+    assert out.converged.all()
+    for i in range(len(seeds)):
+        rn, rv = out.r_sparse(i)
+        assert (np.abs(rv) < hg.theta[rn]).all()
+    idx = np.arange(0, len(seeds), 8)
+    ref = O.batch_local_ch(hg, alpha, eps, seeds[idx], threads=8, mu=mu, L=L, max_sweeps=cap)
+    assert np.array_equal(out.sweeps[idx], ref["sweeps"])
+    assert np.array_equal(out.total_ops[idx], ref["total_ops"])
+    assert np.array_equal(out.converged[idx], ref["converged"])
+    xs = np.array([out.x_sparse(i)[1].sum() for i in idx])
+    np.testing.assert_allclose(xs, ref["xsum"], rtol=1e-9)
