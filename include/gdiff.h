@@ -239,7 +239,10 @@ int gd_batch_solve_device(gd_batch *b, const int64_t *d_seeds, int64_t n_seeds,
                           gd_batch_result *res, void *stream);
 /* Host entry: seeds from host memory, per-seed stats and the sparse x
  * copied back into caller buffers (pinned memory recommended).  x buffers
- * hold x_cap pairs; GD_ERR_CAPACITY (with *x_total set) if too small. */
+ * hold x_cap pairs; GD_ERR_CAPACITY (with *x_total set) if too small.
+ * In the wave (round-kernel) form each finished wave's (node, x) pairs are
+ * copied into x_nodes / x_vals on a second stream while the next wave runs;
+ * every copy has completed when the call returns. */
 int gd_batch_solve_host(gd_batch *b, const int64_t *seeds, int64_t n_seeds,
                         int64_t *sweeps, int64_t *total_ops, int64_t *pushes,
                         int32_t *converged, int64_t *x_offset, int64_t *x_count,
