@@ -100,6 +100,9 @@ namespace gd {
 namespace {
 
 constexpr int BT = 512;   // threads per block of the round kernel
+#ifndef GD_KR_MINB
+#define GD_KR_MINB 2  // resident round-kernel blocks per SM (register budget)
+#endif
 constexpr int UNROLL = 4; // 32-arc chunks in flight per warp in phase B
 constexpr int SUPER = 16; // UNROLL-chunk groups per block super-chunk in phase B
 constexpr int CNT_SHIFT = 36;
@@ -416,7 +419,7 @@ __device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
 // products are fl(fl(r * tau/(t+1)) * fl(1/d_u)).  x accumulates the pushed
 // values stage by stage -- the reference's stages.sum(axis=0) order.
 template <bool HK>
-__global__ void __launch_bounds__(BT, 2) k_rounds(RoundArgs A) {
+__global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Stage S = stage_carve(smem_raw, (int)A.m);
