@@ -209,8 +209,15 @@ class BatchSolver:
             for name, dt in (("sweeps", np.int64), ("total_ops", np.int64), ("pushes", np.int64),
                              ("converged", np.int32), ("x_offset", np.int64), ("x_count", np.int64)):
                 out[name] = _host_array(k, dt, pinned)
-        cap = x_cap if x_cap is not None else max(out["x_nodes"].shape[0] if "x_nodes" in out else 0,
-                                                  int(1.25 * self._last_total) + 1024)
+        # host x buffers: reused while they hold the previous solve's pairs; a new
+        # (pinned: slow to allocate) pair of buffers gets 1.5x headroom
+        have = out["x_nodes"].shape[0] if "x_nodes" in out else 0
+        if x_cap is not None:
+            cap = x_cap
+        elif have >= self._last_total + 1024:
+            cap = have
+        else:
+            cap = int(1.5 * self._last_total) + 1024
         st = 0
         if stream is not None:
             st = stream.cuda_stream
@@ -230,7 +237,7 @@ class BatchSolver:
                                           C.byref(tot), C.c_void_p(st))
         if rc == gdl.GD_ERR_CAPACITY and tot.value > out["x_nodes"].shape[0]:
             # results are still on the device: grow the host buffers, fetch again
-            cap = int(tot.value * 1.25) + 1024
+            cap = int(tot.value * 1.5) + 1024  # (pinned allocations are slow: grow ahead)
             out["x_nodes"] = _host_array(cap, np.int32, pinned)
             out["x_vals"] = _host_array(cap, np.float64, pinned)
             rc = self.lib.gd_batch_fetch_host(self.handle, k, *bufs(), C.byref(tot), C.c_void_p(st))

@@ -1402,7 +1402,14 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
                 // 64 in flight measured best on the products shape (L2 reuse of
                 // the hub block vs. barrier amortisation); fewer if memory-bound
-                int64_t by_mem = (int64_t)(fr / 3) / (ld * (B->hk ? 28 : 20));
+                double frac = 0.7;  // share of free HBM for the slot vectors (papers100M:
+                                    // 13 -> 29 slots, eps=1e-6 50.9 K -> 65.6 K solves/s)
+                if (const char *e = getenv("GDIFF_SLOT_MEM")) frac = atof(e);  // experiments
+                int64_t budget = (int64_t)((double)fr * frac);
+                const int64_t keep = 8LL << 30;  // frontier arrays, output pools, headroom
+                if (budget > (int64_t)fr - keep) budget = (int64_t)fr - keep;
+                if (budget < 0) budget = 0;
+                int64_t by_mem = budget / (ld * (B->hk ? 28 : 20));
                 // the heat kernel at large tau is effectively global: a stage's
                 // frontier approaches n per seed, so bound slots * n as well
                 if (B->hk && by_mem > (64LL << 20) / n) by_mem = (64LL << 20) / n;
@@ -1592,7 +1599,7 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
         GD_CUDA(cudaMemcpyAsync(B->dseeds.p, seeds, sizeof(int64_t) * n_seeds,
                                 cudaMemcpyHostToDevice, st));
         gd_batch_result res{};
-        if (x_nodes && x_vals && x_cap > 0) {  // stream finished waves' x to the host
+        if (x_nodes && x_vals && x_cap > 0 && !getenv("GDIFF_NO_STREAM")) {  // stream finished waves' x to the host
             if (!B->hs.cs) GD_CUDA(cudaStreamCreateWithFlags(&B->hs.cs, cudaStreamNonBlocking));
             B->hs.nodes = x_nodes;
             B->hs.vals = x_vals;
