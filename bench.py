@@ -472,7 +472,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(args, n, m),
+            "data": "synthetic", "config": {**workload_config(args, n, m),
+                                            "slots_used": solver.slots, "exec_form": solver.mode},
             "gteps": ops / sec / 1e9,
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -495,10 +496,6 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def solver_slots(solver):
-    return None
 
 
 if __name__ == "__main__":

@@ -162,6 +162,13 @@ class BatchSolver:
         gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
         return ("rounds", "cta", "fifo", "fifo-win")[m.value]
 
+    @property
+    def slots(self) -> int:
+        """Seeds in flight per wave (chosen from free HBM when slots=0)."""
+        m, s = C.c_int32(), C.c_int64()
+        gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
+        return int(s.value)
+
     def round_log(self) -> np.ndarray:
         """(rounds, 3) int64: frontier entries, arcs, device ns at round start
         for the last wave of the last solve (instrumentation)."""
