@@ -642,6 +642,95 @@ int orc_gradient_descent(int64_t n, const int64_t *off, const int64_t *tgt, cons
 }
 
 /* ------------------------------------------------------------------------ */
+/* per-seed parity of a GPU batch result against the reference x            */
+/* ------------------------------------------------------------------------ */
+
+/* The GPU batch returns x of seed i as (node, value) pairs:
+ * nodes[off[i] .. off[i] + cnt[i]), caller ids.  Compared against the dense
+ * reference x: l1 of the difference and of the reference (the l1 entry of
+ * error_norms, src/metrics.py:157-171) and the top-k ranking. */
+typedef struct {
+    const int64_t *off, *cnt;
+    const int32_t *nodes;
+    const double *vals;
+    double *l1d, *l1r;
+    int32_t *topk; /* bit 0: top-k lists identical; bit 1: identical up to
+                      swaps of entries whose reference values agree to 1e-12 */
+    int32_t k;
+} gpu_cmp;
+
+typedef struct { int64_t node; double val; } kv;
+
+static int kv_better(kv a, kv b) { return a.val > b.val || (a.val == b.val && a.node < b.node); }
+
+/* min-heap of the k best: root = worst kept */
+static void kv_sift(kv *h, int64_t n, int64_t i) {
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, w = i;
+        if (l < n && kv_better(h[w], h[l])) w = l;
+        if (r < n && kv_better(h[w], h[r])) w = r;
+        if (w == i) return;
+        kv t = h[i]; h[i] = h[w]; h[w] = t;
+        i = w;
+    }
+}
+
+static void kv_offer(kv *h, int64_t *n, int64_t k, kv c) {
+    if (*n < k) {
+        int64_t i = (*n)++;
+        h[i] = c;
+        while (i > 0) {  /* sift up: a parent must be worse than its children */
+            int64_t p = (i - 1) / 2;
+            if (!kv_better(h[p], h[i])) break;
+            kv t = h[i]; h[i] = h[p]; h[p] = t;
+            i = p;
+        }
+    } else if (k > 0 && kv_better(c, h[0])) {
+        h[0] = c;
+        kv_sift(h, *n, 0);
+    }
+}
+
+static int kv_cmp_desc(const void *a, const void *b) {
+    kv x = *(const kv *)a, y = *(const kv *)b;
+    return kv_better(x, y) ? -1 : (kv_better(y, x) ? 1 : 0);
+}
+
+/* scratch: n zeroed doubles (left zeroed on return) */
+static void cmp_seed(const gpu_cmp *C, int64_t i, const double *xr, int64_t n, double *scratch) {
+    const int64_t a = C->off[i], c = C->cnt[i];
+    for (int64_t j = 0; j < c; j++) scratch[C->nodes[a + j]] = C->vals[a + j];
+    double d = 0.0, s = 0.0;
+    for (int64_t u = 0; u < n; u++) {
+        d += fabs(scratch[u] - xr[u]);
+        s += fabs(xr[u]);
+    }
+    C->l1d[i] = d;
+    C->l1r[i] = s;
+    if (C->topk) {
+        const int64_t k = C->k;
+        kv *hr = malloc(sizeof(kv) * (k ? k : 1)), *hg = malloc(sizeof(kv) * (k ? k : 1));
+        int64_t nr = 0, ng = 0;
+        for (int64_t u = 0; u < n; u++)
+            if (xr[u] != 0.0) kv_offer(hr, &nr, k, (kv){u, xr[u]});
+        for (int64_t j = 0; j < c; j++)
+            if (C->vals[a + j] != 0.0) kv_offer(hg, &ng, k, (kv){C->nodes[a + j], C->vals[a + j]});
+        qsort(hr, nr, sizeof(kv), kv_cmp_desc);
+        qsort(hg, ng, sizeof(kv), kv_cmp_desc);
+        int strict = nr == ng, ties = nr == ng;
+        for (int64_t j = 0; j < nr && j < ng; j++) {
+            if (hr[j].node == hg[j].node) continue;
+            strict = 0;
+            const double va = xr[hr[j].node], vb = xr[hg[j].node];
+            if (!(fabs(va - vb) <= 1e-12 * fabs(va))) ties = 0;
+        }
+        C->topk[i] = strict | (ties << 1);
+        free(hr); free(hg);
+    }
+    for (int64_t j = 0; j < c; j++) scratch[C->nodes[a + j]] = 0.0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* batched CPU baseline: the reference's per-seed local_gd, many threads    */
 /* ------------------------------------------------------------------------ */
 
@@ -658,22 +747,26 @@ typedef struct {
     int64_t *out_sweeps, *out_ops, *out_pushes;
     int32_t *out_conv;
     double *out_xsum;
+    const gpu_cmp *cmp;  /* optional per-seed parity against a GPU result */
     int64_t next;
 } batch_job;
 
 /* One seed exactly as `local_gd(dataclasses.replace(sys, b=alpha*e_s))`
  * (src/local_solvers.py:428-470) or `local_sor(..., omega)` (:221-253) would
  * run it, including the per-solve O(n) allocations and per-sweep O(n) l1
- * scans of the reference. */
+ * scans of the reference.  The system's b is built once per thread and only
+ * its spike moves from seed to seed: the reference CLI builds systems outside
+ * its timed region (src/cli.py:152-156). */
 static void *batch_worker(void *arg) {
     batch_job *J = arg;
     int64_t n = J->n;
+    double *b = calloc(n ? n : 1, sizeof(double));
+    double *scratch = J->cmp ? calloc(n ? n : 1, sizeof(double)) : NULL;
     for (;;) {
         int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
         if (i >= J->n_seeds) break;
-        double *b = calloc(n, sizeof(double));
-        double *x = malloc(sizeof(double) * n);
-        double *r = malloc(sizeof(double) * n);
+        double *x = malloc(sizeof(double) * (n ? n : 1));
+        double *r = malloc(sizeof(double) * (n ? n : 1));
         b[J->seeds[i]] = J->alpha;
         orc_report rep;
         int64_t pushes = 0;
@@ -694,29 +787,50 @@ static void *batch_worker(void *arg) {
             orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
             for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
         }
+        b[J->seeds[i]] = 0.0;
         J->out_sweeps[i] = rep.sweeps;
         J->out_ops[i] = rep.total_ops;
         J->out_pushes[i] = pushes;
         J->out_conv[i] = rep.converged;
         if (J->out_xsum) J->out_xsum[i] = pw_sum(x, n, 0);
+        if (J->cmp) cmp_seed(J->cmp, i, x, n, scratch);
         orc_report_free(&rep);
-        free(b); free(x); free(r);
+        free(x); free(r);
     }
+    free(b);
+    free(scratch);
     return NULL;
+}
+
+static void run_threads(void *(*fn)(void *), void *job, int32_t n_threads) {
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, fn, job);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+}
+
+/* Optional GPU comparison: g_off == NULL -> none.  topk_k == 0 -> l1 only. */
+static gpu_cmp make_cmp(const int64_t *g_off, const int64_t *g_cnt, const int32_t *g_nodes,
+                        const double *g_vals, double *out_l1d, double *out_l1r,
+                        int32_t *out_topk, int32_t topk_k) {
+    gpu_cmp c = {g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, topk_k > 0 ? out_topk : NULL,
+                 topk_k};
+    return c;
 }
 
 int orc_batch_local(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
                     const double *theta, double alpha, int32_t method, double omega,
                     const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
                     int64_t *out_sweeps, int64_t *out_ops, int64_t *out_pushes,
-                    int32_t *out_conv, double *out_xsum) {
+                    int32_t *out_conv, double *out_xsum, const int64_t *g_off,
+                    const int64_t *g_cnt, const int32_t *g_nodes, const double *g_vals,
+                    double *out_l1d, double *out_l1r, int32_t *out_topk, int32_t topk_k) {
+    gpu_cmp C = make_cmp(g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, out_topk, topk_k);
     batch_job J = {n, off, tgt, w, theta, alpha, method, omega, 0.0, 0.0, seeds, n_seeds,
-                   max_sweeps, out_sweeps, out_ops, out_pushes, out_conv, out_xsum, 0};
-    if (n_threads < 1) n_threads = 1;
-    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
-    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, batch_worker, &J);
-    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
-    free(th);
+                   max_sweeps, out_sweeps, out_ops, out_pushes, out_conv, out_xsum,
+                   g_off ? &C : NULL, 0};
+    run_threads(batch_worker, &J, n_threads);
     return 0;
 }
 
@@ -726,17 +840,139 @@ int orc_batch_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const 
                        const double *theta, double bval, double mu, double L,
                        const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps,
                        int32_t n_threads, int64_t *out_sweeps, int64_t *out_ops,
-                       int32_t *out_conv, double *out_xsum) {
+                       int32_t *out_conv, double *out_xsum, const int64_t *g_off,
+                       const int64_t *g_cnt, const int32_t *g_nodes, const double *g_vals,
+                       double *out_l1d, double *out_l1r, int32_t *out_topk, int32_t topk_k) {
+    gpu_cmp C = make_cmp(g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, out_topk, topk_k);
     batch_job J = {n, off, tgt, w, theta, bval, 2, 1.0, mu, L, seeds, n_seeds, max_sweeps,
-                   out_sweeps, out_ops, NULL, out_conv, out_xsum, 0};
+                   out_sweeps, out_ops, NULL, out_conv, out_xsum, g_off ? &C : NULL, 0};
     int64_t *pushes = malloc(sizeof(int64_t) * (n_seeds ? n_seeds : 1));
     J.out_pushes = pushes;
-    if (n_threads < 1) n_threads = 1;
-    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
-    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, batch_worker, &J);
-    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
-    free(th);
+    run_threads(batch_worker, &J, n_threads);
     free(pushes);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* LocalGD-PPR at papers100M scale: rule weights, int32 targets             */
+/* ------------------------------------------------------------------------ */
+
+/* The same algorithm as orc_local_gd (src/local_solvers.py:428-470 with
+ * _apply_update_seq :267-292 and _filter_frontier :336-350) for the PPR
+ * system of make_ppr_system (src/systems.py:163-191), with the operator and
+ * thresholds evaluated from their rules instead of stored arrays:
+ *   arc_w[j] = fl(fl(1/d_u) * (1 - alpha))   (_gen_arc_weights "rw", :85-108)
+ *   theta_u  = fl(fl(eps*alpha) * d_u), +inf at d_u = 0   (_theta_vec, :157-160)
+ * which are the arrays' values bit for bit (tests/test_host.py).  Targets are
+ * int32 (n < 2^31) and the per-thread dense state is allocated once and
+ * reset over the nodes a seed wrote, so a 111 M-node graph needs ~3 GB per
+ * thread instead of the reference's ~50 GB of per-solve arrays.  The l1 /
+ * min-residual logs of the report are not produced (x, r, sweeps, ops and
+ * pushes are).  A checker only: never a timed baseline. */
+typedef struct {
+    int64_t n;
+    const int64_t *off;
+    const int32_t *tgt;
+    double alpha, beta, tcoeff;
+    const int64_t *seeds;
+    int64_t n_seeds, max_sweeps;
+    int64_t *out_sweeps, *out_ops, *out_pushes;
+    int32_t *out_conv;
+    const gpu_cmp *cmp;
+    int64_t next;
+} rule_job;
+
+static void *rule_worker(void *arg) {
+    rule_job *J = arg;
+    const int64_t n = J->n;
+    const size_t nn = n ? (size_t)n : 1;
+    double *x = calloc(nn, sizeof(double)), *r = calloc(nn, sizeof(double));
+    double *vals = malloc(sizeof(double) * nn);
+    uint8_t *cmark = calloc(nn, 1), *dmark = calloc(nn, 1);
+    int32_t *cand = malloc(sizeof(int32_t) * nn), *front = malloc(sizeof(int32_t) * nn);
+    int32_t *fbuf = malloc(sizeof(int32_t) * nn), *dirty = malloc(sizeof(int32_t) * nn);
+    double *scratch = J->cmp ? calloc(nn, sizeof(double)) : NULL;
+    for (;;) {
+        int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+        if (i >= J->n_seeds) break;
+        const int32_t s = (int32_t)J->seeds[i];
+        int64_t nd = 0;
+        r[s] = J->alpha;
+        dmark[s] = 1;
+        dirty[nd++] = s;
+        const int64_t ds = J->off[s + 1] - J->off[s];
+        const double ths = ds > 0 ? J->tcoeff * (double)ds : INFINITY;
+        int64_t fc = r[s] >= ths ? 1 : 0;
+        front[0] = s;
+        int64_t sweeps = 0, ops = 0, pushes = 0;
+        int32_t conv = 1;
+        while (fc) {
+            if (sweeps >= J->max_sweeps) { conv = 0; break; }
+            int64_t svol = 0;
+            for (int64_t q = 0; q < fc; q++) {
+                const int32_t u = front[q];
+                svol += J->off[u + 1] - J->off[u];
+                vals[q] = r[u];
+            }
+            for (int64_t q = 0; q < fc; q++) x[front[q]] += vals[q];
+            /* _apply_update_seq */
+            int64_t cc = 0;
+            for (int64_t q = 0; q < fc; q++) {
+                const int32_t u = front[q];
+                r[u] -= vals[q];
+                if (!cmark[u]) { cmark[u] = 1; cand[cc++] = u; }
+            }
+            for (int64_t q = 0; q < fc; q++) {
+                const int32_t u = front[q];
+                const double val = vals[q];
+                const double wu = (1.0 / (double)(J->off[u + 1] - J->off[u])) * J->beta;
+                for (int64_t j = J->off[u]; j < J->off[u + 1]; j++) {
+                    const int32_t v = J->tgt[j];
+                    r[v] += val * wu;
+                    if (!dmark[v]) { dmark[v] = 1; dirty[nd++] = v; }
+                    if (!cmark[v]) { cmark[v] = 1; cand[cc++] = v; }
+                }
+            }
+            /* _filter_frontier */
+            int64_t nf = 0;
+            for (int64_t q = 0; q < cc; q++) {
+                const int32_t u = cand[q];
+                cmark[u] = 0;
+                const int64_t du = J->off[u + 1] - J->off[u];
+                const double th = du > 0 ? J->tcoeff * (double)du : INFINITY;
+                if (r[u] >= th) fbuf[nf++] = u;
+            }
+            memcpy(front, fbuf, sizeof(int32_t) * nf);
+            ops += svol;
+            pushes += fc;
+            sweeps += 1;
+            fc = nf;
+        }
+        J->out_sweeps[i] = sweeps;
+        J->out_ops[i] = ops;
+        J->out_pushes[i] = pushes;
+        J->out_conv[i] = conv;
+        if (J->cmp) cmp_seed(J->cmp, i, x, n, scratch);
+        for (int64_t q = 0; q < nd; q++) {
+            const int32_t v = dirty[q];
+            x[v] = 0.0; r[v] = 0.0; dmark[v] = 0;
+        }
+    }
+    free(x); free(r); free(vals); free(cmark); free(dmark);
+    free(cand); free(front); free(fbuf); free(dirty); free(scratch);
+    return NULL;
+}
+
+int orc_batch_gd_rule(int64_t n, const int64_t *off, const int32_t *tgt, double alpha,
+                      double eps, const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps,
+                      int32_t n_threads, int64_t *out_sweeps, int64_t *out_ops,
+                      int64_t *out_pushes, int32_t *out_conv, const int64_t *g_off,
+                      const int64_t *g_cnt, const int32_t *g_nodes, const double *g_vals,
+                      double *out_l1d, double *out_l1r, int32_t *out_topk, int32_t topk_k) {
+    gpu_cmp C = make_cmp(g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, out_topk, topk_k);
+    rule_job J = {n, off, tgt, alpha, 1.0 - alpha, eps * alpha, seeds, n_seeds, max_sweeps,
+                  out_sweeps, out_ops, out_pushes, out_conv, g_off ? &C : NULL, 0};
+    run_threads(rule_worker, &J, n_threads);
     return 0;
 }
 
@@ -756,6 +992,7 @@ typedef struct {
     int64_t *out_sweeps, *out_ops;
     int32_t *out_conv;
     double *out_fsum;
+    const gpu_cmp *cmp;  /* against f_hat */
     int64_t next;
 } hk_job;
 
@@ -764,6 +1001,8 @@ static void *hk_worker(void *arg) {
     const int64_t dim = (J->n_stages + 1) * J->n;
     double *v = malloc(sizeof(double) * (dim ? dim : 1));
     double *r = malloc(sizeof(double) * (dim ? dim : 1));
+    double *f = (J->out_fsum || J->cmp) ? malloc(sizeof(double) * (J->n ? J->n : 1)) : NULL;
+    double *scratch = J->cmp ? calloc(J->n ? J->n : 1, sizeof(double)) : NULL;
     for (;;) {
         int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
         if (i >= J->n_seeds) break;
@@ -776,33 +1015,37 @@ static void *hk_worker(void *arg) {
         J->out_sweeps[i] = rep.sweeps;
         J->out_ops[i] = rep.total_ops;
         J->out_conv[i] = rep.converged;
-        if (J->out_fsum) { /* sum of f_hat = e^-tau * sum_k v_k (stage order per node) */
+        if (f) { /* f_hat = e^-tau * sum_k v_k (stage order per node, back_transform) */
             const double e = exp(-J->tau);
             double s = 0.0;
             for (int64_t u = 0; u < J->n; u++) {
                 double acc = v[u];
                 for (int64_t k = 1; k <= J->n_stages; k++) acc += v[k * J->n + u];
-                s += e * acc;
+                f[u] = e * acc;
+                s += f[u];
             }
-            J->out_fsum[i] = s;
+            if (J->out_fsum) J->out_fsum[i] = s;
+            if (J->cmp) cmp_seed(J->cmp, i, f, J->n, scratch);
         }
         orc_report_free(&rep);
     }
     free(v);
     free(r);
+    free(f);
+    free(scratch);
     return NULL;
 }
 
 int orc_batch_hk(int64_t n, int64_t n_stages, const int64_t *off, const int64_t *tgt,
                  const double *base_w, const double *stage_w, const double *theta, double tau,
                  const int64_t *seeds, int64_t n_seeds, int64_t max_sweeps, int32_t n_threads,
-                 int64_t *out_sweeps, int64_t *out_ops, int32_t *out_conv, double *out_fsum) {
+                 int64_t *out_sweeps, int64_t *out_ops, int32_t *out_conv, double *out_fsum,
+                 const int64_t *g_off, const int64_t *g_cnt, const int32_t *g_nodes,
+                 const double *g_vals, double *out_l1d, double *out_l1r, int32_t *out_topk,
+                 int32_t topk_k) {
+    gpu_cmp C = make_cmp(g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, out_topk, topk_k);
     hk_job J = {n, n_stages, off, tgt, base_w, stage_w, theta, tau, seeds, n_seeds, max_sweeps,
-                out_sweeps, out_ops, out_conv, out_fsum, 0};
-    if (n_threads < 1) n_threads = 1;
-    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
-    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, hk_worker, &J);
-    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
-    free(th);
+                out_sweeps, out_ops, out_conv, out_fsum, g_off ? &C : NULL, 0};
+    run_threads(hk_worker, &J, n_threads);
     return 0;
 }

@@ -216,10 +216,39 @@ def gradient_descent(sys, max_sweeps: int = 10_000) -> dict:
     return out
 
 
+def _cmp_args(gpu, k: int, topk: int):
+    """ctypes arguments of the optional per-seed GPU comparison (x as sparse
+    (node, value) segments, caller ids) and the arrays it fills."""
+    if gpu is None:
+        nul = C.c_void_p()
+        return [nul] * 4 + [nul, nul, nul, C.c_int32(0)], None
+    g_off = _arr64(gpu.x_offset)
+    g_cnt = _arr64(gpu.x_count)
+    g_nodes = np.ascontiguousarray(gpu.x_nodes, dtype=np.int32)
+    g_vals = _arrf(gpu.x_vals)
+    l1d, l1r, tk = np.zeros(k), np.zeros(k), np.zeros(k, np.int32)
+    keep = (g_off, g_cnt, g_nodes, g_vals)
+    args = [_p(g_off, C.c_int64), _p(g_cnt, C.c_int64), _p(g_nodes, C.c_int32), _p(g_vals),
+            _p(l1d), _p(l1r), _p(tk, C.c_int32), C.c_int32(topk)]
+    return args, (l1d, l1r, tk, keep)
+
+
+def _cmp_out(out: dict, res) -> dict:
+    if res is not None:
+        l1d, l1r, tk, _ = res
+        out["x_l1_diff"], out["x_l1_ref"] = l1d, l1r
+        out["x_l1_rel"] = l1d / np.where(l1r > 0, l1r, 1.0)
+        out["topk_identical"] = (tk & 1).astype(bool)
+        out["topk_identical_up_to_ties"] = (tk & 2).astype(bool)
+    return out
+
+
 def batch_local_gd(g, alpha: float, eps: float, seeds, threads: int,
                    max_sweeps: int = 1_000_000, arc_w=None, theta=None, method: str = "local-gd",
-                   omega: float = 1.0) -> dict:
-    """Per-seed reference local_gd (or local_sor) over many host threads (CPU baseline)."""
+                   omega: float = 1.0, gpu=None, topk: int = 100, xsum: bool = True) -> dict:
+    """Per-seed reference local_gd (or local_sor) over many host threads (CPU
+    baseline).  gpu: a BatchOutput of the same seeds -> per-seed l1 of
+    x_gpu - x_ref, l1 of x_ref and the top-k ranking check."""
     from paper_2410_21634_b200.systems import arc_weights_for, theta_vector
     off, tg = _arr64(g.offsets), _arr64(g.targets)
     w = _arrf(arc_w if arc_w is not None else arc_weights_for(g, 1.0 - alpha, "rw"))
@@ -229,16 +258,40 @@ def batch_local_gd(g, alpha: float, eps: float, seeds, threads: int,
     sw, ops, pu = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k, np.int64)
     cv = np.zeros(k, np.int32)
     xs = np.zeros(k)
+    cargs, cres = _cmp_args(gpu, k, topk)
     lib().orc_batch_local(C.c_int64(g.n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th),
                              C.c_double(alpha), C.c_int32(1 if method == "local-sor" else 0),
                              C.c_double(omega), _p(sd, C.c_int64), C.c_int64(k),
                              C.c_int64(max_sweeps), C.c_int32(threads), _p(sw, C.c_int64),
-                             _p(ops, C.c_int64), _p(pu, C.c_int64), _p(cv, C.c_int32), _p(xs))
-    return {"sweeps": sw, "total_ops": ops, "pushes": pu, "converged": cv.astype(bool), "xsum": xs}
+                             _p(ops, C.c_int64), _p(pu, C.c_int64), _p(cv, C.c_int32),
+                             _p(xs) if xsum else C.c_void_p(), *cargs)
+    return _cmp_out({"sweeps": sw, "total_ops": ops, "pushes": pu, "converged": cv.astype(bool),
+                     "xsum": xs}, cres)
+
+
+def batch_gd_rule(n: int, offsets, targets32, alpha: float, eps: float, seeds, threads: int,
+                  max_sweeps: int = 1_000_000, gpu=None, topk: int = 100) -> dict:
+    """Reference LocalGD-PPR per seed with the operator / thresholds evaluated
+    from their rules and int32 targets (papers100M scale; no l1 logs): a
+    checker for the device batch, never a timed baseline."""
+    off = _arr64(offsets)
+    tg = np.ascontiguousarray(targets32, dtype=np.int32)
+    sd = _arr64(seeds)
+    k = sd.shape[0]
+    sw, ops, pu = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k, np.int64)
+    cv = np.zeros(k, np.int32)
+    cargs, cres = _cmp_args(gpu, k, topk)
+    lib().orc_batch_gd_rule(C.c_int64(n), _p(off, C.c_int64), _p(tg, C.c_int32), C.c_double(alpha),
+                            C.c_double(eps), _p(sd, C.c_int64), C.c_int64(k), C.c_int64(max_sweeps),
+                            C.c_int32(threads), _p(sw, C.c_int64), _p(ops, C.c_int64),
+                            _p(pu, C.c_int64), _p(cv, C.c_int32), *cargs)
+    return _cmp_out({"sweeps": sw, "total_ops": ops, "pushes": pu, "converged": cv.astype(bool)},
+                    cres)
 
 
 def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, L: float,
-                   problem: str = "ppr", max_sweeps: int | None = None) -> dict:
+                   problem: str = "ppr", max_sweeps: int | None = None, gpu=None,
+                   topk: int = 100) -> dict:
     """Per-seed reference local_ch over many host threads (CPU baseline of
     the LocalCH batch): PPR (b = alpha e_s) or Katz (b = e_s, w = alpha)."""
     from paper_2410_21634_b200.systems import arc_weights_for, theta_vector
@@ -256,15 +309,18 @@ def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, 
     sw, ops = np.zeros(k, np.int64), np.zeros(k, np.int64)
     cv = np.zeros(k, np.int32)
     xs = np.zeros(k)
+    cargs, cres = _cmp_args(gpu, k, topk)
     lib().orc_batch_local_ch(C.c_int64(g.n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th),
                              C.c_double(bval), C.c_double(mu), C.c_double(L), _p(sd, C.c_int64),
                              C.c_int64(k), C.c_int64(max_sweeps), C.c_int32(threads),
-                             _p(sw, C.c_int64), _p(ops, C.c_int64), _p(cv, C.c_int32), _p(xs))
-    return {"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "xsum": xs}
+                             _p(sw, C.c_int64), _p(ops, C.c_int64), _p(cv, C.c_int32), _p(xs),
+                             *cargs)
+    return _cmp_out({"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "xsum": xs},
+                    cres)
 
 
 def batch_local_hk(g, tau: float, eps: float, seeds, threads: int,
-                   max_sweeps: int = 1_000_000) -> dict:
+                   max_sweeps: int = 1_000_000, gpu=None, topk: int = 100) -> dict:
     """Per-seed reference local_hk over many host threads (CPU baseline of
     the heat-kernel batch); dense (N+1) n state per thread as the reference."""
     from paper_2410_21634_b200.systems import make_hk_system
@@ -279,12 +335,13 @@ def batch_local_hk(g, tau: float, eps: float, seeds, threads: int,
     sw, ops = np.zeros(k, np.int64), np.zeros(k, np.int64)
     cv = np.zeros(k, np.int32)
     fs = np.zeros(k)
+    cargs, cres = _cmp_args(gpu, k, topk)
     lib().orc_batch_hk(C.c_int64(g.n), C.c_int64(N), _p(off, C.c_int64), _p(tg, C.c_int64),
                        _p(base_w), _p(stage_w), _p(th), C.c_double(tau), _p(sd, C.c_int64),
                        C.c_int64(k), C.c_int64(max_sweeps), C.c_int32(threads), _p(sw, C.c_int64),
-                       _p(ops, C.c_int64), _p(cv, C.c_int32), _p(fs))
-    return {"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "fsum": fs,
-            "stage_count": N}
+                       _p(ops, C.c_int64), _p(cv, C.c_int32), _p(fs), *cargs)
+    return _cmp_out({"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "fsum": fs,
+                     "stage_count": N}, cres)
 
 
 def pairwise_sum(a, take_abs: bool = False) -> float:

@@ -130,3 +130,60 @@ def test_oracle_batch_local_hk_matches_single(small):
     assert (out["sweeps"] == small[f"{k}/sweeps"]).all()
     assert (out["total_ops"] == small[f"{k}/total_ops"]).all()
     np.testing.assert_allclose(out["fsum"], small[f"{k}/f_hat"].sum(), rtol=1e-12)
+
+
+class _Sparse:
+    """A BatchOutput-shaped container of per-seed sparse x (test helper)."""
+
+    def __init__(self, xs):
+        nodes, vals, off, cnt = [], [], [], []
+        pos = 0
+        for x in xs:
+            nz = np.flatnonzero(x)
+            nodes.append(nz.astype(np.int32))
+            vals.append(x[nz])
+            off.append(pos)
+            cnt.append(nz.size)
+            pos += nz.size
+        self.x_offset, self.x_count = np.array(off, np.int64), np.array(cnt, np.int64)
+        self.x_nodes = np.concatenate(nodes) if nodes else np.empty(0, np.int32)
+        self.x_vals = np.concatenate(vals) if vals else np.empty(0)
+
+
+def test_oracle_x_parity_against_reference_vectors(cora):
+    """The per-seed comparison (l1 of x_gpu - x_ref, top-k ranking) measures 0
+    and identical rankings on the reference's own x (golden cora batch), and
+    sees a perturbation / a swapped top-2."""
+    g = golden_graph(cora, "cora")
+    seeds, xs = cora["seeds"], cora["batch/x"]
+    out = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=4, gpu=_Sparse(xs))
+    assert (out["x_l1_diff"] == 0).all() and out["topk_identical"].all()
+    np.testing.assert_allclose(out["x_l1_ref"], [np.abs(x).sum() for x in xs], rtol=1e-12)
+    bad = [x.copy() for x in xs]
+    bad[3][np.argmax(bad[3])] *= 1 + 1e-6
+    top2 = np.argsort(-bad[5])[:2]
+    bad[5][top2] = bad[5][top2[::-1]]
+    out = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=4, gpu=_Sparse(bad))
+    assert out["x_l1_rel"][3] > 1e-8 and out["topk_identical"][3]
+    assert not out["topk_identical"][5] and not out["topk_identical_up_to_ties"][5]
+    assert out["x_l1_diff"][0] == 0
+
+
+def test_oracle_rule_mode_is_the_reference_local_gd(cora, pa):
+    """orc_batch_gd_rule (int32 targets, rule weights / thresholds, dirty-list
+    reset: the papers100M checker) == the reference per seed: x bitwise,
+    sweeps, ops, pushes (golden cora batch), and == the array form on pa2000."""
+    g = golden_graph(cora, "cora")
+    seeds = cora["seeds"]
+    out = O.batch_gd_rule(g.n, g.offsets, g.targets.astype(np.int32), 0.1, 1e-6, seeds, 3,
+                          gpu=_Sparse(cora["batch/x"]))
+    assert np.array_equal(out["sweeps"], cora["batch/sweeps"])
+    assert np.array_equal(out["total_ops"], cora["batch/total_ops"])
+    assert np.array_equal(out["pushes"], cora["batch/pushes"])
+    assert (out["x_l1_diff"] == 0).all() and out["topk_identical"].all()
+    gp = golden_graph(pa, "pa2000")
+    sd = sample_sources(gp, 40, seed=3)
+    a = O.batch_local_gd(gp, 0.15, 1e-7, sd, threads=2)
+    b = O.batch_gd_rule(gp.n, gp.offsets, gp.targets.astype(np.int32), 0.15, 1e-7, sd, 2)
+    for f in ("sweeps", "total_ops", "pushes", "converged"):
+        assert np.array_equal(a[f], b[f]), f
