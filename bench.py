@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--eps", type=float, default=1e-7)
     p.add_argument("--seeds", type=int, default=1024, help="seeds per GPU per step")
     p.add_argument("--slots", type=int, default=0, help="seeds in flight (0 = auto)")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--graph-seed", type=int, default=0)
@@ -140,14 +140,20 @@ def dist_env():
     return rank, world, local
 
 
-def make_graph(shape, seed, device):
-    """GPU-built R-MAT graph: (DeviceGraph, host CsrGraph-like with degrees)."""
-    from paper_2410_21634_b200.device import DeviceGraph
+def make_graph(shape, seed, device, native=True):
+    """GPU-built R-MAT graph: (DeviceGraph, row, col, host row_ptr).  native=False
+    (the reference arm) draws it with torch ops only and returns no DeviceGraph,
+    so that process never loads libgdiff."""
     from paper_2410_21634_b200.gen import rmat_csr_device, rmat_csr_device_big
 
     n, m = SHAPES[shape]
     big = 2 * m > (1 << 30)  # beyond a single device sort
-    row, col = (rmat_csr_device_big if big else rmat_csr_device)(n, m, seed=seed, device=device)
+    row, col = (rmat_csr_device_big if big else rmat_csr_device)(n, m, seed=seed, device=device,
+                                                                  native=native)
+    if not native:
+        return None, row, col, row.cpu().numpy()
+    from paper_2410_21634_b200.device import DeviceGraph
+
     dg = DeviceGraph.from_device(n, row, col, device=device)
     row_h = row.cpu().numpy()
     return dg, row, col, row_h
@@ -159,7 +165,11 @@ class _HostGraph:
         self.degrees = np.diff(offsets)
 
 
-def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, ch=None):
+def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, ch=None,
+                  gpu=None):
+    """The reference algorithm per seed on `threads` host threads (oracle/).
+    gpu: a BatchOutput of the same seeds to compare x against (parity pass,
+    not timed by the callers)."""
     from oracle import oracle as O
 
     t0 = time.perf_counter()
@@ -168,16 +178,16 @@ def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, 
 
         per = 25 * (ch["n_stages"] + 1) * hg.n  # v, r, queue, marks per thread (reference layout)
         th = max(1, min(threads, int(0.5 * psutil.virtual_memory().available // max(per, 1))))
-        out = O.batch_local_hk(hg, ch["tau"], eps, seeds, th)
+        out = O.batch_local_hk(hg, ch["tau"], eps, seeds, th, gpu=gpu)
         out["pushes"] = np.zeros_like(out["total_ops"])
         out["threads"] = th
     elif method == "local-ch":
         out = O.batch_local_ch(hg, alpha, eps, seeds, threads, ch["mu"], ch["L"],
-                               problem=ch["problem"], max_sweeps=ch["max_sweeps"])
+                               problem=ch["problem"], max_sweeps=ch["max_sweeps"], gpu=gpu)
         out["pushes"] = np.zeros_like(out["total_ops"])
     else:
         out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w,
-                               theta=hg.theta, method=method, omega=omega)
+                               theta=hg.theta, method=method, omega=omega, gpu=gpu, xsum=False)
     return out, time.perf_counter() - t0
 
 
@@ -247,8 +257,8 @@ def run_reference(args):
         return
     threads = len(os.sched_getaffinity(0))
     n, m = SHAPES[args.shape]
-    if torch.cuda.is_available():  # input synthesis only; the timed path is CPU
-        _, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
+    if torch.cuda.is_available():  # input synthesis only (torch ops); the timed path is CPU
+        _, row, col, row_h = make_graph(args.shape, args.graph_seed, local, native=False)
         args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
         hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
         if args.method == "local-hk":
@@ -270,13 +280,15 @@ def run_reference(args):
     steps_total = args.steps + args.warmup
     allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
     batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
-    # each step: a bounded prefix of that step's batch (about 3 s of CPU work)
-    _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][:threads], threads, args.method,
-                          args.omega, args.ch)
+    # each step: a bounded sample of that step's batch (about 3 s of CPU work),
+    # taken with a uniform stride so it spans the degree-ranked batch
+    _, dt = cpu_reference(hg, args.alpha, args.eps, batches[0][::max(1, args.seeds // threads)],
+                          threads, args.method, args.omega, args.ch)
     per_step = int(min(args.seeds, max(threads, threads * 3.0 / max(dt, 1e-3))))
+    stride = max(1, args.seeds // per_step)
     times, ops, done = [], 0, 0
     for k in range(steps_total):
-        sl = batches[k][:per_step]
+        sl = batches[k][::stride][:per_step]
         out, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega,
                                 args.ch)
         if k >= args.warmup:
@@ -293,8 +305,9 @@ def run_reference(args):
         "config": workload_config(args, n, m),
         "gteps": ops / tot / 1e9,
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
-                         "sample": f"first {per_step} seeds of each step's sample_sources batch, "
-                                   f"reference {args.method.replace('-', '_')} restated in C "
+                         "sample": f"{len(sl)} seeds per step (every {stride}th of the step's "
+                                   f"{args.seeds}-seed sample_sources batch), reference "
+                                   f"{args.method.replace('-', '_')} restated in C "
                                    "(oracle/), per-seed O(n) "
                                    "state as in the reference, one seed per thread"},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -384,6 +397,7 @@ def main():
     solved = 0
     kern_ms = 0.0
     launches = 0
+    amb_total = 0
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.warmup, steps_total):
@@ -391,6 +405,7 @@ def main():
             gather(res)
             kern_ms += solver.last_kernel_ms
             launches += res["kernel_launches"]
+            amb_total += res["n_ambiguous"]
             ops_d += res["total_ops"].sum()
             pushes_d += res["pushes"].sum()
             solved += len(batches[k])
@@ -450,8 +465,12 @@ def main():
         pos = 0
         ref_sweeps, ref_ops = [], []
         used = threads
-        while spent < args.cpu_seconds and pos < len(batches[args.warmup]):
-            sl = batches[args.warmup][pos:pos + chunk]
+        # the sample walks the degree-ranked batch with a stride (chunks taken
+        # in stride order) so it spans low- and high-degree seeds
+        stride = 8
+        order = np.concatenate([batches[args.warmup][o::stride] for o in range(stride)])
+        while spent < args.cpu_seconds and pos < len(order):
+            sl = order[pos:pos + chunk]
             o, dt = cpu_reference(hg, args.alpha, args.eps, sl, threads, args.method, args.omega,
                                   args.ch)
             spent += dt
@@ -463,17 +482,29 @@ def main():
         res = solver.solve(np.asarray(sample, dtype=np.int64))
         parity = bool(np.array_equal(np.concatenate(ref_ops), res.total_ops)
                       and np.array_equal(np.concatenate(ref_sweeps), res.sweeps))
+        # x parity of the same seeds (a second, untimed reference pass that
+        # compares every seed's x against the GPU's sparse x in C)
+        px, _ = cpu_reference(hg, args.alpha, args.eps, np.asarray(sample, dtype=np.int64),
+                              threads, args.method, args.omega, args.ch, gpu=res)
         cpu = {"value": len(sample) / spent, "unit": "solves/s", "cores": used, "kind": "port",
-               "sample": f"first {len(sample)} seeds of the first timed batch, reference "
-                         f"{args.method.replace('-', '_')} restated in C (oracle/), one seed per thread",
-               "parity_sweeps_ops_identical": parity}
+               "sample": f"{len(sample)} seeds (every {stride}th of the first timed batch), "
+                         f"reference {args.method.replace('-', '_')} restated in C (oracle/), "
+                         "one seed per thread",
+               "parity_sweeps_ops_identical": parity,
+               "x_l1_rel_max": float(px["x_l1_rel"].max()),
+               "x_l1_rel_tolerance": 1e-9,
+               "topk": 100,
+               "topk_identical": int(px["topk_identical"].sum()),
+               "topk_identical_up_to_ties": int(px["topk_identical_up_to_ties"].sum()),
+               "ambiguous_seeds_resolved": solver.last_ambiguous}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {**workload_config(args, n, m),
-                                            "slots_used": solver.slots, "exec_form": solver.mode},
+            "data": "synthetic", "config": workload_config(args, n, m),
+            "slots_used": solver.slots, "exec_form": solver.mode,
+            "ambiguous_seeds": amb_total,
             "gteps": ops / sec / 1e9,
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -217,7 +217,10 @@ typedef struct {
     double theta_coeff;      /* eps / (2 (N+1) vol); theta = fl(coeff * d) */
     int32_t want_r;          /* 1: also return each seed's final r as a sparse vector
                                 (GD_M_LOCAL_GD / GD_M_LOCAL_CH / GD_M_LOCAL_SOR) */
-    int32_t reserved;
+    int32_t exact_all;       /* 1: re-solve EVERY seed on the bit-exact path after the
+                                batch (x, r bit-identical with the reference; the
+                                near-threshold detector does this for flagged seeds
+                                only).  Not for GD_M_HK / GD_M_LOCAL_SOR. */
 } gd_batch_params;
 
 typedef struct {
@@ -229,6 +232,13 @@ typedef struct {
     double *x_vals;
     int64_t x_total;              /* filled after synchronisation */
     int64_t kernel_launches;      /* kernels this solve launched */
+    /* near-threshold detector of the atomic-scatter batches: ambiguous[i] = 1
+       when one of seed i's batched updates landed within 2^-36 (relative) of
+       its threshold, where the scatter order could decide frontier
+       membership; such seeds were re-solved on the bit-exact path (their
+       results above are the reference's bit for bit) */
+    int32_t *ambiguous;           /* device, n_seeds entries */
+    int64_t n_ambiguous;
 } gd_batch_result;
 
 int gd_batch_create(const gd_graph *g, const gd_batch_params *p, gd_batch **out);
@@ -263,6 +273,9 @@ int gd_batch_r_device(const gd_batch *b, int64_t **r_offset, int64_t **r_count,
 int gd_batch_fetch_r_host(gd_batch *b, int64_t n_seeds, int64_t *r_offset, int64_t *r_count,
                           int32_t *r_nodes, double *r_vals, int64_t r_cap, int64_t *r_total,
                           void *stream);
+/* Seeds of the last solve that the near-threshold detector flagged and the
+ * bit-exact path re-solved (see gd_batch_result.ambiguous). */
+int gd_batch_last_ambiguous(const gd_batch *b, int64_t *count);
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);

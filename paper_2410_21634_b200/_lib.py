@@ -59,14 +59,15 @@ class BatchParams(C.Structure):
                 ("relabel", C.c_int32), ("problem", C.c_int32), ("omega", C.c_double),
                 ("mu", C.c_double), ("L", C.c_double), ("tau", C.c_double),
                 ("n_stages", C.c_int64), ("stage_w", _f64p), ("theta_coeff", C.c_double),
-                ("want_r", C.c_int32), ("reserved", C.c_int32)]
+                ("want_r", C.c_int32), ("exact_all", C.c_int32)]
 
 
 class BatchResult(C.Structure):
     _fields_ = [("sweeps", _i64p), ("total_ops", _i64p), ("pushes", _i64p),
                 ("support", _i64p), ("converged", _i32p), ("x_offset", _i64p),
                 ("x_count", _i64p), ("x_nodes", _i32p), ("x_vals", _f64p),
-                ("x_total", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("x_total", C.c_int64), ("kernel_launches", C.c_int64),
+                ("ambiguous", _i32p), ("n_ambiguous", C.c_int64)]
 
 
 # name -> (restype, argtypes); mirrors include/gdiff.h
@@ -109,6 +110,7 @@ SIGNATURES = {
     "gd_batch_fetch_host": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _i64p, _i32p, _i64p,
                                       _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
     "gd_batch_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
+    "gd_batch_last_ambiguous": (C.c_int, [C.c_void_p, _i64p]),
     "gd_batch_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), _i64p]),
     "gd_batch_r_device": (C.c_int, [C.c_void_p, C.POINTER(_i64p), C.POINTER(_i64p), C.POINTER(_i32p),
                                     C.POINTER(_f64p), _i64p]),

@@ -94,7 +94,8 @@ class BatchSolver:
                  max_sweeps: int = 1_000_000, frontier_cap: int = 0, out_cap: int = 0,
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
-                 L: float | None = None, hk: dict | None = None, want_r: bool = False):
+                 L: float | None = None, hk: dict | None = None, want_r: bool = False,
+                 exact_all: bool = False):
         if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
         if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
@@ -129,7 +130,8 @@ class BatchSolver:
                             omega=float(omega), mu=float(mu or 0.0), L=float(L or 0.0),
                             tau=float(hk.get("tau", 0.0)), n_stages=int(hk.get("n_stages", 0)),
                             stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)),
-                            want_r=int(bool(want_r) and method != "local-hk"))
+                            want_r=int(bool(want_r) and method != "local-hk"),
+                            exact_all=int(bool(exact_all)))
         self.want_r = bool(want_r) and method != "local-hk"
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
@@ -152,6 +154,14 @@ class BatchSolver:
         ms = C.c_double()
         gdl.check(self.lib.gd_batch_last_kernel_ms(self.handle, C.byref(ms)))
         return ms.value
+
+    @property
+    def last_ambiguous(self) -> int:
+        """Seeds of the last solve flagged by the near-threshold detector (an
+        update within 2^-36 of its threshold) and re-solved bit-exactly."""
+        c = C.c_int64()
+        gdl.check(self.lib.gd_batch_last_ambiguous(self.handle, C.byref(c)))
+        return int(c.value)
 
     @property
     def mode(self) -> str:
@@ -202,6 +212,7 @@ class BatchSolver:
             "x_count": view(res.x_count, k, "<i8"), "x_nodes": view(res.x_nodes, max(tot, 1), "<i4")[:tot],
             "x_vals": view(res.x_vals, max(tot, 1), "<f8")[:tot], "x_total": tot,
             "kernel_launches": int(res.kernel_launches),
+            "ambiguous": view(res.ambiguous, k, "<i4"), "n_ambiguous": int(res.n_ambiguous),
         }
 
     def solve(self, seeds, x_cap: int | None = None, stream=None, out: dict | None = None) -> BatchOutput:

@@ -69,7 +69,8 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
                       int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
-                      cudaStream_t st, const RPool *rp);
+                      cudaStream_t st, const RPool *rp, int32_t *amb,
+                      unsigned long long *amb_cnt);
 int fifo_batch_slots(const FifoBatchState *F);
 struct SorWinState;  // sor_win.cu: LocalSOR/GS seeds in exact windows, one CTA per seed
 SorWinState *sorwin_create(const gd_graph *G, int max_ctas);
@@ -88,7 +89,8 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
                    const int32_t *perm, const int32_t *inv, int64_t *sweeps, int64_t *ops,
                    int64_t *pushes, int64_t *support, int32_t *conv, int64_t *xoff,
                    int64_t *xcnt, int32_t *xnodes, double *xvals, int64_t xcap,
-                   unsigned long long *cursor, cudaStream_t st);
+                   unsigned long long *cursor, int32_t *amb, unsigned long long *amb_cnt,
+                   cudaStream_t st);
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
                     int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
@@ -151,6 +153,7 @@ struct RoundArgs {
     unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
     unsigned long long *s_ops, *s_pushes, *s_negz, *s_pvol;
     int32_t *s_last, *s_conv;
+    int32_t *s_amb;       // per slot: near-threshold update seen (common.cuh)
     int32_t *overflow;
     const int32_t *perm;  // caller id -> working id (nullable)
     unsigned long long *cursor;  // output pool allocation
@@ -654,7 +657,9 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                 const double th = theta_deg(A.tcoeff, dv[q]);
                 const bool first = valid[q] && ob == 0;
                 const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
-                const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
+                const double nw = __dadd_rn(old[q], c[q]);
+                const bool cross = valid[q] && old[q] < th && nw >= th;
+                if (valid[q] && near_theta(nw, th)) A.s_amb[k[q]] = 1;
                 block_count(first, k[q], 1u, S.touch);
                 if (first)  // first write of this r word: remember its 32 B sector
                     atomicOr(mapn + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
@@ -692,6 +697,7 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.s_pvol[k] = 0;
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
+    A.s_amb[k] = 0;
     int32_t d = A.g.deg[s];
     A.sfill[k] = 0ULL;
     if (alpha >= theta_deg(A.tcoeff, d)) {
@@ -715,6 +721,8 @@ struct OutArgs {
     const int32_t *inv;  // working id -> caller id (nullable)
     double xscale;       // x out = fl(xscale * x) (heat kernel: e^-tau; else 1)
     int hk;
+    int32_t *amb;                 // per seed: near-threshold flag
+    unsigned long long *amb_cnt;  // flagged seeds
 };
 
 // grid (CHUNKS, slots): copy x over the pushed list out (caller ids) and zero
@@ -765,6 +773,8 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
         O.support[si] = O.hk ? -1 : (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
         O.xoff[si] = b;
         O.xcnt[si] = pc;
+        O.amb[si] = A.s_amb[k];
+        if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
         if (pc == 0) A.r[off + A.seed[k]] = 0.0;  // an inactive seed keeps r = alpha
     }
 }
@@ -964,7 +974,10 @@ struct gd_batch {
     int grid;
     int64_t fcap, xcap;
     DBuf<double> x, r, fcval;
-    DBuf<int32_t> pushed, seed, s_last, s_conv, overflow;
+    DBuf<int32_t> pushed, seed, s_last, s_conv, s_amb, overflow;
+    DBuf<int32_t> amb;               // per seed: near-threshold flag of the last solve
+    DBuf<unsigned long long> amb_cnt;
+    int64_t last_amb = 0;            // seeds re-solved on the exact path
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
     DBuf<int64_t> ukey, uarc, skey, sarc, frow, slot_base;
     DBuf<unsigned long long> scnt, sfill, cctr;
@@ -1044,7 +1057,7 @@ struct gd_batch {
         A.rlog = rlog.p; A.rlog_cap = RLOG_CAP;
         A.secmap = secmap.p; A.smw = smw;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
-        A.s_last = s_last.p; A.s_conv = s_conv.p;
+        A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
         A.cursor = cursor.p;
@@ -1102,8 +1115,9 @@ struct gd_batch {
 static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cudaStream_t st) {
     const size_t ns = n_seeds ? (size_t)n_seeds : 1;
     B->sweeps.ensure(ns); B->ops.ensure(ns); B->pushes.ensure(ns); B->support.ensure(ns);
-    B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns);
+    B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns); B->amb.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
+    GD_CUDA(cudaMemsetAsync(B->amb_cnt.p, 0, sizeof(unsigned long long), st));
     B->hs.streamed = 0;
     RPool rp{};
     if (B->want_r()) {
@@ -1122,6 +1136,8 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             B->ev.push_back(e1);
         }
         GD_CUDA(cudaMemsetAsync(B->support.p, 0xFF, sizeof(int64_t) * ns, st));  // not tracked
+        // the FIFO replay is bit-exact: nothing is ever ambiguous
+        GD_CUDA(cudaMemsetAsync(B->amb.p, 0, sizeof(int32_t) * ns, st));
         GD_CUDA(cudaEventRecord(B->ev[0], st));
         if (n_seeds && B->sorwin && !rpp)
             sorwin_run(B->sorwin, B->G, B->p, d_seeds, n_seeds, B->sweeps.p, B->ops.p,
@@ -1151,7 +1167,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         cta_batch_run(B->cta, B->work(), B->colp.p, B->p.alpha, B->p.eps, B->p.max_sweeps, d_seeds,
                       n_seeds, B->R ? B->perm.p : nullptr, B->R ? B->inv.p : nullptr, B->sweeps.p,
                       B->ops.p, B->pushes.p, B->support.p, B->conv.p, B->xoff.p, B->xcnt.p,
-                      B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p, st);
+                      B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p, B->amb.p, B->amb_cnt.p, st);
         GD_CUDA(cudaEventRecord(B->ev[1], st));
         GD_CUDA(cudaStreamSynchronize(st));
         float f = 0.f;
@@ -1169,7 +1185,8 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         signed_batch_run(B->sgn, B->work(), B->p, d_seeds, n_seeds, B->R ? B->perm.p : nullptr,
                          B->R ? B->inv.p : nullptr, B->sweeps.p, B->ops.p, B->pushes.p,
                          B->support.p, B->conv.p, B->xoff.p, B->xcnt.p, B->xnodes.p, B->xvals.p,
-                         B->xcap, B->cursor.p, B->ev, &B->last_ms, &B->last_launches, st, rpp);
+                         B->xcap, B->cursor.p, B->ev, &B->last_ms, &B->last_launches, st, rpp,
+                         B->amb.p, B->amb_cnt.p);
         return;
     }
     const int64_t waves = (n_seeds + B->slots - 1) / B->slots;
@@ -1180,7 +1197,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     }
     OutArgs O{B->sweeps.p, B->ops.p, B->pushes.p, B->support.p, B->xoff.p, B->xcnt.p,
               B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr,
-              B->hk ? std::exp(-B->p.tau) : 1.0, B->hk ? 1 : 0};
+              B->hk ? std::exp(-B->p.tau) : 1.0, B->hk ? 1 : 0, B->amb.p, B->amb_cnt.p};
     int64_t launches = 0;
     for (int64_t w = 0; w < waves; ++w) {
         const int64_t base = w * B->slots;
@@ -1301,6 +1318,142 @@ static void build_relabeled(gd_batch *B) {
     GD_CUDA(cudaDeviceSynchronize());
 }
 
+// ---- re-solve of ambiguous seeds on the bit-exact path --------------------
+namespace gd {
+namespace {
+
+__global__ void k_count_nz(const double *__restrict__ v, int64_t n, unsigned long long *cnt) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += v[i] != 0.0;
+    c = __reduce_add_sync(FULL, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// (node, scale * v) for every nonzero of v, appended at *cursor (any order)
+__global__ void k_emit_nz(const double *__restrict__ v, int64_t n, double scale,
+                          int32_t *__restrict__ nodes, double *__restrict__ vals,
+                          unsigned long long *cursor) {
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const double x = i < n ? v[i] : 0.0;
+        const bool nz = x != 0.0;
+        const unsigned am = __ballot_sync(FULL, nz);
+        if (!am) continue;
+        const int lane = threadIdx.x & 31;
+        unsigned long long b = 0;
+        if (lane == __ffs(am) - 1) b = atomicAdd(cursor, (unsigned long long)__popc(am));
+        b = __shfl_sync(FULL, b, __ffs(am) - 1);
+        if (nz) {
+            const unsigned long long at = b + __popc(am & lanemask_lt());
+            nodes[at] = (int32_t)i;
+            vals[at] = __dmul_rn(scale, x);
+        }
+    }
+}
+
+}  // namespace
+
+// grow a device pool to `cap` entries keeping its first `used`
+template <class T>
+static void grow_keep(DBuf<T> &b, size_t cap, size_t used) {
+    DBuf<T> nb(cap);
+    if (used) GD_CUDA(cudaMemcpy(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice));
+    std::swap(b.p, nb.p);
+    std::swap(b.n, nb.n);
+}
+
+}  // namespace gd
+
+// The sweep-synchronous batches flag every seed with an update that landed
+// within AMB_REL of its threshold (common.cuh): there the atomic scatter
+// order could round the residual to the other side of theta than the
+// reference's sequential fold.  Each flagged seed is solved again on the
+// bit-exact path (exact.cu, the reference's own frontier order) and its
+// per-seed results and sparse x / r segments are replaced -- so every seed's
+// frontier sets, sweeps and operation counts are the reference's.
+static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
+                              cudaStream_t st) {
+    unsigned long long cnt = 0;
+    GD_CUDA(cudaMemcpy(&cnt, B->amb_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+    B->last_amb = (int64_t)cnt;
+    const bool all = B->p.exact_all != 0;
+    if ((!cnt && !all) || B->hk || B->fifo) return;  // (heat kernel: reported, not re-solved)
+    std::vector<int32_t> amb(n_seeds);
+    std::vector<int64_t> seeds(n_seeds);
+    GD_CUDA(cudaMemcpy(amb.data(), B->amb.p, sizeof(int32_t) * n_seeds, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(seeds.data(), d_seeds, sizeof(int64_t) * n_seeds, cudaMemcpyDeviceToHost));
+    const bool ch = B->p.method == GD_M_LOCAL_CH, katz = B->p.problem == GD_P_KATZ;
+    gd_operator op{};
+    op.weight_rule = katz ? GD_W_CONST : GD_W_RW;
+    op.theta_rule = GD_T_DEGREE;
+    op.beta = katz ? B->p.alpha : 1.0 - B->p.alpha;
+    op.theta_coeff = katz ? B->p.eps : B->p.eps * B->p.alpha;
+    const double bval = katz ? 1.0 : B->p.alpha;
+    const int64_t n = B->G->n;
+    const int nb = 4 * n_sms(B->G->device);
+    if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));  // pools may move
+    for (int64_t i = 0; i < n_seeds; ++i) {
+        if (!amb[i] && !all) continue;
+        const ExactSeed e = exact_seed_solve(B->G, &op, ch ? GD_M_LOCAL_CH : GD_M_LOCAL_GD,
+                                             seeds[i], bval, B->p.mu, B->p.L, B->p.max_sweeps,
+                                             false, st);
+        unsigned long long *tmp = B->cursor.p;  // (free again: the solve's total is on the host)
+        unsigned long long nz[2] = {0, 0};
+        GD_CUDA(cudaMemset(tmp, 0, sizeof(unsigned long long)));
+        k_count_nz<<<nb, 256>>>(e.x, n, tmp);
+        GD_LAUNCH_CHECK();
+        GD_CUDA(cudaMemcpy(&nz[0], tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemset(tmp, 0, sizeof(unsigned long long)));
+        k_count_nz<<<nb, 256>>>(e.r, n, tmp);
+        GD_LAUNCH_CHECK();
+        GD_CUDA(cudaMemcpy(&nz[1], tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        const int64_t xb = B->last_x_total;
+        if (xb + (int64_t)nz[0] > B->xcap) {
+            const int64_t cap = 2 * (xb + (int64_t)nz[0]);
+            grow_keep(B->xnodes, (size_t)cap, (size_t)xb);
+            grow_keep(B->xvals, (size_t)cap, (size_t)xb);
+            B->xcap = cap;
+        }
+        unsigned long long c0 = (unsigned long long)xb;
+        GD_CUDA(cudaMemcpy(tmp, &c0, sizeof(c0), cudaMemcpyHostToDevice));
+        k_emit_nz<<<nb, 256>>>(e.x, n, 1.0, B->xnodes.p, B->xvals.p, tmp);
+        GD_LAUNCH_CHECK();
+        B->last_x_total = xb + (int64_t)nz[0];
+        const int64_t sw = e.sweeps, ops = e.ops, pu = e.pushes, sup = (int64_t)nz[1];
+        const int64_t xc = (int64_t)nz[0];
+        const int32_t cv = e.converged;
+        GD_CUDA(cudaMemcpy(B->sweeps.p + i, &sw, 8, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->ops.p + i, &ops, 8, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->pushes.p + i, &pu, 8, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->support.p + i, &sup, 8, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->conv.p + i, &cv, 4, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->xoff.p + i, &xb, 8, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(B->xcnt.p + i, &xc, 8, cudaMemcpyHostToDevice));
+        if (B->want_r()) {
+            const int64_t rb = B->last_r_total;
+            if (rb + (int64_t)nz[1] > B->rcap) {
+                const int64_t cap = 2 * (rb + (int64_t)nz[1]);
+                grow_keep(B->rnodes, (size_t)cap, (size_t)rb);
+                grow_keep(B->rvals, (size_t)cap, (size_t)rb);
+                B->rcap = cap;
+            }
+            c0 = (unsigned long long)rb;
+            GD_CUDA(cudaMemcpy(tmp, &c0, sizeof(c0), cudaMemcpyHostToDevice));
+            k_emit_nz<<<nb, 256>>>(e.r, n, 1.0, B->rnodes.p, B->rvals.p, tmp);
+            GD_LAUNCH_CHECK();
+            B->last_r_total = rb + (int64_t)nz[1];
+            const int64_t rc = (int64_t)nz[1];
+            GD_CUDA(cudaMemcpy(B->roff.p + i, &rb, 8, cudaMemcpyHostToDevice));
+            GD_CUDA(cudaMemcpy(B->rcnt.p + i, &rc, 8, cudaMemcpyHostToDevice));
+        }
+    }
+    const unsigned long long tot = (unsigned long long)B->last_x_total;
+    GD_CUDA(cudaMemcpy(B->cursor.p, &tot, sizeof(tot), cudaMemcpyHostToDevice));
+    GD_CUDA(cudaDeviceSynchronize());
+}
+
 extern "C" {
 
 int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out) {
@@ -1351,7 +1504,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 if (const char *e = getenv("GDIFF_SOR_MODE"))
                     use_win = strcmp(e, "win") == 0 ? true : (strcmp(e, "warp") == 0 ? false : use_win);
                 if (use_win && !p->want_r) B->sorwin = sorwin_create(G, p->slots);
-                B->cursor.alloc(1); B->overflow.alloc(1);
+                B->cursor.alloc(1); B->overflow.alloc(1); B->amb_cnt.alloc(1);
                 B->xcap = p->out_cap > 0 ? p->out_cap : (16LL << 20);
                 B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
                 *out = B;
@@ -1385,7 +1538,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 { const int64_t ldr = (n + 3) & ~3LL, smwr = (ldr / 4 + 31) / 32;  // r extraction scratch
                   if (B->rcap) B->rscratch.alloc((size_t)B->slots * (size_t)r_extract_chunks(smwr)); }
                 B->xcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
-                B->cursor.alloc(1); B->overflow.alloc(1);
+                B->cursor.alloc(1); B->overflow.alloc(1); B->amb_cnt.alloc(1);
                 B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
                 B->sgn = signed_batch_create(B->work(), B->p, slots);
                 *out = B;
@@ -1431,6 +1584,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->seed.alloc(slots); B->touched.alloc(slots); B->pushed_cnt.alloc(slots);
             B->s_ops.alloc(slots); B->s_pushes.alloc(slots); B->s_negz.alloc(slots);
             B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
+            B->s_amb.alloc(slots); B->amb_cnt.alloc(1);
             B->slot_base.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
             B->ukey.alloc(fc); B->uarc.alloc(fc); B->skey.alloc(fc); B->sarc.alloc(fc);
@@ -1531,21 +1685,34 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
             // grow (doubling, so a growing workload redoes at most log times) and redo;
             // host-entry copies still reading the old pool finish first
             if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));
+            // new pools are allocated before the old ones go, and the
+            // capacities change only once both exist: a failed grow (OOM)
+            // leaves the handle consistent
             if ((int64_t)used > B->xcap) {
-                B->xcap = 2 * (int64_t)used;
-                B->xnodes.alloc(B->xcap);
-                B->xvals.alloc(B->xcap);
+                const int64_t cap = 2 * (int64_t)used;
+                DBuf<int32_t> nn(cap);
+                DBuf<double> nv(cap);
+                std::swap(B->xnodes.p, nn.p); std::swap(B->xnodes.n, nn.n);
+                std::swap(B->xvals.p, nv.p); std::swap(B->xvals.n, nv.n);
+                B->xcap = cap;
             }
             if ((int64_t)rused > B->rcap) {
-                B->rcap = 2 * (int64_t)rused;
-                B->rnodes.alloc(B->rcap);
-                B->rvals.alloc(B->rcap);
+                const int64_t cap = 2 * (int64_t)rused;
+                DBuf<int32_t> nn(cap);
+                DBuf<double> nv(cap);
+                std::swap(B->rnodes.p, nn.p); std::swap(B->rnodes.n, nn.n);
+                std::swap(B->rvals.p, nv.p); std::swap(B->rvals.n, nv.n);
+                B->rcap = cap;
             }
         }
+        resolve_ambiguous(B, d_seeds, n_seeds, st);
+        res->x_total = B->last_x_total;
         res->sweeps = B->sweeps.p; res->total_ops = B->ops.p; res->pushes = B->pushes.p;
         res->support = B->support.p; res->converged = B->conv.p; res->x_offset = B->xoff.p;
         res->x_count = B->xcnt.p; res->x_nodes = B->xnodes.p; res->x_vals = B->xvals.p;
         res->kernel_launches = B->last_launches;
+        res->ambiguous = B->amb.p;
+        res->n_ambiguous = B->last_amb;
     });
 }
 
@@ -1671,6 +1838,12 @@ int gd_batch_fetch_r_host(gd_batch *B, int64_t n_seeds, int64_t *r_offset, int64
         d2h(r_vals, B->rvals.p, sizeof(double) * B->last_r_total);
         GD_CUDA(cudaStreamSynchronize(st));
     });
+}
+
+int gd_batch_last_ambiguous(const gd_batch *B, int64_t *count) {
+    if (!B || !count) return GD_ERR_ARG;
+    *count = B->last_amb;
+    return GD_OK;
 }
 
 int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {

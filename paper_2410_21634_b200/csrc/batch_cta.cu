@@ -58,6 +58,8 @@ struct CtaArgs {
     int32_t *conv, *xnodes;
     double *xvals;
     int64_t xcap;
+    int32_t *amb;                 // per seed: near-threshold update seen (common.cuh)
+    unsigned long long *amb_cnt;  // flagged seeds
 };
 
 __device__ __forceinline__ double theta_d(double tc, int32_t d) {
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
     __shared__ int64_t s_run, s_seed, s_base;
     __shared__ int s_overflow;
     __shared__ unsigned s_touch, s_negz;
+    __shared__ int s_amb;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = CT / 32;
     const int64_t slot = blockIdx.x;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
             s_touch = 1;  // the seed's r word
             s_negz = 0;
             s_overflow = 0;
+            s_amb = 0;
         }
         unsigned long long my_ops = 0, my_push = 0;
         int64_t t = 0;
@@ -223,7 +227,9 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                     const bool first = valid[q] && ob == 0;
                     const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
                     const double th = theta_d(tc, dv[q]);
-                    const bool cross = valid[q] && old[q] < th && __dadd_rn(old[q], c[q]) >= th;
+                    const double nw = __dadd_rn(old[q], c[q]);
+                    const bool cross = valid[q] && old[q] < th && nw >= th;
+                    if (valid[q] && near_theta(nw, th)) s_amb = 1;
                     if (first) atomicOr(map + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                     const unsigned fm = __ballot_sync(FULLM, first), nm = __ballot_sync(FULLM, negz);
                     if (lane == 0) {
@@ -250,6 +256,8 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
             A.conv[si] = (s_F == 0 && !s_overflow) ? 1 : 0;
             A.support[si] = (int64_t)s_touch - ((int64_t)psh - (int64_t)s_negz);
             A.xcnt[si] = pc;
+            A.amb[si] = s_amb;
+            if (s_amb) atomicAdd(A.amb_cnt, 1ULL);
         }
         __syncthreads();
         const int64_t b = s_base;
@@ -344,7 +352,8 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
                    const int32_t *perm, const int32_t *inv, int64_t *sweeps, int64_t *ops,
                    int64_t *pushes, int64_t *support, int32_t *conv, int64_t *xoff,
                    int64_t *xcnt, int32_t *xnodes, double *xvals, int64_t xcap,
-                   unsigned long long *cursor, cudaStream_t st) {
+                   unsigned long long *cursor, int32_t *amb, unsigned long long *amb_cnt,
+                   cudaStream_t st) {
     if (n_seeds == 0) return;
     CtaArgs A{};
     A.g = W->view();
@@ -362,6 +371,8 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.support = support;
     A.xoff = xoff; A.xcnt = xcnt; A.conv = conv; A.xnodes = xnodes; A.xvals = xvals;
     A.xcap = xcap;
+    A.amb = amb;
+    A.amb_cnt = amb_cnt;
     GD_CUDA(cudaMemsetAsync(S->next.p, 0, sizeof(unsigned long long), st));
     const int grid = (int)(n_seeds < S->slots ? n_seeds : S->slots);
     k_seed_cta<<<grid, CT, 0, st>>>(A);

@@ -92,6 +92,7 @@ struct SArgs {
     unsigned long long *s_ops, *s_pushes;
     double *s_l1, *s_b1;
     int32_t *s_last, *s_conv;
+    int32_t *s_amb;  // per slot: a final |r| within AMB_REL of theta (common.cuh)
     int32_t *overflow;
 };
 
@@ -396,7 +397,9 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 const int64_t idx = (int64_t)k * A.ld + u;
                 const double ru = A.r[idx];
                 d = A.g.deg[u];
-                act = fabs(ru) >= theta_of(A.op, u, d) && !slot_diverged(A, k);
+                const double th = theta_of(A.op, u, d);
+                if (near_theta(fabs(ru), th)) A.s_amb[k] = 1;
+                act = fabs(ru) >= th && !slot_diverged(A, k);
                 if (act && t >= A.max_sweeps) {  // sweep cap reached with work left
                     A.s_conv[k] = 0;
                     act = false;
@@ -563,7 +566,11 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 if (A.secmap && valid[q] && __double_as_longlong(old[q]) == 0)
                     atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7),
                              1u << ((v[q] >> 2) & 31));
-                const bool hot = valid[q] && fabs(nv) >= theta_of(A.op, v[q], dv[q]);
+                const double th = theta_of(A.op, v[q], dv[q]);
+                const bool hot = valid[q] && fabs(nv) >= th;
+                // a node whose final |r| sits just below theta is never a
+                // candidate: its last update (which stores that value) flags it
+                if (valid[q] && near_theta(fabs(nv), th)) A.s_amb[k[q]] = 1;
                 const bool nw = cand_mark(hot, k[q], v[q], A, nxt);
                 cand_stage(nw, k[q], v[q], S, A, nxt);
             }
@@ -611,6 +618,7 @@ __global__ void k_s_init(SArgs A, const int64_t *__restrict__ seeds, const int32
     A.s_b1[k] = fabs(bval);
     A.s_last[k] = -1;
     A.s_conv[k] = 1;
+    A.s_amb[k] = 0;
 }
 
 __global__ void k_s_reserve(SArgs A, unsigned long long *cursor, int64_t *slot_base) {
@@ -626,6 +634,8 @@ struct SOut {
     int64_t xcap;
     const int32_t *inv;
     const int64_t *slot_base;
+    int32_t *amb;
+    unsigned long long *amb_cnt;
 };
 
 // grid (SCHUNKS, slots): x over the pushed list out (caller ids); x, mstamp
@@ -672,6 +682,8 @@ __global__ void k_s_extract(SArgs A, SOut O, int64_t seed_base) {
         O.support[si] = -1;  // not tracked for signed solves
         O.xoff[si] = b;
         O.xcnt[si] = pc;
+        O.amb[si] = A.s_amb[k];
+        if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
     }
 }
 
@@ -808,7 +820,7 @@ struct SignedState {
     double step0 = 0.0, l1cap = 10.0;
     DBuf<double> coef_r, coef_m;
     DBuf<double> x, r, mom, fcval, s_l1, s_b1;
-    DBuf<int32_t> mstamp, pushed, chunk_e, s_last, s_conv, overflow;
+    DBuf<int32_t> mstamp, pushed, chunk_e, s_last, s_conv, s_amb, overflow;
     DBuf<uint32_t> cm0, cm1, secmap;
     DBuf<int64_t> cand0, cand1, fkey, farc, frow, slot_base;
     DBuf<int2> colp;
@@ -868,6 +880,8 @@ struct SignedState {
         candctr.alloc(2); fctr.alloc(1); overflow.alloc(1);
         s_ops.alloc(slots); s_pushes.alloc(slots); pushed_cnt.alloc(slots);
         s_l1.alloc(slots); s_b1.alloc(slots); s_last.alloc(slots); s_conv.alloc(slots);
+        s_amb.alloc(slots);
+        GD_CUDA(cudaMemset(s_amb.p, 0, sizeof(int32_t) * slots));
         slot_base.alloc(slots);
         GD_CUDA(cudaMemset(s_l1.p, 0, sizeof(double) * slots));
         GD_CUDA(cudaMemset(s_b1.p, 0, sizeof(double) * slots));
@@ -929,7 +943,7 @@ struct SignedState {
         A.fkey = fkey.p; A.farc = farc.p; A.frow = frow.p; A.fcval = fcval.p;
         A.chunk_e = chunk_e.p; A.fctr = fctr.p;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_l1 = s_l1.p; A.s_b1 = s_b1.p;
-        A.s_last = s_last.p; A.s_conv = s_conv.p;
+        A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
         A.overflow = overflow.p;
         return A;
     }
@@ -992,7 +1006,8 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
                       int64_t *support, int32_t *conv, int64_t *xoff, int64_t *xcnt,
                       int32_t *xnodes, double *xvals, int64_t xcap, unsigned long long *cursor,
                       std::vector<cudaEvent_t> &ev, double *ms, int64_t *launches,
-                      cudaStream_t st, const RPool *rp) {
+                      cudaStream_t st, const RPool *rp, int32_t *amb,
+                      unsigned long long *amb_cnt) {
     if (S->dirty) {  // a capacity abort left marks / residuals behind
         S->clear_marks(st);
         const size_t sn = (size_t)S->slots * (size_t)S->ld;
@@ -1011,7 +1026,7 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
         ev.push_back(e);
     }
     SOut O{sweeps, ops, pushes, support, xoff, xcnt, conv, xnodes, xvals, xcap, inv,
-           S->slot_base.p};
+           S->slot_base.p, amb, amb_cnt};
     int64_t nl = 0;
     for (int64_t w = 0; w < waves; ++w) {
         const int64_t base = w * S->slots;

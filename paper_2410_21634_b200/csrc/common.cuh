@@ -158,6 +158,37 @@ void report_push_log(gd_report *rep, int64_t &cap, int64_t vol, double gamma, do
                      int8_t sign, int64_t fsize);
 void report_trace(gd_report *rep, int64_t &tcap, const int64_t *f, int64_t cnt);
 
+// ------------------------------------------------- near-threshold detector --
+// Batched sweep-synchronous solvers scatter with fp64 atomics, so a residual
+// is summed in another order than the reference's sequential fold
+// (src/local_solvers.py:282-291) and may differ from it in the last bits.
+// Frontier membership (r_v >= theta_v, :336-350) can then differ only when a
+// residual lands within that rounding of its threshold.  Every batched update
+// whose result lies within a relative AMB_REL of theta_v flags its seed
+// "ambiguous"; flagged seeds are re-solved on the bit-exact path (exact.cu),
+// so the batch's frontier sets, sweeps and operation counts are the
+// reference's.  AMB_REL = 2^-36 (1.46e-11) covers the forward-error bound
+// 2 k u (u = 2^-53) of k <= 2^16 reordered additions into one residual.
+constexpr double AMB_REL = 1.4551915228366852e-11;  // 2^-36
+
+__device__ __forceinline__ bool near_theta(double v, double th) {
+    return fabs(__dsub_rn(v, th)) <= AMB_REL * th;
+}
+
+// Bit-exact single-seed solve on the device (exact.cu): LocalGD (method
+// GD_M_LOCAL_GD, b = bval e_seed, frontier signed when sgn) or LocalCH
+// (GD_M_LOCAL_CH, bounds mu < L).  x and r are left in device buffers owned
+// by the calling thread's solver (valid until its next solve).
+struct ExactSeed {
+    int64_t sweeps, ops, pushes;
+    int32_t converged, diverged;
+    const double *x, *r;
+    int64_t n;
+};
+ExactSeed exact_seed_solve(const gd_graph *G, const gd_operator *op, int32_t method, int64_t seed,
+                           double bval, double mu, double L, int64_t max_sweeps, bool sgn,
+                           cudaStream_t st);
+
 inline int n_sms(int device) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);

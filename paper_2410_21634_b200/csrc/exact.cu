@@ -339,6 +339,22 @@ struct SweepSolver {
         return f;
     }
 
+    // S_0 for b = val e_seed: the same filter, state zeroed on the device
+    int64_t init_spike(int64_t seed, double val) {
+        GD_CUDA(cudaMemsetAsync(r.p, 0, sizeof(double) * (n ? n : 1), s));
+        GD_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * (n ? n : 1), s));
+        GD_CUDA(cudaMemcpyAsync(r.p + seed, &val, sizeof(double), cudaMemcpyHostToDevice, s));
+        const int32_t sd = (int32_t)seed;
+        GD_CUDA(cudaMemcpyAsync(seeds.p, &sd, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        k_flag_active_nodes<<<1, TPB, 0, s>>>(seeds.p, 1, r.p, g, op.dev, sgn, flag.p);
+        GD_LAUNCH_CHECK();
+        uint8_t f = 0;
+        GD_CUDA(cudaMemcpyAsync(&f, flag.p, 1, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        if (f) GD_CUDA(cudaMemcpy(F.p, &sd, sizeof(int32_t), cudaMemcpyHostToDevice));
+        return f ? 1 : 0;
+    }
+
     // one sweep after the gather kernel ran; returns |S_{t+1}| and P
     int64_t scatter_and_filter(int64_t f, int32_t t, int64_t *P_out, double *sgamma) {
         // arc offsets: exclusive scan of frontier degrees (fdeg[f] = 0 -> total)
@@ -445,6 +461,73 @@ SweepSolver &solver_for(const gd_graph *G, const gd_operator *o, bool sgn) {
 }
 
 }  // namespace
+
+// Bit-exact re-solve of one seed for the batched solvers (common.cuh): the
+// sweep loops of local_gd_run / gd_local_ch below without the per-sweep
+// logs (LocalCH keeps its l1 for the divergence abort, :527-530).
+ExactSeed exact_seed_solve(const gd_graph *G, const gd_operator *o, int32_t method, int64_t seed,
+                           double bval, double mu, double L, int64_t max_sweeps, bool sgn,
+                           cudaStream_t st) {
+    GD_CUDA(cudaStreamSynchronize(st));
+    const bool ch = method == GD_M_LOCAL_CH;
+    SweepSolver &S = solver_for(G, o, ch || sgn);
+    ExactSeed out{0, 0, 0, 1, 0, nullptr, nullptr, S.n};
+    size_t nn = S.n ? S.n : 1;
+    if (ch) {
+        S.mom.ensure(nn);
+        S.mstamp.ensure(nn);
+        GD_CUDA(cudaMemset(S.mom.p, 0, sizeof(double) * nn));
+        GD_CUDA(cudaMemset(S.mstamp.p, 0xFE, sizeof(int32_t) * nn));
+    }
+    int64_t f = S.init_spike(seed, bval);
+    const double rho = ch ? (L - mu) / (L + mu) : 0.0, step0 = ch ? 2.0 / (L + mu) : 0.0;
+    const double b_l1 = fabs(bval);
+    double delta = rho;
+    int32_t t = 0;
+    while (f) {
+        if (out.sweeps >= max_sweeps) { out.converged = 0; break; }
+        if (ch) {
+            double coef_r = 0.0, coef_m = 0.0;
+            if (t > 0) {
+                const double dn = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
+                coef_r = 4.0 * dn / (L - mu);
+                coef_m = delta * dn;
+                delta = dn;
+            }
+            k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
+                                                        S.wnode.p, S.fdeg.p, S.fstamp.p, t,
+                                                        S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
+                                                        S.g, S.op.dev);
+        } else {
+            k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
+                                                        S.wnode.p, S.fdeg.p, S.fstamp.p, t, S.g,
+                                                        S.op.dev);
+        }
+        GD_LAUNCH_CHECK();
+        int64_t P = 0;
+        double sgamma = 0.0;
+        const int64_t fnext = S.scatter_and_filter(f, t, &P, &sgamma);
+        out.ops += P;
+        out.pushes += f;
+        out.sweeps += 1;
+        f = fnext;
+        ++t;
+        if (ch) {
+            double lm[2];
+            S.reduce_l1_min(lm);
+            if (lm[0] > 10.0 * b_l1) {
+                out.converged = 0;
+                out.diverged = 1;
+                break;
+            }
+        }
+    }
+    GD_CUDA(cudaStreamSynchronize(S.s));
+    out.x = S.x.p;
+    out.r = S.r.p;
+    return out;
+}
+
 }  // namespace gd
 
 using namespace gd;

@@ -16,25 +16,101 @@ import math
 from . import _lib as gdl
 from .synth import RMAT_SHAPES
 
-__all__ = ["rmat_csr_device", "RMAT_SHAPES"]
+__all__ = ["rmat_csr_device", "rmat_csr_device_big", "rmat_keys_torch", "RMAT_SHAPES"]
 
 
-def rmat_csr_device(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19), device: int = 0):
-    """Return (row_ptr int64[n+1], col int32[2m]) as CUDA tensors."""
+def _s64(c: int) -> int:
+    """A uint64 constant as the int64 with the same bits."""
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _srl(z, s: int):
+    """Logical right shift of int64 tensors holding uint64 bits."""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def _splitmix64_t(z):
+    z = z + _s64(0x9E3779B97F4A7C15)
+    z = (z ^ _srl(z, 30)) * _s64(0xBF58476D1CE4E5B9)
+    z = (z ^ _srl(z, 27)) * _s64(0x94D049BB133111EB)
+    return z ^ _srl(z, 31)
+
+
+def rmat_keys_torch(scale: int, n: int, first: int, count: int, seed: int, abc, dev,
+                    chunk: int = 1 << 24):
+    """The candidate keys of gd_rmat_keys_device (csrc/generate.cu) with torch
+    tensor ops only: no libgdiff.  Same counter-based stream as
+    synth.rmat_edges + permute_ids (int64 arithmetic wraps like uint64);
+    used by bench.py's reference arm so that arm never loads the product
+    library.  Returns int64 keys min*n+max, -1 for dropped candidates."""
     import torch
 
+    ta = int(round(abc[0] * 65536))
+    tb = ta + int(round(abc[1] * 65536))
+    tc = tb + int(round(abc[2] * 65536))
+    base = _s64((seed * 0x632BE59BD9B4E019) & 0xFFFFFFFFFFFFFFFF)
+    z = (seed ^ 0x5EED) + 0x9E3779B97F4A7C15 & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+    pkey = z ^ (z >> 31)
+    mask = (1 << scale) - 1
+    sh = max(1, scale // 2)
+    nchunks = (scale + 3) // 4
+    out = torch.empty(count, dtype=torch.int64, device=dev)
+    for c0 in range(0, count, chunk):
+        e = torch.arange(first + c0, first + min(count, c0 + chunk), dtype=torch.int64, device=dev)
+        u = torch.zeros_like(e)
+        v = torch.zeros_like(e)
+        for k in range(nchunks):
+            h = _splitmix64_t(base ^ (e * nchunks + k))
+            for q in range(4):
+                lvl = 4 * k + q
+                if lvl >= scale:
+                    break
+                f = (h >> (16 * q)) & 0xFFFF
+                bit = scale - 1 - lvl
+                u |= (f >= tb).to(torch.int64) << bit
+                v |= (((f >= ta) & (f < tb)) | (f >= tc)).to(torch.int64) << bit
+        for rnd in range(3):
+            mult = ((pkey >> (rnd * 16)) & 0xFFFF) * 2 + 0x9E37 * 2 + 1
+            u = (u * mult) & mask
+            u = u ^ (u >> sh)
+            v = (v * mult) & mask
+            v = v ^ (v >> sh)
+        ok = (u < n) & (v < n) & (u != v)
+        key = torch.minimum(u, v) * n + torch.maximum(u, v)
+        out[c0:c0 + e.numel()] = torch.where(ok, key, torch.full_like(key, -1))
+    return out
+
+
+def _keys(native: bool, scale, n, first, count, seed, abc, dev):
+    import torch
+
+    if not native:
+        return rmat_keys_torch(scale, n, first, count, seed, abc, dev)
     lib = gdl.load()
-    dev = torch.device("cuda", device)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    buf = torch.empty(count, dtype=torch.int64, device=dev)
+    gdl.check(lib.gd_rmat_keys_device(scale, n, first, count, seed, abc[0], abc[1], abc[2],
+                                      C.c_void_p(buf.data_ptr()), C.c_void_p(st)))
+    return buf
+
+
+def rmat_csr_device(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19), device: int = 0,
+                    native: bool = True):
+    """Return (row_ptr int64[n+1], col int32[2m]) as CUDA tensors.  native=False
+    draws the candidates with torch ops instead of the library kernel (the
+    same graph)."""
+    import torch
+
+    dev = torch.device("cuda", device) if torch.cuda.is_available() else torch.device("cpu")
     scale = max(1, int(math.ceil(math.log2(max(n, 2)))))
     chunk = max(1024, int(m * 1.25) + 1024)
-    st = torch.cuda.current_stream(dev).cuda_stream
     keys = torch.empty(0, dtype=torch.int64, device=dev)
     first = torch.empty(0, dtype=torch.int64, device=dev)
     drawn = 0
     while True:
-        buf = torch.empty(chunk, dtype=torch.int64, device=dev)
-        gdl.check(lib.gd_rmat_keys_device(scale, n, drawn, chunk, seed, abc[0], abc[1], abc[2],
-                                          C.c_void_p(buf.data_ptr()), C.c_void_p(st)))
+        buf = _keys(native, scale, n, drawn, chunk, seed, abc, dev)
         ok = buf >= 0
         idx = torch.arange(drawn, drawn + chunk, dtype=torch.int64, device=dev)[ok]
         keys = torch.cat([keys, buf[ok]])
@@ -89,7 +165,7 @@ def relabel_by_degree(row, col):
 
 
 def rmat_csr_device_big(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19), device: int = 0,
-                        buckets: int = 16, chunk: int = 1 << 28):
+                        buckets: int = 16, chunk: int = 1 << 28, native: bool = True):
     """Same graph as rmat_csr_device for shapes beyond one device sort
     (torch.sort is limited to INT_MAX elements): candidates are partitioned
     by their low endpoint into `buckets` id ranges (a duplicate always lands
@@ -99,10 +175,8 @@ def rmat_csr_device_big(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19), d
     sort), and arcs are sorted per source-range bucket."""
     import torch
 
-    lib = gdl.load()
     dev = torch.device("cuda", device)
     scale = max(1, int(math.ceil(math.log2(max(n, 2)))))
-    st = torch.cuda.current_stream(dev).cuda_stream
     width = (n + buckets - 1) // buckets
     bk = [torch.empty(0, dtype=torch.int64, device=dev) for _ in range(buckets)]
     bi = [torch.empty(0, dtype=torch.int64, device=dev) for _ in range(buckets)]
@@ -118,9 +192,7 @@ def rmat_csr_device_big(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19), d
     while True:
         while drawn < target:
             c = min(chunk, target - drawn)
-            buf = torch.empty(c, dtype=torch.int64, device=dev)
-            gdl.check(lib.gd_rmat_keys_device(scale, n, drawn, c, seed, abc[0], abc[1], abc[2],
-                                              C.c_void_p(buf.data_ptr()), C.c_void_p(st)))
+            buf = _keys(native, scale, n, drawn, c, seed, abc, dev)
             ok = buf >= 0
             keys = buf[ok]
             idx = torch.arange(drawn, drawn + c, dtype=torch.int64, device=dev)[ok]

@@ -27,6 +27,14 @@ def test_reference_arm_json_line(method):
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert "workload" in line["config"] and "model" not in line["config"]
+    # the timed reference path never loads the product library
+    probe = ("import runpy, sys; sys.argv = %r; runpy.run_path(%r, run_name='__main__'); "
+             "print('LIBGDIFF', any('libgdiff' in l for l in open('/proc/self/maps')))"
+             % (cmd[1:], cmd[1]))
+    out2 = subprocess.run([sys.executable, "-c", probe], capture_output=True, text=True,
+                          timeout=600, cwd=ROOT)
+    assert out2.returncode == 0, out2.stderr[-2000:]
+    assert "LIBGDIFF False" in out2.stdout
 
 
 @pytest.mark.gpu
@@ -44,4 +52,15 @@ def test_gpu_arm_json_line(method):
     assert line["gpu_launches"] > 0 and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]
-    assert line["cpu_baseline"]["parity_sweeps_ops_identical"] is True
+    cb = line["cpu_baseline"]
+    assert cb["parity_sweeps_ops_identical"] is True
+    assert cb["x_l1_rel_max"] <= cb["x_l1_rel_tolerance"] == 1e-9
+    assert cb["topk_identical_up_to_ties"] >= 1
+    assert line["exec_form"] and line["slots_used"] >= 1 and line["ambiguous_seeds"] >= 0
+    # the reference arm: same config dict, and it never loads the product library
+    ref = subprocess.run(cmd + ["--impl", "reference"], capture_output=True, text=True,
+                         timeout=900, cwd=ROOT)
+    assert ref.returncode == 0, ref.stderr[-2000:]
+    rline = json.loads(ref.stdout.strip().splitlines()[-1])
+    assert rline["config"] == line["config"]
+    assert rline["impl"] == "reference" and rline["metric"] == line["metric"]

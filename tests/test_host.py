@@ -151,3 +151,27 @@ def test_bulk_events_equal_sequential(small):
     with pytest.raises(G.GraphStructureError):
         G.apply_events(g, evs + [EdgeEvent("insert", evs[-1].u, evs[-1].v)] * 70
                        if evs[-1].kind == "insert" else evs + [EdgeEvent("delete", evs[-1].u, evs[-1].v)] * 70)
+
+
+def test_torch_rmat_stream_is_the_library_stream():
+    """gen.rmat_keys_torch (the reference arm's generator: torch ops, no
+    libgdiff) draws the same candidate keys as synth.rmat_edges + permute_ids
+    (the host twin of csrc/generate.cu) and builds the same CSR."""
+    import torch
+
+    from paper_2410_21634_b200.gen import rmat_csr_device, rmat_keys_torch
+    from paper_2410_21634_b200.synth import permute_ids, rmat_edges, rmat_graph
+
+    for n, scale, seed in [(2708, 12, 0), (169_343, 18, 3), (111_059_433, 27, 1)]:
+        cand = rmat_edges(scale, 12345, 4000, seed)
+        a = permute_ids(cand[:, 0], scale, seed).astype(np.int64)
+        b = permute_ids(cand[:, 1], scale, seed).astype(np.int64)
+        ok = (a < n) & (b < n) & (a != b)
+        want = np.where(ok, np.minimum(a, b) * n + np.maximum(a, b), -1)
+        got = rmat_keys_torch(scale, n, 12345, 4000, seed, (0.57, 0.19, 0.19),
+                              torch.device("cpu"), chunk=999).numpy()
+        assert np.array_equal(want, got), n
+    row, col = rmat_csr_device(2708, 5278, seed=0, native=False)
+    g = rmat_graph(2708, 5278, seed=0)
+    assert np.array_equal(row.numpy(), g.offsets)
+    assert np.array_equal(col.numpy().astype(np.int64), g.targets)
