@@ -153,7 +153,8 @@ struct RoundArgs {
     unsigned long long *fctr;  // [2] packed (entries << 36 | arcs)
     unsigned long long *s_ops, *s_pushes, *s_negz, *s_pvol;
     int32_t *s_last, *s_conv;
-    int32_t *s_amb;       // per slot: near-threshold update seen (common.cuh)
+    int32_t *s_amb;       // per slot: a final residual within AMB_REL of theta (common.cuh)
+    NearList nearl;       // landings just below theta, re-checked after the round
     int32_t *overflow;
     const int32_t *perm;  // caller id -> working id (nullable)
     unsigned long long *cursor;  // output pool allocation
@@ -450,6 +451,17 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
             A.rlog[3 * t + 2] = globaltimer();
             A.rlog[3 * A.rlog_cap] = t + 1;
         }
+        {   // final values of last round's landings just below theta (common.cuh)
+            double *const rl = (HK && (t & 1)) ? A.r2 : A.r;
+            const int64_t nn = min((int64_t)*(volatile unsigned long long *)(A.nearl.cnt[cur]),
+                                   A.nearl.cap);
+            for (int64_t i = gtid; i < nn; i += nthreads) {
+                const int64_t key = A.nearl.key[cur][i];
+                const int32_t k = (int32_t)(key >> 32), v = (int32_t)(key & 0xffffffffLL);
+                if (below_theta(rl[(int64_t)k * A.ld + v], theta_deg(A.tcoeff, A.g.deg[v])))
+                    A.s_amb[k] = 1;
+            }
+        }
         if (F == 0) break;
         if (((P + 31) >> 5) > A.ccap) {  // arc-chunk map too small: report, stop
             if (gtid == 0) A.overflow[0] = 1;
@@ -469,6 +481,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
         if (gtid == 0) {
             A.fctr[nxt] = 0ULL;
             A.cctr[0] = 0ULL;
+            *A.nearl.cnt[nxt] = 0ULL;  // (last read two barriers ago)
         }
         for (int64_t k = gtid; k < A.m; k += nthreads) A.scnt[nxt][k] = 0ULL;
         double *const rc = (HK && (t & 1)) ? A.r2 : A.r;        // layer t
@@ -520,6 +533,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                 A.x[idx] = __dadd_rn(xo, val);
                 rc[idx] = HK ? 0.0 : -0.0;
                 d = A.g.deg[u];
+                if (near_theta(val, theta_deg(A.tcoeff, d))) A.s_amb[k] = 1;  // final r >= theta
             }
             // group-sorted position: one packed reservation per (warp, slot group);
             // ungrouped: the entry keeps its append position and arc offset
@@ -659,7 +673,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                 const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
                 const double nw = __dadd_rn(old[q], c[q]);
                 const bool cross = valid[q] && old[q] < th && nw >= th;
-                if (valid[q] && near_theta(nw, th)) A.s_amb[k[q]] = 1;
+                if (valid[q] && below_theta(nw, th)) near_record(A.nearl, nxt, k[q], v[q], A.s_amb);
                 block_count(first, k[q], 1u, S.touch);
                 if (first)  // first write of this r word: remember its 32 B sector
                     atomicOr(mapn + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
@@ -976,6 +990,9 @@ struct gd_batch {
     DBuf<double> x, r, fcval;
     DBuf<int32_t> pushed, seed, s_last, s_conv, s_amb, overflow;
     DBuf<int32_t> amb;               // per seed: near-threshold flag of the last solve
+    DBuf<int64_t> nearkey;           // near list: 2 x NEAR_CAP keys + 2 counters
+    DBuf<unsigned long long> nearcnt;
+    static constexpr int64_t NEAR_CAP = 1 << 16;
     DBuf<unsigned long long> amb_cnt;
     int64_t last_amb = 0;            // seeds re-solved on the exact path
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
@@ -1058,6 +1075,7 @@ struct gd_batch {
         A.secmap = secmap.p; A.smw = smw;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
+        A.nearl = NearList{{nearkey.p, nearkey.p + NEAR_CAP}, {nearcnt.p, nearcnt.p + 1}, NEAR_CAP};
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
         A.cursor = cursor.p;
@@ -1205,6 +1223,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
         GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
+        GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
         k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
                                                                B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
@@ -1585,6 +1604,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->s_ops.alloc(slots); B->s_pushes.alloc(slots); B->s_negz.alloc(slots);
             B->s_pvol.alloc(slots); B->s_last.alloc(slots); B->s_conv.alloc(slots);
             B->s_amb.alloc(slots); B->amb_cnt.alloc(1);
+            B->nearkey.alloc(2 * gd_batch::NEAR_CAP); B->nearcnt.alloc(2);
             B->slot_base.alloc(slots);
             B->fctr.alloc(2); B->cursor.alloc(1); B->overflow.alloc(1);
             B->ukey.alloc(fc); B->uarc.alloc(fc); B->skey.alloc(fc); B->sarc.alloc(fc);

@@ -33,6 +33,7 @@ namespace {
 constexpr int CT = 512;      // threads per CTA
 constexpr int CUNROLL = 4;   // chunks in flight per warp in phase B
 constexpr unsigned FULLM = 0xffffffffu;
+constexpr int NEAR_CAP = 256;  // landings just below theta per sweep (common.cuh)
 
 struct CtaArgs {
     DevGraph g;
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
     __shared__ int64_t s_run, s_seed, s_base;
     __shared__ int s_overflow;
     __shared__ unsigned s_touch, s_negz;
-    __shared__ int s_amb;
+    __shared__ int s_amb, s_nnear;
+    __shared__ int32_t s_near[NEAR_CAP];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = CT / 32;
     const int64_t slot = blockIdx.x;
@@ -122,11 +124,21 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
             s_negz = 0;
             s_overflow = 0;
             s_amb = 0;
+            s_nnear = 0;
         }
         unsigned long long my_ops = 0, my_push = 0;
         int64_t t = 0;
         __syncthreads();
         for (;; ++t) {
+            {   // final values of last sweep's landings just below theta
+                const int nn = min(s_nnear, NEAR_CAP);
+                for (int i = tid; i < nn; i += CT) {
+                    const int32_t v = s_near[i];
+                    if (below_theta(r[v], theta_d(A.tcoeff, A.g.deg[v]))) s_amb = 1;
+                }
+                __syncthreads();
+                if (tid == 0) s_nnear = 0;
+            }
             const int F = s_F;
             if (F == 0 || t >= A.max_sweeps) break;
             int32_t *const cur = fr0 + (t & 1) * A.ncap;
@@ -149,6 +161,7 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                     x[u] = __dadd_rn(xo, val);
                     r[u] = -0.0;  // pushed (+0.0 = never touched)
                     d = A.g.deg[u];
+                    if (near_theta(val, theta_d(A.tcoeff, d))) s_amb = 1;  // final r >= theta
                     fc[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                     fresh = __double_as_longlong(xo) == 0;
                     my_ops += (unsigned long long)d;
@@ -229,7 +242,10 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                     const double th = theta_d(tc, dv[q]);
                     const double nw = __dadd_rn(old[q], c[q]);
                     const bool cross = valid[q] && old[q] < th && nw >= th;
-                    if (valid[q] && near_theta(nw, th)) s_amb = 1;
+                    if (valid[q] && below_theta(nw, th)) {
+                        const int at = atomicAdd(&s_nnear, 1);
+                        if (at < NEAR_CAP) s_near[at] = v[q]; else s_amb = 1;
+                    }
                     if (first) atomicOr(map + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                     const unsigned fm = __ballot_sync(FULLM, first), nm = __ballot_sync(FULLM, negz);
                     if (lane == 0) {

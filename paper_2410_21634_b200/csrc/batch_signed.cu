@@ -93,6 +93,7 @@ struct SArgs {
     double *s_l1, *s_b1;
     int32_t *s_last, *s_conv;
     int32_t *s_amb;  // per slot: a final |r| within AMB_REL of theta (common.cuh)
+    NearList nearl;  // landings just below theta, re-checked after the round
     int32_t *overflow;
 };
 
@@ -368,6 +369,16 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
     for (int32_t t = 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const int64_t NC = (int64_t)*(volatile unsigned long long *)(A.candctr + cur);
+        {   // final |r| of last round's landings just below theta (common.cuh)
+            const int64_t nn = min((int64_t)*(volatile unsigned long long *)(A.nearl.cnt[cur]),
+                                   A.nearl.cap);
+            for (int64_t i = gtid; i < nn; i += nthreads) {
+                const int64_t key = A.nearl.key[cur][i];
+                const int32_t k = (int32_t)(key >> 32), v = (int32_t)(key & 0xffffffffLL);
+                if (below_theta(fabs(A.r[(int64_t)k * A.ld + v]), theta_of(A.op, v, A.g.deg[v])))
+                    A.s_amb[k] = 1;
+            }
+        }
         if (NC == 0) break;
         if (NC > A.candcap) {
             if (gtid == 0) A.overflow[0] = 1;
@@ -377,6 +388,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
         if (gtid == 0) {
             A.fctr[0] = 0ULL;
             A.candctr[nxt] = 0ULL;
+            *A.nearl.cnt[nxt] = 0ULL;
         }
         grid.sync();  // counter resets visible before any reservation
         // group only rounds with enough work to pay for the placement pass and
@@ -569,8 +581,9 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 const double th = theta_of(A.op, v[q], dv[q]);
                 const bool hot = valid[q] && fabs(nv) >= th;
                 // a node whose final |r| sits just below theta is never a
-                // candidate: its last update (which stores that value) flags it
-                if (valid[q] && near_theta(fabs(nv), th)) A.s_amb[k[q]] = 1;
+                // candidate: its landings there are re-read after the round
+                if (valid[q] && below_theta(fabs(nv), th))
+                    near_record(A.nearl, nxt, k[q], v[q], A.s_amb);
                 const bool nw = cand_mark(hot, k[q], v[q], A, nxt);
                 cand_stage(nw, k[q], v[q], S, A, nxt);
             }
@@ -821,6 +834,9 @@ struct SignedState {
     DBuf<double> coef_r, coef_m;
     DBuf<double> x, r, mom, fcval, s_l1, s_b1;
     DBuf<int32_t> mstamp, pushed, chunk_e, s_last, s_conv, s_amb, overflow;
+    DBuf<int64_t> nearkey;
+    DBuf<unsigned long long> nearcnt;
+    static constexpr int64_t NEAR_CAP = 1 << 16;
     DBuf<uint32_t> cm0, cm1, secmap;
     DBuf<int64_t> cand0, cand1, fkey, farc, frow, slot_base;
     DBuf<int2> colp;
@@ -882,6 +898,9 @@ struct SignedState {
         s_l1.alloc(slots); s_b1.alloc(slots); s_last.alloc(slots); s_conv.alloc(slots);
         s_amb.alloc(slots);
         GD_CUDA(cudaMemset(s_amb.p, 0, sizeof(int32_t) * slots));
+        nearkey.alloc(2 * NEAR_CAP);
+        nearcnt.alloc(2);
+        GD_CUDA(cudaMemset(nearcnt.p, 0, 2 * sizeof(unsigned long long)));
         slot_base.alloc(slots);
         GD_CUDA(cudaMemset(s_l1.p, 0, sizeof(double) * slots));
         GD_CUDA(cudaMemset(s_b1.p, 0, sizeof(double) * slots));
@@ -944,6 +963,7 @@ struct SignedState {
         A.chunk_e = chunk_e.p; A.fctr = fctr.p;
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_l1 = s_l1.p; A.s_b1 = s_b1.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
+        A.nearl = NearList{{nearkey.p, nearkey.p + NEAR_CAP}, {nearcnt.p, nearcnt.p + 1}, NEAR_CAP};
         A.overflow = overflow.p;
         return A;
     }
@@ -954,6 +974,7 @@ struct SignedState {
     }
 
     void rounds(SArgs &A, cudaStream_t st) {
+        GD_CUDA(cudaMemsetAsync(nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
         void *kargs[] = {&A};
         GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_signed_rounds, dim3(grid), dim3(SBT),
                                             kargs, smem, st));

@@ -175,6 +175,31 @@ __device__ __forceinline__ bool near_theta(double v, double th) {
     return fabs(__dsub_rn(v, th)) <= AMB_REL * th;
 }
 
+// Only a residual's FINAL value of a round decides membership, and partial
+// sums of a hub pass near theta all the time, so the detector tests final
+// values: the frontier entries of the next round (final r >= theta) in their
+// push phase, and -- for final values just below theta -- every update that
+// lands in [theta (1 - AMB_REL), theta) is recorded as (slot, node) and
+// re-read once the round is over (a later update may have moved it on).
+struct NearList {
+    int64_t *key[2];              // (slot << 32 | node), per round parity
+    unsigned long long *cnt[2];
+    int64_t cap;
+};
+
+__device__ __forceinline__ bool below_theta(double v, double th) {
+    return v < th && near_theta(v, th);
+}
+
+__device__ __forceinline__ void near_record(const NearList &L, int par, int32_t k, int32_t v,
+                                            int32_t *s_amb) {
+    const unsigned long long i = atomicAdd(L.cnt[par], 1ULL);
+    if (i < (unsigned long long)L.cap)
+        L.key[par][i] = ((int64_t)k << 32) | (uint32_t)v;
+    else
+        s_amb[k] = 1;  // list full: flag conservatively
+}
+
 // Bit-exact single-seed solve on the device (exact.cu): LocalGD (method
 // GD_M_LOCAL_GD, b = bval e_seed, frontier signed when sgn) or LocalCH
 // (GD_M_LOCAL_CH, bounds mu < L).  x and r are left in device buffers owned
