@@ -276,10 +276,15 @@ int gd_batch_fetch_r_host(gd_batch *b, int64_t n_seeds, int64_t *r_offset, int64
 /* Seeds of the last solve that the near-threshold detector flagged and the
  * bit-exact path re-solved (see gd_batch_result.ambiguous). */
 int gd_batch_last_ambiguous(const gd_batch *b, int64_t *count);
+/* The same count, how many of those seeds the exact re-solve changed
+ * (sweeps / operation counts / pushes differed from the batch's), and the
+ * host wall time (ms) the re-solves took. */
+int gd_batch_resolve_stats(const gd_batch *b, int64_t *flagged, int64_t *changed, double *ms);
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
-/* Execution form chosen at creation: GD_BATCH_ROUNDS (the wave round kernel,
+/* Execution form chosen at creation: GD_BATCH_STREAM (the round kernel, slots
+ * refilled in-kernel as seeds finish), GD_BATCH_ROUNDS (the wave round kernel,
  * k_rounds / k_signed_rounds), GD_BATCH_CTA (LocalGD on small graphs: one CTA
  * per seed, k_seed_cta) or GD_BATCH_FIFO (LocalSOR/GS, warp per seed); and
  * the number of seeds in flight. */
@@ -287,6 +292,8 @@ int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
 #define GD_BATCH_CTA 1
 #define GD_BATCH_FIFO 2
 #define GD_BATCH_FIFO_WIN 3 /* LocalSOR/GS in exact windows, one CTA per seed */
+#define GD_BATCH_STREAM 4   /* the round kernel with slots refilled in-kernel
+                               (k_rounds streaming form: LocalGD without want_r) */
 int gd_batch_info(const gd_batch *b, int32_t *mode, int64_t *slots);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */

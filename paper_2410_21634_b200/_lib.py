@@ -111,6 +111,7 @@ SIGNATURES = {
                                       _i64p, _i32p, _f64p, C.c_int64, _i64p, C.c_void_p]),
     "gd_batch_last_kernel_ms": (C.c_int, [C.c_void_p, _f64p]),
     "gd_batch_last_ambiguous": (C.c_int, [C.c_void_p, _i64p]),
+    "gd_batch_resolve_stats": (C.c_int, [C.c_void_p, _i64p, _i64p, _f64p]),
     "gd_batch_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), _i64p]),
     "gd_batch_r_device": (C.c_int, [C.c_void_p, C.POINTER(_i64p), C.POINTER(_i64p), C.POINTER(_i32p),
                                     C.POINTER(_f64p), _i64p]),

@@ -163,14 +163,22 @@ class BatchSolver:
         gdl.check(self.lib.gd_batch_last_ambiguous(self.handle, C.byref(c)))
         return int(c.value)
 
+    def resolve_stats(self) -> dict:
+        """Near-threshold re-solves of the last solve: seeds flagged, seeds
+        whose integer work the bit-exact re-solve changed, host ms spent."""
+        f, c, ms = C.c_int64(), C.c_int64(), C.c_double()
+        gdl.check(self.lib.gd_batch_resolve_stats(self.handle, C.byref(f), C.byref(c), C.byref(ms)))
+        return {"flagged": int(f.value), "changed": int(c.value), "ms": float(ms.value)}
+
     @property
     def mode(self) -> str:
-        """Execution form: "rounds" (wave round kernel), "cta" (one CTA per
+        """Execution form: "stream" (round kernel, slots refilled in-kernel:
+        LocalGD without want_r), "rounds" (wave round kernel), "cta" (one CTA per
         seed, LocalGD on small graphs), "fifo" (LocalSOR/GS, warp per seed) or
         "fifo-win" (LocalSOR/GS in exact windows, CTA per seed)."""
         m, s = C.c_int32(), C.c_int64()
         gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
-        return ("rounds", "cta", "fifo", "fifo-win")[m.value]
+        return ("rounds", "cta", "fifo", "fifo-win", "stream")[m.value]
 
     @property
     def slots(self) -> int:

@@ -35,6 +35,7 @@
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
+#include <chrono>
 #include <cmath>
 #include <vector>
 
@@ -163,6 +164,19 @@ struct RoundArgs {
     int64_t smw;        // words per slot in secmap
     int64_t *rlog;      // per round: F, P, globaltimer ns (3 entries), debug
     int64_t rlog_cap;   // rounds recorded
+    // streaming form (k_rounds<false, true>): slots refilled inside the kernel
+    const int64_t *seeds;         // the solve's seeds (caller ids)
+    int64_t n_seeds;
+    double alpha;
+    unsigned long long *seed_ctr; // next seed index to start
+    unsigned long long *done_ctr; // seeds finished since the solve began
+    int64_t seg_done;             // leave at a round start once done_ctr >= seg_done
+    int32_t *t_state;             // round to resume from (kept across launches)
+    int32_t *s_idx;               // per slot: seed index, -1 = idle
+    int32_t *s_t0;                // per slot: round of the seed's first push
+    unsigned long long *sn[2];    // per slot: entries in the frontier, per round parity
+    int64_t *drain_cnt;           // per slot: pushed count of the finished seed
+    int64_t reset_units;          // sector-map reset work units per finished slot
 };
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -240,11 +254,14 @@ struct Stage {
     unsigned *fcnt;                      // [1]
     unsigned long long *next;            // [1] phase-B chunk claim counter
     unsigned long long *scan;            // [BT/32 + 2]
+    unsigned *nf;                        // [S] next-frontier entries per slot (streaming)
+    int32_t *fin;                        // [S] slots whose seed finished (streaming)
+    unsigned *nfin;                      // [1]
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 + 8 * (BT / 32 + 3) +
-           64;
+    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 +
+           8 * (BT / 32 + 3) + 16 + 64;
 }
 
 __device__ Stage stage_carve(void *base, int S) {
@@ -262,7 +279,10 @@ __device__ Stage stage_carve(void *base, int S) {
     st.fcnt = (unsigned *)p; p += 16;
     st.fk = (int32_t *)p; p += 4 * STAGE_CAP;
     st.fv = (int32_t *)p; p += 4 * STAGE_CAP;
-    st.fd = (int32_t *)p;
+    st.fd = (int32_t *)p; p += 4 * STAGE_CAP;
+    st.nf = (unsigned *)p; p += 4 * S;
+    st.fin = (int32_t *)p; p += 4 * S;
+    st.nfin = (unsigned *)p;
     return st;
 }
 
@@ -283,6 +303,7 @@ __device__ __forceinline__ void stage_append(bool flag, int32_t k, int32_t v, in
                                              const Stage &S, const RoundArgs &A, int nxt) {
     unsigned am = __ballot_sync(FULL, flag);
     if (am == 0) return;
+    if (A.sn[0]) block_count(flag, k, 1u, S.nf);  // streaming: entries per slot
     const int lane = threadIdx.x & 31;
     unsigned base = 0;
     if (lane == 0) base = atomicAdd(S.fcnt, (unsigned)__popc(am));
@@ -368,6 +389,14 @@ __device__ void stage_flush(const Stage &S, const RoundArgs &A, int nxt) {
                 S.scnt[k] = 0;
             }
         }
+    if (A.sn[0])
+        for (int64_t k = tid; k < A.m; k += BT) {
+            const unsigned v = S.nf[k];
+            if (v) {
+                atomicAdd(A.sn[nxt] + k, (unsigned long long)v);
+                S.nf[k] = 0;
+            }
+        }
     __syncthreads();
     if (tid == 0) *S.fcnt = 0;
 }
@@ -415,6 +444,19 @@ __device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
     }
 }
 
+struct OutArgs {
+    int64_t *sweeps, *ops, *pushes, *support, *xoff, *xcnt;
+    int32_t *conv;
+    int32_t *xnodes;
+    double *xvals;
+    int64_t xcap;
+    const int32_t *inv;  // working id -> caller id (nullable)
+    double xscale;       // x out = fl(xscale * x) (heat kernel: e^-tau; else 1)
+    int hk;
+    int32_t *amb;                 // per seed: near-threshold flag
+    unsigned long long *amb_cnt;  // flagged seeds
+};
+
 // Heat kernel (HK = true, GD_M_HK): the stage-expanded push of
 // _hk_push_kernel (src/local_solvers.py:566-661).  Round t pops stage t and
 // feeds stage t+1 only (see hk.cu), so all seeds of a wave are at the same
@@ -422,25 +464,43 @@ __device__ void counters_flush(T *sc, unsigned long long *g, int64_t m) {
 // stage t+1 is cleared of its stage t-1 leftovers in phase A, and the
 // products are fl(fl(r * tau/(t+1)) * fl(1/d_u)).  x accumulates the pushed
 // values stage by stage -- the reference's stages.sum(axis=0) order.
-template <bool HK>
-__global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
+//
+// STREAM = true (LocalGD without sparse r): the slots are refilled inside the
+// kernel instead of running in synchronous waves.  A slot whose seed had no
+// frontier entries in a round (sn == 0) finished in the round before; in
+// that round every block lists it (same data, read after the barrier), and
+//   phase A: one thread reserves the seed's output segment and writes its
+//            counters; warps zero the slot's touched r sectors (sector map);
+//   phase B: warps copy x over its pushed list out (and zero it); one thread
+//            writes the near-threshold flag, takes the next seed from a
+//            counter (r[s] = alpha, counters reset) and appends it to the
+//            next frontier.
+// So a slot idles for one round between seeds, no round waits for the
+// slowest seed of a wave, and there are no extract / reset launches.  The
+// kernel leaves at a round start once `seg_done` seeds have finished (the
+// host copies their x out while the next launch runs) and resumes there.
+template <bool HK, bool STREAM = false>
+__global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs O) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Stage S = stage_carve(smem_raw, (int)A.m);
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
+    const int64_t gwarp = gtid >> 5, nwarps = nthreads >> 5;
     for (int64_t k = threadIdx.x; k < A.m; k += BT) {
         S.ops[k] = S.pvol[k] = S.scnt[k] = 0;
         S.push[k] = S.touch[k] = S.negz[k] = 0;
+        S.nf[k] = 0;
     }
     if (threadIdx.x == 0) {
         *S.fcnt = 0;
         *S.next = 0;
+        *S.nfin = 0;
     }
     __syncthreads();
 
-    for (int32_t t = 0;; ++t) {
+    for (int32_t t = STREAM ? *A.t_state : 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const unsigned long long packed = *(volatile unsigned long long *)(A.fctr + cur);
         const int64_t F = (int64_t)(packed >> CNT_SHIFT);
@@ -451,10 +511,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
             A.rlog[3 * t + 2] = globaltimer();
             A.rlog[3 * A.rlog_cap] = t + 1;
         }
+        int64_t nn = 0;
         {   // final values of last round's landings just below theta (common.cuh)
             double *const rl = (HK && (t & 1)) ? A.r2 : A.r;
-            const int64_t nn = min((int64_t)*(volatile unsigned long long *)(A.nearl.cnt[cur]),
-                                   A.nearl.cap);
+            nn = min((int64_t)*(volatile unsigned long long *)(A.nearl.cnt[cur]), A.nearl.cap);
             for (int64_t i = gtid; i < nn; i += nthreads) {
                 const int64_t key = A.nearl.key[cur][i];
                 const int32_t k = (int32_t)(key >> 32), v = (int32_t)(key & 0xffffffffLL);
@@ -462,12 +522,32 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                     A.s_amb[k] = 1;
             }
         }
-        if (F == 0) break;
+        unsigned nfin = 0;
+        if (STREAM) {
+            // seeds that finished: running slots without entries this round
+            for (int64_t k = threadIdx.x; k < A.m; k += BT)
+                if (A.s_idx[k] >= 0 && *(volatile unsigned long long *)(A.sn[cur] + k) == 0ULL)
+                    S.fin[atomicAdd(S.nfin, 1u)] = (int32_t)k;
+            __syncthreads();
+            nfin = *S.nfin;
+            const unsigned long long done = *(volatile unsigned long long *)A.done_ctr;
+            if ((F == 0 && nfin == 0) || (int64_t)done >= A.seg_done) {
+                if (gtid == 0) *A.t_state = t;
+                break;
+            }
+            if (nn > 0) grid.sync();  // (the reset below must not overtake those reads)
+        } else if (F == 0) {
+            break;
+        }
         if (((P + 31) >> 5) > A.ccap) {  // arc-chunk map too small: report, stop
             if (gtid == 0) A.overflow[0] = 1;
             break;
         }
-        if (t >= A.max_sweeps || F > A.fcap) {
+        if (STREAM && F > A.fcap) {  // (per-slot sweep caps below)
+            if (gtid == 0) A.overflow[0] = 1;
+            break;
+        }
+        if (!STREAM && (t >= A.max_sweeps || F > A.fcap)) {
             for (int64_t e = gtid; e < F && e < A.fcap; e += nthreads)
                 A.s_conv[A.ukey[e] >> 32] = 0;
             break;
@@ -483,7 +563,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
             A.cctr[0] = 0ULL;
             *A.nearl.cnt[nxt] = 0ULL;  // (last read two barriers ago)
         }
-        for (int64_t k = gtid; k < A.m; k += nthreads) A.scnt[nxt][k] = 0ULL;
+        for (int64_t k = gtid; k < A.m; k += nthreads) {
+            A.scnt[nxt][k] = 0ULL;
+            if (STREAM) A.sn[nxt][k] = 0ULL;
+        }
         double *const rc = (HK && (t & 1)) ? A.r2 : A.r;        // layer t
         double *const rn = (HK && !(t & 1)) ? A.r2 : A.r;       // layer t+1 (HK)
         uint32_t *const mapn = (HK && !(t & 1)) ? A.secmap2 : A.secmap;
@@ -523,17 +606,24 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
             int64_t clo = 0, chi = 0, cfull = 0, pos = 0;
             int64_t key = 0;
             double val = 0.0, xo = 0.0;
+            bool capped = false;  // (streaming) the seed's sweep cap: not pushed
             if (live) {
                 key = A.ukey[e];
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
                 const int64_t idx = (int64_t)k * A.ld + u;
-                val = rc[idx];
-                xo = A.x[idx];
-                A.x[idx] = __dadd_rn(xo, val);
-                rc[idx] = HK ? 0.0 : -0.0;
                 d = A.g.deg[u];
-                if (near_theta(val, theta_deg(A.tcoeff, d))) A.s_amb[k] = 1;  // final r >= theta
+                capped = STREAM && (int64_t)(t - A.s_t0[k]) >= A.max_sweeps;
+                if (!capped) {
+                    val = rc[idx];
+                    xo = A.x[idx];
+                    A.x[idx] = __dadd_rn(xo, val);
+                    rc[idx] = HK ? 0.0 : -0.0;
+                    if (near_theta(val, theta_deg(A.tcoeff, d))) A.s_amb[k] = 1;  // final r >= theta
+                } else {
+                    A.s_conv[k] = 0;
+                    xo = 1.0;  // (not a first push)
+                }
             }
             // group-sorted position: one packed reservation per (warp, slot group);
             // ungrouped: the entry keeps its append position and arc offset
@@ -565,9 +655,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                 A.sarc[pos] = a0;
                 A.frow[pos] = A.g.row[u];
                 A.fcval[pos] =
-                    HK ? __dmul_rn(__dmul_rn(val, A.stage_w[t < A.n_stages ? t : 0]),
-                                   __ddiv_rn(1.0, (double)d))
-                       : __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                    capped ? 0.0  // (phase B skips c == 0)
+                    : HK ? __dmul_rn(__dmul_rn(val, A.stage_w[t < A.n_stages ? t : 0]),
+                                     __ddiv_rn(1.0, (double)d))
+                         : __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
                 fresh = __double_as_longlong(xo) == 0;  // first push of u
                 // chunks (32 arcs) whose first arc lies in this entry: [clo, chi)
                 clo = (a0 + 31) >> 5;
@@ -589,11 +680,58 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                 for (int64_t c = lo2 + lane; c < hi2; c += 32)
                     A.chunk_e[c] = (int32_t)(e2 | (c < cf2 ? 0x80000000u : 0u));
             }
-        slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
+            const bool pushed = live && !capped;
+            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
-            block_count(live, k, (unsigned)d, S.ops);
-            block_count(live, k, 1u, S.push);
-            if (live) A.s_last[k] = t;
+            block_count(pushed, k, (unsigned)d, S.ops);
+            block_count(pushed, k, 1u, S.push);
+            if (pushed) A.s_last[k] = t;
+        }
+        if (STREAM && nfin) {
+            // finished seeds: output segment + counters (one thread each) ...
+            for (int64_t j = gtid; j < nfin; j += nthreads) {
+                const int32_t k = S.fin[j];
+                const int64_t si = A.s_idx[k];
+                const unsigned long long pc = A.pushed_cnt[k];
+                const int64_t b = (int64_t)atomicAdd(A.cursor, pc);
+                A.slot_base[k] = b;
+                A.drain_cnt[k] = (int64_t)pc;
+                const int64_t pushes = (int64_t)A.s_pushes[k];
+                O.sweeps[si] = (int64_t)(A.s_last[k] - A.s_t0[k]) + 1;
+                O.ops[si] = (int64_t)A.s_ops[k];
+                O.pushes[si] = pushes;
+                O.conv[si] = A.s_conv[k];
+                O.support[si] = (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
+                O.xoff[si] = b;
+                O.xcnt[si] = (int64_t)pc;
+                atomicAdd(A.done_ctr, 1ULL);
+            }
+            // ... and their r back to +0.0: zero the marked sectors, clear the map
+            const int64_t units = (int64_t)nfin * A.reset_units;
+            const int64_t per = (A.smw + A.reset_units - 1) / A.reset_units;
+            for (int64_t u = gwarp; u < units; u += nwarps) {
+                const int32_t k = S.fin[u / A.reset_units];
+                const int64_t lo = (u % A.reset_units) * per, hi = min(A.smw, lo + per);
+                uint32_t *map = A.secmap + (int64_t)k * A.smw;
+                double *rk = A.r + (int64_t)k * A.ld;
+                for (int64_t w0 = lo; w0 < hi; w0 += 32) {
+                    const uint32_t mine = (w0 + lane < hi) ? map[w0 + lane] : 0u;
+                    unsigned any = __ballot_sync(FULL, mine != 0u);
+                    while (any) {
+                        const int src = __ffs(any) - 1;
+                        any &= any - 1;
+                        const uint32_t wb = __shfl_sync(FULL, mine, src);
+                        if ((wb >> lane) & 1u) {
+                            const int64_t sec = (w0 + src) * 32 + lane;
+                            if (4 * sec + 3 < A.ld)
+                                reinterpret_cast<double4 *>(rk)[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+                            else
+                                for (int64_t i = 4 * sec; i < A.ld; ++i) rk[i] = 0.0;
+                        }
+                    }
+                    if (mine) map[w0 + lane] = 0u;
+                }
+            }
         }
         __syncthreads();
         counters_flush(S.ops, A.s_ops, A.m);
@@ -606,6 +744,57 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
         // one atomic in flight per chunk), so the whole grid sweeps the arc
         // space front to back, slot by slot, without a claim counter.
         for (int64_t k = gtid; k < A.m; k += nthreads) A.sfill[k] = 0ULL;  // for the next round
+        if (STREAM && nfin) {
+            // finished seeds: x over the pushed list out (caller ids), zeroed
+            constexpr int64_t XU = 32;  // extract units per slot
+            for (int64_t u = gwarp; u < (int64_t)nfin * XU; u += nwarps) {
+                const int32_t k = S.fin[u / XU];
+                const int64_t pc = A.drain_cnt[k], b = A.slot_base[k];
+                const int64_t lo = (u % XU) * pc / XU, hi = (u % XU + 1) * pc / XU;
+                const int64_t off = (int64_t)k * A.ld;
+                for (int64_t i = lo + lane; i < hi; i += 32) {
+                    const int32_t v = A.pushed[off + i];
+                    const double xv = A.x[off + v];
+                    A.x[off + v] = 0.0;
+                    if (b + i < O.xcap) {
+                        O.xnodes[b + i] = O.inv ? __ldg(O.inv + v) : v;
+                        O.xvals[b + i] = xv;
+                    }
+                }
+            }
+            // the near-threshold flag (final now), then the slot's next seed
+            for (int64_t j0 = gwarp * 32; j0 < nfin; j0 += nwarps * 32) {
+                const int64_t j = j0 + lane;
+                bool act = false;
+                int32_t k = 0, s = 0, d = 0;
+                if (j < nfin) {
+                    k = S.fin[j];
+                    const int64_t si = A.s_idx[k];
+                    O.amb[si] = A.s_amb[k];
+                    if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
+                    const unsigned long long i = atomicAdd(A.seed_ctr, 1ULL);
+                    if ((int64_t)i < A.n_seeds) {
+                        s = (int32_t)A.seeds[i];
+                        if (A.perm) s = A.perm[s];
+                        A.s_idx[k] = (int32_t)i;
+                        A.s_t0[k] = t + 1;
+                        A.s_last[k] = t;  // (sweeps = s_last - t0 + 1)
+                        A.r[(int64_t)k * A.ld + s] = A.alpha;
+                        A.secmap[(int64_t)k * A.smw + (s >> 7)] |= 1u << ((s >> 2) & 31);
+                        A.touched[k] = 1;
+                        A.pushed_cnt[k] = 0;
+                        A.s_ops[k] = A.s_pushes[k] = A.s_negz[k] = A.s_pvol[k] = 0;
+                        A.s_conv[k] = 1;
+                        A.s_amb[k] = 0;
+                        d = A.g.deg[s];
+                        act = A.alpha >= theta_deg(A.tcoeff, d);
+                    } else {
+                        A.s_idx[k] = -1;  // no seeds left: idle
+                    }
+                }
+                stage_append(act, k, s, d, S, A, nxt);
+            }
+        }
         const int64_t C = (P + 31) >> 5;
         const int64_t *fa = A.sarc;
         if (!HK || t < A.n_stages) {  // (the last heat-kernel stage is absorbing)
@@ -658,6 +847,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
                     const int2 vd = __ldg(A.colp + A.frow[me] + (p - fa[me]));
                     v[q] = vd.x;
                     dv[q] = vd.y;
+                    if (STREAM) valid[q] = c[q] != 0.0;  // (an entry past its seed's sweep cap)
                 }
             }
             // stage 2: the atomics, back to back (UNROLL in flight per lane)
@@ -683,13 +873,16 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A) {
           }
         }
         stage_flush(S, A, nxt);  // (its barriers also order the claim counter reset)
-        if (threadIdx.x == 0) *S.next = 0;
+        if (threadIdx.x == 0) {
+            *S.next = 0;
+            *S.nfin = 0;
+        }
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
     }
     // reserve each slot's output segment (pushed counts are final here)
-    if (blockIdx.x == 0)
+    if (!STREAM && blockIdx.x == 0)
         for (int64_t k = threadIdx.x; k < A.m; k += BT)
             A.slot_base[k] = (int64_t)atomicAdd(A.cursor, A.pushed_cnt[k]);
 }
@@ -714,7 +907,19 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     A.s_amb[k] = 0;
     int32_t d = A.g.deg[s];
     A.sfill[k] = 0ULL;
-    if (alpha >= theta_deg(A.tcoeff, d)) {
+    const bool act = alpha >= theta_deg(A.tcoeff, d);
+    if (A.s_idx) {  // streaming form: slot k starts seed k; the rest follow in-kernel
+        A.s_idx[k] = (int32_t)k;
+        A.s_t0[k] = 0;
+        A.sn[0][k] = act ? 1ULL : 0ULL;
+        A.sn[1][k] = 0ULL;
+        if (k == 0) {
+            *A.seed_ctr = (unsigned long long)A.m;
+            *A.done_ctr = 0ULL;
+            *A.t_state = 0;
+        }
+    }
+    if (act) {
         unsigned long long old = atomicAdd(A.fctr, (1ULL << CNT_SHIFT) + (unsigned long long)d);
         int64_t idx = (int64_t)(old >> CNT_SHIFT);
         if (idx < A.fcap) {
@@ -726,18 +931,6 @@ __global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, doub
     }
 }
 
-struct OutArgs {
-    int64_t *sweeps, *ops, *pushes, *support, *xoff, *xcnt;
-    int32_t *conv;
-    int32_t *xnodes;
-    double *xvals;
-    int64_t xcap;
-    const int32_t *inv;  // working id -> caller id (nullable)
-    double xscale;       // x out = fl(xscale * x) (heat kernel: e^-tau; else 1)
-    int hk;
-    int32_t *amb;                 // per seed: near-threshold flag
-    unsigned long long *amb_cnt;  // flagged seeds
-};
 
 // grid (CHUNKS, slots): copy x over the pushed list out (caller ids) and zero
 // x and r there; block (0, k) writes the seed's counters.
@@ -990,11 +1183,19 @@ struct gd_batch {
     DBuf<double> x, r, fcval;
     DBuf<int32_t> pushed, seed, s_last, s_conv, s_amb, overflow;
     DBuf<int32_t> amb;               // per seed: near-threshold flag of the last solve
+    // streaming form of the round kernel (k_rounds<false, true>)
+    bool stream = false;
+    int sgrid = 0;                   // its cooperative grid
+    DBuf<int32_t> s_idx, s_t0, t_state;
+    DBuf<unsigned long long> sn, sctr;  // per slot entries [2][slots]; seed / done counters
+    DBuf<int64_t> drain_cnt;
     DBuf<int64_t> nearkey;           // near list: 2 x NEAR_CAP keys + 2 counters
     DBuf<unsigned long long> nearcnt;
     static constexpr int64_t NEAR_CAP = 1 << 16;
     DBuf<unsigned long long> amb_cnt;
     int64_t last_amb = 0;            // seeds re-solved on the exact path
+    int64_t last_changed = 0;        // ... whose integer work the re-solve changed
+    double last_resolve_ms = 0.0;    // host wall time of the re-solves
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
     DBuf<int64_t> ukey, uarc, skey, sarc, frow, slot_base;
     DBuf<unsigned long long> scnt, sfill, cctr;
@@ -1076,6 +1277,18 @@ struct gd_batch {
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
         A.nearl = NearList{{nearkey.p, nearkey.p + NEAR_CAP}, {nearcnt.p, nearcnt.p + 1}, NEAR_CAP};
+        if (stream) {
+            A.alpha = p.alpha;
+            A.seed_ctr = sctr.p;
+            A.done_ctr = sctr.p + 1;
+            A.t_state = t_state.p;
+            A.s_idx = s_idx.p;
+            A.s_t0 = s_t0.p;
+            A.sn[0] = sn.p;
+            A.sn[1] = sn.p + slots;
+            A.drain_cnt = drain_cnt.p;
+            A.reset_units = (int64_t)reset_chunks();
+        }
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
         A.cursor = cursor.p;
@@ -1217,7 +1430,31 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
               B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr,
               B->hk ? std::exp(-B->p.tau) : 1.0, B->hk ? 1 : 0, B->amb.p, B->amb_cnt.p};
     int64_t launches = 0;
-    for (int64_t w = 0; w < waves; ++w) {
+    if (B->stream) {
+        // one state for the whole solve; a launch per `slots` finished seeds
+        RoundArgs A = B->args();
+        A.m = n_seeds < B->slots ? n_seeds : B->slots;
+        A.seeds = d_seeds;
+        A.n_seeds = n_seeds;
+        GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
+        GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
+        GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
+        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds, B->p.alpha);
+        GD_LAUNCH_CHECK();
+        launches += 1;
+        for (int64_t w = 0; w < waves; ++w) {
+            A.seg_done = (w + 1) * B->slots < n_seeds ? (w + 1) * B->slots : n_seeds;
+            GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
+            void *kargs[] = {&A, &O};
+            GD_CUDA(cudaLaunchCooperativeKernel((const void *)k_rounds<false, true>,
+                                                dim3(B->sgrid), dim3(BT), kargs,
+                                                stage_bytes(B->slots), st));
+            GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
+            launches += 1;
+            B->hs_wave(w, waves, st);
+        }
+    }
+    for (int64_t w = 0; w < waves && !B->stream; ++w) {
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
@@ -1228,7 +1465,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
                                                                B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
-        void *kargs[] = {&A};
+        void *kargs[] = {&A, &O};
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
         GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
@@ -1397,6 +1634,9 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     unsigned long long cnt = 0;
     GD_CUDA(cudaMemcpy(&cnt, B->amb_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
     B->last_amb = (int64_t)cnt;
+    B->last_changed = 0;
+    B->last_resolve_ms = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
     const bool all = B->p.exact_all != 0;
     if ((!cnt && !all) || B->hk || B->fifo) return;  // (heat kernel: reported, not re-solved)
     std::vector<int32_t> amb(n_seeds);
@@ -1415,9 +1655,15 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));  // pools may move
     for (int64_t i = 0; i < n_seeds; ++i) {
         if (!amb[i] && !all) continue;
+        int64_t before[3] = {0, 0, 0};  // the batch's sweeps, ops, pushes (diagnostic)
+        GD_CUDA(cudaMemcpy(&before[0], B->sweeps.p + i, 8, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(&before[1], B->ops.p + i, 8, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(&before[2], B->pushes.p + i, 8, cudaMemcpyDeviceToHost));
         const ExactSeed e = exact_seed_solve(B->G, &op, ch ? GD_M_LOCAL_CH : GD_M_LOCAL_GD,
                                              seeds[i], bval, B->p.mu, B->p.L, B->p.max_sweeps,
                                              false, st);
+        if (before[0] != e.sweeps || before[1] != e.ops || (!ch && before[2] != e.pushes))
+            B->last_changed += 1;
         unsigned long long *tmp = B->cursor.p;  // (free again: the solve's total is on the host)
         unsigned long long nz[2] = {0, 0};
         GD_CUDA(cudaMemset(tmp, 0, sizeof(unsigned long long)));
@@ -1471,6 +1717,8 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     const unsigned long long tot = (unsigned long long)B->last_x_total;
     GD_CUDA(cudaMemcpy(B->cursor.p, &tot, sizeof(tot), cudaMemcpyHostToDevice));
     GD_CUDA(cudaDeviceSynchronize());
+    B->last_resolve_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 extern "C" {
@@ -1648,6 +1896,22 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, BT, smem));
             GD_CHECK_ARG(per_sm > 0, "round kernel does not fit on an SM");
             B->grid = per_sm * n_sms(G->device);
+            // streaming form (slots refilled in-kernel) for LocalGD without
+            // sparse r; GDIFF_STREAM=0 keeps the synchronous waves (A/B, read
+            // here once)
+            B->stream = !B->hk && !B->want_r();
+            if (const char *e = getenv("GDIFF_STREAM")) B->stream = B->stream && atoi(e) != 0;
+            if (B->stream) {
+                const void *sfn = (const void *)k_rounds<false, true>;
+                GD_CUDA(cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                int ps = 0;
+                GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, sfn, BT, smem));
+                GD_CHECK_ARG(ps > 0, "streaming round kernel does not fit on an SM");
+                B->sgrid = ps * n_sms(G->device);
+                B->s_idx.alloc(slots); B->s_t0.alloc(slots); B->t_state.alloc(1);
+                B->sn.alloc(2 * (size_t)slots); B->sctr.alloc(2); B->drain_cnt.alloc(slots);
+            }
             if (!B->hk && !B->want_r() && p->frontier_cap <= 0) {
                 // small graphs: sweeps scatter too few arcs to amortise two grid
                 // barriers, so each seed runs in a CTA of its own (batch_cta.cu)
@@ -1866,6 +2130,14 @@ int gd_batch_last_ambiguous(const gd_batch *B, int64_t *count) {
     return GD_OK;
 }
 
+int gd_batch_resolve_stats(const gd_batch *B, int64_t *flagged, int64_t *changed, double *ms) {
+    if (!B || !flagged || !changed || !ms) return GD_ERR_ARG;
+    *flagged = B->last_amb;
+    *changed = B->last_changed;
+    *ms = B->last_resolve_ms;
+    return GD_OK;
+}
+
 int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {
     if (!B || !ms) return GD_ERR_ARG;
     *ms = B->last_ms;
@@ -1875,7 +2147,9 @@ int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {
 int gd_batch_info(const gd_batch *B, int32_t *mode, int64_t *slots) {
     if (!B || !mode || !slots) return GD_ERR_ARG;
     *mode = B->cta ? GD_BATCH_CTA
-                   : (B->sorwin ? GD_BATCH_FIFO_WIN : (B->fifo ? GD_BATCH_FIFO : GD_BATCH_ROUNDS));
+                   : (B->sorwin ? GD_BATCH_FIFO_WIN
+                                : (B->fifo ? GD_BATCH_FIFO
+                                           : (B->stream ? GD_BATCH_STREAM : GD_BATCH_ROUNDS)));
     *slots = B->cta ? (int64_t)cta_batch_slots(B->cta) : (int64_t)B->slots;
     return GD_OK;
 }

@@ -28,13 +28,20 @@ def _check_x(out, i, x_ref):
     assert np.array_equal(np.argsort(-x, kind="stable")[:10], top)
 
 
-MODES = ["cta", "rounds"]  # one CTA per seed (small graphs) / the round kernel (large graphs)
+# one CTA per seed (small graphs) / the round kernel with slots refilled in-kernel
+# (large graphs) / the same kernel in synchronous waves (GDIFF_STREAM=0)
+MODES = ["cta", "stream", "waves"]
+
+
+def set_mode(monkeypatch, mode):
+    monkeypatch.setenv("GDIFF_BATCH_MODE", "cta" if mode == "cta" else "rounds")
+    monkeypatch.setenv("GDIFF_STREAM", "0" if mode == "waves" else "1")
 
 
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("slots,relabel", [(0, True), (1, True), (7, False), (64, True), (64, False)])
 def test_cora_config1_batch(gpu, cora, monkeypatch, mode, slots, relabel):
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     g = golden_graph(cora, "cora")
     seeds = cora["seeds"]
     out = local_gd_batch(g, seeds, 0.1, 1e-6, slots=slots, relabel=relabel)
@@ -58,7 +65,7 @@ def test_pa_batch_matches_reference(gpu, pa):
 
 @pytest.mark.parametrize("mode", MODES)
 def test_rmat_batch_matches_oracle(gpu, monkeypatch, mode):
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 48, seed=0)
     ref = O.batch_local_gd(g, 0.1, 1e-6, seeds, threads=8)
@@ -74,7 +81,7 @@ def test_rmat_batch_matches_oracle(gpu, monkeypatch, mode):
 @pytest.mark.parametrize("mode", MODES)
 def test_solver_reuse_and_device_path(gpu, monkeypatch, mode):
     import torch
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     g = rmat_graph(5000, 30000, seed=9)
     seeds = sample_sources(g, 40, seed=1)
     solver = BatchSolver(g, 0.15, 1e-5, slots=8)
@@ -85,14 +92,15 @@ def test_solver_reuse_and_device_path(gpu, monkeypatch, mode):
     d = solver.solve_device(torch.as_tensor(seeds, device="cuda"))
     assert np.array_equal(d["total_ops"].cpu().numpy(), a["total_ops"])
     assert np.array_equal(d["sweeps"].cpu().numpy(), a["sweeps"])
-    assert d["kernel_launches"] == (4 * 5 if mode == "rounds" else 1)
+    assert d["kernel_launches"] == {"waves": 4 * 5, "stream": 1 + 5, "cta": 1}[mode]
+    assert solver.mode == {"waves": "rounds", "stream": "stream", "cta": "cta"}[mode]
     assert solver.last_kernel_ms > 0.0
 
 
 @pytest.mark.parametrize("mode", MODES)
 def test_edge_cases(gpu, monkeypatch, mode):
     from paper_2410_21634_b200.graph import from_edges
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     # isolated nodes, a leaf, max_sweeps cap, empty batch
     g = from_edges(6, [(0, 1), (1, 2), (2, 0), (3, 4)])
     out = local_gd_batch(g, [0, 3], 0.2, 1e-9, max_sweeps=2)
@@ -193,7 +201,7 @@ def test_batch_edge_cases(gpu, monkeypatch, mode):
     """Empty batches, duplicate seeds, sweep caps and a frontier-capacity
     overflow (reported as an error, the solver stays usable)."""
     from paper_2410_21634_b200._lib import GdiffError
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     g = rmat_graph(5000, 30000, seed=4)
     seeds = sample_sources(g, 24, seed=2)
     for method in ("local-gd", "local-ch", "local-sor"):
@@ -295,7 +303,7 @@ def test_host_entry_streams_x_per_wave(gpu, monkeypatch, mode):
     wave runs: the host result equals a device-path solve per seed, on a cold
     call (host buffers too small: capacity path) and on warm calls."""
     import torch
-    monkeypatch.setenv("GDIFF_BATCH_MODE", mode)
+    set_mode(monkeypatch, mode)
     g = rmat_graph(20000, 150000, seed=3)
     seeds = sample_sources(g, 70, seed=4)
     solver = BatchSolver(g, 0.1, 1e-6, slots=8)
