@@ -35,7 +35,11 @@
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
+#include <atomic>
 #include <chrono>
+#include <mutex>
+#include <string>
+#include <thread>
 #include <cmath>
 #include <vector>
 
@@ -524,10 +528,21 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
         }
         unsigned nfin = 0;
         if (STREAM) {
-            // seeds that finished: running slots without entries this round
-            for (int64_t k = threadIdx.x; k < A.m; k += BT)
-                if (A.s_idx[k] >= 0 && *(volatile unsigned long long *)(A.sn[cur] + k) == 0ULL)
-                    S.fin[atomicAdd(S.nfin, 1u)] = (int32_t)k;
+            // seeds that finished: running slots without entries this round,
+            // listed in slot order (every block must see the same list: the
+            // work units below are split across blocks by position in it)
+            if (threadIdx.x < 32) {
+                unsigned cnt = 0;
+                for (int64_t k0 = 0; k0 < A.m; k0 += 32) {
+                    const int64_t k = k0 + lane;
+                    const bool f = k < A.m && A.s_idx[k] >= 0 &&
+                                   *(volatile unsigned long long *)(A.sn[cur] + k) == 0ULL;
+                    const unsigned b = __ballot_sync(FULL, f);
+                    if (f) S.fin[cnt + __popc(b & lanemask_lt())] = (int32_t)k;
+                    cnt += __popc(b);
+                }
+                if (lane == 0) *S.nfin = cnt;
+            }
             __syncthreads();
             nfin = *S.nfin;
             const unsigned long long done = *(volatile unsigned long long *)A.done_ctr;
@@ -1194,6 +1209,8 @@ struct gd_batch {
     static constexpr int64_t NEAR_CAP = 1 << 16;
     DBuf<unsigned long long> amb_cnt;
     int64_t last_amb = 0;            // seeds re-solved on the exact path
+    static constexpr size_t RESOLVE_WORKERS = 8;
+    std::vector<ExactWorker *> workers;  // exact re-solve workers (created on demand)
     int64_t last_changed = 0;        // ... whose integer work the re-solve changed
     double last_resolve_ms = 0.0;    // host wall time of the re-solves
     DBuf<unsigned long long> touched, pushed_cnt, fctr, s_ops, s_pushes, s_negz, s_pvol, cursor;
@@ -1331,6 +1348,7 @@ struct gd_batch {
         if (w == waves - 1) hs_drain(w);
     }
     ~gd_batch() {
+        for (auto w : workers) exact_worker_destroy(w);
         if (hs.curh) cudaFreeHost(hs.curh);
         for (auto e : hs.wev) cudaEventDestroy(e);
         if (hs.cs) cudaStreamDestroy(hs.cs);
@@ -1614,6 +1632,7 @@ __global__ void k_emit_nz(const double *__restrict__ v, int64_t n, double scale,
 // grow a device pool to `cap` entries keeping its first `used`
 template <class T>
 static void grow_keep(DBuf<T> &b, size_t cap, size_t used) {
+    GD_CUDA(cudaDeviceSynchronize());  // (emits of other workers into the old pool)
     DBuf<T> nb(cap);
     if (used) GD_CUDA(cudaMemcpy(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice));
     std::swap(b.p, nb.p);
@@ -1636,13 +1655,21 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     B->last_amb = (int64_t)cnt;
     B->last_changed = 0;
     B->last_resolve_ms = 0.0;
-    const auto t0 = std::chrono::steady_clock::now();
     const bool all = B->p.exact_all != 0;
     if ((!cnt && !all) || B->hk || B->fifo) return;  // (heat kernel: reported, not re-solved)
+    const auto t0 = std::chrono::steady_clock::now();
+    GD_CUDA(cudaStreamSynchronize(st));
     std::vector<int32_t> amb(n_seeds);
-    std::vector<int64_t> seeds(n_seeds);
+    std::vector<int64_t> seeds(n_seeds), before(3 * n_seeds);
     GD_CUDA(cudaMemcpy(amb.data(), B->amb.p, sizeof(int32_t) * n_seeds, cudaMemcpyDeviceToHost));
     GD_CUDA(cudaMemcpy(seeds.data(), d_seeds, sizeof(int64_t) * n_seeds, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(before.data(), B->sweeps.p, 8 * n_seeds, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(before.data() + n_seeds, B->ops.p, 8 * n_seeds, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(before.data() + 2 * n_seeds, B->pushes.p, 8 * n_seeds,
+                       cudaMemcpyDeviceToHost));
+    std::vector<int64_t> todo;
+    for (int64_t i = 0; i < n_seeds; ++i)
+        if (amb[i] || all) todo.push_back(i);
     const bool ch = B->p.method == GD_M_LOCAL_CH, katz = B->p.problem == GD_P_KATZ;
     gd_operator op{};
     op.weight_rule = katz ? GD_W_CONST : GD_W_RW;
@@ -1653,70 +1680,101 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     const int64_t n = B->G->n;
     const int nb = 4 * n_sms(B->G->device);
     if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));  // pools may move
-    for (int64_t i = 0; i < n_seeds; ++i) {
-        if (!amb[i] && !all) continue;
-        int64_t before[3] = {0, 0, 0};  // the batch's sweeps, ops, pushes (diagnostic)
-        GD_CUDA(cudaMemcpy(&before[0], B->sweeps.p + i, 8, cudaMemcpyDeviceToHost));
-        GD_CUDA(cudaMemcpy(&before[1], B->ops.p + i, 8, cudaMemcpyDeviceToHost));
-        GD_CUDA(cudaMemcpy(&before[2], B->pushes.p + i, 8, cudaMemcpyDeviceToHost));
-        const ExactSeed e = exact_seed_solve(B->G, &op, ch ? GD_M_LOCAL_CH : GD_M_LOCAL_GD,
-                                             seeds[i], bval, B->p.mu, B->p.L, B->p.max_sweeps,
-                                             false, st);
-        if (before[0] != e.sweeps || before[1] != e.ops || (!ch && before[2] != e.pushes))
-            B->last_changed += 1;
-        unsigned long long *tmp = B->cursor.p;  // (free again: the solve's total is on the host)
-        unsigned long long nz[2] = {0, 0};
-        GD_CUDA(cudaMemset(tmp, 0, sizeof(unsigned long long)));
-        k_count_nz<<<nb, 256>>>(e.x, n, tmp);
-        GD_LAUNCH_CHECK();
-        GD_CUDA(cudaMemcpy(&nz[0], tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        GD_CUDA(cudaMemset(tmp, 0, sizeof(unsigned long long)));
-        k_count_nz<<<nb, 256>>>(e.r, n, tmp);
-        GD_LAUNCH_CHECK();
-        GD_CUDA(cudaMemcpy(&nz[1], tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        const int64_t xb = B->last_x_total;
-        if (xb + (int64_t)nz[0] > B->xcap) {
-            const int64_t cap = 2 * (xb + (int64_t)nz[0]);
-            grow_keep(B->xnodes, (size_t)cap, (size_t)xb);
-            grow_keep(B->xvals, (size_t)cap, (size_t)xb);
-            B->xcap = cap;
-        }
-        unsigned long long c0 = (unsigned long long)xb;
-        GD_CUDA(cudaMemcpy(tmp, &c0, sizeof(c0), cudaMemcpyHostToDevice));
-        k_emit_nz<<<nb, 256>>>(e.x, n, 1.0, B->xnodes.p, B->xvals.p, tmp);
-        GD_LAUNCH_CHECK();
-        B->last_x_total = xb + (int64_t)nz[0];
-        const int64_t sw = e.sweeps, ops = e.ops, pu = e.pushes, sup = (int64_t)nz[1];
-        const int64_t xc = (int64_t)nz[0];
-        const int32_t cv = e.converged;
-        GD_CUDA(cudaMemcpy(B->sweeps.p + i, &sw, 8, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->ops.p + i, &ops, 8, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->pushes.p + i, &pu, 8, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->support.p + i, &sup, 8, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->conv.p + i, &cv, 4, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->xoff.p + i, &xb, 8, cudaMemcpyHostToDevice));
-        GD_CUDA(cudaMemcpy(B->xcnt.p + i, &xc, 8, cudaMemcpyHostToDevice));
-        if (B->want_r()) {
-            const int64_t rb = B->last_r_total;
-            if (rb + (int64_t)nz[1] > B->rcap) {
-                const int64_t cap = 2 * (rb + (int64_t)nz[1]);
-                grow_keep(B->rnodes, (size_t)cap, (size_t)rb);
-                grow_keep(B->rvals, (size_t)cap, (size_t)rb);
-                B->rcap = cap;
+    // Up to GD_RESOLVE_WORKERS seeds at a time, each on its own worker (own
+    // buffers and stream): one exact solve is a chain of small dependent
+    // kernels and host syncs, so concurrent seeds overlap on the device.
+    const size_t T = std::min<size_t>(todo.size(), gd_batch::RESOLVE_WORKERS);
+    while (B->workers.size() < T) B->workers.push_back(exact_worker_create());
+    std::atomic<size_t> next{0};
+    std::mutex mu;  // output pools, cursor and per-seed records
+    std::atomic<int> err{GD_OK};
+    std::string errmsg;
+    std::atomic<int64_t> changed{0};
+    auto work = [&](size_t w) {
+        try {
+            GD_CUDA(cudaSetDevice(B->G->device));
+            ExactWorker *W = B->workers[w];
+            const cudaStream_t ws = exact_worker_stream(W);
+            DBuf<unsigned long long> cnts(2);
+            for (;;) {
+                const size_t j = next.fetch_add(1);
+                if (j >= todo.size() || err.load() != GD_OK) break;
+                const int64_t i = todo[j];
+                const ExactSeed e = exact_seed_solve(W, B->G, &op, ch ? GD_M_LOCAL_CH : GD_M_LOCAL_GD,
+                                                     seeds[i], bval, B->p.mu, B->p.L,
+                                                     B->p.max_sweeps, false);
+                if (before[i] != e.sweeps || before[n_seeds + i] != e.ops ||
+                    (!ch && before[2 * n_seeds + i] != e.pushes))
+                    changed += 1;
+                unsigned long long nz[2] = {0, 0};
+                GD_CUDA(cudaMemsetAsync(cnts.p, 0, 2 * sizeof(unsigned long long), ws));
+                k_count_nz<<<nb, 256, 0, ws>>>(e.x, n, cnts.p);
+                k_count_nz<<<nb, 256, 0, ws>>>(e.r, n, cnts.p + 1);
+                GD_LAUNCH_CHECK();
+                GD_CUDA(cudaMemcpyAsync(nz, cnts.p, sizeof(nz), cudaMemcpyDeviceToHost, ws));
+                GD_CUDA(cudaStreamSynchronize(ws));
+                std::lock_guard<std::mutex> lk(mu);
+                const int64_t xb = B->last_x_total, xc = (int64_t)nz[0], sup = (int64_t)nz[1];
+                if (xb + xc > B->xcap) {
+                    const int64_t cap = 2 * (xb + xc);
+                    grow_keep(B->xnodes, (size_t)cap, (size_t)xb);
+                    grow_keep(B->xvals, (size_t)cap, (size_t)xb);
+                    B->xcap = cap;
+                }
+                unsigned long long c0 = (unsigned long long)xb;
+                GD_CUDA(cudaMemcpyAsync(cnts.p, &c0, sizeof(c0), cudaMemcpyHostToDevice, ws));
+                k_emit_nz<<<nb, 256, 0, ws>>>(e.x, n, 1.0, B->xnodes.p, B->xvals.p, cnts.p);
+                GD_LAUNCH_CHECK();
+                B->last_x_total = xb + xc;
+                const int64_t rec[7] = {e.sweeps, e.ops, e.pushes, sup, xb, xc, 0};
+                const int32_t cv = e.converged;
+                GD_CUDA(cudaMemcpyAsync(B->sweeps.p + i, &rec[0], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->ops.p + i, &rec[1], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->pushes.p + i, &rec[2], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->support.p + i, &rec[3], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->xoff.p + i, &rec[4], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->xcnt.p + i, &rec[5], 8, cudaMemcpyHostToDevice, ws));
+                GD_CUDA(cudaMemcpyAsync(B->conv.p + i, &cv, 4, cudaMemcpyHostToDevice, ws));
+                int64_t rr[2] = {0, 0};
+                if (B->want_r()) {
+                    const int64_t rb = B->last_r_total;
+                    if (rb + sup > B->rcap) {
+                        const int64_t cap = 2 * (rb + sup);
+                        grow_keep(B->rnodes, (size_t)cap, (size_t)rb);
+                        grow_keep(B->rvals, (size_t)cap, (size_t)rb);
+                        B->rcap = cap;
+                    }
+                    unsigned long long r0 = (unsigned long long)rb;
+                    GD_CUDA(cudaMemcpyAsync(cnts.p + 1, &r0, sizeof(r0), cudaMemcpyHostToDevice, ws));
+                    k_emit_nz<<<nb, 256, 0, ws>>>(e.r, n, 1.0, B->rnodes.p, B->rvals.p, cnts.p + 1);
+                    GD_LAUNCH_CHECK();
+                    B->last_r_total = rb + sup;
+                    rr[0] = rb;
+                    rr[1] = sup;
+                    GD_CUDA(cudaMemcpyAsync(B->roff.p + i, &rr[0], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->rcnt.p + i, &rr[1], 8, cudaMemcpyHostToDevice, ws));
+                }
+                GD_CUDA(cudaStreamSynchronize(ws));  // (host records above go out of scope)
             }
-            c0 = (unsigned long long)rb;
-            GD_CUDA(cudaMemcpy(tmp, &c0, sizeof(c0), cudaMemcpyHostToDevice));
-            k_emit_nz<<<nb, 256>>>(e.r, n, 1.0, B->rnodes.p, B->rvals.p, tmp);
-            GD_LAUNCH_CHECK();
-            B->last_r_total = rb + (int64_t)nz[1];
-            const int64_t rc = (int64_t)nz[1];
-            GD_CUDA(cudaMemcpy(B->roff.p + i, &rb, 8, cudaMemcpyHostToDevice));
-            GD_CUDA(cudaMemcpy(B->rcnt.p + i, &rc, 8, cudaMemcpyHostToDevice));
+        } catch (const Error &e) {
+            std::lock_guard<std::mutex> lk(mu);
+            errmsg = gd_last_error();
+            err = e.code;
+        } catch (...) {
+            err = GD_ERR_CUDA;
         }
+    };
+    std::vector<std::thread> th;
+    for (size_t w = 1; w < T; ++w) th.emplace_back(work, w);
+    if (T) work(0);
+    for (auto &x : th) x.join();
+    if (err.load() != GD_OK) {
+        set_error("exact re-solve failed: %s", errmsg.c_str());
+        throw Error{err.load()};
     }
+    B->last_changed = changed.load();
     const unsigned long long tot = (unsigned long long)B->last_x_total;
     GD_CUDA(cudaMemcpy(B->cursor.p, &tot, sizeof(tot), cudaMemcpyHostToDevice));
-    GD_CUDA(cudaDeviceSynchronize());
     B->last_resolve_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }

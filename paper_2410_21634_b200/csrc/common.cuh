@@ -202,17 +202,22 @@ __device__ __forceinline__ void near_record(const NearList &L, int par, int32_t 
 
 // Bit-exact single-seed solve on the device (exact.cu): LocalGD (method
 // GD_M_LOCAL_GD, b = bval e_seed, frontier signed when sgn) or LocalCH
-// (GD_M_LOCAL_CH, bounds mu < L).  x and r are left in device buffers owned
-// by the calling thread's solver (valid until its next solve).
+// (GD_M_LOCAL_CH, bounds mu < L), on a worker (own buffers, own non-blocking
+// stream; one host thread per worker at a time).  x and r are left in the
+// worker's device buffers (valid until its next solve), the stream idle.
 struct ExactSeed {
     int64_t sweeps, ops, pushes;
     int32_t converged, diverged;
     const double *x, *r;
     int64_t n;
 };
-ExactSeed exact_seed_solve(const gd_graph *G, const gd_operator *op, int32_t method, int64_t seed,
-                           double bval, double mu, double L, int64_t max_sweeps, bool sgn,
-                           cudaStream_t st);
+struct ExactWorker;
+ExactWorker *exact_worker_create();
+void exact_worker_destroy(ExactWorker *w);
+cudaStream_t exact_worker_stream(ExactWorker *w);
+ExactSeed exact_seed_solve(ExactWorker *w, const gd_graph *G, const gd_operator *op,
+                           int32_t method, int64_t seed, double bval, double mu, double L,
+                           int64_t max_sweeps, bool sgn);
 
 inline int n_sms(int device) {
     int v = 0;

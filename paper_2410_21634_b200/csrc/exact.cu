@@ -351,7 +351,10 @@ struct SweepSolver {
         uint8_t f = 0;
         GD_CUDA(cudaMemcpyAsync(&f, flag.p, 1, cudaMemcpyDeviceToHost, s));
         GD_CUDA(cudaStreamSynchronize(s));
-        if (f) GD_CUDA(cudaMemcpy(F.p, &sd, sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (f) {
+            GD_CUDA(cudaMemcpyAsync(F.p, &sd, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            GD_CUDA(cudaStreamSynchronize(s));
+        }
         return f ? 1 : 0;
     }
 
@@ -462,22 +465,36 @@ SweepSolver &solver_for(const gd_graph *G, const gd_operator *o, bool sgn) {
 
 }  // namespace
 
+// A re-solve worker: its own solver buffers and a non-blocking stream, so
+// several host threads can run exact seeds concurrently.
+struct ExactWorker {
+    SweepSolver S;
+    ExactWorker() { GD_CUDA(cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking)); }
+    ~ExactWorker() {
+        if (S.s) cudaStreamDestroy(S.s);
+    }
+};
+
+ExactWorker *exact_worker_create() { return new ExactWorker(); }
+void exact_worker_destroy(ExactWorker *w) { delete w; }
+cudaStream_t exact_worker_stream(ExactWorker *w) { return w->S.s; }
+
 // Bit-exact re-solve of one seed for the batched solvers (common.cuh): the
 // sweep loops of local_gd_run / gd_local_ch below without the per-sweep
 // logs (LocalCH keeps its l1 for the divergence abort, :527-530).
-ExactSeed exact_seed_solve(const gd_graph *G, const gd_operator *o, int32_t method, int64_t seed,
-                           double bval, double mu, double L, int64_t max_sweeps, bool sgn,
-                           cudaStream_t st) {
-    GD_CUDA(cudaStreamSynchronize(st));
+ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator *o,
+                           int32_t method, int64_t seed, double bval, double mu, double L,
+                           int64_t max_sweeps, bool sgn) {
     const bool ch = method == GD_M_LOCAL_CH;
-    SweepSolver &S = solver_for(G, o, ch || sgn);
+    SweepSolver &S = W->S;
+    S.prepare(G, o, ch || sgn);
     ExactSeed out{0, 0, 0, 1, 0, nullptr, nullptr, S.n};
     size_t nn = S.n ? S.n : 1;
     if (ch) {
         S.mom.ensure(nn);
         S.mstamp.ensure(nn);
-        GD_CUDA(cudaMemset(S.mom.p, 0, sizeof(double) * nn));
-        GD_CUDA(cudaMemset(S.mstamp.p, 0xFE, sizeof(int32_t) * nn));
+        GD_CUDA(cudaMemsetAsync(S.mom.p, 0, sizeof(double) * nn, S.s));
+        GD_CUDA(cudaMemsetAsync(S.mstamp.p, 0xFE, sizeof(int32_t) * nn, S.s));
     }
     int64_t f = S.init_spike(seed, bval);
     const double rho = ch ? (L - mu) / (L + mu) : 0.0, step0 = ch ? 2.0 / (L + mu) : 0.0;
