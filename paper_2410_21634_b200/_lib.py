@@ -118,6 +118,7 @@ SIGNATURES = {
     "gd_batch_fetch_r_host": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _i32p, _f64p, C.c_int64,
                                         _i64p, C.c_void_p]),
     "gd_batch_round_log": (C.c_int, [C.c_void_p, _i64p, C.c_int64, _i64p]),
+    "gd_batch_round_phase_log": (C.c_int, [C.c_void_p, _i64p, C.c_int64]),
     "gd_feature_push": (C.c_int, [C.c_void_p, _f64p, _f64p, C.c_double, C.c_double, C.c_int64,
                                   _f64p, C.c_int64, _f64p, _f64p, _i64p, _i64p, _i64p, _i32p]),
     "gd_pairs_create": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, C.c_int64, C.c_int64,

@@ -181,6 +181,8 @@ struct RoundArgs {
     unsigned long long *sn[2];    // per slot: entries in the frontier, per round parity
     int64_t *drain_cnt;           // per slot: pushed count of the finished seed
     int64_t reset_units;          // sector-map reset work units per finished slot
+    int64_t cohort;               // refill only once this many slots are free (they
+                                  // then start together: see k_rounds)
 };
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -260,11 +262,12 @@ struct Stage {
     unsigned long long *scan;            // [BT/32 + 2]
     unsigned *nf;                        // [S] next-frontier entries per slot (streaming)
     int32_t *fin;                        // [S] slots whose seed finished (streaming)
-    unsigned *nfin;                      // [1]
+    unsigned *nfin;                      // [2] finished, idle slots
+    int32_t *idle;                       // [S] idle slots (streaming)
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 +
+    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 +
            8 * (BT / 32 + 3) + 16 + 64;
 }
 
@@ -286,6 +289,7 @@ __device__ Stage stage_carve(void *base, int S) {
     st.fd = (int32_t *)p; p += 4 * STAGE_CAP;
     st.nf = (unsigned *)p; p += 4 * S;
     st.fin = (int32_t *)p; p += 4 * S;
+    st.idle = (int32_t *)p; p += 4 * S;
     st.nfin = (unsigned *)p;
     return st;
 }
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
     if (threadIdx.x == 0) {
         *S.fcnt = 0;
         *S.next = 0;
-        *S.nfin = 0;
+        S.nfin[0] = S.nfin[1] = 0;
     }
     __syncthreads();
 
@@ -526,27 +530,42 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
                     A.s_amb[k] = 1;
             }
         }
-        unsigned nfin = 0;
+        unsigned nfin = 0, nidle = 0;
+        bool refill = false;
         if (STREAM) {
             // seeds that finished: running slots without entries this round,
             // listed in slot order (every block must see the same list: the
             // work units below are split across blocks by position in it)
             if (threadIdx.x < 32) {
-                unsigned cnt = 0;
+                unsigned cnt = 0, ci = 0;
                 for (int64_t k0 = 0; k0 < A.m; k0 += 32) {
                     const int64_t k = k0 + lane;
-                    const bool f = k < A.m && A.s_idx[k] >= 0 &&
+                    const int32_t si = k < A.m ? A.s_idx[k] : 0;
+                    const bool f = k < A.m && si >= 0 &&
                                    *(volatile unsigned long long *)(A.sn[cur] + k) == 0ULL;
-                    const unsigned b = __ballot_sync(FULL, f);
+                    const bool id = k < A.m && si < 0;
+                    const unsigned b = __ballot_sync(FULL, f), bi = __ballot_sync(FULL, id);
                     if (f) S.fin[cnt + __popc(b & lanemask_lt())] = (int32_t)k;
+                    if (id) S.idle[ci + __popc(bi & lanemask_lt())] = (int32_t)k;
                     cnt += __popc(b);
+                    ci += __popc(bi);
                 }
-                if (lane == 0) *S.nfin = cnt;
+                if (lane == 0) {
+                    S.nfin[0] = cnt;
+                    S.nfin[1] = ci;
+                }
             }
             __syncthreads();
-            nfin = *S.nfin;
+            nfin = S.nfin[0];
+            nidle = S.nfin[1];
+            // cohorts: free slots take new seeds only once `cohort` of them are
+            // free (or nothing else runs), so seeds start -- and reach their
+            // big rounds -- together
+            const bool left =
+                *(volatile unsigned long long *)A.seed_ctr < (unsigned long long)A.n_seeds;
+            refill = left && (nfin + nidle >= (unsigned)A.cohort || nfin + nidle == (unsigned)A.m);
             const unsigned long long done = *(volatile unsigned long long *)A.done_ctr;
-            if ((F == 0 && nfin == 0) || (int64_t)done >= A.seg_done) {
+            if ((F == 0 && nfin == 0 && !refill) || (int64_t)done >= A.seg_done) {
                 if (gtid == 0) *A.t_state = t;
                 break;
             }
@@ -719,7 +738,6 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
                 O.support[si] = (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
                 O.xoff[si] = b;
                 O.xcnt[si] = (int64_t)pc;
-                atomicAdd(A.done_ctr, 1ULL);
             }
             // ... and their r back to +0.0: zero the marked sectors, clear the map
             const int64_t units = (int64_t)nfin * A.reset_units;
@@ -753,15 +771,18 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
         counters_flush(S.pvol, A.s_pvol, A.m);
         counters_flush(S.push, A.s_pushes, A.m);
         grid.sync();
+        if (gtid == 0 && t < A.rlog_cap) A.rlog[3 * A.rlog_cap + 1 + t] = globaltimer();
         // ---------------- phase B: arc-balanced scatter ----------------------
         // chunk c = arcs [32c, 32c+32) of the slot-grouped frontier.  Warp w
         // takes chunk groups w, w + W, w + 2W, ... (UNROLL chunks, each lane
         // one atomic in flight per chunk), so the whole grid sweeps the arc
         // space front to back, slot by slot, without a claim counter.
         for (int64_t k = gtid; k < A.m; k += nthreads) A.sfill[k] = 0ULL;  // for the next round
-        if (STREAM && nfin) {
+        if (STREAM && (nfin || refill)) {
             // finished seeds: x over the pushed list out (caller ids), zeroed
-            constexpr int64_t XU = 32;  // extract units per slot
+            // (many small units: a few finished slots must not hold the
+            // whole grid at the next barrier behind a handful of warps)
+            constexpr int64_t XU = 256;  // extract units per slot
             for (int64_t u = gwarp; u < (int64_t)nfin * XU; u += nwarps) {
                 const int32_t k = S.fin[u / XU];
                 const int64_t pc = A.drain_cnt[k], b = A.slot_base[k];
@@ -777,17 +798,25 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
                     }
                 }
             }
-            // the near-threshold flag (final now), then the slot's next seed
-            for (int64_t j0 = gwarp * 32; j0 < nfin; j0 += nwarps * 32) {
+            // the near-threshold flag (final now), then -- once the cohort is
+            // complete -- the free slots' next seeds
+            const unsigned nfree = refill ? nfin + nidle : nfin;
+            for (int64_t j0 = gwarp * 32; j0 < nfree; j0 += nwarps * 32) {
                 const int64_t j = j0 + lane;
                 bool act = false;
                 int32_t k = 0, s = 0, d = 0;
-                if (j < nfin) {
-                    k = S.fin[j];
-                    const int64_t si = A.s_idx[k];
-                    O.amb[si] = A.s_amb[k];
-                    if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
-                    const unsigned long long i = atomicAdd(A.seed_ctr, 1ULL);
+                if (j < nfree) {
+                    k = j < nfin ? S.fin[j] : S.idle[j - nfin];
+                    if (j < nfin) {
+                        const int64_t si = A.s_idx[k];
+                        O.amb[si] = A.s_amb[k];
+                        if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
+                        // (counted here, not in phase A: every block reads the
+                        // counter at the next round start, after the barrier)
+                        atomicAdd(A.done_ctr, 1ULL);
+                    }
+                    const unsigned long long i = refill ? atomicAdd(A.seed_ctr, 1ULL)
+                                                        : (unsigned long long)A.n_seeds;
                     if ((int64_t)i < A.n_seeds) {
                         s = (int32_t)A.seeds[i];
                         if (A.perm) s = A.perm[s];
@@ -888,10 +917,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
           }
         }
         stage_flush(S, A, nxt);  // (its barriers also order the claim counter reset)
-        if (threadIdx.x == 0) {
-            *S.next = 0;
-            *S.nfin = 0;
-        }
+        if (threadIdx.x == 0) *S.next = 0;
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
@@ -1201,6 +1227,7 @@ struct gd_batch {
     // streaming form of the round kernel (k_rounds<false, true>)
     bool stream = false;
     int sgrid = 0;                   // its cooperative grid
+    int64_t cohort = 0;              // free slots that start new seeds together (0 = all)
     DBuf<int32_t> s_idx, s_t0, t_state;
     DBuf<unsigned long long> sn, sctr;  // per slot entries [2][slots]; seed / done counters
     DBuf<int64_t> drain_cnt;
@@ -1304,7 +1331,11 @@ struct gd_batch {
             A.sn[0] = sn.p;
             A.sn[1] = sn.p + slots;
             A.drain_cnt = drain_cnt.p;
-            A.reset_units = (int64_t)reset_chunks();
+            A.cohort = cohort > 0 ? cohort : slots;
+            {   // sector-map reset units per finished slot: ~64 map words each
+                const int64_t u = (smw + 63) / 64;
+                A.reset_units = u < 256 ? 256 : (u > 16384 ? 16384 : u);
+            }
         }
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
@@ -1929,7 +1960,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 if (cc > B->ccap) B->ccap = cc;
             }
             B->chunk_e.alloc(B->ccap);
-            B->rlog.alloc(3 * gd_batch::RLOG_CAP + 1);
+            B->rlog.alloc(4 * gd_batch::RLOG_CAP + 1);  // (F, P, t0) per round, count, tB
             B->smw = (ld / 4 + 31) / 32;  // one bit per 4 doubles (32 B sector)
             B->secmap.alloc((size_t)slots * (size_t)B->smw);
             GD_CUDA(cudaMemset(B->secmap.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
@@ -1959,6 +1990,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             // here once)
             B->stream = !B->hk && !B->want_r();
             if (const char *e = getenv("GDIFF_STREAM")) B->stream = B->stream && atoi(e) != 0;
+            if (const char *e = getenv("GDIFF_COHORT")) B->cohort = atoll(e);  // (A/B)
             if (B->stream) {
                 const void *sfn = (const void *)k_rounds<false, true>;
                 GD_CUDA(cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2126,6 +2158,16 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
             B->hs.vals = nullptr;
         }
         if (rc != GD_OK) throw Error{rc};
+    });
+}
+
+int gd_batch_round_phase_log(const gd_batch *B, int64_t *out, int64_t cap) {
+    return guarded([&] {
+        GD_CHECK_ARG(B && out, "null pointer");
+        GD_CHECK_ARG(B->rlog.p, "no round kernel");
+        const int64_t k = cap < gd_batch::RLOG_CAP ? cap : gd_batch::RLOG_CAP;
+        GD_CUDA(cudaMemcpy(out, B->rlog.p + 3 * gd_batch::RLOG_CAP + 1, sizeof(int64_t) * k,
+                           cudaMemcpyDeviceToHost));
     });
 }
 
