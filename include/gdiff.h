@@ -298,7 +298,8 @@ int gd_batch_info(const gd_batch *b, int32_t *mode, int64_t *slots);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */
 int gd_batch_round_log(const gd_batch *b, int64_t *out, int64_t cap, int64_t *rounds);
-/* ... and the device ns at which each round's scatter phase began (cap entries). */
+/* ... and the device ns at which each round's scatter phase began (cap/2
+ * entries), then per round the slots whose seed finished (| refill << 32). */
 int gd_batch_round_phase_log(const gd_batch *b, int64_t *out, int64_t cap);
 
 /* ---- multi-column degree-generalized feature push (new) -------------- */

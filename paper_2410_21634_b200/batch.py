@@ -188,17 +188,19 @@ class BatchSolver:
         return int(s.value)
 
     def round_log(self) -> np.ndarray:
-        """(rounds, 4) int64: frontier entries, arcs, device ns at round start
-        and at the start of its scatter phase, for the last wave (streaming
+        """(rounds, 5) int64: frontier entries, arcs, device ns at round start
+        and at the start of its scatter phase, finished slots (| refill << 32),
+        for the last wave (streaming
         form: the whole solve) of the last solve (instrumentation)."""
         buf = np.zeros(3 * 4096, np.int64)
         cnt = C.c_int64()
         gdl.check(self.lib.gd_batch_round_log(self.handle, gdl.ptr(buf, C.c_int64), 4096,
                                               C.byref(cnt)))
         k = min(cnt.value, 4096)
-        tb = np.zeros(4096, np.int64)
-        gdl.check(self.lib.gd_batch_round_phase_log(self.handle, gdl.ptr(tb, C.c_int64), 4096))
-        return np.concatenate([buf[:3 * k].reshape(-1, 3), tb[:k, None]], axis=1)
+        tb = np.zeros(2 * 4096, np.int64)
+        gdl.check(self.lib.gd_batch_round_phase_log(self.handle, gdl.ptr(tb, C.c_int64), 2 * 4096))
+        return np.concatenate([buf[:3 * k].reshape(-1, 3), tb[:k, None], tb[4096:4096 + k, None]],
+                              axis=1)
 
     def solve_device(self, seeds, stream=None) -> dict:
         """seeds: CUDA int64 tensor.  Returns torch CUDA tensors (views of the

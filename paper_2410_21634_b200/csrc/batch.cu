@@ -181,6 +181,7 @@ struct RoundArgs {
     unsigned long long *sn[2];    // per slot: entries in the frontier, per round parity
     int64_t *drain_cnt;           // per slot: pushed count of the finished seed
     int64_t reset_units;          // sector-map reset work units per finished slot
+    int32_t dbg;                  // (experiments) 1: skip x extract, 2: skip r reset
     int64_t cohort;               // refill only once this many slots are free (they
                                   // then start together: see k_rounds)
 };
@@ -465,13 +466,6 @@ struct OutArgs {
     unsigned long long *amb_cnt;  // flagged seeds
 };
 
-// Heat kernel (HK = true, GD_M_HK): the stage-expanded push of
-// _hk_push_kernel (src/local_solvers.py:566-661).  Round t pops stage t and
-// feeds stage t+1 only (see hk.cu), so all seeds of a wave are at the same
-// stage: layer t lives in r (t even) or r2 (t odd), the layer receiving
-// stage t+1 is cleared of its stage t-1 leftovers in phase A, and the
-// products are fl(fl(r * tau/(t+1)) * fl(1/d_u)).  x accumulates the pushed
-// values stage by stage -- the reference's stages.sum(axis=0) order.
 //
 // STREAM = true (LocalGD without sparse r): the slots are refilled inside the
 // kernel instead of running in synchronous waves.  A slot whose seed had no
@@ -488,14 +482,18 @@ struct OutArgs {
 // kernel leaves at a round start once `seg_done` seeds have finished (the
 // host copies their x out while the next launch runs) and resumes there.
 template <bool HK, bool STREAM = false>
-__global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs O) {
+__global__ void __launch_bounds__(BT, GD_KR_MINB)
+    k_rounds(const __grid_constant__ RoundArgs A, const __grid_constant__ OutArgs O) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Stage S = stage_carve(smem_raw, (int)A.m);
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
-    const int64_t gwarp = gtid >> 5, nwarps = nthreads >> 5;
+    const int64_t nwarps = nthreads >> 5;
+    // warp index that walks the blocks first: consecutive work units land on
+    // different SMs (the finishing work of a few slots must use them all)
+    const int64_t swarp = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     for (int64_t k = threadIdx.x; k < A.m; k += BT) {
         S.ops[k] = S.pvol[k] = S.scnt[k] = 0;
         S.push[k] = S.touch[k] = S.negz[k] = 0;
@@ -742,7 +740,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
             // ... and their r back to +0.0: zero the marked sectors, clear the map
             const int64_t units = (int64_t)nfin * A.reset_units;
             const int64_t per = (A.smw + A.reset_units - 1) / A.reset_units;
-            for (int64_t u = gwarp; u < units; u += nwarps) {
+            for (int64_t u = swarp; u < units && !(A.dbg & 2); u += nwarps) {
                 const int32_t k = S.fin[u / A.reset_units];
                 const int64_t lo = (u % A.reset_units) * per, hi = min(A.smw, lo + per);
                 uint32_t *map = A.secmap + (int64_t)k * A.smw;
@@ -771,7 +769,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
         counters_flush(S.pvol, A.s_pvol, A.m);
         counters_flush(S.push, A.s_pushes, A.m);
         grid.sync();
-        if (gtid == 0 && t < A.rlog_cap) A.rlog[3 * A.rlog_cap + 1 + t] = globaltimer();
+        if (gtid == 0 && t < A.rlog_cap) {
+            A.rlog[3 * A.rlog_cap + 1 + t] = globaltimer();
+            A.rlog[4 * A.rlog_cap + 1 + t] = (int64_t)nfin | ((int64_t)refill << 32);
+        }
         // ---------------- phase B: arc-balanced scatter ----------------------
         // chunk c = arcs [32c, 32c+32) of the slot-grouped frontier.  Warp w
         // takes chunk groups w, w + W, w + 2W, ... (UNROLL chunks, each lane
@@ -779,29 +780,70 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB) k_rounds(RoundArgs A, OutArgs 
         // space front to back, slot by slot, without a claim counter.
         for (int64_t k = gtid; k < A.m; k += nthreads) A.sfill[k] = 0ULL;  // for the next round
         if (STREAM && (nfin || refill)) {
-            // finished seeds: x over the pushed list out (caller ids), zeroed
-            // (many small units: a few finished slots must not hold the
-            // whole grid at the next barrier behind a handful of warps)
-            constexpr int64_t XU = 256;  // extract units per slot
-            for (int64_t u = gwarp; u < (int64_t)nfin * XU; u += nwarps) {
-                const int32_t k = S.fin[u / XU];
-                const int64_t pc = A.drain_cnt[k], b = A.slot_base[k];
-                const int64_t lo = (u % XU) * pc / XU, hi = (u % XU + 1) * pc / XU;
-                const int64_t off = (int64_t)k * A.ld;
-                for (int64_t i = lo + lane; i < hi; i += 32) {
-                    const int32_t v = A.pushed[off + i];
-                    const double xv = A.x[off + v];
-                    A.x[off + v] = 0.0;
-                    if (b + i < O.xcap) {
-                        O.xnodes[b + i] = O.inv ? __ldg(O.inv + v) : v;
-                        O.xvals[b + i] = xv;
+            // finished seeds: x over the pushed list out (caller ids), zeroed.
+            // Work-balanced: the finished slots' pushed lists are one
+            // concatenated index space (prefix in shared memory, same in every
+            // block), walked 256 entries per warp step with all 8 gathers of a
+            // lane in flight before any store
+            if (threadIdx.x < 32) {
+                unsigned long long run = 0;
+                for (unsigned j0 = 0; j0 < nfin; j0 += 32) {
+                    const unsigned j = j0 + lane;
+                    const unsigned long long c = j < nfin ? (unsigned long long)A.drain_cnt[S.fin[j]] : 0ULL;
+                    unsigned long long incl = c;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (j < nfin) S.sbase[j] = run + incl - c;
+                    run += __shfl_sync(FULL, incl, 31);
+                }
+                if (lane == 0) S.scan[0] = run;
+            }
+            __syncthreads();
+            const int64_t total = (int64_t)S.scan[0];
+            constexpr int XQ = 8;
+            for (int64_t e0 = swarp * 32 * XQ; e0 < total && !(A.dbg & 1); e0 += nwarps * 32 * XQ) {
+                int32_t v[XQ], id[XQ];
+                int64_t at[XQ], xo[XQ];
+                double xv[XQ];
+#pragma unroll
+                for (int q = 0; q < XQ; ++q) {
+                    const int64_t e = e0 + q * 32 + lane;
+                    v[q] = -1;
+                    if (e < total) {
+                        unsigned lo = 0, hi = nfin;  // last j with prefix[j] <= e
+                        while (hi - lo > 1) {
+                            const unsigned mid = (lo + hi) >> 1;
+                            if ((int64_t)S.sbase[mid] <= e) lo = mid; else hi = mid;
+                        }
+                        const int32_t k = S.fin[lo];
+                        const int64_t i = e - (int64_t)S.sbase[lo];
+                        xo[q] = (int64_t)k * A.ld;
+                        at[q] = A.slot_base[k] + i;
+                        v[q] = A.pushed[xo[q] + i];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < XQ; ++q) {
+                    if (v[q] < 0) continue;
+                    xv[q] = A.x[xo[q] + v[q]];
+                    id[q] = O.inv ? __ldg(O.inv + v[q]) : v[q];
+                }
+#pragma unroll
+                for (int q = 0; q < XQ; ++q) {
+                    if (v[q] < 0) continue;
+                    A.x[xo[q] + v[q]] = 0.0;
+                    if (at[q] < O.xcap) {
+                        O.xnodes[at[q]] = id[q];
+                        O.xvals[at[q]] = xv[q];
                     }
                 }
             }
             // the near-threshold flag (final now), then -- once the cohort is
             // complete -- the free slots' next seeds
             const unsigned nfree = refill ? nfin + nidle : nfin;
-            for (int64_t j0 = gwarp * 32; j0 < nfree; j0 += nwarps * 32) {
+            for (int64_t j0 = swarp * 32; j0 < nfree; j0 += nwarps * 32) {
                 const int64_t j = j0 + lane;
                 bool act = false;
                 int32_t k = 0, s = 0, d = 0;
@@ -1228,6 +1270,8 @@ struct gd_batch {
     bool stream = false;
     int sgrid = 0;                   // its cooperative grid
     int64_t cohort = 0;              // free slots that start new seeds together (0 = all)
+    int32_t dbg = 0;                 // (experiments, GDIFF_DBG)
+    int32_t resolve_workers = (int32_t)RESOLVE_WORKERS;
     DBuf<int32_t> s_idx, s_t0, t_state;
     DBuf<unsigned long long> sn, sctr;  // per slot entries [2][slots]; seed / done counters
     DBuf<int64_t> drain_cnt;
@@ -1332,6 +1376,7 @@ struct gd_batch {
             A.sn[1] = sn.p + slots;
             A.drain_cnt = drain_cnt.p;
             A.cohort = cohort > 0 ? cohort : slots;
+            A.dbg = dbg;
             {   // sector-map reset units per finished slot: ~64 map words each
                 const int64_t u = (smw + 63) / 64;
                 A.reset_units = u < 256 ? 256 : (u > 16384 ? 16384 : u);
@@ -1714,7 +1759,7 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     // Up to GD_RESOLVE_WORKERS seeds at a time, each on its own worker (own
     // buffers and stream): one exact solve is a chain of small dependent
     // kernels and host syncs, so concurrent seeds overlap on the device.
-    const size_t T = std::min<size_t>(todo.size(), gd_batch::RESOLVE_WORKERS);
+    const size_t T = std::min<size_t>(todo.size(), (size_t)B->resolve_workers);
     while (B->workers.size() < T) B->workers.push_back(exact_worker_create());
     std::atomic<size_t> next{0};
     std::mutex mu;  // output pools, cursor and per-seed records
@@ -1838,6 +1883,8 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
         try {
             B->G = G;
             B->p = *p;
+            if (const char *e = getenv("GDIFF_RESOLVE_WORKERS"))  // (experiments)
+                B->resolve_workers = atoi(e) < 1 ? 1 : atoi(e);
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
             if (p->want_r && p->method != GD_M_HK) {  // sparse r pool (per-slot scratch below)
                 B->rcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
@@ -1960,7 +2007,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                 if (cc > B->ccap) B->ccap = cc;
             }
             B->chunk_e.alloc(B->ccap);
-            B->rlog.alloc(4 * gd_batch::RLOG_CAP + 1);  // (F, P, t0) per round, count, tB
+            B->rlog.alloc(5 * gd_batch::RLOG_CAP + 1);  // (F, P, t0) per round, count, tB, nfin
             B->smw = (ld / 4 + 31) / 32;  // one bit per 4 doubles (32 B sector)
             B->secmap.alloc((size_t)slots * (size_t)B->smw);
             GD_CUDA(cudaMemset(B->secmap.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
@@ -1985,12 +2032,18 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, BT, smem));
             GD_CHECK_ARG(per_sm > 0, "round kernel does not fit on an SM");
             B->grid = per_sm * n_sms(G->device);
-            // streaming form (slots refilled in-kernel) for LocalGD without
-            // sparse r; GDIFF_STREAM=0 keeps the synchronous waves (A/B, read
-            // here once)
-            B->stream = !B->hk && !B->want_r();
-            if (const char *e = getenv("GDIFF_STREAM")) B->stream = B->stream && atoi(e) != 0;
+            // streaming form (slots refilled in-kernel, LocalGD without sparse
+            // r) only on request (GDIFF_STREAM=1, read here once): measured on
+            // the products shape it loses to the synchronous waves (33.0 vs
+            // 26.5 + 4.3 ms per 1,024 seeds) -- a wave's seeds reach their big
+            // round together, and that round (~100 M arcs) keeps each slot's
+            // residual sectors hot in L2 far better than streamed rounds of
+            // ~8 M arcs do
+            B->stream = false;
+            if (const char *e = getenv("GDIFF_STREAM"))
+                B->stream = !B->hk && !B->want_r() && atoi(e) != 0;
             if (const char *e = getenv("GDIFF_COHORT")) B->cohort = atoll(e);  // (A/B)
+            if (const char *e = getenv("GDIFF_DBG")) B->dbg = atoi(e);        // (experiments)
             if (B->stream) {
                 const void *sfn = (const void *)k_rounds<false, true>;
                 GD_CUDA(cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2165,8 +2218,12 @@ int gd_batch_round_phase_log(const gd_batch *B, int64_t *out, int64_t cap) {
     return guarded([&] {
         GD_CHECK_ARG(B && out, "null pointer");
         GD_CHECK_ARG(B->rlog.p, "no round kernel");
-        const int64_t k = cap < gd_batch::RLOG_CAP ? cap : gd_batch::RLOG_CAP;
+        // cap entries of scatter-phase start ns, then cap of (streaming)
+        // finished slots | refill << 32
+        const int64_t k = cap / 2 < gd_batch::RLOG_CAP ? cap / 2 : gd_batch::RLOG_CAP;
         GD_CUDA(cudaMemcpy(out, B->rlog.p + 3 * gd_batch::RLOG_CAP + 1, sizeof(int64_t) * k,
+                           cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(out + k, B->rlog.p + 4 * gd_batch::RLOG_CAP + 1, sizeof(int64_t) * k,
                            cudaMemcpyDeviceToHost));
     });
 }

@@ -19,8 +19,15 @@ seeds = sample_sources(hg, 1024, seed=0)
 for mode in (sys.argv[3].split(",") if len(sys.argv) > 3 else ("1", "0")):
     os.environ["GDIFF_STREAM"] = mode
     s = BatchSolver(dg, 0.1, eps)
-    s.solve(seeds)
-    o = s.solve(seeds)
+    if os.environ.get("DEV"):
+        import torch
+        ds = torch.as_tensor(seeds, device="cuda")
+        s.solve_device(ds)
+        o = s.solve_device(ds)
+        torch.cuda.synchronize()
+    else:
+        s.solve(seeds)
+        o = s.solve(seeds)
     log = s.round_log()
     rs = s.resolve_stats()
     ms = s.last_kernel_ms
@@ -32,6 +39,6 @@ for mode in (sys.argv[3].split(",") if len(sys.argv) > 3 else ("1", "0")):
         print(f"  phase A total {ta.sum()/1e3:.2f} ms")
         print(f"  sum F={F.sum()} sum P={P.sum()} median dt={np.median(dt):.1f}us "
               f"sum dt={dt.sum()/1e3:.2f}ms")
-        for i in range(0, len(dt), max(1, len(dt) // 25)):
-            print(f"  r{i:4d} F={F[i]:9d} P={P[i]:11d} {dt[i]:8.1f}us A={ta[i]:7.1f}us {P[i]/max(dt[i],1e-9)/1e3:6.2f} Garc/s")
+        for i in range(0, len(dt), int(os.environ.get("EVERY", max(1, len(dt) // 25)))):
+            print(f"  r{i:4d} F={F[i]:9d} P={P[i]:11d} {dt[i]:8.1f}us A={ta[i]:7.1f}us fin={log[i, 4] & 0xffffffff:3d}{"R" if log[i, 4] >> 32 else " "} {P[i]/max(dt[i],1e-9)/1e3:6.2f} Garc/s")
     s.close()
