@@ -16,6 +16,7 @@
 // The batched throughput path (batch.cu) trades the sort for fp64 atomics.
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <memory>
 #include <vector>
 
@@ -523,7 +524,13 @@ ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator 
         GD_LAUNCH_CHECK();
         int64_t P = 0;
         double sgamma = 0.0;
+        const auto tt0 = std::chrono::steady_clock::now();
         const int64_t fnext = S.scatter_and_filter(f, t, &P, &sgamma);
+        static const bool trace = getenv("GDIFF_EXACT_TRACE") != nullptr;  // (diagnostic)
+        if (trace)
+            fprintf(stderr, "exact sweep %d f=%lld P=%lld %.1f us\n", t, (long long)f, (long long)P,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tt0)
+                        .count());
         out.ops += P;
         out.pushes += f;
         out.sweeps += 1;
