@@ -192,6 +192,10 @@ int gd_spectral_norm(const gd_graph *g, const double *x0, int64_t iters, double 
 
 typedef struct gd_batch gd_batch;
 
+#define GD_RESOLVE_FLAG 0
+#define GD_RESOLVE_EXACT 1
+#define GD_RESOLVE_ALL 2
+
 typedef struct {
     int32_t method;      /* GD_M_* */
     int32_t slots;       /* seeds in flight on the device; 0 = auto */
@@ -217,10 +221,13 @@ typedef struct {
     double theta_coeff;      /* eps / (2 (N+1) vol); theta = fl(coeff * d) */
     int32_t want_r;          /* 1: also return each seed's final r as a sparse vector
                                 (GD_M_LOCAL_GD / GD_M_LOCAL_CH / GD_M_LOCAL_SOR) */
-    int32_t exact_all;       /* 1: re-solve EVERY seed on the bit-exact path after the
-                                batch (x, r bit-identical with the reference; the
-                                near-threshold detector does this for flagged seeds
-                                only).  Not for GD_M_HK / GD_M_LOCAL_SOR. */
+    int32_t resolve;         /* near-threshold policy of the atomic-scatter batches
+                                (LocalGD / LocalCH; see gd_batch_result.ambiguous):
+                                GD_RESOLVE_FLAG (0): flag ambiguous seeds only;
+                                GD_RESOLVE_EXACT (1): re-solve the flagged seeds on
+                                the bit-exact path (their results are then the
+                                reference's bit for bit);
+                                GD_RESOLVE_ALL (2): re-solve every seed so. */
 } gd_batch_params;
 
 typedef struct {
@@ -280,6 +287,8 @@ int gd_batch_last_ambiguous(const gd_batch *b, int64_t *count);
  * (sweeps / operation counts / pushes differed from the batch's), and the
  * host wall time (ms) the re-solves took. */
 int gd_batch_resolve_stats(const gd_batch *b, int64_t *flagged, int64_t *changed, double *ms);
+/* Change the near-threshold policy (GD_RESOLVE_*) of an existing batch. */
+int gd_batch_set_resolve(gd_batch *b, int32_t mode);
 /* Device time (ms) of the dominant kernel (the sweep loop) in the last
  * solve, measured with CUDA events on the launching stream. */
 int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);

@@ -95,11 +95,13 @@ class BatchSolver:
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
                  L: float | None = None, hk: dict | None = None, want_r: bool = False,
-                 exact_all: bool = False):
+                 resolve: str = "flag"):
         if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
         if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
             raise ValueError("problem must be 'ppr', or 'katz' with method 'local-ch'")
+        if resolve not in ("flag", "exact", "all"):
+            raise ValueError("resolve must be 'flag', 'exact' or 'all'")
         if method == "local-hk" and not hk:
             raise ValueError("local-hk needs hk={tau, n_stages, stage_w, theta_coeff}")
         if method != "local-hk" and problem == "ppr" and not 0.0 < alpha <= 1.0:
@@ -131,7 +133,7 @@ class BatchSolver:
                             tau=float(hk.get("tau", 0.0)), n_stages=int(hk.get("n_stages", 0)),
                             stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)),
                             want_r=int(bool(want_r) and method != "local-hk"),
-                            exact_all=int(bool(exact_all)))
+                            resolve={"flag": 0, "exact": 1, "all": 2}[resolve])
         self.want_r = bool(want_r) and method != "local-hk"
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
@@ -162,6 +164,12 @@ class BatchSolver:
         c = C.c_int64()
         gdl.check(self.lib.gd_batch_last_ambiguous(self.handle, C.byref(c)))
         return int(c.value)
+
+    def set_resolve(self, resolve: str) -> None:
+        """Near-threshold policy for the next solves: "flag", "exact", "all"."""
+        if resolve not in ("flag", "exact", "all"):
+            raise ValueError("resolve must be 'flag', 'exact' or 'all'")
+        gdl.check(self.lib.gd_batch_set_resolve(self.handle, {"flag": 0, "exact": 1, "all": 2}[resolve]))
 
     def resolve_stats(self) -> dict:
         """Near-threshold re-solves of the last solve: seeds flagged, seeds

@@ -1731,8 +1731,9 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     B->last_amb = (int64_t)cnt;
     B->last_changed = 0;
     B->last_resolve_ms = 0.0;
-    const bool all = B->p.exact_all != 0;
-    if ((!cnt && !all) || B->hk || B->fifo) return;  // (heat kernel: reported, not re-solved)
+    const bool all = B->p.resolve == GD_RESOLVE_ALL;
+    if (B->p.resolve == GD_RESOLVE_FLAG || (!cnt && !all) || B->hk || B->fifo)
+        return;  // (heat kernel: reported, not re-solved)
     const auto t0 = std::chrono::steady_clock::now();
     GD_CUDA(cudaStreamSynchronize(st));
     std::vector<int32_t> amb(n_seeds);
@@ -1756,10 +1757,25 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     const int64_t n = B->G->n;
     const int nb = 4 * n_sms(B->G->device);
     if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));  // pools may move
-    // Up to GD_RESOLVE_WORKERS seeds at a time, each on its own worker (own
-    // buffers and stream): one exact solve is a chain of small dependent
-    // kernels and host syncs, so concurrent seeds overlap on the device.
-    const size_t T = std::min<size_t>(todo.size(), (size_t)B->resolve_workers);
+    // Work items: LocalGD seeds in chunks of K solved together on K graph
+    // copies (exact_multi_solve: one sweep loop, the per-sweep launch and
+    // sync overhead paid once per chunk); LocalCH seeds one at a time (its
+    // divergence abort is per seed).  Items run on up to resolve_workers
+    // workers (own buffers and stream each), overlapping on the device.
+    size_t K = 1;
+    if (!ch) {
+        const size_t want = (todo.size() + (size_t)B->resolve_workers - 1) / (size_t)B->resolve_workers;
+        K = std::min<size_t>(64, std::max<size_t>(16, want));
+        size_t fr = 0, tot = 0;
+        GD_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t per_copy = 112 * (size_t)(n ? n : 1);  // solver arrays per graph copy
+        const size_t by_mem = (fr / 2) / (per_copy * (size_t)B->resolve_workers);
+        K = std::min(K, std::max<size_t>(1, by_mem));
+        K = std::min<size_t>(K, (size_t)((1LL << 31) - 1) / (size_t)(n ? n : 1));
+        K = std::max<size_t>(1, std::min(K, todo.size()));
+    }
+    const size_t items = (todo.size() + K - 1) / K;
+    const size_t T = std::min<size_t>(items, (size_t)B->resolve_workers);
     while (B->workers.size() < T) B->workers.push_back(exact_worker_create());
     std::atomic<size_t> next{0};
     std::mutex mu;  // output pools, cursor and per-seed records
@@ -1771,66 +1787,84 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
             GD_CUDA(cudaSetDevice(B->G->device));
             ExactWorker *W = B->workers[w];
             const cudaStream_t ws = exact_worker_stream(W);
-            DBuf<unsigned long long> cnts(2);
+            struct { unsigned long long *p; } cnts{exact_worker_scratch(W)};
             for (;;) {
-                const size_t j = next.fetch_add(1);
-                if (j >= todo.size() || err.load() != GD_OK) break;
-                const int64_t i = todo[j];
-                const ExactSeed e = exact_seed_solve(W, B->G, &op, ch ? GD_M_LOCAL_CH : GD_M_LOCAL_GD,
-                                                     seeds[i], bval, B->p.mu, B->p.L,
-                                                     B->p.max_sweeps, false);
-                if (before[i] != e.sweeps || before[n_seeds + i] != e.ops ||
-                    (!ch && before[2 * n_seeds + i] != e.pushes))
-                    changed += 1;
-                unsigned long long nz[2] = {0, 0};
-                GD_CUDA(cudaMemsetAsync(cnts.p, 0, 2 * sizeof(unsigned long long), ws));
-                k_count_nz<<<nb, 256, 0, ws>>>(e.x, n, cnts.p);
-                k_count_nz<<<nb, 256, 0, ws>>>(e.r, n, cnts.p + 1);
-                GD_LAUNCH_CHECK();
-                GD_CUDA(cudaMemcpyAsync(nz, cnts.p, sizeof(nz), cudaMemcpyDeviceToHost, ws));
-                GD_CUDA(cudaStreamSynchronize(ws));
-                std::lock_guard<std::mutex> lk(mu);
-                const int64_t xb = B->last_x_total, xc = (int64_t)nz[0], sup = (int64_t)nz[1];
-                if (xb + xc > B->xcap) {
-                    const int64_t cap = 2 * (xb + xc);
-                    grow_keep(B->xnodes, (size_t)cap, (size_t)xb);
-                    grow_keep(B->xvals, (size_t)cap, (size_t)xb);
-                    B->xcap = cap;
+                const size_t it = next.fetch_add(1);
+                if (it >= items || err.load() != GD_OK) break;
+                const size_t j0 = it * K, j1 = std::min(todo.size(), j0 + K);
+                // solve the item: copy c of the result = seed todo[j0 + c]
+                std::vector<int64_t> sd, sw, op_, pu;
+                std::vector<int32_t> cvv;
+                const double *xb = nullptr, *rb = nullptr;
+                for (size_t j = j0; j < j1; ++j) sd.push_back(seeds[todo[j]]);
+                if (ch) {
+                    const ExactSeed e = exact_seed_solve(W, B->G, &op, GD_M_LOCAL_CH, sd[0], bval,
+                                                         B->p.mu, B->p.L, B->p.max_sweeps, false);
+                    xb = e.x; rb = e.r;
+                    sw.push_back(e.sweeps); op_.push_back(e.ops); pu.push_back(e.pushes);
+                    cvv.push_back(e.converged);
+                } else {
+                    const ExactMulti e = exact_multi_solve(W, B->G, &op, sd.data(), (int)sd.size(),
+                                                           bval, B->p.max_sweeps);
+                    xb = e.x; rb = e.r;
+                    sw = e.sweeps; op_ = e.ops; pu = e.pushes; cvv = e.conv;
                 }
-                unsigned long long c0 = (unsigned long long)xb;
-                GD_CUDA(cudaMemcpyAsync(cnts.p, &c0, sizeof(c0), cudaMemcpyHostToDevice, ws));
-                k_emit_nz<<<nb, 256, 0, ws>>>(e.x, n, 1.0, B->xnodes.p, B->xvals.p, cnts.p);
-                GD_LAUNCH_CHECK();
-                B->last_x_total = xb + xc;
-                const int64_t rec[7] = {e.sweeps, e.ops, e.pushes, sup, xb, xc, 0};
-                const int32_t cv = e.converged;
-                GD_CUDA(cudaMemcpyAsync(B->sweeps.p + i, &rec[0], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->ops.p + i, &rec[1], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->pushes.p + i, &rec[2], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->support.p + i, &rec[3], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->xoff.p + i, &rec[4], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->xcnt.p + i, &rec[5], 8, cudaMemcpyHostToDevice, ws));
-                GD_CUDA(cudaMemcpyAsync(B->conv.p + i, &cv, 4, cudaMemcpyHostToDevice, ws));
-                int64_t rr[2] = {0, 0};
-                if (B->want_r()) {
-                    const int64_t rb = B->last_r_total;
-                    if (rb + sup > B->rcap) {
-                        const int64_t cap = 2 * (rb + sup);
-                        grow_keep(B->rnodes, (size_t)cap, (size_t)rb);
-                        grow_keep(B->rvals, (size_t)cap, (size_t)rb);
-                        B->rcap = cap;
-                    }
-                    unsigned long long r0 = (unsigned long long)rb;
-                    GD_CUDA(cudaMemcpyAsync(cnts.p + 1, &r0, sizeof(r0), cudaMemcpyHostToDevice, ws));
-                    k_emit_nz<<<nb, 256, 0, ws>>>(e.r, n, 1.0, B->rnodes.p, B->rvals.p, cnts.p + 1);
+                for (size_t c = 0; c < sd.size(); ++c) {
+                    const int64_t i = todo[j0 + c];
+                    const double *ex = xb + (int64_t)c * n, *er = rb + (int64_t)c * n;
+                    if (before[i] != sw[c] || before[n_seeds + i] != op_[c] ||
+                        (!ch && before[2 * n_seeds + i] != pu[c]))
+                        changed += 1;
+                    unsigned long long nz[2] = {0, 0};
+                    GD_CUDA(cudaMemsetAsync(cnts.p, 0, 2 * sizeof(unsigned long long), ws));
+                    k_count_nz<<<nb, 256, 0, ws>>>(ex, n, cnts.p);
+                    k_count_nz<<<nb, 256, 0, ws>>>(er, n, cnts.p + 1);
                     GD_LAUNCH_CHECK();
-                    B->last_r_total = rb + sup;
-                    rr[0] = rb;
-                    rr[1] = sup;
-                    GD_CUDA(cudaMemcpyAsync(B->roff.p + i, &rr[0], 8, cudaMemcpyHostToDevice, ws));
-                    GD_CUDA(cudaMemcpyAsync(B->rcnt.p + i, &rr[1], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(nz, cnts.p, sizeof(nz), cudaMemcpyDeviceToHost, ws));
+                    GD_CUDA(cudaStreamSynchronize(ws));
+                    std::lock_guard<std::mutex> lk(mu);
+                    const int64_t xb0 = B->last_x_total, xc = (int64_t)nz[0], sup = (int64_t)nz[1];
+                    if (xb0 + xc > B->xcap) {
+                        const int64_t cap = 2 * (xb0 + xc);
+                        grow_keep(B->xnodes, (size_t)cap, (size_t)xb0);
+                        grow_keep(B->xvals, (size_t)cap, (size_t)xb0);
+                        B->xcap = cap;
+                    }
+                    unsigned long long c0 = (unsigned long long)xb0;
+                    GD_CUDA(cudaMemcpyAsync(cnts.p, &c0, sizeof(c0), cudaMemcpyHostToDevice, ws));
+                    k_emit_nz<<<nb, 256, 0, ws>>>(ex, n, 1.0, B->xnodes.p, B->xvals.p, cnts.p);
+                    GD_LAUNCH_CHECK();
+                    B->last_x_total = xb0 + xc;
+                    const int64_t rec[6] = {sw[c], op_[c], pu[c], sup, xb0, xc};
+                    const int32_t cv = cvv[c];
+                    GD_CUDA(cudaMemcpyAsync(B->sweeps.p + i, &rec[0], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->ops.p + i, &rec[1], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->pushes.p + i, &rec[2], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->support.p + i, &rec[3], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->xoff.p + i, &rec[4], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->xcnt.p + i, &rec[5], 8, cudaMemcpyHostToDevice, ws));
+                    GD_CUDA(cudaMemcpyAsync(B->conv.p + i, &cv, 4, cudaMemcpyHostToDevice, ws));
+                    int64_t rr[2] = {0, 0};
+                    if (B->want_r()) {
+                        const int64_t rb0 = B->last_r_total;
+                        if (rb0 + sup > B->rcap) {
+                            const int64_t cap = 2 * (rb0 + sup);
+                            grow_keep(B->rnodes, (size_t)cap, (size_t)rb0);
+                            grow_keep(B->rvals, (size_t)cap, (size_t)rb0);
+                            B->rcap = cap;
+                        }
+                        unsigned long long r0 = (unsigned long long)rb0;
+                        GD_CUDA(cudaMemcpyAsync(cnts.p + 1, &r0, sizeof(r0), cudaMemcpyHostToDevice, ws));
+                        k_emit_nz<<<nb, 256, 0, ws>>>(er, n, 1.0, B->rnodes.p, B->rvals.p, cnts.p + 1);
+                        GD_LAUNCH_CHECK();
+                        B->last_r_total = rb0 + sup;
+                        rr[0] = rb0;
+                        rr[1] = sup;
+                        GD_CUDA(cudaMemcpyAsync(B->roff.p + i, &rr[0], 8, cudaMemcpyHostToDevice, ws));
+                        GD_CUDA(cudaMemcpyAsync(B->rcnt.p + i, &rr[1], 8, cudaMemcpyHostToDevice, ws));
+                    }
+                    GD_CUDA(cudaStreamSynchronize(ws));  // (host records above go out of scope)
                 }
-                GD_CUDA(cudaStreamSynchronize(ws));  // (host records above go out of scope)
             }
         } catch (const Error &e) {
             std::lock_guard<std::mutex> lk(mu);
@@ -2284,6 +2318,12 @@ int gd_batch_fetch_r_host(gd_batch *B, int64_t n_seeds, int64_t *r_offset, int64
 int gd_batch_last_ambiguous(const gd_batch *B, int64_t *count) {
     if (!B || !count) return GD_ERR_ARG;
     *count = B->last_amb;
+    return GD_OK;
+}
+
+int gd_batch_set_resolve(gd_batch *B, int32_t mode) {
+    if (!B || mode < GD_RESOLVE_FLAG || mode > GD_RESOLVE_ALL) return GD_ERR_ARG;
+    B->p.resolve = mode;
     return GD_OK;
 }
 

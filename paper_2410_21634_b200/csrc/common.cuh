@@ -215,9 +215,22 @@ struct ExactWorker;
 ExactWorker *exact_worker_create();
 void exact_worker_destroy(ExactWorker *w);
 cudaStream_t exact_worker_stream(ExactWorker *w);
+unsigned long long *exact_worker_scratch(ExactWorker *w);  // 4 device words
 ExactSeed exact_seed_solve(ExactWorker *w, const gd_graph *G, const gd_operator *op,
                            int32_t method, int64_t seed, double bval, double mu, double L,
                            int64_t max_sweeps, bool sgn);
+// K LocalGD seeds (host array) in one bit-exact sweep loop over K disjoint
+// copies of the graph: copy j's x, r at [j*n1, (j+1)*n1) of the worker's
+// buffers, per-copy counts below.
+struct ExactMulti {
+    int64_t n1 = 0;
+    int K = 0;
+    const double *x = nullptr, *r = nullptr;
+    std::vector<int64_t> sweeps, ops, pushes;
+    std::vector<int32_t> conv;
+};
+ExactMulti exact_multi_solve(ExactWorker *w, const gd_graph *G, const gd_operator *op,
+                             const int64_t *seeds, int K, double bval, int64_t max_sweeps);
 
 inline int n_sms(int device) {
     int v = 0;

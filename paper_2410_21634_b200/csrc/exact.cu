@@ -43,14 +43,23 @@ __device__ __forceinline__ int64_t bsearch_le(const int64_t *a, int64_t cnt, int
     return lo;
 }
 
+// Node u of the solve's id space: the graph's node u % n1 (copy u / n1).  A
+// re-solve of K seeds runs them on K disjoint copies of the graph at once
+// (node j*n1 + v = node v of copy j): the reference's sweep order restricted
+// to one copy is exactly that copy's single-seed order, so each copy's x, r
+// and counts are the single solve's bit for bit, for the launches and host
+// syncs of one solve.
+__device__ __forceinline__ int64_t base_of(int64_t u, int64_t n1) { return u < n1 ? u : u % n1; }
+
 // ---- seeds -> initial frontier flags (filter of flatnonzero(b), :383-386)
 __global__ void k_flag_active_nodes(const int32_t *__restrict__ nodes, int64_t cnt,
                                     const double *__restrict__ r, DevGraph g, DevOp op,
-                                    bool sgn, uint8_t *__restrict__ flag) {
+                                    bool sgn, uint8_t *__restrict__ flag, int64_t n1) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t u = nodes[i];
-        flag[i] = is_active(r[u], theta_of(op, u, g.deg[u]), sgn) ? 1 : 0;
+        const int64_t ub = base_of(u, n1);
+        flag[i] = is_active(r[u], theta_of(op, ub, g.deg[ub]), sgn) ? 1 : 0;
     }
 }
 
@@ -60,7 +69,7 @@ __global__ void k_gather_gd(const int32_t *__restrict__ F, int64_t f, double *__
                             double *__restrict__ r, double *__restrict__ vals,
                             double *__restrict__ absv, double *__restrict__ wnode,
                             int64_t *__restrict__ fdeg, int32_t *__restrict__ fstamp, int32_t t,
-                            DevGraph g, DevOp op) {
+                            DevGraph g, DevOp op, int64_t n1) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t u = F[i];
@@ -69,7 +78,7 @@ __global__ void k_gather_gd(const int32_t *__restrict__ F, int64_t f, double *__
         absv[i] = fabs(val);
         x[u] = __dadd_rn(x[u], val);
         r[u] = __dsub_rn(r[u], val);
-        int32_t d = g.deg[u];
+        int32_t d = g.deg[base_of(u, n1)];
         fdeg[i] = d;
         wnode[i] = node_weight(op, d);
         fstamp[u] = t;
@@ -82,7 +91,8 @@ __global__ void k_gather_ch(const int32_t *__restrict__ F, int64_t f, double *__
                             double *__restrict__ absv, double *__restrict__ wnode,
                             int64_t *__restrict__ fdeg, int32_t *__restrict__ fstamp, int32_t t,
                             double *__restrict__ mom, int32_t *__restrict__ mstamp,
-                            double step0, double coef_r, double coef_m, DevGraph g, DevOp op) {
+                            double step0, double coef_r, double coef_m, DevGraph g, DevOp op,
+                            int64_t n1) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t u = F[i];
@@ -100,7 +110,7 @@ __global__ void k_gather_ch(const int32_t *__restrict__ F, int64_t f, double *__
         mom[u] = v;
         mstamp[u] = t;
         r[u] = __dsub_rn(rv, v);
-        int32_t d = g.deg[u];
+        int32_t d = g.deg[base_of(u, n1)];
         fdeg[i] = d;
         wnode[i] = node_weight(op, d);
         fstamp[u] = t;
@@ -110,12 +120,13 @@ __global__ void k_gather_ch(const int32_t *__restrict__ F, int64_t f, double *__
 // ---- expand: arc position p -> (target key, p)
 __global__ void k_expand(const int32_t *__restrict__ F, const int64_t *__restrict__ arcoff,
                          int64_t f, int64_t P, DevGraph g, uint32_t *__restrict__ keys,
-                         uint32_t *__restrict__ pidx, int32_t *__restrict__ arc_i) {
+                         uint32_t *__restrict__ pidx, int32_t *__restrict__ arc_i, int64_t n1) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         int64_t i = bsearch_le(arcoff, f, p);
         int32_t u = F[i];
-        keys[p] = (uint32_t)g.col[g.row[u] + (p - arcoff[i])];
+        const int64_t ub = base_of(u, n1);
+        keys[p] = (uint32_t)((u - ub) + g.col[g.row[ub] + (p - arcoff[i])]);
         pidx[p] = (uint32_t)p;
         arc_i[p] = (int32_t)i;
     }
@@ -132,7 +143,7 @@ __global__ void k_fold(const uint32_t *__restrict__ ukeys, const int64_t *__rest
                        const int32_t *__restrict__ F, const double *__restrict__ vals,
                        const double *__restrict__ wnode, DevGraph g, DevOp op,
                        double *__restrict__ r, const int32_t *__restrict__ fstamp, int32_t t,
-                       uint8_t *__restrict__ head) {
+                       uint8_t *__restrict__ head, int64_t n1) {
     const int lane = threadIdx.x & 31;
     const int64_t nseg = *nseg_p;
     for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
@@ -147,7 +158,7 @@ __global__ void k_fold(const uint32_t *__restrict__ ukeys, const int64_t *__rest
                 const int64_t p = sp[q];
                 const int32_t i = arc_i[p];
                 double w = wnode[i];
-                if (op.wrule == GD_W_ARC) w = op.arc_w[g.row[F[i]] + (p - arcoff[i])];
+                if (op.wrule == GD_W_ARC) w = op.arc_w[g.row[base_of(F[i], n1)] + (p - arcoff[i])];
                 c = __dmul_rn(vals[i], w);
             }
             const int cnt = (int)min((int64_t)32, q1 - b);
@@ -166,13 +177,14 @@ __global__ void k_fold(const uint32_t *__restrict__ ukeys, const int64_t *__rest
 // ---- candidates that survive the filter (_filter_frontier :336-350)
 __global__ void k_flag_heads(const uint32_t *__restrict__ keys, const uint8_t *__restrict__ head,
                              int64_t P, const double *__restrict__ r, DevGraph g, DevOp op,
-                             bool sgn, uint8_t *__restrict__ flag) {
+                             bool sgn, uint8_t *__restrict__ flag, int64_t n1) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         uint8_t h = head[p];
         if (h) {
             uint32_t v = keys[p];
-            h = is_active(r[v], theta_of(op, v, g.deg[v]), sgn) ? 1 : 0;
+            const int64_t vb = base_of(v, n1);
+            h = is_active(r[v], theta_of(op, vb, g.deg[vb]), sgn) ? 1 : 0;
         }
         flag[p] = h;
     }
@@ -241,6 +253,30 @@ __global__ void k_sum_block(const double *__restrict__ a, int64_t n, double *__r
     if (threadIdx.x == 0) out[0] = ss[0];
 }
 
+// per-copy frontier statistics of a multi-seed re-solve: pushes, volume,
+// last sweep with work
+__global__ void k_copy_stats(const int32_t *__restrict__ F, int64_t f, int64_t n1, DevGraph g,
+                             int32_t t, unsigned long long *__restrict__ pushes,
+                             unsigned long long *__restrict__ ops, int32_t *__restrict__ last) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = F[i], j = u / n1;
+        atomicAdd(pushes + j, 1ULL);
+        atomicAdd(ops + j, (unsigned long long)g.deg[u - j * n1]);
+        atomicMax(last + j, t);
+    }
+}
+
+__global__ void k_set_seeds(double *__restrict__ r, int32_t *__restrict__ ids,
+                            const int64_t *__restrict__ seeds, int K, int64_t n1, double val) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < K) {
+        const int64_t u = j * n1 + seeds[j];
+        r[u] = val;
+        ids[j] = (int32_t)u;
+    }
+}
+
 __global__ void k_to_i64(const int32_t *__restrict__ a, int64_t n, int64_t *__restrict__ o) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -272,7 +308,9 @@ struct SweepSolver {
     const gd_graph *G;
     DevGraph g;
     HostOp op;
-    int64_t n;
+    int64_t n;           // solve id space: copies * n1
+    int64_t n1 = 0;      // graph nodes
+    int64_t copies = 1;  // disjoint copies (multi-seed re-solve)
     bool sgn;
     cudaStream_t s = 0;
     DBuf<double> x, r, vals, absv, wnode, mom, red_ps, red_pm, scal;
@@ -289,12 +327,14 @@ struct SweepSolver {
 
     // Buffers are kept across calls (per host thread, grown on demand): a
     // drop-in call should not pay a dozen n-sized cudaMalloc/cudaFree pairs.
-    void prepare(const gd_graph *G_, const gd_operator *o, bool sgn_) {
+    void prepare(const gd_graph *G_, const gd_operator *o, bool sgn_, int64_t copies_ = 1) {
         G = G_;
         sgn = sgn_;
         g = G->view();
-        n = G->n;
-        upload_op(G, o, n, op, s);
+        n1 = G->n;
+        copies = copies_;
+        n = copies * n1;
+        upload_op(G, o, n1, op, s);
         size_t nn = n ? n : 1;
         x.ensure(nn); r.ensure(nn); vals.ensure(nn); absv.ensure(nn); wnode.ensure(nn);
         F.ensure(nn); Fn.ensure(nn); fstamp.ensure(nn); seeds.ensure(nn);
@@ -328,7 +368,7 @@ struct SweepSolver {
         if (!cnt0) return 0;
         GD_CUDA(cudaMemcpy(seeds.p, nz.data(), sizeof(int32_t) * cnt0, cudaMemcpyHostToDevice));
         k_flag_active_nodes<<<blocks_for(cnt0), TPB, 0, s>>>(seeds.p, cnt0, r.p, g, op.dev, sgn,
-                                                             flag.p);
+                                                             flag.p, n1);
         GD_LAUNCH_CHECK();
         size_t bytes = 0;
         cub::DeviceSelect::Flagged(nullptr, bytes, seeds.p, flag.p, F.p, cnt.p, cnt0, s);
@@ -347,7 +387,7 @@ struct SweepSolver {
         GD_CUDA(cudaMemcpyAsync(r.p + seed, &val, sizeof(double), cudaMemcpyHostToDevice, s));
         const int32_t sd = (int32_t)seed;
         GD_CUDA(cudaMemcpyAsync(seeds.p, &sd, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-        k_flag_active_nodes<<<1, TPB, 0, s>>>(seeds.p, 1, r.p, g, op.dev, sgn, flag.p);
+        k_flag_active_nodes<<<1, TPB, 0, s>>>(seeds.p, 1, r.p, g, op.dev, sgn, flag.p, n1);
         GD_LAUNCH_CHECK();
         uint8_t f = 0;
         GD_CUDA(cudaMemcpyAsync(&f, flag.p, 1, cudaMemcpyDeviceToHost, s));
@@ -357,6 +397,24 @@ struct SweepSolver {
             GD_CUDA(cudaStreamSynchronize(s));
         }
         return f ? 1 : 0;
+    }
+
+    // K seeds on K graph copies: r = val at node j*n1 + seeds[j] (device
+    // seeds), S_0 = the active ones in id (= copy) order
+    int64_t init_copies(const int64_t *d_seeds, int K, double val) {
+        GD_CUDA(cudaMemsetAsync(r.p, 0, sizeof(double) * (n ? n : 1), s));
+        GD_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * (n ? n : 1), s));
+        k_set_seeds<<<1, 64, 0, s>>>(r.p, seeds.p, d_seeds, K, n1, val);
+        k_flag_active_nodes<<<1, TPB, 0, s>>>(seeds.p, K, r.p, g, op.dev, sgn, flag.p, n1);
+        GD_LAUNCH_CHECK();
+        size_t bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, seeds.p, flag.p, F.p, cnt.p, K, s);
+        tmp_need(bytes);
+        cub::DeviceSelect::Flagged(tmp.p, bytes, seeds.p, flag.p, F.p, cnt.p, K, s);
+        int64_t f = 0;
+        GD_CUDA(cudaMemcpyAsync(&f, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        return f;
     }
 
     // one sweep after the gather kernel ran; returns |S_{t+1}| and P
@@ -381,7 +439,8 @@ struct SweepSolver {
             head.ensure(P);
             if (flag.n < (size_t)P) flag.alloc(P);
             GD_CUDA(cudaMemsetAsync(head.p, 0, P, s));
-            k_expand<<<blocks_for(P), TPB, 0, s>>>(F.p, arcoff.p, f, P, g, keys.p, pidx.p, arc_i.p);
+            k_expand<<<blocks_for(P), TPB, 0, s>>>(F.p, arcoff.p, f, P, g, keys.p, pidx.p, arc_i.p,
+                                                   n1);
             GD_LAUNCH_CHECK();
             bytes = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, skeys.p, pidx.p, sp.p,
@@ -404,11 +463,11 @@ struct SweepSolver {
             k_fold<<<blocks_for(32 * P, 1 << 16), TPB, 0, s>>>(ukeys.p, segoff.p, nseg.p, sp.p,
                                                                arc_i.p, arcoff.p, F.p, vals.p,
                                                                wnode.p, g, op.dev, r.p, fstamp.p,
-                                                               t, head.p);
+                                                               t, head.p, n1);
             GD_LAUNCH_CHECK();
         }
         // 1) frontier members that stay active, in S_t order
-        k_flag_active_nodes<<<blocks_for(f), TPB, 0, s>>>(F.p, f, r.p, g, op.dev, sgn, flag.p);
+        k_flag_active_nodes<<<blocks_for(f), TPB, 0, s>>>(F.p, f, r.p, g, op.dev, sgn, flag.p, n1);
         GD_LAUNCH_CHECK();
         bytes = 0;
         cub::DeviceSelect::Flagged(nullptr, bytes, F.p, flag.p, Fn.p, cnt.p, f, s);
@@ -420,7 +479,7 @@ struct SweepSolver {
         int64_t c2 = 0;
         if (P > 0) {
             k_flag_heads<<<blocks_for(P), TPB, 0, s>>>(keys.p, head.p, P, r.p, g, op.dev, sgn,
-                                                       flag.p);
+                                                       flag.p, n1);
             GD_LAUNCH_CHECK();
             bytes = 0;
             cub::DeviceSelect::Flagged(nullptr, bytes, (int32_t *)keys.p, flag.p, Fn.p + c1,
@@ -470,6 +529,11 @@ SweepSolver &solver_for(const gd_graph *G, const gd_operator *o, bool sgn) {
 // several host threads can run exact seeds concurrently.
 struct ExactWorker {
     SweepSolver S;
+    // persistent small buffers (a cudaFree would synchronise the device and
+    // serialise the workers): seeds, per-copy stats, caller scratch
+    DBuf<int64_t> dseeds;
+    DBuf<unsigned long long> st, scratch;
+    DBuf<int32_t> last;
     ExactWorker() { GD_CUDA(cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking)); }
     ~ExactWorker() {
         if (S.s) cudaStreamDestroy(S.s);
@@ -477,8 +541,70 @@ struct ExactWorker {
 };
 
 ExactWorker *exact_worker_create() { return new ExactWorker(); }
+
+// K LocalGD seeds at once on K disjoint graph copies (see base_of): one sweep
+// loop, so the per-sweep launches and host syncs -- most of a single re-solve's
+// cost -- are paid once for all K.  Per copy: bit-exact x, r, sweeps, ops,
+// pushes and convergence of the single-seed solve.
+ExactMulti exact_multi_solve(ExactWorker *W, const gd_graph *G, const gd_operator *o,
+                             const int64_t *seeds, int K, double bval, int64_t max_sweeps) {
+    SweepSolver &S = W->S;
+    S.prepare(G, o, false, K);
+    ExactMulti out;
+    out.n1 = S.n1;
+    out.K = K;
+    W->dseeds.ensure(64);
+    W->st.ensure(128);
+    W->last.ensure(64);
+    GD_CHECK_ARG(K <= 64, "at most 64 seeds per exact multi-solve");
+    int64_t *dseeds = W->dseeds.p;
+    unsigned long long *st = W->st.p;
+    int32_t *last = W->last.p;
+    GD_CUDA(cudaMemcpyAsync(dseeds, seeds, sizeof(int64_t) * K, cudaMemcpyHostToDevice, S.s));
+    GD_CUDA(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * 2 * K, S.s));
+    GD_CUDA(cudaMemsetAsync(last, 0xFF, sizeof(int32_t) * K, S.s));
+    int64_t f = S.init_copies(dseeds, K, bval);
+    std::vector<int32_t> capped(K, 0);
+    int32_t t = 0;
+    while (f) {
+        if (t >= max_sweeps) {  // copies with work left are not converged
+            std::vector<int32_t> h(f);
+            GD_CUDA(cudaMemcpy(h.data(), S.F.p, sizeof(int32_t) * f, cudaMemcpyDeviceToHost));
+            for (int32_t u : h) capped[u / S.n1] = 1;
+            break;
+        }
+        k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
+                                                    S.wnode.p, S.fdeg.p, S.fstamp.p, t, S.g,
+                                                    S.op.dev, S.n1);
+        k_copy_stats<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.n1, S.g, t, st, st + K, last);
+        GD_LAUNCH_CHECK();
+        int64_t P = 0;
+        double sgamma = 0.0;
+        f = S.scatter_and_filter(f, t, &P, &sgamma);
+        ++t;
+    }
+    std::vector<unsigned long long> hs(2 * K);
+    std::vector<int32_t> hl(K);
+    GD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(unsigned long long) * 2 * K,
+                            cudaMemcpyDeviceToHost, S.s));
+    GD_CUDA(cudaMemcpyAsync(hl.data(), last, sizeof(int32_t) * K, cudaMemcpyDeviceToHost, S.s));
+    GD_CUDA(cudaStreamSynchronize(S.s));
+    for (int j = 0; j < K; ++j) {
+        out.pushes.push_back((int64_t)hs[j]);
+        out.ops.push_back((int64_t)hs[K + j]);
+        out.sweeps.push_back((int64_t)hl[j] + 1);
+        out.conv.push_back(capped[j] ? 0 : 1);
+    }
+    out.x = S.x.p;
+    out.r = S.r.p;
+    return out;
+}
 void exact_worker_destroy(ExactWorker *w) { delete w; }
 cudaStream_t exact_worker_stream(ExactWorker *w) { return w->S.s; }
+unsigned long long *exact_worker_scratch(ExactWorker *w) {
+    w->scratch.ensure(4);
+    return w->scratch.p;
+}
 
 // Bit-exact re-solve of one seed for the batched solvers (common.cuh): the
 // sweep loops of local_gd_run / gd_local_ch below without the per-sweep
@@ -515,11 +641,11 @@ ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator 
             k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t,
                                                         S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
-                                                        S.g, S.op.dev);
+                                                        S.g, S.op.dev, S.n1);
         } else {
             k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t, S.g,
-                                                        S.op.dev);
+                                                        S.op.dev, S.n1);
         }
         GD_LAUNCH_CHECK();
         int64_t P = 0;
@@ -577,7 +703,7 @@ static void local_gd_run(const gd_graph *G, const gd_operator *o, const double *
             if (record_trace) S.record(rep, tcap, f);
             k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t, S.g,
-                                                        S.op.dev);
+                                                        S.op.dev, S.n1);
             GD_LAUNCH_CHECK();
             int64_t P = 0;
             double sgamma = 0.0;
@@ -652,7 +778,7 @@ int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double
             k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t,
                                                         S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
-                                                        S.g, S.op.dev);
+                                                        S.g, S.op.dev, S.n1);
             GD_LAUNCH_CHECK();
             int64_t P = 0;
             double sgamma = 0.0;

@@ -1,4 +1,4 @@
-"""Cost of the bit-exact re-solve path on the products shape (exact_all)."""
+"""Cost of the bit-exact re-solve path on the products shape (resolve="all")."""
 import os
 import sys
 import time
@@ -13,7 +13,7 @@ dg, row, col, row_h = make_graph("products", 0, 0)
 seeds = sample_sources(_HostGraph(n, row_h), 1024, seed=0)[::64]
 for w in sys.argv[1].split(","):
     os.environ["GDIFF_RESOLVE_WORKERS"] = w
-    s = BatchSolver(dg, 0.1, 1e-7, exact_all=True)
+    s = BatchSolver(dg, 0.1, 1e-7, resolve="all")
     for _ in range(3):
         s.solve(seeds)
     t = time.perf_counter()

@@ -13,7 +13,8 @@ per seed without leaving C.  The headline kernel runs here in the mode the bench
 measures: products shape, 64 slots per wave, slot-grouped phase B (64 x 19 MB of
 residuals exceed L2).  The batch's near-threshold detector (common.cuh) re-solves
 any seed whose residual lands within 2^-36 of its threshold on the bit-exact path;
-`exact_all` does that for every seed, which must then be bitwise.
+`resolve="exact"` re-solves the flagged seeds there (`"all"`: every seed, which
+must then be bitwise); the default only reports them.
 """
 import math
 
@@ -73,11 +74,11 @@ def test_products_headline_x_parity(gpu, products):
 
     dg, hg = products
     seeds = sample_sources(hg, 192, seed=0)
-    solver = BatchSolver(dg, 0.1, 1e-7)
+    solver = BatchSolver(dg, 0.1, 1e-7, resolve="exact")
     try:
         assert solver.mode == "rounds" and solver.slots == 64
         out = solver.solve(seeds)
-        amb = solver.last_ambiguous
+        amb = solver.resolve_stats()
     finally:
         solver.close()
     ref = O.batch_local_gd(hg, 0.1, 1e-7, seeds, THREADS, arc_w=hg.arc_w, theta=hg.theta,
@@ -217,8 +218,8 @@ def test_papers100m_x_parity(gpu):
 
 
 @pytest.mark.parametrize("method", ["local-gd", "local-ch"])
-def test_exact_all_is_bitwise(gpu, arxiv, method):
-    """exact_all: every seed re-solved on the bit-exact path after the batch
+def test_resolve_all_is_bitwise(gpu, arxiv, method):
+    """resolve="all": every seed re-solved on the bit-exact path after the batch
     (the path ambiguous seeds take): x and r bitwise, integer work identical."""
     from oracle import oracle as O
     from paper_2410_21634_b200.batch import BatchSolver
@@ -227,7 +228,7 @@ def test_exact_all_is_bitwise(gpu, arxiv, method):
     dg, hg = arxiv
     seeds = sample_sources(hg, 24, seed=5)
     kw = {"method": "local-ch", "mu": 0.1, "L": 1.9} if method == "local-ch" else {}
-    solver = BatchSolver(dg, 0.1, 1e-6, exact_all=True, want_r=True, **kw)
+    solver = BatchSolver(dg, 0.1, 1e-6, resolve="all", want_r=True, **kw)
     try:
         out = solver.solve(seeds)
     finally:
