@@ -1524,7 +1524,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
               B->conv.p, B->xnodes.p, B->xvals.p, B->xcap, B->R ? B->inv.p : nullptr,
               B->hk ? std::exp(-B->p.tau) : 1.0, B->hk ? 1 : 0, B->amb.p, B->amb_cnt.p};
     int64_t launches = 0;
-    if (B->stream) {
+    if (B->stream && n_seeds > 0) {
         // one state for the whole solve; a launch per `slots` finished seeds
         RoundArgs A = B->args();
         A.m = n_seeds < B->slots ? n_seeds : B->slots;
