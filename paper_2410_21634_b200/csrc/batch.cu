@@ -1272,6 +1272,7 @@ struct gd_batch {
     int64_t cohort = 0;              // free slots that start new seeds together (0 = all)
     int32_t dbg = 0;                 // (experiments, GDIFF_DBG)
     int32_t resolve_workers = (int32_t)RESOLVE_WORKERS;
+    bool host_stream = true;         // host entry copies finished waves' x during the solve
     DBuf<int32_t> s_idx, s_t0, t_state;
     DBuf<unsigned long long> sn, sctr;  // per slot entries [2][slots]; seed / done counters
     DBuf<int64_t> drain_cnt;
@@ -1891,7 +1892,26 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
 
 extern "C" {
 
+static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_batch **out);
+
+// Creation with an out-of-memory fallback: the slot count chosen from free
+// HBM can still be too many once the other allocations are made (another
+// solver, NCCL buffers, torch's cache); then halve the slots and retry.
 int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out) {
+    int rc = batch_create_once(G, p, out);
+    if (rc != GD_ERR_OOM || !p || !out) return rc;
+    gd_batch_params q = *p;
+    int slots = p->slots;
+    if (slots <= 0) slots = 64;  // (the automatic choice is at most 64)
+    for (slots /= 2; rc == GD_ERR_OOM && slots >= 1; slots /= 2) {
+        cudaGetLastError();  // (clear the sticky-free allocation error)
+        q.slots = slots;
+        rc = batch_create_once(G, &q, out);
+    }
+    return rc;
+}
+
+static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_batch **out) {
     return guarded([&] {
         GD_CHECK_ARG(G && p && out, "null pointer");
         GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR ||
@@ -1919,6 +1939,7 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
             B->p = *p;
             if (const char *e = getenv("GDIFF_RESOLVE_WORKERS"))  // (experiments)
                 B->resolve_workers = atoi(e) < 1 ? 1 : atoi(e);
+            B->host_stream = getenv("GDIFF_NO_STREAM") == nullptr;  // (A/B, read once)
             if (B->p.max_sweeps <= 0) B->p.max_sweeps = 1000000;
             if (p->want_r && p->method != GD_M_HK) {  // sparse r pool (per-slot scratch below)
                 B->rcap = p->out_cap > 0 ? p->out_cap : (64LL << 20);
@@ -1996,7 +2017,14 @@ int gd_batch_create(const gd_graph *G, const gd_batch_params *p, gd_batch **out)
                                     // 13 -> 29 slots, eps=1e-6 50.9 K -> 65.6 K solves/s)
                 if (const char *e = getenv("GDIFF_SLOT_MEM")) frac = atof(e);  // experiments
                 int64_t budget = (int64_t)((double)fr * frac);
-                const int64_t keep = 8LL << 30;  // frontier arrays, output pools, headroom
+                // what is allocated after this sizing, explicitly: frontier
+                // arrays (6 x 8 B per entry, 64 M entries at most), chunk map
+                // (4 B), the x pool and -- with want_r -- the r pool (12 B per
+                // pair, 64 M at first); plus headroom for pool growth, the
+                // exact re-solve workers and a multi-GPU gather on rank 0
+                const int64_t fc_est = 64LL << 20;
+                const int64_t fixed = fc_est * (48 + 4) + (64LL << 20) * 12 * (p->want_r ? 2 : 1);
+                const int64_t keep = fixed + std::max<int64_t>(8LL << 30, (int64_t)(0.1 * (double)fr));
                 if (budget > (int64_t)fr - keep) budget = (int64_t)fr - keep;
                 if (budget < 0) budget = 0;
                 int64_t by_mem = budget / (ld * (B->hk ? 28 : 20));
@@ -2227,7 +2255,7 @@ int gd_batch_solve_host(gd_batch *B, const int64_t *seeds, int64_t n_seeds, int6
         GD_CUDA(cudaMemcpyAsync(B->dseeds.p, seeds, sizeof(int64_t) * n_seeds,
                                 cudaMemcpyHostToDevice, st));
         gd_batch_result res{};
-        if (x_nodes && x_vals && x_cap > 0 && !getenv("GDIFF_NO_STREAM")) {  // stream finished waves' x to the host
+        if (x_nodes && x_vals && x_cap > 0 && B->host_stream) {  // stream finished waves' x to the host
             if (!B->hs.cs) GD_CUDA(cudaStreamCreateWithFlags(&B->hs.cs, cudaStreamNonBlocking));
             B->hs.nodes = x_nodes;
             B->hs.vals = x_vals;

@@ -63,8 +63,12 @@ def _upload(mm: np.ndarray, out, dtype, torch, stage):
         out[a:b] = d if dtype == torch.int64 else d.to(dtype)
 
 
-def _validate_device(n: int, row_ptr, col, torch) -> None:
-    """The checks of CsrGraph.validate (src/graph.py:105-123) on the GPU."""
+def _validate_device(n: int, row_ptr, col, torch, chunk: int = 1 << 26) -> None:
+    """The checks of CsrGraph.validate (src/graph.py:105-123) on the GPU, in
+    row ranges of about `chunk` arcs so the temporaries stay O(chunk) (a few GB
+    at most) whatever the graph size: self loops and strictly sorted rows per
+    range, symmetry by a vectorised binary search of every arc's reverse in its
+    target's (sorted) row."""
     arcs = col.numel()
     if int(row_ptr[0]) != 0:
         raise GraphStructureError("bad offsets array")
@@ -77,18 +81,39 @@ def _validate_device(n: int, row_ptr, col, torch) -> None:
         return
     if int(col.min()) < 0 or int(col.max()) >= n:
         raise GraphStructureError("target id out of range")
-    src = torch.repeat_interleave(torch.arange(n, device=col.device, dtype=torch.int64), deg)
-    t = col.to(torch.int64)
-    if bool((src == t).any()):
-        raise GraphStructureError("self-loop present")
-    same = src[1:] == src[:-1]
-    if bool((same & (t[1:] <= t[:-1])).any()):
-        raise GraphStructureError("row targets not strictly sorted")
-    # Rows are strictly sorted, so the arc keys src*n+t are ascending; the
-    # graph is symmetric iff the sorted reversed keys are the same sequence.
-    rev, _ = torch.sort(t * n + src)
-    if not torch.equal(src * n + t, rev):
-        raise GraphStructureError("missing reverse arc")
+    dmax = int(deg.max())
+    steps = max(1, dmax.bit_length())
+    r0 = 0
+    while r0 < n:
+        # rows [r0, r1) holding at most `chunk` arcs (at least one row)
+        lim = int(row_ptr[r0]) + chunk
+        r1 = int(torch.searchsorted(row_ptr, torch.tensor([lim], device=row_ptr.device),
+                                    right=True)[0]) - 1
+        r1 = min(n, max(r0 + 1, r1))
+        a0, a1 = int(row_ptr[r0]), int(row_ptr[r1])
+        if a1 > a0:
+            src = torch.repeat_interleave(
+                torch.arange(r0, r1, device=col.device, dtype=torch.int64), deg[r0:r1])
+            t = col[a0:a1].to(torch.int64)
+            if bool((src == t).any()):
+                raise GraphStructureError("self-loop present")
+            same = src[1:] == src[:-1]
+            if bool((same & (t[1:] <= t[:-1])).any()):
+                raise GraphStructureError("row targets not strictly sorted")
+            # reverse arc (t -> src): binary search for src in row t
+            lo, hi = row_ptr[t], row_ptr[t + 1]
+            end = hi.clone()
+            for _ in range(steps + 1):
+                act = lo < hi
+                mid = torch.where(act, (lo + hi) >> 1, lo)
+                go = act & (col[mid.clamp(max=arcs - 1)].to(torch.int64) < src)
+                lo = torch.where(go, mid + 1, lo)
+                hi = torch.where(act & ~go, mid, hi)
+            found = (lo < end) & (col[lo.clamp(max=arcs - 1)].to(torch.int64) == src)
+            if not bool(found.all()):
+                raise GraphStructureError("missing reverse arc")
+            del src, t, lo, hi, end, mid, go, act, found
+        r0 = r1
 
 
 def load_device_graph(path, device: int = 0, validate: bool = True):

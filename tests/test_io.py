@@ -158,3 +158,39 @@ def test_cli_bench_matches_reference_ops(gpu, tmp_path, cora):
     for r in sor[:5]:
         ref = O.local_sor(S.make_ppr_system(g, 0.1, r["source"], 1e-6), r["omega"])
         assert r["total_ops"] == ref["total_ops"] and r["sweeps"] == ref["sweeps"]
+
+
+def test_chunked_device_validation_on_cpu_tensors():
+    """gdcsr._validate_device in small row ranges (the papers100M-scale form:
+    O(chunk) temporaries) accepts a valid CSR and rejects each structural
+    error of CsrGraph.validate (src/graph.py:105-123); run on CPU tensors."""
+    import numpy as np
+    import pytest
+    import torch
+
+    from paper_2410_21634_b200.gdcsr import GraphStructureError, _validate_device
+    from paper_2410_21634_b200.synth import rmat_graph
+
+    g = rmat_graph(3000, 12000, seed=2)
+    row = torch.as_tensor(g.offsets)
+    col = torch.as_tensor(g.targets.astype(np.int32))
+    for chunk in (1, 97, 5000, 1 << 26):
+        _validate_device(g.n, row, col, torch, chunk=chunk)
+    # a missing reverse arc: drop one arc of a row (and shift offsets)
+    u = int(np.argmax(g.degrees))
+    a = int(g.offsets[u])
+    col2 = torch.cat([col[:a], col[a + 1:]])
+    row2 = row.clone()
+    row2[u + 1:] -= 1
+    with pytest.raises(GraphStructureError):
+        _validate_device(g.n, row2, col2, torch, chunk=300)
+    # unsorted row
+    col3 = col.clone()
+    col3[a], col3[a + 1] = col[a + 1], col[a]
+    with pytest.raises(GraphStructureError):
+        _validate_device(g.n, row, col3, torch, chunk=300)
+    # self loop: replace the arc u->v by u->u (and keep rows sorted is not needed)
+    col4 = col.clone()
+    col4[a] = u
+    with pytest.raises(GraphStructureError):
+        _validate_device(g.n, row, col4, torch, chunk=300)
