@@ -39,11 +39,12 @@ def _deps_newer(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > t for d in dep)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, verbose: bool, checked: bool = False) -> str:
+    bdir = BUILD + ("_checked" if checked else "")
+    obj = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
     if _deps_newer(obj, path):
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DGD_CHECKED"] if checked else []), "-c", path, "-o", obj]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr}")
@@ -52,17 +53,20 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: libgdiff_checked.so with the device-side GD_DCHECK bounds
+    checks compiled in (csrc/common.cuh), for debugging runs via GDIFF_LIB."""
+    os.makedirs(BUILD + ("_checked" if checked else ""), exist_ok=True)
+    out = OUT.replace("libgdiff.so", "libgdiff_checked.so") if checked else OUT
     with ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+        objs = list(ex.map(lambda s: _compile(s, verbose, checked), SOURCES))
+    if not os.path.exists(out) or any(os.path.getmtime(o) > os.path.getmtime(out) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, checked="--checked" in sys.argv))

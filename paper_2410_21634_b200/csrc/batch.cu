@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
                 k = (int32_t)(key >> 32);
                 u = (int32_t)(key & 0xffffffffLL);
                 const int64_t idx = (int64_t)k * A.ld + u;
+                GD_DCHECK(k >= 0 && k < A.m && u >= 0 && u < A.n);
                 d = A.g.deg[u];
                 capped = STREAM && (int64_t)(t - A.s_t0[k]) >= A.max_sweeps;
                 if (!capped) {
@@ -912,6 +913,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
             for (int q = 0; q < UNROLL; q++) {
                 const int64_t ch = cb + q;
                 const bool live = ch < cend;
+                GD_DCHECK(!live || ch < A.ccap);
                 const uint32_t raw = live ? (uint32_t)A.chunk_e[ch] : 0u;  // same for all lanes
                 const int64_t e = raw & 0x7fffffffu;
                 const int64_t a = ch << 5;
@@ -928,8 +930,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
                 valid[q] = live && p < P;
                 k[q] = 0; v[q] = 0; dv[q] = 0; c[q] = 0.0;
                 if (valid[q]) {
+                    GD_DCHECK(me >= 0 && me < F && fa[me] <= p && p < fa[me] + A.g.n_arcs);
                     k[q] = (int32_t)(A.skey[me] >> 32);
                     c[q] = A.fcval[me];
+                    GD_DCHECK(A.frow[me] + (p - fa[me]) < A.g.n_arcs);
                     const int2 vd = __ldg(A.colp + A.frow[me] + (p - fa[me]));
                     v[q] = vd.x;
                     dv[q] = vd.y;
@@ -938,8 +942,10 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
             }
             // stage 2: the atomics, back to back (UNROLL in flight per lane)
 #pragma unroll
-            for (int q = 0; q < UNROLL; q++)
+            for (int q = 0; q < UNROLL; q++) {
+                GD_DCHECK(!valid[q] || (k[q] >= 0 && k[q] < A.m && v[q] >= 0 && v[q] < A.n));
                 old[q] = valid[q] ? atomicAdd(rn + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+            }
             // stage 3: first touch / re-touch of a pushed node / frontier entry
 #pragma unroll
             for (int q = 0; q < UNROLL; q++) {

@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < CUNROLL; ++q)
+                for (int q = 0; q < CUNROLL; ++q) {
+                    GD_DCHECK(!valid[q] || (v[q] >= 0 && v[q] < A.g.n));
                     old[q] = valid[q] ? atomicAdd(r + v[q], c[q]) : 0.0;
+                }
 #pragma unroll
                 for (int q = 0; q < CUNROLL; ++q) {
                     const long long ob = __double_as_longlong(old[q]);

@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 u = (int32_t)(key & 0xffffffffLL);
                 atomicAnd(A.cmark[cur] + (int64_t)k * A.cmw + (u >> 5), ~(1u << (u & 31)));
                 const int64_t idx = (int64_t)k * A.ld + u;
+                GD_DCHECK(k >= 0 && k < A.m && u >= 0 && u < A.g.n);
                 const double ru = A.r[idx];
                 d = A.g.deg[u];
                 const double th = theta_of(A.op, u, d);
@@ -566,8 +567,10 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                 }
             }
 #pragma unroll
-            for (int q = 0; q < SUNROLL; q++)
+            for (int q = 0; q < SUNROLL; q++) {
+                GD_DCHECK(!valid[q] || (k[q] >= 0 && k[q] < A.m && v[q] >= 0 && v[q] < A.g.n));
                 old[q] = valid[q] ? atomicAdd(A.r + (int64_t)k[q] * A.ld + v[q], c[q]) : 0.0;
+            }
 #pragma unroll
             for (int q = 0; q < SUNROLL; q++) {
                 // the value this atomic stored; the LAST update of a node in

@@ -158,6 +158,25 @@ void report_push_log(gd_report *rep, int64_t &cap, int64_t vol, double gamma, do
                      int8_t sign, int64_t fsize);
 void report_trace(gd_report *rep, int64_t &tcap, const int64_t *f, int64_t cnt);
 
+// ------------------------------------------------------- checked builds --
+// `python -m paper_2410_21634_b200.build --checked` compiles with
+// -DGD_CHECKED into libgdiff_checked.so: every GD_DCHECK traps with a message
+// on a failed index / state invariant (the bounds checks this pool allows in
+// place of compute-sanitizer); the product build compiles them out.
+#ifdef GD_CHECKED
+#define GD_DCHECK(cond)                                                              \
+    do {                                                                             \
+        if (!(cond)) {                                                               \
+            printf("GD_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+            __trap();                                                                \
+        }                                                                            \
+    } while (0)
+#else
+#define GD_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // ------------------------------------------------- near-threshold detector --
 // Batched sweep-synchronous solvers scatter with fp64 atomics, so a residual
 // is summed in another order than the reference's sequential fold
