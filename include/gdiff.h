@@ -228,6 +228,11 @@ typedef struct {
                                 the bit-exact path (their results are then the
                                 reference's bit for bit);
                                 GD_RESOLVE_ALL (2): re-solve every seed so. */
+    int32_t log_sweeps;      /* LocalGD: > 0 = record per seed the first log_sweeps
+                                sweeps' frontier size |S_t|, volume vol(S_t) and
+                                sum |r_u| over S_t (the LocalReport logs,
+                                src/reports.py:51-79; see gd_batch_logs) */
+    int32_t reserved2;
 } gd_batch_params;
 
 typedef struct {
@@ -280,6 +285,13 @@ int gd_batch_r_device(const gd_batch *b, int64_t **r_offset, int64_t **r_count,
 int gd_batch_fetch_r_host(gd_batch *b, int64_t n_seeds, int64_t *r_offset, int64_t *r_count,
                           int32_t *r_nodes, double *r_vals, int64_t r_cap, int64_t *r_total,
                           void *stream);
+/* Per-seed sweep logs of the last solve (log_sweeps > 0): host arrays of
+ * n_seeds * log_sweeps entries, row i = seed i, entry t = sweep t (rows hold
+ * min(sweeps, log_sweeps) entries, the rest 0): |S_t|, vol(S_t) and the sum
+ * of |r_u| pushed in sweep t (gamma_t = that / l1_t; for PPR l1_{t+1} =
+ * l1_t - alpha * that).  Any pointer may be NULL. */
+int gd_batch_logs(const gd_batch *b, int64_t n_seeds, int64_t *frontier_sizes, int64_t *vol_log,
+                  double *pushed_mass);
 /* Seeds of the last solve that the near-threshold detector flagged and the
  * bit-exact path re-solved (see gd_batch_result.ambiguous). */
 int gd_batch_last_ambiguous(const gd_batch *b, int64_t *count);

@@ -59,7 +59,8 @@ class BatchParams(C.Structure):
                 ("relabel", C.c_int32), ("problem", C.c_int32), ("omega", C.c_double),
                 ("mu", C.c_double), ("L", C.c_double), ("tau", C.c_double),
                 ("n_stages", C.c_int64), ("stage_w", _f64p), ("theta_coeff", C.c_double),
-                ("want_r", C.c_int32), ("resolve", C.c_int32)]
+                ("want_r", C.c_int32), ("resolve", C.c_int32),
+                ("log_sweeps", C.c_int32), ("reserved2", C.c_int32)]
 
 
 class BatchResult(C.Structure):
@@ -113,6 +114,7 @@ SIGNATURES = {
     "gd_batch_last_ambiguous": (C.c_int, [C.c_void_p, _i64p]),
     "gd_batch_resolve_stats": (C.c_int, [C.c_void_p, _i64p, _i64p, _f64p]),
     "gd_batch_set_resolve": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gd_batch_logs": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _f64p]),
     "gd_batch_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), _i64p]),
     "gd_batch_r_device": (C.c_int, [C.c_void_p, C.POINTER(_i64p), C.POINTER(_i64p), C.POINTER(_i32p),
                                     C.POINTER(_f64p), _i64p]),

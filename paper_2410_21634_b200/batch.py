@@ -54,6 +54,37 @@ class BatchOutput:
     r_count: np.ndarray | None = None
     r_nodes: np.ndarray | None = None
     r_vals: np.ndarray | None = None
+    # (log_sweeps) per seed and sweep: |S_t|, vol(S_t), sum of pushed |r_u|
+    frontier_sizes: np.ndarray | None = None
+    vol_log: np.ndarray | None = None
+    pushed_mass: np.ndarray | None = None
+    alpha: float = 0.0
+    eps: float = 0.0
+
+    def report(self, i: int):
+        """Seed i's LocalReport (src/reports.py:51-79) from the sweep logs:
+        vol_log, gamma_log (pushed |r| / l1 before the sweep), the l1 trace
+        (PPR: l1_0 = alpha, l1_{t+1} = l1_t - alpha * pushed |r|; the reference
+        sums |r| over all nodes -- equal to rounding) and frontier_sizes in
+        notes, as local_gd reports them (src/local_solvers.py:459-467)."""
+        from .reports import LocalReport
+
+        if self.frontier_sizes is None:
+            raise ValueError("the solver was created without log_sweeps")
+        k = int(self.sweeps[i])
+        if k > self.frontier_sizes.shape[1]:
+            raise ValueError(f"seed {i} ran {k} sweeps, only {self.frontier_sizes.shape[1]} logged")
+        mass = self.pushed_mass[i, :k]
+        l1 = [self.alpha]
+        for g in mass:
+            l1.append(l1[-1] - self.alpha * float(g))
+        gamma = [float(g) / l if l > 0 else 0.0 for g, l in zip(mass, l1)]
+        return LocalReport(
+            method="local-gd", problem="ppr", converged=bool(self.converged[i]), sweeps=k,
+            total_ops=int(self.total_ops[i]), eps=self.eps, residual_l1_trace=l1,
+            gamma_log=gamma, vol_log=[int(v) for v in self.vol_log[i, :k]],
+            notes={"parallel": False, "frontier_sizes": [int(v) for v in self.frontier_sizes[i, :k]],
+                   "batched": True})
 
     def r_sparse(self, i: int) -> tuple[np.ndarray, np.ndarray]:
         if self.r_offset is None:
@@ -95,7 +126,7 @@ class BatchSolver:
                  device: int = 0, relabel: bool = True, method: str = "local-gd",
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
                  L: float | None = None, hk: dict | None = None, want_r: bool = False,
-                 resolve: str = "flag"):
+                 resolve: str = "flag", log_sweeps: int = 0):
         if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
         if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
@@ -133,7 +164,9 @@ class BatchSolver:
                             tau=float(hk.get("tau", 0.0)), n_stages=int(hk.get("n_stages", 0)),
                             stage_w=gdl.ptr(sw), theta_coeff=float(hk.get("theta_coeff", 0.0)),
                             want_r=int(bool(want_r) and method != "local-hk"),
-                            resolve={"flag": 0, "exact": 1, "all": 2}[resolve])
+                            resolve={"flag": 0, "exact": 1, "all": 2}[resolve],
+                            log_sweeps=int(log_sweeps) if method == "local-gd" else 0)
+        self.log_sweeps = int(log_sweeps) if method == "local-gd" else 0
         self.want_r = bool(want_r) and method != "local-hk"
         h = C.c_void_p()
         gdl.check(self.lib.gd_batch_create(self.graph.handle, C.byref(p), C.byref(h)))
@@ -287,6 +320,16 @@ class BatchSolver:
         res = BatchOutput(out["sweeps"][:k], out["total_ops"][:k], out["pushes"][:k],
                           out["converged"][:k].astype(bool), out["x_offset"][:k],
                           out["x_count"][:k], out["x_nodes"][:t], out["x_vals"][:t])
+        if self.log_sweeps:
+            L = self.log_sweeps
+            res.frontier_sizes = np.zeros((k, L), np.int64)
+            res.vol_log = np.zeros((k, L), np.int64)
+            res.pushed_mass = np.zeros((k, L))
+            if k:
+                gdl.check(self.lib.gd_batch_logs(self.handle, k, gdl.ptr(res.frontier_sizes, C.c_int64),
+                                                 gdl.ptr(res.vol_log, C.c_int64),
+                                                 gdl.ptr(res.pushed_mass)))
+            res.alpha, res.eps = self.alpha, self.eps
         if self.want_r:
             roff, rcnt = np.empty(k, np.int64), np.empty(k, np.int64)
             rt = C.c_int64()

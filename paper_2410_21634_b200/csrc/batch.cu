@@ -95,7 +95,8 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
                    int64_t *pushes, int64_t *support, int32_t *conv, int64_t *xoff,
                    int64_t *xcnt, int32_t *xnodes, double *xvals, int64_t xcap,
                    unsigned long long *cursor, int32_t *amb, unsigned long long *amb_cnt,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t *lg_f, int64_t *lg_ops, double *lg_g,
+                   int64_t lg_cap);
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
                     int64_t *pushes, int32_t *conv, int64_t *xoff, int64_t *xcnt, int32_t *xnodes,
@@ -166,6 +167,9 @@ struct RoundArgs {
     int64_t *slot_base;
     uint32_t *secmap;   // per slot: bit per 32 B sector of r ever written (reset map)
     int64_t smw;        // words per slot in secmap
+    int64_t *lg_f, *lg_ops;  // per-seed sweep logs (log_sweeps > 0; else null):
+    double *lg_g;            //   |S_t|, vol(S_t), sum |r_u| -- row (seed_base + k)
+    int64_t lg_cap, seed_base;
     int64_t *rlog;      // per round: F, P, globaltimer ns (3 entries), debug
     int64_t rlog_cap;   // rounds recorded
     // streaming form (k_rounds<false, true>): slots refilled inside the kernel
@@ -265,16 +269,18 @@ struct Stage {
     int32_t *fin;                        // [S] slots whose seed finished (streaming)
     unsigned *nfin;                      // [2] finished, idle slots
     int32_t *idle;                       // [S] idle slots (streaming)
+    double *gsum;                        // [S] pushed |r| of the round (sweep logs)
 };
 
 __host__ __device__ inline size_t stage_bytes(int S) {
-    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 4) + (size_t)STAGE_CAP * 12 + 16 +
+    return (size_t)S * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 4 + 8) + (size_t)STAGE_CAP * 12 + 16 +
            8 * (BT / 32 + 3) + 16 + 64;
 }
 
 __device__ Stage stage_carve(void *base, int S) {
     char *p = (char *)base;
     Stage st;
+    st.gsum = (double *)p; p += 8 * S;
     st.ops = (unsigned long long *)p; p += 8 * S;
     st.pvol = (unsigned long long *)p; p += 8 * S;
     st.scnt = (unsigned long long *)p; p += 8 * S;
@@ -498,6 +504,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
         S.ops[k] = S.pvol[k] = S.scnt[k] = 0;
         S.push[k] = S.touch[k] = S.negz[k] = 0;
         S.nf[k] = 0;
+        S.gsum[k] = 0.0;
     }
     if (threadIdx.x == 0) {
         *S.fcnt = 0;
@@ -714,6 +721,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
                     A.chunk_e[c] = (int32_t)(e2 | (c < cf2 ? 0x80000000u : 0u));
             }
             const bool pushed = live && !capped;
+            if (A.lg_f && pushed) atomicAdd(S.gsum + k, fabs(val));
             slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
             block_count(fresh, k, (unsigned)d, S.pvol);
             block_count(pushed, k, (unsigned)d, S.ops);
@@ -766,6 +774,16 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
             }
         }
         __syncthreads();
+        if (A.lg_f && !STREAM && t < A.lg_cap)  // per-seed sweep logs (waves: t = sweep)
+            for (int64_t k = threadIdx.x; k < A.m; k += BT) {
+                if (S.push[k]) {
+                    const int64_t at = (A.seed_base + k) * A.lg_cap + t;
+                    atomicAdd((unsigned long long *)A.lg_f + at, (unsigned long long)S.push[k]);
+                    atomicAdd((unsigned long long *)A.lg_ops + at, S.ops[k]);
+                    atomicAdd(A.lg_g + at, S.gsum[k]);
+                }
+                S.gsum[k] = 0.0;
+            }
         counters_flush(S.ops, A.s_ops, A.m);
         counters_flush(S.pvol, A.s_pvol, A.m);
         counters_flush(S.push, A.s_pushes, A.m);
@@ -1287,6 +1305,9 @@ struct gd_batch {
     static constexpr int64_t NEAR_CAP = 1 << 16;
     DBuf<unsigned long long> amb_cnt;
     int64_t last_amb = 0;            // seeds re-solved on the exact path
+    DBuf<int64_t> lg_f, lg_ops;      // per-seed sweep logs (p.log_sweeps > 0)
+    DBuf<double> lg_g;
+    bool logs_on() const { return p.log_sweeps > 0 && p.method == GD_M_LOCAL_GD && !stream; }
     static constexpr size_t RESOLVE_WORKERS = 8;
     std::vector<ExactWorker *> workers;  // exact re-solve workers (created on demand)
     int64_t last_changed = 0;        // ... whose integer work the re-solve changed
@@ -1372,6 +1393,9 @@ struct gd_batch {
         A.s_ops = s_ops.p; A.s_pushes = s_pushes.p; A.s_negz = s_negz.p; A.s_pvol = s_pvol.p;
         A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
         A.nearl = NearList{{nearkey.p, nearkey.p + NEAR_CAP}, {nearcnt.p, nearcnt.p + 1}, NEAR_CAP};
+        if (logs_on()) {
+            A.lg_f = lg_f.p; A.lg_ops = lg_ops.p; A.lg_g = lg_g.p; A.lg_cap = p.log_sweeps;
+        }
         if (stream) {
             A.alpha = p.alpha;
             A.seed_ctr = sctr.p;
@@ -1450,6 +1474,13 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     B->xoff.ensure(ns); B->xcnt.ensure(ns); B->conv.ensure(ns); B->amb.ensure(ns);
     GD_CUDA(cudaMemsetAsync(B->cursor.p, 0, sizeof(unsigned long long), st));
     GD_CUDA(cudaMemsetAsync(B->amb_cnt.p, 0, sizeof(unsigned long long), st));
+    if (B->logs_on()) {
+        const size_t cells = ns * (size_t)B->p.log_sweeps;
+        B->lg_f.ensure(cells); B->lg_ops.ensure(cells); B->lg_g.ensure(cells);
+        GD_CUDA(cudaMemsetAsync(B->lg_f.p, 0, sizeof(int64_t) * cells, st));
+        GD_CUDA(cudaMemsetAsync(B->lg_ops.p, 0, sizeof(int64_t) * cells, st));
+        GD_CUDA(cudaMemsetAsync(B->lg_g.p, 0, sizeof(double) * cells, st));
+    }
     B->hs.streamed = 0;
     RPool rp{};
     if (B->want_r()) {
@@ -1499,7 +1530,9 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         cta_batch_run(B->cta, B->work(), B->colp.p, B->p.alpha, B->p.eps, B->p.max_sweeps, d_seeds,
                       n_seeds, B->R ? B->perm.p : nullptr, B->R ? B->inv.p : nullptr, B->sweeps.p,
                       B->ops.p, B->pushes.p, B->support.p, B->conv.p, B->xoff.p, B->xcnt.p,
-                      B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p, B->amb.p, B->amb_cnt.p, st);
+                      B->xnodes.p, B->xvals.p, B->xcap, B->cursor.p, B->amb.p, B->amb_cnt.p, st,
+                      B->logs_on() ? B->lg_f.p : nullptr, B->lg_ops.p, B->lg_g.p,
+                      B->p.log_sweeps);
         GD_CUDA(cudaEventRecord(B->ev[1], st));
         GD_CUDA(cudaStreamSynchronize(st));
         float f = 0.f;
@@ -1559,6 +1592,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
+        A.seed_base = base;
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
         GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
         GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
@@ -2353,6 +2387,21 @@ int gd_batch_last_ambiguous(const gd_batch *B, int64_t *count) {
     if (!B || !count) return GD_ERR_ARG;
     *count = B->last_amb;
     return GD_OK;
+}
+
+int gd_batch_logs(const gd_batch *B, int64_t n_seeds, int64_t *frontier_sizes, int64_t *vol_log,
+                  double *pushed_mass) {
+    return guarded([&] {
+        GD_CHECK_ARG(B, "null pointer");
+        GD_CHECK_ARG(B->logs_on(), "the batch records no sweep logs (log_sweeps, LocalGD)");
+        const size_t cells = (size_t)n_seeds * (size_t)B->p.log_sweeps;
+        GD_CHECK_ARG(cells <= B->lg_f.n, "n_seeds exceeds the last solve");
+        if (frontier_sizes)
+            GD_CUDA(cudaMemcpy(frontier_sizes, B->lg_f.p, 8 * cells, cudaMemcpyDeviceToHost));
+        if (vol_log) GD_CUDA(cudaMemcpy(vol_log, B->lg_ops.p, 8 * cells, cudaMemcpyDeviceToHost));
+        if (pushed_mass)
+            GD_CUDA(cudaMemcpy(pushed_mass, B->lg_g.p, 8 * cells, cudaMemcpyDeviceToHost));
+    });
 }
 
 int gd_batch_set_resolve(gd_batch *B, int32_t mode) {

@@ -61,6 +61,9 @@ struct CtaArgs {
     int64_t xcap;
     int32_t *amb;                 // per seed: near-threshold update seen (common.cuh)
     unsigned long long *amb_cnt;  // flagged seeds
+    int64_t *lg_f, *lg_ops;       // per-seed sweep logs (nullable): |S_t|, vol(S_t),
+    double *lg_g;                 //   sum |r_u| pushed
+    int64_t lg_cap;
 };
 
 __device__ __forceinline__ double theta_d(double tc, int32_t d) {
@@ -87,6 +90,8 @@ __device__ __forceinline__ void cta_append(bool flag, int32_t item, int32_t *lis
 __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
     using Scan = cub::BlockScan<int64_t, CT>;
     using Red = cub::BlockReduce<unsigned long long, CT>;
+    using RedD = cub::BlockReduce<double, CT>;
+    __shared__ typename RedD::TempStorage redd_tmp;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ typename Red::TempStorage red_tmp;
     __shared__ int s_F, s_nf, s_pc;
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                 s_nf = 0;
             }
             __syncthreads();
+            double my_g = 0.0;  // (sweep log) this thread's pushed |r|
             for (int tile = 0; tile < F; tile += CT) {
                 const int e = tile + tid;
                 const bool live = e < F;
@@ -160,6 +166,7 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                     const double xo = x[u];
                     x[u] = __dadd_rn(xo, val);
                     r[u] = -0.0;  // pushed (+0.0 = never touched)
+                    my_g += fabs(val);
                     d = A.g.deg[u];
                     if (near_theta(val, theta_d(A.tcoeff, d))) s_amb = 1;  // final r >= theta
                     fc[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
@@ -198,6 +205,15 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
                 __syncthreads();
             }
             const int64_t P = s_run;
+            if (A.lg_f && t < A.lg_cap) {  // sweep log: |S_t|, vol(S_t), sum |r_u|
+                const double g = RedD(redd_tmp).Sum(my_g);
+                if (tid == 0) {
+                    A.lg_f[si * A.lg_cap + t] = F;
+                    A.lg_ops[si * A.lg_cap + t] = P;
+                    A.lg_g[si * A.lg_cap + t] = g;
+                }
+                __syncthreads();
+            }
             // ------------- phase B: scatter 32-arc chunks ----------------------
             const int64_t C = min((P + 31) >> 5, A.ccap);
             const double tc = A.tcoeff;
@@ -371,7 +387,8 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
                    int64_t *pushes, int64_t *support, int32_t *conv, int64_t *xoff,
                    int64_t *xcnt, int32_t *xnodes, double *xvals, int64_t xcap,
                    unsigned long long *cursor, int32_t *amb, unsigned long long *amb_cnt,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t *lg_f, int64_t *lg_ops, double *lg_g,
+                   int64_t lg_cap) {
     if (n_seeds == 0) return;
     CtaArgs A{};
     A.g = W->view();
@@ -391,6 +408,10 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
     A.xcap = xcap;
     A.amb = amb;
     A.amb_cnt = amb_cnt;
+    A.lg_f = lg_f;
+    A.lg_ops = lg_ops;
+    A.lg_g = lg_g;
+    A.lg_cap = lg_cap;
     GD_CUDA(cudaMemsetAsync(S->next.p, 0, sizeof(unsigned long long), st));
     const int grid = (int)(n_seeds < S->slots ? n_seeds : S->slots);
     k_seed_cta<<<grid, CT, 0, st>>>(A);

@@ -323,3 +323,24 @@ def test_host_entry_streams_x_per_wave(gpu, monkeypatch, mode):
             np.testing.assert_allclose(h.x_vals[h.x_offset[i]:][:cnt[i]][a],
                                        dv[off[i]:][:cnt[i]][b], rtol=1e-9, atol=1e-15)
     solver.close()
+
+
+@pytest.mark.parametrize("mode", ["cta", "waves"])
+def test_batch_sweep_logs_are_the_reference_report(gpu, monkeypatch, mode):
+    """log_sweeps: each seed's LocalReport fields from a batched solve --
+    vol_log and frontier_sizes identical to the reference's local_gd, gamma_log
+    and the l1 trace to rounding (src/reports.py:51-79, local_solvers.py:448-467)."""
+    set_mode(monkeypatch, mode)
+    g = rmat_graph(20000, 150000, seed=5)
+    seeds = sample_sources(g, 24, seed=3)
+    solver = BatchSolver(g, 0.1, 1e-6, slots=8, log_sweeps=256)
+    out = solver.solve(seeds)
+    solver.close()
+    for i, s in enumerate(seeds):
+        ref = O.local_gd(S.make_ppr_system(g, 0.1, int(s), 1e-6))
+        rep = out.report(i)
+        assert rep.sweeps == ref["sweeps"] and rep.total_ops == ref["total_ops"]
+        assert rep.vol_log == [int(v) for v in ref["vol_log"]]
+        assert rep.notes["frontier_sizes"] == [int(v) for v in ref["frontier_sizes"]]
+        np.testing.assert_allclose(rep.gamma_log, ref["gamma_log"], rtol=1e-12)
+        np.testing.assert_allclose(rep.residual_l1_trace, ref["l1_log"], rtol=1e-12, atol=1e-300)
