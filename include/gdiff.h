@@ -352,6 +352,17 @@ typedef struct gd_pairs gd_pairs;
 int gd_pairs_create(const gd_graph *g, double alpha, double eps, const int64_t *sources,
                     int64_t k, int64_t frontier_cap, int64_t max_sweeps, gd_pairs **out,
                     int64_t *sweeps, int64_t *total_ops, int64_t *pushes, int32_t *converged);
+/* Repair method of a pool: GD_PAIRS_GD (default above) = warm-started signed
+ * LocalGD, sweep-synchronous over all pairs (p, r to rounding); GD_PAIRS_PUSH =
+ * the reference's own repair (src/dynamic.py:131-162: seeds flatnonzero(|r| >=
+ * eps d), signed FIFO push _push_kernel with omega = 1), one warp per pair,
+ * bit-identical p, r, sweeps and operation counts. */
+#define GD_PAIRS_GD 0
+#define GD_PAIRS_PUSH 1
+int gd_pairs_create_ex(const gd_graph *g, double alpha, double eps, const int64_t *sources,
+                       int64_t k, int64_t frontier_cap, int64_t max_sweeps, int32_t method,
+                       gd_pairs **out, int64_t *sweeps, int64_t *total_ops, int64_t *pushes,
+                       int32_t *converged);
 int gd_pairs_destroy(gd_pairs *p);
 /* g_new must be the previous graph with the events applied (checked on the
  * degrees); kinds[i] = 1 insert, 0 delete of edge (us[i], vs[i]). */

@@ -126,6 +126,9 @@ SIGNATURES = {
                                   _f64p, C.c_int64, _f64p, _f64p, _i64p, _i64p, _i64p, _i32p]),
     "gd_pairs_create": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, C.c_int64, C.c_int64,
                                   C.c_int64, C.POINTER(C.c_void_p), _i64p, _i64p, _i64p, _i32p]),
+    "gd_pairs_create_ex": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, C.c_int64,
+                                     C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_void_p),
+                                     _i64p, _i64p, _i64p, _i32p]),
     "gd_pairs_destroy": (C.c_int, [C.c_void_p]),
     "gd_pairs_update": (C.c_int, [C.c_void_p, C.c_void_p, _i32p, _i64p, _i64p, C.c_int64, C.c_int64,
                                   _i64p, _i64p, _i64p, _i32p]),

@@ -1092,10 +1092,22 @@ using namespace gd;
 // ---------------------------------------------------------------------------
 // gd_pairs: K resident PPR pairs on an evolving graph.
 // ---------------------------------------------------------------------------
+namespace gd {
+void fifo_pairs_run(const gd_graph *G, double *p, double *r, int64_t ld, int64_t k, double alpha,
+                    double eps, int64_t max_sweeps, int32_t *queue, uint32_t *qmark, int64_t qw,
+                    int64_t *sweeps, int64_t *ops, int64_t *pushes, int32_t *conv, cudaStream_t st);
+}
+
 struct gd_pairs {
     SignedState S;
     double alpha = 0.0, eps = 0.0;
     int64_t k = 0;
+    int32_t method = GD_PAIRS_GD;      // repair: warm signed LocalGD or the reference FIFO push
+    DBuf<int32_t> fq;                  // (push) per-pair FIFO queue
+    DBuf<uint32_t> fqm;                // (push) per-pair queued marks
+    int64_t fqw = 0;
+    DBuf<int64_t> fst;                 // (push) sweeps, ops, pushes per pair
+    DBuf<int32_t> fconv;
     std::vector<int32_t> deg;  // host copy of the current degrees (event bookkeeping)
     int64_t n_arcs = 0;
     DBuf<int32_t> gnodes, gdeg;
@@ -1131,6 +1143,40 @@ static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_
         k_pair_events<<<(int)((threads + 255) / 256), 256, 0, st>>>(A, dev_ev + e0, ne,
                                                                     1.0 - P->alpha);
     }
+    const int64_t K = P->k;
+    if (P->method == GD_PAIRS_PUSH) {  // the reference's repair: signed FIFO push per pair
+        GD_LAUNCH_CHECK();
+        const int64_t n = G->n ? G->n : 1;
+        if (!P->fq.p) {
+            P->fq.alloc((size_t)K * (size_t)(n + 2));
+            P->fqw = n / 32 + 1;
+            P->fqm.alloc((size_t)K * (size_t)P->fqw);
+            GD_CUDA(cudaMemset(P->fqm.p, 0, sizeof(uint32_t) * (size_t)K * (size_t)P->fqw));
+            P->fst.alloc(3 * (size_t)K);
+            P->fconv.alloc((size_t)K);
+        }
+        GD_CUDA(cudaEventRecord(P->e0, st));
+        fifo_pairs_run(G, S.x.p, S.r.p, S.ld, K, P->alpha, P->eps, max_sweeps, P->fq.p, P->fqm.p,
+                       P->fqw, P->fst.p, P->fst.p + K, P->fst.p + 2 * K, P->fconv.p, st);
+        GD_CUDA(cudaEventRecord(P->e1, st));
+        GD_CUDA(cudaStreamSynchronize(st));
+        float f = 0.f;
+        GD_CUDA(cudaEventElapsedTime(&f, P->e0, P->e1));
+        P->last_ms = f;
+        std::vector<int64_t> h(3 * K);
+        std::vector<int32_t> cv(K);
+        GD_CUDA(cudaMemcpy(h.data(), P->fst.p, 8 * 3 * K, cudaMemcpyDeviceToHost));
+        GD_CUDA(cudaMemcpy(cv.data(), P->fconv.p, 4 * K, cudaMemcpyDeviceToHost));
+        P->all_converged = true;
+        for (int64_t i = 0; i < K; ++i) {
+            if (sweeps) sweeps[i] = h[i];
+            if (ops) ops[i] = h[K + i];
+            if (pushes) pushes[i] = h[2 * K + i];
+            if (conv) conv[i] = cv[i];
+            P->all_converged = P->all_converged && cv[i];
+        }
+        return;
+    }
     if (scan) k_pair_scan<<<4 * n_sms(S.device), 256, 0, st>>>(A);
     GD_LAUNCH_CHECK();
     GD_CUDA(cudaEventRecord(P->e0, st));
@@ -1140,7 +1186,6 @@ static void pairs_repair(gd_pairs *P, const gd_graph *G, bool scan, int64_t max_
     float f = 0.f;
     GD_CUDA(cudaEventElapsedTime(&f, P->e0, P->e1));
     P->last_ms = f;
-    const int64_t K = P->k;
     std::vector<int32_t> last(K), cv(K);
     std::vector<unsigned long long> o(K), pu(K);
     GD_CUDA(cudaMemcpy(last.data(), S.s_last.p, 4 * K, cudaMemcpyDeviceToHost));
@@ -1162,7 +1207,16 @@ extern "C" {
 int gd_pairs_create(const gd_graph *G, double alpha, double eps, const int64_t *sources,
                     int64_t k, int64_t frontier_cap, int64_t max_sweeps, gd_pairs **out,
                     int64_t *sweeps, int64_t *total_ops, int64_t *pushes, int32_t *converged) {
+    return gd_pairs_create_ex(G, alpha, eps, sources, k, frontier_cap, max_sweeps, GD_PAIRS_GD, out,
+                              sweeps, total_ops, pushes, converged);
+}
+
+int gd_pairs_create_ex(const gd_graph *G, double alpha, double eps, const int64_t *sources,
+                       int64_t k, int64_t frontier_cap, int64_t max_sweeps, int32_t method,
+                       gd_pairs **out, int64_t *sweeps, int64_t *total_ops, int64_t *pushes,
+                       int32_t *converged) {
     return guarded([&] {
+        GD_CHECK_ARG(method == GD_PAIRS_GD || method == GD_PAIRS_PUSH, "unknown pair repair method");
         GD_CHECK_ARG(G && sources && out, "null pointer");
         GD_CHECK_ARG(k >= 1 && k <= 4096, "pair count must be in [1, 4096]");
         GD_CHECK_ARG(alpha > 0.0 && alpha < 1.0, "alpha must be in (0, 1)");
@@ -1173,6 +1227,7 @@ int gd_pairs_create(const gd_graph *G, double alpha, double eps, const int64_t *
             P->alpha = alpha;
             P->eps = eps;
             P->k = k;
+            P->method = method;
             P->deg.resize(G->n);
             P->n_arcs = G->n_arcs;
             if (G->n)

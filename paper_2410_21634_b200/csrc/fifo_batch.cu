@@ -299,6 +299,133 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
     }
 }
 
+// ---- the reference's repair for resident pairs ------------------------------
+// dynamic.repair (src/dynamic.py:131-162) on every pair of a gd_pairs pool at
+// once, one warp per pair: seeds = flatnonzero(|r| >= eps d) in index order
+// (:141), then the signed FIFO push of _push_kernel (src/local_solvers.py:
+// 48-188) with omega = 1, x_gain = 1 and weights fl(fl(1/d_u) (1 - alpha))
+// on the new graph -- pop for pop and fl() for fl() the reference, so p, r,
+// sweeps and operation counts are bit-identical with the per-pair loop.
+// p and r stay resident (no reset): values are stored exactly as computed.
+struct FifoPairsArgs {
+    DevGraph g;
+    double beta, tcoeff;
+    int64_t n, ld, k, max_sweeps;
+    double *p, *r;
+    int32_t *queue;   // (n + 2) per pair
+    uint32_t *qmark;  // qw words per pair (all clear between calls)
+    int64_t qw;
+    int64_t *sweeps, *ops, *pushes;
+    int32_t *conv;
+};
+
+__global__ void __launch_bounds__(FB_THREADS) k_fifo_pairs(FifoPairsArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t pair = (blockIdx.x * (int64_t)FB_THREADS + threadIdx.x) >> 5;
+    if (pair >= A.k) return;
+    double *x = A.p + pair * A.ld, *r = A.r + pair * A.ld;
+    int32_t *queue = A.queue + pair * (A.n + 2);
+    uint32_t *qmark = A.qmark + pair * A.qw;
+    const int64_t sent = A.n, qcap = A.n + 2;
+    // seeds in index order (:141 + :59-69): ordered warp compaction
+    int64_t rear = 0;
+    for (int64_t v0 = 0; v0 < A.n; v0 += 32) {
+        const int64_t v = v0 + lane;
+        bool act = false;
+        if (v < A.n) act = fabs(r[v]) >= theta_d(A.tcoeff, A.g.deg[v]);
+        const unsigned bal = __ballot_sync(FULL, act);
+        if (act) {
+            queue[rear + __popc(bal & lanemask_lt())] = (int32_t)v;
+            atomicOr(qmark + (v >> 5), 1u << (v & 31));
+        }
+        rear += __popc(bal);
+    }
+    int64_t front = 0, sweeps = 0, ops = 0, pushes = 0;
+    int conv = 1;
+    __syncwarp();
+    if (rear > 0) {
+        if (lane == 0) queue[rear] = (int32_t)sent;
+        rear = rear + 1 == qcap ? 0 : rear + 1;
+        int64_t svol = 0;
+        __syncwarp();
+        for (;;) {
+            const int64_t u = queue[front];
+            front = (front + 1 == qcap) ? 0 : front + 1;
+            if (u == sent) {  // sweep boundary (:102-144)
+                ops += svol;
+                sweeps += 1;
+                if (front == rear) break;
+                if (sweeps >= A.max_sweeps) {
+                    conv = 0;
+                    break;
+                }
+                if (lane == 0) queue[rear] = (int32_t)sent;
+                rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                svol = 0;
+                __syncwarp();
+                continue;
+            }
+            const double ru = r[u];
+            const int32_t d = A.g.deg[u];
+            const int64_t rs = A.g.row[u];
+            if (lane == 0) atomicAnd(qmark + (u >> 5), ~(1u << (u & 31)));
+            const double th = theta_d(A.tcoeff, d);
+            if (fabs(ru) < th) {
+                __syncwarp();
+                continue;
+            }
+            svol += d;
+            pushes += 1;
+            const double res = ru;  // omega = 1
+            if (lane == 0) {
+                x[u] = __dadd_rn(x[u], res);  // x_gain = 1
+                r[u] = __dsub_rn(ru, res);
+            }
+            __syncwarp();
+            const double w = __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta);
+            for (int64_t base = 0; base < d; base += 32) {
+                const int64_t j = base + lane;
+                bool act = false;
+                int32_t v = 0;
+                if (j < d) {
+                    v = A.g.col[rs + j];
+                    const double rv = __dadd_rn(r[v], __dmul_rn(res, w));
+                    r[v] = rv;
+                    if (!((qmark[v >> 5] >> (v & 31)) & 1u))
+                        act = fabs(rv) >= theta_d(A.tcoeff, A.g.deg[v]);
+                }
+                const unsigned bal = __ballot_sync(FULL, act);
+                if (act) {
+                    int64_t q = rear + __popc(bal & lanemask_lt());
+                    if (q >= qcap) q -= qcap;
+                    queue[q] = v;
+                    atomicOr(qmark + (v >> 5), 1u << (v & 31));
+                }
+                rear += __popc(bal);
+                if (rear >= qcap) rear -= qcap;
+                __syncwarp();
+            }
+            const double ru2 = r[u];  // self re-check (:176-185)
+            if (!((qmark[u >> 5] >> (u & 31)) & 1u) && fabs(ru2) >= th) {
+                if (lane == 0) {
+                    queue[rear] = (int32_t)u;
+                    atomicOr(qmark + (u >> 5), 1u << (u & 31));
+                }
+                rear = (rear + 1 == qcap) ? 0 : rear + 1;
+            }
+            __syncwarp();
+        }
+    }
+    if (!conv)  // a sweep cap left nodes queued: clear their marks
+        for (int64_t w = lane; w < A.qw; w += 32) qmark[w] = 0u;
+    if (lane == 0) {
+        A.sweeps[pair] = sweeps;
+        A.ops[pair] = ops;
+        A.pushes[pair] = pushes;
+        A.conv[pair] = conv;
+    }
+}
+
 }  // namespace
 
 // Host side, called from batch.cu for GD_M_LOCAL_SOR batches.
@@ -376,6 +503,24 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
     const int64_t warps = F->nslots < n_seeds ? F->nslots : (n_seeds ? n_seeds : 1);
     const int blocks = (int)((warps * 32 + FB_THREADS - 1) / FB_THREADS);
     k_fifo_batch<<<blocks, FB_THREADS, 0, st>>>(A);
+    GD_LAUNCH_CHECK();
+}
+
+void fifo_pairs_run(const gd_graph *G, double *p, double *r, int64_t ld, int64_t k, double alpha,
+                    double eps, int64_t max_sweeps, int32_t *queue, uint32_t *qmark, int64_t qw,
+                    int64_t *sweeps, int64_t *ops, int64_t *pushes, int32_t *conv, cudaStream_t st) {
+    FifoPairsArgs A{};
+    A.g = G->view();
+    A.beta = 1.0 - alpha;
+    A.tcoeff = eps;  // repair thresholds eps * d_u (src/dynamic.py:139-141)
+    A.n = G->n;
+    A.ld = ld;
+    A.k = k;
+    A.max_sweeps = max_sweeps;
+    A.p = p; A.r = r; A.queue = queue; A.qmark = qmark; A.qw = qw;
+    A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.conv = conv;
+    const int blocks = (int)((k * 32 + FB_THREADS - 1) / FB_THREADS);
+    k_fifo_pairs<<<blocks, FB_THREADS, 0, st>>>(A);
     GD_LAUNCH_CHECK();
 }
 

@@ -237,3 +237,51 @@ def test_signed_grouped_mode(gpu, monkeypatch, group):
         if not g.has_edge(u, v) and all((e.u, e.v) != (u, v) for e in b):
             b.append(EdgeEvent("insert", u, v))
     _pool_against_oracle(g, [b], sample_sources(g, 12, seed=4).tolist(), 0.15, 1e-5)
+
+
+def test_pair_pool_push_is_the_reference_run_snapshots(gpu, dyn):
+    """PairPool(method="push"): the reference's own repair (signed FIFO push,
+    src/dynamic.py:131-162) for every resident pair -- the golden dynamic
+    stream of the reference itself bit for bit (p, r, per-snapshot sweeps and
+    operation counts), and every source of an R-MAT stream bitwise with the
+    per-pair run_snapshots loop (src/dynamic.py:165-196)."""
+    from paper_2410_21634_b200.dynamic import PairPool, make_pair, run_snapshots
+    from paper_2410_21634_b200.graph import EdgeEvent, apply_events
+    g0 = golden_graph(dyn, "er120")
+    ev = dyn["events"]
+    batches = [[EdgeEvent("insert" if k else "delete", int(u), int(v))
+                for b, k, u, v in ev if b == bi] for bi in range(int(ev[:, 0].max()) + 1)]
+    pool = PairPool(g0, [0], 0.2, 0.2 * 1e-4, method="push")
+    sweeps, ops = [int(pool.last["sweeps"][0])], [int(pool.last["total_ops"][0])]
+    for b in batches:
+        st = pool.update(b)
+        sweeps.append(int(st["sweeps"][0]))
+        ops.append(int(st["total_ops"][0]))
+    got = pool.pair(0)
+    assert np.array_equal(got.p, dyn["dynamic/p"]) and np.array_equal(got.r, dyn["dynamic/r"])
+    assert sweeps == dyn["dynamic/sweeps"].tolist() and ops == dyn["dynamic/total_ops"].tolist()
+    pool.close()
+    # R-MAT stream, many sources at once
+    g = rmat_graph(6000, 40000, seed=11)
+    rng = np.random.default_rng(0)
+    stream, sim = [], g
+    for _ in range(3):
+        b = []
+        for _ in range(80):
+            u, v = sorted(rng.choice(g.n, 2, replace=False).tolist())
+            if any((e.u, e.v) == (u, v) for e in b):
+                continue
+            b.append(EdgeEvent("delete" if sim.has_edge(u, v) else "insert", u, v))
+        sim = apply_events(sim, b)
+        stream.append(b)
+    sources = sample_sources(g, 24, seed=3).tolist()
+    alpha, eps = 0.15, 0.15 * 1e-5
+    pool = PairPool(g, sources, alpha, eps, method="push")
+    stats = [pool.last] + [pool.update(b) for b in stream]
+    for i, s in enumerate(sources):
+        reps, pair, _ = run_snapshots(g, stream, make_pair(g, alpha, eps, int(s)), mode="dynamic")
+        assert [int(st["sweeps"][i]) for st in stats] == [r.sweeps for r in reps]
+        assert [int(st["total_ops"][i]) for st in stats] == [r.total_ops for r in reps]
+        got = pool.pair(i)
+        assert np.array_equal(got.p, pair.p) and np.array_equal(got.r, pair.r)
+    pool.close()
