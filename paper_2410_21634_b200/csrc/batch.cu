@@ -2170,6 +2170,7 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                     int64_t cap = (int64_t)(fr / 4) / per;
                     if (p->slots > 0 && p->slots < cap) cap = p->slots;
                     if (cap >= 1) B->cta = cta_batch_create(B->work(), (int)(cap < (1 << 20) ? cap : (1 << 20)));
+                    if (B->cta) B->stream = false;  // (the round kernel is not used)
                 }
             }
         } catch (...) {

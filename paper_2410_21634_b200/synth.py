@@ -22,7 +22,7 @@ from .graph import CsrGraph, csr_from_pairs, from_edges
 
 __all__ = [
     "path_graph", "complete_graph", "star_graph", "erdos_renyi",
-    "preferential_attachment", "rmat_edges", "rmat_graph", "RMAT_SHAPES",
+    "preferential_attachment", "rmat_edges", "rmat_graph", "rmat_edge_order", "RMAT_SHAPES",
     "splitmix64", "permute_ids", "csr_hash",
 ]
 
@@ -154,6 +154,15 @@ def rmat_graph(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19),
     and candidates are drawn in chunks until m distinct edges exist; the
     first m distinct edges (by first appearance) are kept.
     """
+    sel = rmat_edge_order(n, m, seed, abc, chunk)
+    pairs = np.stack([sel // n, sel % n], axis=1)
+    return csr_from_pairs(n, pairs)
+
+
+def rmat_edge_order(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19),
+                    chunk: int | None = None) -> np.ndarray:
+    """The m edges of rmat_graph as undirected keys min*n+max in generation
+    (first appearance) order -- the order config 5 splits into snapshots."""
     scale = max(1, int(np.ceil(np.log2(max(n, 2)))))
     chunk = chunk or max(1024, int(m * 1.25) + 1024)
     keys = np.empty(0, dtype=np.int64)
@@ -171,11 +180,8 @@ def rmat_graph(n: int, m: int, seed: int = 0, abc=(0.57, 0.19, 0.19),
         drawn += chunk
         uk, pos = np.unique(keys, return_index=True)
         if uk.shape[0] >= m:
-            sel = uk[np.argsort(first[pos], kind="stable")[:m]]
-            break
+            return uk[np.argsort(first[pos], kind="stable")[:m]]
         keys, first = uk, first[pos]
-    pairs = np.stack([sel // n, sel % n], axis=1)
-    return csr_from_pairs(n, pairs)
 
 
 def csr_hash(g) -> str:

@@ -35,7 +35,10 @@ MODES = ["cta", "stream", "waves"]
 
 def set_mode(monkeypatch, mode):
     monkeypatch.setenv("GDIFF_BATCH_MODE", "cta" if mode == "cta" else "rounds")
-    monkeypatch.setenv("GDIFF_STREAM", "0" if mode == "waves" else "1")
+    if mode == "cta":
+        monkeypatch.delenv("GDIFF_STREAM", raising=False)
+    else:
+        monkeypatch.setenv("GDIFF_STREAM", "0" if mode == "waves" else "1")
 
 
 @pytest.mark.parametrize("mode", MODES)
