@@ -278,7 +278,10 @@ def run_reference(args):
         if args.method == "local-hk":
             args.ch = {k: v for k, v in hk_config(args, hg).items() if k != "stage_w"}
     steps_total = args.steps + args.warmup
-    allseeds = sample_sources(hg, args.seeds * world * steps_total, seed=0)
+    want = args.seeds * world * steps_total
+    allseeds = sample_sources(hg, want, seed=0)
+    if len(allseeds) < want:  # small graphs: fewer eligible nodes than seeds asked for
+        allseeds = np.resize(allseeds, want)
     batches = [allseeds[k * args.seeds:(k + 1) * args.seeds] for k in range(steps_total)]
     # each step: a bounded sample of that step's batch (about 3 s of CPU work),
     # taken with a uniform stride so it spans the degree-ranked batch
@@ -359,7 +362,10 @@ def main():
         col = None
         torch.cuda.empty_cache()
     steps_total = args.warmup + args.steps
-    allseeds = sample_sources(hdeg, args.seeds * world * steps_total, seed=0)
+    want = args.seeds * world * steps_total
+    allseeds = sample_sources(hdeg, want, seed=0)
+    if len(allseeds) < want:  # small graphs: fewer eligible nodes than seeds asked for
+        allseeds = np.resize(allseeds, want)
     from paper_2410_21634_b200.shard import STAT_FIELDS, gather_results, shard_seeds
 
     mine = shard_seeds(allseeds, rank, world)  # round-robin over the degree-ranked sample

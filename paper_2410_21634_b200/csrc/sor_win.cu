@@ -8,11 +8,9 @@
 // folds, the reference's enqueue order), so one seed's pops overlap their
 // memory round trips instead of paying them one pop at a time.  Persistent
 // CTAs (one per SM: the window tables take ~210 KB of shared memory) pull
-// seeds from a counter; a CTA's slot is a dense x / r pair plus the lists of
-// nodes whose x / r became nonzero (window.cuh tracking): at the end of the
-// seed x is output over the pushed list (caller ids are the graph's: the FIFO
-// replay needs the caller's CSR order, no relabel) and x, r are zeroed over
-// the two lists -- no O(n) scan per seed.
+// seeds from a counter; a CTA's slot is a dense x / r pair, scanned once at
+// the end of the seed (x != 0 -> output, caller ids are the graph's: the FIFO
+// replay needs the caller's CSR order, no relabel) and returned to zero.
 #include "common.cuh"
 #include "window.cuh"
 
@@ -27,7 +25,6 @@ struct SwArgs {
     double *x, *r;        // per CTA: ld
     int32_t *queue;       // per CTA: n + 2
     uint32_t *qmark;      // per CTA: qw words
-    int32_t *tlist, *plist;  // per CTA: n (touched r / pushed x nodes)
     const int64_t *seeds;
     int64_t n_seeds;
     unsigned long long *next_seed, *cursor;
@@ -44,15 +41,12 @@ __global__ void __launch_bounds__(win::WT, 1) k_sor_win(SwArgs A) {
     __shared__ int64_t sh_sweeps, sh_ops, sh_base;
     __shared__ int sh_done, sh_conv;
     __shared__ int sh_wc[win::WT / 32];
-    __shared__ int sh_tcnt, sh_pcnt;
     win::init_smem(S);
     const int64_t qcap = A.n + 2;
     double *const x = A.x + (int64_t)blockIdx.x * A.ld;
     double *const r = A.r + (int64_t)blockIdx.x * A.ld;
     win::Sys Y{A.g, A.op, x, r, A.queue + (int64_t)blockIdx.x * qcap,
-               A.qmark + (int64_t)blockIdx.x * A.qw, qcap, A.omega, 1.0, A.omega > 1.0 ? 1 : 0, 0,
-               A.tlist + (int64_t)blockIdx.x * A.n, A.plist + (int64_t)blockIdx.x * A.n, &sh_tcnt,
-               &sh_pcnt};
+               A.qmark + (int64_t)blockIdx.x * A.qw, qcap, A.omega, 1.0, A.omega > 1.0 ? 1 : 0, 0};
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     for (;;) {
         if (t == 0) sh_seed = (long long)atomicAdd(A.next_seed, 1ULL);
@@ -62,9 +56,6 @@ __global__ void __launch_bounds__(win::WT, 1) k_sor_win(SwArgs A) {
         const int32_t s = (int32_t)A.seeds[si];
         if (t == 0) {
             r[s] = A.alpha;
-            Y.tlist[0] = s;
-            sh_tcnt = 1;
-            sh_pcnt = 0;
             const bool act = is_active(A.alpha, theta_of(A.op, s, A.g.deg[s]), Y.sgn);
             if (act) {
                 Y.queue[0] = s;
@@ -101,13 +92,15 @@ __global__ void __launch_bounds__(win::WT, 1) k_sor_win(SwArgs A) {
         }
         if (!sh_conv)  // marks of the nodes still queued
             for (int64_t w = t; w < A.qw; w += win::WT) Y.qmark[w] = 0u;
-        // x out over the pushed list (x > 0 there: unsigned push); x and r
-        // back to zero over the pushed / touched lists
-        const int np = sh_pcnt, nt = sh_tcnt;
-        (void)lane;
-        (void)wid;
+        // x out: nonzero entries in node order; x and r back to zero
+        int mine = 0;
+        for (int64_t u = t; u < A.n; u += win::WT) mine += __double_as_longlong(x[u]) != 0;
+        mine = __reduce_add_sync(0xffffffffu, mine);
+        if (lane == 0) sh_wc[wid] = mine;
+        __syncthreads();
         if (t == 0) {
-            const int tot = np;
+            int tot = 0;
+            for (int w = 0; w < win::WT / 32; ++w) tot += sh_wc[w];
             sh_base = (int64_t)atomicAdd(A.cursor, (unsigned long long)tot);
             A.sweeps[si] = sh_sweeps;
             A.ops[si] = sh_ops;
@@ -117,18 +110,35 @@ __global__ void __launch_bounds__(win::WT, 1) k_sor_win(SwArgs A) {
             A.xoff[si] = sh_base;
         }
         __syncthreads();
-        const int64_t pos = sh_base;
-        for (int i = t; i < np; i += win::WT) {
-            const int32_t u = Y.plist[i];
-            const double xv = x[u];
-            x[u] = 0.0;
-            if (pos + i < A.xcap) {
-                A.xnodes[pos + i] = u;
-                A.xvals[pos + i] = xv;
+        int64_t pos = sh_base;
+        for (int64_t b0 = 0; b0 < A.n; b0 += win::WT) {
+            const int64_t u = b0 + t;
+            double xv = 0.0;
+            if (u < A.n) {
+                xv = x[u];
+                r[u] = 0.0;
             }
+            const bool nz = __double_as_longlong(xv) != 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) sh_wc[wid] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+            for (int w = 0; w < win::WT / 32; ++w) {
+                const int c = sh_wc[w];
+                off += w < wid ? c : 0;
+                tot += c;
+            }
+            if (nz) {
+                const int64_t p = pos + off + __popc(bal & win::lanemask_lt());
+                if (p < A.xcap) {
+                    A.xnodes[p] = (int32_t)u;
+                    A.xvals[p] = xv;
+                }
+                x[u] = 0.0;
+            }
+            pos += tot;
+            __syncthreads();
         }
-        for (int i = t; i < nt; i += win::WT) r[Y.tlist[i]] = 0.0;
-        __syncthreads();
     }
 }
 
@@ -138,7 +148,7 @@ struct SorWinState {
     int ctas = 0;
     int64_t ld = 0, qw = 0;
     DBuf<double> x, r;
-    DBuf<int32_t> queue, tlist, plist;
+    DBuf<int32_t> queue;
     DBuf<uint32_t> qmark;
     DBuf<unsigned long long> next;
 };
@@ -164,8 +174,6 @@ SorWinState *sorwin_create(const gd_graph *G, int max_ctas) {
         GD_CUDA(cudaMemset(W->x.p, 0, sizeof(double) * sn));
         GD_CUDA(cudaMemset(W->r.p, 0, sizeof(double) * sn));
         W->queue.alloc((size_t)ctas * (size_t)(n + 2));
-        W->tlist.alloc((size_t)ctas * (size_t)n);
-        W->plist.alloc((size_t)ctas * (size_t)n);
         W->qmark.alloc((size_t)ctas * (size_t)W->qw);
         GD_CUDA(cudaMemset(W->qmark.p, 0, sizeof(uint32_t) * (size_t)ctas * (size_t)W->qw));
         W->next.alloc(1);
@@ -193,7 +201,6 @@ void sorwin_run(SorWinState *W, const gd_graph *G, const gd_batch_params &p,
     A.max_sweeps = p.max_sweeps > 0 ? p.max_sweeps : 1000000;
     A.qw = W->qw;
     A.x = W->x.p; A.r = W->r.p; A.queue = W->queue.p; A.qmark = W->qmark.p;
-    A.tlist = W->tlist.p; A.plist = W->plist.p;
     A.seeds = d_seeds; A.n_seeds = n_seeds;
     A.next_seed = W->next.p; A.cursor = cursor;
     A.sweeps = sweeps; A.ops = ops; A.pushes = pushes; A.xoff = xoff; A.xcnt = xcnt;

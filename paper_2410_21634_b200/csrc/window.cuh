@@ -93,21 +93,7 @@ struct Sys {
     double omega, gain;
     int sgn;
     int stats;  // accumulate sgamma / sign flags (the logs)
-    // optional (batched seeds): nodes whose r / x first became nonzero, so the
-    // slot is cleared over them instead of by an O(n) scan; with tracking on,
-    // a residual that becomes exactly zero is stored as -0.0 (adds like +0.0)
-    // so a node enters the touched list once
-    int32_t *tlist = nullptr, *plist = nullptr;
-    int *tcnt = nullptr, *pcnt = nullptr;  // (shared-memory counters)
 };
-
-__device__ __forceinline__ double track_zero(const Sys &Y, double v) {
-    return (Y.tlist && __double_as_longlong(v) == 0) ? -0.0 : v;
-}
-
-__device__ __forceinline__ void track_append(int32_t *list, int *cnt, int32_t v) {
-    list[atomicAdd(cnt, 1)] = v;
-}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -187,9 +173,8 @@ __device__ void big_pop(const Sys &Y, Smem &S) {
     const int nslots = S.nslots;  // (thread 0 resets it at the end)
     if (t == 0) {
         atomicAnd(Y.qmark + (u >> 5), ~(1u << (u & 31)));
-        Y.r[u] = track_zero(Y, __dsub_rn(ru, res));
+        Y.r[u] = __dsub_rn(ru, res);
         Y.x[u] = __dadd_rn(S.px[0], __dmul_rn(Y.gain, res));
-        if (Y.plist && __double_as_longlong(S.px[0]) == 0) track_append(Y.plist, Y.pcnt, u);
         pop_stats(Y, S, 0);
     }
     __syncthreads();
@@ -206,8 +191,7 @@ __device__ void big_pop(const Sys &Y, Smem &S) {
             const uint32_t qm = Y.qmark[v >> 5];
             const double th = theta_of(Y.op, v, Y.g.deg[v]);
             const double rv = __dadd_rn(old, __dmul_rn(res, w));
-            Y.r[v] = track_zero(Y, rv);
-            if (Y.tlist && __double_as_longlong(old) == 0) track_append(Y.tlist, Y.tcnt, v);
+            Y.r[v] = rv;
             act = !((qm >> (v & 31)) & 1u) && is_active(rv, th, Y.sgn);
         }
         const unsigned bal = __ballot_sync(FULL, act);
@@ -548,9 +532,7 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
                     S.keynode[key] = v;
                 }
             }
-            if (c || (popped && S.pact[hp])) Y.r[v] = track_zero(Y, val);
-            if (Y.tlist && c && hp == 0xff && __double_as_longlong(sval[q]) == 0)
-                track_append(Y.tlist, Y.tcnt, v);
+            if (c || (popped && S.pact[hp])) Y.r[v] = val;
             if (popped) {
                 if (!mark) atomicAnd(Y.qmark + (v >> 5), ~(1u << (v & 31)));
             } else if (mark && !(sinfo[q] & 1)) {
@@ -560,7 +542,6 @@ __device__ void run_sweep(const Sys &Y, Smem &S) {
         if (t < cut && S.pact[t]) {
             const double ru = S.pr[t];
             Y.x[S.pu[t]] = __dadd_rn(S.px[t], __dmul_rn(Y.gain, __dmul_rn(Y.omega, ru)));
-            if (Y.plist && __double_as_longlong(S.px[t]) == 0) track_append(Y.plist, Y.pcnt, S.pu[t]);
             if (Y.stats) {
                 if (ru > 0.0) S.pos = 1;
                 else if (ru < 0.0) S.neg = 1;
