@@ -130,6 +130,12 @@ int gd_local_gd_warm(const gd_graph *g, const gd_operator *op, double *x, double
 int gd_local_ch(const gd_graph *g, const gd_operator *op, const double *b, double *x,
                 double *r, double mu, double L, int64_t max_sweeps, int32_t record_trace,
                 gd_report *rep);
+/* LocalHB (heavy-ball momentum, no reference counterpart): local_ch's loop with
+ * eta = 4/(sqrt(L)+sqrt(mu))^2, beta = ((sqrt(L)-sqrt(mu))/(sqrt(L)+sqrt(mu)))^2;
+ * bit-exact with the restatement oracle/ orc_local_hb. */
+int gd_local_hb(const gd_graph *g, const gd_operator *op, const double *b, double *x,
+                double *r, double mu, double L, int64_t max_sweeps, int32_t record_trace,
+                gd_report *rep);
 
 /* FIFO push: replaces _push_kernel (src/local_solvers.py:48-188); x, r are
  * updated in place (LocalGS/LocalSOR, dynamic repair). */
@@ -181,6 +187,10 @@ int gd_spectral_norm(const gd_graph *g, const double *x0, int64_t iters, double 
                             with the same frontier sets, sweeps and operation
                             counts, x to rounding of the atomic scatter */
 
+#define GD_M_LOCAL_HB 4  /* LocalHB: LocalCH's sweep loop with Polyak's heavy-ball
+                            coefficients (no reference counterpart; restatement
+                            oracle/ orc_local_hb), same frontier rule, momentum
+                            stamps and divergence abort (batch_signed.cu) */
 #define GD_M_HK 3        /* heat-kernel push on the stage-expanded system, run as
                             layered sweeps (batch.cu): per seed local_hk(g, tau,
                             s, eps) with the same sweeps and operation counts,

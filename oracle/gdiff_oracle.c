@@ -333,9 +333,34 @@ int orc_local_gd_warm(int64_t n, const int64_t *off, const int64_t *tgt, const d
 
 /* src/local_solvers.py:473-538 (local_ch); mu, L resolved by the caller via
  * the _cheby_bounds rule (src/local_solvers.py:541-558). */
+static int local_momentum(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                          const double *theta, const double *b, double *x, double *r, double mu,
+                          double L, int64_t max_sweeps, int32_t record_trace, orc_report *rep,
+                          int hb);
+
 int orc_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
                  const double *theta, const double *b, double *x, double *r, double mu,
                  double L, int64_t max_sweeps, int32_t record_trace, orc_report *rep) {
+    return local_momentum(n, off, tgt, w, theta, b, x, r, mu, L, max_sweeps, record_trace, rep, 0);
+}
+
+/* LocalHB (heavy-ball momentum): NOT in the reference -- its momentum method
+ * is local_ch.  Restated as local_ch (src/local_solvers.py:473-538) with
+ * Polyak's stationary coefficients for eigenvalues in [mu, L] (the limit of
+ * the Chebyshev recurrence): eta = 4/(sqrt(L)+sqrt(mu))^2, beta = ((sqrt(L)-
+ * sqrt(mu))/(sqrt(L)+sqrt(mu)))^2; sweep 0 vals = eta r, then eta r + beta
+ * prev.  Pinned to the reference's own _SweepDriver by tests/golden/hb.npz
+ * (tests/golden/make_golden_hb.py). */
+int orc_local_hb(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                 const double *theta, const double *b, double *x, double *r, double mu,
+                 double L, int64_t max_sweeps, int32_t record_trace, orc_report *rep) {
+    return local_momentum(n, off, tgt, w, theta, b, x, r, mu, L, max_sweeps, record_trace, rep, 1);
+}
+
+static int local_momentum(int64_t n, const int64_t *off, const int64_t *tgt, const double *w,
+                          const double *theta, const double *b, double *x, double *r, double mu,
+                          double L, int64_t max_sweeps, int32_t record_trace, orc_report *rep,
+                          int hb) {
     rep_init(rep);
     sweep_driver d;
     drv_init(&d, n, off, tgt, w, theta, b, x, r, 1, rep);
@@ -361,7 +386,21 @@ int orc_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const double
             rvals[i] = r[u];
         }
         double sgamma = pw_sum(rvals, d.fcount, 1);
-        if (t == 0) {
+        if (hb) {
+            const double sq = sqrt(L), sm = sqrt(mu);
+            const double eta = 4.0 / ((sq + sm) * (sq + sm));
+            const double q = (sq - sm) / (sq + sm);
+            const double beta = q * q;  /* (python ** 2 of a double: one product) */
+            for (int64_t i = 0; i < d.fcount; i++) {
+                int64_t u = d.front[i];
+                if (t == 0) {
+                    vals[i] = eta * rvals[i];
+                } else {
+                    double prev = (stamp[u] == t - 1) ? mom[u] : 0.0;
+                    vals[i] = eta * rvals[i] + beta * prev;
+                }
+            }
+        } else if (t == 0) {
             for (int64_t i = 0; i < d.fcount; i++) vals[i] = step0 * rvals[i];
         } else {
             double delta_next = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
@@ -739,7 +778,7 @@ typedef struct {
     const int64_t *off, *tgt;
     const double *w, *theta;
     double alpha;
-    int32_t method;  /* 0 local_gd, 1 local_sor, 2 local_ch */
+    int32_t method;  /* 0 local_gd, 1 local_sor, 2 local_ch, 3 local_hb */
     double omega;
     double mu, L;    /* local_ch bounds */
     const int64_t *seeds;
@@ -778,11 +817,12 @@ static void *batch_worker(void *arg) {
             orc_push_kernel(n, J->off, J->tgt, J->w, J->theta, x, r, &sd, 1, J->omega, 1.0,
                             J->omega > 1.0, J->max_sweeps, &rep);
             pushes = -1;
-        } else if (J->method == 2) {
-            /* local_ch (src/local_solvers.py:473-538) on b = bval e_s */
-            orc_local_ch(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->mu, J->L, J->max_sweeps,
-                         0, &rep);
-            pushes = -1;
+        } else if (J->method == 2 || J->method == 3) {
+            /* local_ch (src/local_solvers.py:473-538) / its heavy-ball form on b = bval e_s */
+            local_momentum(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->mu, J->L, J->max_sweeps,
+                           0, &rep, J->method == 3);
+            pushes = 0;
+            for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
         } else {
             orc_local_gd(n, J->off, J->tgt, J->w, J->theta, b, x, r, J->max_sweeps, 0, &rep);
             for (int64_t t = 0; t < rep.n_logs; t++) pushes += rep.frontier_sizes[t];
@@ -842,9 +882,10 @@ int orc_batch_local_ch(int64_t n, const int64_t *off, const int64_t *tgt, const 
                        int32_t n_threads, int64_t *out_sweeps, int64_t *out_ops,
                        int32_t *out_conv, double *out_xsum, const int64_t *g_off,
                        const int64_t *g_cnt, const int32_t *g_nodes, const double *g_vals,
-                       double *out_l1d, double *out_l1r, int32_t *out_topk, int32_t topk_k) {
+                       double *out_l1d, double *out_l1r, int32_t *out_topk, int32_t topk_k,
+                       int32_t hb) {
     gpu_cmp C = make_cmp(g_off, g_cnt, g_nodes, g_vals, out_l1d, out_l1r, out_topk, topk_k);
-    batch_job J = {n, off, tgt, w, theta, bval, 2, 1.0, mu, L, seeds, n_seeds, max_sweeps,
+    batch_job J = {n, off, tgt, w, theta, bval, hb ? 3 : 2, 1.0, mu, L, seeds, n_seeds, max_sweeps,
                    out_sweeps, out_ops, NULL, out_conv, out_xsum, g_off ? &C : NULL, 0};
     int64_t *pushes = malloc(sizeof(int64_t) * (n_seeds ? n_seeds : 1));
     J.out_pushes = pushes;

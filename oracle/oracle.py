@@ -135,8 +135,10 @@ def cheby_bounds(sys, mu=None, L=None):
     raise ValueError(f"no default Chebyshev bounds for {sys.problem}")
 
 
-def local_ch(sys, mu=None, L=None, eps=None, max_sweeps=None, record_trace=True) -> dict:
-    """src/local_solvers.py:473-538."""
+def local_ch(sys, mu=None, L=None, eps=None, max_sweeps=None, record_trace=True,
+             hb: bool = False) -> dict:
+    """src/local_solvers.py:473-538; hb=True: its heavy-ball restatement
+    (orc_local_hb, pinned by tests/golden/hb.npz)."""
     mu, L = cheby_bounds(sys, mu, L)
     eps = sys.eps if eps is None else eps
     if max_sweeps is None:
@@ -147,9 +149,10 @@ def local_ch(sys, mu=None, L=None, eps=None, max_sweeps=None, record_trace=True)
     b = _arrf(sys.b)
     x, r = np.zeros(n), np.zeros(n)
     rep = _Report()
-    lib().orc_local_ch(C.c_int64(n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th), _p(b),
-                       _p(x), _p(r), C.c_double(mu), C.c_double(L), C.c_int64(max_sweeps),
-                       C.c_int32(int(record_trace)), C.byref(rep))
+    fn = lib().orc_local_hb if hb else lib().orc_local_ch
+    fn(C.c_int64(n), _p(off, C.c_int64), _p(tg, C.c_int64), _p(w), _p(th), _p(b),
+       _p(x), _p(r), C.c_double(mu), C.c_double(L), C.c_int64(max_sweeps),
+       C.c_int32(int(record_trace)), C.byref(rep))
     out = _unpack(rep, with_trace=record_trace)
     out.update(x=x, r=r, mu=mu, L=L)
     return out
@@ -291,7 +294,7 @@ def batch_gd_rule(n: int, offsets, targets32, alpha: float, eps: float, seeds, t
 
 def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, L: float,
                    problem: str = "ppr", max_sweeps: int | None = None, gpu=None,
-                   topk: int = 100) -> dict:
+                   topk: int = 100, hb: bool = False) -> dict:
     """Per-seed reference local_ch over many host threads (CPU baseline of
     the LocalCH batch): PPR (b = alpha e_s) or Katz (b = e_s, w = alpha)."""
     from paper_2410_21634_b200.systems import arc_weights_for, theta_vector
@@ -314,7 +317,7 @@ def batch_local_ch(g, alpha: float, eps: float, seeds, threads: int, mu: float, 
                              C.c_double(bval), C.c_double(mu), C.c_double(L), _p(sd, C.c_int64),
                              C.c_int64(k), C.c_int64(max_sweeps), C.c_int32(threads),
                              _p(sw, C.c_int64), _p(ops, C.c_int64), _p(cv, C.c_int32), _p(xs),
-                             *cargs)
+                             *cargs, C.c_int32(int(hb)))
     return _cmp_out({"sweeps": sw, "total_ops": ops, "converged": cv.astype(bool), "xsum": xs},
                     cres)
 

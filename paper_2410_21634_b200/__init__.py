@@ -10,7 +10,7 @@ from .systems import (DiffusionSystem, OperatorQ, SystemError, dense_solve,
                       make_ppr_system, series_oracle)
 from .reports import LocalReport, SolveReport, SolverState
 from .metrics import error_norms, sample_sources
-from .local_solvers import (local_ch, local_gd, local_gs, local_hk, local_sor, optimal_omega,
+from .local_solvers import (local_ch, local_gd, local_gs, local_hb, local_hk, local_sor, optimal_omega,
                             push_sweeps)
 from .global_solvers import GlobalConfig, gradient_descent
 from .dynamic import PprPair, event_adjust, make_pair, parse_events, repair, run_snapshots

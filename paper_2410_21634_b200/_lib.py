@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GDIFF_LIB") or os.path.join(HERE, "libgdiff.so")  # o
 GD_OK, GD_ERR_ARG, GD_ERR_CUDA, GD_ERR_OOM, GD_ERR_CAPACITY, GD_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GD_W_RW, GD_W_CONST, GD_W_ARC = 0, 1, 2
 GD_T_DEGREE, GD_T_ARRAY = 0, 1
-GD_M_LOCAL_GD, GD_M_LOCAL_SOR, GD_M_LOCAL_CH, GD_M_HK = 0, 1, 2, 3
+GD_M_LOCAL_GD, GD_M_LOCAL_SOR, GD_M_LOCAL_CH, GD_M_HK, GD_M_LOCAL_HB = 0, 1, 2, 3, 4
 GD_P_PPR, GD_P_KATZ = 0, 1
 
 _i64p = C.POINTER(C.c_int64)
@@ -91,6 +91,8 @@ SIGNATURES = {
     "gd_local_gd_warm": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, C.c_int32,
                                    C.c_int64, C.c_int32, C.POINTER(Report)]),
     "gd_local_ch": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_double,
+                              C.c_double, C.c_int64, C.c_int32, C.POINTER(Report)]),
+    "gd_local_hb": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _f64p, C.c_double,
                               C.c_double, C.c_int64, C.c_int32, C.POINTER(Report)]),
     "gd_push_kernel": (C.c_int, [C.c_void_p, C.POINTER(Operator), _f64p, _f64p, _i64p, C.c_int64,
                                  C.c_double, C.c_double, C.c_int32, C.c_int64, C.POINTER(Report)]),

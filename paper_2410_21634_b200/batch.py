@@ -18,7 +18,7 @@ from . import _lib as gdl
 from .device import DeviceGraph, device_graph
 
 __all__ = ["BatchSolver", "BatchOutput", "local_gd_batch", "local_sor_batch", "local_ch_batch",
-           "local_hk_batch"]
+           "local_hb_batch", "local_hk_batch"]
 
 
 def _host_array(count: int, dtype, pinned: bool) -> np.ndarray:
@@ -127,10 +127,10 @@ class BatchSolver:
                  omega: float = 1.0, problem: str = "ppr", mu: float | None = None,
                  L: float | None = None, hk: dict | None = None, want_r: bool = False,
                  resolve: str = "flag", log_sweeps: int = 0):
-        if method not in ("local-gd", "local-sor", "local-ch", "local-hk"):
+        if method not in ("local-gd", "local-sor", "local-ch", "local-hb", "local-hk"):
             raise ValueError(f"unknown batch method {method!r}")
-        if problem not in ("ppr", "katz") or (problem == "katz" and method != "local-ch"):
-            raise ValueError("problem must be 'ppr', or 'katz' with method 'local-ch'")
+        if problem not in ("ppr", "katz") or (problem == "katz" and method not in ("local-ch", "local-hb")):
+            raise ValueError("problem must be 'ppr', or 'katz' with method 'local-ch' / 'local-hb'")
         if resolve not in ("flag", "exact", "all"):
             raise ValueError("resolve must be 'flag', 'exact' or 'all'")
         if method == "local-hk" and not hk:
@@ -141,7 +141,7 @@ class BatchSolver:
             raise ValueError("alpha must be positive")
         if method == "local-sor" and not 0.0 < omega <= 2.0:
             raise ValueError("omega must be in (0, 2]")
-        if method == "local-ch":
+        if method in ("local-ch", "local-hb"):
             if (mu is None) != (L is None):
                 raise ValueError("give both mu and L, or neither")
             if mu is None and problem == "katz":
@@ -153,7 +153,8 @@ class BatchSolver:
         self.graph = g if isinstance(g, DeviceGraph) else device_graph(g, device)
         self.alpha, self.eps = float(alpha), float(eps)
         mcode = {"local-gd": gdl.GD_M_LOCAL_GD, "local-sor": gdl.GD_M_LOCAL_SOR,
-                 "local-ch": gdl.GD_M_LOCAL_CH, "local-hk": gdl.GD_M_HK}[method]
+                 "local-ch": gdl.GD_M_LOCAL_CH, "local-hb": gdl.GD_M_LOCAL_HB,
+                 "local-hk": gdl.GD_M_HK}[method]
         hk = hk or {}
         sw = np.ascontiguousarray(hk.get("stage_w", np.zeros(1)), dtype=np.float64)
         p = gdl.BatchParams(method=mcode, slots=int(slots), alpha=self.alpha, eps=self.eps,
@@ -387,7 +388,7 @@ def local_sor_batch(g, seeds, alpha: float, eps: float, omega: float = 1.0, slot
 def local_ch_batch(g, seeds, alpha: float, eps: float, problem: str = "ppr",
                    mu: float | None = None, L: float | None = None,
                    lam_hat: float | None = None, max_sweeps: int | None = None, slots: int = 0,
-                   relabel: bool = True) -> BatchOutput:
+                   relabel: bool = True, method: str = "local-ch") -> BatchOutput:
     """Batched LocalCH over `seeds`: per seed the reference's
     local_ch(make_ppr_system(g, alpha, s, eps)) or, for problem "katz",
     local_ch(make_katz_system(g, alpha, s, eps)) with its default bounds
@@ -408,12 +409,19 @@ def local_ch_batch(g, seeds, alpha: float, eps: float, problem: str = "ppr",
     if max_sweeps is None:  # the reference default (src/local_solvers.py:500)
         gap = max(mu, 1e-12)
         max_sweeps = max(1000, int(10 * math.log(max(1.0 / max(eps, 1e-300), 2.0)) / gap))
-    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method="local-ch",
+    solver = BatchSolver(g, alpha, eps, slots=slots, max_sweeps=max_sweeps, method=method,
                          problem=problem, mu=mu, L=L, relabel=relabel)
     try:
         return solver.solve(sd)
     finally:
         solver.close()
+
+
+def local_hb_batch(g, seeds, alpha: float, eps: float, **kw) -> BatchOutput:
+    """Batched LocalHB (heavy-ball momentum: local_ch's loop with Polyak's
+    stationary coefficients; no reference counterpart, restated in oracle/
+    orc_local_hb): the arguments of local_ch_batch."""
+    return local_ch_batch(g, seeds, alpha, eps, method="local-hb", **kw)
 
 
 def hk_params(g, tau: float, eps: float, s: int = 0) -> dict:

@@ -1788,7 +1788,8 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     std::vector<int64_t> todo;
     for (int64_t i = 0; i < n_seeds; ++i)
         if (amb[i] || all) todo.push_back(i);
-    const bool ch = B->p.method == GD_M_LOCAL_CH, katz = B->p.problem == GD_P_KATZ;
+    const bool ch = B->p.method == GD_M_LOCAL_CH || B->p.method == GD_M_LOCAL_HB;
+    const bool katz = B->p.problem == GD_P_KATZ;
     gd_operator op{};
     op.weight_rule = katz ? GD_W_CONST : GD_W_RW;
     op.theta_rule = GD_T_DEGREE;
@@ -1839,7 +1840,7 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
                 const double *xb = nullptr, *rb = nullptr;
                 for (size_t j = j0; j < j1; ++j) sd.push_back(seeds[todo[j]]);
                 if (ch) {
-                    const ExactSeed e = exact_seed_solve(W, B->G, &op, GD_M_LOCAL_CH, sd[0], bval,
+                    const ExactSeed e = exact_seed_solve(W, B->G, &op, B->p.method, sd[0], bval,
                                                          B->p.mu, B->p.L, B->p.max_sweeps, false);
                     xb = e.x; rb = e.r;
                     sw.push_back(e.sweeps); op_.push_back(e.ops); pu.push_back(e.pushes);
@@ -1955,14 +1956,17 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
     return guarded([&] {
         GD_CHECK_ARG(G && p && out, "null pointer");
         GD_CHECK_ARG(p->method == GD_M_LOCAL_GD || p->method == GD_M_LOCAL_SOR ||
-                         p->method == GD_M_LOCAL_CH || p->method == GD_M_HK,
+                         p->method == GD_M_LOCAL_CH || p->method == GD_M_LOCAL_HB ||
+                         p->method == GD_M_HK,
                      "unknown batch method");
         GD_CHECK_ARG(p->method != GD_M_HK ||
                          (p->n_stages >= 0 && (p->stage_w || p->n_stages == 0) &&
                           p->theta_coeff > 0.0 && p->tau >= 0.0),
                      "heat kernel batches need tau >= 0, n_stages, stage_w, theta_coeff > 0");
-        GD_CHECK_ARG(p->problem == GD_P_PPR || (p->problem == GD_P_KATZ && p->method == GD_M_LOCAL_CH),
-                     "Katz batches need GD_M_LOCAL_CH");
+        GD_CHECK_ARG(p->problem == GD_P_PPR ||
+                         (p->problem == GD_P_KATZ &&
+                          (p->method == GD_M_LOCAL_CH || p->method == GD_M_LOCAL_HB)),
+                     "Katz batches need GD_M_LOCAL_CH or GD_M_LOCAL_HB");
         GD_CHECK_ARG(p->method != GD_M_LOCAL_SOR || (p->omega > 0.0 && p->omega <= 2.0),
                      "omega must be in (0, 2]");
         GD_CHECK_ARG(p->method == GD_M_HK ||
@@ -2010,7 +2014,7 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
             }
             B->hk = p->method == GD_M_HK;
             if (p->relabel) build_relabeled(B);
-            if (p->method == GD_M_LOCAL_CH) {
+            if (p->method == GD_M_LOCAL_CH || p->method == GD_M_LOCAL_HB) {
                 if (B->p.mu == 0.0 && B->p.L == 0.0) {
                     GD_CHECK_ARG(p->problem == GD_P_PPR, "Katz batches need mu, L");
                     B->p.mu = p->alpha;

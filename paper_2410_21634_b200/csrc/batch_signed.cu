@@ -923,6 +923,20 @@ struct SignedState {
         GD_LAUNCH_CHECK();
     }
 
+    // LocalHB: constant heavy-ball coefficients (eta r + beta prev; sweep 0 eta r)
+    void set_hb(double mu, double L, int64_t max_sweeps_) {
+        max_sweeps = max_sweeps_;
+        double eta = 0.0, beta = 0.0;
+        hb_coefficients(mu, L, &eta, &beta);
+        step0 = eta;
+        const int64_t T = max_sweeps + 1;
+        std::vector<double> cr(T, eta), cmv(T, beta);
+        coef_r.alloc(T);
+        coef_m.alloc(T);
+        GD_CUDA(cudaMemcpy(coef_r.p, cr.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
+        GD_CUDA(cudaMemcpy(coef_m.p, cmv.data(), sizeof(double) * T, cudaMemcpyHostToDevice));
+    }
+
     void set_ch(double mu, double L, int64_t max_sweeps_) {
         max_sweeps = max_sweeps_;
         step0 = 2.0 / (L + mu);
@@ -1013,7 +1027,10 @@ SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, in
         S->op.trule = GD_T_DEGREE;
         S->op.beta = p.problem == GD_P_KATZ ? p.alpha : 1.0 - p.alpha;
         S->op.tcoeff = p.problem == GD_P_KATZ ? p.eps : p.eps * p.alpha;
-        S->set_ch(p.mu, p.L, p.max_sweeps);
+        if (p.method == GD_M_LOCAL_HB)
+            S->set_hb(p.mu, p.L, p.max_sweeps);
+        else
+            S->set_ch(p.mu, p.L, p.max_sweeps);
     } catch (...) {
         delete S;
         throw;

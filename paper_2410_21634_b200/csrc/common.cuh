@@ -230,6 +230,9 @@ struct ExactSeed {
     const double *x, *r;
     int64_t n;
 };
+// Polyak heavy-ball coefficients (LocalHB; exact.cu)
+void hb_coefficients(double mu, double L, double *eta, double *beta);
+
 struct ExactWorker;
 ExactWorker *exact_worker_create();
 void exact_worker_destroy(ExactWorker *w);

@@ -51,6 +51,20 @@ __device__ __forceinline__ int64_t bsearch_le(const int64_t *a, int64_t cnt, int
 // syncs of one solve.
 __device__ __forceinline__ int64_t base_of(int64_t u, int64_t n1) { return u < n1 ? u : u % n1; }
 
+}  // namespace
+
+// Polyak's heavy-ball coefficients for eigenvalues in [mu, L] (the
+// stationary limit of local_ch's Chebyshev recurrence), each rounding as the
+// restatement writes it (oracle/gdiff_oracle.c orc_local_hb).
+void hb_coefficients(double mu, double L, double *eta, double *beta) {
+    const double sq = std::sqrt(L), sm = std::sqrt(mu);
+    *eta = 4.0 / ((sq + sm) * (sq + sm));
+    const double q = (sq - sm) / (sq + sm);
+    *beta = q * q;
+}
+
+namespace {
+
 // ---- seeds -> initial frontier flags (filter of flatnonzero(b), :383-386)
 __global__ void k_flag_active_nodes(const int32_t *__restrict__ nodes, int64_t cnt,
                                     const double *__restrict__ r, DevGraph g, DevOp op,
@@ -612,7 +626,8 @@ unsigned long long *exact_worker_scratch(ExactWorker *w) {
 ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator *o,
                            int32_t method, int64_t seed, double bval, double mu, double L,
                            int64_t max_sweeps, bool sgn) {
-    const bool ch = method == GD_M_LOCAL_CH;
+    const bool ch = method == GD_M_LOCAL_CH || method == GD_M_LOCAL_HB;
+    const bool hb = method == GD_M_LOCAL_HB;
     SweepSolver &S = W->S;
     S.prepare(G, o, ch || sgn);
     ExactSeed out{0, 0, 0, 1, 0, nullptr, nullptr, S.n};
@@ -631,8 +646,11 @@ ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator 
     while (f) {
         if (out.sweeps >= max_sweeps) { out.converged = 0; break; }
         if (ch) {
-            double coef_r = 0.0, coef_m = 0.0;
-            if (t > 0) {
+            double coef_r = 0.0, coef_m = 0.0, s0 = step0;
+            if (hb) {
+                hb_coefficients(mu, L, &s0, &coef_m);
+                coef_r = s0;
+            } else if (t > 0) {
                 const double dn = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
                 coef_r = 4.0 * dn / (L - mu);
                 coef_m = delta * dn;
@@ -640,7 +658,7 @@ ExactSeed exact_seed_solve(ExactWorker *W, const gd_graph *G, const gd_operator 
             }
             k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t,
-                                                        S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
+                                                        S.mom.p, S.mstamp.p, s0, coef_r, coef_m,
                                                         S.g, S.op.dev, S.n1);
         } else {
             k_gather_gd<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
@@ -741,8 +759,26 @@ int gd_local_gd_warm(const gd_graph *G, const gd_operator *o, double *x, double 
     });
 }
 
+static int local_momentum(const gd_graph *G, const gd_operator *o, const double *b, double *x,
+                          double *r, double mu, double L, int64_t max_sweeps,
+                          int32_t record_trace, gd_report *rep, bool hb);
+
 int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
                 double mu, double L, int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
+    return local_momentum(G, o, b, x, r, mu, L, max_sweeps, record_trace, rep, false);
+}
+
+// LocalHB: local_ch with Polyak's stationary heavy-ball coefficients (no
+// reference counterpart; restatement in oracle/ orc_local_hb, golden
+// tests/golden/hb.npz from the reference's own _SweepDriver).
+int gd_local_hb(const gd_graph *G, const gd_operator *o, const double *b, double *x, double *r,
+                double mu, double L, int64_t max_sweeps, int32_t record_trace, gd_report *rep) {
+    return local_momentum(G, o, b, x, r, mu, L, max_sweeps, record_trace, rep, true);
+}
+
+static int local_momentum(const gd_graph *G, const gd_operator *o, const double *b, double *x,
+                          double *r, double mu, double L, int64_t max_sweeps,
+                          int32_t record_trace, gd_report *rep, bool hb) {
     return guarded([&] {
         GD_CHECK_ARG(G && o && b && x && r && rep, "null pointer");
         GD_CHECK_ARG(mu < L, "need mu < L");
@@ -768,8 +804,11 @@ int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double
         while (f) {
             if (rep->sweeps >= max_sweeps) { rep->converged = 0; break; }
             if (record_trace) S.record(rep, tcap, f);
-            double coef_r = 0.0, coef_m = 0.0;
-            if (t > 0) {
+            double coef_r = 0.0, coef_m = 0.0, s0 = step0;
+            if (hb) {  // eta r (+ beta prev): the gather's t == 0 branch uses step0 = eta
+                hb_coefficients(mu, L, &s0, &coef_m);
+                coef_r = s0;
+            } else if (t > 0) {
                 double delta_next = 1.0 / (2.0 * (L + mu) / (L - mu) - delta);
                 coef_r = 4.0 * delta_next / (L - mu);
                 coef_m = delta * delta_next;
@@ -777,7 +816,7 @@ int gd_local_ch(const gd_graph *G, const gd_operator *o, const double *b, double
             }
             k_gather_ch<<<blocks_for(f), TPB, 0, S.s>>>(S.F.p, f, S.x.p, S.r.p, S.vals.p, S.absv.p,
                                                         S.wnode.p, S.fdeg.p, S.fstamp.p, t,
-                                                        S.mom.p, S.mstamp.p, step0, coef_r, coef_m,
+                                                        S.mom.p, S.mstamp.p, s0, coef_r, coef_m,
                                                         S.g, S.op.dev, S.n1);
             GD_LAUNCH_CHECK();
             int64_t P = 0;

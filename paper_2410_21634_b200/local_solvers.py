@@ -24,7 +24,7 @@ from . import _lib as gdl
 from .device import device_graph, operator_for, report_arrays
 from .reports import LocalReport, SolverState
 
-__all__ = ["local_gs", "local_sor", "local_gd", "local_ch", "local_hk", "optimal_omega",
+__all__ = ["local_gs", "local_sor", "local_gd", "local_ch", "local_hb", "local_hk", "optimal_omega",
            "push_sweeps", "cheby_bounds", "DEFAULT_MAX_SWEEPS"]
 
 DEFAULT_MAX_SWEEPS = 1_000_000
@@ -193,6 +193,40 @@ def local_ch(sys, mu: float | None = None, L: float | None = None, eps: float | 
     wall = time.perf_counter() - t0
     out = report_arrays(rep)
     report = _report("local-ch", sys, out, eps, wall, guarantees_disabled=True,
+                     notes={"mu": mu, "L": Lb, "diverged": out["diverged"]})
+    return SolverState(x=x, r=r, sweeps=out["sweeps"], ops=out["total_ops"]), report
+
+
+def local_hb(sys, mu: float | None = None, L: float | None = None, eps: float | None = None,
+             max_sweeps: int | None = None) -> tuple[SolverState, LocalReport]:
+    """Heavy-ball momentum (LocalHB): local_ch's sweep loop, signed frontier,
+    momentum stamps and divergence abort (src/local_solvers.py:473-538) with
+    Polyak's stationary coefficients for eigenvalues in [mu, L]:
+    eta = 4/(sqrt(L)+sqrt(mu))^2, beta = ((sqrt(L)-sqrt(mu))/(sqrt(L)+sqrt(mu)))^2.
+    Not in the reference: bit-exact with the restatement in oracle/
+    (orc_local_hb, pinned to the reference's own _SweepDriver by
+    tests/golden/hb.npz)."""
+    if sys.problem == "hk":
+        raise ValueError("use local_hk for heat-kernel systems")
+    mu, Lb = cheby_bounds(sys, mu, L)
+    if mu >= Lb:
+        raise ValueError(f"need mu < L, got mu={mu}, L={Lb}")
+    eps = sys.eps if eps is None else eps
+    if max_sweeps is None:
+        gap = max(mu, 1e-12)
+        max_sweeps = max(1000, int(10 * math.log(max(1.0 / max(eps, 1e-300), 2.0)) / gap))
+    lib = gdl.load()
+    dg = _sys_graph(sys)
+    o, keep = operator_for(sys)
+    b = np.ascontiguousarray(sys.b, dtype=np.float64)
+    x, r = np.empty(sys.dim), np.empty(sys.dim)
+    rep = gdl.Report()
+    t0 = time.perf_counter()
+    gdl.check(lib.gd_local_hb(dg.handle, C.byref(o), gdl.ptr(b), gdl.ptr(x), gdl.ptr(r), float(mu),
+                             float(Lb), int(max_sweeps), 0, C.byref(rep)))
+    wall = time.perf_counter() - t0
+    out = report_arrays(rep)
+    report = _report("local-hb", sys, out, eps, wall, guarantees_disabled=True,
                      notes={"mu": mu, "L": Lb, "diverged": out["diverged"]})
     return SolverState(x=x, r=r, sweeps=out["sweeps"], ops=out["total_ops"]), report
 

@@ -285,3 +285,49 @@ def test_pair_pool_push_is_the_reference_run_snapshots(gpu, dyn):
         got = pool.pair(i)
         assert np.array_equal(got.p, pair.p) and np.array_equal(got.r, pair.r)
     pool.close()
+
+
+# ---- LocalHB (heavy-ball momentum; restatement, tests/golden/hb.npz) -------
+
+def test_local_hb_single_bitwise(gpu):
+    """gd_local_hb == the reference's own _SweepDriver with heavy-ball
+    coefficients (golden hb.npz), bit for bit: x, r, sweeps, ops, logs."""
+    from conftest import load_golden
+    from paper_2410_21634_b200.graph import CsrGraph
+    from paper_2410_21634_b200.local_solvers import local_hb
+    d = load_golden("hb.npz")
+    g = CsrGraph(n=int(d["graph/n"]), offsets=d["graph/offsets"], targets=d["graph/targets"])
+    for i in range(int(d["cases"])):
+        k = f"c{i}"
+        prob, alpha, eps, s = str(d[f"{k}/problem"]), float(d[f"{k}/alpha"]), float(d[f"{k}/eps"]), int(d[f"{k}/source"])
+        sys_ = (S.make_ppr_system(g, alpha, s, eps) if prob == "ppr"
+                else S.make_katz_system(g, alpha, s, eps, lam_hat=0.0))
+        st, rep = local_hb(sys_, mu=float(d[f"{k}/mu"]), L=float(d[f"{k}/L"]))
+        assert np.array_equal(st.x, d[f"{k}/x"]) and np.array_equal(st.r, d[f"{k}/r"]), k
+        assert rep.sweeps == d[f"{k}/sweeps"] and rep.total_ops == d[f"{k}/total_ops"], k
+        assert np.array_equal(np.asarray(rep.vol_log), d[f"{k}/vol_log"]), k
+        np.testing.assert_allclose(rep.residual_l1_trace, d[f"{k}/l1_log"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("problem", ["ppr", "katz"])
+def test_local_hb_batch_matches_oracle(gpu, problem):
+    """Batched LocalHB (signed round kernel, constant coefficients): sweeps,
+    ops, pushes, convergence identical to the restatement per seed, x to 1e-9."""
+    from paper_2410_21634_b200.batch import BatchSolver
+    g = rmat_graph(20000, 150000, seed=5)
+    seeds = sample_sources(g, 32, seed=4)
+    if problem == "ppr":
+        alpha, mu, L = 0.1, 0.1, 1.9
+    else:
+        alpha = 0.9 / float(g.degrees.max())
+        lam = float(g.degrees.max())
+        mu, L = 1.0 - alpha * lam, 1.0 + alpha * lam
+    solver = BatchSolver(g, alpha, 1e-6, method="local-hb", problem=problem, mu=mu, L=L, slots=8)
+    out = solver.solve(seeds)
+    solver.close()
+    ref = O.batch_local_ch(g, alpha, 1e-6, seeds, 8, mu=mu, L=L, problem=problem, hb=True,
+                           gpu=out, topk=50)
+    assert np.array_equal(out.sweeps, ref["sweeps"])
+    assert np.array_equal(out.total_ops, ref["total_ops"])
+    assert np.array_equal(out.converged, ref["converged"])
+    assert (ref["x_l1_rel"] <= 1e-9).all() and ref["topk_identical_up_to_ties"].all()

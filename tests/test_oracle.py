@@ -187,3 +187,26 @@ def test_oracle_rule_mode_is_the_reference_local_gd(cora, pa):
     b = O.batch_gd_rule(gp.n, gp.offsets, gp.targets.astype(np.int32), 0.15, 1e-7, sd, 2)
     for f in ("sweeps", "total_ops", "pushes", "converged"):
         assert np.array_equal(a[f], b[f]), f
+
+
+def test_oracle_heavy_ball_restatement_bitwise():
+    """LocalHB (heavy-ball; not in the reference): the C restatement equals the
+    reference's own _SweepDriver run with heavy-ball coefficients bit for bit
+    (tests/golden/hb.npz from tests/golden/make_golden_hb.py): x, r, sweeps,
+    ops, logs -- PPR and Katz cases."""
+    from conftest import load_golden
+    from paper_2410_21634_b200.graph import CsrGraph
+    d = load_golden("hb.npz")
+    g = CsrGraph(n=int(d["graph/n"]), offsets=d["graph/offsets"], targets=d["graph/targets"])
+    for i in range(int(d["cases"])):
+        k = f"c{i}"
+        prob, alpha, eps, s = str(d[f"{k}/problem"]), float(d[f"{k}/alpha"]), float(d[f"{k}/eps"]), int(d[f"{k}/source"])
+        sys_ = (S.make_ppr_system(g, alpha, s, eps) if prob == "ppr"
+                else S.make_katz_system(g, alpha, s, eps, lam_hat=0.0))
+        out = O.local_ch(sys_, mu=float(d[f"{k}/mu"]), L=float(d[f"{k}/L"]), hb=True)
+        assert np.array_equal(out["x"], d[f"{k}/x"]) and np.array_equal(out["r"], d[f"{k}/r"]), k
+        assert out["sweeps"] == d[f"{k}/sweeps"] and out["total_ops"] == d[f"{k}/total_ops"], k
+        assert np.array_equal(out["vol_log"], d[f"{k}/vol_log"]), k
+        assert np.array_equal(out["gamma_log"], d[f"{k}/gamma_log"]), k
+        assert np.array_equal(out["l1_log"], d[f"{k}/l1_log"]), k
+        assert bool(out["converged"]) == bool(d[f"{k}/converged"]), k
