@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--graph-seed", type=int, default=0)
     p.add_argument("--no-relabel", action="store_true", help="run on the caller's node order")
     p.add_argument("--method", default="local-gd",
-                   choices=["local-gd", "local-sor", "local-ch", "local-hk"])
+                   choices=["local-gd", "local-sor", "local-ch", "local-hb", "local-hk"])
     p.add_argument("--tau", type=float, default=10.0, help="local-hk: heat-kernel time")
     p.add_argument("--omega", type=float, default=1.0, help="local-sor relaxation")
     p.add_argument("--problem", default="ppr", choices=["ppr", "katz"],
@@ -181,9 +181,10 @@ def cpu_reference(hg, alpha, eps, seeds, threads, method="local-gd", omega=1.0, 
         out = O.batch_local_hk(hg, ch["tau"], eps, seeds, th, gpu=gpu)
         out["pushes"] = np.zeros_like(out["total_ops"])
         out["threads"] = th
-    elif method == "local-ch":
+    elif method in ("local-ch", "local-hb"):
         out = O.batch_local_ch(hg, alpha, eps, seeds, threads, ch["mu"], ch["L"],
-                               problem=ch["problem"], max_sweeps=ch["max_sweeps"], gpu=gpu)
+                               problem=ch["problem"], max_sweeps=ch["max_sweeps"], gpu=gpu,
+                               hb=method == "local-hb")
         out["pushes"] = np.zeros_like(out["total_ops"])
     else:
         out = O.batch_local_gd(hg, alpha, eps, seeds, threads=threads, arc_w=hg.arc_w,
@@ -259,7 +260,7 @@ def run_reference(args):
     n, m = SHAPES[args.shape]
     if torch.cuda.is_available():  # input synthesis only (torch ops); the timed path is CPU
         _, row, col, row_h = make_graph(args.shape, args.graph_seed, local, native=False)
-        args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
+        args.ch = ch_params(args, row, col, n) if args.method in ("local-ch", "local-hb") else None
         hg = host_graph_full(n, row_h, col, args.alpha, args.eps)
         if args.method == "local-hk":
             args.ch = {k: v for k, v in hk_config(args, hg).items() if k != "stage_w"}
@@ -274,7 +275,7 @@ def run_reference(args):
         hg.theta = theta_vector(hg, args.eps * args.alpha)
         hg.d_max = int(hg.degrees.max()) if n else 0
         args.ch = (ch_params(args, torch.as_tensor(g.offsets), torch.as_tensor(g.targets), n)
-                   if args.method == "local-ch" else None)
+                   if args.method in ("local-ch", "local-hb") else None)
         if args.method == "local-hk":
             args.ch = {k: v for k, v in hk_config(args, hg).items() if k != "stage_w"}
     steps_total = args.steps + args.warmup
@@ -319,9 +320,9 @@ def run_reference(args):
 
 
 def workload_config(args, n, m):
-    name = {"local-gd": "LocalGD", "local-ch": "LocalCH", "local-hk": "push",
+    name = {"local-gd": "LocalGD", "local-ch": "LocalCH", "local-hb": "LocalHB", "local-hk": "push",
             "local-sor": f"LocalSOR(omega={args.omega:g})"}[args.method]
-    prob = ("Katz" if args.method == "local-ch" and args.problem == "katz" else
+    prob = ("Katz" if args.method in ("local-ch", "local-hb") and args.problem == "katz" else
             "heat-kernel" if args.method == "local-hk" else "PPR")
     par = f"tau={args.tau:g}" if args.method == "local-hk" else f"alpha={args.alpha:.6g}"
     return {"workload": f"batched {name}-{prob} {par} eps={args.eps:g}, "
@@ -352,7 +353,7 @@ def main():
     n, m = SHAPES[args.shape]
     dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
     hdeg = _HostGraph(n, row_h)
-    args.ch = ch_params(args, row, col, n) if args.method == "local-ch" else None
+    args.ch = ch_params(args, row, col, n) if args.method in ("local-ch", "local-hb") else None
     hkp = None
     if args.method == "local-hk":
         hkp = hk_config(args, hdeg)
@@ -426,7 +427,7 @@ def main():
     # the guaranteed-parity policy on the timed batch with the most flagged
     # seeds (outside the timed region): those re-solved on the bit-exact path
     exact_probe = None
-    if args.method in ("local-gd", "local-ch") and solver.mode != "fifo" and solver.mode != "fifo-win":
+    if args.method in ("local-gd", "local-ch", "local-hb") and solver.mode not in ("fifo", "fifo-win"):
         solver.set_resolve("exact")
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -475,6 +476,7 @@ def main():
     win = solver.mode == "fifo-win"  # LocalGS / unsigned SOR: exact windows, CTA per seed
     traffic, traffic_src = ncu_traffic("k_seed_cta" if cta else "k_sor_win" if win else
                                        {"local-gd": "k_rounds", "local-ch": "k_signed_rounds",
+                                        "local-hb": "k_signed_rounds",
                                         "local-hk": "k_rounds_hk",
                                         "local-sor": "k_fifo_batch"}[args.method])
     # e2e: the public host API with host buffers, copies inside the timed region
@@ -559,11 +561,13 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // (1 if cta else 4),
                                                                 "local-ch": launches // 5,
+                                                                "local-hb": launches // 5,
                                                                 "local-hk": launches // 5}.get(args.method, launches)),
                          "peak_kind": peak_kind,
                          "kernel": {"local-gd": "k_seed_cta (one CTA per seed)" if cta else
                                                     "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
+                                    "local-hb": "k_signed_rounds (heavy-ball coefficients)",
                                     "local-hk": "k_rounds<HK> (layered heat-kernel stage sweeps)",
                                     "local-sor": "k_sor_win (exact windows, CTA per seed)" if win
                                                  else "k_fifo_batch (warp per seed)"}[args.method],

@@ -60,5 +60,5 @@ def b_alg_bytes(total_ops: int, pushes: int, method: str = "local-gd") -> int:
     52 B per pushed node (frontier id, row_ptr pair, r[u] rw, x[u] rw);
     LocalCH adds 24 B per push (momentum value + stamp), FIFO solvers 8 B.
     """
-    per_push = 52 + (24 if method == "local-ch" else 0) + (8 if method in ("local-sor", "local-gs") else 0)
+    per_push = 52 + (24 if method in ("local-ch", "local-hb") else 0) + (8 if method in ("local-sor", "local-gs") else 0)
     return 20 * int(total_ops) + per_push * int(pushes)
