@@ -1454,7 +1454,12 @@ struct gd_batch {
         if (w >= 1) hs_drain(w - 1);
         if (w == waves - 1) hs_drain(w);
     }
+    cudaStream_t aux = nullptr;      // second stream of the wave transitions
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~gd_batch() {
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (aux) cudaStreamDestroy(aux);
         for (auto w : workers) exact_worker_destroy(w);
         if (hs.curh) cudaFreeHost(hs.curh);
         for (auto e : hs.wev) cudaEventDestroy(e);
@@ -1588,6 +1593,11 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             B->hs_wave(w, waves, st);
         }
     }
+    if (!B->aux && !B->stream && waves > 0) {
+        GD_CUDA(cudaStreamCreateWithFlags(&B->aux, cudaStreamNonBlocking));
+        GD_CUDA(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
+        GD_CUDA(cudaEventCreateWithFlags(&B->ev_join, cudaEventDisableTiming));
+    }
     for (int64_t w = 0; w < waves && !B->stream; ++w) {
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
@@ -1605,18 +1615,26 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
-        k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
+        // x extraction (random gathers: latency-bound) on st, the r reset
+        // (sector stores: bandwidth-bound) concurrently on a second stream;
+        // they touch disjoint data.  The next wave waits for both.
+        GD_CUDA(cudaEventRecord(B->ev_fork, st));
+        GD_CUDA(cudaStreamWaitEvent(B->aux, B->ev_fork, 0));
         if (rpp)  // the r extraction zeroes the slots' r itself
             r_extract_wave(A.secmap, A.smw, A.r, A.ld, A.m, B->R ? B->inv.p : nullptr, base,
-                           rp.scratch, rp.cursor, rp.off, rp.cnt, rp.nodes, rp.vals, rp.cap, st);
+                           rp.scratch, rp.cursor, rp.off, rp.cnt, rp.nodes, rp.vals, rp.cap,
+                           B->aux);
         else
-            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A);
+            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, B->aux>>>(A);
         if (B->hk) {  // the other residual layer
             RoundArgs A2 = A;
             A2.r = A.r2;
             A2.secmap = A.secmap2;
-            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, st>>>(A2);
+            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, B->aux>>>(A2);
         }
+        k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
+        GD_CUDA(cudaEventRecord(B->ev_join, B->aux));
+        GD_CUDA(cudaStreamWaitEvent(st, B->ev_join, 0));
         GD_LAUNCH_CHECK();
         launches += B->hk ? 5 : 4;
         B->hs_wave(w, waves, st);
@@ -1804,26 +1822,30 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
     // sync overhead paid once per chunk); LocalCH seeds one at a time (its
     // divergence abort is per seed).  Items run on up to resolve_workers
     // workers (own buffers and stream each), overlapping on the device.
-    size_t K = 1;
+    // Workers and K are bounded by free HBM (a graph copy needs ~112 B per
+    // node plus frontier-sized sort scratch); an out-of-memory failure frees
+    // the workers' buffers and retries the unfinished seeds with half the
+    // workers (then half the copies), down to one seed on one worker.
+    const size_t per_copy = 112 * (size_t)(n ? n : 1);  // solver arrays per graph copy
+    size_t fr = 0, hbm = 0;
+    GD_CUDA(cudaMemGetInfo(&fr, &hbm));
+    size_t K = 1, Tcap = (size_t)B->resolve_workers;
     if (!ch) {
-        const size_t want = (todo.size() + (size_t)B->resolve_workers - 1) / (size_t)B->resolve_workers;
+        const size_t want = (todo.size() + Tcap - 1) / Tcap;
         K = std::min<size_t>(64, std::max<size_t>(16, want));
-        size_t fr = 0, tot = 0;
-        GD_CUDA(cudaMemGetInfo(&fr, &tot));
-        const size_t per_copy = 112 * (size_t)(n ? n : 1);  // solver arrays per graph copy
-        const size_t by_mem = (fr / 2) / (per_copy * (size_t)B->resolve_workers);
+        const size_t by_mem = (fr / 2) / (per_copy * Tcap);
         K = std::min(K, std::max<size_t>(1, by_mem));
         K = std::min<size_t>(K, (size_t)((1LL << 31) - 1) / (size_t)(n ? n : 1));
         K = std::max<size_t>(1, std::min(K, todo.size()));
     }
-    const size_t items = (todo.size() + K - 1) / K;
-    const size_t T = std::min<size_t>(items, (size_t)B->resolve_workers);
-    while (B->workers.size() < T) B->workers.push_back(exact_worker_create());
+    Tcap = std::min(Tcap, std::max<size_t>(1, (fr / 2) / (per_copy * K)));
+    std::vector<char> done(todo.size(), 0), chg(todo.size(), 0);
+    std::vector<size_t> pend;
     std::atomic<size_t> next{0};
     std::mutex mu;  // output pools, cursor and per-seed records
     std::atomic<int> err{GD_OK};
     std::string errmsg;
-    std::atomic<int64_t> changed{0};
+    size_t items = 0;
     auto work = [&](size_t w) {
         try {
             GD_CUDA(cudaSetDevice(B->G->device));
@@ -1833,12 +1855,12 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
             for (;;) {
                 const size_t it = next.fetch_add(1);
                 if (it >= items || err.load() != GD_OK) break;
-                const size_t j0 = it * K, j1 = std::min(todo.size(), j0 + K);
-                // solve the item: copy c of the result = seed todo[j0 + c]
+                const size_t j0 = it * K, j1 = std::min(pend.size(), j0 + K);
+                // solve the item: copy c of the result = seed todo[pend[j0 + c]]
                 std::vector<int64_t> sd, sw, op_, pu;
                 std::vector<int32_t> cvv;
                 const double *xb = nullptr, *rb = nullptr;
-                for (size_t j = j0; j < j1; ++j) sd.push_back(seeds[todo[j]]);
+                for (size_t j = j0; j < j1; ++j) sd.push_back(seeds[todo[pend[j]]]);
                 if (ch) {
                     const ExactSeed e = exact_seed_solve(W, B->G, &op, B->p.method, sd[0], bval,
                                                          B->p.mu, B->p.L, B->p.max_sweeps, false);
@@ -1852,11 +1874,11 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
                     sw = e.sweeps; op_ = e.ops; pu = e.pushes; cvv = e.conv;
                 }
                 for (size_t c = 0; c < sd.size(); ++c) {
-                    const int64_t i = todo[j0 + c];
+                    const size_t q = pend[j0 + c];
+                    const int64_t i = todo[q];
                     const double *ex = xb + (int64_t)c * n, *er = rb + (int64_t)c * n;
-                    if (before[i] != sw[c] || before[n_seeds + i] != op_[c] ||
-                        (!ch && before[2 * n_seeds + i] != pu[c]))
-                        changed += 1;
+                    chg[q] = before[i] != sw[c] || before[n_seeds + i] != op_[c] ||
+                             (!ch && before[2 * n_seeds + i] != pu[c]);
                     unsigned long long nz[2] = {0, 0};
                     GD_CUDA(cudaMemsetAsync(cnts.p, 0, 2 * sizeof(unsigned long long), ws));
                     k_count_nz<<<nb, 256, 0, ws>>>(ex, n, cnts.p);
@@ -1906,6 +1928,7 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
                         GD_CUDA(cudaMemcpyAsync(B->rcnt.p + i, &rr[1], 8, cudaMemcpyHostToDevice, ws));
                     }
                     GD_CUDA(cudaStreamSynchronize(ws));  // (host records above go out of scope)
+                    done[q] = 1;
                 }
             }
         } catch (const Error &e) {
@@ -1916,15 +1939,35 @@ static void resolve_ambiguous(gd_batch *B, const int64_t *d_seeds, int64_t n_see
             err = GD_ERR_CUDA;
         }
     };
-    std::vector<std::thread> th;
-    for (size_t w = 1; w < T; ++w) th.emplace_back(work, w);
-    if (T) work(0);
-    for (auto &x : th) x.join();
-    if (err.load() != GD_OK) {
-        set_error("exact re-solve failed: %s", errmsg.c_str());
-        throw Error{err.load()};
+    for (;;) {
+        pend.clear();
+        for (size_t q = 0; q < todo.size(); ++q)
+            if (!done[q]) pend.push_back(q);
+        if (pend.empty()) break;
+        K = std::min(K, pend.size());
+        items = (pend.size() + K - 1) / K;
+        const size_t T = std::min(items, Tcap);
+        while (B->workers.size() < T) B->workers.push_back(exact_worker_create());
+        next = 0;
+        err = GD_OK;
+        std::vector<std::thread> th;
+        for (size_t w = 1; w < T; ++w) th.emplace_back(work, w);
+        work(0);
+        for (auto &x : th) x.join();
+        if (err.load() == GD_OK) continue;
+        if (err.load() != GD_ERR_OOM || (T == 1 && K == 1)) {
+            set_error("exact re-solve failed: %s", errmsg.c_str());
+            throw Error{err.load()};
+        }
+        for (auto w : B->workers) exact_worker_destroy(w);  // free their buffers
+        B->workers.clear();
+        cudaGetLastError();
+        if (T > 1) Tcap = T / 2;
+        else K = std::max<size_t>(1, K / 2);
     }
-    B->last_changed = changed.load();
+    int64_t changed = 0;
+    for (char c : chg) changed += c;
+    B->last_changed = changed;
     const unsigned long long tot = (unsigned long long)B->last_x_total;
     GD_CUDA(cudaMemcpy(B->cursor.p, &tot, sizeof(tot), cudaMemcpyHostToDevice));
     B->last_resolve_ms =
