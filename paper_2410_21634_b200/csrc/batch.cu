@@ -1093,36 +1093,95 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
     }
 }
 
-// grid (CHUNKS, slots): return r of every slot to +0.0 -- zero exactly the
-// 32 B sectors this slot ever wrote (sector map set on first touch) and clear
-// the map.  A warp takes 32 map words at a time and, word by word, each lane
-// stores one sector, so the stores of a word are one coalesced 1 KB run.
-__global__ void k_wave_reset(RoundArgs A) {
-    const int k = blockIdx.y;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t off = (int64_t)k * A.ld;
-    uint32_t *map = A.secmap + (int64_t)k * A.smw;
-    const int64_t per = (A.smw + gridDim.x - 1) / gridDim.x;  // gridDim.x scales with the map
-    const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
-    double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
-    for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
-        const uint32_t mine = (w0 + lane < hi) ? map[w0 + lane] : 0u;
-        unsigned any = __ballot_sync(FULL, mine != 0u);
-        while (any) {
-            const int src = __ffs(any) - 1;
-            any &= any - 1;
-            const uint32_t wb = __shfl_sync(FULL, mine, src);
-            if ((wb >> lane) & 1u) {
-                const int64_t sec = (w0 + src) * 32 + lane;  // doubles [4 sec, 4 sec + 4)
-                if (4 * sec + 3 < A.ld) {
-                    r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
-                } else {
-                    for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
+// Work-balanced form of k_wave_extract: the wave's pushed lists are treated
+// as one concatenated index space (per-slot prefix of pushed_cnt in shared
+// memory, slot found by binary search), so every thread of a full-GPU grid
+// has XB independent gathers in flight whatever the slots' sizes -- the
+// per-slot grid leaves most warps with one or two entries and the kernel
+// waits on the longest dependent chain (pushed -> x / inv -> store) per block
+// wave.  Per-seed counters: threads k < m of block 0.
+constexpr int XB = 4;
+constexpr int EXB_MAX_SLOTS = 1024;
+__global__ void __launch_bounds__(256) k_wave_extract_bal(RoundArgs A, OutArgs O, int64_t seed_base) {
+    __shared__ int64_t pre[EXB_MAX_SLOTS + 1];
+    const int m = (int)A.m;
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int k = 0; k < m; ++k) {
+            pre[k] = run;
+            run += (int64_t)A.pushed_cnt[k];
+        }
+        pre[m] = run;
+    }
+    __syncthreads();
+    const int64_t total = pre[m];
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < total; g0 += XB * nth) {
+        int32_t u[XB], id[XB];
+        int64_t at[XB], xo[XB];
+        double xv[XB];
+#pragma unroll
+        for (int j = 0; j < XB; ++j) {
+            const int64_t g = g0 + j * nth;
+            u[j] = -1;
+            if (g < total) {
+                int lo = 0, hi = m - 1;  // last k with pre[k] <= g
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (pre[mid] <= g) lo = mid; else hi = mid - 1;
                 }
+                const int64_t i = g - pre[lo];
+                xo[j] = (int64_t)lo * A.ld;
+                at[j] = A.slot_base[lo] + i;
+                u[j] = __ldg(A.pushed + (int64_t)lo * A.ld + i);
             }
         }
-        if (mine) map[w0 + lane] = 0u;
+#pragma unroll
+        for (int j = 0; j < XB; ++j) {
+            xv[j] = u[j] >= 0 ? A.x[xo[j] + u[j]] : 0.0;
+            id[j] = (u[j] >= 0 && O.inv) ? __ldg(O.inv + u[j]) : u[j];
+        }
+#pragma unroll
+        for (int j = 0; j < XB; ++j) {
+            if (u[j] < 0) continue;
+            A.x[xo[j] + u[j]] = 0.0;
+            if (at[j] < O.xcap) {
+                O.xnodes[at[j]] = id[j];
+                O.xvals[at[j]] = __dmul_rn(O.xscale, xv[j]);
+            }
+        }
     }
+    if (blockIdx.x == 0) {
+        for (int k = threadIdx.x; k < m; k += blockDim.x) {
+            const int64_t si = seed_base + k;
+            const int64_t pushes = (int64_t)A.s_pushes[k];
+            const int64_t pc = pre[k + 1] - pre[k];
+            O.sweeps[si] = (int64_t)A.s_last[k] + 1;
+            O.ops[si] = (int64_t)A.s_ops[k];
+            O.pushes[si] = pushes;
+            O.conv[si] = A.s_conv[k];
+            O.support[si] = O.hk ? -1 : (int64_t)A.touched[k] - (pushes - (int64_t)A.s_negz[k]);
+            O.xoff[si] = A.slot_base[k];
+            O.xcnt[si] = pc;
+            O.amb[si] = A.s_amb[k];
+            if (A.s_amb[k]) atomicAdd(O.amb_cnt, 1ULL);
+            if (pc == 0) A.r[(int64_t)k * A.ld + A.seed[k]] = 0.0;  // inactive seed: r = alpha
+        }
+    }
+}
+
+// grid (CHUNKS, slots): return r of every slot to +0.0 -- zero exactly the
+// 32 B sectors this slot ever wrote (sector map set on first touch) and clear
+// the map (reset_sector_words, common.cuh).
+__global__ void k_wave_reset(RoundArgs A) {
+    const int k = blockIdx.y;
+    const int64_t per = (A.smw + gridDim.x - 1) / gridDim.x;  // gridDim.x scales with the map
+    const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
+    reset_sector_words(A.secmap + (int64_t)k * A.smw, A.r + (int64_t)k * A.ld, A.ld, lo, hi);
+}
+
+static void wave_reset(const RoundArgs &A, unsigned chunks, cudaStream_t st) {
+    k_wave_reset<<<dim3(chunks, (unsigned)A.m), 256, 0, st>>>(A);
 }
 
 // (neighbour, degree) per arc, for the threshold test without a second load
@@ -1454,9 +1513,15 @@ struct gd_batch {
         if (w >= 1) hs_drain(w - 1);
         if (w == waves - 1) hs_drain(w);
     }
+    bool trace = false;              // GDIFF_WAVE_TRACE: per-wave timeline to stderr
+    bool serial = false;             // GDIFF_WAVE_SERIAL: no second stream
+    bool ext_bal = false;            // work-balanced x extraction
+    int ext_blocks = 0;
+    std::vector<cudaEvent_t> tev;
     cudaStream_t aux = nullptr;      // second stream of the wave transitions
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~gd_batch() {
+        for (auto e : tev) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (aux) cudaStreamDestroy(aux);
@@ -1593,6 +1658,22 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             B->hs_wave(w, waves, st);
         }
     }
+    B->trace = getenv("GDIFF_WAVE_TRACE") != nullptr;  // (diagnostics: per-wave timeline)
+    B->serial = getenv("GDIFF_WAVE_SERIAL") != nullptr;  // (A/B: reset after extract on st)
+    {   // GDIFF_EXTRACT_BAL=0: the per-slot extraction grid (A/B)
+        const char *e = getenv("GDIFF_EXTRACT_BAL");
+        B->ext_bal = !(e && atoi(e) == 0);
+    }
+    if (!B->ext_blocks) {
+        int per = 0;
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave_extract_bal, 256, 0));
+        B->ext_blocks = std::max(1, per) * n_sms(B->G->device);
+    }
+    while (B->trace && (int64_t)B->tev.size() < 2 * waves) {
+        cudaEvent_t e;
+        GD_CUDA(cudaEventCreate(&e));
+        B->tev.push_back(e);
+    }
     if (!B->aux && !B->stream && waves > 0) {
         GD_CUDA(cudaStreamCreateWithFlags(&B->aux, cudaStreamNonBlocking));
         GD_CUDA(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
@@ -1618,22 +1699,31 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         // x extraction (random gathers: latency-bound) on st, the r reset
         // (sector stores: bandwidth-bound) concurrently on a second stream;
         // they touch disjoint data.  The next wave waits for both.
+        const cudaStream_t tst = B->serial ? st : B->aux;
         GD_CUDA(cudaEventRecord(B->ev_fork, st));
-        GD_CUDA(cudaStreamWaitEvent(B->aux, B->ev_fork, 0));
+        GD_CUDA(cudaStreamWaitEvent(tst, B->ev_fork, 0));
         if (rpp)  // the r extraction zeroes the slots' r itself
             r_extract_wave(A.secmap, A.smw, A.r, A.ld, A.m, B->R ? B->inv.p : nullptr, base,
                            rp.scratch, rp.cursor, rp.off, rp.cnt, rp.nodes, rp.vals, rp.cap,
-                           B->aux);
+                           tst);
         else
-            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, B->aux>>>(A);
+            wave_reset(A, B->reset_chunks(), tst);
         if (B->hk) {  // the other residual layer
             RoundArgs A2 = A;
             A2.r = A.r2;
             A2.secmap = A.secmap2;
-            k_wave_reset<<<dim3(B->reset_chunks(), (unsigned)A.m), 256, 0, B->aux>>>(A2);
+            wave_reset(A2, B->reset_chunks(), tst);
         }
-        k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
-        GD_CUDA(cudaEventRecord(B->ev_join, B->aux));
+        if (B->trace && B->serial) GD_CUDA(cudaEventRecord(B->tev[2 * w + 1], st));
+        if (B->ext_bal && A.m <= EXB_MAX_SLOTS)
+            k_wave_extract_bal<<<B->ext_blocks, 256, 0, st>>>(A, O, base);
+        else
+            k_wave_extract<<<dim3(CHUNKS, (unsigned)A.m), 256, 0, st>>>(A, O, base);
+        if (B->trace) {
+            GD_CUDA(cudaEventRecord(B->tev[2 * w], st));
+            if (!B->serial) GD_CUDA(cudaEventRecord(B->tev[2 * w + 1], tst));
+        }
+        GD_CUDA(cudaEventRecord(B->ev_join, tst));
         GD_CUDA(cudaStreamWaitEvent(st, B->ev_join, 0));
         GD_LAUNCH_CHECK();
         launches += B->hk ? 5 : 4;
@@ -1648,6 +1738,17 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
     }
     B->last_ms = ms;
     B->last_launches = launches;
+    if (B->trace && !B->stream) {
+        for (int64_t w = 0; w < waves; ++w) {
+            float f = 0.f, g = 0.f, ex = 0.f, rs = 0.f;
+            GD_CUDA(cudaEventElapsedTime(&f, B->ev[2 * w], B->ev[2 * w + 1]));
+            GD_CUDA(cudaEventElapsedTime(&ex, B->ev[2 * w + 1], B->tev[2 * w]));
+            GD_CUDA(cudaEventElapsedTime(&rs, B->ev[2 * w + 1], B->tev[2 * w + 1]));
+            if (w + 1 < waves) GD_CUDA(cudaEventElapsedTime(&g, B->ev[2 * w + 1], B->ev[2 * w + 2]));
+            fprintf(stderr, "wave %lld kernel %.1f us, extract done +%.1f, reset done +%.1f, next "
+                    "wave +%.1f us\n", (long long)w, 1e3 * f, 1e3 * ex, 1e3 * rs, 1e3 * g);
+        }
+    }
 }
 
 struct RebaseOp {

@@ -707,30 +707,9 @@ __global__ void k_s_extract(SArgs A, SOut O, int64_t seed_base) {
 // warp clears one map word (1 KB of r) per step with one store per lane.
 __global__ void k_s_reset(SArgs A) {
     const int k = blockIdx.y;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t off = (int64_t)k * A.ld;
-    uint32_t *map = A.secmap + (int64_t)k * A.smw;
     const int64_t per = (A.smw + gridDim.x - 1) / gridDim.x;  // gridDim.x scales with the map
     const int64_t lo = blockIdx.x * per, hi = min(A.smw, lo + per);
-    double4 *r4 = reinterpret_cast<double4 *>(A.r + off);
-    for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
-        const uint32_t mine = (w0 + lane < hi) ? map[w0 + lane] : 0u;
-        unsigned any = __ballot_sync(SFULL, mine != 0u);
-        while (any) {
-            const int src = __ffs(any) - 1;
-            any &= any - 1;
-            const uint32_t wb = __shfl_sync(SFULL, mine, src);
-            if ((wb >> lane) & 1u) {
-                const int64_t sec = (w0 + src) * 32 + lane;
-                if (4 * sec + 3 < A.ld) {
-                    r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
-                } else {
-                    for (int64_t i = 4 * sec; i < A.ld; ++i) A.r[off + i] = 0.0;
-                }
-            }
-        }
-        if (mine) map[w0 + lane] = 0u;
-    }
+    reset_sector_words(A.secmap + (int64_t)k * A.smw, A.r + (int64_t)k * A.ld, A.ld, lo, hi);
 }
 
 // ---- resident pairs (gd_pairs) ------------------------------------------

@@ -190,6 +190,46 @@ void report_trace(gd_report *rep, int64_t &tcap, const int64_t *f, int64_t cnt);
 // 2 k u (u = 2^-53) of k <= 2^16 reordered additions into one residual.
 constexpr double AMB_REL = 1.4551915228366852e-11;  // 2^-36
 
+// Sector-map reset of one slot's residual over map words [lo, hi): every set
+// bit b of word w marks the 32 B sector of doubles [4(32w+b), 4(32w+b)+4)
+// written since the last reset; zero those sectors and clear the words.  A
+// dense word (>= 8 sectors) is stored by the whole warp, lane j taking bit j,
+// so its stores are one coalesced run; a sparse word's few sectors are stored
+// by its own lane (a warp-serial walk of sparse words would spend a warp
+// iteration per word on one or two stores).
+__device__ __forceinline__ void reset_sector_words(uint32_t *map, double *r, int64_t ld,
+                                                   int64_t lo, int64_t hi) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double4 *r4 = reinterpret_cast<double4 *>(r);
+    auto zero = [&](int64_t sec) {
+        if (4 * sec + 3 < ld) {
+            r4[sec] = make_double4(0.0, 0.0, 0.0, 0.0);
+        } else {
+            for (int64_t i = 4 * sec; i < ld; ++i) r[i] = 0.0;
+        }
+    };
+    for (int64_t w0 = lo + warp * 32; w0 < hi; w0 += nw * 32) {
+        const uint32_t mine = (w0 + lane < hi) ? map[w0 + lane] : 0u;
+        const bool dense = __popc(mine) >= 8;
+        unsigned any = __ballot_sync(0xffffffffu, dense);
+        while (any) {
+            const int src = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t wb = __shfl_sync(0xffffffffu, mine, src);
+            if ((wb >> lane) & 1u) zero((w0 + src) * 32 + lane);
+        }
+        if (!dense) {
+            uint32_t b = mine;
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                zero((w0 + lane) * 32 + j);
+            }
+        }
+        if (mine) map[w0 + lane] = 0u;
+    }
+}
+
 __device__ __forceinline__ bool near_theta(double v, double th) {
     return fabs(__dsub_rn(v, th)) <= AMB_REL * th;
 }
