@@ -1,7 +1,7 @@
 """Summarise an A/B file written by scripts/ab.sh."""
 import json, re, sys
 for l in open(sys.argv[1]):
-    m = re.match(r"(\w+) \[(.*?)\] (.*)", l)
+    m = re.match(r"(\S+) \[(.*?)\] (.*)", l)
     if not m:
         continue
     try:
