@@ -479,9 +479,9 @@ def main():
     peak, peak_kind = peaks()
     my_balg = b_alg_bytes(int(t[1]), int(t[2]), args.method)
     achieved = my_balg / (float(t[4]) / 1e3) / 1e9
-    cta = solver.mode == "cta"  # small graphs: one CTA per seed, one launch per solve
+    cta = solver.mode in ("cta", "cta-smem")  # small graphs: one CTA per seed, one launch
     win = solver.mode == "fifo-win"  # LocalGS / unsigned SOR: exact windows, CTA per seed
-    kname = ("k_seed_cta" if cta else "k_sor_win" if win else
+    kname = ("k_seed_smem" if solver.mode == "cta-smem" else "k_seed_cta" if cta else "k_sor_win" if win else
              {"local-gd": "k_rounds", "local-ch": "k_signed_rounds", "local-hb": "k_signed_rounds",
               "local-hk": "k_rounds_hk", "local-sor": "k_fifo_batch"}[args.method])
     traffic, traffic_src = ncu_traffic(kname, workload_config(args, n, m))

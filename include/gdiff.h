@@ -325,6 +325,8 @@ int gd_batch_last_kernel_ms(const gd_batch *b, double *ms);
 #define GD_BATCH_FIFO_WIN 3 /* LocalSOR/GS in exact windows, one CTA per seed */
 #define GD_BATCH_STREAM 4   /* the round kernel with slots refilled in-kernel
                                (k_rounds streaming form: LocalGD without want_r) */
+#define GD_BATCH_CTA_SMEM 5 /* GD_BATCH_CTA with each seed's whole state in shared
+                               memory (k_seed_smem: graphs of up to ~6 K nodes) */
 int gd_batch_info(const gd_batch *b, int32_t *mode, int64_t *slots);
 /* Instrumentation of the last wave: per sweep round (F entries, P arcs,
  * device globaltimer ns) as 3*min(cap, rounds) int64 values. */

@@ -216,11 +216,12 @@ class BatchSolver:
     def mode(self) -> str:
         """Execution form: "stream" (round kernel, slots refilled in-kernel:
         LocalGD without want_r), "rounds" (wave round kernel), "cta" (one CTA per
-        seed, LocalGD on small graphs), "fifo" (LocalSOR/GS, warp per seed) or
-        "fifo-win" (LocalSOR/GS in exact windows, CTA per seed)."""
+        seed, LocalGD on small graphs), "cta-smem" (the same with each seed's
+        state in shared memory, graphs of up to ~6 K nodes), "fifo" (LocalSOR/GS,
+        warp per seed) or "fifo-win" (LocalSOR/GS in exact windows, CTA per seed)."""
         m, s = C.c_int32(), C.c_int64()
         gdl.check(self.lib.gd_batch_info(self.handle, C.byref(m), C.byref(s)))
-        return ("rounds", "cta", "fifo", "fifo-win", "stream")[m.value]
+        return ("rounds", "cta", "fifo", "fifo-win", "stream", "cta-smem")[m.value]
 
     @property
     def slots(self) -> int:

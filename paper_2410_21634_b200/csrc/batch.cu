@@ -88,6 +88,7 @@ struct CtaState;  // batch_cta.cu: one CTA per seed (small graphs)
 CtaState *cta_batch_create(const gd_graph *W, int max_slots);
 void cta_batch_destroy(CtaState *S);
 int cta_batch_slots(const CtaState *S);
+bool cta_batch_smem(const CtaState *S);
 int64_t cta_slot_bytes(int64_t n, int64_t n_arcs);
 void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alpha, double eps,
                    int64_t max_sweeps, const int64_t *d_seeds, int64_t n_seeds,
@@ -2575,7 +2576,7 @@ int gd_batch_last_kernel_ms(const gd_batch *B, double *ms) {
 
 int gd_batch_info(const gd_batch *B, int32_t *mode, int64_t *slots) {
     if (!B || !mode || !slots) return GD_ERR_ARG;
-    *mode = B->cta ? GD_BATCH_CTA
+    *mode = B->cta ? (cta_batch_smem(B->cta) ? GD_BATCH_CTA_SMEM : GD_BATCH_CTA)
                    : (B->sorwin ? GD_BATCH_FIFO_WIN
                                 : (B->fifo ? GD_BATCH_FIFO
                                            : (B->stream ? GD_BATCH_STREAM : GD_BATCH_ROUNDS)));

@@ -324,6 +324,254 @@ __global__ void __launch_bounds__(CT, 2) k_seed_cta(CtaArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_seed_smem: the same per-seed sweep loop with the seed's whole state in
+// shared memory -- graphs whose x, r, frontier lists, c_u, arc offsets and
+// chunk map fit in one SM (cora-class, n up to ~6 K nodes).  Every access of
+// the sweep except the graph reads (row, (neighbour, degree) pairs, degree:
+// L1-resident at these sizes) is a shared-memory one, so a sweep's dependent
+// chain (entry -> r -> scan -> chunk map -> arc -> atomic -> append) runs at
+// shared-memory instead of L2 latency; there is nothing to reset between
+// seeds but a zero fill.  Residual updates: fp64 shared-memory atomics
+// (compare-and-swap loops; the returned old value decides the threshold
+// crossing exactly as in k_seed_cta).  Support = nonzero residuals at the end;
+// x goes out in node order.
+struct SmemView {
+    double *r, *x, *fc;
+    int32_t *front, *fa, *cmap;
+};
+__host__ __device__ inline size_t smem_seed_bytes(int64_t n, int64_t ccap) {
+    const int64_t ld = (n + 3) & ~3LL;
+    return (size_t)(8 * (2 * ld + ld) + 4 * (2 * ld + ld + ccap));
+}
+__device__ inline SmemView smem_carve(unsigned char *p, int64_t n) {
+    const int64_t ld = (n + 3) & ~3LL;
+    SmemView V;
+    V.r = reinterpret_cast<double *>(p);
+    V.x = V.r + ld;
+    V.fc = V.x + ld;
+    V.front = reinterpret_cast<int32_t *>(V.fc + ld);
+    V.fa = V.front + 2 * ld;
+    V.cmap = V.fa + ld;
+    return V;
+}
+
+__global__ void __launch_bounds__(CT, 1) k_seed_smem(CtaArgs A) {
+    using Scan = cub::BlockScan<int64_t, CT>;
+    using Red = cub::BlockReduce<unsigned long long, CT>;
+    using RedD = cub::BlockReduce<double, CT>;
+    __shared__ typename RedD::TempStorage redd_tmp;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ typename Red::TempStorage red_tmp;
+    __shared__ int s_F, s_nf, s_xc, s_rc;
+    __shared__ int64_t s_run, s_seed, s_base;
+    __shared__ int s_amb, s_nnear;
+    __shared__ int32_t s_near[NEAR_CAP];
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = CT / 32;
+    const int64_t n = A.g.n, ld = (n + 3) & ~3LL;
+    const SmemView V = smem_carve(smem_dyn, n);
+    double *const r = V.r;
+    double *const x = V.x;
+
+    for (;;) {
+        if (tid == 0) s_seed = (int64_t)atomicAdd(A.next_seed, 1ULL);
+        for (int64_t i = tid; i < ld; i += CT) {
+            r[i] = 0.0;
+            x[i] = 0.0;
+        }
+        __syncthreads();
+        const int64_t si = s_seed;
+        if (si >= A.n_seeds) return;
+        int32_t s = (int32_t)A.seeds[si];
+        if (A.perm) s = A.perm[s];
+        if (tid == 0) {
+            r[s] = A.alpha;
+            s_F = A.alpha >= theta_d(A.tcoeff, A.g.deg[s]) ? 1 : 0;
+            V.front[0] = s;
+            s_amb = 0;
+            s_nnear = 0;
+        }
+        unsigned long long my_ops = 0, my_push = 0;
+        int64_t t = 0;
+        __syncthreads();
+        for (;; ++t) {
+            {   // final values of last sweep's landings just below theta
+                const int nn = min(s_nnear, NEAR_CAP);
+                for (int i = tid; i < nn; i += CT) {
+                    const int32_t v = s_near[i];
+                    if (below_theta(r[v], theta_d(A.tcoeff, A.g.deg[v]))) s_amb = 1;
+                }
+                __syncthreads();
+                if (tid == 0) s_nnear = 0;
+            }
+            const int F = s_F;
+            if (F == 0 || t >= A.max_sweeps) break;
+            int32_t *const cur = V.front + (t & 1) * ld;
+            int32_t *const nxt = V.front + ((t & 1) ^ 1) * ld;
+            // ------------- phase A: push, arc offsets, chunk map -------------
+            if (tid == 0) {
+                s_run = 0;
+                s_nf = 0;
+            }
+            __syncthreads();
+            double my_g = 0.0;
+            for (int tile = 0; tile < F; tile += CT) {
+                const int e = tile + tid;
+                const bool live = e < F;
+                int32_t u = 0, d = 0;
+                if (live) {
+                    u = cur[e];
+                    const double val = r[u];
+                    x[u] = __dadd_rn(x[u], val);
+                    r[u] = 0.0;
+                    my_g += fabs(val);
+                    d = A.g.deg[u];
+                    if (near_theta(val, theta_d(A.tcoeff, d))) s_amb = 1;  // final r >= theta
+                    V.fc[e] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                    my_ops += (unsigned long long)d;
+                    my_push += 1ULL;
+                }
+                int64_t excl = 0, total = 0;
+                Scan(scan_tmp).ExclusiveSum((int64_t)d, excl, total);
+                const int64_t a0 = s_run + excl;
+                int64_t clo = 0, chi = 0, cfull = 0;
+                if (live) {
+                    V.fa[e] = (int32_t)a0;
+                    clo = (a0 + 31) >> 5;
+                    chi = min((a0 + d + 31) >> 5, A.ccap);
+                    cfull = (a0 + d) >> 5;
+                }
+                unsigned big = __ballot_sync(FULLM, chi - clo > 4);
+                if (!(big >> lane & 1u))
+                    for (int64_t c = clo; c < chi; ++c)
+                        V.cmap[c] = (int32_t)((uint32_t)e | (c < cfull ? 0x80000000u : 0u));
+                while (big) {
+                    const int src = __ffs(big) - 1;
+                    big &= big - 1;
+                    const int64_t lo2 = __shfl_sync(FULLM, clo, src), hi2 = __shfl_sync(FULLM, chi, src);
+                    const int64_t cf2 = __shfl_sync(FULLM, cfull, src);
+                    const uint32_t e2 = (uint32_t)__shfl_sync(FULLM, e, src);
+                    for (int64_t c = lo2 + lane; c < hi2; c += 32)
+                        V.cmap[c] = (int32_t)(e2 | (c < cf2 ? 0x80000000u : 0u));
+                }
+                __syncthreads();
+                if (tid == 0) s_run += total;
+                __syncthreads();
+            }
+            const int64_t P = s_run;
+            if (A.lg_f && t < A.lg_cap) {  // sweep log: |S_t|, vol(S_t), sum |r_u|
+                const double g = RedD(redd_tmp).Sum(my_g);
+                if (tid == 0) {
+                    A.lg_f[si * A.lg_cap + t] = F;
+                    A.lg_ops[si * A.lg_cap + t] = P;
+                    A.lg_g[si * A.lg_cap + t] = g;
+                }
+                __syncthreads();
+            }
+            // ------------- phase B: scatter 32-arc chunks ----------------------
+            const int64_t C = min((P + 31) >> 5, A.ccap);
+            const double tc = A.tcoeff;
+            for (int64_t cb = (int64_t)warp * CUNROLL; cb < C; cb += (int64_t)nwarps * CUNROLL) {
+                int32_t v[CUNROLL], dv[CUNROLL];
+                double c[CUNROLL], old[CUNROLL];
+                bool valid[CUNROLL];
+#pragma unroll
+                for (int q = 0; q < CUNROLL; ++q) {
+                    const int64_t ch = cb + q;
+                    const bool lv = ch < C;
+                    const uint32_t raw = lv ? (uint32_t)V.cmap[ch] : 0u;
+                    const int e = (int)(raw & 0x7fffffffu);
+                    const int64_t a = ch << 5;
+                    int me = e;
+                    if (!(raw >> 31)) {  // entries starting inside (a, a + 32)
+                        const int wi = e + 1 + lane;
+                        const int64_t st = (lv && wi < F) ? (int64_t)V.fa[wi] : INT64_MAX;
+                        const int64_t pos = st - a;
+                        const unsigned starts = __reduce_or_sync(FULLM, pos < 32 ? (1u << pos) : 0u);
+                        me = e + __popc(starts & ((2u << lane) - 1u));
+                    }
+                    const int64_t p = a + lane;
+                    valid[q] = lv && p < P;
+                    v[q] = 0; dv[q] = 0; c[q] = 0.0;
+                    if (valid[q]) {
+                        const int32_t u = cur[me];
+                        c[q] = V.fc[me];
+                        const int2 vd = __ldg(A.colp + A.g.row[u] + (p - V.fa[me]));
+                        v[q] = vd.x;
+                        dv[q] = vd.y;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < CUNROLL; ++q) {
+                    GD_DCHECK(!valid[q] || (v[q] >= 0 && v[q] < A.g.n));
+                    old[q] = valid[q] ? atomicAdd(r + v[q], c[q]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < CUNROLL; ++q) {
+                    const double th = theta_d(tc, dv[q]);
+                    const double nw = __dadd_rn(old[q], c[q]);
+                    const bool cross = valid[q] && old[q] < th && nw >= th;
+                    if (valid[q] && below_theta(nw, th)) {
+                        const int at = atomicAdd(&s_nnear, 1);
+                        if (at < NEAR_CAP) s_near[at] = v[q]; else s_amb = 1;
+                    }
+                    cta_append(cross, v[q], nxt, &s_nf);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) s_F = s_nf;
+            __syncthreads();
+        }
+        // ------------------ end of seed: counters, x out --------------------
+        const unsigned long long ops = Red(red_tmp).Sum(my_ops);
+        __syncthreads();
+        const unsigned long long psh = Red(red_tmp).Sum(my_push);
+        unsigned long long nzx = 0, nzr = 0;
+        for (int64_t i = tid; i < n; i += CT) {
+            nzx += x[i] != 0.0;
+            nzr += r[i] != 0.0;
+        }
+        __syncthreads();
+        const unsigned long long xc = Red(red_tmp).Sum(nzx);
+        __syncthreads();
+        const unsigned long long rc = Red(red_tmp).Sum(nzr);
+        if (tid == 0) {
+            s_base = (int64_t)atomicAdd(A.cursor, xc);
+            s_xc = 0;
+            A.sweeps[si] = t;
+            A.ops[si] = (int64_t)ops;
+            A.pushes[si] = (int64_t)psh;
+            A.conv[si] = s_F == 0 ? 1 : 0;
+            A.support[si] = (int64_t)rc;
+            A.xcnt[si] = (int64_t)xc;
+            A.xoff[si] = s_base;
+            A.amb[si] = s_amb;
+            if (s_amb) atomicAdd(A.amb_cnt, 1ULL);
+        }
+        __syncthreads();
+        const int64_t b = s_base;
+        for (int64_t i0 = 0; i0 < n; i0 += CT) {  // warp-uniform trip count
+            const int64_t i = i0 + tid;
+            const bool nz = i < n && x[i] != 0.0;
+            const unsigned am = __ballot_sync(FULLM, nz);
+            int base = 0;
+            if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_xc, __popc(am));
+            base = __shfl_sync(FULLM, base, __ffs(am ? am : 1u) - 1);
+            if (nz) {
+                const int64_t at = b + base + __popc(am & lanemask_lt_());
+                if (at < A.xcap) {
+                    A.xnodes[at] = A.inv ? A.inv[i] : (int32_t)i;
+                    A.xvals[at] = x[i];
+                }
+            }
+        }
+        __syncthreads();
+        (void)s_rc;
+    }
+}
+
 }  // namespace
 
 struct CtaState {
@@ -333,6 +581,13 @@ struct CtaState {
     DBuf<int32_t> front, fa, cmap, pushed;
     DBuf<uint32_t> secmap;
     DBuf<unsigned long long> next;
+    // k_seed_smem: the whole per-seed state in shared memory, one CTA per SM;
+    // used for batches of at most smem_cap seeds (larger batches run more
+    // CTAs per SM in the HBM form, which measured faster there: cora 1,024
+    // seeds 6.2 vs 6.3 ms, 50 seeds 1.18 vs 0.93 ms)
+    bool smem = false;
+    size_t smem_bytes = 0;
+    int smem_cap = 0, smem_slots = 0;  // CTAs resident at once; CTAs launched
 };
 
 // Slots = CTAs resident at once (capped by `max_slots` when > 0 and by the
@@ -341,6 +596,27 @@ CtaState *cta_batch_create(const gd_graph *W, int max_slots) {
     CtaState *S = new CtaState();
     try {
         int per_sm = 0;
+        {   // shared-memory form when one seed's state fits (GDIFF_CTA_SMEM=0: off)
+            const char *e = getenv("GDIFF_CTA_SMEM");
+            int maxo = 0;
+            GD_CUDA(cudaDeviceGetAttribute(&maxo, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                           W->device));
+            const int64_t ccap = (W->n_arcs + 31) / 32 + 1;
+            const size_t need = smem_seed_bytes(W->n ? W->n : 1, ccap);
+            const size_t stat = 16 * 1024;  // static shared memory of the kernel (upper bound)
+            if (!(e && atoi(e) == 0) && need + stat <= (size_t)maxo) {
+                GD_CUDA(cudaFuncSetAttribute(k_seed_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)need));
+                GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seed_smem, CT,
+                                                                      need));
+                if (per_sm > 0) {
+                    S->smem = true;
+                    S->smem_bytes = need;
+                    S->smem_cap = S->smem_slots = per_sm * n_sms(W->device);
+                    if (max_slots > 0 && max_slots < S->smem_slots) S->smem_slots = max_slots;
+                }
+            }
+        }
         GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seed_cta, CT, 0));
         GD_CHECK_ARG(per_sm > 0, "seed kernel does not fit on an SM");
         int slots = per_sm * n_sms(W->device);
@@ -374,6 +650,7 @@ CtaState *cta_batch_create(const gd_graph *W, int max_slots) {
 void cta_batch_destroy(CtaState *S) { delete S; }
 
 int cta_batch_slots(const CtaState *S) { return S->slots; }
+bool cta_batch_smem(const CtaState *S) { return S->smem; }
 
 // Bytes of device memory one slot needs (for the host's mode choice).
 int64_t cta_slot_bytes(int64_t n, int64_t n_arcs) {
@@ -413,8 +690,13 @@ void cta_batch_run(CtaState *S, const gd_graph *W, const int2 *colp, double alph
     A.lg_g = lg_g;
     A.lg_cap = lg_cap;
     GD_CUDA(cudaMemsetAsync(S->next.p, 0, sizeof(unsigned long long), st));
-    const int grid = (int)(n_seeds < S->slots ? n_seeds : S->slots);
-    k_seed_cta<<<grid, CT, 0, st>>>(A);
+    if (S->smem && n_seeds <= S->smem_cap) {
+        k_seed_smem<<<(int)(n_seeds < S->smem_slots ? n_seeds : S->smem_slots), CT, S->smem_bytes,
+                      st>>>(A);
+    } else {
+        const int grid = (int)(n_seeds < S->slots ? n_seeds : S->slots);
+        k_seed_cta<<<grid, CT, 0, st>>>(A);
+    }
     GD_LAUNCH_CHECK();
 }
 

@@ -30,12 +30,19 @@ def _check_x(out, i, x_ref):
 
 # one CTA per seed (small graphs) / the round kernel with slots refilled in-kernel
 # (large graphs) / the same kernel in synchronous waves (GDIFF_STREAM=0)
-MODES = ["cta", "stream", "waves"]
+MODES = ["cta", "cta-global", "stream", "waves"]
 
 
 def set_mode(monkeypatch, mode):
-    monkeypatch.setenv("GDIFF_BATCH_MODE", "cta" if mode == "cta" else "rounds")
-    if mode == "cta":
+    """cta: one CTA per seed (shared-memory state when the graph fits);
+    cta-global: the same with the state in HBM; stream / waves: round kernel."""
+    cta = mode in ("cta", "cta-global")
+    monkeypatch.setenv("GDIFF_BATCH_MODE", "cta" if cta else "rounds")
+    if mode == "cta-global":
+        monkeypatch.setenv("GDIFF_CTA_SMEM", "0")
+    else:
+        monkeypatch.delenv("GDIFF_CTA_SMEM", raising=False)
+    if cta:
         monkeypatch.delenv("GDIFF_STREAM", raising=False)
     else:
         monkeypatch.setenv("GDIFF_STREAM", "0" if mode == "waves" else "1")
@@ -95,8 +102,10 @@ def test_solver_reuse_and_device_path(gpu, monkeypatch, mode):
     d = solver.solve_device(torch.as_tensor(seeds, device="cuda"))
     assert np.array_equal(d["total_ops"].cpu().numpy(), a["total_ops"])
     assert np.array_equal(d["sweeps"].cpu().numpy(), a["sweeps"])
-    assert d["kernel_launches"] == {"waves": 4 * 5, "stream": 1 + 5, "cta": 1}[mode]
-    assert solver.mode == {"waves": "rounds", "stream": "stream", "cta": "cta"}[mode]
+    assert d["kernel_launches"] == {"waves": 4 * 5, "stream": 1 + 5, "cta": 1, "cta-global": 1}[mode]
+    # (5,000 nodes: one seed's state fits in shared memory)
+    assert solver.mode == {"waves": "rounds", "stream": "stream", "cta": "cta-smem",
+                           "cta-global": "cta"}[mode]
     assert solver.last_kernel_ms > 0.0
 
 
