@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-global-gd", action="store_true", help="skip the global GD reference point")
     p.add_argument("--graph-seed", type=int, default=0)
     p.add_argument("--no-relabel", action="store_true", help="run on the caller's node order")
     p.add_argument("--method", default="local-gd",
@@ -322,6 +323,43 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def global_gd_point(dg, n, alpha, eps, seeds):
+    """The global power-iteration GD solver on the GPU for the same PPR systems
+    (north_star's reference point; src/global_solvers.py:124-152 semantics:
+    every sweep x += r, r <- beta P r over all nodes, until no node is active),
+    through the drop-in gd_gradient_descent call: host b in, host x and r out,
+    one convergence check per sweep.  One untimed call, then the seeds timed."""
+    import ctypes as C
+
+    from paper_2410_21634_b200 import _lib as gdl
+    from paper_2410_21634_b200.device import report_arrays
+
+    lib = gdl.load()
+    op = gdl.Operator(weight_rule=gdl.GD_W_RW, theta_rule=gdl.GD_T_DEGREE, beta=1.0 - alpha,
+                      theta_coeff=eps * alpha)
+    b, x, r = np.zeros(n), np.empty(n), np.empty(n)
+    walls, sweeps, ops = [], [], 0
+    for i, s in enumerate([int(seeds[0])] + [int(v) for v in seeds]):
+        b[:] = 0.0
+        b[s] = alpha
+        rep = gdl.Report()
+        t0 = time.perf_counter()
+        gdl.check(lib.gd_gradient_descent(dg.handle, C.byref(op), gdl.ptr(b), gdl.ptr(x),
+                                          gdl.ptr(r), 10_000, C.byref(rep)))
+        wall = time.perf_counter() - t0
+        out = report_arrays(rep)
+        if i:
+            walls.append(wall)
+            sweeps.append(int(out["sweeps"]))
+            ops += int(out["total_ops"])
+    return {"solves_per_s": len(walls) / sum(walls), "ms_per_solve": 1e3 * sum(walls) / len(walls),
+            "sweeps": sweeps, "gteps": ops / sum(walls) / 1e9, "seeds": len(walls),
+            "solver": "gd_gradient_descent (global GD, warp-per-row ordered pull, bitwise with "
+                      "the reference)",
+            "timing": "host wall clock of the drop-in call (H2D b, per-sweep convergence check, "
+                      "D2H x and r)"}
+
+
 def workload_config(args, n, m):
     name = {"local-gd": "LocalGD", "local-ch": "LocalCH", "local-hb": "LocalHB", "local-hk": "push",
             "local-sor": f"LocalSOR(omega={args.omega:g})"}[args.method]
@@ -485,6 +523,10 @@ def main():
              {"local-gd": "k_rounds", "local-ch": "k_signed_rounds", "local-hb": "k_signed_rounds",
               "local-hk": "k_rounds_hk", "local-sor": "k_fifo_batch"}[args.method])
     traffic, traffic_src = ncu_traffic(kname, workload_config(args, n, m))
+    # the global GD reference point (rank 0, LocalGD-PPR configs up to products size)
+    global_gd = None
+    if (rank == 0 and args.method == "local-gd" and not args.no_global_gd and n <= 10_000_000):
+        global_gd = global_gd_point(dg, n, args.alpha, args.eps, batches[args.warmup][:2])
     # e2e: the public host API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -570,7 +612,9 @@ def main():
                                                                 "local-hb": launches // 5,
                                                                 "local-hk": launches // 5}.get(args.method, launches)),
                          "peak_kind": peak_kind,
-                         "kernel": {"local-gd": "k_seed_cta (one CTA per seed)" if cta else
+                         "kernel": {"local-gd": ("k_seed_smem (one CTA per seed, state in shared "
+                                                 "memory)" if solver.mode == "cta-smem" else
+                                                 "k_seed_cta (one CTA per seed)") if cta else
                                                     "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
                                     "local-hb": "k_signed_rounds (heavy-ball coefficients)",
@@ -579,7 +623,7 @@ def main():
                                                  else "k_fifo_batch (warp per seed)"}[args.method],
                          "kernel_ms_per_step": float(t[4]) / args.steps},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "with_gather": with_gather,
+            "with_gather": with_gather, "global_gd_reference": global_gd,
             "clocks": clk.summary(), "relabel": not args.no_relabel,
         }
         print(json.dumps(line), flush=True)

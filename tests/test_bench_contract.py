@@ -61,6 +61,9 @@ def test_gpu_arm_json_line(method):
     assert amb["flagged_per_step"] >= 0
     if method in ("local-gd", "local-ch"):
         assert amb["exact_resolve"]["changed_by_exact_resolve"] <= amb["exact_resolve"]["flagged"]
+    if method == "local-gd":  # the global GD reference point beside the batched line
+        gg = line["global_gd_reference"]
+        assert gg["solves_per_s"] > 0 and gg["seeds"] == 2 and all(s >= 1 for s in gg["sweeps"])
     # the reference arm: same config dict, and it never loads the product library
     ref = subprocess.run(cmd + ["--impl", "reference"], capture_output=True, text=True,
                          timeout=900, cwd=ROOT)
