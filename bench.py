@@ -389,9 +389,25 @@ def main():
     from paper_2410_21634_b200.metrics import b_alg_bytes, sample_sources
 
     rank, world, local = dist_env()
+    # one rank per GPU; GDIFF_BENCH_BACKEND=gloo (tests) runs the same code path with
+    # gloo collectives on host copies, ranks sharing the visible GPUs round-robin
+    backend = os.environ.get("GDIFF_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def allreduce(t, op=dist.ReduceOp.SUM):
+        """In place on a CUDA tensor (through a host copy under gloo)."""
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
     n, m = SHAPES[args.shape]
     dg, row, col, row_h = make_graph(args.shape, args.graph_seed, local)
     hdeg = _HostGraph(n, row_h)
@@ -426,6 +442,9 @@ def main():
         only collective of the data path; timed separately below)."""
         if world == 1:
             return None
+        if backend != "nccl":  # (gloo: host tensors)
+            return gather_results({f: res[f].cpu() for f in STAT_FIELDS}, res["x_nodes"].cpu(),
+                                  res["x_vals"].cpu(), device=torch.device("cpu"), dst=0)
         return gather_results({f: res[f] for f in STAT_FIELDS}, res["x_nodes"], res["x_vals"],
                               dst=0, to_host=False)  # (results stay in rank 0's HBM)
 
@@ -489,9 +508,9 @@ def main():
     t = torch.tensor([ms, ops, pushes, solved, kern_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         tmax = t[:1].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        allreduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t[1:].clone()
-        dist.all_reduce(tsum)
+        allreduce(tsum)
         ms = float(tmax[0])
         ops, pushes, solved, kern_all = (float(v) for v in tsum)
     sec = ms / 1e3
@@ -508,10 +527,10 @@ def main():
         g1.record(stream)
         torch.cuda.synchronize()
         tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        allreduce(tg, op=dist.ReduceOp.MAX)
         with_gather = {"value": (args.seeds * args.steps * world) / (float(tg[0]) / 1e3),
                        "ms_per_step": float(tg[0]) / args.steps,
-                       "gather": "NCCL gather of counters + sparse x to rank 0 every step"}
+                       "gather": f"{backend} gather of counters + sparse x to rank 0 every step"}
     balg = b_alg_bytes(int(ops), int(pushes), args.method)
     # roofline of the dominant kernel (the sweep loop), rank-0 device events
     peak, peak_kind = peaks()
@@ -544,7 +563,7 @@ def main():
         wall = time.perf_counter() - t0
         if world > 1:
             w = torch.tensor([wall], dtype=torch.float64, device="cuda")
-            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            allreduce(w, op=dist.ReduceOp.MAX)
             wall = float(w[0])
         e2e = {"value": (args.seeds * args.steps * world) / wall, "unit": "solves/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,

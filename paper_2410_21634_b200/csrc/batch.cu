@@ -186,7 +186,8 @@ struct RoundArgs {
     unsigned long long *sn[2];    // per slot: entries in the frontier, per round parity
     int64_t *drain_cnt;           // per slot: pushed count of the finished seed
     int64_t reset_units;          // sector-map reset work units per finished slot
-    int32_t dbg;                  // (experiments) 1: skip x extract, 2: skip r reset
+    int32_t dbg;                  // (experiments) 1: skip x extract, 2: skip r reset,
+                                  //   4: no sector-map marks (timing probes only)
     int64_t cohort;               // refill only once this many slots are free (they
                                   // then start together: see k_rounds)
 };
@@ -976,7 +977,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
                 const bool cross = valid[q] && old[q] < th && nw >= th;
                 if (valid[q] && below_theta(nw, th)) near_record(A.nearl, nxt, k[q], v[q], A.s_amb);
                 block_count(first, k[q], 1u, S.touch);
-                if (first)  // first write of this r word: remember its 32 B sector
+                if (first && !(A.dbg & 4))  // first write of this r word: remember its 32 B sector
                     atomicOr(mapn + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                 block_count(negz, k[q], 1u, S.negz);
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
@@ -1473,6 +1474,7 @@ struct gd_batch {
                 A.reset_units = u < 256 ? 256 : (u > 16384 ? 16384 : u);
             }
         }
+        A.dbg = dbg;
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
         A.cursor = cursor.p;

@@ -71,3 +71,28 @@ def test_gpu_arm_json_line(method):
     rline = json.loads(ref.stdout.strip().splitlines()[-1])
     assert rline["config"] == line["config"]
     assert rline["impl"] == "reference" and rline["metric"] == line["metric"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_torchrun_two_ranks():
+    """The multi-rank code path of bench.py (torchrun, seed sharding, max-over-ranks
+    timing, the per-step result gather) with 2 ranks; on a one-GPU box both ranks
+    share cuda:0 and the collectives go through gloo (GDIFF_BENCH_BACKEND) -- a
+    code-path check, not a scaling number."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--shape", "cora", "--eps", "1e-6",
+           "--seeds", "16", "--steps", "2", "--warmup", "3"]
+    env = dict(os.environ, GDIFF_BENCH_BACKEND="gloo")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "weak"
+    assert line["with_gather"]["value"] > 0 and line["e2e"]["value"] > 0
