@@ -626,10 +626,12 @@ def main():
             "b_alg_gb": balg / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "b_alg_per_launch": my_balg / max(1, {"local-gd": launches // (1 if cta else 4),
-                                                                "local-ch": launches // 5,
-                                                                "local-hb": launches // 5,
-                                                                "local-hk": launches // 5}.get(args.method, launches)),
+                         # per launch of the sweep kernel: one per wave of `slots` seeds
+                         # (round kernels), one per solve (CTA / FIFO forms)
+                         "b_alg_per_launch": my_balg / max(1, args.steps * (
+                             -(-args.seeds // solver.slots)
+                             if args.method in ("local-ch", "local-hb", "local-hk") or
+                             (args.method == "local-gd" and not cta) else 1)),
                          "peak_kind": peak_kind,
                          "kernel": {"local-gd": ("k_seed_smem (one CTA per seed, state in shared "
                                                  "memory)" if solver.mode == "cta-smem" else

@@ -186,10 +186,17 @@ struct RoundArgs {
     unsigned long long *sn[2];    // per slot: entries in the frontier, per round parity
     int64_t *drain_cnt;           // per slot: pushed count of the finished seed
     int64_t reset_units;          // sector-map reset work units per finished slot
-    int32_t dbg;                  // (experiments) 1: skip x extract, 2: skip r reset,
-                                  //   4: no sector-map marks (timing probes only)
+    int32_t dbg;                  // (experiments) 1: skip x extract, 2: skip r reset
     int64_t cohort;               // refill only once this many slots are free (they
                                   // then start together: see k_rounds)
+    // CTA-local tail (k_tail): once a round past the wave's peak has <=
+    // tail_p arcs and <= tail_f entries, k_rounds leaves (t, F) in tail_state
+    // and k_tail finishes slot k in block k; frontier lists in tail_list
+    // (2 x n per slot), c_u in tail_c (n per slot)
+    int64_t tail_p, tail_f;
+    int32_t *tail_list;
+    double *tail_c;
+    int64_t *tail_state;
 };
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -489,6 +496,216 @@ struct OutArgs {
 // slowest seed of a wave, and there are no extract / reset launches.  The
 // kernel leaves at a round start once `seg_done` seeds have finished (the
 // host copies their x out while the next launch runs) and resumes there.
+// ---------------------------------------------------------------------------
+// CTA-local tail of a wave (k_tail).  The last rounds of a wave carry a few
+// hundred arcs but each costs the round kernel two grid barriers and a dozen
+// dependent global accesses (~10-15 us; ~8 % of a products wave).  Once a
+// round past the wave's peak is small (<= tail_p arcs, <= tail_f entries;
+// every block sees the same F and P), k_rounds stops and leaves (t, F) in
+// tail_state; k_tail then runs one block per slot: block k takes slot k's
+// entries of round t and runs the remaining sweeps of that seed alone with
+// block barriers only -- the same push, threshold-crossing, first-touch and
+// near-threshold rules as k_rounds, the whole frontier pushed before any
+// scatter, arcs block-balanced (entries in segments of TAIL_SEG, degrees
+// block-scanned, UNROLL_T arcs in flight per thread, entry found by binary
+// search in shared memory), the next frontier in the slot's own list.  Sweeps
+// stay numbered as rounds, so sweeps, ops and frontier sets are unchanged.  A
+// separate kernel rather than a branch of k_rounds: inlined there it cost the
+// round loop ~3 % through register allocation.
+constexpr int TAIL_SEG = 1024;
+constexpr int TAIL_NEAR = 256;
+constexpr int UNROLL_T = 4;
+
+__global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArgs A) {
+    using Scan = cub::BlockScan<int, BT>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ double tc[TAIL_SEG];
+    __shared__ int64_t trow[TAIL_SEG];
+    __shared__ int32_t toff[TAIL_SEG + 1], tnear[TAIL_NEAR];
+    __shared__ unsigned long long c_ops[1], c_pvol[1];
+    __shared__ unsigned c_push[1], c_touch[1], c_negz[1];
+    __shared__ double c_g;
+    __shared__ int s_cur, s_nxt, s_nn, s_amb;
+    const int64_t F = A.tail_state[1];
+    if (F < 0) return;  // the wave ended in the round kernel
+    int32_t t = (int32_t)A.tail_state[0];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t k = (int32_t)blockIdx.x;
+    const int64_t n = A.n;
+    int32_t *const l0 = A.tail_list + (int64_t)k * 2 * n, *const l1 = l0 + n;
+    double *const cval = A.tail_c + (int64_t)k * n;  // c_u of the sweep's entries
+    if (tid == 0) {
+        s_cur = s_nn = s_amb = 0;
+        c_ops[0] = c_pvol[0] = 0;
+        c_push[0] = c_touch[0] = c_negz[0] = 0;
+        c_g = 0.0;
+    }
+    __syncthreads();
+    for (int64_t e0 = 0; e0 < F; e0 += BT) {  // this slot's entries of round t
+        const int64_t e = e0 + tid;
+        const int64_t key = e < F ? A.ukey[e] : -1;
+        const bool mine = e < F && (int32_t)(key >> 32) == k;
+        const unsigned am = __ballot_sync(FULL, mine);
+        int base = 0;
+        if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_cur, __popc(am));
+        base = __shfl_sync(FULL, base, __ffs(am ? am : 1u) - 1);
+        if (mine) l0[base + __popc(am & lanemask_lt())] = (int32_t)(key & 0xffffffffLL);
+    }
+    double *const r = A.r + (int64_t)k * A.ld;
+    double *const x = A.x + (int64_t)k * A.ld;
+    uint32_t *const map = A.secmap + (int64_t)k * A.smw;
+    const double tcf = A.tcoeff;
+    int cur = 0;
+    __syncthreads();
+    for (;; ++t) {
+        const int nn = min(s_nn, TAIL_NEAR);
+        for (int i = tid; i < nn; i += BT)
+            if (below_theta(r[tnear[i]], theta_deg(tcf, A.g.deg[tnear[i]]))) s_amb = 1;
+        __syncthreads();
+        const int Fc = s_cur;
+        if (Fc == 0) break;
+        if (t >= A.max_sweeps) {
+            if (tid == 0) A.s_conv[k] = 0;
+            break;
+        }
+        int32_t *const cl = cur ? l1 : l0, *const nl = cur ? l0 : l1;
+        // push every entry of the sweep before any scatter (the reference reads
+        // r over the whole frontier first): x += r, r = -0, c_u kept per entry
+        double my_g = 0.0;
+        for (int i0 = 0; i0 < Fc; i0 += BT) {  // warp-uniform trips
+            const int i = i0 + tid;
+            const bool live = i < Fc;
+            int32_t u = 0, d = 0;
+            bool fresh = false;
+            if (live) {
+                u = cl[i];
+                d = A.g.deg[u];
+                const double val = r[u];
+                const double xo = x[u];
+                x[u] = __dadd_rn(xo, val);
+                r[u] = -0.0;
+                my_g += fabs(val);
+                if (near_theta(val, theta_deg(tcf, d))) s_amb = 1;  // final r >= theta
+                cval[i] = __dmul_rn(val, __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta));
+                fresh = __double_as_longlong(xo) == 0;
+            }
+            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
+            block_count(fresh, 0, (unsigned)d, c_pvol);
+            block_count(live, 0, (unsigned)d, c_ops);
+            block_count(live, 0, 1u, c_push);
+        }
+        if (A.lg_f) atomicAdd(&c_g, my_g);
+        if (tid == 0) {
+            s_nn = 0;
+            s_nxt = 0;
+            A.s_last[k] = t;
+        }
+        __syncthreads();
+        // scatter, TAIL_SEG entries at a time, arcs block-balanced
+        for (int seg0 = 0; seg0 < Fc; seg0 += TAIL_SEG) {
+            const int ns = min(TAIL_SEG, Fc - seg0);
+            constexpr int PER = TAIL_SEG / BT;
+            int dd[PER];
+            int mine = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid * PER + j;
+                dd[j] = 0;
+                if (i < ns) {
+                    const int32_t u = cl[seg0 + i];
+                    dd[j] = A.g.deg[u];
+                    trow[i] = A.g.row[u];
+                    tc[i] = cval[seg0 + i];
+                }
+                mine += dd[j];
+            }
+            int excl = 0, tot = 0;
+            Scan(scan_tmp).ExclusiveSum(mine, excl, tot);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid * PER + j;
+                if (i < ns) toff[i] = excl;
+                excl += dd[j];
+            }
+            if (tid == 0) toff[ns] = tot;
+            __syncthreads();
+            const int P = tot;
+            for (int p0 = tid; p0 - tid < P; p0 += BT * UNROLL_T) {  // warp-uniform trips
+                int32_t v[UNROLL_T], dv[UNROLL_T];
+                double c[UNROLL_T], old[UNROLL_T];
+                bool valid[UNROLL_T];
+#pragma unroll
+                for (int q = 0; q < UNROLL_T; ++q) {
+                    const int p = p0 + q * BT;
+                    valid[q] = p < P;
+                    v[q] = 0; dv[q] = 0; c[q] = 0.0;
+                    if (valid[q]) {
+                        int lo = 0, hi = ns - 1;  // last entry with toff <= p
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (toff[mid] <= p) lo = mid; else hi = mid - 1;
+                        }
+                        c[q] = tc[lo];
+                        const int2 vd = __ldg(A.colp + trow[lo] + (p - toff[lo]));
+                        v[q] = vd.x;
+                        dv[q] = vd.y;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < UNROLL_T; ++q) {
+                    GD_DCHECK(!valid[q] || (v[q] >= 0 && v[q] < A.n));
+                    old[q] = valid[q] ? atomicAdd(r + v[q], c[q]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < UNROLL_T; ++q) {
+                    const long long ob = __double_as_longlong(old[q]);
+                    const double th = theta_deg(tcf, dv[q]);
+                    const bool first = valid[q] && ob == 0;
+                    const bool negz = valid[q] && ob == (long long)0x8000000000000000ULL;
+                    const double nw = __dadd_rn(old[q], c[q]);
+                    const bool cross = valid[q] && old[q] < th && nw >= th;
+                    if (valid[q] && below_theta(nw, th)) {
+                        const int at = atomicAdd(&s_nn, 1);
+                        if (at < TAIL_NEAR) tnear[at] = v[q]; else s_amb = 1;
+                    }
+                    block_count(first, 0, 1u, c_touch);
+                    if (first) atomicOr(map + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
+                    block_count(negz, 0, 1u, c_negz);
+                    const unsigned am = __ballot_sync(FULL, cross);
+                    int base = 0;
+                    if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_nxt, __popc(am));
+                    base = __shfl_sync(FULL, base, __ffs(am ? am : 1u) - 1);
+                    if (cross) nl[base + __popc(am & lanemask_lt())] = v[q];  // (< n: a node
+                }                                                              //  crosses once)
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            if (A.lg_f && t < A.lg_cap) {
+                const int64_t at = (A.seed_base + k) * A.lg_cap + t;
+                atomicAdd((unsigned long long *)A.lg_f + at, (unsigned long long)c_push[0]);
+                atomicAdd((unsigned long long *)A.lg_ops + at, c_ops[0]);
+                atomicAdd(A.lg_g + at, c_g);
+            }
+            A.s_ops[k] += c_ops[0];
+            A.s_pvol[k] += c_pvol[0];
+            A.s_pushes[k] += c_push[0];
+            A.touched[k] += c_touch[0];
+            A.s_negz[k] += c_negz[0];
+            c_ops[0] = c_pvol[0] = 0;
+            c_push[0] = c_touch[0] = c_negz[0] = 0;
+            c_g = 0.0;
+            s_cur = s_nxt;
+        }
+        cur ^= 1;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (s_amb) A.s_amb[k] = 1;
+        A.slot_base[k] = (int64_t)atomicAdd(A.cursor, A.pushed_cnt[k]);  // (final here)
+    }
+}
+
 template <bool HK, bool STREAM = false>
 __global__ void __launch_bounds__(BT, GD_KR_MINB)
     k_rounds(const __grid_constant__ RoundArgs A, const __grid_constant__ OutArgs O) {
@@ -515,6 +732,8 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
     }
     __syncthreads();
 
+    bool tail = false;
+    int64_t pmax = 0;  // largest round so far (the same in every block)
     for (int32_t t = STREAM ? *A.t_state : 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const unsigned long long packed = *(volatile unsigned long long *)(A.fctr + cur);
@@ -578,6 +797,16 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
             }
             if (nn > 0) grid.sync();  // (the reset below must not overtake those reads)
         } else if (F == 0) {
+            break;
+        }
+        pmax = P > pmax ? P : pmax;
+        if (!HK && !STREAM && A.tail_list && P <= A.tail_p && F <= A.tail_f && 16 * P <= pmax) {
+            // the rest of the wave (past its peak) in k_tail, one block per slot
+            if (gtid == 0) {
+                A.tail_state[0] = t;
+                A.tail_state[1] = F;
+            }
+            tail = true;
             break;
         }
         if (((P + 31) >> 5) > A.ccap) {  // arc-chunk map too small: report, stop
@@ -977,7 +1206,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
                 const bool cross = valid[q] && old[q] < th && nw >= th;
                 if (valid[q] && below_theta(nw, th)) near_record(A.nearl, nxt, k[q], v[q], A.s_amb);
                 block_count(first, k[q], 1u, S.touch);
-                if (first && !(A.dbg & 4))  // first write of this r word: remember its 32 B sector
+                if (first)  // first write of this r word: remember its 32 B sector
                     atomicOr(mapn + (int64_t)k[q] * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
                 block_count(negz, k[q], 1u, S.negz);
                 stage_append(cross, k[q], v[q], dv[q], S, A, nxt);
@@ -990,8 +1219,9 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
         counters_flush(S.negz, A.s_negz, A.m);
         grid.sync();
     }
-    // reserve each slot's output segment (pushed counts are final here)
-    if (!STREAM && blockIdx.x == 0)
+    // reserve each slot's output segment (pushed counts are final here; after
+    // a tail handed to k_tail, it reserves them)
+    if (!STREAM && !tail && blockIdx.x == 0)
         for (int64_t k = threadIdx.x; k < A.m; k += BT)
             A.slot_base[k] = (int64_t)atomicAdd(A.cursor, A.pushed_cnt[k]);
 }
@@ -1475,6 +1705,13 @@ struct gd_batch {
             }
         }
         A.dbg = dbg;
+        if (tail_list.p) {
+            A.tail_list = tail_list.p;
+            A.tail_c = tail_c.p;
+            A.tail_state = tail_state.p;
+            A.tail_p = tail_p;
+            A.tail_f = tail_f;
+        }
         A.overflow = overflow.p;
         A.perm = R ? perm.p : nullptr;
         A.cursor = cursor.p;
@@ -1516,6 +1753,12 @@ struct gd_batch {
         if (w >= 1) hs_drain(w - 1);
         if (w == waves - 1) hs_drain(w);
     }
+    // CTA-local wave tails (tail_sweeps): 2 x n int32 frontier lists and n c_u
+    // per slot, allocated when they cost at most 4 GB (GDIFF_TAIL=0: off)
+    DBuf<int32_t> tail_list;
+    DBuf<double> tail_c;
+    DBuf<int64_t> tail_state;
+    int64_t tail_p = 1 << 14, tail_f = 1 << 13;
     bool trace = false;              // GDIFF_WAVE_TRACE: per-wave timeline to stderr
     bool serial = false;             // GDIFF_WAVE_SERIAL: no second stream
     bool ext_bal = false;            // work-balanced x extraction
@@ -1693,11 +1936,17 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
                                                                B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
+        if (B->tail_list.p && !B->hk)  // (-1: no tail handed over)
+            GD_CUDA(cudaMemsetAsync(B->tail_state.p, 0xFF, 2 * sizeof(int64_t), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A, &O};
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
         GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
+        if (B->tail_list.p && !B->hk) {
+            k_tail<<<(unsigned)A.m, BT, 0, st>>>(A);
+            launches += 1;
+        }
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
         // x extraction (random gathers: latency-bound) on st, the r reset
         // (sector stores: bandwidth-bound) concurrently on a second stream;
@@ -2277,6 +2526,17 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                 B->p.stage_w = nullptr;  // (the caller's array is not kept)
             }
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
+            {
+                const char *e = getenv("GDIFF_TAIL");
+                const size_t tl = 2 * (size_t)slots * (size_t)n;
+                if (!B->hk && !(e && atoi(e) == 0) && tl * 8 <= (4ULL << 30)) {
+                    B->tail_list.alloc(tl);
+                    B->tail_c.alloc(tl / 2);
+                    B->tail_state.alloc(2);
+                    if (const char *v = getenv("GDIFF_TAIL_P")) B->tail_p = atoll(v);  // (A/B)
+                    if (const char *v = getenv("GDIFF_TAIL_F")) B->tail_f = atoll(v);
+                }
+            }
             const size_t smem = stage_bytes(slots);
             const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
             GD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
