@@ -193,7 +193,7 @@ struct RoundArgs {
     // tail_p arcs and <= tail_f entries, k_rounds leaves (t, F) in tail_state
     // and k_tail finishes slot k in block k; frontier lists in tail_list
     // (2 x n per slot), c_u in tail_c (n per slot)
-    int64_t tail_p, tail_f;
+    int64_t tail_p, tail_f, tail_cap;
     int32_t *tail_list;
     double *tail_c;
     int64_t *tail_state;
@@ -525,17 +525,18 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
     __shared__ unsigned long long c_ops[1], c_pvol[1];
     __shared__ unsigned c_push[1], c_touch[1], c_negz[1];
     __shared__ double c_g;
-    __shared__ int s_cur, s_nxt, s_nn, s_amb;
+    __shared__ int s_cur, s_nxt, s_nn, s_amb, s_ovf;
     const int64_t F = A.tail_state[1];
     if (F < 0) return;  // the wave ended in the round kernel
     int32_t t = (int32_t)A.tail_state[0];
     const int tid = threadIdx.x, lane = tid & 31;
     const int32_t k = (int32_t)blockIdx.x;
     const int64_t n = A.n;
-    int32_t *const l0 = A.tail_list + (int64_t)k * 2 * n, *const l1 = l0 + n;
-    double *const cval = A.tail_c + (int64_t)k * n;  // c_u of the sweep's entries
+    const int64_t C = A.tail_cap;  // list capacity per slot (n, or less on huge graphs)
+    int32_t *const l0 = A.tail_list + (int64_t)k * 2 * C, *const l1 = l0 + C;
+    double *const cval = A.tail_c + (int64_t)k * C;  // c_u of the sweep's entries
     if (tid == 0) {
-        s_cur = s_nn = s_amb = 0;
+        s_cur = s_nn = s_amb = s_ovf = 0;
         c_ops[0] = c_pvol[0] = 0;
         c_push[0] = c_touch[0] = c_negz[0] = 0;
         c_g = 0.0;
@@ -549,13 +550,19 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
         int base = 0;
         if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_cur, __popc(am));
         base = __shfl_sync(FULL, base, __ffs(am ? am : 1u) - 1);
-        if (mine) l0[base + __popc(am & lanemask_lt())] = (int32_t)(key & 0xffffffffLL);
+        const int at = base + __popc(am & lanemask_lt());
+        if (mine && at < C) l0[at] = (int32_t)(key & 0xffffffffLL);
     }
     double *const r = A.r + (int64_t)k * A.ld;
     double *const x = A.x + (int64_t)k * A.ld;
     uint32_t *const map = A.secmap + (int64_t)k * A.smw;
     const double tcf = A.tcoeff;
     int cur = 0;
+    __syncthreads();
+    if (s_cur > C) {  // (see the list overflow below)
+        if (tid == 0) A.overflow[0] = 2;
+        s_cur = 0;  // (every thread writes the same)
+    }
     __syncthreads();
     for (;; ++t) {
         const int nn = min(s_nn, TAIL_NEAR);
@@ -675,8 +682,11 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
                     int base = 0;
                     if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_nxt, __popc(am));
                     base = __shfl_sync(FULL, base, __ffs(am ? am : 1u) - 1);
-                    if (cross) nl[base + __popc(am & lanemask_lt())] = v[q];  // (< n: a node
-                }                                                              //  crosses once)
+                    if (cross) {
+                        const int at = base + __popc(am & lanemask_lt());
+                        if (at < C) nl[at] = v[q]; else s_ovf = 1;
+                    }
+                }
             }
             __syncthreads();
         }
@@ -696,9 +706,11 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
             c_push[0] = c_touch[0] = c_negz[0] = 0;
             c_g = 0.0;
             s_cur = s_nxt;
-        }
+            if (s_ovf) A.overflow[0] = 2;  // list capacity: the host redoes the solve
+        }                                  // without tails
         cur ^= 1;
         __syncthreads();
+        if (s_ovf) break;
     }
     if (tid == 0) {
         if (s_amb) A.s_amb[k] = 1;
@@ -1705,8 +1717,9 @@ struct gd_batch {
             }
         }
         A.dbg = dbg;
-        if (tail_list.p) {
+        if (tail_list.p && tail_on) {
             A.tail_list = tail_list.p;
+            A.tail_cap = tail_cap;
             A.tail_c = tail_c.p;
             A.tail_state = tail_state.p;
             A.tail_p = tail_p;
@@ -1758,7 +1771,8 @@ struct gd_batch {
     DBuf<int32_t> tail_list;
     DBuf<double> tail_c;
     DBuf<int64_t> tail_state;
-    int64_t tail_p = 1 << 14, tail_f = 1 << 13;
+    int64_t tail_p = 1 << 14, tail_f = 1 << 13, tail_cap = 0;
+    bool tail_on = false;            // (off for good after a list overflow)
     bool trace = false;              // GDIFF_WAVE_TRACE: per-wave timeline to stderr
     bool serial = false;             // GDIFF_WAVE_SERIAL: no second stream
     bool ext_bal = false;            // work-balanced x extraction
@@ -1936,14 +1950,14 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
                                                                B->hk ? 1.0 : B->p.alpha);
         GD_LAUNCH_CHECK();
-        if (B->tail_list.p && !B->hk)  // (-1: no tail handed over)
+        if (B->tail_on && !B->hk)  // (-1: no tail handed over)
             GD_CUDA(cudaMemsetAsync(B->tail_state.p, 0xFF, 2 * sizeof(int64_t), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A, &O};
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
         GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
-        if (B->tail_list.p && !B->hk) {
+        if (B->tail_on && !B->hk) {
             k_tail<<<(unsigned)A.m, BT, 0, st>>>(A);
             launches += 1;
         }
@@ -2528,11 +2542,18 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
             B->xnodes.alloc(B->xcap); B->xvals.alloc(B->xcap);
             {
                 const char *e = getenv("GDIFF_TAIL");
-                const size_t tl = 2 * (size_t)slots * (size_t)n;
-                if (!B->hk && !(e && atoi(e) == 0) && tl * 8 <= (4ULL << 30)) {
-                    B->tail_list.alloc(tl);
-                    B->tail_c.alloc(tl / 2);
+                // lists of n entries per slot (a tail frontier can never exceed
+                // them) when that costs <= 4 GB, else 1 M (huge graphs: a tail
+                // frontier that outgrows them makes the solve rerun without tails)
+                int64_t cap = (int64_t)n;
+                if ((size_t)slots * (size_t)n * 16 > (4ULL << 30)) cap = std::min<int64_t>(n, 1 << 20);
+                if (const char *v = getenv("GDIFF_TAIL_CAP")) cap = atoll(v);  // (tests)
+                if (!B->hk && !(e && atoi(e) == 0) && cap > 0) {
+                    B->tail_cap = cap;
+                    B->tail_list.alloc(2 * (size_t)slots * (size_t)cap);
+                    B->tail_c.alloc((size_t)slots * (size_t)cap);
                     B->tail_state.alloc(2);
+                    B->tail_on = true;
                     if (const char *v = getenv("GDIFF_TAIL_P")) B->tail_p = atoll(v);  // (A/B)
                     if (const char *v = getenv("GDIFF_TAIL_F")) B->tail_f = atoll(v);
                 }
@@ -2609,6 +2630,12 @@ int gd_batch_solve_device(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds,
             unsigned long long used = 0;
             GD_CUDA(cudaMemcpy(&ovf, B->overflow.p, sizeof(ovf), cudaMemcpyDeviceToHost));
             GD_CUDA(cudaMemcpy(&used, B->cursor.p, sizeof(used), cudaMemcpyDeviceToHost));
+            if (ovf == 2 && B->tail_on) {  // a CTA-local tail outgrew its list: redo
+                B->tail_on = false;        // the solve (the slots were reset) without
+                if (B->hs_on) GD_CUDA(cudaStreamSynchronize(B->hs.cs));  // tails
+                --attempt;
+                continue;
+            }
             if (ovf) {
                 set_error("frontier capacity %lld (entries or arc chunks per round) exceeded; "
                           "raise frontier_cap",

@@ -73,8 +73,15 @@ def test_pa_batch_matches_reference(gpu, pa):
         _check_x(out, i, pa[f"{k}/x"])
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + ["waves-notail", "waves-tailcap"])
 def test_rmat_batch_matches_oracle(gpu, monkeypatch, mode):
+    """waves-notail: the round kernel without CTA-local tails; waves-tailcap: tail
+    lists of 4 entries per slot, so a tail overflows and the solve is redone
+    without tails (the results must not show it)."""
+    if mode.startswith("waves-"):
+        monkeypatch.setenv("GDIFF_TAIL" if mode == "waves-notail" else "GDIFF_TAIL_CAP",
+                           "0" if mode == "waves-notail" else "4")
+        mode = "waves"
     set_mode(monkeypatch, mode)
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 48, seed=0)
