@@ -582,12 +582,17 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
                     atomicOr(A.secmap + (int64_t)k[q] * A.smw + (v[q] >> 7),
                              1u << ((v[q] >> 2) & 31));
                 const double th = theta_of(A.op, v[q], dv[q]);
-                const bool hot = valid[q] && fabs(nv) >= th;
+                // mark on a cold -> hot transition only: an update that finds
+                // |old| >= theta follows one that stored that hot value (and
+                // marks, or has marked, the node) -- at the round start every
+                // hot node is a frontier node already re-marked by phase A
+                // ("again") or was filtered out as inactive (cap / divergence)
+                const bool rise = valid[q] && fabs(nv) >= th && !(fabs(old[q]) >= th);
                 // a node whose final |r| sits just below theta is never a
                 // candidate: its landings there are re-read after the round
                 if (valid[q] && below_theta(fabs(nv), th))
                     near_record(A.nearl, nxt, k[q], v[q], A.s_amb);
-                const bool nw = cand_mark(hot, k[q], v[q], A, nxt);
+                const bool nw = cand_mark(rise, k[q], v[q], A, nxt);
                 cand_stage(nw, k[q], v[q], S, A, nxt);
             }
         }
