@@ -1773,6 +1773,11 @@ struct gd_batch {
     DBuf<int64_t> tail_state;
     int64_t tail_p = 1 << 14, tail_f = 1 << 13, tail_cap = 0;
     bool tail_on = false;            // (off for good after a list overflow)
+    // two residual sets (see batch_run): r / secmap and r_alt / secmap_alt
+    bool dbuf = false;
+    DBuf<double> r_alt;
+    DBuf<uint32_t> secmap_alt;
+    cudaEvent_t ev_rs[2] = {nullptr, nullptr};  // set s reset on the second stream
     bool trace = false;              // GDIFF_WAVE_TRACE: per-wave timeline to stderr
     bool serial = false;             // GDIFF_WAVE_SERIAL: no second stream
     bool ext_bal = false;            // work-balanced x extraction
@@ -1783,6 +1788,7 @@ struct gd_batch {
     ~gd_batch() {
         for (auto e : tev) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
+        for (auto e : ev_rs) if (e) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
         if (aux) cudaStreamDestroy(aux);
         for (auto w : workers) exact_worker_destroy(w);
@@ -1938,12 +1944,26 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaStreamCreateWithFlags(&B->aux, cudaStreamNonBlocking));
         GD_CUDA(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
         GD_CUDA(cudaEventCreateWithFlags(&B->ev_join, cudaEventDisableTiming));
+        GD_CUDA(cudaEventCreateWithFlags(&B->ev_rs[0], cudaEventDisableTiming));
+        GD_CUDA(cudaEventCreateWithFlags(&B->ev_rs[1], cudaEventDisableTiming));
     }
+    // two residual sets (dbuf): wave w runs on set w & 1 while wave w-1's set
+    // is reset on the second stream beside wave w's CTA-local tail and x
+    // extraction -- the part of a wave that leaves most SMs idle (the
+    // cooperative round kernel itself leaves no room for another kernel)
+    const bool dbuf = B->dbuf && !rpp && !B->hk && !B->stream;
+    int64_t m_prev = 0;
     for (int64_t w = 0; w < waves && !B->stream; ++w) {
         const int64_t base = w * B->slots;
         RoundArgs A = B->args();
         A.m = n_seeds - base < B->slots ? n_seeds - base : B->slots;
         A.seed_base = base;
+        const int set = dbuf ? (int)(w & 1) : 0;
+        if (dbuf) {
+            A.r = set ? B->r_alt.p : B->r.p;
+            A.secmap = set ? B->secmap_alt.p : B->secmap.p;
+            if (w >= 2) GD_CUDA(cudaStreamWaitEvent(st, B->ev_rs[set], 0));  // set is clean
+        }
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
         GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
         GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
@@ -1957,6 +1977,17 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
         GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
                                             stage_bytes(B->slots), st));
+        if (dbuf && w >= 1) {  // wave w-1's set, beside this wave's tail and extraction
+            RoundArgs Ap = A;
+            Ap.r = set ? B->r.p : B->r_alt.p;
+            Ap.secmap = set ? B->secmap.p : B->secmap_alt.p;
+            Ap.m = m_prev;
+            GD_CUDA(cudaEventRecord(B->ev_fork, st));
+            GD_CUDA(cudaStreamWaitEvent(B->aux, B->ev_fork, 0));
+            wave_reset(Ap, B->reset_chunks(), B->aux);
+            GD_CUDA(cudaEventRecord(B->ev_rs[set ^ 1], B->aux));
+            launches += 1;
+        }
         if (B->tail_on && !B->hk) {
             k_tail<<<(unsigned)A.m, BT, 0, st>>>(A);
             launches += 1;
@@ -1966,6 +1997,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         // (sector stores: bandwidth-bound) concurrently on a second stream;
         // they touch disjoint data.  The next wave waits for both.
         const cudaStream_t tst = B->serial ? st : B->aux;
+        if (!dbuf) {
         GD_CUDA(cudaEventRecord(B->ev_fork, st));
         GD_CUDA(cudaStreamWaitEvent(tst, B->ev_fork, 0));
         if (rpp)  // the r extraction zeroes the slots' r itself
@@ -1980,6 +2012,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             A2.secmap = A.secmap2;
             wave_reset(A2, B->reset_chunks(), tst);
         }
+        }
         if (B->trace && B->serial) GD_CUDA(cudaEventRecord(B->tev[2 * w + 1], st));
         if (B->ext_bal && A.m <= EXB_MAX_SLOTS)
             k_wave_extract_bal<<<B->ext_blocks, 256, 0, st>>>(A, O, base);
@@ -1989,11 +2022,25 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             GD_CUDA(cudaEventRecord(B->tev[2 * w], st));
             if (!B->serial) GD_CUDA(cudaEventRecord(B->tev[2 * w + 1], tst));
         }
-        GD_CUDA(cudaEventRecord(B->ev_join, tst));
-        GD_CUDA(cudaStreamWaitEvent(st, B->ev_join, 0));
+        if (!dbuf) {
+            GD_CUDA(cudaEventRecord(B->ev_join, tst));
+            GD_CUDA(cudaStreamWaitEvent(st, B->ev_join, 0));
+        }
         GD_LAUNCH_CHECK();
-        launches += B->hk ? 5 : 4;
+        launches += B->hk ? 5 : (dbuf ? 3 : 4);
         B->hs_wave(w, waves, st);
+        m_prev = A.m;
+    }
+    if (dbuf && waves > 0) {  // both sets clean on return: the last wave's here,
+        RoundArgs A = B->args();  // the one before on the second stream
+        const int set = (int)((waves - 1) & 1);
+        A.r = set ? B->r_alt.p : B->r.p;
+        A.secmap = set ? B->secmap_alt.p : B->secmap.p;
+        A.m = m_prev;
+        wave_reset(A, B->reset_chunks(), st);
+        if (waves >= 2) GD_CUDA(cudaStreamWaitEvent(st, B->ev_rs[set ^ 1], 0));
+        GD_LAUNCH_CHECK();
+        launches += 1;
     }
     GD_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
@@ -2527,6 +2574,23 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
             B->smw = (ld / 4 + 31) / 32;  // one bit per 4 doubles (32 B sector)
             B->secmap.alloc((size_t)slots * (size_t)B->smw);
             GD_CUDA(cudaMemset(B->secmap.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
+            {   // second residual set: when it costs no slots (slots not bound by
+                // memory) and 8 GB stay free (GDIFF_DBUF=0: off)
+                const char *e = getenv("GDIFF_DBUF");
+                bool want = !B->hk && !p->want_r && !(e && atoi(e) == 0);
+                if (want && p->slots <= 0 && slots < 64) want = false;
+                size_t fr = 0, tot = 0;
+                GD_CUDA(cudaMemGetInfo(&fr, &tot));
+                const size_t need = sn * sizeof(double) + (size_t)slots * B->smw * 4;
+                if (want && fr > need + (8ULL << 30)) {
+                    B->r_alt.alloc(sn);
+                    GD_CUDA(cudaMemset(B->r_alt.p, 0, sizeof(double) * sn));
+                    B->secmap_alt.alloc((size_t)slots * (size_t)B->smw);
+                    GD_CUDA(cudaMemset(B->secmap_alt.p, 0,
+                                       sizeof(uint32_t) * (size_t)slots * (size_t)B->smw));
+                    B->dbuf = true;
+                }
+            }
             if (B->hk) {
                 B->r2.alloc(sn);
                 GD_CUDA(cudaMemset(B->r2.p, 0, sizeof(double) * sn));
