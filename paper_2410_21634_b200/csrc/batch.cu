@@ -1239,9 +1239,31 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
 }
 
 // Seeds -> slots: r[s] = alpha, S_0 = {s} if alpha >= theta_s.
-__global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, double alpha) {
+// One block (zero_ctrs, m <= blockDim.x * 8): also zeroes the wave's round
+// counters first -- the frontier counters, per-group counts, near-list counters
+// and the tail hand-over -- instead of four memset launches per wave.
+__device__ void wave_init_slot(const RoundArgs &A, const int64_t *__restrict__ seeds,
+                               double alpha, int64_t k);
+__global__ void k_wave_init(RoundArgs A, const int64_t *__restrict__ seeds, double alpha,
+                            int zero_ctrs, int64_t scnt_n) {
+    if (zero_ctrs) {
+        for (int64_t i = threadIdx.x; i < scnt_n; i += blockDim.x) A.scnt[0][i] = 0ULL;
+        if (threadIdx.x < 2) {
+            A.fctr[threadIdx.x] = 0ULL;
+            *A.nearl.cnt[threadIdx.x] = 0ULL;
+            if (A.tail_state) A.tail_state[threadIdx.x] = -1;
+        }
+        __syncthreads();
+        for (int64_t k = threadIdx.x; k < A.m; k += blockDim.x) wave_init_slot(A, seeds, alpha, k);
+        return;
+    }
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= A.m) return;
+    wave_init_slot(A, seeds, alpha, k);
+}
+
+__device__ void wave_init_slot(const RoundArgs &A, const int64_t *__restrict__ seeds,
+                               double alpha, int64_t k) {
     int32_t s = (int32_t)seeds[k];
     if (A.perm) s = A.perm[s];
     A.seed[k] = s;
@@ -1909,7 +1931,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
         GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
         GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
-        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds, B->p.alpha);
+        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds, B->p.alpha, 0, 0);
         GD_LAUNCH_CHECK();
         launches += 1;
         for (int64_t w = 0; w < waves; ++w) {
@@ -1964,14 +1986,18 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             A.secmap = set ? B->secmap_alt.p : B->secmap.p;
             if (w >= 2) GD_CUDA(cudaStreamWaitEvent(st, B->ev_rs[set], 0));  // set is clean
         }
-        GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
-        GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
-        GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
-        k_wave_init<<<(int)((A.m + 255) / 256), 256, 0, st>>>(A, d_seeds + base,
-                                                               B->hk ? 1.0 : B->p.alpha);
+        const bool one = A.m <= 8 * 1024;  // init + counter zeroing in one block
+        if (!one) {
+            GD_CUDA(cudaMemsetAsync(B->fctr.p, 0, 2 * sizeof(unsigned long long), st));
+            GD_CUDA(cudaMemsetAsync(B->scnt.p, 0, 2 * sizeof(unsigned long long) * B->slots, st));
+            GD_CUDA(cudaMemsetAsync(B->nearcnt.p, 0, 2 * sizeof(unsigned long long), st));
+            if (B->tail_on && !B->hk)  // (-1: no tail handed over)
+                GD_CUDA(cudaMemsetAsync(B->tail_state.p, 0xFF, 2 * sizeof(int64_t), st));
+        }
+        A.tail_state = (B->tail_on && !B->hk) ? B->tail_state.p : nullptr;
+        k_wave_init<<<one ? 1 : (int)((A.m + 255) / 256), 256, 0, st>>>(
+            A, d_seeds + base, B->hk ? 1.0 : B->p.alpha, one ? 1 : 0, 2 * (int64_t)B->slots);
         GD_LAUNCH_CHECK();
-        if (B->tail_on && !B->hk)  // (-1: no tail handed over)
-            GD_CUDA(cudaMemsetAsync(B->tail_state.p, 0xFF, 2 * sizeof(int64_t), st));
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A, &O};
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
