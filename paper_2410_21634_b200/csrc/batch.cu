@@ -195,6 +195,13 @@ struct RoundArgs {
     // (2 x n per slot), c_u in tail_c (n per slot)
     int64_t tail_p, tail_f, tail_cap;
     int32_t *tail_list;
+    // heat kernel, dense stages (hk_pull_*): c_u per (node, slot), node-major
+    // (n x m), and the prefix of nodes with >= HEAVY_DEG arcs (degree-sorted ids)
+    double *cn;
+    int64_t heavy;
+    const int64_t *hitem;  // heavy-row segments: (node << 20) | segment
+    int64_t hitems;
+    double *hacc;          // heavy (node, slot) partial sums, node-major
     double *tail_c;
     int64_t *tail_state;
 };
@@ -254,8 +261,17 @@ __device__ __forceinline__ void frontier_append(bool flag, int32_t k, int32_t v,
         } else {
             A.overflow[0] = 1;
         }
-        if (A.grouped)
-            atomicAdd(A.scnt[nxt] + k / A.sgroup, (1ULL << CNT_SHIFT) + (unsigned long long)d);
+    }
+    if (A.grouped) {  // per slot group (entries, arcs): one atomic per group present
+        const int32_t g = flag ? k / (int32_t)A.sgroup : -1;
+        const unsigned peers = __match_any_sync(FULL, g);
+        unsigned long long pv = flag ? (1ULL << CNT_SHIFT) + (unsigned long long)d : 0ULL;
+        unsigned long long sum = 0;
+        for (int i = 0; i < 32; ++i) {
+            const unsigned long long vi = __shfl_sync(FULL, pv, i);
+            if ((peers >> i) & 1u) sum += vi;
+        }
+        if (flag && lane == __ffs(peers) - 1) atomicAdd(A.scnt[nxt] + g, sum);
     }
 }
 
@@ -718,6 +734,204 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
     }
 }
 
+// ---------------------------------------------------------------------------
+// Heat kernel, dense stages.  At tau = 10 on the products shape every stage
+// after the third covers all of every slot's arcs (profiles: 3.46 G arcs per
+// round for 28 slots); the push then does 3.46 G returning atomics per stage.
+// A dense stage instead (a) pushes every active (slot, node) -- r >= theta in
+// the stage layer, the same test the frontier entries passed -- and writes
+// c_u = fl(fl(r tau/(k+1)) fl(1/d_u)) (0 when inactive) into a node-major
+// n x m array, then (b) PULLS: r_next[k][v] = sum over the arcs (v, u) of
+// c[u][k], the m slots of a row in chunks of HKC registers, warp per node for
+// the degree-sorted heavy prefix, lane per node after it; the row sum is the
+// final value, so the threshold test, the near-threshold check and the next
+// frontier need no atomics.  Same c values as the push, summed in another
+// order (x to rounding; integer work identical up to the near-threshold
+// detector, as for the atomic scatter).
+constexpr int HKC = 8;          // slots per accumulator chunk
+constexpr int HEAVY_DEG = 256;  // rows split into segments at or above this degree
+constexpr int HSEG = 2048;      // arcs per heavy-row segment
+
+__device__ __forceinline__ void hk_dense_push(const RoundArgs &A, const Stage &S, double *rc,
+                                              int32_t t) {
+    const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * BT;
+    const int lane = threadIdx.x & 31;
+    const double w = t < A.n_stages ? A.stage_w[t] : 0.0;  // (the last stage absorbs)
+    for (int64_t u0 = gtid - lane; u0 < A.n; u0 += nthreads) {  // lane = node (warp-uniform trips)
+        const int32_t u = (int32_t)(u0 + lane);
+        const bool live = u < A.n;
+        const int32_t d = live ? A.g.deg[u] : 0;
+        const double th = theta_deg(A.tcoeff, d);
+        for (int32_t k = 0; k < (int32_t)A.m; ++k) {
+            const int64_t idx = (int64_t)k * A.ld + u;
+            const double val = live ? rc[idx] : 0.0;
+            const bool act = live && val >= th;
+            bool fresh = false;
+            double c = 0.0;
+            if (act) {
+                const double xo = A.x[idx];
+                A.x[idx] = __dadd_rn(xo, val);
+                rc[idx] = 0.0;
+                if (near_theta(val, th)) A.s_amb[k] = 1;  // final r >= theta
+                c = __dmul_rn(__dmul_rn(val, w), __ddiv_rn(1.0, (double)d));
+                fresh = __double_as_longlong(xo) == 0;
+                A.s_last[k] = t;
+            }
+            if (live) A.cn[(int64_t)u * A.m + k] = c;
+            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
+            block_count(act, k, (unsigned)d, S.ops);
+            block_count(act, k, 1u, S.push);
+        }
+    }
+}
+
+// (slot k, node v) of a dense stage: its final value val of layer t+1
+// same_word: all lanes hold the same slot and 32 consecutive nodes of one
+// 128-node block, so the sector marks of the warp go into one map word
+// append: write the next frontier's entries; else only count them (entries,
+// arcs) in cnt[0..1] (shared): the next stage then runs densely without a list
+__device__ __forceinline__ void hk_pull_finish(bool live, int32_t k, int32_t v, int32_t dv,
+                                               double val, const RoundArgs &A, const Stage &S,
+                                               double *rn, uint32_t *mapn, int nxt,
+                                               bool same_word, bool append,
+                                               unsigned long long *cnt) {
+    const double th = theta_deg(A.tcoeff, dv);
+    const bool nz = live && val != 0.0;
+    if (nz) {
+        rn[(int64_t)k * A.ld + v] = val;  // (the layer is zero here)
+        if (below_theta(val, th)) A.s_amb[k] = 1;
+    }
+    if (same_word) {
+        const unsigned bits = __reduce_or_sync(FULL, nz ? 1u << ((v >> 2) & 31) : 0u);
+        const unsigned any = __ballot_sync(FULL, nz);
+        if (bits && (threadIdx.x & 31) == __ffs(any) - 1)
+            atomicOr(mapn + (int64_t)k * A.smw + (v >> 7), bits);
+    } else if (nz) {
+        atomicOr(mapn + (int64_t)k * A.smw + (v >> 7), 1u << ((v >> 2) & 31));
+    }
+    const bool cross = nz && val >= th;
+    if (append) {
+        stage_append(cross, k, v, dv, S, A, nxt);
+    } else {
+        const unsigned cm = __ballot_sync(FULL, cross);
+        const unsigned long long ds = __reduce_add_sync(FULL, cross ? (unsigned)dv : 0u);
+        if (cm && (threadIdx.x & 31) == 0) {
+            atomicAdd(cnt, (unsigned long long)__popc(cm));
+            atomicAdd(cnt + 1, ds);
+        }
+    }
+}
+
+__device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t *mapn, int nxt,
+                        int64_t swarp, int64_t nwarps, bool append) {
+    __shared__ unsigned long long cnt[2];
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0ULL;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t m = A.m;
+    // heavy prefix: rows cut into segments of HSEG arcs, one warp per segment,
+    // lanes split it; the warp-reduced partial sums go into hacc (node, slot)
+    // with fp64 adds; after a grid barrier every heavy (node, slot) is finished
+    // from hacc (which is cleared for the next dense stage)
+    for (int64_t it = swarp; it < A.hitems; it += nwarps) {
+        const int64_t key = A.hitem[it];
+        const int64_t v = key >> 20, sg = key & 0xfffff;
+        const int64_t row = A.g.row[v];
+        const int32_t d = A.g.deg[v];
+        const int32_t j0 = (int32_t)(sg * HSEG), j1 = min(d, (int32_t)(j0 + HSEG));
+        for (int64_t k0 = 0; k0 < m; k0 += HKC) {
+            double acc[HKC];
+#pragma unroll
+            for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
+            for (int32_t j = j0 + lane; j < j1; j += 32) {
+                const int32_t u = __ldg(A.colp + row + j).x;
+                const double *cu = A.cn + (int64_t)u * m + k0;
+#pragma unroll
+                for (int q = 0; q < HKC; ++q)
+                    if (k0 + q < m) acc[q] += cu[q];
+            }
+#pragma unroll
+            for (int q = 0; q < HKC; ++q)
+                for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(FULL, acc[q], o);
+            double mine = 0.0;
+#pragma unroll
+            for (int q = 0; q < HKC; ++q)
+                if (lane == q) mine = acc[q];
+            if (lane < HKC && k0 + lane < m && mine != 0.0)
+                atomicAdd(A.hacc + v * m + k0 + lane, mine);
+        }
+    }
+    // light nodes: one lane per node (32 consecutive, similar degrees)
+    const int64_t lo = (A.heavy + 31) & ~31LL;
+    for (int64_t v = A.heavy + swarp; v < lo && v < A.n; v += nwarps)  // (up to the 32-aligned start)
+        for (int64_t k0 = 0; k0 < m; k0 += HKC) {
+            const int64_t row = A.g.row[v];
+            const int32_t d = A.g.deg[v];
+            double acc[HKC];
+#pragma unroll
+            for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
+            for (int32_t j = lane; j < d; j += 32) {
+                const int32_t u = __ldg(A.colp + row + j).x;
+                const double *cu = A.cn + (int64_t)u * m + k0;
+#pragma unroll
+                for (int q = 0; q < HKC; ++q)
+                    if (k0 + q < m) acc[q] += cu[q];
+            }
+#pragma unroll
+            for (int q = 0; q < HKC; ++q)
+                for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(FULL, acc[q], o);
+            double mine = 0.0;
+#pragma unroll
+            for (int q = 0; q < HKC; ++q)
+                if (lane == q) mine = acc[q];
+            hk_pull_finish(lane < HKC && k0 + lane < m, (int32_t)(k0 + lane), (int32_t)v, d,
+                           mine, A, S, rn, mapn, nxt, false, append, cnt);
+        }
+    for (int64_t v0 = lo + swarp * 32; v0 < A.n; v0 += nwarps * 32) {
+        const int64_t v = v0 + lane;
+        const bool live = v < A.n;
+        const int64_t row = live ? A.g.row[v] : 0;
+        const int32_t d = live ? A.g.deg[v] : 0;
+        for (int64_t k0 = 0; k0 < m; k0 += HKC) {
+            double acc[HKC];
+#pragma unroll
+            for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
+            for (int32_t j = 0; j < d; ++j) {
+                const int32_t u = __ldg(A.colp + row + j).x;
+                const double *cu = A.cn + (int64_t)u * m + k0;
+#pragma unroll
+                for (int q = 0; q < HKC; ++q)
+                    if (k0 + q < m) acc[q] += cu[q];
+            }
+#pragma unroll
+            for (int q = 0; q < HKC; ++q)
+                hk_pull_finish(live && k0 + q < m, (int32_t)(k0 + q), (int32_t)v, d, acc[q], A, S,
+                               rn, mapn, nxt, true, append, cnt);
+        }
+    }
+    cg::this_grid().sync();  // (every heavy partial sum is in hacc)
+    const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * BT;
+    const int64_t hm = A.heavy * m;
+    for (int64_t i0 = gtid - lane; i0 < hm; i0 += nthreads) {  // (warp-uniform trips)
+        const int64_t i = i0 + lane;
+        const bool live = i < hm;
+        const int64_t v = live ? i / m : 0;
+        const int32_t k = live ? (int32_t)(i - v * m) : 0;
+        double val = 0.0;
+        if (live) {
+            val = A.hacc[i];
+            A.hacc[i] = 0.0;
+        }
+        hk_pull_finish(live, k, (int32_t)v, live ? A.g.deg[v] : 0, val, A, S, rn, mapn, nxt,
+                       false, append, cnt);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt[0])  // (counted, not listed: the next stage is dense)
+        atomicAdd(A.fctr + nxt, (cnt[0] << CNT_SHIFT) + cnt[1]);
+}
+
 template <bool HK, bool STREAM = false>
 __global__ void __launch_bounds__(BT, GD_KR_MINB)
     k_rounds(const __grid_constant__ RoundArgs A, const __grid_constant__ OutArgs O) {
@@ -745,6 +959,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
     __syncthreads();
 
     bool tail = false;
+    bool nolist = false;  // (heat kernel) the current stage's frontier was only counted
     int64_t pmax = 0;  // largest round so far (the same in every block)
     for (int32_t t = STREAM ? *A.t_state : 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
@@ -878,9 +1093,18 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
         }
         // group this round only when it is large enough to be L2-bound (small
         // rounds are barrier-bound and keep the append order)
-        const bool grp = A.grouped && P >= A.group_min;
+        // heat kernel: a stage whose frontier covers at least half of every slot's
+        // arcs is run densely -- push every active (slot, node) here, then a PULL
+        // SpMM over all nodes in phase B (no atomics; see hk_pull_node)
+        // (nolist: the previous dense stage only counted its crossings, so this one
+        // is dense too; a dense stage lists them only below 3/4 density)
+        const bool dense = HK && A.cn && (nolist || (t < A.n_stages && 2 * P >= A.m * A.g.n_arcs));
+        const bool dense_pull = dense && t < A.n_stages;
+        const bool list_next = !(dense_pull && 4 * P >= 3 * A.m * A.g.n_arcs);
+        const bool grp = !dense && A.grouped && P >= A.group_min;
         if (grp) slot_bases(S, A, cur);
-        for (int64_t e0 = gtid - lane; e0 < F; e0 += nthreads) {  // warp-uniform trip count
+        if (dense) hk_dense_push(A, S, rc, t);
+        for (int64_t e0 = gtid - lane; e0 < (dense ? 0 : F); e0 += nthreads) {  // warp-uniform
             const int64_t e = e0 + lane;
             const bool live = e < F;
             int32_t k = 0, u = 0, d = 0;
@@ -1145,7 +1369,8 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
         }
         const int64_t C = (P + 31) >> 5;
         const int64_t *fa = A.sarc;
-        if (!HK || t < A.n_stages) {  // (the last heat-kernel stage is absorbing)
+        if (dense_pull) hk_pull(A, S, rn, mapn, nxt, swarp, nwarps, list_next);
+        else if (!dense && (!HK || t < A.n_stages)) {  // (the last heat-kernel stage is absorbing)
             const int64_t c1 = C;
           for (;;) {
             // block b owns super-chunks b, b + G, b + 2G, ... (SUPER groups of
@@ -1226,6 +1451,7 @@ __global__ void __launch_bounds__(BT, GD_KR_MINB)
           }
         }
         stage_flush(S, A, nxt);  // (its barriers also order the claim counter reset)
+        nolist = dense_pull && !list_next;
         if (threadIdx.x == 0) *S.next = 0;
         counters_flush(S.touch, A.touched, A.m);
         counters_flush(S.negz, A.s_negz, A.m);
@@ -1660,6 +1886,11 @@ struct gd_batch {
         return RPool{roff.p, rcnt.p, rnodes.p, rvals.p, rcap, rcursor.p, rscratch.p};
     }
     DBuf<double> r2, stage_w;  // (heat kernel) second residual layer, tau/(k+1)
+    DBuf<double> cn;           // (heat kernel) dense stages: c per (node, slot)
+    int64_t heavy = 0;         //   nodes with >= HEAVY_DEG arcs (degree-sorted prefix)
+    DBuf<int64_t> hitem;       //   their row segments
+    int64_t hitems = 0;
+    DBuf<double> hacc;         //   partial sums per (heavy node, slot)
     DBuf<uint32_t> secmap2;
     // results
     DBuf<int64_t> sweeps, ops, pushes, support, xoff, xcnt;
@@ -1739,6 +1970,11 @@ struct gd_batch {
             }
         }
         A.dbg = dbg;
+        A.cn = cn.p;
+        A.heavy = heavy;
+        A.hitem = hitem.p;
+        A.hitems = hitems;
+        A.hacc = hacc.p;
         if (tail_list.p && tail_on) {
             A.tail_list = tail_list.p;
             A.tail_cap = tail_cap;
@@ -2618,6 +2854,35 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                 }
             }
             if (B->hk) {
+                // dense stages (hk_pull): c per (node, slot), when it fits (GDIFF_HK_PULL=0: off)
+                const char *e = getenv("GDIFF_HK_PULL");
+                size_t fr = 0, tot = 0;
+                GD_CUDA(cudaMemGetInfo(&fr, &tot));
+                if (!(e && atoi(e) == 0) && fr > sn * 8 + (8ULL << 30)) {
+                    B->cn.alloc(sn);
+                    // heavy prefix: nodes with >= HEAVY_DEG arcs (ids sorted by degree
+                    // when relabeled; otherwise none: lane per node everywhere)
+                    if (B->R) {
+                        std::vector<int32_t> deg((size_t)n);
+                        GD_CUDA(cudaMemcpy(deg.data(), B->work()->view().deg, sizeof(int32_t) * n,
+                                           cudaMemcpyDeviceToHost));
+                        int64_t h = 0;
+                        while (h < n && deg[(size_t)h] >= HEAVY_DEG) ++h;
+                        B->heavy = h;
+                        std::vector<int64_t> items;
+                        for (int64_t v = 0; v < h; ++v)
+                            for (int64_t sg = 0; sg * HSEG < deg[(size_t)v]; ++sg)
+                                items.push_back((v << 20) | sg);
+                        B->hitem.alloc(items.size() ? items.size() : 1);
+                        if (!items.empty())
+                            GD_CUDA(cudaMemcpy(B->hitem.p, items.data(), 8 * items.size(),
+                                               cudaMemcpyHostToDevice));
+                        B->hitems = (int64_t)items.size();
+                        B->hacc.alloc((size_t)(h ? h : 1) * (size_t)slots);
+                        GD_CUDA(cudaMemset(B->hacc.p, 0, sizeof(double) * (size_t)(h ? h : 1) *
+                                                             (size_t)slots));
+                    }
+                }
                 B->r2.alloc(sn);
                 GD_CUDA(cudaMemset(B->r2.p, 0, sizeof(double) * sn));
                 B->secmap2.alloc((size_t)slots * (size_t)B->smw);
