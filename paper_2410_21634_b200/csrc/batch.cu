@@ -112,6 +112,12 @@ constexpr int BT = 512;   // threads per block of the round kernel
 #ifndef GD_KR_MINB
 #define GD_KR_MINB 2  // resident round-kernel blocks per SM (register budget)
 #endif
+#ifndef GD_KR_MINB_HK
+#define GD_KR_MINB_HK 1  // (heat kernel: one block per SM, registers for the pull's HKC sums)
+#endif
+#ifndef GD_HKC
+#define GD_HKC 14
+#endif
 constexpr int UNROLL = 4; // 32-arc chunks in flight per warp in phase B
 constexpr int SUPER = 16; // UNROLL-chunk groups per block super-chunk in phase B
 constexpr int CNT_SHIFT = 36;
@@ -748,7 +754,7 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
 // frontier need no atomics.  Same c values as the push, summed in another
 // order (x to rounding; integer work identical up to the near-threshold
 // detector, as for the atomic scatter).
-constexpr int HKC = 8;          // slots per accumulator chunk
+constexpr int HKC = GD_HKC;     // slots per accumulator chunk
 constexpr int HEAVY_DEG = 256;  // rows split into segments at or above this degree
 constexpr int HSEG = 2048;      // arcs per heavy-row segment
 
@@ -933,7 +939,7 @@ __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t
 }
 
 template <bool HK, bool STREAM = false>
-__global__ void __launch_bounds__(BT, GD_KR_MINB)
+__global__ void __launch_bounds__(BT, HK ? GD_KR_MINB_HK : GD_KR_MINB)
     k_rounds(const __grid_constant__ RoundArgs A, const __grid_constant__ OutArgs O) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
