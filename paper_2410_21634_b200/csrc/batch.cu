@@ -204,7 +204,7 @@ struct RoundArgs {
     // heat kernel, dense stages (hk_pull_*): c_u per (node, slot), node-major
     // (n x m), and the prefix of nodes with >= HEAVY_DEG arcs (degree-sorted ids)
     double *cn;
-    int64_t heavy;
+    int64_t heavy, mid;    //   mid: nodes with >= MEDIUM_DEG arcs (heavy included)
     const int64_t *hitem;  // heavy-row segments: (node << 20) | segment
     int64_t hitems;
     double *hacc;          // heavy (node, slot) partial sums, node-major
@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
 constexpr int HKC = GD_HKC;     // slots per accumulator chunk
 constexpr int HEAVY_DEG = 256;  // rows split into segments at or above this degree
 constexpr int HSEG = 2048;      // arcs per heavy-row segment
+constexpr int MEDIUM_DEG = 32;  // warp per node at or above this degree
 
 __device__ __forceinline__ void hk_dense_push(const RoundArgs &A, const Stage &S, double *rc,
                                               int32_t t) {
@@ -868,9 +869,11 @@ __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t
                 atomicAdd(A.hacc + v * m + k0 + lane, mine);
         }
     }
-    // light nodes: one lane per node (32 consecutive, similar degrees)
-    const int64_t lo = (A.heavy + 31) & ~31LL;
-    for (int64_t v = A.heavy + swarp; v < lo && v < A.n; v += nwarps)  // (up to the 32-aligned start)
+    // medium nodes (>= MEDIUM_DEG arcs) and the few up to the next multiple of 32:
+    // one warp per node; light nodes: one lane per node (32 consecutive ids,
+    // similar degrees) -- so no lane walks a row of more than MEDIUM_DEG arcs
+    const int64_t lo = (A.mid + 31) & ~31LL;
+    for (int64_t v = A.heavy + swarp; v < lo && v < A.n; v += nwarps)
         for (int64_t k0 = 0; k0 < m; k0 += HKC) {
             const int64_t row = A.g.row[v];
             const int32_t d = A.g.deg[v];
@@ -1894,6 +1897,7 @@ struct gd_batch {
     DBuf<double> r2, stage_w;  // (heat kernel) second residual layer, tau/(k+1)
     DBuf<double> cn;           // (heat kernel) dense stages: c per (node, slot)
     int64_t heavy = 0;         //   nodes with >= HEAVY_DEG arcs (degree-sorted prefix)
+    int64_t mid = 0;           //   ... with >= MEDIUM_DEG arcs
     DBuf<int64_t> hitem;       //   their row segments
     int64_t hitems = 0;
     DBuf<double> hacc;         //   partial sums per (heavy node, slot)
@@ -1978,6 +1982,7 @@ struct gd_batch {
         A.dbg = dbg;
         A.cn = cn.p;
         A.heavy = heavy;
+        A.mid = mid;
         A.hitem = hitem.p;
         A.hitems = hitems;
         A.hacc = hacc.p;
@@ -2875,6 +2880,9 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                         int64_t h = 0;
                         while (h < n && deg[(size_t)h] >= HEAVY_DEG) ++h;
                         B->heavy = h;
+                        int64_t md = h;
+                        while (md < n && deg[(size_t)md] >= MEDIUM_DEG) ++md;
+                        B->mid = md;
                         std::vector<int64_t> items;
                         for (int64_t v = 0; v < h; ++v)
                             for (int64_t sg = 0; sg * HSEG < deg[(size_t)v]; ++sg)
