@@ -786,9 +786,22 @@ __device__ __forceinline__ void hk_dense_push(const RoundArgs &A, const Stage &S
                 A.s_last[k] = t;
             }
             if (live) A.cn[(int64_t)u * A.m + k] = c;
-            slot_append(fresh, k, u, A.ld, A.pushed, A.pushed_cnt);
-            block_count(act, k, (unsigned)d, S.ops);
-            block_count(act, k, 1u, S.push);
+            // (k is the same in every lane: plain warp reductions, no slot matching)
+            const unsigned am = __ballot_sync(FULL, act);
+            if (am) {
+                const unsigned ds = __reduce_add_sync(FULL, act ? (unsigned)d : 0u);
+                if (lane == 0) {
+                    atomicAdd(S.ops + k, (unsigned long long)ds);
+                    atomicAdd(S.push + k, (unsigned)__popc(am));
+                }
+            }
+            const unsigned fm = __ballot_sync(FULL, fresh);
+            if (fm) {
+                unsigned long long b = 0;
+                if (lane == 0) b = atomicAdd(A.pushed_cnt + k, (unsigned long long)__popc(fm));
+                b = __shfl_sync(FULL, b, 0);
+                if (fresh) A.pushed[(int64_t)k * A.ld + (int64_t)b + __popc(fm & lanemask_lt())] = u;
+            }
         }
     }
 }
