@@ -639,7 +639,7 @@ def main():
                                                     "k_rounds (persistent sweep loop)",
                                     "local-ch": "k_signed_rounds (persistent signed sweep loop)",
                                     "local-hb": "k_signed_rounds (heavy-ball coefficients)",
-                                    "local-hk": "k_rounds<HK> (layered heat-kernel stage sweeps)",
+                                    "local-hk": "k_rounds<HK> (heat-kernel stages: dense ones as a pull SpMM)",
                                     "local-sor": "k_sor_win (exact windows, CTA per seed)" if win
                                                  else "k_fifo_batch (warp per seed)"}[args.method],
                          "kernel_ms_per_step": float(t[4]) / args.steps},

@@ -60,5 +60,13 @@ def b_alg_bytes(total_ops: int, pushes: int, method: str = "local-gd") -> int:
     52 B per pushed node (frontier id, row_ptr pair, r[u] rw, x[u] rw);
     LocalCH adds 24 B per push (momentum value + stamp), FIFO solvers 8 B.
     """
+    if method == "local-hk":
+        # heat kernel: its dense stages (>= 97 % of the operations at tau = 10,
+        # eps = 1e-7 on the benchmark graphs) run as a pull -- per arc and slot an
+        # 8 B gather of c[u][k] plus the 8 B (neighbour, degree) record once per
+        # 14-slot chunk; per push r read + write, x read + write, c write (40 B)
+        # and the pulled r_next write (8 B).  The few sparse stages are charged
+        # the same (fewer bytes than their push would move: conservative).
+        return int(8.6 * int(total_ops)) + 48 * int(pushes)
     per_push = 52 + (24 if method in ("local-ch", "local-hb") else 0) + (8 if method in ("local-sor", "local-gs") else 0)
     return 20 * int(total_ops) + per_push * int(pushes)
