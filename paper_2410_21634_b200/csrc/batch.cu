@@ -2206,12 +2206,6 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             B->hs_wave(w, waves, st);
         }
     }
-    B->trace = getenv("GDIFF_WAVE_TRACE") != nullptr;  // (diagnostics: per-wave timeline)
-    B->serial = getenv("GDIFF_WAVE_SERIAL") != nullptr;  // (A/B: reset after extract on st)
-    {   // GDIFF_EXTRACT_BAL=0: the per-slot extraction grid (A/B)
-        const char *e = getenv("GDIFF_EXTRACT_BAL");
-        B->ext_bal = !(e && atoi(e) == 0);
-    }
     if (!B->ext_blocks) {
         int per = 0;
         GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave_extract_bal, 256, 0));
@@ -2959,6 +2953,12 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
             if (const char *e = getenv("GDIFF_STREAM"))
                 B->stream = !B->hk && !B->want_r() && atoi(e) != 0;
             if (const char *e = getenv("GDIFF_COHORT")) B->cohort = atoll(e);  // (A/B)
+            B->trace = getenv("GDIFF_WAVE_TRACE") != nullptr;   // (diagnostics: per-wave timeline)
+            B->serial = getenv("GDIFF_WAVE_SERIAL") != nullptr; // (A/B: reset after extract on st)
+            {   // GDIFF_EXTRACT_BAL=0: the per-slot extraction grid (A/B)
+                const char *e = getenv("GDIFF_EXTRACT_BAL");
+                B->ext_bal = !(e && atoi(e) == 0);
+            }
             if (const char *e = getenv("GDIFF_DBG")) B->dbg = atoi(e);        // (experiments)
             if (B->stream) {
                 const void *sfn = (const void *)k_rounds<false, true>;
