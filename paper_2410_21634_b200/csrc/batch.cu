@@ -204,6 +204,7 @@ struct RoundArgs {
     // heat kernel, dense stages (hk_pull_*): c_u per (node, slot), node-major
     // (n x m), and the prefix of nodes with >= HEAVY_DEG arcs (degree-sorted ids)
     double *cn;
+    int tma;               //   stage the pull's arc records with bulk async copies
     int64_t heavy, mid;    //   mid: nodes with >= MEDIUM_DEG arcs (heavy included)
     const int64_t *hitem;  // heavy-row segments: (node << 20) | segment
     int64_t hitems;
@@ -756,8 +757,46 @@ __global__ void __launch_bounds__(BT, 2) k_tail(const __grid_constant__ RoundArg
 // detector, as for the atomic scatter).
 constexpr int HKC = GD_HKC;     // slots per accumulator chunk
 constexpr int HEAVY_DEG = 256;  // rows split into segments at or above this degree
-constexpr int HSEG = 2048;      // arcs per heavy-row segment
+constexpr int HSEG = 2048;      // arcs per heavy-row segment (HSEG_TMA when staged:
+constexpr int HSEG_TMA = 1024;  //  a segment fits a warp's TMA buffer)
 constexpr int MEDIUM_DEG = 32;  // warp per node at or above this degree
+
+// Bulk asynchronous copy (the TMA engine, cp.async.bulk) of the arc records
+// [a0, a1) of the pull into this warp's shared-memory buffer, completion on the
+// warp's mbarrier; returns the first staged index (a0 rounded down to 16 B).
+// The buffer holds TBUF records: every range passed here is shorter (light
+// warps: 32 rows of < MEDIUM_DEG arcs; medium rows < HEAVY_DEG; heavy segments
+// HSEG_TMA).  Records stay in shared memory for all the stage's slot chunks.
+constexpr int TBUF = 1026;       // int2 records per warp buffer (8 KB + 16 B)
+__host__ __device__ inline size_t tma_bytes() { return 16 + (BT / 32) * (8 + (size_t)TBUF * 8); }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ int64_t tma_stage(const int2 *colp, int64_t a0, int64_t a1, int2 *buf,
+                                             uint64_t *bar, uint32_t &ph) {
+    const int64_t s0 = a0 & ~1LL;
+    if (a1 <= a0) return s0;  // (warp-uniform: nothing to copy, no phase)
+    if (a1 - s0 + 1 > TBUF) return -1;  // (does not fit: the caller reads global memory)
+    const uint32_t bytes = (uint32_t)((((a1 - s0) * 8) + 15) & ~15LL);
+    __syncwarp();  // every lane is done with the previous contents
+    if ((threadIdx.x & 31) == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                     "[%0], [%1], %2, [%3];"
+                     :: "r"(smem_u32(buf)), "l"(colp + s0), "r"(bytes), "r"(smem_u32(bar))
+                     : "memory");
+    }
+    uint32_t ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                     "selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(ph) : "memory");
+    } while (!ok);
+    ph ^= 1;
+    return s0;
+}
 
 __device__ __forceinline__ void hk_dense_push(const RoundArgs &A, const Stage &S, double *rc,
                                               int32_t t) {
@@ -844,7 +883,8 @@ __device__ __forceinline__ void hk_pull_finish(bool live, int32_t k, int32_t v, 
 }
 
 __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t *mapn, int nxt,
-                        int64_t swarp, int64_t nwarps, bool append) {
+                        int64_t swarp, int64_t nwarps, bool append, int2 *tbuf, uint64_t *tbar,
+                        uint32_t &tph) {
     __shared__ unsigned long long cnt[2];
     if (threadIdx.x < 2) cnt[threadIdx.x] = 0ULL;
     __syncthreads();
@@ -859,13 +899,15 @@ __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t
         const int64_t v = key >> 20, sg = key & 0xfffff;
         const int64_t row = A.g.row[v];
         const int32_t d = A.g.deg[v];
-        const int32_t j0 = (int32_t)(sg * HSEG), j1 = min(d, (int32_t)(j0 + HSEG));
+        const int32_t hs = A.tma ? HSEG_TMA : HSEG;
+        const int32_t j0 = (int32_t)(sg * hs), j1 = min(d, (int32_t)(j0 + hs));
+        const int64_t sb = A.tma ? tma_stage(A.colp, row + j0, row + j1, tbuf, tbar, tph) : -1;
         for (int64_t k0 = 0; k0 < m; k0 += HKC) {
             double acc[HKC];
 #pragma unroll
             for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
             for (int32_t j = j0 + lane; j < j1; j += 32) {
-                const int32_t u = __ldg(A.colp + row + j).x;
+                const int32_t u = sb >= 0 ? tbuf[row + j - sb].x : __ldg(A.colp + row + j).x;
                 const double *cu = A.cn + (int64_t)u * m + k0;
 #pragma unroll
                 for (int q = 0; q < HKC; ++q)
@@ -886,15 +928,16 @@ __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t
     // one warp per node; light nodes: one lane per node (32 consecutive ids,
     // similar degrees) -- so no lane walks a row of more than MEDIUM_DEG arcs
     const int64_t lo = (A.mid + 31) & ~31LL;
-    for (int64_t v = A.heavy + swarp; v < lo && v < A.n; v += nwarps)
+    for (int64_t v = A.heavy + swarp; v < lo && v < A.n; v += nwarps) {
+        const int64_t row = A.g.row[v];
+        const int32_t d = A.g.deg[v];
+        const int64_t sb = A.tma ? tma_stage(A.colp, row, row + d, tbuf, tbar, tph) : -1;
         for (int64_t k0 = 0; k0 < m; k0 += HKC) {
-            const int64_t row = A.g.row[v];
-            const int32_t d = A.g.deg[v];
             double acc[HKC];
 #pragma unroll
             for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
             for (int32_t j = lane; j < d; j += 32) {
-                const int32_t u = __ldg(A.colp + row + j).x;
+                const int32_t u = sb >= 0 ? tbuf[row + j - sb].x : __ldg(A.colp + row + j).x;
                 const double *cu = A.cn + (int64_t)u * m + k0;
 #pragma unroll
                 for (int q = 0; q < HKC; ++q)
@@ -910,17 +953,22 @@ __device__ void hk_pull(const RoundArgs &A, const Stage &S, double *rn, uint32_t
             hk_pull_finish(lane < HKC && k0 + lane < m, (int32_t)(k0 + lane), (int32_t)v, d,
                            mine, A, S, rn, mapn, nxt, false, append, cnt);
         }
+    }
     for (int64_t v0 = lo + swarp * 32; v0 < A.n; v0 += nwarps * 32) {
         const int64_t v = v0 + lane;
         const bool live = v < A.n;
         const int64_t row = live ? A.g.row[v] : 0;
         const int32_t d = live ? A.g.deg[v] : 0;
+        // the 32 nodes' rows are one contiguous range of arc records
+        const int64_t sb = A.tma ? tma_stage(A.colp, A.g.row[v0], A.g.row[min(v0 + 32, A.n)], tbuf,
+                                             tbar, tph)
+                                 : -1;
         for (int64_t k0 = 0; k0 < m; k0 += HKC) {
             double acc[HKC];
 #pragma unroll
             for (int q = 0; q < HKC; ++q) acc[q] = 0.0;
             for (int32_t j = 0; j < d; ++j) {
-                const int32_t u = __ldg(A.colp + row + j).x;
+                const int32_t u = sb >= 0 ? tbuf[row + j - sb].x : __ldg(A.colp + row + j).x;
                 const double *cu = A.cn + (int64_t)u * m + k0;
 #pragma unroll
                 for (int q = 0; q < HKC; ++q)
@@ -960,6 +1008,16 @@ __global__ void __launch_bounds__(BT, HK ? GD_KR_MINB_HK : GD_KR_MINB)
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Stage S = stage_carve(smem_raw, (int)A.m);
+    // (heat kernel, A.tma) per warp: an mbarrier and a buffer for the pull's arc records
+    uint64_t *const tbars = reinterpret_cast<uint64_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + stage_bytes((int)A.m) + 15) & ~(uintptr_t)15);
+    int2 *const tbuf = reinterpret_cast<int2 *>(tbars + BT / 32) + (size_t)(threadIdx.x >> 5) * TBUF;
+    uint64_t *const tbar = tbars + (threadIdx.x >> 5);
+    uint32_t tph = 0;
+    if (HK && A.tma && (threadIdx.x & 31) == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(tbar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)BT + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * BT;
@@ -1391,7 +1449,7 @@ __global__ void __launch_bounds__(BT, HK ? GD_KR_MINB_HK : GD_KR_MINB)
         }
         const int64_t C = (P + 31) >> 5;
         const int64_t *fa = A.sarc;
-        if (dense_pull) hk_pull(A, S, rn, mapn, nxt, swarp, nwarps, list_next);
+        if (dense_pull) hk_pull(A, S, rn, mapn, nxt, swarp, nwarps, list_next, tbuf, tbar, tph);
         else if (!dense && (!HK || t < A.n_stages)) {  // (the last heat-kernel stage is absorbing)
             const int64_t c1 = C;
           for (;;) {
@@ -1909,6 +1967,9 @@ struct gd_batch {
     }
     DBuf<double> r2, stage_w;  // (heat kernel) second residual layer, tau/(k+1)
     DBuf<double> cn;           // (heat kernel) dense stages: c per (node, slot)
+    bool tma_on = false;       //   the pull stages its arc records by bulk async copy
+    size_t kr_smem = 0;        // dynamic shared memory of the round kernel
+    bool kr_tma() const { return hk && cn.p && tma_on; }
     int64_t heavy = 0;         //   nodes with >= HEAVY_DEG arcs (degree-sorted prefix)
     int64_t mid = 0;           //   ... with >= MEDIUM_DEG arcs
     DBuf<int64_t> hitem;       //   their row segments
@@ -1994,6 +2055,7 @@ struct gd_batch {
         }
         A.dbg = dbg;
         A.cn = cn.p;
+        A.tma = kr_tma() ? 1 : 0;
         A.heavy = heavy;
         A.mid = mid;
         A.hitem = hitem.p;
@@ -2255,8 +2317,7 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
         GD_CUDA(cudaEventRecord(B->ev[2 * w], st));
         void *kargs[] = {&A, &O};
         const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
-        GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs,
-                                            stage_bytes(B->slots), st));
+        GD_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(B->grid), dim3(BT), kargs, B->kr_smem, st));
         if (dbuf && w >= 1) {  // wave w-1's set, beside this wave's tail and extraction
             RoundArgs Ap = A;
             Ap.r = set ? B->r.p : B->r_alt.p;
@@ -2783,7 +2844,7 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                 *out = B;
                 return;
             }
-            B->colp.alloc(G->n_arcs ? G->n_arcs : 1);
+            B->colp.alloc(G->n_arcs + 2);  // (+2: bulk copies round their size up to 16 B)
             k_pack_cols<<<4 * n_sms(G->device), 256>>>(B->work()->view(), B->colp.p);
             GD_LAUNCH_CHECK();
             GD_CUDA(cudaDeviceSynchronize());
@@ -2878,6 +2939,11 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                 GD_CUDA(cudaMemGetInfo(&fr, &tot));
                 if (!(e && atoi(e) == 0) && fr > sn * 8 + (8ULL << 30)) {
                     B->cn.alloc(sn);
+                    const char *tm = getenv("GDIFF_HK_TMA");  // (A/B: 0 = plain loads)
+                    // staging pays when a stage re-reads the records for >= 3 slot chunks
+                    // (arxiv, 64 slots: +2 %; products, 28 slots in 2 chunks: -1 %)
+                    const bool reuse = (slots + HKC - 1) / HKC >= 3;
+                    B->tma_on = (tm ? atoi(tm) != 0 : reuse) && B->R;  // (degree-sorted ids)
                     // heavy prefix: nodes with >= HEAVY_DEG arcs (ids sorted by degree
                     // when relabeled; otherwise none: lane per node everywhere)
                     if (B->R) {
@@ -2892,7 +2958,8 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                         B->mid = md;
                         std::vector<int64_t> items;
                         for (int64_t v = 0; v < h; ++v)
-                            for (int64_t sg = 0; sg * HSEG < deg[(size_t)v]; ++sg)
+                            for (int64_t sg = 0; sg * (B->tma_on ? HSEG_TMA : HSEG) < deg[(size_t)v];
+                                 ++sg)
                                 items.push_back((v << 20) | sg);
                         B->hitem.alloc(items.size() ? items.size() : 1);
                         if (!items.empty())
@@ -2934,7 +3001,8 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                     if (const char *v = getenv("GDIFF_TAIL_F")) B->tail_f = atoll(v);
                 }
             }
-            const size_t smem = stage_bytes(slots);
+            const size_t smem = stage_bytes(slots) + (B->kr_tma() ? tma_bytes() : 0);
+            B->kr_smem = smem;
             const void *kfn = B->hk ? (const void *)k_rounds<true> : (const void *)k_rounds<false>;
             GD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
