@@ -28,6 +28,8 @@
 // l1 sits within rounding of the abort level.
 #include <cooperative_groups.h>
 
+#include <cub/block/block_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <unordered_map>
@@ -95,6 +97,13 @@ struct SArgs {
     int32_t *s_amb;  // per slot: a final |r| within AMB_REL of theta (common.cuh)
     NearList nearl;  // landings just below theta, re-checked after the round
     int32_t *overflow;
+    // CTA-local tail (k_s_tail): once a round has <= tail_f candidates past the
+    // wave's peak (or after 16 rounds), block k finishes slot k alone; lists of n
+    // entries per slot: candidates (two) and frontier entries, and their c
+    int32_t *tail_list;
+    double *tail_c;
+    int64_t tail_f;
+    int64_t *tail_state;  // round, candidates (-1: no tail)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt_s() {
@@ -366,6 +375,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
         *S.next = 0;
     }
     __syncthreads();
+    int64_t ncmax = 0;  // largest candidate round so far (the same in every block)
     for (int32_t t = 0;; ++t) {
         const int cur = t & 1, nxt = cur ^ 1;
         const int64_t NC = (int64_t)*(volatile unsigned long long *)(A.candctr + cur);
@@ -380,6 +390,14 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
             }
         }
         if (NC == 0) break;
+        ncmax = NC > ncmax ? NC : ncmax;
+        if (A.tail_list && NC <= A.tail_f && (16 * NC <= ncmax || t >= 16)) {
+            if (gtid == 0) {  // the rest of the wave in k_s_tail, one block per slot
+                A.tail_state[0] = t;
+                A.tail_state[1] = NC;
+            }
+            break;
+        }
         if (NC > A.candcap) {
             if (gtid == 0) A.overflow[0] = 1;
             break;
@@ -605,6 +623,261 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
             }
         grid.sync();
     }
+}
+
+// ---------------------------------------------------------------------------
+// k_s_tail: the CTA-local tail of a signed wave (LocalCH / LocalHB), the
+// counterpart of batch.cu's k_tail.  Katz waves on the products shape run ~100-
+// 240 rounds of a few hundred arcs per seed, where the cooperative round
+// kernel's three grid barriers per round are the whole cost.  Block k takes
+// slot k's candidates of round t and runs the remaining sweeps alone with the
+// same rules as k_signed_rounds: phase A filters candidates (|r| >= theta, not
+// diverged, sweep cap) and pushes them with the Chebyshev / heavy-ball
+// recurrence, keeping the momentum and the incremental l1; phase B scatters
+// the entries' arcs (block-balanced: degrees block-scanned per segment, binary
+// search per arc) with returning atomics, marks a candidate on a cold -> hot
+// transition, the sector map on first touch, landings just below theta for the
+// final check.  Sweeps stay numbered as rounds.
+constexpr int STAIL_SEG = 1024;
+constexpr int STAIL_NEAR = 256;
+constexpr int SUNROLL_T = 4;
+
+__global__ void __launch_bounds__(SBT, 1) k_s_tail(const __grid_constant__ SArgs A) {
+    using Scan = cub::BlockScan<int, SBT>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ double tc[STAIL_SEG];
+    __shared__ int64_t trow[STAIL_SEG];
+    __shared__ int32_t toff[STAIL_SEG + 1], tnear[STAIL_NEAR];
+    __shared__ int s_cur, s_nxt, s_ne, s_nn, s_amb;
+    __shared__ unsigned long long c_ops, c_push;
+    __shared__ double c_l1;
+    const int64_t NC = A.tail_state[1];
+    if (NC < 0) return;  // the wave ended in the round kernel
+    int32_t t = (int32_t)A.tail_state[0];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t k = (int32_t)blockIdx.x;
+    const int64_t C = A.g.n;
+    int32_t *const l0 = A.tail_list + (int64_t)k * 3 * C, *const l1 = l0 + C, *const eu = l1 + C;
+    double *const ec = A.tail_c + (int64_t)k * C;
+    const int64_t off = (int64_t)k * A.ld;
+    double *const r = A.r + off;
+    const bool ch = A.method == 1;
+    if (tid == 0) {
+        s_cur = s_nn = s_amb = 0;
+    }
+    __syncthreads();
+    for (int64_t e0 = 0; e0 < NC; e0 += SBT) {  // this slot's candidates of round t
+        const int64_t e = e0 + tid;
+        const int64_t key = e < NC ? A.cand[t & 1][e] : -1;
+        const bool mine = e < NC && (int32_t)(key >> 32) == k;
+        const unsigned am = __ballot_sync(SFULL, mine);
+        int base = 0;
+        if (am && lane == __ffs(am) - 1) base = atomicAdd(&s_cur, __popc(am));
+        base = __shfl_sync(SFULL, base, __ffs(am ? am : 1u) - 1);
+        if (mine) l0[base + __popc(am & lanemask_lt_s())] = (int32_t)(key & 0xffffffffLL);
+    }
+    int cur = 0;
+    __syncthreads();
+    for (;; ++t) {
+        const int par = t & 1, npar = par ^ 1;
+        const int nn = min(s_nn, STAIL_NEAR);
+        for (int i = tid; i < nn; i += SBT)
+            if (below_theta(fabs(r[tnear[i]]), theta_of(A.op, tnear[i], A.g.deg[tnear[i]])))
+                s_amb = 1;
+        __syncthreads();
+        const int Fc = s_cur;
+        if (Fc == 0) break;
+        if (tid == 0) {
+            s_nn = 0;
+            s_nxt = 0;
+            s_ne = 0;
+            c_ops = c_push = 0ULL;
+            c_l1 = 0.0;
+        }
+        __syncthreads();
+        int32_t *const cl = cur ? l1 : l0, *const nl = cur ? l0 : l1;
+        const bool div = slot_diverged(A, k);
+        const double cr = (ch && t > 0) ? A.coef_r[t] : 0.0;
+        const double cm = (ch && t > 0) ? A.coef_m[t] : 0.0;
+        // ---- phase A: candidates -> |r| >= theta ? push : skip
+        double my_l1 = 0.0;
+        for (int i0 = 0; i0 < Fc; i0 += SBT) {  // warp-uniform trips
+            const int i = i0 + tid;
+            const bool live = i < Fc;
+            bool act = false, fresh = false;
+            int32_t u = 0, d = 0;
+            double c = 0.0;
+            if (live) {
+                u = cl[i];
+                atomicAnd(A.cmark[par] + (int64_t)k * A.cmw + (u >> 5), ~(1u << (u & 31)));
+                const int64_t idx = off + u;
+                const double ru = A.r[idx];
+                d = A.g.deg[u];
+                const double th = theta_of(A.op, u, d);
+                if (near_theta(fabs(ru), th)) s_amb = 1;
+                act = fabs(ru) >= th && !div;
+                if (act && t >= A.max_sweeps) {  // sweep cap reached with work left
+                    A.s_conv[k] = 0;
+                    act = false;
+                }
+                if (act) {
+                    double v;
+                    if (!ch) {
+                        v = ru;
+                    } else if (t == 0) {
+                        v = __dmul_rn(A.step0, ru);
+                    } else {
+                        const double prev = (A.mstamp[idx] == t - 1) ? A.mom[idx] : 0.0;
+                        v = __dadd_rn(__dmul_rn(cr, ru), __dmul_rn(cm, prev));
+                    }
+                    A.x[idx] = __dadd_rn(A.x[idx], v);
+                    const double rn = __dsub_rn(ru, v);
+                    A.r[idx] = rn;
+                    if (ch) {
+                        my_l1 += fabs(rn) - fabs(ru);
+                        fresh = A.mstamp[idx] == -1;
+                        A.mom[idx] = v;
+                        A.mstamp[idx] = t;
+                    }
+                    c = __dmul_rn(v, node_weight(A.op, d));
+                    A.s_last[k] = t;
+                }
+            }
+            {   // pushed-node list (x support)
+                const unsigned fm = __ballot_sync(SFULL, fresh);
+                if (fm) {
+                    unsigned long long b = 0;
+                    if (lane == __ffs(fm) - 1)
+                        b = atomicAdd(A.pushed_cnt + k, (unsigned long long)__popc(fm));
+                    b = __shfl_sync(SFULL, b, __ffs(fm) - 1);
+                    if (fresh) A.pushed[off + (int64_t)b + __popc(fm & lanemask_lt_s())] = u;
+                }
+            }
+            {   // frontier entry (u, c) and the counters
+                const unsigned am = __ballot_sync(SFULL, act);
+                if (am) {
+                    int b = 0;
+                    if (lane == __ffs(am) - 1) b = atomicAdd(&s_ne, __popc(am));
+                    b = __shfl_sync(SFULL, b, __ffs(am) - 1);
+                    if (act) {
+                        const int at = b + __popc(am & lanemask_lt_s());
+                        eu[at] = u;
+                        ec[at] = c;
+                    }
+                    const unsigned ds = __reduce_add_sync(SFULL, act ? (unsigned)d : 0u);
+                    if (lane == __ffs(am) - 1) {
+                        atomicAdd(&c_ops, (unsigned long long)ds);
+                        atomicAdd(&c_push, (unsigned long long)__popc(am));
+                    }
+                }
+            }
+            {   // under momentum a pushed node keeps a residual: candidate again
+                const bool again = cand_mark(ch && act, k, u, A, npar);
+                const unsigned gm = __ballot_sync(SFULL, again);
+                if (gm) {
+                    int b = 0;
+                    if (lane == __ffs(gm) - 1) b = atomicAdd(&s_nxt, __popc(gm));
+                    b = __shfl_sync(SFULL, b, __ffs(gm) - 1);
+                    if (again) nl[b + __popc(gm & lanemask_lt_s())] = u;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- phase B: the entries' arcs
+        const int Fe = s_ne;
+        for (int seg0 = 0; seg0 < Fe; seg0 += STAIL_SEG) {
+            const int ns = min(STAIL_SEG, Fe - seg0);
+            constexpr int PER = STAIL_SEG / SBT;
+            int dd[PER];
+            int mine = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid * PER + j;
+                dd[j] = 0;
+                if (i < ns) {
+                    const int32_t u = eu[seg0 + i];
+                    dd[j] = A.g.deg[u];
+                    trow[i] = A.g.row[u];
+                    tc[i] = ec[seg0 + i];
+                }
+                mine += dd[j];
+            }
+            int excl = 0, tot = 0;
+            Scan(scan_tmp).ExclusiveSum(mine, excl, tot);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid * PER + j;
+                if (i < ns) toff[i] = excl;
+                excl += dd[j];
+            }
+            if (tid == 0) toff[ns] = tot;
+            __syncthreads();
+            const int P = tot;
+            for (int p0 = tid; p0 - tid < P; p0 += SBT * SUNROLL_T) {  // warp-uniform trips
+                int32_t v[SUNROLL_T], dv[SUNROLL_T];
+                double c[SUNROLL_T], old[SUNROLL_T];
+                bool valid[SUNROLL_T];
+#pragma unroll
+                for (int q = 0; q < SUNROLL_T; ++q) {
+                    const int p = p0 + q * SBT;
+                    valid[q] = p < P;
+                    v[q] = 0; dv[q] = 0; c[q] = 0.0;
+                    if (valid[q]) {
+                        int lo = 0, hi = ns - 1;  // last entry with toff <= p
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (toff[mid] <= p) lo = mid; else hi = mid - 1;
+                        }
+                        c[q] = tc[lo];
+                        const int2 nd = A.colp[trow[lo] + (p - toff[lo])];
+                        v[q] = nd.x;
+                        dv[q] = nd.y;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < SUNROLL_T; ++q) {
+                    GD_DCHECK(!valid[q] || (v[q] >= 0 && v[q] < A.g.n));
+                    old[q] = valid[q] ? atomicAdd(r + v[q], c[q]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < SUNROLL_T; ++q) {
+                    const double nv = __dadd_rn(old[q], c[q]);
+                    if (ch && valid[q]) my_l1 += fabs(nv) - fabs(old[q]);
+                    if (A.secmap && valid[q] && __double_as_longlong(old[q]) == 0)
+                        atomicOr(A.secmap + (int64_t)k * A.smw + (v[q] >> 7), 1u << ((v[q] >> 2) & 31));
+                    const double th = theta_of(A.op, v[q], dv[q]);
+                    const bool rise = valid[q] && fabs(nv) >= th && !(fabs(old[q]) >= th);
+                    if (valid[q] && below_theta(fabs(nv), th)) {
+                        const int at = atomicAdd(&s_nn, 1);
+                        if (at < STAIL_NEAR) tnear[at] = v[q]; else s_amb = 1;
+                    }
+                    const bool nw = cand_mark(rise, k, v[q], A, npar);
+                    const unsigned gm = __ballot_sync(SFULL, nw);
+                    if (gm) {
+                        int b = 0;
+                        if (lane == __ffs(gm) - 1) b = atomicAdd(&s_nxt, __popc(gm));
+                        b = __shfl_sync(SFULL, b, __ffs(gm) - 1);
+                        if (nw) nl[b + __popc(gm & lanemask_lt_s())] = v[q];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (ch) {
+            for (int o = 16; o > 0; o >>= 1) my_l1 += __shfl_xor_sync(SFULL, my_l1, o);
+            if (lane == 0 && my_l1 != 0.0) atomicAdd(&c_l1, my_l1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            A.s_ops[k] += c_ops;
+            A.s_pushes[k] += c_push;
+            if (ch) A.s_l1[k] += c_l1;
+            s_cur = s_nxt;
+        }
+        cur ^= 1;
+        __syncthreads();
+    }
+    if (tid == 0 && s_amb) A.s_amb[k] = 1;
 }
 
 __global__ void k_s_pack_cols(DevGraph g, int2 *__restrict__ colp) {
@@ -835,6 +1108,13 @@ struct SignedState {
     DBuf<unsigned long long> candctr, fctr, s_ops, s_pushes, pushed_cnt;
     bool dirty = false;  // an aborted run left marks behind: full clear next time
     size_t smem = 0;
+    // CTA-local tails (k_s_tail, cold LocalCH / LocalHB waves): 3 x n int32 + n
+    // doubles per slot, when that costs <= 4 GB (GDIFF_TAIL=0: off)
+    DBuf<int32_t> tail_list;
+    DBuf<double> tail_c;
+    DBuf<int64_t> tail_state;
+    int64_t tail_f = 1 << 13;
+    bool tail_on = false;
 
     void alloc(const gd_graph *W, int method_, int slots_, int64_t fcap_, bool cold) {
         device = W->device;
@@ -966,6 +1246,12 @@ struct SignedState {
         A.s_last = s_last.p; A.s_conv = s_conv.p; A.s_amb = s_amb.p;
         A.nearl = NearList{{nearkey.p, nearkey.p + NEAR_CAP}, {nearcnt.p, nearcnt.p + 1}, NEAR_CAP};
         A.overflow = overflow.p;
+        if (tail_on) {
+            A.tail_list = tail_list.p;
+            A.tail_c = tail_c.p;
+            A.tail_f = tail_f;
+            A.tail_state = tail_state.p;
+        }
         return A;
     }
 
@@ -1015,6 +1301,17 @@ SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, in
             S->set_hb(p.mu, p.L, p.max_sweeps);
         else
             S->set_ch(p.mu, p.L, p.max_sweeps);
+        {
+            const char *e = getenv("GDIFF_TAIL");
+            const size_t per = (size_t)slots * (size_t)n;
+            if (!(e && atoi(e) == 0) && per * 20 <= (4ULL << 30)) {
+                S->tail_list.alloc(3 * per);
+                S->tail_c.alloc(per);
+                S->tail_state.alloc(2);
+                S->tail_on = true;
+                if (const char *v = getenv("GDIFF_TAIL_F")) S->tail_f = atoll(v);  // (A/B)
+            }
+        }
     } catch (...) {
         delete S;
         throw;
@@ -1059,8 +1356,14 @@ void signed_batch_run(SignedState *S, const gd_graph *W, const gd_batch_params &
         SArgs A = S->args(W, m);
         k_s_init<<<(int)((m + 255) / 256), 256, 0, st>>>(A, d_seeds + base, perm, bval);
         GD_LAUNCH_CHECK();
+        if (S->tail_on)  // (-1: no tail handed over)
+            GD_CUDA(cudaMemsetAsync(S->tail_state.p, 0xFF, 2 * sizeof(int64_t), st));
         GD_CUDA(cudaEventRecord(ev[2 * w], st));
         S->rounds(A, st);
+        if (S->tail_on) {
+            k_s_tail<<<(unsigned)m, SBT, 0, st>>>(A);
+            nl += 1;
+        }
         GD_CUDA(cudaEventRecord(ev[2 * w + 1], st));
         k_s_reserve<<<(int)((m + 255) / 256), 256, 0, st>>>(A, cursor, S->slot_base.p);
         k_s_extract<<<dim3(SCHUNKS, (unsigned)m), 256, 0, st>>>(A, O, base);
