@@ -103,6 +103,7 @@ struct SArgs {
     int32_t *tail_list;
     double *tail_c;
     int64_t tail_f;
+    int32_t tail_t;       // (or from this round on)
     int64_t *tail_state;  // round, candidates (-1: no tail)
 };
 
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(SBT) k_signed_rounds(SArgs A) {
         }
         if (NC == 0) break;
         ncmax = NC > ncmax ? NC : ncmax;
-        if (A.tail_list && NC <= A.tail_f && (16 * NC <= ncmax || t >= 16)) {
+        if (A.tail_list && NC <= A.tail_f && (16 * NC <= ncmax || t >= A.tail_t)) {
             if (gtid == 0) {  // the rest of the wave in k_s_tail, one block per slot
                 A.tail_state[0] = t;
                 A.tail_state[1] = NC;
@@ -1114,6 +1115,7 @@ struct SignedState {
     DBuf<double> tail_c;
     DBuf<int64_t> tail_state;
     int64_t tail_f = 1 << 13;
+    int32_t tail_t = 16;
     bool tail_on = false;
 
     void alloc(const gd_graph *W, int method_, int slots_, int64_t fcap_, bool cold) {
@@ -1250,6 +1252,7 @@ struct SignedState {
             A.tail_list = tail_list.p;
             A.tail_c = tail_c.p;
             A.tail_f = tail_f;
+            A.tail_t = tail_t;
             A.tail_state = tail_state.p;
         }
         return A;
@@ -1310,6 +1313,7 @@ SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, in
                 S->tail_state.alloc(2);
                 S->tail_on = true;
                 if (const char *v = getenv("GDIFF_TAIL_F")) S->tail_f = atoll(v);  // (A/B)
+                if (const char *v = getenv("GDIFF_TAIL_T")) S->tail_t = atoi(v);
             }
         }
     } catch (...) {
