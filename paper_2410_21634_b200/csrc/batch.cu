@@ -2831,7 +2831,12 @@ static int batch_create_once(const gd_graph *G, const gd_batch_params *p, gd_bat
                     size_t fr = 0, tot = 0;
                     GD_CUDA(cudaMemGetInfo(&fr, &tot));
                     const int64_t by_mem = (int64_t)(fr / 4) / (ld * 33);
-                    slots = (int)(by_mem < 64 ? (by_mem < 1 ? 1 : by_mem) : 64);
+                    // Katz seeds (alpha < 1/lambda) do little work each (products:
+                    // ~26 K operations over ~110 sweeps), so a wave is bound by its
+                    // slowest seed's sweep chain: more seeds per wave (products Katz
+                    // 64 -> 512 slots: 8.4 K -> 10.8 K solves/s); PPR keeps 64
+                    const int64_t cap = p->problem == GD_P_KATZ ? 512 : 64;
+                    slots = (int)(by_mem < cap ? (by_mem < 1 ? 1 : by_mem) : cap);
                 }
                 if (slots > 2048) slots = 2048;
                 B->slots = slots;

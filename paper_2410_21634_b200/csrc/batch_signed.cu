@@ -1307,11 +1307,16 @@ SignedState *signed_batch_create(const gd_graph *W, const gd_batch_params &p, in
         {
             const char *e = getenv("GDIFF_TAIL");
             const size_t per = (size_t)slots * (size_t)n;
-            if (!(e && atoi(e) == 0) && per * 20 <= (4ULL << 30)) {
+            size_t fr = 0, tot = 0;  // lists cost at most a quarter of the free HBM
+            GD_CUDA(cudaMemGetInfo(&fr, &tot));
+            size_t cap = std::max<size_t>(4ULL << 30, fr / 4);
+            if (const char *v = getenv("GDIFF_TAIL_MEM_GB")) cap = (size_t)atoll(v) << 30;  // (A/B)
+            if (!(e && atoi(e) == 0) && per * 20 <= cap) {
                 S->tail_list.alloc(3 * per);
                 S->tail_c.alloc(per);
                 S->tail_state.alloc(2);
                 S->tail_on = true;
+                S->tail_f = std::max<int64_t>(1 << 13, 128LL * slots);  // (~128 per slot)
                 if (const char *v = getenv("GDIFF_TAIL_F")) S->tail_f = atoll(v);  // (A/B)
                 if (const char *v = getenv("GDIFF_TAIL_T")) S->tail_t = atoi(v);
             }
