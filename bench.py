@@ -636,9 +636,9 @@ def main():
                          "kernel": {"local-gd": ("k_seed_smem (one CTA per seed, state in shared "
                                                  "memory)" if solver.mode == "cta-smem" else
                                                  "k_seed_cta (one CTA per seed)") if cta else
-                                                    "k_rounds (persistent sweep loop)",
-                                    "local-ch": "k_signed_rounds (persistent signed sweep loop)",
-                                    "local-hb": "k_signed_rounds (heavy-ball coefficients)",
+                                                    "k_rounds + k_tail (persistent sweep loop, CTA-local wave tails)",
+                                    "local-ch": "k_signed_rounds + k_s_tail (persistent signed sweep loop, CTA-local tails)",
+                                    "local-hb": "k_signed_rounds + k_s_tail (heavy-ball coefficients)",
                                     "local-hk": "k_rounds<HK> (heat-kernel stages: dense ones as a pull SpMM)",
                                     "local-sor": "k_sor_win (exact windows, CTA per seed)" if win
                                                  else "k_fifo_batch (warp per seed)"}[args.method],
