@@ -1672,7 +1672,7 @@ __global__ void k_wave_extract(RoundArgs A, OutArgs O, int64_t seed_base) {
 // per-slot grid leaves most warps with one or two entries and the kernel
 // waits on the longest dependent chain (pushed -> x / inv -> store) per block
 // wave.  Per-seed counters: threads k < m of block 0.
-constexpr int XB = 4;
+constexpr int XB = 8;
 constexpr int EXB_MAX_SLOTS = 1024;
 __global__ void __launch_bounds__(256) k_wave_extract_bal(RoundArgs A, OutArgs O, int64_t seed_base) {
     __shared__ int64_t pre[EXB_MAX_SLOTS + 1];
