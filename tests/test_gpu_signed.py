@@ -59,8 +59,16 @@ def test_ch_batch_matches_reference_small(gpu, small, key):
         _check_seed(out, 0, small[f"{key}/x"], g.n)
 
 
+@pytest.mark.parametrize("tail", ["default", "from-round-1", "off"])
 @pytest.mark.parametrize("problem", ["ppr", "katz"])
-def test_ch_batch_rmat_matches_oracle(gpu, problem):
+def test_ch_batch_rmat_matches_oracle(gpu, monkeypatch, problem, tail):
+    """tail: the CTA-local tail (k_s_tail) at its default trigger, from round 1
+    on (nearly the whole solve block-local), or off (round kernel only)."""
+    if tail == "from-round-1":
+        monkeypatch.setenv("GDIFF_TAIL_T", "1")
+        monkeypatch.setenv("GDIFF_TAIL_F", str(1 << 30))
+    elif tail == "off":
+        monkeypatch.setenv("GDIFF_TAIL", "0")
     from paper_2410_21634_b200.graph import spectral_norm_estimate
     g = rmat_graph(20000, 150000, seed=5)
     seeds = sample_sources(g, 40, seed=2)
@@ -85,9 +93,14 @@ def _katz_bounds(g, alpha, lam):
     return 1.0 - alpha * lam, 1.0 + alpha * lam
 
 
-def test_ch_batch_divergence_and_sweep_cap(gpu):
+@pytest.mark.parametrize("tail", ["default", "from-round-1"])
+def test_ch_batch_divergence_and_sweep_cap(gpu, monkeypatch, tail):
     """Bad bounds make LocalCH diverge (abort at l1 > 10 ||b||_1); a sweep cap
-    stops unconverged -- both per seed exactly as the reference."""
+    stops unconverged -- both per seed exactly as the reference (also with the
+    CTA-local tail running nearly the whole solve)."""
+    if tail == "from-round-1":
+        monkeypatch.setenv("GDIFF_TAIL_T", "1")
+        monkeypatch.setenv("GDIFF_TAIL_F", str(1 << 30))
     g = rmat_graph(5000, 30000, seed=3)
     seeds = sample_sources(g, 12, seed=4)
     solver = BatchSolver(g, 0.1, 1e-6, slots=5, method="local-ch", mu=0.6, L=0.7,
