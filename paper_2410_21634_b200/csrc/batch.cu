@@ -2334,9 +2334,10 @@ static void batch_run(gd_batch *B, const int64_t *d_seeds, int64_t n_seeds, cuda
             launches += 1;
         }
         GD_CUDA(cudaEventRecord(B->ev[2 * w + 1], st));
-        // x extraction (random gathers: latency-bound) on st, the r reset
-        // (sector stores: bandwidth-bound) concurrently on a second stream;
-        // they touch disjoint data.  The next wave waits for both.
+        // x extraction (random gathers: latency-bound) on st.  Without a second
+        // residual set the r reset (sector stores: bandwidth-bound) runs beside
+        // it on the second stream (disjoint data) and the next wave waits for
+        // both; with one (dbuf) this set is reset during the next wave's tail.
         const cudaStream_t tst = B->serial ? st : B->aux;
         if (!dbuf) {
         GD_CUDA(cudaEventRecord(B->ev_fork, st));
