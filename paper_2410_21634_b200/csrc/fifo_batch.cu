@@ -299,6 +299,158 @@ __global__ void __launch_bounds__(FB_THREADS) k_fifo_batch(FifoBatchArgs A) {
     }
 }
 
+// ---- small graphs: the same replay with the seed's state in shared memory --
+// k_fifo_smem: one warp per CTA and seed, x, r, the queue marks and the ring
+// queue in shared memory (graphs of up to ~4 K nodes: cora), so every step of
+// a pop's dependent chain except the CSR reads is a shared-memory access.  The
+// pops, enqueue order and fl() sequence are k_fifo_batch's (the reference's);
+// values are stored as computed.  Between seeds the arrays are zero-filled;
+// x goes out in node order.
+__host__ inline size_t fifo_smem_bytes(int64_t n) {
+    const int64_t ld = (n + 1) & ~1LL;
+    return (size_t)(16 * ld + 4 * (ld / 32 + 1) + 4 * (n + 2)) + 16;
+}
+
+__global__ void __launch_bounds__(32) k_fifo_smem(FifoBatchArgs A) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int lane = threadIdx.x & 31;
+    const int64_t n = A.n, ld = (n + 1) & ~1LL, qw = ld / 32 + 1;
+    double *const x = reinterpret_cast<double *>(fsm);
+    double *const r = x + ld;
+    uint32_t *const qmark = reinterpret_cast<uint32_t *>(r + ld);
+    int32_t *const queue = reinterpret_cast<int32_t *>(qmark + qw);
+    const int64_t sent = n, qcap = n + 2;
+    for (;;) {
+        unsigned long long si = 0;
+        if (lane == 0) si = atomicAdd(A.next_seed, 1ULL);
+        si = __shfl_sync(FULL, si, 0);
+        if ((int64_t)si >= A.n_seeds) break;
+        for (int64_t i = lane; i < ld; i += 32) {
+            x[i] = 0.0;
+            r[i] = 0.0;
+        }
+        for (int64_t i = lane; i < qw; i += 32) qmark[i] = 0u;
+        __syncwarp();
+        const int32_t s = (int32_t)A.seeds[si];
+        if (lane == 0) r[s] = A.alpha;
+        int64_t front = 0, rear = 0;
+        const double ths = theta_d(A.tcoeff, A.g.deg[s]);
+        const bool act0 = A.sgn ? fabs(A.alpha) >= ths : A.alpha >= ths;
+        int64_t sweeps = 0, ops = 0, pushes = 0;
+        int conv = 1;
+        if (act0) {
+            if (lane == 0) {
+                queue[0] = s;
+                qmark[s >> 5] |= 1u << (s & 31);
+                queue[1] = (int32_t)sent;
+            }
+            rear = 2;
+            int64_t svol = 0;
+            __syncwarp();
+            for (;;) {
+                const int64_t u = queue[front];
+                front = (front + 1 == qcap) ? 0 : front + 1;
+                if (u == sent) {  // sweep boundary (:102-144)
+                    ops += svol;
+                    sweeps += 1;
+                    if (front == rear) break;
+                    if (sweeps >= A.max_sweeps) {
+                        conv = 0;
+                        break;
+                    }
+                    if (lane == 0) queue[rear] = (int32_t)sent;
+                    rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                    svol = 0;
+                    __syncwarp();
+                    continue;
+                }
+                const double ru = r[u], xu = x[u];
+                const int32_t d = A.g.deg[u];
+                const int64_t rs = A.g.row[u];
+                __syncwarp();
+                if (lane == 0) qmark[u >> 5] &= ~(1u << (u & 31));
+                const double th = theta_d(A.tcoeff, d);
+                if (A.sgn ? fabs(ru) < th : ru < th) {
+                    __syncwarp();
+                    continue;
+                }
+                svol += d;
+                pushes += 1;
+                const double res = __dmul_rn(A.omega, ru);
+                if (lane == 0) {
+                    x[u] = __dadd_rn(xu, res);  // x_gain = 1
+                    r[u] = __dsub_rn(ru, res);
+                }
+                __syncwarp();
+                const double w = __dmul_rn(__ddiv_rn(1.0, (double)d), A.beta);
+                for (int64_t base = 0; base < d; base += 32) {
+                    const int64_t j = base + lane;
+                    bool act = false;
+                    int32_t v = 0;
+                    if (j < d) {
+                        v = A.g.col[rs + j];
+                        const double rv = __dadd_rn(r[v], __dmul_rn(res, w));
+                        r[v] = rv;
+                        if (!((qmark[v >> 5] >> (v & 31)) & 1u)) {
+                            const double tv = theta_d(A.tcoeff, A.g.deg[v]);
+                            act = A.sgn ? fabs(rv) >= tv : rv >= tv;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(FULL, act);
+                    if (act) {
+                        int64_t q = rear + __popc(bal & lanemask_lt());
+                        if (q >= qcap) q -= qcap;
+                        queue[q] = v;
+                        atomicOr(qmark + (v >> 5), 1u << (v & 31));
+                    }
+                    rear += __popc(bal);
+                    if (rear >= qcap) rear -= qcap;
+                    __syncwarp();
+                }
+                const double ru2 = __dsub_rn(ru, res);  // self re-check (:176-185)
+                if (A.sgn ? fabs(ru2) >= th : ru2 >= th) {
+                    if (lane == 0) {
+                        queue[rear] = (int32_t)u;
+                        qmark[u >> 5] |= 1u << (u & 31);
+                    }
+                    rear = (rear + 1 == qcap) ? 0 : rear + 1;
+                }
+                __syncwarp();
+            }
+        }
+        // x out in node order
+        int64_t nx = 0;
+        for (int64_t i = lane; i < n; i += 32) nx += x[i] != 0.0;
+        for (int o = 16; o > 0; o >>= 1) nx += __shfl_xor_sync(FULL, nx, o);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.cursor, (unsigned long long)nx);
+        base = __shfl_sync(FULL, base, 0);
+        int64_t wpos = (int64_t)base;
+        for (int64_t i0 = 0; i0 < n; i0 += 32) {
+            const int64_t i = i0 + lane;
+            const double xv = i < n ? x[i] : 0.0;
+            const unsigned nzb = __ballot_sync(FULL, xv != 0.0);
+            if (xv != 0.0) {
+                const int64_t pos = wpos + __popc(nzb & lanemask_lt());
+                if (pos < A.xcap) {
+                    A.xnodes[pos] = (int32_t)i;
+                    A.xvals[pos] = xv;
+                }
+            }
+            wpos += __popc(nzb);
+        }
+        if (lane == 0) {
+            A.sweeps[si] = sweeps;
+            A.ops[si] = ops;
+            A.pushes[si] = pushes;
+            A.conv[si] = conv;
+            A.xoff[si] = (int64_t)base;
+            A.xcnt[si] = nx;
+        }
+        __syncwarp();
+    }
+}
+
 // ---- the reference's repair for resident pairs ------------------------------
 // dynamic.repair (src/dynamic.py:131-162) on every pair of a gd_pairs pool at
 // once, one warp per pair: seeds = flatnonzero(|r| >= eps d) in index order
@@ -437,6 +589,9 @@ struct FifoBatchState {
     DBuf<uint32_t> qmark;
     int64_t qw = 0;
     DBuf<unsigned long long> ctr;  // next_seed
+    bool smem = false;             // k_fifo_smem (small graphs)
+    size_t smem_bytes = 0;
+    int64_t smem_ctas = 0;
 };
 
 FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
@@ -463,6 +618,24 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
         GD_CUDA(cudaMemset(F->r.p, 0, sizeof(double) * sn));
         GD_CUDA(cudaMemset(F->qmark.p, 0, sizeof(uint32_t) * (size_t)slots * (size_t)F->qw));
         F->ctr.alloc(1);
+        {   // shared-memory form when a seed's state fits (GDIFF_FIFO_SMEM=0: off)
+            const char *e = getenv("GDIFF_FIFO_SMEM");
+            const size_t need = fifo_smem_bytes(n);
+            int maxo = 0;
+            GD_CUDA(cudaDeviceGetAttribute(&maxo, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                           G->device));
+            if (!(e && atoi(e) == 0) && need <= (size_t)maxo && need <= (96u << 10)) {
+                GD_CUDA(cudaFuncSetAttribute(k_fifo_smem,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+                int per_sm = 0;
+                GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fifo_smem, 32, need));
+                if (per_sm > 0) {
+                    F->smem = true;
+                    F->smem_bytes = need;
+                    F->smem_ctas = (int64_t)per_sm * n_sms(G->device);
+                }
+            }
+        }
     } catch (...) {
         delete F;
         throw;
@@ -473,6 +646,7 @@ FifoBatchState *fifo_batch_create(const gd_graph *G, int slots) {
 void fifo_batch_destroy(FifoBatchState *F) { delete F; }
 
 int fifo_batch_slots(const FifoBatchState *F) { return F->nslots; }
+bool fifo_batch_smem(const FifoBatchState *F) { return F->smem; }
 
 void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params &p,
                     const int64_t *d_seeds, int64_t n_seeds, int64_t *sweeps, int64_t *ops,
@@ -500,6 +674,12 @@ void fifo_batch_run(FifoBatchState *F, const gd_graph *G, const gd_batch_params 
         A.rcap = rp->cap; A.rcursor = rp->cursor;
     }
     GD_CUDA(cudaMemsetAsync(F->ctr.p, 0, sizeof(unsigned long long), st));
+    if (F->smem && !rp) {  // small graph: the seed's state in shared memory
+        const int64_t ctas = F->smem_ctas < n_seeds ? F->smem_ctas : (n_seeds ? n_seeds : 1);
+        k_fifo_smem<<<(int)ctas, 32, F->smem_bytes, st>>>(A);
+        GD_LAUNCH_CHECK();
+        return;
+    }
     const int64_t warps = F->nslots < n_seeds ? F->nslots : (n_seeds ? n_seeds : 1);
     const int blocks = (int)((warps * 32 + FB_THREADS - 1) / FB_THREADS);
     k_fifo_batch<<<blocks, FB_THREADS, 0, st>>>(A);
